@@ -1,0 +1,178 @@
+/*
+ * gpurir.h — C ABI of libgpurir.so, the B200 (sm_100a) Image Source Method
+ * room-impulse-response engine (the hot path of gpuRIR, arXiv 1810.11359).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n; readings "C<k>" are
+ * listed in DESIGN.md §Readings.
+ *
+ * Conventions (all entry points):
+ *   - extern "C", no exceptions; every call returns a gpurir_status (0 = OK)
+ *     unless documented otherwise.
+ *   - Arrays documented "device" are caller-owned CUDA device pointers on the
+ *     calling thread's current device; "host" arrays are read before return.
+ *   - Output buffers are written in place and never allocated or freed by the
+ *     library.  Calls are stream-ordered on opts->stream and return without a
+ *     device synchronisation unless GPURIR_FLAG_SYNC is set.
+ *   - There is no global mutable state (the paper's global LUT / mixed-
+ *     precision switches, become the per-call opts->mode).
+ *   - Validation runs on the host before any launch.  Conditions that can
+ *     only be seen on the device (a zero orientation vector, an image source
+ *     coinciding with a receiver) raise a per-device status word that is
+ *     returned by the call when GPURIR_FLAG_SYNC is set, and otherwise by the
+ *     next gpurir_device_status() call.
+ */
+#ifndef GPURIR_H
+#define GPURIR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GPURIR_OK = 0,
+  GPURIR_EINVAL = 1,       /* bad argument: sizes, |beta| > 1, pattern, times, zero orientation */
+  GPURIR_EDEGENERATE = 2,  /* an image source coincides with a receiver, d_n = 0 */
+  GPURIR_EINFEASIBLE = 3,  /* Sabine target T60 below the room's minimum */
+  GPURIR_ENOMEM = 4,       /* device allocation failed */
+  GPURIR_ECUDA = 5         /* CUDA runtime error; see gpurir_last_cuda_error() */
+} gpurir_status;
+
+/* Receiver polar patterns, g = a + (1 - a) cos(theta) (reading C4). */
+typedef enum {
+  GPURIR_OMNI = 0,          /* a = 1    */
+  GPURIR_SUBCARDIOID = 1,   /* a = 0.75 */
+  GPURIR_CARDIOID = 2,      /* a = 0.5  */
+  GPURIR_HYPERCARDIOID = 3, /* a = 0.25 */
+  GPURIR_BIDIRECTIONAL = 4  /* a = 0    */
+} gpurir_pattern;
+
+/* Sinc evaluation mode (mutually exclusive). */
+typedef enum {
+  GPURIR_FP32 = 0, /* Eq. 6 evaluated in fp32 (the paper's "base" kernel)               */
+  GPURIR_LUT = 1,  /* Eq. 9 windowed-sinc table, Q-times oversampled, linear interp.    */
+  GPURIR_FP16 = 2  /* half2 tap arithmetic with the Eq. 10-12 style polynomials */
+} gpurir_mode;
+
+#define GPURIR_FLAG_SYNC 1u /* synchronise the stream before returning and report device-side status */
+
+typedef struct {
+  int mode;                 /* gpurir_mode, default GPURIR_FP32                                    */
+  double Tw;                /* Peterson window length in seconds, default 4e-3              */
+  int lut_Q;                /* LUT oversampling factor Q, default 16                        */
+  uint64_t seed;            /* diffuse-tail RNG key (Philox4x32-10, reading C16), default 0         */
+  uint64_t rir_index_base;  /* global index of this call's first RIR (tail RNG stream id), default 0 */
+  void* stream;             /* cudaStream_t to launch on; NULL = the legacy default stream          */
+  int split;                /* CTAs cooperating on one time tile (thread-block cluster), 0 = auto   */
+  unsigned flags;           /* GPURIR_FLAG_*                                                        */
+} gpurir_opts;
+
+/* Fill *opts with the defaults above. */
+void gpurir_opts_default(gpurir_opts* opts);
+
+/*
+ * gpurir_simulate_rir — RIRs of every (source, receiver) pair of one shoebox
+ * room (Eqs. 1-6 for 0 <= t < Tdiff, diffuse tail Eqs. 7-8 / P:160 for
+ * Tdiff <= t < Tmax).
+ *   room_sz  host  float[3]   room size L (m), each > 0
+ *   beta     host  float[6]   signed reflection coefficients (x0,x1,y0,y1,z0,z1), |beta| <= 1
+ *   pos_src  device float[M_src][3]  source positions (m)
+ *   pos_rcv  device float[M_rcv][3]  receiver positions (m)
+ *   orV_rcv  device float[M_rcv][3]  receiver orientations (normalised on the device), may be NULL
+ *                                    only when mic_pattern == GPURIR_OMNI
+ *   nb_img   host  int[3]     images per axis N_x, N_y, N_z >= 1; lattice ceil(-N/2) <= n < ceil(N/2)
+ *   Tdiff    ISM / diffuse switch time (s) >= 0; nISM = ceil(Tdiff fs) samples (reading C9)
+ *   Tmax     RIR length (s) > 0; nSamples = ceil(Tmax fs) (C9); Tdiff >= Tmax means ISM only
+ *   fs, c    sampling rate (Hz) and speed of sound (m/s), > 0
+ *   out      device float[M_src][M_rcv][nSamples], caller-owned, row-major RIR r = m_src*M_rcv + m_rcv
+ *   opts     NULL for defaults
+ * Errors: EINVAL (host validation), EDEGENERATE / EINVAL from the device word
+ * (see file header), ECUDA on a launch failure.
+ */
+int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float* pos_src, int M_src,
+                        const float* pos_rcv, int M_rcv, const float* orV_rcv, int mic_pattern, const int nb_img[3],
+                        double Tdiff, double Tmax, double fs, double c, float* out, const gpurir_opts* opts);
+
+/* One independent room of a batch (config 5; a deviation from the paper's
+ * same-room-only batching).  out_offset = element offset of this RIR's
+ * row in the batch output buffer (ragged rows of ceil(Tmax fs) samples). */
+typedef struct {
+  float room_sz[3];
+  float beta[6];
+  float pos_src[3];
+  float pos_rcv[3];
+  float orV_rcv[3]; /* ignored for GPURIR_OMNI */
+  int mic_pattern;
+  int nb_img[3];
+  double Tdiff;
+  double Tmax;
+  long long out_offset;
+} gpurir_room;
+
+/*
+ * gpurir_simulate_rir_batch — one RIR per room for n_rooms independent rooms.
+ *   rooms  host gpurir_room[n_rooms] (copied to the device inside the call, stream-ordered)
+ *   out    device float buffer; room i writes out[rooms[i].out_offset + k], 0 <= k < ceil(Tmax_i fs)
+ *   The tail RNG stream of room i is rir_index_base + i.
+ * Errors as gpurir_simulate_rir; ENOMEM if the internal job table cannot be allocated.
+ */
+int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, float* out,
+                              const gpurir_opts* opts);
+
+/* Number of samples ceil(T fs) under reading C9 (a product within 1e-6 of an integer from above
+ * counts as that integer). */
+long long gpurir_nsamples(double T, double fs);
+
+/* ---- host helpers (pure, thread-safe) ---------------------------------------------- */
+
+/* Eq. 7: Sabine T60 = 0.161 V / sum_i S_i (1 - beta_i^2); +inf if no wall absorbs. */
+double gpurir_sabine_t60(const float room_sz[3], const float beta[6]);
+
+/* A17 (reading C17): uniform alpha = 0.161 V / (T60 S), beta_i = sign * sqrt(1 - alpha).
+ * sign < 0 (default in the paper's spirit) gives negative coefficients.  alpha > 1 returns
+ * EINFEASIBLE unless clamp != 0, which returns beta = 0 (anechoic) and sets *clamped = 1. */
+int gpurir_beta_sabine(const float room_sz[3], double T60, int sign, int clamp, float beta_out[6], int* clamped);
+
+/* A18: time at which the exponential decay reaches att_dB: att_dB / 60 * T60. */
+double gpurir_att2t_sabine(double att_dB, double T60);
+
+/* A19 (reading C6): images per axis reaching time T without lost reflections,
+ * N = 2 (ceil(c T / L) + 1) + 1 (odd). */
+int gpurir_t2n(double T, const float room_sz[3], double c, int nb_img_out[3]);
+
+/* ---- test / inspection hooks ---------------------------------------------------------------- */
+
+/*
+ * gpurir_image_params — the image-parameter stage (calcAmpTau; Eqs. 1-4 + A16) of
+ * one (source, receiver) pair for every lattice image, in lattice order (n_x fastest, then n_y,
+ * then n_z), computed by the same device code the accumulation kernel inlines.
+ *   src, rcv, orv  host float[3] (orv ignored for omni)
+ *   x_out  device double[N]  delay in samples, tau_n * fs
+ *   A_out  device float[N]   amplitude beta_n g / (4 pi d_n)
+ * Synchronises the stream.  Returns EDEGENERATE if some d_n = 0.
+ */
+int gpurir_image_params(const float room_sz[3], const float beta[6], const float src[3], const float rcv[3],
+                        const float orv[3], int mic_pattern, const int nb_img[3], double fs, double c,
+                        double* x_out, float* A_out, void* stream);
+
+/* Windowed-sinc table of Eq. 9 (erratum C11) exactly as uploaded for GPURIR_LUT: entries
+ * LUT[n], n = -half..half, written to host lut_out[0 .. 2 half] when lut_out != NULL and
+ * cap >= 2 half + 1.  Returns half (>= 0) or -GPURIR_EINVAL. */
+long long gpurir_lut_table(double Tw, double fs, int Q, float* lut_out, long long cap);
+
+/* Read and (if reset) clear the current device's status word (see file header). Synchronises. */
+int gpurir_device_status(int reset);
+
+const char* gpurir_strerror(int status);
+/* Last CUDA error string recorded by this thread ("" if none). */
+const char* gpurir_last_cuda_error(void);
+/* Library version string. */
+const char* gpurir_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GPURIR_H */

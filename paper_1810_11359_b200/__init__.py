@@ -1,0 +1,14 @@
+"""paper_1810_11359_b200 — B200-native (sm_100a) Image Source Method RIR engine.
+
+The hot path of gpuRIR (Diaz-Guerra et al., arXiv 1810.11359) as hand-written
+CUDA kernels behind the C ABI in include/gpurir.h (libgpurir.so); this package is
+the thin Python binding (same names) plus the multi-GPU shard planner.
+There is no CPU fallback: without the built extension every call raises.
+"""
+from .api import (att2t_sabine, beta_sabine, device_status, image_params, lut_table, make_opts, nsamples,
+                  room_array, sabine_t60, simulate_rir, simulate_rir_batch, t2n, version)
+from ._lib import EXPORTS, LIB_PATH, MODES, PATTERNS, GpurirError
+
+__all__ = ["simulate_rir", "simulate_rir_batch", "sabine_t60", "beta_sabine", "att2t_sabine", "t2n", "nsamples",
+           "lut_table", "image_params", "device_status", "make_opts", "room_array", "version", "GpurirError",
+           "MODES", "PATTERNS", "EXPORTS", "LIB_PATH"]

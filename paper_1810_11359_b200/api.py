@@ -1,0 +1,193 @@
+"""Thin Python binding of libgpurir (include/gpurir.h), same names as the C ABI.
+
+Argument marshalling only: torch supplies device memory and streams; every step
+of the RIR path runs in the library's CUDA kernels.  Citations as in the header.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import FLAG_SYNC, MODES, PATTERNS, GpurirError, Opts, Room, check, lib
+
+
+def _f3(v, n=3):
+    a = (C.c_float * n)(*[float(x) for x in np.asarray(v, dtype=np.float64).reshape(-1)[:n]])
+    if len(np.asarray(v).reshape(-1)) != n:
+        raise ValueError(f"expected {n} values")
+    return a
+
+
+def _i3(v):
+    vv = [int(x) for x in np.asarray(v).reshape(-1)]
+    if len(vv) != 3:
+        raise ValueError("expected 3 values")
+    return (C.c_int * 3)(*vv)
+
+
+def _pattern(p) -> int:
+    return PATTERNS[p] if isinstance(p, str) else int(p)
+
+
+def _mode(m) -> int:
+    return MODES[m] if isinstance(m, str) else int(m)
+
+
+def _stream_handle(stream) -> int | None:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def make_opts(mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0, stream=None, split=0, sync=False) -> Opts:
+    o = Opts()
+    lib().gpurir_opts_default(C.byref(o))
+    o.mode = _mode(mode)
+    o.Tw = float(Tw)
+    o.lut_Q = int(lut_Q)
+    o.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    o.rir_index_base = int(rir_index_base)
+    o.stream = _stream_handle(stream)
+    o.split = int(split)
+    o.flags = FLAG_SYNC if sync else 0
+    return o
+
+
+def nsamples(T: float, fs: float) -> int:
+    """ceil(T fs) under reading C9."""
+    return int(lib().gpurir_nsamples(float(T), float(fs)))
+
+
+def _dev_f32(t, name, rows=None):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA torch tensor")
+    if t.dtype != torch.float32 or not t.is_contiguous():
+        raise TypeError(f"{name} must be contiguous float32")
+    if rows is not None and (t.dim() != 2 or t.shape[1] != 3):
+        raise ValueError(f"{name} must have shape [M, 3]")
+    return t
+
+
+def simulate_rir(room_sz, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs, c=343.0, orV_rcv=None,
+                 mic_pattern="omni", mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0, out=None,
+                 stream=None, split=0, sync=False):
+    """gpurir_simulate_rir: RIRs [M_src][M_rcv][ceil(Tmax fs)] (float32, on pos_src's device).
+
+    room_sz (3) and beta (6, wall order x0,x1,y0,y1,z0,z1) are host values; pos_src [M_src,3],
+    pos_rcv [M_rcv,3] and orV_rcv [M_rcv,3] are CUDA float32 tensors.  Stream-ordered; returns `out`.
+    """
+    import torch
+    pos_src = _dev_f32(pos_src, "pos_src", rows=True)
+    pos_rcv = _dev_f32(pos_rcv, "pos_rcv", rows=True)
+    pat = _pattern(mic_pattern)
+    if orV_rcv is not None:
+        orV_rcv = _dev_f32(orV_rcv, "orV_rcv", rows=True)
+    Ms, Mr = pos_src.shape[0], pos_rcv.shape[0]
+    nS = nsamples(Tmax, fs)
+    if out is None:
+        out = torch.empty((Ms, Mr, nS), dtype=torch.float32, device=pos_src.device)
+    elif out.dtype != torch.float32 or not out.is_contiguous() or out.numel() < Ms * Mr * nS:
+        raise ValueError("out must be contiguous float32 with M_src*M_rcv*nSamples elements")
+    o = make_opts(mode, Tw, lut_Q, seed, rir_index_base, stream, split, sync)
+    st = lib().gpurir_simulate_rir(_f3(room_sz), _f3(beta, 6), pos_src.data_ptr(), Ms, pos_rcv.data_ptr(), Mr,
+                                   orV_rcv.data_ptr() if orV_rcv is not None else None, pat, _i3(nb_img),
+                                   float(Tdiff), float(Tmax), float(fs), float(c), out.data_ptr(), C.byref(o))
+    check(st, "gpurir_simulate_rir")
+    return out
+
+
+def room_array(rooms) -> C.Array:
+    """Build a gpurir_room[n] array from a sequence of dicts with the struct's field names."""
+    arr = (Room * len(rooms))()
+    for i, r in enumerate(rooms):
+        R = arr[i]
+        R.room_sz[:] = [float(x) for x in r["room_sz"]]
+        R.beta[:] = [float(x) for x in r["beta"]]
+        R.pos_src[:] = [float(x) for x in r["pos_src"]]
+        R.pos_rcv[:] = [float(x) for x in r["pos_rcv"]]
+        R.orV_rcv[:] = [float(x) for x in r.get("orV_rcv", (0.0, 0.0, 1.0))]
+        R.mic_pattern = _pattern(r.get("mic_pattern", 0))
+        R.nb_img[:] = [int(x) for x in r["nb_img"]]
+        R.Tdiff = float(r["Tdiff"])
+        R.Tmax = float(r["Tmax"])
+        R.out_offset = int(r["out_offset"])
+    return arr
+
+
+def simulate_rir_batch(rooms, fs, out, c=343.0, mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0,
+                       stream=None, split=0, sync=False):
+    """gpurir_simulate_rir_batch: one RIR per independent room into ragged rows of `out` (CUDA float32).
+
+    `rooms` is a ctypes gpurir_room array (see room_array) or a sequence of dicts.
+    """
+    arr = rooms if isinstance(rooms, C.Array) else room_array(rooms)
+    o = make_opts(mode, Tw, lut_Q, seed, rir_index_base, stream, split, sync)
+    st = lib().gpurir_simulate_rir_batch(len(arr), arr, float(fs), float(c), out.data_ptr(), C.byref(o))
+    check(st, "gpurir_simulate_rir_batch")
+    return out
+
+
+# ---- host helpers ------------------------------------------------------------------
+
+def sabine_t60(room_sz, beta) -> float:
+    """Eq. 7."""
+    return float(lib().gpurir_sabine_t60(_f3(room_sz), _f3(beta, 6)))
+
+
+def beta_sabine(room_sz, T60: float, sign: int = -1, clamp: bool = False) -> tuple[np.ndarray, bool]:
+    """A17 / reading C17: uniform-absorption beta for a target T60 (negative by default)."""
+    out = (C.c_float * 6)()
+    cl = C.c_int(0)
+    st = lib().gpurir_beta_sabine(_f3(room_sz), float(T60), int(sign), int(bool(clamp)), out, C.byref(cl))
+    check(st, "gpurir_beta_sabine")
+    return np.array(list(out), dtype=np.float32), bool(cl.value)
+
+
+def att2t_sabine(att_dB: float, T60: float) -> float:
+    return float(lib().gpurir_att2t_sabine(float(att_dB), float(T60)))
+
+
+def t2n(T: float, room_sz, c: float = 343.0) -> np.ndarray:
+    out = (C.c_int * 3)()
+    st = lib().gpurir_t2n(float(T), _f3(room_sz), float(c), out)
+    check(st, "gpurir_t2n")
+    return np.array(list(out), dtype=np.int32)
+
+
+def lut_table(Tw: float = 4e-3, fs: float = 16000.0, Q: int = 16) -> tuple[np.ndarray, int]:
+    half = int(lib().gpurir_lut_table(float(Tw), float(fs), int(Q), None, 0))
+    if half < 0:
+        raise GpurirError(-half, "gpurir_lut_table")
+    buf = (C.c_float * (2 * half + 1))()
+    lib().gpurir_lut_table(float(Tw), float(fs), int(Q), buf, 2 * half + 1)
+    return np.array(list(buf), dtype=np.float32), half
+
+
+def image_params(room_sz, beta, src, rcv, nb_img, fs, c=343.0, mic_pattern="omni", orv=None, device=None):
+    """gpurir_image_params: (delay in samples float64 [N], amplitude float32 [N]) in lattice order."""
+    import torch
+    N = int(np.prod(np.asarray(nb_img, dtype=np.int64)))
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    x = torch.empty(N, dtype=torch.float64, device=dev)
+    A = torch.empty(N, dtype=torch.float32, device=dev)
+    o = _f3(orv) if orv is not None else None
+    st = lib().gpurir_image_params(_f3(room_sz), _f3(beta, 6), _f3(src), _f3(rcv), o, _pattern(mic_pattern),
+                                   _i3(nb_img), float(fs), float(c), x.data_ptr(), A.data_ptr(),
+                                   _stream_handle(None))
+    check(st, "gpurir_image_params")
+    return x, A
+
+
+def device_status(reset: bool = True) -> int:
+    return int(lib().gpurir_device_status(int(bool(reset))))
+
+
+def version() -> str:
+    return lib().gpurir_version().decode()

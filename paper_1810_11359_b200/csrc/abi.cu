@@ -1,0 +1,454 @@
+// abi.cu — C ABI of libgpurir.so (include/gpurir.h): host-side validation,
+// sizing (hot-path row a0 of SURVEY.md §8(a)), planning and launch sequence.
+//
+// Every step of the RIR path runs in the CUDA kernels of ism_kernel.cu and
+// tail_kernel.cu; this file only validates, sizes and launches.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "../../include/gpurir.h"
+#include "device_common.cuh"
+#include "kernels.h"
+
+using namespace gpurir;
+
+namespace {
+
+thread_local char g_cuda_err[256] = "";
+
+int cuda_fail(cudaError_t e, const char* where) {
+  snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
+  return GPURIR_ECUDA;
+}
+
+// Per-device status word and LUT cache (lazily created, process lifetime).
+struct DeviceState {
+  int* status = nullptr;
+  float2* lut = nullptr;
+  size_t lut_cap = 0;
+  double lut_Tw = 0, lut_fs = 0;
+  int lut_Q = 0, lut_rows = 0, lut_cols = 0, lut_joff = 0;
+};
+std::mutex g_mu;
+std::vector<DeviceState> g_dev;
+
+DeviceState* device_state(int* err) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) { *err = cuda_fail(e, "cudaGetDevice"); return nullptr; }
+  std::lock_guard<std::mutex> lk(g_mu);
+  if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
+  DeviceState& d = g_dev[dev];
+  if (!d.status) {
+    e = cudaMalloc(&d.status, sizeof(int));
+    if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMalloc(status)"); return nullptr; }
+    e = cudaMemset(d.status, 0, sizeof(int));
+    if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMemset(status)"); return nullptr; }
+  }
+  *err = GPURIR_OK;
+  return &d;
+}
+
+// Eq. 9 with the window argument 2 pi n / (Q fs T_w) (erratum C11).
+double lut_entry(long long n, double Tw, double fs, int Q, long long half) {
+  if (n < -half || n > half) return 0.0;
+  double t = (double)n / (Q * fs);
+  if (!(t > -Tw / 2 && t < Tw / 2)) return 0.0;  // open support (C8)
+  double win = 0.5 * (1.0 + cos(2.0 * M_PI * (double)n / (Q * fs * Tw)));
+  double arg = M_PI * (double)n / Q;
+  return win * (n == 0 ? 1.0 : sin(arg) / arg);
+}
+
+long long lut_half(double Tw, double fs, int Q) { return (long long)ceil(Tw * Q * fs / 2.0 - 1e-9); }
+
+// Phase-major interpolation table for the LUT kernel:
+// TP[ph][jj + joff] = (T[Q jj + ph + 1], T[Q jj + ph] - T[Q jj + ph + 1]).
+int ensure_lut(DeviceState* d, double Tw, double fs, int Q, double H, cudaStream_t stream) {
+  if (d->lut && d->lut_Tw == Tw && d->lut_fs == fs && d->lut_Q == Q) return GPURIR_OK;
+  long long half = lut_half(Tw, fs, Q);
+  int joff = (int)ceil(H) + kS + 2;
+  int cols = 2 * joff + 1;
+  int rows = Q;
+  std::vector<float2> tab((size_t)rows * cols);
+  for (int ph = 0; ph < rows; ph++)
+    for (int c = 0; c < cols; c++) {
+      long long jj = c - joff;
+      long long n = (long long)Q * jj + ph;
+      double t0 = lut_entry(n, Tw, fs, Q, half), t1 = lut_entry(n + 1, Tw, fs, Q, half);
+      tab[(size_t)ph * cols + c] = make_float2((float)t1, (float)(t0 - t1));
+    }
+  size_t bytes = tab.size() * sizeof(float2);
+  if (bytes > d->lut_cap) {
+    if (d->lut) cudaFree(d->lut);
+    cudaError_t e = cudaMalloc(&d->lut, bytes);
+    if (e != cudaSuccess) { d->lut = nullptr; d->lut_cap = 0; return cuda_fail(e, "cudaMalloc(lut)"); }
+    d->lut_cap = bytes;
+  }
+  cudaError_t e = cudaMemcpyAsync(d->lut, tab.data(), bytes, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(lut)");
+  e = cudaStreamSynchronize(stream);  // host vector goes out of scope
+  if (e != cudaSuccess) return cuda_fail(e, "sync(lut)");
+  d->lut_Tw = Tw; d->lut_fs = fs; d->lut_Q = Q; d->lut_rows = rows; d->lut_cols = cols; d->lut_joff = joff;
+  return GPURIR_OK;
+}
+
+double sabine(const float L[3], const float b[6]) {
+  double V = (double)L[0] * L[1] * L[2];
+  double S[6] = {(double)L[1] * L[2], (double)L[1] * L[2], (double)L[0] * L[2],
+                 (double)L[0] * L[2], (double)L[0] * L[1], (double)L[0] * L[1]};
+  double den = 0.0;
+  for (int i = 0; i < 6; i++) den += S[i] * (1.0 - (double)b[i] * b[i]);
+  if (den <= 0.0) return INFINITY;
+  return 0.161 * V / den;
+}
+
+int validate_room(const float L[3], const float b[6], const int nb[3], int pattern) {
+  for (int i = 0; i < 3; i++) {
+    if (!(L[i] > 0.f) || !isfinite(L[i])) return GPURIR_EINVAL;
+    if (nb[i] < 1) return GPURIR_EINVAL;
+  }
+  for (int i = 0; i < 6; i++)
+    if (!(fabsf(b[i]) <= 1.f)) return GPURIR_EINVAL;
+  if (pattern < 0 || pattern > 4) return GPURIR_EINVAL;
+  return GPURIR_OK;
+}
+
+void fill_common(IsmArgs& A, double fs, double c, double Tw) {
+  A.fs_over_c = fs / c;
+  A.c_over_fs = c / fs;
+  double H = Tw * fs / 2.0;
+  A.H = (float)H;
+  A.invH = (float)(1.0 / H);
+  A.nbw = (int)floor(((double)kS - 1.0 + 2.0 * H) / kS) + 1;
+}
+
+int auto_split(long long nclusters, int requested) {
+  if (requested > 0) return requested > kMaxSplit ? kMaxSplit : requested;
+  int s = 1;
+  while (s < kMaxSplit && nclusters * s < 148LL * 4) s *= 2;
+  return s;
+}
+
+int finish(const gpurir_opts& o, cudaStream_t st, DeviceState* d) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "launch");
+  if (o.flags & GPURIR_FLAG_SYNC) {
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "sync");
+    int s = 0;
+    e = cudaMemcpy(&s, d->status, sizeof(int), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "status");
+    if (s) {
+      cudaMemset(d->status, 0, sizeof(int));
+      return (s & kStatusDegenerate) ? GPURIR_EDEGENERATE : GPURIR_EINVAL;
+    }
+  }
+  return GPURIR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void gpurir_opts_default(gpurir_opts* o) {
+  memset(o, 0, sizeof(*o));
+  o->mode = GPURIR_FP32;
+  o->Tw = 4e-3;
+  o->lut_Q = 16;
+}
+
+long long gpurir_nsamples(double T, double fs) {
+  long long n = (long long)ceil(T * fs - 1e-6);  // reading C9
+  return n < 0 ? 0 : n;
+}
+
+double gpurir_sabine_t60(const float room_sz[3], const float beta[6]) { return sabine(room_sz, beta); }
+
+int gpurir_beta_sabine(const float room_sz[3], double T60, int sign, int clamp, float beta_out[6], int* clamped) {
+  if (clamped) *clamped = 0;
+  if (!(T60 > 0.0)) return GPURIR_EINVAL;
+  for (int i = 0; i < 3; i++)
+    if (!(room_sz[i] > 0.f)) return GPURIR_EINVAL;
+  double Lx = room_sz[0], Ly = room_sz[1], Lz = room_sz[2];
+  double V = Lx * Ly * Lz, S = 2.0 * (Lx * Ly + Lx * Lz + Ly * Lz);
+  double alpha = 0.161 * V / (T60 * S);
+  if (alpha > 1.0) {
+    if (!clamp) return GPURIR_EINFEASIBLE;
+    if (clamped) *clamped = 1;
+    for (int i = 0; i < 6; i++) beta_out[i] = 0.f;
+    return GPURIR_OK;
+  }
+  float b = (float)(sqrt(1.0 - alpha) * (sign < 0 ? -1.0 : 1.0));
+  for (int i = 0; i < 6; i++) beta_out[i] = b;
+  return GPURIR_OK;
+}
+
+double gpurir_att2t_sabine(double att_dB, double T60) { return att_dB / 60.0 * T60; }
+
+int gpurir_t2n(double T, const float room_sz[3], double c, int nb_img_out[3]) {
+  if (!(T > 0.0) || !(c > 0.0)) return GPURIR_EINVAL;
+  for (int i = 0; i < 3; i++) {
+    if (!(room_sz[i] > 0.f)) return GPURIR_EINVAL;
+    nb_img_out[i] = 2 * ((int)ceil(c * T / (double)room_sz[i]) + 1) + 1;
+  }
+  return GPURIR_OK;
+}
+
+long long gpurir_lut_table(double Tw, double fs, int Q, float* lut_out, long long cap) {
+  if (!(Tw > 0) || !(fs > 0) || Q < 1) return -GPURIR_EINVAL;
+  long long half = lut_half(Tw, fs, Q);
+  if (lut_out) {
+    if (cap < 2 * half + 1) return -GPURIR_EINVAL;
+    for (long long n = -half; n <= half; n++) lut_out[n + half] = (float)lut_entry(n, Tw, fs, Q, half);
+  }
+  return half;
+}
+
+int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float* pos_src, int M_src,
+                        const float* pos_rcv, int M_rcv, const float* orV_rcv, int mic_pattern, const int nb_img[3],
+                        double Tdiff, double Tmax, double fs, double c, float* out, const gpurir_opts* opts) {
+  gpurir_opts o;
+  if (opts) o = *opts; else gpurir_opts_default(&o);
+  if (!(o.Tw > 0)) o.Tw = 4e-3;
+  if (o.lut_Q <= 0) o.lut_Q = 16;
+  if (M_src <= 0 || M_rcv <= 0 || !pos_src || !pos_rcv || !out) return GPURIR_EINVAL;
+  if (!(fs > 0) || !(c > 0) || !(Tmax > 0) || !(Tdiff >= 0)) return GPURIR_EINVAL;
+  int st = validate_room(room_sz, beta, nb_img, mic_pattern);
+  if (st) return st;
+  if (mic_pattern != GPURIR_OMNI && !orV_rcv) return GPURIR_EINVAL;
+  if (o.mode < 0 || o.mode > 2) return GPURIR_EINVAL;
+  if (o.mode == GPURIR_LUT && (o.lut_Q & (o.lut_Q - 1))) return GPURIR_EINVAL;  // power of two
+  double H = o.Tw * fs / 2.0;
+  if ((int)ceil((kTC + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;  // window too long for a tile
+  long long nS = gpurir_nsamples(Tmax, fs);
+  long long nISM = gpurir_nsamples(Tdiff, fs);
+  if (nISM > nS) nISM = nS;
+  if (nS > (1LL << 30)) return GPURIR_EINVAL;
+  long long M = (long long)M_src * M_rcv;
+  if (M > (1LL << 30)) return GPURIR_EINVAL;
+
+  DeviceState* d = device_state(&st);
+  if (!d) return st;
+  cudaStream_t stream = (cudaStream_t)o.stream;
+
+  if (nISM > 0) {
+    IsmArgs A;
+    memset(&A, 0, sizeof(A));
+    for (int i = 0; i < 3; i++) { A.L[i] = room_sz[i]; A.nb[i] = nb_img[i]; }
+    for (int i = 0; i < 6; i++) A.beta[i] = beta[i];
+    A.pattern = mic_pattern;
+    A.pos_src = pos_src; A.pos_rcv = pos_rcv; A.orv = mic_pattern == GPURIR_OMNI ? nullptr : orV_rcv;
+    A.M_src = M_src; A.M_rcv = M_rcv; A.M = (int)M;
+    A.nISM = (int)nISM;
+    A.row_stride = nS;
+    A.nTiles = (int)((nISM + kTC - 1) / kTC);
+    fill_common(A, fs, c, o.Tw);
+    A.out = out;
+    A.status = d->status;
+    if (o.mode == GPURIR_LUT) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      st = ensure_lut(d, o.Tw, fs, o.lut_Q, H, stream);
+      if (st) return st;
+      A.lut = d->lut; A.lut_rows = d->lut_rows; A.lut_cols = d->lut_cols; A.lut_joff = d->lut_joff;
+      A.lutQ = o.lut_Q;
+    }
+    long long nclusters = (long long)A.nTiles * M;
+    int split = auto_split(nclusters, o.split);
+    cudaError_t e = launch_ism(A, o.mode, split, nclusters, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_ism");
+  }
+  if (nISM < nS) {
+    TailArgs T;
+    memset(&T, 0, sizeof(T));
+    T.pos_src = pos_src; T.pos_rcv = pos_rcv; T.M_rcv = M_rcv; T.M = (int)M;
+    T.nISM = (int)nISM; T.nS = (int)nS; T.row_stride = nS;
+    double T60 = sabine(room_sz, beta);
+    T.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);  // Eq. 8, reading C14
+    T.rir_base = o.rir_index_base;
+    T.fs_over_c = fs / c;
+    T.win = (int)llround(0.010 * fs);
+    T.seed = o.seed;
+    T.out = out;
+    long long groups = (nS + 3) / 4 - nISM / 4;
+    T.chunks_per_rir = (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4));
+    cudaError_t e = launch_tail(T, (long long)T.chunks_per_rir * M, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_tail");
+  }
+  return finish(o, stream, d);
+}
+
+int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, float* out,
+                              const gpurir_opts* opts) {
+  gpurir_opts o;
+  if (opts) o = *opts; else gpurir_opts_default(&o);
+  if (!(o.Tw > 0)) o.Tw = 4e-3;
+  if (o.lut_Q <= 0) o.lut_Q = 16;
+  if (n_rooms <= 0 || !rooms || !out || !(fs > 0) || !(c > 0)) return GPURIR_EINVAL;
+  if (o.mode < 0 || o.mode > 2) return GPURIR_EINVAL;
+  if (o.mode == GPURIR_LUT && (o.lut_Q & (o.lut_Q - 1))) return GPURIR_EINVAL;
+  double H = o.Tw * fs / 2.0;
+  if ((int)ceil((kTC + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;
+
+  std::vector<BatchJob> jobs(n_rooms);
+  std::vector<int2> tiles, chunks;
+  std::vector<std::pair<double, int2>> order;  // (estimated cost, (job, tile)) for heavy-first scheduling
+  for (int i = 0; i < n_rooms; i++) {
+    const gpurir_room& R = rooms[i];
+    if (int st = validate_room(R.room_sz, R.beta, R.nb_img, R.mic_pattern)) return st;
+    if (!(R.Tmax > 0) || !(R.Tdiff >= 0) || R.out_offset < 0) return GPURIR_EINVAL;
+    BatchJob& J = jobs[i];
+    memset(&J, 0, sizeof(J));
+    for (int a = 0; a < 3; a++) {
+      J.L[a] = R.room_sz[a]; J.src[a] = R.pos_src[a]; J.rcv[a] = R.pos_rcv[a]; J.orv[a] = R.orV_rcv[a];
+      J.nb[a] = R.nb_img[a];
+    }
+    for (int w = 0; w < 6; w++) J.beta[w] = R.beta[w];
+    J.pattern = R.mic_pattern;
+    long long nS = gpurir_nsamples(R.Tmax, fs), nISM = gpurir_nsamples(R.Tdiff, fs);
+    if (nISM > nS) nISM = nS;
+    if (nS > (1LL << 30)) return GPURIR_EINVAL;
+    J.nISM = (int)nISM; J.nS = (int)nS; J.out_offset = R.out_offset;
+    double T60 = sabine(R.room_sz, R.beta);
+    J.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);
+    J.rir_global = o.rir_index_base + (unsigned long long)i;
+    int nT = (int)((nISM + kTC - 1) / kTC);
+    double V = (double)R.room_sz[0] * R.room_sz[1] * R.room_sz[2];
+    for (int t = 0; t < nT; t++) {
+      double tm = (t + 1) * kTC / fs;  // image density ~ 4 pi c^3 t^2 / V (SURVEY §7 hard part 2)
+      order.push_back({tm * tm / V + 1e-9, make_int2(i, t)});
+    }
+    long long groups = (nS + 3) / 4 - nISM / 4;
+    int nch = nISM < nS ? (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4)) : 0;
+    for (int ch = 0; ch < nch; ch++) chunks.push_back(make_int2(i, ch));
+  }
+  std::stable_sort(order.begin(), order.end(),
+                   [](const std::pair<double, int2>& a, const std::pair<double, int2>& b) { return a.first > b.first; });
+  tiles.reserve(order.size());
+  for (auto& p : order) tiles.push_back(p.second);
+
+  int st = GPURIR_OK;
+  DeviceState* d = device_state(&st);
+  if (!d) return st;
+  cudaStream_t stream = (cudaStream_t)o.stream;
+
+  size_t bj = jobs.size() * sizeof(BatchJob), bt = tiles.size() * sizeof(int2), bc = chunks.size() * sizeof(int2);
+  size_t total = bj + bt + bc + 64;
+  unsigned char* ws = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&ws, total, stream);
+  if (e != cudaSuccess) return GPURIR_ENOMEM;
+  BatchJob* djobs = (BatchJob*)ws;
+  int2* dtiles = (int2*)(ws + ((bj + 15) & ~(size_t)15));
+  int2* dchunks = dtiles + tiles.size();
+  // the host vectors must outlive the async copies: copy, then synchronise before returning
+  e = cudaMemcpyAsync(djobs, jobs.data(), bj, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess && bt) e = cudaMemcpyAsync(dtiles, tiles.data(), bt, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess && bc) e = cudaMemcpyAsync(dchunks, chunks.data(), bc, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "batch upload"); }
+
+  if (!tiles.empty()) {
+    IsmArgs A;
+    memset(&A, 0, sizeof(A));
+    A.jobs = djobs; A.tiles = dtiles;
+    fill_common(A, fs, c, o.Tw);
+    A.out = out;
+    A.status = d->status;
+    if (o.mode == GPURIR_LUT) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      st = ensure_lut(d, o.Tw, fs, o.lut_Q, H, stream);
+      if (st) { cudaFreeAsync(ws, stream); return st; }
+      A.lut = d->lut; A.lut_rows = d->lut_rows; A.lut_cols = d->lut_cols; A.lut_joff = d->lut_joff;
+      A.lutQ = o.lut_Q;
+    }
+    int split = auto_split((long long)tiles.size(), o.split);
+    e = launch_ism(A, o.mode, split, (long long)tiles.size(), stream);
+    if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_ism(batch)"); }
+  }
+  if (!chunks.empty()) {
+    TailArgs T;
+    memset(&T, 0, sizeof(T));
+    T.jobs = djobs; T.chunks = dchunks;
+    T.fs_over_c = fs / c;
+    T.win = (int)llround(0.010 * fs);
+    T.seed = o.seed;
+    T.out = out;
+    e = launch_tail(T, (long long)chunks.size(), stream);
+    if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_tail(batch)"); }
+  }
+  cudaFreeAsync(ws, stream);
+  e = cudaStreamSynchronize(stream);  // host staging vectors are released on return
+  if (e != cudaSuccess) return cuda_fail(e, "batch sync");
+  return finish(o, stream, d);
+}
+
+int gpurir_image_params(const float room_sz[3], const float beta[6], const float src[3], const float rcv[3],
+                        const float orv[3], int mic_pattern, const int nb_img[3], double fs, double c,
+                        double* x_out, float* A_out, void* stream_) {
+  int st = validate_room(room_sz, beta, nb_img, mic_pattern);
+  if (st) return st;
+  if (!(fs > 0) || !(c > 0) || !x_out || !A_out || !src || !rcv) return GPURIR_EINVAL;
+  DeviceState* d = device_state(&st);
+  if (!d) return st;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  BatchJob J;
+  memset(&J, 0, sizeof(J));
+  for (int a = 0; a < 3; a++) {
+    J.L[a] = room_sz[a]; J.src[a] = src[a]; J.rcv[a] = rcv[a]; J.orv[a] = orv ? orv[a] : 0.f; J.nb[a] = nb_img[a];
+  }
+  for (int w = 0; w < 6; w++) J.beta[w] = beta[w];
+  J.pattern = mic_pattern;
+  if (mic_pattern != GPURIR_OMNI && !orv) return GPURIR_EINVAL;
+  BatchJob* dj = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&dj, sizeof(BatchJob), stream);
+  if (e != cudaSuccess) return GPURIR_ENOMEM;
+  e = cudaMemcpyAsync(dj, &J, sizeof(J), cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "image_params upload");
+  IsmArgs A;
+  memset(&A, 0, sizeof(A));
+  A.jobs = dj;
+  fill_common(A, fs, c, 4e-3);
+  A.status = d->status;
+  long long N = (long long)nb_img[0] * nb_img[1] * nb_img[2];
+  e = launch_image_params(A, x_out, A_out, N, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "launch_image_params");
+  cudaFreeAsync(dj, stream);
+  gpurir_opts o;
+  gpurir_opts_default(&o);
+  o.flags = GPURIR_FLAG_SYNC;
+  return finish(o, stream, d);
+}
+
+int gpurir_device_status(int reset) {
+  int st = GPURIR_OK;
+  DeviceState* d = device_state(&st);
+  if (!d) return st;
+  int s = 0;
+  cudaError_t e = cudaMemcpy(&s, d->status, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "status");
+  if (reset) cudaMemset(d->status, 0, sizeof(int));
+  if (!s) return GPURIR_OK;
+  return (s & kStatusDegenerate) ? GPURIR_EDEGENERATE : GPURIR_EINVAL;
+}
+
+const char* gpurir_strerror(int status) {
+  switch (status) {
+    case GPURIR_OK: return "ok";
+    case GPURIR_EINVAL: return "invalid argument";
+    case GPURIR_EDEGENERATE: return "degenerate geometry (image source on a receiver)";
+    case GPURIR_EINFEASIBLE: return "infeasible target T60";
+    case GPURIR_ENOMEM: return "out of device memory";
+    case GPURIR_ECUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+const char* gpurir_last_cuda_error(void) { return g_cuda_err; }
+
+const char* gpurir_version(void) { return "gpurir-b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

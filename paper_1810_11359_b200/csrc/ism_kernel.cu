@@ -1,0 +1,560 @@
+// ism_kernel.cu — fused image-parameter + delay-binning + RIR-accumulation kernel
+// (hot-path rows a1, a2, a3, a4, a5 of SURVEY.md §8(a)) for sm_100a.
+//
+// What it computes (§2.1-2.2, Eqs. 1-6):
+//   h[m][k] = sum_n A_n * delta'(k/fs - tau_n),   0 <= k < nISM,
+//   A_n = beta_n g_n / (4 pi d_n), tau_n = d_n / c, delta' = Hann-windowed sinc of length T_w.
+// How: one CTA owns a tile of kTC output samples of one RIR.
+// It enumerates only the lattice images whose window can touch the tile (a
+// spherical shell around the receiver) column by column (n_x, n_y) with the
+// n_z ranges solved in closed form, computes each image's parameters in
+// registers (fp64 delay split, C1/C2/C4), bins the records by delay with a
+// stable counting sort in shared memory (deterministic order), and then every
+// warp accumulates its kS-sample sub-tile from the contiguous record range of
+// its bins: 4 lane groups x 2 packed (f32x2) records per step, accumulators in
+// registers, shuffle reduction at the end, no global atomics.  Thread-block
+// clusters split the images of one tile across `split` CTAs whose partial
+// tiles are reduced through distributed shared memory (fixed order).
+#include <cooperative_groups.h>
+#include <cuda_fp16.h>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace gpurir {
+
+// ----------------------------------------------------------------------------
+// shared-memory layout
+// ----------------------------------------------------------------------------
+struct ColRec {         // one lattice column (n_x, n_y) of the current batch (32 B)
+  double rho2;          // (x_n - x_r)^2 + (y_n - y_r)^2
+  float dx, dy;         // x_n - x_r, y_n - y_r (directivity)
+  float lxy;            // log2 |beta product| of the x and y walls
+  int r1lo, r2lo;       // n_z ranges [r1lo, r1lo + r1n) then [r2lo, ...)
+  uint32_t r1n_flags;   // r1n | sign << 30 | zero << 31
+};
+
+struct TileInfo {
+  RirGeom g;
+  double dlo2, dhi2;    // shell in distance^2
+  int m, tile, t0, te, tc;
+  int nx0, ny0, NX, ncols_mine;
+  long long row;        // element offset of the RIR row
+  float xrel_max;       // records with xrel in (0, xrel_max) are kept
+  int nbins;
+};
+
+struct Smem {
+  TileInfo ti;
+  int colpre[kColBatch];          // inclusive prefix of candidate counts
+  ColRec col[kColBatch];
+  float2 rec[kCap];               // unsorted records: fp32/fp16 (-x/H, C'), LUT (rowbase, phi)
+  float recA[kCap];               // LUT amplitude
+  uint8_t bin[kCap];
+  float4 sorted[kCap + 8];        // sorted records; fp32/fp16 modes pack pairs
+  int warpcnt[kWarps][kMaxBins];  // per-warp bin counts -> offsets
+  int binstart[kMaxBins + 1];
+  int scan_tmp[kWarps];
+  float outtile[kTC];
+};
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// Block-wide inclusive scan (kThreads values); returns the inclusive prefix for this thread.
+__device__ __forceinline__ int block_incl_scan(int v, int* tmp) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = warp_incl_scan(v, lane);
+  if (lane == 31) tmp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < kWarps ? tmp[lane] : 0;
+    t = warp_incl_scan(t, lane);
+    if (lane < kWarps) tmp[lane] = t;
+  }
+  __syncthreads();
+  int r = x + (w > 0 ? tmp[w - 1] : 0);
+  __syncthreads();
+  return r;
+}
+
+// ----------------------------------------------------------------------------
+// Per-RIR geometry (single-room call or batch job)
+// ----------------------------------------------------------------------------
+__device__ void load_geom(const IsmArgs& A, int m, RirGeom& g, int* status) {
+  float L[3], beta[6], src[3], rcv[3], orv[3] = {0.f, 0.f, 0.f};
+  int nb[3], pattern;
+  if (A.jobs) {
+    const BatchJob& J = A.jobs[m];
+    for (int i = 0; i < 3; i++) { L[i] = J.L[i]; src[i] = J.src[i]; rcv[i] = J.rcv[i]; orv[i] = J.orv[i]; nb[i] = J.nb[i]; }
+    for (int i = 0; i < 6; i++) beta[i] = J.beta[i];
+    pattern = J.pattern;
+  } else {
+    int ms = m / A.M_rcv, mr = m % A.M_rcv;
+    for (int i = 0; i < 3; i++) {
+      L[i] = A.L[i]; nb[i] = A.nb[i];
+      src[i] = A.pos_src[3 * ms + i];
+      rcv[i] = A.pos_rcv[3 * mr + i];
+      if (A.orv) orv[i] = A.orv[3 * mr + i];
+    }
+    for (int i = 0; i < 6; i++) beta[i] = A.beta[i];
+    pattern = A.pattern;
+  }
+  const float pa[5] = {1.f, 0.75f, 0.5f, 0.25f, 0.f};  // C4
+  g.a = pa[pattern];
+  float on = sqrtf(orv[0] * orv[0] + orv[1] * orv[1] + orv[2] * orv[2]);
+  if (pattern != 0 && !(on > 0.f)) { atomicOr(status, kStatusZeroOrient); on = 1.f; }
+  for (int i = 0; i < 3; i++) {
+    g.L[i] = L[i]; g.s[i] = src[i]; g.r[i] = rcv[i];
+    g.o[i] = pattern != 0 ? orv[i] / on : 0.f;
+    g.nlo[i] = -(nb[i] / 2);          // ceil(-N/2)
+    g.nhi[i] = (nb[i] + 1) / 2;       // ceil(N/2)
+  }
+  g.neg = 0; g.zero = 0;
+  for (int w = 0; w < 6; w++) {
+    float b = beta[w];
+    if (b < 0.f) g.neg |= 1u << w;
+    if (b == 0.f) { g.zero |= 1u << w; g.lb[w] = 0.f; }
+    else g.lb[w] = log2f(fabsf(b));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// The kernel
+// ----------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  float2* lut = reinterpret_cast<float2*>(smem_raw + sizeof(Smem));
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int P = (int)cluster.num_blocks();
+  const int prank = (int)cluster.block_rank();
+  const int cid = blockIdx.x / P;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double c_over_fs = A.c_over_fs;
+  const float H = A.H;
+
+  // ---- tile setup (thread 0) ------------------------------------------------
+  if (tid == 0) {
+    TileInfo& T = sm.ti;
+    int m, tile, nISM;
+    long long row;
+    if (A.jobs) {
+      int2 jt = A.tiles[cid];
+      m = jt.x; tile = jt.y;
+      nISM = A.jobs[m].nISM;
+      row = A.jobs[m].out_offset;
+    } else {
+      tile = A.nTiles - 1 - cid / A.M;  // heaviest (latest) tiles first
+      m = cid % A.M;
+      nISM = A.nISM;
+      row = (long long)m * A.row_stride;
+    }
+    load_geom(A, m, T.g, A.status);
+    T.m = m; T.tile = tile; T.row = row;
+    T.t0 = tile * kTC;
+    T.te = min(T.t0 + kTC, nISM);
+    T.tc = T.t0 + kTC / 2;
+    // shell: images with x in (t0 - H, te - 1 + H) can touch samples [t0, te)
+    double xlo = (double)T.t0 - H, xhi = (double)(T.te - 1) + H;
+    double dlo = xlo > 0.0 ? xlo * c_over_fs : 0.0;
+    double dhi = xhi * c_over_fs;
+    T.dlo2 = dlo * dlo;
+    T.dhi2 = dhi * dhi;
+    T.xrel_max = (float)(T.te - 1 - T.t0) + 2.f * H;
+    int lo[2], hi[2];
+    for (int ax = 0; ax < 2; ax++) {
+      double L = T.g.L[ax], r = T.g.r[ax];
+      int a = (int)floor((r - dhi) / L) - 1, b = (int)floor((r + dhi) / L) + 1;
+      lo[ax] = max(a, T.g.nlo[ax]);
+      hi[ax] = min(b, T.g.nhi[ax] - 1);
+    }
+    T.nx0 = lo[0]; T.ny0 = lo[1];
+    T.NX = max(0, hi[0] - lo[0] + 1);
+    int NY = max(0, hi[1] - lo[1] + 1);
+    long long ncols = (long long)T.NX * NY;
+    T.ncols_mine = (int)((ncols - prank + P - 1) / P);
+    if (T.ncols_mine < 0) T.ncols_mine = 0;
+    T.nbins = (int)ceilf(((float)kTC + 2.f * H) / (float)kS) + 1;
+  }
+  // LUT table -> shared memory
+  if (MODE == 1) {
+    int n = A.lut_rows * A.lut_cols;
+    for (int i = tid; i < n; i += kThreads) lut[i] = A.lut[i];
+  }
+  __syncthreads();
+  const TileInfo& T = sm.ti;
+  const RirGeom& g = T.g;
+  const int nbins = T.nbins;
+
+  // ---- per-lane accumulation constants ---------------------------------------
+  const int grp = lane >> 3, li = lane & 7;
+  const int s0 = warp * kS;                 // sub-tile start relative to t0
+  const int kf = T.t0 + s0 + li - T.tc;     // sample relative to tc (integer)
+  float2 acc2 = make_float2(0.f, 0.f);
+  const float kv = (float)kf * A.invH;      // fp32 mode: v = (k - x)/H
+  const float kx = (float)kf * (0.5f * A.invH);  // fp16 mode: x = (k - x)/(2H)
+  const int bfirst = warp, blast = warp + A.nbw;  // bins [bfirst, blast) touch this sub-tile
+
+  const double fs_over_c = A.fs_over_c;
+  const double sc2 = fs_over_c * fs_over_c;
+  const float inv4pi = 0.0795774715459476679f;
+
+  for (int qb = 0; qb < T.ncols_mine; qb += kColBatch) {
+    // ---- column records (one column per thread) ------------------------------
+    int cnt = 0;
+    {
+      int q = qb + tid;
+      ColRec cr;
+      cr.r1lo = 0; cr.r2lo = 0;
+      int r1n = 0;
+      uint32_t fl = 0;
+      if (q < T.ncols_mine) {
+        int ci = prank + P * q;
+        int nx = T.nx0 + ci % T.NX, ny = T.ny0 + ci / T.NX;
+        double dx = image_coord(nx, g.L[0], g.s[0]) - g.r[0];
+        double dy = image_coord(ny, g.L[1], g.s[1]) - g.r[1];
+        double rho2 = dx * dx + dy * dy;
+        cr.rho2 = rho2; cr.dx = (float)dx; cr.dy = (float)dy;
+        uint32_t sgn = 0; bool zero = false;
+        cr.lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
+        fl = (sgn << 30) | (zero ? (1u << 31) : 0u);
+        if (rho2 < T.dhi2) {
+          double zhi = sqrt(T.dhi2 - rho2);
+          double zlo = T.dlo2 > rho2 ? sqrt(T.dlo2 - rho2) : 0.0;
+          double Lz = g.L[2], rz = g.r[2];
+          // cells [nL, (n+1)L] meeting (zlo, zhi) (positive side) / (-zhi, -zlo), widened by one cell
+          int plo = (int)floor((rz + zlo) / Lz) - 1, phi = (int)ceil((rz + zhi) / Lz);
+          int nlo = (int)floor((rz - zhi) / Lz) - 1, nhi = (int)ceil((rz - zlo) / Lz);
+          int zl = g.nlo[2], zh = g.nhi[2] - 1;
+          if (nhi >= plo - 1) { plo = min(plo, nlo); nlo = 1; nhi = 0; }  // merged
+          plo = max(plo, zl); phi = min(phi, zh);
+          nlo = max(nlo, zl); nhi = min(nhi, zh);
+          int n1 = max(0, phi - plo + 1), n2 = max(0, nhi - nlo + 1);
+          cr.r1lo = plo; r1n = n1; cr.r2lo = nlo;
+          cnt = n1 + n2;
+        }
+      }
+      cr.r1n_flags = (uint32_t)r1n | fl;
+      sm.col[tid] = cr;
+    }
+    int incl = block_incl_scan(cnt, sm.scan_tmp);
+    sm.colpre[tid] = incl;
+    __syncthreads();
+    const int total = sm.colpre[kColBatch - 1];
+
+    for (int base = 0; base < total; base += kCap) {
+      const int nw = min(kCap, total - base);
+      // ---- emission: image parameters (Eqs. 1-4, A16) -> records ---------------
+      for (int i = tid; i < nw; i += kThreads) {
+        int gi = base + i;
+        int lo = 0, hi = kColBatch - 1;  // first column with colpre > gi
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (sm.colpre[mid] > gi) hi = mid; else lo = mid + 1;
+        }
+        const ColRec& cr = sm.col[lo];
+        int l = gi - (lo > 0 ? sm.colpre[lo - 1] : 0);
+        const int r1n = (int)(cr.r1n_flags & 0x3FFFFFFFu);
+        int nz = l < r1n ? cr.r1lo + l : cr.r2lo + (l - r1n);
+        double dz = image_coord(nz, g.L[2], g.s[2]) - g.r[2];
+        double x2 = fma(dz, dz, cr.rho2) * sc2;  // (d fs / c)^2
+        uint8_t b = kDiscard;
+        float2 rec = make_float2(0.f, 0.f);
+        float recA = 0.f;
+        if (x2 == 0.0) {
+          atomicOr(A.status, kStatusDegenerate);
+        } else {
+          float x0f;
+          float xr = delay_rel(x2, T.tc, x0f);
+          float xrel = xr + (float)(kTC / 2) + H;  // x - (t0 - H)
+          if (xrel > 0.f && xrel < T.xrel_max) {
+            b = (uint8_t)(int)(xrel * (1.f / (float)kS));
+            // amplitude A = beta_n g / (4 pi d), 1/d = fs / (c x)
+            float invd = (float)fs_over_c * __frcp_rn(x0f);
+            uint32_t sgn = (cr.r1n_flags >> 30) & 1u;
+            bool zero = (cr.r1n_flags >> 31) != 0;
+            float lz = axis_beta(nz, 2, g, sgn, zero);
+            float bn = zero ? 0.f : exp2f(cr.lxy + lz);
+            if (sgn) bn = -bn;
+            float cth = (cr.dx * g.o[0] + cr.dy * g.o[1] + (float)dz * g.o[2]) * invd;
+            float gain = g.a + (1.f - g.a) * cth;
+            float amp = bn * gain * invd * inv4pi;
+            if (MODE == 1) {
+              // Eq. 9 LUT: position u Q = kf Q - xq, xq = xr Q = iq + phi
+              float xq = xr * (float)A.lutQ;
+              float fiq = floorf(xq);
+              float phi = xq - fiq;
+              int iq1 = (int)fiq + 1;
+              int php = iq1 & (A.lutQ - 1);           // (iq+1) mod Q (Q power of 2)
+              int aa = (iq1 - php) / A.lutQ;            // floor((iq+1)/Q)
+              int ph = (A.lutQ - php) & (A.lutQ - 1);
+              int jsh = aa + (php > 0 ? 1 : 0);
+              int rowbase = ph * A.lut_cols + A.lut_joff - jsh;
+              rec = make_float2(__int_as_float(rowbase), phi);
+              recA = amp;
+            } else {
+              // hoisted sinc numerator: sin(pi u) = -(-1)^(kf - j) sin(pi f), u = kf - xr, xr = j + f
+              float fj = floorf(xr);
+              float f = xr - fj;
+              if (f == 0.f) {  // exact integer delay: nudge by one ulp (C-nudge)
+                xr = nextafterf(xr, 1e30f);
+                fj = floorf(xr);
+                f = xr - fj;
+              }
+              int j = (int)fj;
+              float cc = -amp * sinpif(f) * 0.318309886183790672f;
+              if (j & 1) cc = -cc;
+              if (MODE == 0) rec = make_float2(-xr * A.invH, cc * A.invH);
+              else rec = make_float2(-xr * (0.5f * A.invH), cc * (0.5f * A.invH) * 1024.f);
+            }
+          }
+        }
+        sm.rec[i] = rec;
+        if (MODE == 1) sm.recA[i] = recA;
+        sm.bin[i] = b;
+      }
+      // clear per-warp bin counters
+      for (int i = tid; i < kWarps * kMaxBins; i += kThreads) (&sm.warpcnt[0][0])[i] = 0;
+      __syncthreads();
+
+      // ---- stable counting sort by delay bin (deterministic order) -------------
+      const int per_warp = (nw + kWarps - 1) / kWarps;
+      const int wbeg = warp * per_warp, wend = min(nw, wbeg + per_warp);
+      const unsigned lt = (1u << lane) - 1u;
+      for (int r0 = wbeg; r0 < wend; r0 += 32) {
+        int r = r0 + lane;
+        int b = r < wend ? (int)sm.bin[r] : (int)kDiscard;
+        unsigned peers = __match_any_sync(0xffffffffu, b);
+        if (b != kDiscard && (peers & lt) == 0) sm.warpcnt[warp][b] += __popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();
+      if (tid < nbins) {  // per bin: prefix over warps
+        int s = 0;
+        for (int w = 0; w < kWarps; w++) { int c = sm.warpcnt[w][tid]; sm.warpcnt[w][tid] = s; s += c; }
+        sm.binstart[tid] = s;  // bin total for now
+      }
+      __syncthreads();
+      if (warp == 0) {  // exclusive scan of bin totals (nbins <= 128)
+        int carry = 0;
+        for (int b0 = 0; b0 < nbins; b0 += 32) {
+          int b = b0 + lane;
+          int v = b < nbins ? sm.binstart[b] : 0;
+          int x = warp_incl_scan(v, lane);
+          if (b < nbins) sm.binstart[b] = carry + x - v;
+          carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) sm.binstart[nbins] = carry;
+      }
+      __syncthreads();
+      for (int r0 = wbeg; r0 < wend; r0 += 32) {
+        int r = r0 + lane;
+        int b = r < wend ? (int)sm.bin[r] : (int)kDiscard;
+        unsigned peers = __match_any_sync(0xffffffffu, b);
+        if (b != kDiscard) {
+          int pos = sm.binstart[b] + sm.warpcnt[warp][b] + __popc(peers & lt);
+          float2 rc = sm.rec[r];
+          if (MODE == 1) {
+            sm.sorted[pos] = make_float4(rc.x, rc.y, sm.recA[r], 0.f);
+          } else {  // pair layout: sorted[p>>1] = (nxv_even, nxv_odd, C_even, C_odd)
+            float* pp = reinterpret_cast<float*>(&sm.sorted[pos >> 1]);
+            pp[pos & 1] = rc.x;
+            pp[2 + (pos & 1)] = rc.y;
+          }
+        }
+        __syncwarp();
+        if (b != kDiscard && (peers & lt) == 0) sm.warpcnt[warp][b] += __popc(peers);
+        __syncwarp();
+      }
+      // dummy records after the last one (never in any window: v = kv - 1e4)
+      if (tid < 8) {
+        int pos = sm.binstart[nbins] + tid;
+        if (MODE == 1) {
+          sm.sorted[pos] = make_float4(__int_as_float(0), 0.f, 0.f, 0.f);
+        } else {
+          float* pp = reinterpret_cast<float*>(&sm.sorted[pos >> 1]);
+          pp[pos & 1] = -1.0e4f;
+          pp[2 + (pos & 1)] = 0.f;
+        }
+      }
+      __syncthreads();
+
+      // ---- accumulation: warp sub-tile from its contiguous record range --------
+      const int ra = sm.binstart[bfirst], rb = sm.binstart[min(blast, nbins)];
+      if (MODE == 0) {
+        const float2 kv2 = make_float2(kv, kv);
+        const float2 m1 = make_float2(-1.f, -1.f);
+        const float2 z2 = make_float2(0.f, 0.f);
+        for (int j = (ra & ~1) + 2 * grp; j < rb; j += 2 * kG) {
+          float4 pr = sm.sorted[j >> 1];
+          float2 v = __fadd2_rn(kv2, make_float2(pr.x, pr.y));     // v = (k - x) / H
+          float2 sp = __ffma2_rn(v, v, m1);                          // s' = v^2 - 1
+          sp.x = fminf(sp.x, 0.f); sp.y = fminf(sp.y, 0.f);          // window support |v| < 1
+          float2 p = __ffma2_rn(make_float2(kWb3, kWb3), sp, make_float2(kWb2, kWb2));
+          p = __ffma2_rn(p, sp, make_float2(kWb1, kWb1));
+          p = __ffma2_rn(p, sp, make_float2(kWb0, kWb0));
+          float2 cw = __fmul2_rn(p, sp);                             // -cos(pi v / 2)
+          float2 w = __fmul2_rn(cw, cw);                             // Hann window (Eq. 6)
+          float2 r;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(v.x));
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(v.y));
+          float2 t = __fmul2_rn(w, r);
+          acc2 = __ffma2_rn(make_float2(pr.z, pr.w), t, acc2);       // += C' w / v
+        }
+        (void)z2;
+      } else if (MODE == 2) {
+        // fp16 / half2: t - tau in fp32, window by the Eq. 11 polynomial
+        // cos(pi x) at x = u / (2H) (reading C12), half2 Horner (Eq. 12), fp32 accumulation (C13).
+        const float2 kx2 = make_float2(kx, kx);
+        const __half2 c6 = __float2half2_rn(-1.2294921875f), c4 = __float2half2_rn(4.04296875f);
+        const __half2 c2 = __float2half2_rn(-4.93359375f), c0 = __float2half2_rn(1.f);
+        const __half2 quarter = __float2half2_rn(0.25f);
+        __half2 acch = __float2half2_rn(0.f);
+        int steps = 0;
+        for (int j = (ra & ~1) + 2 * grp; j < rb; j += 2 * kG) {
+          float4 pr = sm.sorted[j >> 1];
+          float2 x = __fadd2_rn(kx2, make_float2(pr.x, pr.y));      // x = (k - tau fs) / (2H), fp32
+          __half2 hx = __float22half2_rn(x);
+          __half2 x2 = __hmin2(__hmul2(hx, hx), quarter);            // clamp: |x| <= 1/2 (window edge)
+          __half2 p = __hfma2(c6, x2, c4);
+          p = __hfma2(p, x2, c2);
+          p = __hfma2(p, x2, c0);                                    // cos(pi x), Eq. 11
+          __half2 w = __hmul2(p, p);                                 // Hann window
+          float2 r;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(x.x));
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(x.y));
+          float2 q = __fmul2_rn(make_float2(pr.z, pr.w), r);         // bounded by ~A (scaled 2^10)
+          acch = __hfma2(w, __float22half2_rn(q), acch);
+          if (++steps == 8) {
+            float2 f = __half22float2(acch);
+            acc2.x += f.x; acc2.y += f.y;
+            acch = __float2half2_rn(0.f);
+            steps = 0;
+          }
+        }
+        float2 f = __half22float2(acch);
+        acc2.x += f.x; acc2.y += f.y;
+      } else {
+        // LUT (Eq. 9): one table pair per tap, phase-major rows, linear interpolation
+        for (int j = ra + grp; j < rb; j += kG) {
+          float4 rc = sm.sorted[j];
+          int idx = __float_as_int(rc.x) + kf;
+          float2 d = lut[idx];
+          acc2.x = fmaf(rc.z, fmaf(rc.y, d.y, d.x), acc2.x);
+        }
+      }
+      __syncthreads();  // records of this window are consumed
+    }
+  }
+
+  // ---- reduce lane groups, apply the lane sign, write the tile ----------------
+  float acc = acc2.x + acc2.y;
+  acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+  if (MODE == 0) { if (kf & 1) acc = -acc; }
+  else if (MODE == 2) { acc *= (1.f / 1024.f); if (kf & 1) acc = -acc; }
+  if (grp == 0) sm.outtile[s0 + li] = acc;
+  if (P > 1) {
+    cluster.sync();
+    if (prank == 0 && tid < kTC) {
+      float s = sm.outtile[tid];
+      for (int r = 1; r < P; r++) s += cluster.map_shared_rank(&sm.outtile[0], r)[tid];
+      sm.outtile[tid] = s;
+    }
+    cluster.sync();
+  } else {
+    __syncthreads();
+  }
+  if (prank == 0 && tid < T.te - T.t0) A.out[T.row + T.t0 + tid] = sm.outtile[tid];
+}
+
+// ----------------------------------------------------------------------------
+// image-parameter hook (gpurir_image_params): one thread per lattice image
+// ----------------------------------------------------------------------------
+__global__ void image_params_kernel(IsmArgs A, double* x_out, float* A_out) {
+  __shared__ RirGeom g;
+  if (threadIdx.x == 0) load_geom(A, 0, g, A.status);
+  __syncthreads();
+  int Nx = g.nhi[0] - g.nlo[0], Ny = g.nhi[1] - g.nlo[1], Nz = g.nhi[2] - g.nlo[2];
+  long long N = (long long)Nx * Ny * Nz;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    int nx = g.nlo[0] + (int)(i % Nx), ny = g.nlo[1] + (int)((i / Nx) % Ny), nz = g.nlo[2] + (int)(i / ((long long)Nx * Ny));
+    double dx = image_coord(nx, g.L[0], g.s[0]) - g.r[0];
+    double dy = image_coord(ny, g.L[1], g.s[1]) - g.r[1];
+    double dz = image_coord(nz, g.L[2], g.s[2]) - g.r[2];
+    double x2 = fma(dz, dz, dx * dx + dy * dy) * (A.fs_over_c * A.fs_over_c);
+    if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); x_out[i] = 0.0; A_out[i] = 0.f; continue; }
+    float x0f;
+    float xr = delay_rel(x2, 0, x0f);  // reference 0: full delay in fp32 + fp64 residual
+    double x0d = (double)x0f;
+    double xfull = x0d + (x2 - x0d * x0d) / (2.0 * x0d);
+    (void)xr;
+    float invd = (float)A.fs_over_c * __frcp_rn(x0f);
+    uint32_t sgn = 0; bool zero = false;
+    float lb = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero) + axis_beta(nz, 2, g, sgn, zero);
+    float bn = zero ? 0.f : exp2f(lb);
+    if (sgn) bn = -bn;
+    float cth = ((float)dx * g.o[0] + (float)dy * g.o[1] + (float)dz * g.o[2]) * invd;
+    float gain = g.a + (1.f - g.a) * cth;
+    x_out[i] = xfull;
+    A_out[i] = bn * gain * invd * 0.0795774715459476679f;
+  }
+}
+
+size_t ism_smem_bytes(int mode, int lut_rows, int lut_cols) {
+  size_t s = sizeof(Smem);
+  if (mode == 1) s += (size_t)lut_rows * lut_cols * sizeof(float2);
+  return s;
+}
+
+cudaError_t launch_ism(const IsmArgs& A, int mode, int split, long long nclusters, cudaStream_t stream) {
+  size_t smem = ism_smem_bytes(mode, A.lut_rows, A.lut_cols);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nclusters * split), 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = split;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  switch (mode) {
+    case 0:
+      e = cudaFuncSetAttribute(ism_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      return cudaLaunchKernelEx(&cfg, ism_kernel<0>, A);
+    case 1:
+      e = cudaFuncSetAttribute(ism_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      return cudaLaunchKernelEx(&cfg, ism_kernel<1>, A);
+    default:
+      e = cudaFuncSetAttribute(ism_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      return cudaLaunchKernelEx(&cfg, ism_kernel<2>, A);
+  }
+}
+
+cudaError_t launch_image_params(const IsmArgs& A, double* x_out, float* A_out, long long N, cudaStream_t stream) {
+  long long nb = (N + 255) / 256;
+  int blocks = (int)(nb < 148LL * 16 ? nb : 148LL * 16);
+  if (blocks < 1) blocks = 1;
+  image_params_kernel<<<blocks, 256, 0, stream>>>(A, x_out, A_out);
+  return cudaGetLastError();
+}
+
+}  // namespace gpurir

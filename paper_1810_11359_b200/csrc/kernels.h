@@ -1,0 +1,82 @@
+// kernels.h — host <-> device argument blocks and launchers of libgpurir.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace gpurir {
+
+// One RIR of a multi-room batch (device copy built by the host planner).
+struct BatchJob {
+  float L[3];
+  float beta[6];
+  float src[3];
+  float rcv[3];
+  float orv[3];
+  int pattern;
+  int nb[3];
+  int nISM;             // ISM samples of this RIR
+  int nS;               // total samples of this RIR
+  long long out_offset; // element offset of the RIR row in the output
+  float kappa_fs;       // kappa / fs (1/sample) of the Sabine envelope (Eq. 8, C14)
+  float pad;
+  unsigned long long rir_global;  // tail RNG stream id (C16)
+};
+
+struct IsmArgs {
+  // single-room call (jobs == nullptr)
+  float L[3];
+  float beta[6];
+  int nb[3];
+  int pattern;
+  const float* pos_src;
+  const float* pos_rcv;
+  const float* orv;
+  int M_src, M_rcv, M;
+  int nISM;
+  long long row_stride;  // nSamples
+  int nTiles;
+  // batch call
+  const BatchJob* jobs;
+  const int2* tiles;     // per cluster: (job, tile)
+  // common
+  double fs_over_c, c_over_fs;
+  float H, invH;         // half window (samples) and 1/H
+  int nbw;               // delay bins touching one warp sub-tile
+  float* out;
+  int* status;
+  // LUT mode
+  const float2* lut;     // phase-major rows [Q][cols] of (T[n+1], T[n]-T[n+1])
+  int lut_rows, lut_cols, lut_joff, lutQ;
+};
+
+struct TailArgs {
+  // single-room call (jobs == nullptr)
+  const float* pos_src;
+  const float* pos_rcv;
+  int M_rcv, M;
+  int nISM, nS;
+  long long row_stride;
+  float kappa_fs;
+  unsigned long long rir_base;
+  // batch
+  const BatchJob* jobs;
+  const int2* chunks;    // per CTA: (job, chunk)
+  // common
+  double fs_over_c;
+  int win;               // estimation window length in samples, round(0.010 fs) (C15)
+  unsigned long long seed;
+  float* out;
+  int chunks_per_rir;
+};
+
+size_t ism_smem_bytes(int mode, int lut_rows, int lut_cols);
+cudaError_t launch_ism(const IsmArgs& A, int mode, int split, long long nclusters, cudaStream_t stream);
+cudaError_t launch_image_params(const IsmArgs& A, double* x_out, float* A_out, long long N, cudaStream_t stream);
+cudaError_t launch_tail(const TailArgs& A, long long nblocks, cudaStream_t stream);
+
+constexpr int kTailThreads = 256;
+constexpr int kTailChunk = kTailThreads * 8;  // samples per tail CTA (2 Philox blocks per thread)
+
+}  // namespace gpurir

@@ -1,0 +1,80 @@
+"""The C-ABI library loads and exports every symbol include/gpurir.h declares; host helpers agree with
+the oracle's (-m "not gpu": no device compute is called)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_1810_11359_b200 import build as B
+    B.build()
+    import paper_1810_11359_b200 as P
+    return P
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "gpurir.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gpurir_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(P):
+    names = _declared()
+    assert len(names) >= 14
+    lib = ctypes.CDLL(P.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert sorted(P.EXPORTS) == names
+
+
+def test_version(P):
+    assert "sm_100a" in P.version()
+
+
+def test_lib_is_sm100a_fatbin(P):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", P.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_helpers_match_oracle(P, oracle):
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        room = rng.uniform(2, 10, 3).astype(np.float32)
+        T60 = float(rng.uniform(0.2, 2.0))
+        try:
+            bo, clo = oracle.beta_sabine(room, T60)
+        except oracle.OracleError as e:
+            with pytest.raises(P.GpurirError) as ei:
+                P.beta_sabine(room, T60)
+            assert ei.value.status == e.status == 3
+            continue
+        bg, clg = P.beta_sabine(room, T60)
+        assert clg == clo and np.allclose(bg, bo, rtol=1e-6)
+        beta = rng.uniform(-1, 1, 6).astype(np.float32)
+        assert P.sabine_t60(room, beta) == pytest.approx(oracle.sabine_t60(room, beta), rel=1e-12)
+        T = float(rng.uniform(0.01, 2.0))
+        assert list(P.t2n(T, room)) == list(oracle.t2n(T, room))
+        assert P.att2t_sabine(15.0, T60) == pytest.approx(oracle.att2t(15.0, T60), rel=1e-15)
+        assert P.nsamples(T, 16000.0) == oracle.nsamples(T, 16000.0)
+
+
+def test_lut_table_matches_eq9_oracle(P, oracle):
+    for fs in (16000.0, 44100.0, 48000.0):
+        g, hg = P.lut_table(4e-3, fs, 16)
+        r, hr = oracle.lut_build(4e-3, fs, 16)
+        assert hg == hr
+        assert np.max(np.abs(g - r)) < 1e-7
+
+
+def test_invalid_arguments_rejected_on_host(P):
+    # host validation happens before any device work: EINVAL without touching CUDA
+    assert P._lib.lib().gpurir_simulate_rir(None, None, None, 0, None, 0, None, 0, None, 0.1, 0.1, 16000.0, 343.0,
+                                            None, None) == 1

@@ -1,0 +1,282 @@
+"""CUDA path vs the CPU oracle, element by element on identical seeded inputs (-m gpu).
+
+Tolerances (north_star): per RIR, max |h_gpu - h_oracle| <= tol * max |h_oracle| over all
+samples, tail included (reading C20): fp32 1e-4, LUT 5e-3, fp16 2e-2.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import workloads as W
+from helpers import TOL, derive, rel_err, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_1810_11359_b200 as P
+    from paper_1810_11359_b200 import build as B
+    B.build()
+    return P
+
+
+# ---------------------------------------------------------------- a1: image parameters
+
+@pytest.mark.parametrize("pattern,orv", [(0, None), (2, [0.0, 1.0, 0.0]), (3, [1.0, 1.0, 0.0]), (4, [0.3, -0.2, 0.9])])
+def test_image_params_vs_oracle(P, oracle, pattern, orv):
+    room = np.float32([3, 4, 2.5])
+    beta = np.float32([-0.9, 0.8, -0.7, 0.95, 0.6, -0.85])
+    src, rcv = np.float32([0.7, 1.3, 0.9]), np.float32([2.2, 3.1, 1.7])
+    nb = [9, 8, 7]
+    x, A = P.image_params(room, beta, src, rcv, nb, 16000.0, mic_pattern=pattern, orv=orv)
+    ref = oracle.image_set(room, beta, src, rcv, nb, fs=16000.0, pattern=pattern, orv=orv)
+    x = x.cpu().numpy()
+    A = A.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(x - ref["x"])) < 1e-9 * np.max(ref["x"])
+    assert np.max(np.abs(A - ref["A"])) < 2e-6 * np.max(np.abs(ref["A"]))
+
+
+def test_image_params_degenerate(P):
+    room = np.float32([3, 4, 2.5])
+    with pytest.raises(P.GpurirError) as e:
+        P.image_params(room, [0.5] * 6, [1, 1, 1], [1, 1, 1], [3, 3, 3], 16000.0)
+    assert e.value.status == 2
+
+
+# ---------------------------------------------------------------- golden + random scenes (a3)
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "survey_appendix_b.json")
+
+
+@pytest.mark.parametrize("case", ["G1", "G2", "G3", "G4"])
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16"])
+def test_goldens(P, oracle, case, mode):
+    import torch
+    g = json.load(open(GOLD))["cases"][case]
+    T = g["nS"] / g["fs"]
+    room, beta = np.float32(g["room"]), np.float32(g["beta"])
+    orv = None if g["orv"] is None else np.float32([g["orv"]])
+    h = P.simulate_rir(room, beta, torch.tensor([g["src"]], dtype=torch.float32).cuda(),
+                       torch.tensor([g["rcv"]], dtype=torch.float32).cuda(), g["nb"], T, T, g["fs"],
+                       orV_rcv=None if orv is None else torch.from_numpy(orv).cuda(), mic_pattern=g["pattern"],
+                       mode=mode, sync=True).cpu().numpy().astype(np.float64)[0, 0]
+    ref = oracle.simulate_rir(room, beta, [g["src"]], [g["rcv"]], g["nb"], T, T, fs=g["fs"], pattern=g["pattern"],
+                              orV_rcv=orv)[0, 0]
+    assert h.shape == ref.shape
+    assert rel_err(h, ref)[0] <= TOL[mode]
+    if mode == "fp32":
+        assert int(np.argmax(np.abs(h))) == g["argmax"]
+        assert abs(h[g["argmax"]] - g["h_argmax"]) <= 1e-4 * abs(g["h_argmax"])
+
+
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16"])
+def test_random_scenes(P, oracle, mode):
+    """S:525 style: random rooms 2-8 m, T60 0.3-1.0, <=2 src x 3 rcv, all patterns, 16 and 48 kHz."""
+    rng = np.random.default_rng(525)
+    worst = 0.0
+    for i in range(30):
+        fs = 16000.0 if i % 3 else 48000.0
+        sc = W.random_small_scene(rng, fs=fs)
+        beta, nb = derive(oracle, sc)
+        g = run_gpu(P, sc, beta, nb, mode=mode)
+        r = run_oracle(oracle, sc, beta, nb)
+        e = rel_err(g, r).max()
+        worst = max(worst, e)
+        assert e <= TOL[mode], (i, sc.room, sc.pattern, fs, e)
+    print(f"random scenes {mode}: worst {worst:.3e}")
+
+
+# ---------------------------------------------------------------- configs (BASELINE.json)
+
+def test_cfg1_fp32(P, oracle):
+    sc = W.cfg1()
+    beta, nb = derive(oracle, sc)
+    assert list(nb) == [73, 55, 87]
+    g = run_gpu(P, sc, beta, nb)
+    r = run_oracle(oracle, sc, beta, nb)
+    assert g.shape == r.shape == (1, 1, 4800)
+    assert rel_err(g, r)[0] <= TOL["fp32"]
+
+
+@pytest.mark.parametrize("mode", ["lut", "fp16"])
+def test_cfg1_modes(P, oracle, mode):
+    sc = W.cfg1()
+    beta, nb = derive(oracle, sc)
+    g = run_gpu(P, sc, beta, nb, mode=mode)
+    r = run_oracle(oracle, sc, beta, nb)
+    assert rel_err(g, r)[0] <= TOL[mode]
+
+
+@pytest.mark.parametrize("T60", [0.1, 0.2, 0.5, 0.9, 1.4, 2.0])
+def test_cfg2_t60_sweep(P, oracle, T60):
+    """ISM to T60/4 + diffuse tail to T60 (tail RNG is bit-reproducible, so parity covers every sample)."""
+    sc = W.cfg2(T60)
+    beta, nb = derive(oracle, sc)
+    g = run_gpu(P, sc, beta, nb)
+    r = run_oracle(oracle, sc, beta, nb)
+    assert rel_err(g, r)[0] <= TOL["fp32"], T60
+
+
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16"])
+def test_cfg3_subset(P, oracle, mode):
+    """#RIR sweep room, cardioid with random orientations, diffuse variant; first 24 receivers."""
+    sc = W.cfg3(24, "diffuse")
+    beta, nb = derive(oracle, sc)
+    g = run_gpu(P, sc, beta, nb, mode=mode)
+    r = run_oracle(oracle, sc, beta, nb)
+    assert rel_err(g, r).max() <= TOL[mode]
+
+
+def test_cfg3_full_size_sampled(P, oracle):
+    """M = 16384 in the bench launch configuration; 6 sampled RIRs re-computed by the oracle."""
+    sc = W.cfg3(16384, "diffuse")
+    beta, nb = derive(oracle, sc)
+    g = run_gpu(P, sc, beta, nb)
+    assert np.all(np.isfinite(g))
+    idx = [0, 1, 4097, 8191, 12345, 16383]
+    for m in idx:  # each sampled RIR with its own global tail stream id
+        rj = oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[m:m + 1], nb, sc.Tdiff, sc.Tmax, fs=sc.fs,
+                                 pattern=sc.pattern, orV_rcv=sc.orV_rcv[m:m + 1], seed=sc.seed, rir_index_base=m)
+        assert rel_err(g[0, m], rj[0, 0])[0] <= TOL["fp32"], m
+
+
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16"])
+def test_cfg4_48k_array(P, oracle, mode):
+    sc = W.cfg4("a")
+    sc.pos_rcv = sc.pos_rcv[:8]
+    beta, nb = derive(oracle, sc)
+    g = run_gpu(P, sc, beta, nb, mode=mode)
+    r = run_oracle(oracle, sc, beta, nb)
+    assert rel_err(g, r).max() <= TOL[mode]
+
+
+# ---------------------------------------------------------------- edge cases
+
+def _scene(**kw):
+    base = dict(name="edge", room=np.float32([3, 4, 2.5]), T60=0.4, pos_src=np.float32([[1.0, 1.0, 1.0]]),
+                pos_rcv=np.float32([[2.0, 3.0, 1.5]]), orV_rcv=None, pattern=0, Tdiff=0.03, Tmax=0.05, fs=16000.0,
+                seed=99)
+    base.update(kw)
+    return W.Scene(**base)
+
+
+@pytest.mark.parametrize("kw", [
+    dict(Tdiff=0.0, Tmax=0.03),                      # tail only -> silent
+    dict(Tdiff=0.05, Tmax=0.05),                     # ISM only
+    dict(Tdiff=0.1, Tmax=0.05),                      # Tdiff > Tmax -> ISM to Tmax
+    dict(Tdiff=0.0301, Tmax=0.0511),                 # ragged lengths (not multiples of the tile / of 4)
+    dict(pos_src=np.float32([[1.0, 2.0, 1.25]]), pos_rcv=np.float32([[3.14375, 2.0, 1.25]]),
+         room=np.float32([5, 4, 2.5])),             # direct path on an integer sample delay
+    dict(pos_rcv=np.float32([[3.0, 3.0, 1.5]])),     # receiver on a wall
+    dict(pos_src=np.float32([[1.0, 1.0, 1.0], [0.5, 3.5, 2.0]]), pos_rcv=np.float32([[2.0, 3.0, 1.5], [1.1, 0.2, 0.3],
+                                                                                      [2.9, 3.9, 2.4]])),  # M_src > 1
+    dict(T60=0.05, clamp=True),                      # infeasible T60 clamped -> beta = 0, direct path only
+])
+def test_edge_cases(P, oracle, kw):
+    sc = _scene(**kw)
+    beta, nb = derive(oracle, sc)
+    g = run_gpu(P, sc, beta, nb)
+    r = run_oracle(oracle, sc, beta, nb)
+    assert g.shape == r.shape
+    if np.max(np.abs(r)) == 0:
+        assert np.max(np.abs(g)) == 0
+    else:
+        assert rel_err(g, r).max() <= TOL["fp32"]
+
+
+def test_nb_img_one(P, oracle):
+    sc = _scene(Tdiff=0.02, Tmax=0.02)
+    beta, _ = derive(oracle, sc)
+    g = run_gpu(P, sc, beta, [1, 1, 1])
+    r = run_oracle(oracle, sc, beta, [1, 1, 1])
+    assert rel_err(g, r)[0] <= TOL["fp32"]
+
+
+def test_degenerate_and_invalid(P):
+    import torch
+    room = np.float32([3, 4, 2.5])
+    s = torch.tensor([[1.0, 1.0, 1.0]], device="cuda")
+    with pytest.raises(P.GpurirError) as e:
+        P.simulate_rir(room, [0.9] * 6, s, s.clone(), [3, 3, 3], 0.02, 0.02, 16000.0, sync=True)
+    assert e.value.status == 2
+    with pytest.raises(P.GpurirError) as e:
+        P.simulate_rir(room, [1.1] + [0.9] * 5, s, s + 0.5, [3, 3, 3], 0.02, 0.02, 16000.0)
+    assert e.value.status == 1
+    with pytest.raises(P.GpurirError) as e:
+        P.simulate_rir(room, [0.9] * 6, s, s + 0.5, [3, 3, 3], 0.02, 0.02, 16000.0, mic_pattern="cardioid",
+                       orV_rcv=torch.zeros((1, 3), device="cuda"), sync=True)
+    assert e.value.status == 1
+    assert P.device_status() == 0
+
+
+# ---------------------------------------------------------------- determinism, sharding, batch
+
+def test_run_to_run_deterministic(P, oracle):
+    sc = W.cfg3(32, "diffuse")
+    beta, nb = derive(oracle, sc)
+    a = run_gpu(P, sc, beta, nb)
+    b = run_gpu(P, sc, beta, nb)
+    assert np.array_equal(a, b)
+
+
+def test_shard_invariance(P, oracle):
+    """§8(e): running the receivers in 4 shards with rir_index_base offsets reproduces the unsharded
+    call bit for bit (fixed split so the per-tile summation order is identical)."""
+    sc = W.cfg3(64, "diffuse")
+    beta, nb = derive(oracle, sc)
+    full = run_gpu(P, sc, beta, nb, split=2)
+    parts = []
+    for s in range(4):
+        sl = slice(16 * s, 16 * (s + 1))
+        parts.append(run_gpu(P, sc, beta, nb, split=2, rir_index_base=16 * s, pos_rcv=sc.pos_rcv[sl],
+                             orv=sc.orV_rcv[sl]))
+    assert np.array_equal(full, np.concatenate(parts, axis=1))
+
+
+def test_split_factor_within_tolerance(P, oracle):
+    sc = W.cfg1()
+    beta, nb = derive(oracle, sc)
+    r = run_oracle(oracle, sc, beta, nb)
+    for split in (1, 2, 4, 8):
+        g = run_gpu(P, sc, beta, nb, split=split)
+        assert rel_err(g, r)[0] <= TOL["fp32"], split
+
+
+def test_reciprocity_gpu(P, oracle):
+    sc = W.cfg1()
+    beta, nb = derive(oracle, sc)
+    a = run_gpu(P, sc, beta, nb)
+    sw = W.Scene("swap", sc.room, sc.T60, sc.pos_rcv, sc.pos_src, None, 0, sc.Tdiff, sc.Tmax, sc.fs)
+    b = run_gpu(P, sw, beta, nb)
+    assert rel_err(a, b)[0] <= 1e-5
+
+
+def test_batch_rooms_vs_oracle(P, oracle):
+    """config 5 shape: independent rooms, ragged rows, tail streams rir_index_base + i."""
+    import torch
+    rb = W.cfg5(12)
+    rooms, refs, off = [], [], 0
+    for i in range(rb.n):
+        beta, _ = oracle.beta_sabine(rb.room[i], rb.T60[i])
+        beta = beta.astype(np.float32)
+        nb = oracle.t2n(rb.Tdiff[i], rb.room[i])
+        nS = oracle.nsamples(rb.Tmax[i], rb.fs)
+        rooms.append(dict(room_sz=rb.room[i], beta=beta, pos_src=rb.pos_src[i], pos_rcv=rb.pos_rcv[i], nb_img=nb,
+                          Tdiff=rb.Tdiff[i], Tmax=rb.Tmax[i], out_offset=off))
+        refs.append(oracle.simulate_rir(rb.room[i], beta, rb.pos_src[i:i + 1], rb.pos_rcv[i:i + 1], nb, rb.Tdiff[i],
+                                        rb.Tmax[i], fs=rb.fs, seed=rb.seed, rir_index_base=1000 + i)[0, 0])
+        off += nS
+    out = torch.full((off,), float("nan"), device="cuda")
+    P.simulate_rir_batch(rooms, rb.fs, out, seed=rb.seed, rir_index_base=1000, sync=True)
+    o = out.cpu().numpy().astype(np.float64)
+    off = 0
+    for i, r in enumerate(refs):
+        g = o[off:off + r.size]
+        off += r.size
+        assert rel_err(g, r)[0] <= TOL["fp32"], i
