@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""bench.py — RIR-synthesis throughput of the B200 ISM engine (contract: see DESIGN.md §Measurement).
+
+Workload (BASELINE.json config 3, the paper's #RIR sweep room): 3x4x2.5 m, T60 = 0.7 s
+(beta = -0.9397, Sabine), source (1.5, 1.0, 1.2), M = 16384 cardioid receivers per GPU uniform in the
+room (seed 3) with random orientations, fs = 16 kHz, ISM to Tdiff = 0.175 s + diffuse tail to 0.7 s,
+fp32 mode.  One step = one gpurir_simulate_rir call over the rank's 16384 receivers (ISM kernel + tail
+kernel).  Weak scaling: rank r owns receivers [16384 r, 16384 (r+1)) of the N*16384-receiver workload.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--mode fp32|lut|fp16]
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on the host cores: the paper's
+comparison arm for this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+M_PER_GPU = 16384
+METRIC = "RIRs/s and image contributions/s vs T60 and #RIRs at 1/2/4/8 B200"
+ISSUE_SLOTS_PER_TAP = 13  # algorithmic FP32-pipe issue slots per in-window tap
+
+
+def workload_name(mode="fp32"):
+    return f"cfg3_diffuse_M{M_PER_GPU}perGPU_T60_0.7_fs16k_cardioid_{mode}"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def count_taps(room, src, rcv, nb, nISM, fs, c, H):
+    """Algorithmic work: in-window (image, sample) pairs for samples [0, nISM) (Eqs. 5-6 support)."""
+    lo = [-(int(n) // 2) for n in nb]
+    hi = [(int(n) + 1) // 2 for n in nb]
+    ax = []
+    for a in range(3):
+        n = np.arange(lo[a], hi[a])
+        q = np.where(n % 2 == 0, n * room[a] + src[a], (n + 1) * room[a] - src[a]) - rcv[a]
+        ax.append(q * q)
+    d2 = ax[0][None, None, :] + ax[1][None, :, None] + ax[2][:, None, None]
+    x = np.sqrt(d2).ravel() * fs / c
+    k0 = np.maximum(np.floor(x - H) + 1, 0)
+    k1 = np.minimum(np.ceil(x + H) - 1, nISM - 1)
+    return float(np.maximum(k1 - k0 + 1, 0).sum())
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=open(self.path, "w"),
+                stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return None
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle arms
+
+def oracle_rate(sc, beta, nb, n_rir, base_index=0):
+    """Time the CPU oracle (as it stands) on the first n_rir receivers of the workload; RIRs/s."""
+    import oracle
+    t = time.perf_counter()
+    oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[:n_rir], nb, sc.Tdiff, sc.Tmax, fs=sc.fs, c=sc.c,
+                        pattern=sc.pattern, orV_rcv=sc.orV_rcv[:n_rir], seed=sc.seed, rir_index_base=base_index)
+    dt = time.perf_counter() - t
+    return n_rir / dt, dt
+
+
+def cpu_baseline(sc, budget_s=15.0):
+    import oracle
+    beta, _ = oracle.beta_sabine(sc.room, sc.T60)
+    beta = beta.astype(np.float32)
+    nb = oracle.t2n(sc.Tdiff, sc.room, sc.c)
+    cores = oracle.max_threads()
+    n0 = max(cores, 8)
+    r0, dt0 = oracle_rate(sc, beta, nb, n0)
+    n = int(min(len(sc.pos_rcv), max(n0, round(r0 * budget_s / cores) * cores)))
+    r, dt = oracle_rate(sc, beta, nb, n)
+    return {"value": r, "unit": "RIRs/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n} of the {len(sc.pos_rcv)} receivers of the workload ({dt:.1f} s, OpenMP over RIRs, "
+                      f"fp64 C oracle, -O2)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    sc = W.cfg3(M_PER_GPU, "diffuse")
+    beta, _ = oracle.beta_sabine(sc.room, sc.T60)
+    beta = beta.astype(np.float32)
+    nb = oracle.t2n(sc.Tdiff, sc.room, sc.c)
+    cores = oracle.max_threads()
+    per_step = max(cores, 16)
+    r0, dt0 = oracle_rate(sc, beta, nb, per_step)
+    # size each step so warmup + steps finish in ~2-3 minutes
+    target = 150.0 / max(1, args.steps + args.warmup)
+    per_step = int(min(M_PER_GPU, max(cores, round(r0 * target / cores) * cores)))
+    times = []
+    for i in range(args.warmup + args.steps):
+        off = (i * per_step) % (M_PER_GPU - per_step + 1)
+        t = time.perf_counter()
+        oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[off:off + per_step], nb, sc.Tdiff, sc.Tmax,
+                            fs=sc.fs, c=sc.c, pattern=sc.pattern, orV_rcv=sc.orV_rcv[off:off + per_step],
+                            seed=sc.seed, rir_index_base=off)
+        dt = time.perf_counter() - t
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * sum(times) / len(times)
+    value = per_step / (ms / 1000.0)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "RIRs/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name("fp32"), "reference_arm": "CPU oracle (oracle/oracle.c), each step "
+                       f"{per_step} receivers of the workload"},
+            "cpu_baseline": {"value": value, "unit": "RIRs/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} RIRs per step x {args.steps} steps"},
+            "e2e": {"value": value, "unit": "RIRs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--mode", default="fp32", choices=["fp32", "lut", "fp16"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    import torch
+    import paper_1810_11359_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- workload (weak scaling: this rank's 16384 receivers of the N*16384 workload) ----
+    sc = W.cfg3(M_PER_GPU * world, "diffuse")
+    sl = slice(rank * M_PER_GPU, (rank + 1) * M_PER_GPU)
+    beta, _ = P.beta_sabine(sc.room, sc.T60)           # library helpers on the product path
+    nb = P.t2n(sc.Tdiff, sc.room, sc.c)
+    nS, nISM = P.nsamples(sc.Tmax, sc.fs), P.nsamples(sc.Tdiff, sc.fs)
+    src = torch.from_numpy(sc.pos_src).to(dev)
+    rcv = torch.from_numpy(np.ascontiguousarray(sc.pos_rcv[sl])).to(dev)
+    orv = torch.from_numpy(np.ascontiguousarray(sc.orV_rcv[sl])).to(dev)
+    out = torch.empty((1, M_PER_GPU, nS), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    base = rank * M_PER_GPU
+
+    def step(ev=None):
+        P.simulate_rir(sc.room, beta, src, rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=orv,
+                       mic_pattern=sc.pattern, mode=args.mode, seed=sc.seed, rir_index_base=base, out=out,
+                       stream=stream, ev_ism=ev)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    n_ev = args.steps
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    ism_s = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    ism_e = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                       # L2 flushed between timed steps (outside the events)
+            ev_s[i].record(stream)
+            step((ism_s[i], ism_e[i]))
+            ev_e[i].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
+    ism_ms = [a.elapsed_time(b) for a, b in zip(ism_s, ism_e)]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    ms_per_step = total_ms / args.steps
+    value = world * M_PER_GPU * args.steps / (total_ms / 1000.0)
+
+    # ---- end to end through the public API with HOST buffers (H2D inputs, D2H RIRs in the region) ----
+    h_src = torch.from_numpy(sc.pos_src).pin_memory()
+    h_rcv = torch.from_numpy(np.ascontiguousarray(sc.pos_rcv[sl])).pin_memory()
+    h_orv = torch.from_numpy(np.ascontiguousarray(sc.orV_rcv[sl])).pin_memory()
+    h_out = torch.empty((1, M_PER_GPU, nS), dtype=torch.float32).pin_memory()
+    e2e_steps = max(1, args.e2e_steps)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        d_src = h_src.to(dev, non_blocking=True)
+        d_rcv = h_rcv.to(dev, non_blocking=True)
+        d_orv = h_orv.to(dev, non_blocking=True)
+        P.simulate_rir(sc.room, beta, d_src, d_rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=d_orv,
+                       mic_pattern=sc.pattern, mode=args.mode, seed=sc.seed, rir_index_base=base, out=out,
+                       stream=stream)
+        h_out.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * M_PER_GPU * e2e_steps / (float(e2e_ms.item()) / 1000.0)
+    h2d = (h_src.numel() + h_rcv.numel() + h_orv.numel()) * 4
+    d2h = h_out.numel() * 4
+    # e2e parity spot check against the device-timed output (same inputs, deterministic kernels)
+    assert torch.equal(h_out[0, :4].to(dev), out[0, :4])
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (the ISM accumulation kernel) ----
+    sample = np.linspace(0, M_PER_GPU - 1, 256).astype(int)
+    H = 4e-3 * sc.fs / 2
+    r64 = sc.pos_rcv[sl].astype(np.float64)
+    taps_sample = [count_taps(sc.room.astype(np.float64), sc.pos_src[0].astype(np.float64), r64[m], nb, nISM,
+                              sc.fs, sc.c, H) for m in sample]
+    taps_per_rir = float(np.mean(taps_sample))
+    taps_launch = taps_per_rir * M_PER_GPU
+    ism_avg_s = float(np.mean(ism_ms)) / 1000.0
+    pk, pk_kind = peaks()
+    f_clk = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+    issue_peak = 148 * 128 * f_clk  # FP32 lane issue slots / s (B200_PROFILING.md unit counts)
+    achieved = taps_launch * ISSUE_SLOTS_PER_TAP / ism_avg_s
+    lattice = float(np.prod(nb.astype(np.float64)))
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "RIRs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.mode != "fp16" else "f16x2-taps/f32-acc", "data": "synthetic",
+        "config": {"workload": workload_name(args.mode), "M_per_gpu": M_PER_GPU, "room": [3, 4, 2.5], "T60": 0.7,
+                   "beta": float(beta[0]), "nb_img": [int(v) for v in nb], "fs": sc.fs, "Tdiff": sc.Tdiff,
+                   "Tmax": sc.Tmax, "pattern": "cardioid", "mode": args.mode, "nSamples": nS, "nISM": nISM,
+                   "l2": "256 MB buffer written between timed steps (L2 126 MB); step output 734 MB"},
+        "image_contributions_per_s": value * lattice,
+        "taps_per_s": world * taps_launch / ism_avg_s if world == 1 else None,
+        "ism_ms": float(np.mean(ism_ms)),
+        "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": issue_peak / 1e12,
+                     "unit": "T FP32-lane-issue-slots/s", "frac": achieved / issue_peak, "traffic": None,
+                     "kernel": "ism_kernel<0>",
+                     "basis": f"{ISSUE_SLOTS_PER_TAP} issue slots per in-window tap (SURVEY §8(d)) x {taps_launch:.4g} "
+                              f"taps per launch (exact count on 256 sampled receivers x {M_PER_GPU}); peak = 148 SM x "
+                              f"128 lanes x {f_clk / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)"},
+        "e2e": {"value": e2e_value, "unit": "RIRs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk.summary(),
+        "paper_context": "gpuRIR V100 fp32, 1024 RIRs, T60 0.7 s diffuse: 195.69 ms = 5,233 RIRs/s (P:362); "
+                         "different fs/positions/pattern, context only",
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(W.cfg3(M_PER_GPU, "diffuse"))
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

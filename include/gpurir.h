@@ -67,6 +67,8 @@ typedef struct {
   void* stream;             /* cudaStream_t to launch on; NULL = the legacy default stream          */
   int split;                /* CTAs cooperating on one time tile (thread-block cluster), 0 = auto   */
   unsigned flags;           /* GPURIR_FLAG_*                                                        */
+  void* ev_ism[2];          /* optional cudaEvent_t pair recorded on `stream` around the ISM kernel  */
+  void* ev_tail[2];         /* optional cudaEvent_t pair recorded around the diffuse-tail kernel     */
 } gpurir_opts;
 
 /* Fill *opts with the defaults above. */

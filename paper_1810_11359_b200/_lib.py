@@ -26,7 +26,8 @@ EXPORTS = [
 
 class Opts(C.Structure):
     _fields_ = [("mode", C.c_int), ("Tw", C.c_double), ("lut_Q", C.c_int), ("seed", C.c_uint64),
-                ("rir_index_base", C.c_uint64), ("stream", C.c_void_p), ("split", C.c_int), ("flags", C.c_uint)]
+                ("rir_index_base", C.c_uint64), ("stream", C.c_void_p), ("split", C.c_int), ("flags", C.c_uint),
+                ("ev_ism", C.c_void_p * 2), ("ev_tail", C.c_void_p * 2)]
 
 
 class Room(C.Structure):

@@ -45,7 +45,8 @@ def _stream_handle(stream) -> int | None:
     return stream.cuda_stream
 
 
-def make_opts(mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0, stream=None, split=0, sync=False) -> Opts:
+def make_opts(mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0, stream=None, split=0, sync=False,
+              ev_ism=None, ev_tail=None) -> Opts:
     o = Opts()
     lib().gpurir_opts_default(C.byref(o))
     o.mode = _mode(mode)
@@ -56,6 +57,10 @@ def make_opts(mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0, stream=N
     o.stream = _stream_handle(stream)
     o.split = int(split)
     o.flags = FLAG_SYNC if sync else 0
+    if ev_ism is not None:  # torch.cuda.Event pair recorded around the ISM kernel
+        o.ev_ism[0], o.ev_ism[1] = ev_ism[0].cuda_event, ev_ism[1].cuda_event
+    if ev_tail is not None:
+        o.ev_tail[0], o.ev_tail[1] = ev_tail[0].cuda_event, ev_tail[1].cuda_event
     return o
 
 
@@ -77,7 +82,7 @@ def _dev_f32(t, name, rows=None):
 
 def simulate_rir(room_sz, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs, c=343.0, orV_rcv=None,
                  mic_pattern="omni", mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0, out=None,
-                 stream=None, split=0, sync=False):
+                 stream=None, split=0, sync=False, ev_ism=None, ev_tail=None):
     """gpurir_simulate_rir: RIRs [M_src][M_rcv][ceil(Tmax fs)] (float32, on pos_src's device).
 
     room_sz (3) and beta (6, wall order x0,x1,y0,y1,z0,z1) are host values; pos_src [M_src,3],
@@ -95,7 +100,7 @@ def simulate_rir(room_sz, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs, c=343
         out = torch.empty((Ms, Mr, nS), dtype=torch.float32, device=pos_src.device)
     elif out.dtype != torch.float32 or not out.is_contiguous() or out.numel() < Ms * Mr * nS:
         raise ValueError("out must be contiguous float32 with M_src*M_rcv*nSamples elements")
-    o = make_opts(mode, Tw, lut_Q, seed, rir_index_base, stream, split, sync)
+    o = make_opts(mode, Tw, lut_Q, seed, rir_index_base, stream, split, sync, ev_ism, ev_tail)
     st = lib().gpurir_simulate_rir(_f3(room_sz), _f3(beta, 6), pos_src.data_ptr(), Ms, pos_rcv.data_ptr(), Mr,
                                    orV_rcv.data_ptr() if orV_rcv is not None else None, pat, _i3(nb_img),
                                    float(Tdiff), float(Tmax), float(fs), float(c), out.data_ptr(), C.byref(o))

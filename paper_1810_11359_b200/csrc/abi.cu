@@ -126,6 +126,17 @@ void fill_common(IsmArgs& A, double fs, double c, double Tw) {
   A.H = (float)H;
   A.invH = (float)(1.0 / H);
   A.nbw = (int)floor(((double)kS - 1.0 + 2.0 * H) / kS) + 1;
+  double Hs = exp2(ceil(log2(H)));
+  double rho = H / Hs, r2 = rho * rho;
+  A.invHs = (float)(1.0 / Hs);
+  A.rho2 = (float)r2;
+  const double b[4] = {kWb0, kWb1, kWb2, kWb3};
+  for (int i = 0; i < 4; i++) A.wb[i] = (float)(b[i] / pow(r2, i + 1));
+  // Eq. 11 coefficients, argument rescaled from u/(2H) to u/(2Hs)
+  A.hc[0] = (float)(-4.93359375 / r2);
+  A.hc[1] = (float)(4.04296875 / (r2 * r2));
+  A.hc[2] = (float)(-1.2294921875 / (r2 * r2 * r2));
+  A.x2clamp = (float)(r2 / 4.0);
 }
 
 int auto_split(long long nclusters, int requested) {
@@ -260,8 +271,10 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
     }
     long long nclusters = (long long)A.nTiles * M;
     int split = auto_split(nclusters, o.split);
+    if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e = launch_ism(A, o.mode, split, nclusters, stream);
     if (e != cudaSuccess) return cuda_fail(e, "launch_ism");
+    if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);
   }
   if (nISM < nS) {
     TailArgs T;
@@ -277,8 +290,10 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
     T.out = out;
     long long groups = (nS + 3) / 4 - nISM / 4;
     T.chunks_per_rir = (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4));
+    if (o.ev_tail[0]) cudaEventRecord((cudaEvent_t)o.ev_tail[0], stream);
     cudaError_t e = launch_tail(T, (long long)T.chunks_per_rir * M, stream);
     if (e != cudaSuccess) return cuda_fail(e, "launch_tail");
+    if (o.ev_tail[1]) cudaEventRecord((cudaEvent_t)o.ev_tail[1], stream);
   }
   return finish(o, stream, d);
 }
@@ -366,8 +381,10 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
       A.lutQ = o.lut_Q;
     }
     int split = auto_split((long long)tiles.size(), o.split);
+    if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     e = launch_ism(A, o.mode, split, (long long)tiles.size(), stream);
     if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_ism(batch)"); }
+    if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);
   }
   if (!chunks.empty()) {
     TailArgs T;
@@ -377,8 +394,10 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     T.win = (int)llround(0.010 * fs);
     T.seed = o.seed;
     T.out = out;
+    if (o.ev_tail[0]) cudaEventRecord((cudaEvent_t)o.ev_tail[0], stream);
     e = launch_tail(T, (long long)chunks.size(), stream);
     if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_tail(batch)"); }
+    if (o.ev_tail[1]) cudaEventRecord((cudaEvent_t)o.ev_tail[1], stream);
   }
   cudaFreeAsync(ws, stream);
   e = cudaStreamSynchronize(stream);  // host staging vectors are released on return

@@ -202,8 +202,8 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
   const int s0 = warp * kS;                 // sub-tile start relative to t0
   const int kf = T.t0 + s0 + li - T.tc;     // sample relative to tc (integer)
   float2 acc2 = make_float2(0.f, 0.f);
-  const float kv = (float)kf * A.invH;      // fp32 mode: v = (k - x)/H
-  const float kx = (float)kf * (0.5f * A.invH);  // fp16 mode: x = (k - x)/(2H)
+  const float kv = (float)kf * A.invHs;            // fp32 mode: v = (k - x)/Hs (exact scaling)
+  const float kx = (float)kf * (0.5f * A.invHs);   // fp16 mode: x' = (k - x)/(2 Hs)
   const int bfirst = warp, blast = warp + A.nbw;  // bins [bfirst, blast) touch this sub-tile
 
   const double fs_over_c = A.fs_over_c;
@@ -315,8 +315,8 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
               int j = (int)fj;
               float cc = -amp * sinpif(f) * 0.318309886183790672f;
               if (j & 1) cc = -cc;
-              if (MODE == 0) rec = make_float2(-xr * A.invH, cc * A.invH);
-              else rec = make_float2(-xr * (0.5f * A.invH), cc * (0.5f * A.invH) * 1024.f);
+              if (MODE == 0) rec = make_float2(-xr * A.invHs, cc * A.invHs);
+              else rec = make_float2(-xr * (0.5f * A.invHs), cc * (0.5f * A.invHs) * 1024.f);
             }
           }
         }
@@ -394,17 +394,18 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
       const int ra = sm.binstart[bfirst], rb = sm.binstart[min(blast, nbins)];
       if (MODE == 0) {
         const float2 kv2 = make_float2(kv, kv);
-        const float2 m1 = make_float2(-1.f, -1.f);
-        const float2 z2 = make_float2(0.f, 0.f);
+        const float2 mr2 = make_float2(-A.rho2, -A.rho2);
+        const float2 b3 = make_float2(A.wb[3], A.wb[3]), b2 = make_float2(A.wb[2], A.wb[2]);
+        const float2 b1 = make_float2(A.wb[1], A.wb[1]), b0 = make_float2(A.wb[0], A.wb[0]);
         for (int j = (ra & ~1) + 2 * grp; j < rb; j += 2 * kG) {
           float4 pr = sm.sorted[j >> 1];
-          float2 v = __fadd2_rn(kv2, make_float2(pr.x, pr.y));     // v = (k - x) / H
-          float2 sp = __ffma2_rn(v, v, m1);                          // s' = v^2 - 1
-          sp.x = fminf(sp.x, 0.f); sp.y = fminf(sp.y, 0.f);          // window support |v| < 1
-          float2 p = __ffma2_rn(make_float2(kWb3, kWb3), sp, make_float2(kWb2, kWb2));
-          p = __ffma2_rn(p, sp, make_float2(kWb1, kWb1));
-          p = __ffma2_rn(p, sp, make_float2(kWb0, kWb0));
-          float2 cw = __fmul2_rn(p, sp);                             // -cos(pi v / 2)
+          float2 v = __fadd2_rn(kv2, make_float2(pr.x, pr.y));     // v = (k - x) / Hs
+          float2 sp = __ffma2_rn(v, v, mr2);                         // sigma = v^2 - rho^2
+          sp.x = fminf(sp.x, 0.f); sp.y = fminf(sp.y, 0.f);          // window support |u| < H
+          float2 p = __ffma2_rn(b3, sp, b2);
+          p = __ffma2_rn(p, sp, b1);
+          p = __ffma2_rn(p, sp, b0);
+          float2 cw = __fmul2_rn(p, sp);                             // -cos(pi u / (2H))
           float2 w = __fmul2_rn(cw, cw);                             // Hann window (Eq. 6)
           float2 r;
           asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(v.x));
@@ -412,21 +413,20 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
           float2 t = __fmul2_rn(w, r);
           acc2 = __ffma2_rn(make_float2(pr.z, pr.w), t, acc2);       // += C' w / v
         }
-        (void)z2;
       } else if (MODE == 2) {
         // fp16 / half2: t - tau in fp32, window by the Eq. 11 polynomial
         // cos(pi x) at x = u / (2H) (reading C12), half2 Horner (Eq. 12), fp32 accumulation (C13).
         const float2 kx2 = make_float2(kx, kx);
-        const __half2 c6 = __float2half2_rn(-1.2294921875f), c4 = __float2half2_rn(4.04296875f);
-        const __half2 c2 = __float2half2_rn(-4.93359375f), c0 = __float2half2_rn(1.f);
-        const __half2 quarter = __float2half2_rn(0.25f);
+        const __half2 c6 = __float2half2_rn(A.hc[2]), c4 = __float2half2_rn(A.hc[1]);
+        const __half2 c2 = __float2half2_rn(A.hc[0]), c0 = __float2half2_rn(1.f);
+        const __half2 quarter = __float2half2_rn(A.x2clamp);
         __half2 acch = __float2half2_rn(0.f);
         int steps = 0;
         for (int j = (ra & ~1) + 2 * grp; j < rb; j += 2 * kG) {
           float4 pr = sm.sorted[j >> 1];
-          float2 x = __fadd2_rn(kx2, make_float2(pr.x, pr.y));      // x = (k - tau fs) / (2H), fp32
+          float2 x = __fadd2_rn(kx2, make_float2(pr.x, pr.y));      // x' = (k - tau fs) / (2 Hs), fp32
           __half2 hx = __float22half2_rn(x);
-          __half2 x2 = __hmin2(__hmul2(hx, hx), quarter);            // clamp: |x| <= 1/2 (window edge)
+          __half2 x2 = __hmin2(__hmul2(hx, hx), quarter);            // clamp: |u/(2H)| <= 1/2 (window edge)
           __half2 p = __hfma2(c6, x2, c4);
           p = __hfma2(p, x2, c2);
           p = __hfma2(p, x2, c0);                                    // cos(pi x), Eq. 11

@@ -44,6 +44,13 @@ struct IsmArgs {
   double fs_over_c, c_over_fs;
   float H, invH;         // half window (samples) and 1/H
   int nbw;               // delay bins touching one warp sub-tile
+  // exact power-of-two scaling of the tap argument: Hs = 2^ceil(log2 H),
+  // v = u / Hs, rho = H / Hs; window polynomial in sigma = v^2 - rho^2 with coefficients wb[i]
+  float invHs;           // 1 / Hs
+  float rho2;            // rho^2
+  float wb[4];           // b_i / rho^(2i+2)
+  float hc[3];           // fp16 mode: Eq. 11 coefficients of x^2, x^4, x^6 divided by rho^2, rho^4, rho^6
+  float x2clamp;         // fp16 mode: rho^2 / 4
   float* out;
   int* status;
   // LUT mode
