@@ -64,6 +64,30 @@ def count_taps(room, src, rcv, nb, nISM, fs, c, H):
     return float(np.maximum(k1 - k0 + 1, 0).sum())
 
 
+class RawEvent:
+    """A cudaEvent_t created through the CUDA runtime torch already loaded (the library records it)."""
+    _rt = None
+
+    @classmethod
+    def rt(cls):
+        if cls._rt is None:
+            import ctypes
+            cls._rt = ctypes.CDLL("libcudart.so.12")
+        return cls._rt
+
+    def __init__(self):
+        import ctypes
+        self.h = ctypes.c_void_p()
+        assert self.rt().cudaEventCreate(ctypes.byref(self.h)) == 0
+        self.cuda_event = self.h.value
+
+    def elapsed_ms(self, end) -> float:
+        import ctypes
+        ms = ctypes.c_float()
+        assert self.rt().cudaEventElapsedTime(ctypes.byref(ms), self.h, end.h) == 0
+        return float(ms.value)
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
 
@@ -241,8 +265,8 @@ def main():
     n_ev = args.steps
     ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
     ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
-    ism_s = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
-    ism_e = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    ism_s = [RawEvent() for _ in range(n_ev)]
+    ism_e = [RawEvent() for _ in range(n_ev)]
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -256,7 +280,7 @@ def main():
         if dist:
             dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
-    ism_ms = [a.elapsed_time(b) for a, b in zip(ism_s, ism_e)]
+    ism_ms = [a.elapsed_ms(b) for a, b in zip(ism_s, ism_e)]
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
