@@ -4,17 +4,19 @@
 // What it computes (§2.1-2.2, Eqs. 1-6):
 //   h[m][k] = sum_n A_n * delta'(k/fs - tau_n),   0 <= k < nISM,
 //   A_n = beta_n g_n / (4 pi d_n), tau_n = d_n / c, delta' = Hann-windowed sinc of length T_w.
-// How (DESIGN.md §Kernels): one CTA owns a tile of kTC output samples of one RIR.
-// It enumerates only the lattice images whose window can touch the tile (a
-// spherical shell around the receiver) column by column (n_x, n_y) with the
-// n_z ranges solved in closed form, computes each image's parameters in
-// registers (fp64 delay split, C1/C2/C4), bins the records by delay with a
-// stable counting sort in shared memory (deterministic order), and then every
-// warp accumulates its kS-sample sub-tile from the contiguous record range of
-// its bins: 4 lane groups x 2 packed (f32x2) records per step, accumulators in
-// registers, shuffle reduction at the end, no global atomics.  Thread-block
-// clusters split the images of one tile across `split` CTAs whose partial
-// tiles are reduced through distributed shared memory (fixed order).
+// How (DESIGN.md §5.1): one CTA owns a tile of kTC output samples of one RIR.
+//  1. It enumerates only the lattice images whose window can touch the tile (a
+//     spherical shell around the receiver), column by column (n_x, n_y), with the
+//     n_z range of each column solved exactly (Delta_z is monotone in n_z).
+//  2. Image parameters are computed in registers (fp64 delay, C1/C2/C4) and
+//     written as compact records into a shared-memory window of kCap records;
+//     windows are filled across column batches.
+//  3. A stable counting sort bins the window's records by delay (deterministic).
+//  4. Every warp accumulates its two 8-sample sub-tiles from the contiguous
+//     record range of their bins: 4 lane groups x 2 packed (f32x2) records per
+//     step, accumulators in registers, shuffle reduction at the end.
+// Thread-block clusters split the columns of one tile across `split` CTAs
+// whose partial tiles are summed through distributed shared memory (fixed order).
 #include <cooperative_groups.h>
 #include <cuda_fp16.h>
 
@@ -24,6 +26,9 @@
 namespace cg = cooperative_groups;
 
 namespace gpurir {
+
+constexpr int kSubPerWarp = kTC / (kWarps * kS);  // 8-sample sub-tiles per warp
+static_assert(kSubPerWarp * kWarps * kS == kTC, "tile geometry");
 
 // ----------------------------------------------------------------------------
 // shared-memory layout
@@ -39,6 +44,7 @@ struct ColRec {         // one lattice column (n_x, n_y) of the current batch (3
 struct TileInfo {
   RirGeom g;
   double dlo2, dhi2;    // shell in distance^2
+  double invLz;         // 1 / L_z
   int m, tile, t0, te, tc;
   int nx0, ny0, NX, ncols_mine;
   long long row;        // element offset of the RIR row
@@ -50,7 +56,7 @@ struct Smem {
   TileInfo ti;
   int colpre[kColBatch];          // inclusive prefix of candidate counts
   ColRec col[kColBatch];
-  float2 rec[kCap];               // unsorted records: fp32/fp16 (-x/H, C'), LUT (rowbase, phi)
+  float2 rec[kCap];               // unsorted records: fp32/fp16 (-x/Hs, C'), LUT (rowbase, phi)
   float recA[kCap];               // LUT amplitude
   uint8_t bin[kCap];
   float4 sorted[kCap + 8];        // sorted records; fp32/fp16 modes pack pairs
@@ -82,8 +88,31 @@ __device__ __forceinline__ int block_incl_scan(int v, int* tmp) {
   }
   __syncthreads();
   int r = x + (w > 0 ? tmp[w - 1] : 0);
-  __syncthreads();
   return r;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// sin(pi f) for f in [0, 1) with ~2e-7 relative accuracy (also near f = 0 and f = 1):
+// h = min(f, 1 - f) (exact), sin(pi h) = h P(h^2), minimax degree 4.
+__device__ __forceinline__ float sinpi01(float f) {
+  float h = fminf(f, 1.f - f);
+  float y = h * h;
+  float p = fmaf(0.07768171280622482f, y, -0.5983065366744995f);
+  p = fmaf(p, y, 2.5500807762145996f);
+  p = fmaf(p, y, -5.167710304260254f);
+  p = fmaf(p, y, 3.1415927410125732f);
+  return h * p;
 }
 
 // ----------------------------------------------------------------------------
@@ -108,8 +137,7 @@ __device__ void load_geom(const IsmArgs& A, int m, RirGeom& g, int* status) {
     for (int i = 0; i < 6; i++) beta[i] = A.beta[i];
     pattern = A.pattern;
   }
-  const float pa[5] = {1.f, 0.75f, 0.5f, 0.25f, 0.f};  // C4
-  g.a = pa[pattern];
+  g.a = pattern == 0 ? 1.f : pattern == 1 ? 0.75f : pattern == 2 ? 0.5f : pattern == 3 ? 0.25f : 0.f;  // C4
   float on = sqrtf(orv[0] * orv[0] + orv[1] * orv[1] + orv[2] * orv[2]);
   if (pattern != 0 && !(on > 0.f)) { atomicOr(status, kStatusZeroOrient); on = 1.f; }
   for (int i = 0; i < 3; i++) {
@@ -127,6 +155,19 @@ __device__ void load_geom(const IsmArgs& A, int m, RirGeom& g, int* status) {
   }
 }
 
+// Exact n_z range of one side of a column: all n with lo <= Delta_z(n) <= hi, where
+// Delta_z(n) = z_n - z_r is strictly increasing in n (image n lies in cell [nL, (n+1)L]).
+__device__ __forceinline__ void z_range(const RirGeom& g, double invLz, double lo, double hi, int& first,
+                                        int& last) {
+  const double Lz = g.L[2], sz = g.s[2], rz = g.r[2];
+  int a = (int)floor((rz + lo) * invLz);
+  if (image_coord(a, Lz, sz) - rz < lo) a++;
+  int b = (int)floor((rz + hi) * invLz);
+  if (image_coord(b, Lz, sz) - rz > hi) b--;
+  first = a;
+  last = b;
+}
+
 // ----------------------------------------------------------------------------
 // The kernel
 // ----------------------------------------------------------------------------
@@ -141,7 +182,6 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
   const int prank = (int)cluster.block_rank();
   const int cid = blockIdx.x / P;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double c_over_fs = A.c_over_fs;
   const float H = A.H;
 
   // ---- tile setup (thread 0) ------------------------------------------------
@@ -165,10 +205,11 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
     T.t0 = tile * kTC;
     T.te = min(T.t0 + kTC, nISM);
     T.tc = T.t0 + kTC / 2;
+    T.invLz = 1.0 / T.g.L[2];
     // shell: images with x in (t0 - H, te - 1 + H) can touch samples [t0, te)
     double xlo = (double)T.t0 - H, xhi = (double)(T.te - 1) + H;
-    double dlo = xlo > 0.0 ? xlo * c_over_fs : 0.0;
-    double dhi = xhi * c_over_fs;
+    double dlo = xlo > 0.0 ? xlo * A.c_over_fs : 0.0;
+    double dhi = xhi * A.c_over_fs;
     T.dlo2 = dlo * dlo;
     T.dhi2 = dhi * dhi;
     T.xrel_max = (float)(T.te - 1 - T.t0) + 2.f * H;
@@ -187,8 +228,7 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
     if (T.ncols_mine < 0) T.ncols_mine = 0;
     T.nbins = (int)ceilf(((float)kTC + 2.f * H) / (float)kS) + 1;
   }
-  // LUT table -> shared memory
-  if (MODE == 1) {
+  if (MODE == 1) {  // LUT table -> shared memory
     int n = A.lut_rows * A.lut_cols;
     for (int i = tid; i < n; i += kThreads) lut[i] = A.lut[i];
   }
@@ -197,21 +237,181 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
   const RirGeom& g = T.g;
   const int nbins = T.nbins;
 
-  // ---- per-lane accumulation constants ---------------------------------------
+  // ---- per-lane accumulation constants (two 8-sample sub-tiles per warp) ------
   const int grp = lane >> 3, li = lane & 7;
-  const int s0 = warp * kS;                 // sub-tile start relative to t0
-  const int kf = T.t0 + s0 + li - T.tc;     // sample relative to tc (integer)
-  float2 acc2 = make_float2(0.f, 0.f);
-  const float kv = (float)kf * A.invHs;            // fp32 mode: v = (k - x)/Hs (exact scaling)
-  const float kx = (float)kf * (0.5f * A.invHs);   // fp16 mode: x' = (k - x)/(2 Hs)
-  const int bfirst = warp, blast = warp + A.nbw;  // bins [bfirst, blast) touch this sub-tile
+  int kfs[kSubPerWarp];
+  float2 acc[kSubPerWarp];
+#pragma unroll
+  for (int s = 0; s < kSubPerWarp; s++) {
+    kfs[s] = T.t0 + (warp * kSubPerWarp + s) * kS + li - T.tc;  // sample relative to tc
+    acc[s] = make_float2(0.f, 0.f);
+  }
 
   const double fs_over_c = A.fs_over_c;
   const double sc2 = fs_over_c * fs_over_c;
-  const float inv4pi = 0.0795774715459476679f;
+  const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f;
 
+  // ---- window processing: stable bin sort + accumulation -----------------------
+  auto process_window = [&](int nw) {
+    for (int i = tid; i < kWarps * kMaxBins; i += kThreads) (&sm.warpcnt[0][0])[i] = 0;
+    __syncthreads();
+    const int per_warp = (nw + kWarps - 1) / kWarps;
+    const int wbeg = warp * per_warp, wend = min(nw, wbeg + per_warp);
+    const unsigned lt = (1u << lane) - 1u;
+    for (int r0 = wbeg; r0 < wend; r0 += 32) {
+      int r = r0 + lane;
+      int b = r < wend ? (int)sm.bin[r] : (int)kDiscard;
+      unsigned peers = __match_any_sync(0xffffffffu, b);
+      if (b != kDiscard && (peers & lt) == 0) sm.warpcnt[warp][b] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    if (tid < nbins) {  // per bin: prefix over warps
+      int s = 0;
+      for (int w = 0; w < kWarps; w++) { int c = sm.warpcnt[w][tid]; sm.warpcnt[w][tid] = s; s += c; }
+      sm.binstart[tid] = s;  // bin total for now
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of bin totals (nbins <= 128)
+      int carry = 0;
+      for (int b0 = 0; b0 < nbins; b0 += 32) {
+        int b = b0 + lane;
+        int v = b < nbins ? sm.binstart[b] : 0;
+        int x = warp_incl_scan(v, lane);
+        if (b < nbins) sm.binstart[b] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (lane == 0) sm.binstart[nbins] = carry;
+    }
+    __syncthreads();
+    for (int r0 = wbeg; r0 < wend; r0 += 32) {
+      int r = r0 + lane;
+      int b = r < wend ? (int)sm.bin[r] : (int)kDiscard;
+      unsigned peers = __match_any_sync(0xffffffffu, b);
+      if (b != kDiscard) {
+        int pos = sm.binstart[b] + sm.warpcnt[warp][b] + __popc(peers & lt);
+        float2 rc = sm.rec[r];
+        if (MODE == 1) {
+          sm.sorted[pos] = make_float4(rc.x, rc.y, sm.recA[r], 0.f);
+        } else {  // pair layout: sorted[p>>1] = (nxv_even, nxv_odd, C_even, C_odd)
+          float* pp = reinterpret_cast<float*>(&sm.sorted[pos >> 1]);
+          pp[pos & 1] = rc.x;
+          pp[2 + (pos & 1)] = rc.y;
+        }
+      }
+      __syncwarp();
+      if (b != kDiscard && (peers & lt) == 0) sm.warpcnt[warp][b] += __popc(peers);
+      __syncwarp();
+    }
+    if (tid < 8) {  // dummy records after the last one (outside every window: v = kv - 1e4)
+      int pos = sm.binstart[nbins] + tid;
+      if (MODE == 1) {
+        sm.sorted[pos] = make_float4(__int_as_float(0), 0.f, 0.f, 0.f);
+      } else {
+        float* pp = reinterpret_cast<float*>(&sm.sorted[pos >> 1]);
+        pp[pos & 1] = -1.0e4f;
+        pp[2 + (pos & 1)] = 0.f;
+      }
+    }
+    __syncthreads();
+
+#pragma unroll
+    for (int s = 0; s < kSubPerWarp; s++) {
+      const int sub = warp * kSubPerWarp + s;
+      const int ra = sm.binstart[sub], rb = sm.binstart[min(sub + A.nbw, nbins)];
+      if (MODE == 0) {
+        // Eq. 5-6: acc += C' w(u) / v, v = (k - x)/Hs, w = Hann window (R5), C' = -A sin(pi f)/(pi Hs)
+        const float kv = (float)kfs[s] * A.invHs;
+        const float2 kv2 = make_float2(kv, kv);
+        const float2 mr2 = make_float2(-A.rho2, -A.rho2);
+        const float2 b3 = make_float2(A.wb[3], A.wb[3]), b2 = make_float2(A.wb[2], A.wb[2]);
+        const float2 b1 = make_float2(A.wb[1], A.wb[1]), b0 = make_float2(A.wb[0], A.wb[0]);
+        float2 a2 = acc[s];
+        int j = (ra & ~1) + 2 * grp;
+        for (; j + 2 * kG < rb; j += 4 * kG) {  // two independent pairs per iteration (ILP)
+          float4 p0 = sm.sorted[j >> 1];
+          float4 p1 = sm.sorted[(j + 2 * kG) >> 1];
+          float2 v0 = __fadd2_rn(kv2, make_float2(p0.x, p0.y));
+          float2 v1 = __fadd2_rn(kv2, make_float2(p1.x, p1.y));
+          float2 s0 = __ffma2_rn(v0, v0, mr2);
+          float2 s1 = __ffma2_rn(v1, v1, mr2);
+          s0.x = fminf(s0.x, 0.f); s0.y = fminf(s0.y, 0.f);
+          s1.x = fminf(s1.x, 0.f); s1.y = fminf(s1.y, 0.f);
+          float2 q0 = __ffma2_rn(b3, s0, b2), q1 = __ffma2_rn(b3, s1, b2);
+          q0 = __ffma2_rn(q0, s0, b1); q1 = __ffma2_rn(q1, s1, b1);
+          q0 = __ffma2_rn(q0, s0, b0); q1 = __ffma2_rn(q1, s1, b0);
+          float2 c0 = __fmul2_rn(q0, s0), c1 = __fmul2_rn(q1, s1);
+          float2 w0 = __fmul2_rn(c0, c0), w1 = __fmul2_rn(c1, c1);
+          float2 r0 = make_float2(rcp_approx(v0.x), rcp_approx(v0.y));
+          float2 r1 = make_float2(rcp_approx(v1.x), rcp_approx(v1.y));
+          a2 = __ffma2_rn(make_float2(p0.z, p0.w), __fmul2_rn(w0, r0), a2);
+          a2 = __ffma2_rn(make_float2(p1.z, p1.w), __fmul2_rn(w1, r1), a2);
+        }
+        if (j < rb) {
+          float4 p0 = sm.sorted[j >> 1];
+          float2 v0 = __fadd2_rn(kv2, make_float2(p0.x, p0.y));
+          float2 s0 = __ffma2_rn(v0, v0, mr2);
+          s0.x = fminf(s0.x, 0.f); s0.y = fminf(s0.y, 0.f);
+          float2 q0 = __ffma2_rn(b3, s0, b2);
+          q0 = __ffma2_rn(q0, s0, b1);
+          q0 = __ffma2_rn(q0, s0, b0);
+          float2 c0 = __fmul2_rn(q0, s0);
+          float2 w0 = __fmul2_rn(c0, c0);
+          float2 r0 = make_float2(rcp_approx(v0.x), rcp_approx(v0.y));
+          a2 = __ffma2_rn(make_float2(p0.z, p0.w), __fmul2_rn(w0, r0), a2);
+        }
+        acc[s] = a2;
+      } else if (MODE == 2) {
+        // fp16 / half2 (P:242-269): t - tau in fp32 (P:267), window by the Eq. 11 polynomial
+        // cos(pi x) at x = u / (2H) (reading C12), half2 Horner (Eq. 12), fp32 accumulation (C13).
+        const float kx = (float)kfs[s] * (0.5f * A.invHs);
+        const float2 kx2 = make_float2(kx, kx);
+        const __half2 c6 = __float2half2_rn(A.hc[2]), c4 = __float2half2_rn(A.hc[1]);
+        const __half2 c2 = __float2half2_rn(A.hc[0]), c0 = __float2half2_rn(1.f);
+        const __half2 xcl = __float2half2_rn(A.x2clamp);
+        __half2 acch = __float2half2_rn(0.f);
+        float2 a2 = acc[s];
+        int steps = 0;
+        for (int j = (ra & ~1) + 2 * grp; j < rb; j += 2 * kG) {
+          float4 pr = sm.sorted[j >> 1];
+          float2 x = __fadd2_rn(kx2, make_float2(pr.x, pr.y));      // x' = (k - tau fs) / (2 Hs), fp32
+          __half2 hx = __float22half2_rn(x);
+          __half2 x2 = __hmin2(__hmul2(hx, hx), xcl);                // clamp: |u/(2H)| <= 1/2 (window edge)
+          __half2 p = __hfma2(c6, x2, c4);
+          p = __hfma2(p, x2, c2);
+          p = __hfma2(p, x2, c0);                                    // cos(pi x), Eq. 11
+          __half2 w = __hmul2(p, p);                                 // Hann window
+          float2 r = make_float2(rcp_approx(x.x), rcp_approx(x.y));
+          float2 q = __fmul2_rn(make_float2(pr.z, pr.w), r);         // bounded by ~A (scaled 2^10)
+          acch = __hfma2(w, __float22half2_rn(q), acch);
+          if (++steps == 8) {
+            float2 f = __half22float2(acch);
+            a2.x += f.x; a2.y += f.y;
+            acch = __float2half2_rn(0.f);
+            steps = 0;
+          }
+        }
+        float2 f = __half22float2(acch);
+        a2.x += f.x; a2.y += f.y;
+        acc[s] = a2;
+      } else {
+        // LUT (Eq. 9, P:229-238): one table pair per tap, phase-major rows, linear interpolation
+        float a = acc[s].x;
+        for (int j = ra + grp; j < rb; j += kG) {
+          float4 rc = sm.sorted[j];
+          int idx = __float_as_int(rc.x) + kfs[s];
+          float2 d = lut[idx];
+          a = fmaf(rc.z, fmaf(rc.y, d.y, d.x), a);
+        }
+        acc[s].x = a;
+      }
+    }
+    __syncthreads();  // records of this window are consumed
+  };
+
+  // ---- enumeration: column batches, candidate stream, windows of kCap records ----
+  int filled = 0;
   for (int qb = 0; qb < T.ncols_mine; qb += kColBatch) {
-    // ---- column records (one column per thread) ------------------------------
     int cnt = 0;
     {
       int q = qb + tid;
@@ -232,16 +432,15 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
         if (rho2 < T.dhi2) {
           double zhi = sqrt(T.dhi2 - rho2);
           double zlo = T.dlo2 > rho2 ? sqrt(T.dlo2 - rho2) : 0.0;
-          double Lz = g.L[2], rz = g.r[2];
-          // cells [nL, (n+1)L] meeting (zlo, zhi) (positive side) / (-zhi, -zlo), widened by one cell
-          int plo = (int)floor((rz + zlo) / Lz) - 1, phi = (int)ceil((rz + zhi) / Lz);
-          int nlo = (int)floor((rz - zhi) / Lz) - 1, nhi = (int)ceil((rz - zlo) / Lz);
-          int zl = g.nlo[2], zh = g.nhi[2] - 1;
-          if (nhi >= plo - 1) { plo = min(plo, nlo); nlo = 1; nhi = 0; }  // merged
-          plo = max(plo, zl); phi = min(phi, zh);
-          nlo = max(nlo, zl); nhi = min(nhi, zh);
-          int n1 = max(0, phi - plo + 1), n2 = max(0, nhi - nlo + 1);
-          cr.r1lo = plo; r1n = n1; cr.r2lo = nlo;
+          int pa, pb, na, nbz;
+          z_range(g, T.invLz, zlo, zhi, pa, pb);     // Delta_z in [zlo, zhi]
+          z_range(g, T.invLz, -zhi, -zlo, na, nbz);  // Delta_z in [-zhi, -zlo]
+          if (nbz >= pa - 1) { pa = min(pa, na); na = 1; nbz = 0; }  // sides touch (zlo ~ 0): merge
+          const int zl = g.nlo[2], zh = g.nhi[2] - 1;
+          pa = max(pa, zl); pb = min(pb, zh);
+          na = max(na, zl); nbz = min(nbz, zh);
+          int n1 = max(0, pb - pa + 1), n2 = max(0, nbz - na + 1);
+          cr.r1lo = pa; r1n = n1; cr.r2lo = na;
           cnt = n1 + n2;
         }
       }
@@ -253,218 +452,109 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
     __syncthreads();
     const int total = sm.colpre[kColBatch - 1];
 
-    for (int base = 0; base < total; base += kCap) {
-      const int nw = min(kCap, total - base);
-      // ---- emission: image parameters (Eqs. 1-4, A16) -> records ---------------
-      for (int i = tid; i < nw; i += kThreads) {
-        int gi = base + i;
-        int lo = 0, hi = kColBatch - 1;  // first column with colpre > gi
+    for (int base = 0; base < total;) {
+      const int take = min(kCap - filled, total - base);
+      // ---- emission: contiguous candidate runs per thread, one binary search each ----
+      const int R = (take + kThreads - 1) / kThreads;
+      const int g0 = base + tid * R, g1 = min(g0 + R, base + take);
+      if (g0 < g1) {
+        int lo = 0, hi = kColBatch - 1;  // first column with colpre > g0
         while (lo < hi) {
           int mid = (lo + hi) >> 1;
-          if (sm.colpre[mid] > gi) hi = mid; else lo = mid + 1;
+          if (sm.colpre[mid] > g0) hi = mid; else lo = mid + 1;
         }
-        const ColRec& cr = sm.col[lo];
-        int l = gi - (lo > 0 ? sm.colpre[lo - 1] : 0);
-        const int r1n = (int)(cr.r1n_flags & 0x3FFFFFFFu);
-        int nz = l < r1n ? cr.r1lo + l : cr.r2lo + (l - r1n);
-        double dz = image_coord(nz, g.L[2], g.s[2]) - g.r[2];
-        double x2 = fma(dz, dz, cr.rho2) * sc2;  // (d fs / c)^2
-        uint8_t b = kDiscard;
-        float2 rec = make_float2(0.f, 0.f);
-        float recA = 0.f;
-        if (x2 == 0.0) {
-          atomicOr(A.status, kStatusDegenerate);
-        } else {
-          float x0f;
-          float xr = delay_rel(x2, T.tc, x0f);
-          float xrel = xr + (float)(kTC / 2) + H;  // x - (t0 - H)
-          if (xrel > 0.f && xrel < T.xrel_max) {
-            b = (uint8_t)(int)(xrel * (1.f / (float)kS));
-            // amplitude A = beta_n g / (4 pi d), 1/d = fs / (c x)
-            float invd = (float)fs_over_c * __frcp_rn(x0f);
-            uint32_t sgn = (cr.r1n_flags >> 30) & 1u;
-            bool zero = (cr.r1n_flags >> 31) != 0;
-            float lz = axis_beta(nz, 2, g, sgn, zero);
-            float bn = zero ? 0.f : exp2f(cr.lxy + lz);
-            if (sgn) bn = -bn;
-            float cth = (cr.dx * g.o[0] + cr.dy * g.o[1] + (float)dz * g.o[2]) * invd;
-            float gain = g.a + (1.f - g.a) * cth;
-            float amp = bn * gain * invd * inv4pi;
-            if (MODE == 1) {
-              // Eq. 9 LUT: position u Q = kf Q - xq, xq = xr Q = iq + phi
-              float xq = xr * (float)A.lutQ;
-              float fiq = floorf(xq);
-              float phi = xq - fiq;
-              int iq1 = (int)fiq + 1;
-              int php = iq1 & (A.lutQ - 1);           // (iq+1) mod Q (Q power of 2)
-              int aa = (iq1 - php) / A.lutQ;            // floor((iq+1)/Q)
-              int ph = (A.lutQ - php) & (A.lutQ - 1);
-              int jsh = aa + (php > 0 ? 1 : 0);
-              int rowbase = ph * A.lut_cols + A.lut_joff - jsh;
-              rec = make_float2(__int_as_float(rowbase), phi);
-              recA = amp;
-            } else {
-              // hoisted sinc numerator: sin(pi u) = -(-1)^(kf - j) sin(pi f), u = kf - xr, xr = j + f
-              float fj = floorf(xr);
-              float f = xr - fj;
-              if (f == 0.f) {  // exact integer delay: nudge by one ulp (C-nudge)
-                xr = nextafterf(xr, 1e30f);
-                fj = floorf(xr);
-                f = xr - fj;
+        int j = lo;
+        int before = j > 0 ? sm.colpre[j - 1] : 0;
+        for (int gi = g0; gi < g1; gi++) {
+          while (sm.colpre[j] <= gi) { before = sm.colpre[j]; j++; }
+          const ColRec& cr = sm.col[j];
+          const int l = gi - before;
+          const int r1n = (int)(cr.r1n_flags & 0x3FFFFFFFu);
+          const int nz = l < r1n ? cr.r1lo + l : cr.r2lo + (l - r1n);
+          const double dz = image_coord(nz, g.L[2], g.s[2]) - g.r[2];
+          const double x2 = fma(dz, dz, cr.rho2) * sc2;  // (d fs / c)^2
+          uint8_t b = kDiscard;
+          float2 rec = make_float2(0.f, 0.f);
+          float recA = 0.f;
+          if (x2 == 0.0) {
+            atomicOr(A.status, kStatusDegenerate);
+          } else {
+            float x0f;
+            float xr = delay_rel(x2, T.tc, x0f);
+            float xrel = xr + (float)(kTC / 2) + H;  // x - (t0 - H)
+            if (xrel > 0.f && xrel < T.xrel_max) {
+              b = (uint8_t)(int)(xrel * (1.f / (float)kS));
+              // amplitude A = beta_n g / (4 pi d), 1/d = fs / (c x)     (Eq. 4, A16)
+              const float rx = rcp_approx(x0f);
+              uint32_t sgn = (cr.r1n_flags >> 30) & 1u;
+              bool zero = (cr.r1n_flags >> 31) != 0;
+              const float lz = axis_beta(nz, 2, g, sgn, zero);
+              float bn = zero ? 0.f : ex2_approx(cr.lxy + lz);
+              if (sgn) bn = -bn;
+              const float cth = (cr.dx * g.o[0] + cr.dy * g.o[1] + (float)dz * g.o[2]) * ((float)fs_over_c * rx);
+              const float gain = g.a + (1.f - g.a) * cth;
+              const float amp = bn * gain * rx * fs_over_c_4pi;
+              if (MODE == 1) {
+                // Eq. 9 LUT: position u Q = kf Q - xq, xq = xr Q = iq + phi
+                float xq = xr * (float)A.lutQ;
+                float fiq = floorf(xq);
+                float phi = xq - fiq;
+                int iq1 = (int)fiq + 1;
+                int php = iq1 & (A.lutQ - 1);           // (iq+1) mod Q (Q power of 2)
+                int aa = (iq1 - php) / A.lutQ;          // floor((iq+1)/Q)
+                int ph = (A.lutQ - php) & (A.lutQ - 1);
+                int jsh = aa + (php > 0 ? 1 : 0);
+                int rowbase = ph * A.lut_cols + A.lut_joff - jsh;
+                rec = make_float2(__int_as_float(rowbase), phi);
+                recA = amp;
+              } else {
+                // hoisted sinc numerator: sin(pi u) = -(-1)^(kf - j) sin(pi f), u = kf - xr, xr = j + f
+                float fj = floorf(xr);
+                float f = xr - fj;
+                if (f == 0.f) {  // exact integer delay: nudge by one ulp (reading R3)
+                  xr = nextafterf(xr, 1e30f);
+                  fj = floorf(xr);
+                  f = xr - fj;
+                }
+                const int jj = (int)fj;
+                float cc = -amp * sinpi01(f) * 0.318309886183790672f;
+                if (jj & 1) cc = -cc;
+                if (MODE == 0) rec = make_float2(-xr * A.invHs, cc * A.invHs);
+                else rec = make_float2(-xr * (0.5f * A.invHs), cc * (0.5f * A.invHs) * 1024.f);
               }
-              int j = (int)fj;
-              float cc = -amp * sinpif(f) * 0.318309886183790672f;
-              if (j & 1) cc = -cc;
-              if (MODE == 0) rec = make_float2(-xr * A.invHs, cc * A.invHs);
-              else rec = make_float2(-xr * (0.5f * A.invHs), cc * (0.5f * A.invHs) * 1024.f);
             }
           }
-        }
-        sm.rec[i] = rec;
-        if (MODE == 1) sm.recA[i] = recA;
-        sm.bin[i] = b;
-      }
-      // clear per-warp bin counters
-      for (int i = tid; i < kWarps * kMaxBins; i += kThreads) (&sm.warpcnt[0][0])[i] = 0;
-      __syncthreads();
-
-      // ---- stable counting sort by delay bin (deterministic order) -------------
-      const int per_warp = (nw + kWarps - 1) / kWarps;
-      const int wbeg = warp * per_warp, wend = min(nw, wbeg + per_warp);
-      const unsigned lt = (1u << lane) - 1u;
-      for (int r0 = wbeg; r0 < wend; r0 += 32) {
-        int r = r0 + lane;
-        int b = r < wend ? (int)sm.bin[r] : (int)kDiscard;
-        unsigned peers = __match_any_sync(0xffffffffu, b);
-        if (b != kDiscard && (peers & lt) == 0) sm.warpcnt[warp][b] += __popc(peers);
-        __syncwarp();
-      }
-      __syncthreads();
-      if (tid < nbins) {  // per bin: prefix over warps
-        int s = 0;
-        for (int w = 0; w < kWarps; w++) { int c = sm.warpcnt[w][tid]; sm.warpcnt[w][tid] = s; s += c; }
-        sm.binstart[tid] = s;  // bin total for now
-      }
-      __syncthreads();
-      if (warp == 0) {  // exclusive scan of bin totals (nbins <= 128)
-        int carry = 0;
-        for (int b0 = 0; b0 < nbins; b0 += 32) {
-          int b = b0 + lane;
-          int v = b < nbins ? sm.binstart[b] : 0;
-          int x = warp_incl_scan(v, lane);
-          if (b < nbins) sm.binstart[b] = carry + x - v;
-          carry += __shfl_sync(0xffffffffu, x, 31);
-        }
-        if (lane == 0) sm.binstart[nbins] = carry;
-      }
-      __syncthreads();
-      for (int r0 = wbeg; r0 < wend; r0 += 32) {
-        int r = r0 + lane;
-        int b = r < wend ? (int)sm.bin[r] : (int)kDiscard;
-        unsigned peers = __match_any_sync(0xffffffffu, b);
-        if (b != kDiscard) {
-          int pos = sm.binstart[b] + sm.warpcnt[warp][b] + __popc(peers & lt);
-          float2 rc = sm.rec[r];
-          if (MODE == 1) {
-            sm.sorted[pos] = make_float4(rc.x, rc.y, sm.recA[r], 0.f);
-          } else {  // pair layout: sorted[p>>1] = (nxv_even, nxv_odd, C_even, C_odd)
-            float* pp = reinterpret_cast<float*>(&sm.sorted[pos >> 1]);
-            pp[pos & 1] = rc.x;
-            pp[2 + (pos & 1)] = rc.y;
-          }
-        }
-        __syncwarp();
-        if (b != kDiscard && (peers & lt) == 0) sm.warpcnt[warp][b] += __popc(peers);
-        __syncwarp();
-      }
-      // dummy records after the last one (never in any window: v = kv - 1e4)
-      if (tid < 8) {
-        int pos = sm.binstart[nbins] + tid;
-        if (MODE == 1) {
-          sm.sorted[pos] = make_float4(__int_as_float(0), 0.f, 0.f, 0.f);
-        } else {
-          float* pp = reinterpret_cast<float*>(&sm.sorted[pos >> 1]);
-          pp[pos & 1] = -1.0e4f;
-          pp[2 + (pos & 1)] = 0.f;
+          const int dst = filled + (gi - base);
+          sm.rec[dst] = rec;
+          if (MODE == 1) sm.recA[dst] = recA;
+          sm.bin[dst] = b;
         }
       }
-      __syncthreads();
-
-      // ---- accumulation: warp sub-tile from its contiguous record range --------
-      const int ra = sm.binstart[bfirst], rb = sm.binstart[min(blast, nbins)];
-      if (MODE == 0) {
-        const float2 kv2 = make_float2(kv, kv);
-        const float2 mr2 = make_float2(-A.rho2, -A.rho2);
-        const float2 b3 = make_float2(A.wb[3], A.wb[3]), b2 = make_float2(A.wb[2], A.wb[2]);
-        const float2 b1 = make_float2(A.wb[1], A.wb[1]), b0 = make_float2(A.wb[0], A.wb[0]);
-        for (int j = (ra & ~1) + 2 * grp; j < rb; j += 2 * kG) {
-          float4 pr = sm.sorted[j >> 1];
-          float2 v = __fadd2_rn(kv2, make_float2(pr.x, pr.y));     // v = (k - x) / Hs
-          float2 sp = __ffma2_rn(v, v, mr2);                         // sigma = v^2 - rho^2
-          sp.x = fminf(sp.x, 0.f); sp.y = fminf(sp.y, 0.f);          // window support |u| < H
-          float2 p = __ffma2_rn(b3, sp, b2);
-          p = __ffma2_rn(p, sp, b1);
-          p = __ffma2_rn(p, sp, b0);
-          float2 cw = __fmul2_rn(p, sp);                             // -cos(pi u / (2H))
-          float2 w = __fmul2_rn(cw, cw);                             // Hann window (Eq. 6)
-          float2 r;
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(v.x));
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(v.y));
-          float2 t = __fmul2_rn(w, r);
-          acc2 = __ffma2_rn(make_float2(pr.z, pr.w), t, acc2);       // += C' w / v
-        }
-      } else if (MODE == 2) {
-        // fp16 / half2 (P:242-269): t - tau in fp32 (P:267), window by the Eq. 11 polynomial
-        // cos(pi x) at x = u / (2H) (reading C12), half2 Horner (Eq. 12), fp32 accumulation (C13).
-        const float2 kx2 = make_float2(kx, kx);
-        const __half2 c6 = __float2half2_rn(A.hc[2]), c4 = __float2half2_rn(A.hc[1]);
-        const __half2 c2 = __float2half2_rn(A.hc[0]), c0 = __float2half2_rn(1.f);
-        const __half2 quarter = __float2half2_rn(A.x2clamp);
-        __half2 acch = __float2half2_rn(0.f);
-        int steps = 0;
-        for (int j = (ra & ~1) + 2 * grp; j < rb; j += 2 * kG) {
-          float4 pr = sm.sorted[j >> 1];
-          float2 x = __fadd2_rn(kx2, make_float2(pr.x, pr.y));      // x' = (k - tau fs) / (2 Hs), fp32
-          __half2 hx = __float22half2_rn(x);
-          __half2 x2 = __hmin2(__hmul2(hx, hx), quarter);            // clamp: |u/(2H)| <= 1/2 (window edge)
-          __half2 p = __hfma2(c6, x2, c4);
-          p = __hfma2(p, x2, c2);
-          p = __hfma2(p, x2, c0);                                    // cos(pi x), Eq. 11
-          __half2 w = __hmul2(p, p);                                 // Hann window
-          float2 r;
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(x.x));
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(x.y));
-          float2 q = __fmul2_rn(make_float2(pr.z, pr.w), r);         // bounded by ~A (scaled 2^10)
-          acch = __hfma2(w, __float22half2_rn(q), acch);
-          if (++steps == 8) {
-            float2 f = __half22float2(acch);
-            acc2.x += f.x; acc2.y += f.y;
-            acch = __float2half2_rn(0.f);
-            steps = 0;
-          }
-        }
-        float2 f = __half22float2(acch);
-        acc2.x += f.x; acc2.y += f.y;
-      } else {
-        // LUT (Eq. 9, P:229-238): one table pair per tap, phase-major rows, linear interpolation
-        for (int j = ra + grp; j < rb; j += kG) {
-          float4 rc = sm.sorted[j];
-          int idx = __float_as_int(rc.x) + kf;
-          float2 d = lut[idx];
-          acc2.x = fmaf(rc.z, fmaf(rc.y, d.y, d.x), acc2.x);
-        }
+      filled += take;
+      base += take;
+      if (filled == kCap) {
+        __syncthreads();
+        process_window(filled);
+        filled = 0;
       }
-      __syncthreads();  // records of this window are consumed
     }
+    __syncthreads();  // column records are replaced by the next batch
+  }
+  if (filled > 0) {
+    __syncthreads();
+    process_window(filled);
   }
 
   // ---- reduce lane groups, apply the lane sign, write the tile ----------------
-  float acc = acc2.x + acc2.y;
-  acc += __shfl_xor_sync(0xffffffffu, acc, 8);
-  acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-  if (MODE == 0) { if (kf & 1) acc = -acc; }
-  else if (MODE == 2) { acc *= (1.f / 1024.f); if (kf & 1) acc = -acc; }
-  if (grp == 0) sm.outtile[s0 + li] = acc;
+#pragma unroll
+  for (int s = 0; s < kSubPerWarp; s++) {
+    float a = acc[s].x + acc[s].y;
+    a += __shfl_xor_sync(0xffffffffu, a, 8);
+    a += __shfl_xor_sync(0xffffffffu, a, 16);
+    if (MODE == 0) { if (kfs[s] & 1) a = -a; }
+    else if (MODE == 2) { a *= (1.f / 1024.f); if (kfs[s] & 1) a = -a; }
+    if (grp == 0) sm.outtile[(warp * kSubPerWarp + s) * kS + li] = a;
+  }
   if (P > 1) {
     cluster.sync();
     if (prank == 0 && tid < kTC) {
@@ -496,19 +586,18 @@ __global__ void image_params_kernel(IsmArgs A, double* x_out, float* A_out) {
     double x2 = fma(dz, dz, dx * dx + dy * dy) * (A.fs_over_c * A.fs_over_c);
     if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); x_out[i] = 0.0; A_out[i] = 0.f; continue; }
     float x0f;
-    float xr = delay_rel(x2, 0, x0f);  // reference 0: full delay in fp32 + fp64 residual
+    (void)delay_rel(x2, 0, x0f);
     double x0d = (double)x0f;
-    double xfull = x0d + (x2 - x0d * x0d) / (2.0 * x0d);
-    (void)xr;
-    float invd = (float)A.fs_over_c * __frcp_rn(x0f);
+    double xfull = x0d + (x2 - x0d * x0d) / (2.0 * x0d);  // same fp64 Newton step, reference 0
+    const float rx = rcp_approx(x0f);
     uint32_t sgn = 0; bool zero = false;
     float lb = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero) + axis_beta(nz, 2, g, sgn, zero);
-    float bn = zero ? 0.f : exp2f(lb);
+    float bn = zero ? 0.f : ex2_approx(lb);
     if (sgn) bn = -bn;
-    float cth = ((float)dx * g.o[0] + (float)dy * g.o[1] + (float)dz * g.o[2]) * invd;
+    float cth = ((float)dx * g.o[0] + (float)dy * g.o[1] + (float)dz * g.o[2]) * ((float)A.fs_over_c * rx);
     float gain = g.a + (1.f - g.a) * cth;
     x_out[i] = xfull;
-    A_out[i] = bn * gain * invd * 0.0795774715459476679f;
+    A_out[i] = bn * gain * rx * (float)A.fs_over_c * 0.0795774715459476679f;
   }
 }
 
@@ -518,12 +607,19 @@ size_t ism_smem_bytes(int mode, int lut_rows, int lut_cols) {
   return s;
 }
 
+template <int MODE>
+static cudaError_t launch_mode(const cudaLaunchConfig_t& cfg, const IsmArgs& A) {
+  cudaError_t e = cudaFuncSetAttribute(ism_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)cfg.dynamicSmemBytes);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernelEx(&cfg, ism_kernel<MODE>, A);
+}
+
 cudaError_t launch_ism(const IsmArgs& A, int mode, int split, long long nclusters, cudaStream_t stream) {
-  size_t smem = ism_smem_bytes(mode, A.lut_rows, A.lut_cols);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nclusters * split), 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = ism_smem_bytes(mode, A.lut_rows, A.lut_cols);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -532,20 +628,10 @@ cudaError_t launch_ism(const IsmArgs& A, int mode, int split, long long ncluster
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e;
   switch (mode) {
-    case 0:
-      e = cudaFuncSetAttribute(ism_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      return cudaLaunchKernelEx(&cfg, ism_kernel<0>, A);
-    case 1:
-      e = cudaFuncSetAttribute(ism_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      return cudaLaunchKernelEx(&cfg, ism_kernel<1>, A);
-    default:
-      e = cudaFuncSetAttribute(ism_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      return cudaLaunchKernelEx(&cfg, ism_kernel<2>, A);
+    case 0: return launch_mode<0>(cfg, A);
+    case 1: return launch_mode<1>(cfg, A);
+    default: return launch_mode<2>(cfg, A);
   }
 }
 
