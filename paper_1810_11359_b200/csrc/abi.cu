@@ -30,6 +30,8 @@ int cuda_fail(cudaError_t e, const char* where) {
 // Per-device status word and LUT cache (lazily created, process lifetime).
 struct DeviceState {
   int* status = nullptr;
+  int* work_counter = nullptr;  // persistent-kernel work queue head
+  int num_sms = 0;
   float2* lut = nullptr;
   size_t lut_cap = 0;
   double lut_Tw = 0, lut_fs = 0;
@@ -50,6 +52,10 @@ DeviceState* device_state(int* err) {
     if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMalloc(status)"); return nullptr; }
     e = cudaMemset(d.status, 0, sizeof(int));
     if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMemset(status)"); return nullptr; }
+    e = cudaMalloc(&d.work_counter, sizeof(int));
+    if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMalloc(counter)"); return nullptr; }
+    e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) { *err = cuda_fail(e, "num_sms"); return nullptr; }
   }
   *err = GPURIR_OK;
   return &d;
@@ -144,6 +150,14 @@ int auto_split(long long nclusters, int requested) {
   int s = 1;
   while (s < kMaxSplit && nclusters * s < 148LL * 4) s *= 2;
   return s;
+}
+
+// Persistent warp-specialised kernel when there are enough (RIR, tile) work items to keep one CTA per
+// SM busy; the cluster-split kernel otherwise (latency-bound small calls).  split < 0 forces persistent.
+bool use_persistent(long long n_work, int split, const DeviceState* d) {
+  if (split < 0) return true;
+  if (split > 0) return false;
+  return n_work >= 4LL * d->num_sms;
 }
 
 int finish(const gpurir_opts& o, cudaStream_t st, DeviceState* d) {
@@ -270,9 +284,14 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
       A.lutQ = o.lut_Q;
     }
     long long nclusters = (long long)A.nTiles * M;
-    int split = auto_split(nclusters, o.split);
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
-    cudaError_t e = launch_ism(A, o.mode, split, nclusters, stream);
+    cudaError_t e;
+    if (use_persistent(nclusters, o.split, d)) {
+      e = launch_ism_ws(A, o.mode, nclusters, d->work_counter, d->num_sms, stream);
+    } else {
+      int split = auto_split(nclusters, o.split);
+      e = launch_ism(A, o.mode, split, nclusters, stream);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "launch_ism");
     if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);
   }
@@ -380,9 +399,10 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
       A.lut = d->lut; A.lut_rows = d->lut_rows; A.lut_cols = d->lut_cols; A.lut_joff = d->lut_joff;
       A.lutQ = o.lut_Q;
     }
-    int split = auto_split((long long)tiles.size(), o.split);
+    long long nw = (long long)tiles.size();
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
-    e = launch_ism(A, o.mode, split, (long long)tiles.size(), stream);
+    if (use_persistent(nw, o.split, d)) e = launch_ism_ws(A, o.mode, nw, d->work_counter, d->num_sms, stream);
+    else e = launch_ism(A, o.mode, auto_split(nw, o.split), nw, stream);
     if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_ism(batch)"); }
     if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);
   }

@@ -1,0 +1,536 @@
+// ism_ws_kernel.cu — persistent, warp-specialised ISM kernel for large batches
+// (hot-path rows a1-a5 of SURVEY.md §8(a); same mathematics as ism_kernel.cu).
+//
+// One CTA per SM loops over (RIR, 256-sample tile) work items taken heaviest-first
+// from a global counter.  Inside the CTA:
+//   producer warps (8): enumerate the shell images of a tile column by column
+//     (exact n_z ranges), compute each image's parameters in registers
+//     (Eqs. 1-4; fp64 delay), append compact records to a
+//     private window, stable-sort the window by delay bin and publish it into
+//     one of two shared buffers;
+//   consumer warps (16): wait for a published buffer, accumulate their two
+//     8-sample sub-tiles from the contiguous record range of their bins
+//     (Eqs. 5-6), release the buffer, and write the tile when its last window
+//     has been consumed.
+// Producer -> consumer hand-off uses named barriers (bar.arrive / bar.sync),
+// so emission and sorting of window i+1 overlap the accumulation of window i
+// and the consumer warps never wait on producer-internal phases.
+#include <cuda_fp16.h>
+
+#include "ism_common.cuh"
+
+namespace gpurir {
+
+constexpr int kPW = 8;                       // producer warps
+constexpr int kCW = 16;                      // consumer warps
+constexpr int kPT = kPW * 32;                // producer threads
+constexpr int kWsThreads = (kPW + kCW) * 32; // 768
+constexpr int kWsTC = kCW * 2 * kS;          // 256 samples per tile
+template <int MODE> struct WsCap { static constexpr int v = MODE == 1 ? 2048 : 4096; };  // records per window
+constexpr int kWsColBatch = kPT;             // columns per enumeration batch
+constexpr int kBzMax = 1024;                 // z-factor table entries
+static_assert(kWsTC == kTC, "tile size shared with the host planner");
+
+constexpr int kBarFull0 = 1;   // + buffer: producers arrive, consumers sync
+constexpr int kBarEmpty0 = 3;  // + buffer: consumers arrive, producers sync
+constexpr int kBarProd = 5;    // producer-internal
+
+constexpr int kWinLast = 1, kWinTerminate = 2;
+
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct WsColRec {  // 32 B
+  double rho2;     // (x_n - x_r)^2 + (y_n - y_r)^2
+  float bxy;       // signed beta product of the x and y walls (C2)
+  float cdot;      // (x_n - x_r) o_x + (y_n - y_r) o_y (polar pattern, C4)
+  int r1lo, r2lo;  // n_z ranges [r1lo, r1lo + r1n), [r2lo, ...)
+  int r1n, pad;
+};
+
+struct WsTile {
+  RirGeom g;
+  double dlo2, dhi2, invLz, offE, offO;
+  long long row;
+  int m, t0, te, tc, nx0, ny0, NX, ncols, zl, zh;
+  float xrel_max;
+  int use_bz;
+};
+
+struct WinInfo {
+  long long row;
+  int t0, te, nbins, flags;
+};
+
+template <int MODE>
+struct WsSmem {
+  WsTile ti;
+  int next_work;
+  WsColRec col[kWsColBatch];
+  int colpre[kWsColBatch];
+  float2 rec[WsCap<MODE>::v];
+  float recA[MODE == 1 ? WsCap<MODE>::v : 1];
+  uint8_t bin[WsCap<MODE>::v];
+  int warpcnt[kPW][kMaxBins];
+  int pbinstart[kMaxBins + 1];
+  int scan_tmp[kPW];
+  float bz[kBzMax];
+  float4 sorted[2][MODE == 1 ? WsCap<MODE>::v + 8 : WsCap<MODE>::v / 2 + 8];
+  int binstart[2][kMaxBins + 1];
+  WinInfo win[2];
+};
+
+// z-axis factor of beta_n (C2): signed beta_z0^|floor(n/2)| beta_z1^|ceil(n/2)|
+__device__ __forceinline__ float z_factor(int nz, const RirGeom& g) {
+  uint32_t sgn = 0;
+  bool zero = false;
+  float lz = axis_beta(nz, 2, g, sgn, zero);
+  float v = zero ? 0.f : ex2_approx(lz);
+  return sgn ? -v : v;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long long n_work, int* work_counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WsSmem<MODE>& sm = *reinterpret_cast<WsSmem<MODE>*>(smem_raw);
+  float2* lut = reinterpret_cast<float2*>(smem_raw + sizeof(WsSmem<MODE>));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float H = A.H;
+
+  if (MODE == 1) {  // LUT table -> shared memory (once per persistent CTA)
+    int n = A.lut_rows * A.lut_cols;
+    for (int i = tid; i < n; i += kWsThreads) lut[i] = A.lut[i];
+  }
+  __syncthreads();
+
+  if (warp < kPW) {
+    // =========================== producers ===========================
+    const int ptid = tid;
+    const unsigned lt = (1u << lane) - 1u;
+    const double fs_over_c = A.fs_over_c;
+    const double sc2 = fs_over_c * fs_over_c;
+    const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f;
+    int win_i = 0, filled = 0;
+
+    // stable counting sort of rec[0, filled) by bin, then publish to buffer win_i & 1
+    auto publish = [&](int flags, int nbins) {
+      for (int i = ptid; i < kPW * kMaxBins; i += kPT) (&sm.warpcnt[0][0])[i] = 0;
+      bar_sync(kBarProd, kPT);
+      const int per_warp = (filled + kPW - 1) / kPW;
+      const int wbeg = warp * per_warp, wend = min(filled, wbeg + per_warp);
+      for (int r0 = wbeg; r0 < wend; r0 += 32) {
+        int r = r0 + lane;
+        int b = r < wend ? (int)sm.bin[r] : (int)kDiscard;
+        unsigned peers = __match_any_sync(0xffffffffu, b);
+        if (b != kDiscard && (peers & lt) == 0) sm.warpcnt[warp][b] += __popc(peers);
+        __syncwarp();
+      }
+      bar_sync(kBarProd, kPT);
+      if (ptid < nbins) {
+        int s = 0;
+        for (int w = 0; w < kPW; w++) { int c = sm.warpcnt[w][ptid]; sm.warpcnt[w][ptid] = s; s += c; }
+        sm.pbinstart[ptid] = s;
+      }
+      bar_sync(kBarProd, kPT);
+      if (warp == 0) {
+        int carry = 0;
+        for (int b0 = 0; b0 < nbins; b0 += 32) {
+          int b = b0 + lane;
+          int v = b < nbins ? sm.pbinstart[b] : 0;
+          int x = warp_incl_scan(v, lane);
+          if (b < nbins) sm.pbinstart[b] = carry + x - v;
+          carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) sm.pbinstart[nbins] = carry;
+      }
+      const int buf = win_i & 1;
+      if (win_i >= 2) bar_sync(kBarEmpty0 + buf, kWsThreads);  // consumers released this buffer
+      else bar_sync(kBarProd, kPT);
+      float4* sorted = sm.sorted[buf];
+      for (int r0 = wbeg; r0 < wend; r0 += 32) {
+        int r = r0 + lane;
+        int b = r < wend ? (int)sm.bin[r] : (int)kDiscard;
+        unsigned peers = __match_any_sync(0xffffffffu, b);
+        if (b != kDiscard) {
+          int pos = sm.pbinstart[b] + sm.warpcnt[warp][b] + __popc(peers & lt);
+          float2 rc = sm.rec[r];
+          if (MODE == 1) {
+            sorted[pos] = make_float4(rc.x, rc.y, sm.recA[r], 0.f);
+          } else {  // pair layout: sorted[p>>1] = (nxv_even, nxv_odd, C_even, C_odd)
+            float* pp = reinterpret_cast<float*>(&sorted[pos >> 1]);
+            pp[pos & 1] = rc.x;
+            pp[2 + (pos & 1)] = rc.y;
+          }
+        }
+        __syncwarp();
+        if (b != kDiscard && (peers & lt) == 0) sm.warpcnt[warp][b] += __popc(peers);
+        __syncwarp();
+      }
+      const int ntot = sm.pbinstart[nbins];
+      if (ptid < 8) {  // dummy records after the last one (outside every window)
+        int pos = ntot + ptid;
+        if (MODE == 1) {
+          sorted[pos] = make_float4(__int_as_float(0), 0.f, 0.f, 0.f);
+        } else {
+          float* pp = reinterpret_cast<float*>(&sorted[pos >> 1]);
+          pp[pos & 1] = -1.0e4f;
+          pp[2 + (pos & 1)] = 0.f;
+        }
+      }
+      for (int i = ptid; i <= nbins; i += kPT) sm.binstart[buf][i] = sm.pbinstart[i];
+      if (ptid == 0) {
+        WinInfo w;
+        w.row = sm.ti.row; w.t0 = sm.ti.t0; w.te = sm.ti.te; w.nbins = nbins; w.flags = flags;
+        sm.win[buf] = w;
+      }
+      bar_arrive(kBarFull0 + buf, kWsThreads);  // hand the buffer to the consumers
+      bar_sync(kBarProd, kPT);                  // rec / warpcnt / pbinstart reusable
+      win_i++;
+      filled = 0;
+    };
+
+    for (;;) {
+      if (ptid == 0) sm.next_work = atomicAdd(work_counter, 1);
+      bar_sync(kBarProd, kPT);
+      const long long wi = sm.next_work;
+      if (wi >= n_work) break;
+      if (ptid == 0) {
+        WsTile& T = sm.ti;
+        int m, tile, nISM;
+        long long row;
+        if (A.jobs) {
+          int2 jt = A.tiles[wi];
+          m = jt.x; tile = jt.y;
+          nISM = A.jobs[m].nISM;
+          row = A.jobs[m].out_offset;
+        } else {
+          tile = A.nTiles - 1 - (int)(wi / A.M);  // heaviest (latest) tiles first
+          m = (int)(wi % A.M);
+          nISM = A.nISM;
+          row = (long long)m * A.row_stride;
+        }
+        load_geom(A, m, T.g, A.status);
+        T.m = m; T.row = row;
+        T.t0 = tile * kWsTC;
+        T.te = min(T.t0 + kWsTC, nISM);
+        T.tc = T.t0 + kWsTC / 2;
+        T.invLz = 1.0 / T.g.L[2];
+        T.offE = T.g.s[2] - T.g.r[2];
+        T.offO = -T.g.s[2] - T.g.r[2];
+        double xlo = (double)T.t0 - H, xhi = (double)(T.te - 1) + H;
+        double dlo = xlo > 0.0 ? xlo * A.c_over_fs : 0.0;
+        double dhi = xhi * A.c_over_fs;
+        T.dlo2 = dlo * dlo;
+        T.dhi2 = dhi * dhi;
+        T.xrel_max = (float)(T.te - 1 - T.t0) + 2.f * H;
+        int lo[2], hi[2];
+        for (int ax = 0; ax < 2; ax++) {
+          double L = T.g.L[ax], r = T.g.r[ax];
+          int a = (int)floor((r - dhi) / L) - 1, b = (int)floor((r + dhi) / L) + 1;
+          lo[ax] = max(a, T.g.nlo[ax]);
+          hi[ax] = min(b, T.g.nhi[ax] - 1);
+        }
+        T.nx0 = lo[0]; T.ny0 = lo[1];
+        T.NX = max(0, hi[0] - lo[0] + 1);
+        T.ncols = T.NX * max(0, hi[1] - lo[1] + 1);
+        T.zl = T.g.nlo[2];
+        T.zh = T.g.nhi[2] - 1;
+        T.use_bz = (T.zh - T.zl + 1) <= kBzMax;
+      }
+      bar_sync(kBarProd, kPT);
+      const WsTile& T = sm.ti;
+      const RirGeom& g = T.g;
+      const int nbins = (int)ceilf(((float)kWsTC + 2.f * H) / (float)kS) + 1;
+      if (T.use_bz)
+        for (int i = ptid; i <= T.zh - T.zl; i += kPT) sm.bz[i] = z_factor(T.zl + i, g);
+      // (the first column batch below syncs before any bz read)
+
+      for (int qb = 0; qb < T.ncols; qb += kWsColBatch) {
+        int cnt = 0;
+        {
+          const int q = qb + ptid;
+          WsColRec cr;
+          cr.r1lo = 0; cr.r2lo = 0; cr.r1n = 0; cr.rho2 = 0.0; cr.bxy = 0.f; cr.cdot = 0.f; cr.pad = 0;
+          if (q < T.ncols) {
+            const int nx = T.nx0 + q % T.NX, ny = T.ny0 + q / T.NX;
+            const double dx = image_coord(nx, g.L[0], g.s[0]) - g.r[0];
+            const double dy = image_coord(ny, g.L[1], g.s[1]) - g.r[1];
+            const double rho2 = dx * dx + dy * dy;
+            cr.rho2 = rho2;
+            cr.cdot = (float)dx * g.o[0] + (float)dy * g.o[1];
+            uint32_t sgn = 0; bool zero = false;
+            float lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
+            float bxy = zero ? 0.f : ex2_approx(lxy);
+            cr.bxy = sgn ? -bxy : bxy;
+            if (rho2 < T.dhi2) {
+              double zhi = sqrt(T.dhi2 - rho2);
+              double zlo = T.dlo2 > rho2 ? sqrt(T.dlo2 - rho2) : 0.0;
+              int pa, pb, na, nbz;
+              z_range(g, T.invLz, zlo, zhi, pa, pb);
+              z_range(g, T.invLz, -zhi, -zlo, na, nbz);
+              if (nbz >= pa - 1) { pa = min(pa, na); na = 1; nbz = 0; }
+              pa = max(pa, T.zl); pb = min(pb, T.zh);
+              na = max(na, T.zl); nbz = min(nbz, T.zh);
+              int n1 = max(0, pb - pa + 1), n2 = max(0, nbz - na + 1);
+              cr.r1lo = pa; cr.r1n = n1; cr.r2lo = na;
+              cnt = n1 + n2;
+            }
+          }
+          sm.col[ptid] = cr;
+        }
+        // block scan over the producer threads
+        int x = warp_incl_scan(cnt, lane);
+        if (lane == 31) sm.scan_tmp[warp] = x;
+        bar_sync(kBarProd, kPT);
+        int add = 0;
+        for (int w = 0; w < warp; w++) add += sm.scan_tmp[w];
+        sm.colpre[ptid] = x + add;
+        bar_sync(kBarProd, kPT);
+        const int total = sm.colpre[kWsColBatch - 1];
+
+        for (int base = 0; base < total;) {
+          const int take = min(WsCap<MODE>::v - filled, total - base);
+          const int R = (take + kPT - 1) / kPT;
+          const int g0 = base + ptid * R, g1 = min(g0 + R, base + take);
+          if (g0 < g1) {
+            int lo = 0, hi = kWsColBatch - 1;  // first column with colpre > g0
+            while (lo < hi) {
+              int mid = (lo + hi) >> 1;
+              if (sm.colpre[mid] > g0) hi = mid; else lo = mid + 1;
+            }
+            int j = lo;
+            int before = j > 0 ? sm.colpre[j - 1] : 0;
+            for (int gi = g0; gi < g1; gi++) {
+              while (sm.colpre[j] <= gi) { before = sm.colpre[j]; j++; }
+              const WsColRec& cr = sm.col[j];
+              const int l = gi - before;
+              const int nz = l < cr.r1n ? cr.r1lo + l : cr.r2lo + (l - cr.r1n);
+              // Eq. 1 along z: even nz -> nz L + s, odd nz -> (nz + 1) L - s; Delta_z = z_n - z_r
+              const int odd = nz & 1;
+              const double dz = fma((double)(nz + odd), g.L[2], odd ? T.offO : T.offE);
+              const double x2 = fma(dz, dz, cr.rho2) * sc2;  // (d fs / c)^2
+              uint8_t b = kDiscard;
+              float2 rec = make_float2(0.f, 0.f);
+              float recA = 0.f;
+              if (x2 == 0.0) {
+                atomicOr(A.status, kStatusDegenerate);
+              } else {
+                float x0f;
+                float xr = delay_rel(x2, T.tc, x0f);
+                float xrel = xr + (float)(kWsTC / 2) + H;  // x - (t0 - H)
+                if (xrel > 0.f && xrel < T.xrel_max) {
+                  b = (uint8_t)(int)(xrel * (1.f / (float)kS));
+                  const float rx = rcp_approx(x0f);          // 1/d = fs / (c x)
+                  const float bz = T.use_bz ? sm.bz[nz - T.zl] : z_factor(nz, g);
+                  const float cth = fmaf((float)dz, g.o[2], cr.cdot) * ((float)fs_over_c * rx);
+                  const float gain = g.a + (1.f - g.a) * cth;
+                  const float amp = cr.bxy * bz * gain * rx * fs_over_c_4pi;  // Eq. 4
+                  if (MODE == 1) {
+                    float xq = xr * (float)A.lutQ;
+                    float fiq = floorf(xq);
+                    float phi = xq - fiq;
+                    int iq1 = (int)fiq + 1;
+                    int php = iq1 & (A.lutQ - 1);
+                    int aa = (iq1 - php) / A.lutQ;
+                    int ph = (A.lutQ - php) & (A.lutQ - 1);
+                    int jsh = aa + (php > 0 ? 1 : 0);
+                    rec = make_float2(__int_as_float(ph * A.lut_cols + A.lut_joff - jsh), phi);
+                    recA = amp;
+                  } else {
+                    float fj = floorf(xr);
+                    float f = xr - fj;
+                    if (f == 0.f) {  // reading R3
+                      xr = nextafterf(xr, 1e30f);
+                      fj = floorf(xr);
+                      f = xr - fj;
+                    }
+                    float cc = -amp * sinpi01(f) * 0.318309886183790672f;
+                    if ((int)fj & 1) cc = -cc;
+                    if (MODE == 0) rec = make_float2(-xr * A.invHs, cc * A.invHs);
+                    else rec = make_float2(-xr * (0.5f * A.invHs), cc * (0.5f * A.invHs) * 1024.f);
+                  }
+                }
+              }
+              const int dst = filled + (gi - base);
+              sm.rec[dst] = rec;
+              if (MODE == 1) sm.recA[dst] = recA;
+              sm.bin[dst] = b;
+            }
+          }
+          filled += take;
+          base += take;
+          if (filled == WsCap<MODE>::v) {
+            bar_sync(kBarProd, kPT);
+            publish(0, nbins);
+          }
+        }
+        bar_sync(kBarProd, kPT);  // column records are replaced by the next batch
+      }
+      bar_sync(kBarProd, kPT);
+      publish(kWinLast, nbins);  // the tile's last window (possibly empty)
+    }
+    publish(kWinTerminate, 1);
+    // match the consumers' releases of the last two buffers
+    for (int w = max(0, win_i - 2); w < win_i; w++) bar_sync(kBarEmpty0 + (w & 1), kWsThreads);
+  } else {
+    // =========================== consumers ===========================
+    const int cw = warp - kPW;
+    const int grp = lane >> 3, li = lane & 7;
+    int kfs[2];
+    float2 acc[2];
+#pragma unroll
+    for (int s = 0; s < 2; s++) {
+      kfs[s] = (cw * 2 + s) * kS + li - kWsTC / 2;  // sample relative to the tile centre
+      acc[s] = make_float2(0.f, 0.f);
+    }
+    int win_i = 0;
+    for (;;) {
+      const int buf = win_i & 1;
+      bar_sync(kBarFull0 + buf, kWsThreads);
+      const WinInfo w = sm.win[buf];
+      if (w.flags & kWinTerminate) {
+        bar_arrive(kBarEmpty0 + buf, kWsThreads);
+        break;
+      }
+      const float4* sorted = sm.sorted[buf];
+#pragma unroll
+      for (int s = 0; s < 2; s++) {
+        const int sub = cw * 2 + s;
+        const int ra = sm.binstart[buf][sub], rb = sm.binstart[buf][min(sub + A.nbw, w.nbins)];
+        if (MODE == 0) {
+          const float kv = (float)kfs[s] * A.invHs;
+          const float2 kv2 = make_float2(kv, kv);
+          const float2 mr2 = make_float2(-A.rho2, -A.rho2);
+          const float2 b3 = make_float2(A.wb[3], A.wb[3]), b2 = make_float2(A.wb[2], A.wb[2]);
+          const float2 b1 = make_float2(A.wb[1], A.wb[1]), b0 = make_float2(A.wb[0], A.wb[0]);
+          float2 a2 = acc[s];
+          int j = (ra & ~1) + 2 * grp;
+          for (; j + 2 * kG < rb; j += 4 * kG) {
+            float4 p0 = sorted[j >> 1];
+            float4 p1 = sorted[(j + 2 * kG) >> 1];
+            float2 v0 = __fadd2_rn(kv2, make_float2(p0.x, p0.y));
+            float2 v1 = __fadd2_rn(kv2, make_float2(p1.x, p1.y));
+            float2 s0 = __ffma2_rn(v0, v0, mr2);
+            float2 s1 = __ffma2_rn(v1, v1, mr2);
+            s0.x = fminf(s0.x, 0.f); s0.y = fminf(s0.y, 0.f);
+            s1.x = fminf(s1.x, 0.f); s1.y = fminf(s1.y, 0.f);
+            float2 q0 = __ffma2_rn(b3, s0, b2), q1 = __ffma2_rn(b3, s1, b2);
+            q0 = __ffma2_rn(q0, s0, b1); q1 = __ffma2_rn(q1, s1, b1);
+            q0 = __ffma2_rn(q0, s0, b0); q1 = __ffma2_rn(q1, s1, b0);
+            float2 c0 = __fmul2_rn(q0, s0), c1 = __fmul2_rn(q1, s1);
+            float2 w0 = __fmul2_rn(c0, c0), w1 = __fmul2_rn(c1, c1);
+            float2 r0 = make_float2(rcp_approx(v0.x), rcp_approx(v0.y));
+            float2 r1 = make_float2(rcp_approx(v1.x), rcp_approx(v1.y));
+            a2 = __ffma2_rn(make_float2(p0.z, p0.w), __fmul2_rn(w0, r0), a2);
+            a2 = __ffma2_rn(make_float2(p1.z, p1.w), __fmul2_rn(w1, r1), a2);
+          }
+          if (j < rb) {
+            float4 p0 = sorted[j >> 1];
+            float2 v0 = __fadd2_rn(kv2, make_float2(p0.x, p0.y));
+            float2 s0 = __ffma2_rn(v0, v0, mr2);
+            s0.x = fminf(s0.x, 0.f); s0.y = fminf(s0.y, 0.f);
+            float2 q0 = __ffma2_rn(b3, s0, b2);
+            q0 = __ffma2_rn(q0, s0, b1);
+            q0 = __ffma2_rn(q0, s0, b0);
+            float2 c0 = __fmul2_rn(q0, s0);
+            float2 w0 = __fmul2_rn(c0, c0);
+            float2 r0 = make_float2(rcp_approx(v0.x), rcp_approx(v0.y));
+            a2 = __ffma2_rn(make_float2(p0.z, p0.w), __fmul2_rn(w0, r0), a2);
+          }
+          acc[s] = a2;
+        } else if (MODE == 2) {
+          const float kx = (float)kfs[s] * (0.5f * A.invHs);
+          const float2 kx2 = make_float2(kx, kx);
+          const __half2 c6 = __float2half2_rn(A.hc[2]), c4 = __float2half2_rn(A.hc[1]);
+          const __half2 c2 = __float2half2_rn(A.hc[0]), c0 = __float2half2_rn(1.f);
+          const __half2 xcl = __float2half2_rn(A.x2clamp);
+          __half2 acch = __float2half2_rn(0.f);
+          float2 a2 = acc[s];
+          int steps = 0;
+          for (int j = (ra & ~1) + 2 * grp; j < rb; j += 2 * kG) {
+            float4 pr = sorted[j >> 1];
+            float2 x = __fadd2_rn(kx2, make_float2(pr.x, pr.y));
+            __half2 hx = __float22half2_rn(x);
+            __half2 x2 = __hmin2(__hmul2(hx, hx), xcl);
+            __half2 p = __hfma2(c6, x2, c4);
+            p = __hfma2(p, x2, c2);
+            p = __hfma2(p, x2, c0);
+            __half2 wv = __hmul2(p, p);
+            float2 r = make_float2(rcp_approx(x.x), rcp_approx(x.y));
+            float2 q = __fmul2_rn(make_float2(pr.z, pr.w), r);
+            acch = __hfma2(wv, __float22half2_rn(q), acch);
+            if (++steps == 8) {
+              float2 f = __half22float2(acch);
+              a2.x += f.x; a2.y += f.y;
+              acch = __float2half2_rn(0.f);
+              steps = 0;
+            }
+          }
+          float2 f = __half22float2(acch);
+          a2.x += f.x; a2.y += f.y;
+          acc[s] = a2;
+        } else {
+          float a = acc[s].x;
+          for (int j = ra + grp; j < rb; j += kG) {
+            float4 rc = sorted[j];
+            int idx = __float_as_int(rc.x) + kfs[s];
+            float2 d = lut[idx];
+            a = fmaf(rc.z, fmaf(rc.y, d.y, d.x), a);
+          }
+          acc[s].x = a;
+        }
+      }
+      bar_arrive(kBarEmpty0 + buf, kWsThreads);  // buffer consumed
+      if (w.flags & kWinLast) {
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+          float a = acc[s].x + acc[s].y;
+          a += __shfl_xor_sync(0xffffffffu, a, 8);
+          a += __shfl_xor_sync(0xffffffffu, a, 16);
+          if (MODE == 0) { if (kfs[s] & 1) a = -a; }
+          else if (MODE == 2) { a *= (1.f / 1024.f); if (kfs[s] & 1) a = -a; }
+          const int k = w.t0 + (cw * 2 + s) * kS + li;
+          if (grp == 0 && k < w.te) A.out[w.row + k] = a;
+          acc[s] = make_float2(0.f, 0.f);
+        }
+      }
+      win_i++;
+    }
+  }
+}
+
+size_t ism_ws_smem_bytes(int mode, int lut_rows, int lut_cols) {
+  switch (mode) {
+    case 0: return sizeof(WsSmem<0>);
+    case 1: return sizeof(WsSmem<1>) + (size_t)lut_rows * lut_cols * sizeof(float2);
+    default: return sizeof(WsSmem<2>);
+  }
+}
+
+template <int MODE>
+static cudaError_t launch_ws_mode(const IsmArgs& A, long long n_work, int* counter, int grid, size_t smem,
+                                  cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(ism_ws_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  ism_ws_kernel<MODE><<<grid, kWsThreads, smem, stream>>>(A, n_work, counter);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* counter, int num_sms,
+                          cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  int grid = (int)(n_work < num_sms ? n_work : num_sms);
+  size_t smem = ism_ws_smem_bytes(mode, A.lut_rows, A.lut_cols);
+  switch (mode) {
+    case 0: return launch_ws_mode<0>(A, n_work, counter, grid, smem, stream);
+    case 1: return launch_ws_mode<1>(A, n_work, counter, grid, smem, stream);
+    default: return launch_ws_mode<2>(A, n_work, counter, grid, smem, stream);
+  }
+}
+
+}  // namespace gpurir

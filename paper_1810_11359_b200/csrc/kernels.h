@@ -81,6 +81,9 @@ struct TailArgs {
 size_t ism_smem_bytes(int mode, int lut_rows, int lut_cols);
 cudaError_t launch_ism(const IsmArgs& A, int mode, int split, long long nclusters, cudaStream_t stream);
 cudaError_t launch_image_params(const IsmArgs& A, double* x_out, float* A_out, long long N, cudaStream_t stream);
+size_t ism_ws_smem_bytes(int mode, int lut_rows, int lut_cols);
+cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* counter, int num_sms,
+                          cudaStream_t stream);
 cudaError_t launch_tail(const TailArgs& A, long long nblocks, cudaStream_t stream);
 
 constexpr int kTailThreads = 256;

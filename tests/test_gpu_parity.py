@@ -75,16 +75,18 @@ def test_goldens(P, oracle, case, mode):
         assert abs(h[g["argmax"]] - g["h_argmax"]) <= 1e-4 * abs(g["h_argmax"])
 
 
+@pytest.mark.parametrize("kernel", ["auto", "persistent"])
 @pytest.mark.parametrize("mode", ["fp32", "lut", "fp16"])
-def test_random_scenes(P, oracle, mode):
-    """S:525 style: random rooms 2-8 m, T60 0.3-1.0, <=2 src x 3 rcv, all patterns, 16 and 48 kHz."""
+def test_random_scenes(P, oracle, mode, kernel):
+    """S:525 style: random rooms 2-8 m, T60 0.3-1.0, <=2 src x 3 rcv, all patterns, 16 and 48 kHz.
+    kernel = persistent forces the warp-specialised kernel (split = -1) on these small calls."""
     rng = np.random.default_rng(525)
     worst = 0.0
     for i in range(30):
         fs = 16000.0 if i % 3 else 48000.0
         sc = W.random_small_scene(rng, fs=fs)
         beta, nb = derive(oracle, sc)
-        g = run_gpu(P, sc, beta, nb, mode=mode)
+        g = run_gpu(P, sc, beta, nb, mode=mode, split=-1 if kernel == "persistent" else 0)
         r = run_oracle(oracle, sc, beta, nb)
         e = rel_err(g, r).max()
         worst = max(worst, e)
@@ -123,12 +125,13 @@ def test_cfg2_t60_sweep(P, oracle, T60):
     assert rel_err(g, r)[0] <= TOL["fp32"], T60
 
 
+@pytest.mark.parametrize("kernel", ["auto", "persistent"])
 @pytest.mark.parametrize("mode", ["fp32", "lut", "fp16"])
-def test_cfg3_subset(P, oracle, mode):
+def test_cfg3_subset(P, oracle, mode, kernel):
     """#RIR sweep room, cardioid with random orientations, diffuse variant; first 24 receivers."""
     sc = W.cfg3(24, "diffuse")
     beta, nb = derive(oracle, sc)
-    g = run_gpu(P, sc, beta, nb, mode=mode)
+    g = run_gpu(P, sc, beta, nb, mode=mode, split=-1 if kernel == "persistent" else 0)
     r = run_oracle(oracle, sc, beta, nb)
     assert rel_err(g, r).max() <= TOL[mode]
 
@@ -146,12 +149,13 @@ def test_cfg3_full_size_sampled(P, oracle):
         assert rel_err(g[0, m], rj[0, 0])[0] <= TOL["fp32"], m
 
 
+@pytest.mark.parametrize("kernel", ["auto", "persistent"])
 @pytest.mark.parametrize("mode", ["fp32", "lut", "fp16"])
-def test_cfg4_48k_array(P, oracle, mode):
+def test_cfg4_48k_array(P, oracle, mode, kernel):
     sc = W.cfg4("a")
     sc.pos_rcv = sc.pos_rcv[:8]
     beta, nb = derive(oracle, sc)
-    g = run_gpu(P, sc, beta, nb, mode=mode)
+    g = run_gpu(P, sc, beta, nb, mode=mode, split=-1 if kernel == "persistent" else 0)
     r = run_oracle(oracle, sc, beta, nb)
     assert rel_err(g, r).max() <= TOL[mode]
 
@@ -217,24 +221,36 @@ def test_degenerate_and_invalid(P):
 
 # ---------------------------------------------------------------- determinism, sharding, batch
 
-def test_run_to_run_deterministic(P, oracle):
+@pytest.mark.parametrize("split", [0, -1])
+def test_run_to_run_deterministic(P, oracle, split):
     sc = W.cfg3(32, "diffuse")
     beta, nb = derive(oracle, sc)
-    a = run_gpu(P, sc, beta, nb)
-    b = run_gpu(P, sc, beta, nb)
+    a = run_gpu(P, sc, beta, nb, split=split)
+    b = run_gpu(P, sc, beta, nb, split=split)
     assert np.array_equal(a, b)
 
 
-def test_shard_invariance(P, oracle):
-    """§8(e): running the receivers in 4 shards with rir_index_base offsets reproduces the unsharded
-    call bit for bit (fixed split so the per-tile summation order is identical)."""
+def test_persistent_matches_cluster_kernel(P, oracle):
+    """The two ISM kernels evaluate the same records in the same bin order per tile (the persistent one
+    windows them differently), so they agree to fp32 rounding."""
     sc = W.cfg3(64, "diffuse")
     beta, nb = derive(oracle, sc)
-    full = run_gpu(P, sc, beta, nb, split=2)
+    a = run_gpu(P, sc, beta, nb, split=1)
+    b = run_gpu(P, sc, beta, nb, split=-1)
+    assert rel_err(b, a).max() <= 2e-6
+
+
+@pytest.mark.parametrize("split", [2, -1])
+def test_shard_invariance(P, oracle, split):
+    """§8(e): running the receivers in 4 shards with rir_index_base offsets reproduces the unsharded
+    call bit for bit (fixed kernel choice so the per-tile summation order is identical)."""
+    sc = W.cfg3(64, "diffuse")
+    beta, nb = derive(oracle, sc)
+    full = run_gpu(P, sc, beta, nb, split=split)
     parts = []
     for s in range(4):
         sl = slice(16 * s, 16 * (s + 1))
-        parts.append(run_gpu(P, sc, beta, nb, split=2, rir_index_base=16 * s, pos_rcv=sc.pos_rcv[sl],
+        parts.append(run_gpu(P, sc, beta, nb, split=split, rir_index_base=16 * s, pos_rcv=sc.pos_rcv[sl],
                              orv=sc.orV_rcv[sl]))
     assert np.array_equal(full, np.concatenate(parts, axis=1))
 
