@@ -3,7 +3,7 @@
 //
 // One CTA per SM loops over (RIR, 256-sample tile) work items taken heaviest-first
 // from a global counter.  Inside the CTA:
-//   producer warps (8): enumerate the shell images of a tile column by column
+//   producer warps (16): enumerate the shell images of a tile column by column
 //     (exact n_z ranges), compute each image's parameters in registers
 //     (Eqs. 1-4; fp64 delay), append compact records to a
 //     private window, stable-sort the window by delay bin and publish it into
@@ -21,10 +21,10 @@
 
 namespace gpurir {
 
-constexpr int kPW = 8;                       // producer warps
+constexpr int kPW = 16;                      // producer warps
 constexpr int kCW = 16;                      // consumer warps
 constexpr int kPT = kPW * 32;                // producer threads
-constexpr int kWsThreads = (kPW + kCW) * 32; // 768
+constexpr int kWsThreads = (kPW + kCW) * 32; // 1024
 constexpr int kWsTC = kCW * 2 * kS;          // 256 samples per tile
 template <int MODE> struct WsCap { static constexpr int v = MODE == 1 ? 2048 : 4096; };  // records per window
 constexpr int kWsColBatch = kPT;             // columns per enumeration batch
@@ -75,6 +75,7 @@ struct WsSmem {
   float2 rec[WsCap<MODE>::v];
   float recA[MODE == 1 ? WsCap<MODE>::v : 1];
   uint8_t bin[WsCap<MODE>::v];
+  uint16_t rank[WsCap<MODE>::v];  // rank of a record among its warp segment's records of the same bin
   int warpcnt[kPW][kMaxBins];
   int pbinstart[kMaxBins + 1];
   int scan_tmp[kPW];
@@ -122,10 +123,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
       bar_sync(kBarProd, kPT);
       const int per_warp = (filled + kPW - 1) / kPW;
       const int wbeg = warp * per_warp, wend = min(filled, wbeg + per_warp);
-      for (int r0 = wbeg; r0 < wend; r0 += 32) {
+      for (int r0 = wbeg; r0 < wend; r0 += 32) {  // pass 1: per-warp bin counts and stable ranks
         int r = r0 + lane;
         int b = r < wend ? (int)sm.bin[r] : (int)kDiscard;
         unsigned peers = __match_any_sync(0xffffffffu, b);
+        if (b != kDiscard) {
+          const int before = sm.warpcnt[warp][b];
+          sm.rank[r] = (uint16_t)(before + __popc(peers & lt));
+        }
+        __syncwarp();
         if (b != kDiscard && (peers & lt) == 0) sm.warpcnt[warp][b] += __popc(peers);
         __syncwarp();
       }
@@ -151,13 +157,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
       if (win_i >= 2) bar_sync(kBarEmpty0 + buf, kWsThreads);  // consumers released this buffer
       else bar_sync(kBarProd, kPT);
       float4* sorted = sm.sorted[buf];
-      for (int r0 = wbeg; r0 < wend; r0 += 32) {
-        int r = r0 + lane;
-        int b = r < wend ? (int)sm.bin[r] : (int)kDiscard;
-        unsigned peers = __match_any_sync(0xffffffffu, b);
+      for (int r = wbeg + lane; r < wend; r += 32) {  // pass 2: scatter (no warp collectives)
+        const int b = (int)sm.bin[r];
         if (b != kDiscard) {
-          int pos = sm.pbinstart[b] + sm.warpcnt[warp][b] + __popc(peers & lt);
-          float2 rc = sm.rec[r];
+          const int pos = sm.pbinstart[b] + sm.warpcnt[warp][b] + (int)sm.rank[r];
+          const float2 rc = sm.rec[r];
           if (MODE == 1) {
             sorted[pos] = make_float4(rc.x, rc.y, sm.recA[r], 0.f);
           } else {  // pair layout: sorted[p>>1] = (nxv_even, nxv_odd, C_even, C_odd)
@@ -166,9 +170,6 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
             pp[2 + (pos & 1)] = rc.y;
           }
         }
-        __syncwarp();
-        if (b != kDiscard && (peers & lt) == 0) sm.warpcnt[warp][b] += __popc(peers);
-        __syncwarp();
       }
       const int ntot = sm.pbinstart[nbins];
       if (ptid < 8) {  // dummy records after the last one (outside every window)
