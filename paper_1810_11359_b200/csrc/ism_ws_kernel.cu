@@ -31,9 +31,10 @@ constexpr int kWsColBatch = kPT;             // columns per enumeration batch
 constexpr int kBzMax = 1024;                 // z-factor table entries
 static_assert(kWsTC == kTC, "tile size shared with the host planner");
 
+constexpr int kNBuf = 3;       // published window buffers (producers may run kNBuf - 1 windows ahead)
 constexpr int kBarFull0 = 1;   // + buffer: producers arrive, consumers sync
-constexpr int kBarEmpty0 = 3;  // + buffer: consumers arrive, producers sync
-constexpr int kBarProd = 5;    // producer-internal
+constexpr int kBarEmpty0 = kBarFull0 + kNBuf;   // + buffer: consumers arrive, producers sync
+constexpr int kBarProd = kBarEmpty0 + kNBuf;    // producer-internal
 
 constexpr int kWinLast = 1, kWinTerminate = 2;
 
@@ -80,9 +81,9 @@ struct WsSmem {
   int pbinstart[kMaxBins + 1];
   int scan_tmp[kPW];
   float bz[kBzMax];
-  float4 sorted[2][MODE == 1 ? WsCap<MODE>::v + 8 : WsCap<MODE>::v / 2 + 8];
-  int binstart[2][kMaxBins + 1];
-  WinInfo win[2];
+  float4 sorted[kNBuf][MODE == 1 ? WsCap<MODE>::v + 8 : WsCap<MODE>::v / 2 + 8];
+  int binstart[kNBuf][kMaxBins + 1];
+  WinInfo win[kNBuf];
 };
 
 // z-axis factor of beta_n (C2): signed beta_z0^|floor(n/2)| beta_z1^|ceil(n/2)|
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
     const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f;
     int win_i = 0, filled = 0;
 
-    // stable counting sort of rec[0, filled) by bin, then publish to buffer win_i & 1
+    // stable counting sort of rec[0, filled) by bin, then publish to buffer win_i % kNBuf
     auto publish = [&](int flags, int nbins) {
       for (int i = ptid; i < kPW * kMaxBins; i += kPT) (&sm.warpcnt[0][0])[i] = 0;
       bar_sync(kBarProd, kPT);
@@ -153,8 +154,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
         }
         if (lane == 0) sm.pbinstart[nbins] = carry;
       }
-      const int buf = win_i & 1;
-      if (win_i >= 2) bar_sync(kBarEmpty0 + buf, kWsThreads);  // consumers released this buffer
+      const int buf = win_i % kNBuf;
+      if (win_i >= kNBuf) bar_sync(kBarEmpty0 + buf, kWsThreads);  // consumers released this buffer
       else bar_sync(kBarProd, kPT);
       float4* sorted = sm.sorted[buf];
       for (int r = wbeg + lane; r < wend; r += 32) {  // pass 2: scatter (no warp collectives)
@@ -375,8 +376,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
       publish(kWinLast, nbins);  // the tile's last window (possibly empty)
     }
     publish(kWinTerminate, 1);
-    // match the consumers' releases of the last two buffers
-    for (int w = max(0, win_i - 2); w < win_i; w++) bar_sync(kBarEmpty0 + (w & 1), kWsThreads);
+    // match the consumers' releases of the last kNBuf buffers
+    for (int w = max(0, win_i - kNBuf); w < win_i; w++) bar_sync(kBarEmpty0 + (w % kNBuf), kWsThreads);
   } else {
     // =========================== consumers ===========================
     const int cw = warp - kPW;
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
     }
     int win_i = 0;
     for (;;) {
-      const int buf = win_i & 1;
+      const int buf = win_i % kNBuf;
       bar_sync(kBarFull0 + buf, kWsThreads);
       const WinInfo w = sm.win[buf];
       if (w.flags & kWinTerminate) {
