@@ -114,6 +114,16 @@ double sabine(const float L[3], const float b[6]) {
   return 0.161 * V / den;
 }
 
+// log2 |beta_w| and sign / zero masks of the six walls, shared by every image of a room.
+void beta_logs(const float b[6], float lb[6], unsigned* neg, unsigned* zero) {
+  *neg = 0; *zero = 0;
+  for (int w = 0; w < 6; w++) {
+    if (b[w] < 0.f) *neg |= 1u << w;
+    if (b[w] == 0.f) { *zero |= 1u << w; lb[w] = 0.f; }
+    else lb[w] = (float)log2(fabs((double)b[w]));
+  }
+}
+
 int validate_room(const float L[3], const float b[6], const int nb[3], int pattern) {
   for (int i = 0; i < 3; i++) {
     if (!(L[i] > 0.f) || !isfinite(L[i])) return GPURIR_EINVAL;
@@ -267,6 +277,7 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
     memset(&A, 0, sizeof(A));
     for (int i = 0; i < 3; i++) { A.L[i] = room_sz[i]; A.nb[i] = nb_img[i]; }
     for (int i = 0; i < 6; i++) A.beta[i] = beta[i];
+    beta_logs(beta, A.lb, &A.neg, &A.zero);
     A.pattern = mic_pattern;
     A.pos_src = pos_src; A.pos_rcv = pos_rcv; A.orv = mic_pattern == GPURIR_OMNI ? nullptr : orV_rcv;
     A.M_src = M_src; A.M_rcv = M_rcv; A.M = (int)M;
@@ -343,6 +354,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
       J.nb[a] = R.nb_img[a];
     }
     for (int w = 0; w < 6; w++) J.beta[w] = R.beta[w];
+    beta_logs(R.beta, J.lb, &J.neg, &J.zero);
     J.pattern = R.mic_pattern;
     long long nS = gpurir_nsamples(R.Tmax, fs), nISM = gpurir_nsamples(R.Tdiff, fs);
     if (nISM > nS) nISM = nS;
@@ -440,6 +452,7 @@ int gpurir_image_params(const float room_sz[3], const float beta[6], const float
     J.L[a] = room_sz[a]; J.src[a] = src[a]; J.rcv[a] = rcv[a]; J.orv[a] = orv ? orv[a] : 0.f; J.nb[a] = nb_img[a];
   }
   for (int w = 0; w < 6; w++) J.beta[w] = beta[w];
+  beta_logs(beta, J.lb, &J.neg, &J.zero);
   J.pattern = mic_pattern;
   if (mic_pattern != GPURIR_OMNI && !orv) return GPURIR_EINVAL;
   BatchJob* dj = nullptr;

@@ -42,40 +42,33 @@ __device__ __forceinline__ float sinpi01(float f) {
 // ----------------------------------------------------------------------------
 // Per-RIR geometry (single-room call or batch job)
 // ----------------------------------------------------------------------------
-static __device__ void load_geom(const IsmArgs& A, int m, RirGeom& g, int* status) {
-  float L[3], beta[6], src[3], rcv[3], orv[3] = {0.f, 0.f, 0.f};
-  int nb[3], pattern;
-  if (A.jobs) {
-    const BatchJob& J = A.jobs[m];
-    for (int i = 0; i < 3; i++) { L[i] = J.L[i]; src[i] = J.src[i]; rcv[i] = J.rcv[i]; orv[i] = J.orv[i]; nb[i] = J.nb[i]; }
-    for (int i = 0; i < 6; i++) beta[i] = J.beta[i];
-    pattern = J.pattern;
-  } else {
-    int ms = m / A.M_rcv, mr = m % A.M_rcv;
-    for (int i = 0; i < 3; i++) {
-      L[i] = A.L[i]; nb[i] = A.nb[i];
-      src[i] = A.pos_src[3 * ms + i];
-      rcv[i] = A.pos_rcv[3 * mr + i];
-      if (A.orv) orv[i] = A.orv[3 * mr + i];
-    }
-    for (int i = 0; i < 6; i++) beta[i] = A.beta[i];
-    pattern = A.pattern;
-  }
+static __device__ void geom_from(const float* L, const float* src, const float* rcv, const float* orv, const int* nb,
+                                 int pattern, const float* lb, unsigned neg, unsigned zero, RirGeom& g, int* status) {
   g.a = pattern == 0 ? 1.f : pattern == 1 ? 0.75f : pattern == 2 ? 0.5f : pattern == 3 ? 0.25f : 0.f;  // C4
-  float on = sqrtf(orv[0] * orv[0] + orv[1] * orv[1] + orv[2] * orv[2]);
-  if (pattern != 0 && !(on > 0.f)) { atomicOr(status, kStatusZeroOrient); on = 1.f; }
+  float o0 = orv[0], o1 = orv[1], o2 = orv[2];
+  float on2 = o0 * o0 + o1 * o1 + o2 * o2;
+  if (pattern != 0 && !(on2 > 0.f)) { atomicOr(status, kStatusZeroOrient); on2 = 1.f; }
+  const float inv = pattern != 0 ? rsqrtf(on2) : 0.f;
+  g.o[0] = o0 * inv; g.o[1] = o1 * inv; g.o[2] = o2 * inv;
   for (int i = 0; i < 3; i++) {
     g.L[i] = L[i]; g.s[i] = src[i]; g.r[i] = rcv[i];
-    g.o[i] = pattern != 0 ? orv[i] / on : 0.f;
     g.nlo[i] = -(nb[i] / 2);          // ceil(-N/2)
     g.nhi[i] = (nb[i] + 1) / 2;       // ceil(N/2)
   }
-  g.neg = 0; g.zero = 0;
-  for (int w = 0; w < 6; w++) {
-    float b = beta[w];
-    if (b < 0.f) g.neg |= 1u << w;
-    if (b == 0.f) { g.zero |= 1u << w; g.lb[w] = 0.f; }
-    else g.lb[w] = log2f(fabsf(b));
+  g.neg = neg; g.zero = zero;
+  for (int w = 0; w < 6; w++) g.lb[w] = lb[w];
+}
+
+// Per-RIR geometry (single-room call or batch job) read straight from global memory.
+static __device__ void load_geom(const IsmArgs& A, int m, RirGeom& g, int* status) {
+  if (A.jobs) {
+    const BatchJob& J = A.jobs[m];
+    geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.lb, J.neg, J.zero, g, status);
+  } else {
+    int ms = m / A.M_rcv, mr = m % A.M_rcv;
+    const float zero3[3] = {0.f, 0.f, 0.f};
+    geom_from(A.L, A.pos_src + 3 * ms, A.pos_rcv + 3 * mr, A.orv ? A.orv + 3 * mr : zero3, A.nb, A.pattern, A.lb,
+              A.neg, A.zero, g, status);
   }
 }
 

@@ -44,6 +44,42 @@ __device__ __forceinline__ void bar_sync(int id, int n) {
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+struct WsStage {        // next work item's inputs, prefetched with cp.async by warp 0
+  BatchJob job;          // batch call
+  float pos[12];         // single-room call: src[3], rcv[3], orv[3]
+  long long wi;          // work index
+  int2 jt;               // (job, tile) of a batch work item
+};
+
+// Warp 0 of the producers: issue the asynchronous loads of work item wi's per-RIR inputs into stage.
+__device__ __forceinline__ void ws_prefetch(const IsmArgs& A, long long wi, long long n_work, WsStage& st, int lane) {
+  if (lane == 0) st.wi = wi;
+  if (wi >= n_work) return;
+  if (A.jobs) {
+    int2 jt = A.tiles[wi];  // dependent: the job index selects the record to stage
+    if (lane == 0) st.jt = jt;
+    constexpr int n16 = (int)(sizeof(BatchJob) / 16);
+    if (lane < n16) cp_async16(reinterpret_cast<char*>(&st.job) + 16 * lane, reinterpret_cast<const char*>(A.jobs + jt.x) + 16 * lane);
+  } else {
+    const int m = (int)(wi % A.M);
+    const int ms = m / A.M_rcv, mr = m % A.M_rcv;
+    if (lane < 3) cp_async4(&st.pos[lane], A.pos_src + 3 * ms + lane);
+    else if (lane < 6) cp_async4(&st.pos[lane], A.pos_rcv + 3 * mr + (lane - 3));
+    else if (lane < 9 && A.orv) cp_async4(&st.pos[lane], A.orv + 3 * mr + (lane - 6));
+    else if (lane < 9) st.pos[lane] = 0.f;
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
 struct WsColRec {  // 32 B
   double rho2;     // (x_n - x_r)^2 + (y_n - y_r)^2
@@ -67,9 +103,11 @@ struct WinInfo {
   int t0, te, nbins, flags;
 };
 
+
 template <int MODE>
 struct WsSmem {
   WsTile ti;
+  WsStage stage;
   int next_work;
   WsColRec col[kWsColBatch];
   int colpre[kWsColBatch];
@@ -195,54 +233,71 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
       filled = 0;
     };
 
+    long long wi_pending = 0;  // warp 0, lane 0: the atomicAdd result for the item after the current one
+    if (warp == 0) {
+      long long wi0 = 0;
+      if (lane == 0) wi0 = atomicAdd(work_counter, 1);
+      wi0 = __shfl_sync(0xffffffffu, wi0, 0);
+      ws_prefetch(A, wi0, n_work, sm.stage, lane);
+    }
     for (;;) {
-      if (ptid == 0) sm.next_work = atomicAdd(work_counter, 1);
-      bar_sync(kBarProd, kPT);
-      const long long wi = sm.next_work;
-      if (wi >= n_work) break;
-      if (ptid == 0) {
-        WsTile& T = sm.ti;
-        int m, tile, nISM;
-        long long row;
-        if (A.jobs) {
-          int2 jt = A.tiles[wi];
-          m = jt.x; tile = jt.y;
-          nISM = A.jobs[m].nISM;
-          row = A.jobs[m].out_offset;
-        } else {
-          tile = A.nTiles - 1 - (int)(wi / A.M);  // heaviest (latest) tiles first
-          m = (int)(wi % A.M);
-          nISM = A.nISM;
-          row = (long long)m * A.row_stride;
+      if (warp == 0) {
+        cp_async_wait_all();
+        __syncwarp();
+        if (lane == 0) {
+          const long long wi = sm.stage.wi;
+          sm.next_work = (int)min(wi, n_work);
+          if (wi < n_work) {
+            wi_pending = atomicAdd(work_counter, 1);  // consumed at the end of this tile (latency hidden)
+            WsTile& T = sm.ti;
+            int m, tile, nISM;
+            long long row;
+            const float zero3[3] = {0.f, 0.f, 0.f};
+            if (A.jobs) {
+              const BatchJob& J = sm.stage.job;
+              m = sm.stage.jt.x; tile = sm.stage.jt.y;
+              nISM = J.nISM;
+              row = J.out_offset;
+              geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.lb, J.neg, J.zero, T.g, A.status);
+            } else {
+              tile = A.nTiles - 1 - (int)(wi / A.M);  // heaviest (latest) tiles first
+              m = (int)(wi % A.M);
+              nISM = A.nISM;
+              row = (long long)m * A.row_stride;
+              geom_from(A.L, sm.stage.pos, sm.stage.pos + 3, A.orv ? sm.stage.pos + 6 : zero3, A.nb, A.pattern, A.lb,
+                        A.neg, A.zero, T.g, A.status);
+            }
+            T.m = m; T.row = row;
+            T.t0 = tile * kWsTC;
+            T.te = min(T.t0 + kWsTC, nISM);
+            T.tc = T.t0 + kWsTC / 2;
+            T.invLz = 1.0 / T.g.L[2];
+            T.offE = T.g.s[2] - T.g.r[2];
+            T.offO = -T.g.s[2] - T.g.r[2];
+            double xlo = (double)T.t0 - H, xhi = (double)(T.te - 1) + H;
+            double dlo = xlo > 0.0 ? xlo * A.c_over_fs : 0.0;
+            double dhi = xhi * A.c_over_fs;
+            T.dlo2 = dlo * dlo;
+            T.dhi2 = dhi * dhi;
+            T.xrel_max = (float)(T.te - 1 - T.t0) + 2.f * H;
+            int lo[2], hi[2];
+            for (int ax = 0; ax < 2; ax++) {
+              double L = T.g.L[ax], r = T.g.r[ax];
+              int a = (int)floor((r - dhi) / L) - 1, b = (int)floor((r + dhi) / L) + 1;
+              lo[ax] = max(a, T.g.nlo[ax]);
+              hi[ax] = min(b, T.g.nhi[ax] - 1);
+            }
+            T.nx0 = lo[0]; T.ny0 = lo[1];
+            T.NX = max(0, hi[0] - lo[0] + 1);
+            T.ncols = T.NX * max(0, hi[1] - lo[1] + 1);
+            T.zl = T.g.nlo[2];
+            T.zh = T.g.nhi[2] - 1;
+            T.use_bz = (T.zh - T.zl + 1) <= kBzMax;
+          }
         }
-        load_geom(A, m, T.g, A.status);
-        T.m = m; T.row = row;
-        T.t0 = tile * kWsTC;
-        T.te = min(T.t0 + kWsTC, nISM);
-        T.tc = T.t0 + kWsTC / 2;
-        T.invLz = 1.0 / T.g.L[2];
-        T.offE = T.g.s[2] - T.g.r[2];
-        T.offO = -T.g.s[2] - T.g.r[2];
-        double xlo = (double)T.t0 - H, xhi = (double)(T.te - 1) + H;
-        double dlo = xlo > 0.0 ? xlo * A.c_over_fs : 0.0;
-        double dhi = xhi * A.c_over_fs;
-        T.dlo2 = dlo * dlo;
-        T.dhi2 = dhi * dhi;
-        T.xrel_max = (float)(T.te - 1 - T.t0) + 2.f * H;
-        int lo[2], hi[2];
-        for (int ax = 0; ax < 2; ax++) {
-          double L = T.g.L[ax], r = T.g.r[ax];
-          int a = (int)floor((r - dhi) / L) - 1, b = (int)floor((r + dhi) / L) + 1;
-          lo[ax] = max(a, T.g.nlo[ax]);
-          hi[ax] = min(b, T.g.nhi[ax] - 1);
-        }
-        T.nx0 = lo[0]; T.ny0 = lo[1];
-        T.NX = max(0, hi[0] - lo[0] + 1);
-        T.ncols = T.NX * max(0, hi[1] - lo[1] + 1);
-        T.zl = T.g.nlo[2];
-        T.zh = T.g.nhi[2] - 1;
-        T.use_bz = (T.zh - T.zl + 1) <= kBzMax;
       }
+      bar_sync(kBarProd, kPT);
+      if ((long long)sm.next_work >= n_work) break;
       bar_sync(kBarProd, kPT);
       const WsTile& T = sm.ti;
       const RirGeom& g = T.g;
@@ -371,6 +426,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
           }
         }
         bar_sync(kBarProd, kPT);  // column records are replaced by the next batch
+      }
+      if (warp == 0) {  // stage the next work item while the last window is sorted and published
+        const long long wn = __shfl_sync(0xffffffffu, wi_pending, 0);
+        ws_prefetch(A, wn, n_work, sm.stage, lane);
       }
       bar_sync(kBarProd, kPT);
       publish(kWinLast, nbins);  // the tile's last window (possibly empty)

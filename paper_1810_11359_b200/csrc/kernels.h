@@ -8,7 +8,7 @@
 namespace gpurir {
 
 // One RIR of a multi-room batch (device copy built by the host planner).
-struct BatchJob {
+struct alignas(16) BatchJob {
   float L[3];
   float beta[6];
   float src[3];
@@ -22,12 +22,16 @@ struct BatchJob {
   float kappa_fs;       // kappa / fs (1/sample) of the Sabine envelope (Eq. 8, C14)
   float pad;
   unsigned long long rir_global;  // tail RNG stream id (C16)
+  float lb[6];          // log2 |beta_w| (0 where beta_w == 0), precomputed on the host
+  unsigned neg, zero;   // bit w: beta_w < 0 / beta_w == 0
 };
 
 struct IsmArgs {
   // single-room call (jobs == nullptr)
   float L[3];
   float beta[6];
+  float lb[6];           // log2 |beta_w| (0 where beta_w == 0), precomputed on the host
+  unsigned neg, zero;    // bit w: beta_w < 0 / beta_w == 0
   int nb[3];
   int pattern;
   const float* pos_src;
@@ -87,6 +91,6 @@ cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* cou
 cudaError_t launch_tail(const TailArgs& A, long long nblocks, cudaStream_t stream);
 
 constexpr int kTailThreads = 256;
-constexpr int kTailChunk = kTailThreads * 8;  // samples per tail CTA (2 Philox blocks per thread)
+constexpr int kTailChunk = kTailThreads * 16;  // samples per tail CTA (4 Philox blocks per thread)
 
 }  // namespace gpurir
