@@ -94,7 +94,7 @@ struct WsTile {
   double dlo2, dhi2, invLz, offE, offO;
   long long row;
   int m, t0, te, tc, nx0, ny0, NX, ncols, zl, zh;
-  float xrel_max;
+  float xrel_max, invNX;
   int use_bz;
 };
 
@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
             T.nx0 = lo[0]; T.ny0 = lo[1];
             T.NX = max(0, hi[0] - lo[0] + 1);
             T.ncols = T.NX * max(0, hi[1] - lo[1] + 1);
+            T.invNX = T.NX > 0 ? 1.f / (float)T.NX : 0.f;
             T.zl = T.g.nlo[2];
             T.zh = T.g.nhi[2] - 1;
             T.use_bz = (T.zh - T.zl + 1) <= kBzMax;
@@ -313,7 +314,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
           WsColRec cr;
           cr.r1lo = 0; cr.r2lo = 0; cr.r1n = 0; cr.rho2 = 0.0; cr.bxy = 0.f; cr.cdot = 0.f; cr.pad = 0;
           if (q < T.ncols) {
-            const int nx = T.nx0 + q % T.NX, ny = T.ny0 + q / T.NX;
+            const int qy = (int)(((float)q + 0.5f) * T.invNX);  // q / NX, exact for q < 2^20
+            const int nx = T.nx0 + (q - qy * T.NX), ny = T.ny0 + qy;
             const double dx = image_coord(nx, g.L[0], g.s[0]) - g.r[0];
             const double dy = image_coord(ny, g.L[1], g.s[1]) - g.r[1];
             const double rho2 = dx * dx + dy * dy;
@@ -324,8 +326,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
             float bxy = zero ? 0.f : ex2_approx(lxy);
             cr.bxy = sgn ? -bxy : bxy;
             if (rho2 < T.dhi2) {
-              double zhi = sqrt(T.dhi2 - rho2);
-              double zlo = T.dlo2 > rho2 ? sqrt(T.dlo2 - rho2) : 0.0;
+              // shell bounds along z: fp32 square roots suffice (an image misplaced by their rounding sits on the
+              // shell edge, where its window weight is ~0); the ranges below are exact for these bounds
+              const double zhi = (double)sqrtf((float)(T.dhi2 - rho2));
+              const double zlo = T.dlo2 > rho2 ? (double)sqrtf((float)(T.dlo2 - rho2)) : 0.0;
               int pa, pb, na, nbz;
               z_range(g, T.invLz, zlo, zhi, pa, pb);
               z_range(g, T.invLz, -zhi, -zlo, na, nbz);
