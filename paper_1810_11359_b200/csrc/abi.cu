@@ -260,7 +260,7 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
   if (o.mode < 0 || o.mode > 2) return GPURIR_EINVAL;
   if (o.mode == GPURIR_LUT && (o.lut_Q & (o.lut_Q - 1))) return GPURIR_EINVAL;  // power of two
   double H = o.Tw * fs / 2.0;
-  if ((int)ceil((kTC + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;  // window too long for a tile
+  if ((int)ceil((kTCPersistent + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;  // window too long
   long long nS = gpurir_nsamples(Tmax, fs);
   long long nISM = gpurir_nsamples(Tdiff, fs);
   if (nISM > nS) nISM = nS;
@@ -283,7 +283,9 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
     A.M_src = M_src; A.M_rcv = M_rcv; A.M = (int)M;
     A.nISM = (int)nISM;
     A.row_stride = nS;
-    A.nTiles = (int)((nISM + kTC - 1) / kTC);
+    const bool persistent = use_persistent(((nISM + kTC - 1) / kTC) * M, o.split, d);
+    const int tile_len = persistent ? kTCPersistent : kTC;
+    A.nTiles = (int)((nISM + tile_len - 1) / tile_len);
     fill_common(A, fs, c, o.Tw);
     A.out = out;
     A.status = d->status;
@@ -297,7 +299,7 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
     long long nclusters = (long long)A.nTiles * M;
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
-    if (use_persistent(nclusters, o.split, d)) {
+    if (persistent) {
       e = launch_ism_ws(A, o.mode, nclusters, d->work_counter, d->num_sms, stream);
     } else {
       int split = auto_split(nclusters, o.split);
@@ -338,14 +340,19 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
   if (o.mode < 0 || o.mode > 2) return GPURIR_EINVAL;
   if (o.mode == GPURIR_LUT && (o.lut_Q & (o.lut_Q - 1))) return GPURIR_EINVAL;
   double H = o.Tw * fs / 2.0;
-  if ((int)ceil((kTC + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;
+  if ((int)ceil((kTCPersistent + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;
+
+  int st = GPURIR_OK;
+  DeviceState* d = device_state(&st);
+  if (!d) return st;
+  cudaStream_t stream = (cudaStream_t)o.stream;
 
   std::vector<BatchJob> jobs(n_rooms);
   std::vector<int2> tiles, chunks;
-  std::vector<std::pair<double, int2>> order;  // (estimated cost, (job, tile)) for heavy-first scheduling
+  long long small_tiles = 0;  // work items at the cluster kernel's tile length (kernel choice)
   for (int i = 0; i < n_rooms; i++) {
     const gpurir_room& R = rooms[i];
-    if (int st = validate_room(R.room_sz, R.beta, R.nb_img, R.mic_pattern)) return st;
+    if (int e0 = validate_room(R.room_sz, R.beta, R.nb_img, R.mic_pattern)) return e0;
     if (!(R.Tmax > 0) || !(R.Tdiff >= 0) || R.out_offset < 0) return GPURIR_EINVAL;
     BatchJob& J = jobs[i];
     memset(&J, 0, sizeof(J));
@@ -363,25 +370,27 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     double T60 = sabine(R.room_sz, R.beta);
     J.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);
     J.rir_global = o.rir_index_base + (unsigned long long)i;
-    int nT = (int)((nISM + kTC - 1) / kTC);
-    double V = (double)R.room_sz[0] * R.room_sz[1] * R.room_sz[2];
-    for (int t = 0; t < nT; t++) {
-      double tm = (t + 1) * kTC / fs;  // image density ~ 4 pi c^3 t^2 / V (SURVEY §7 hard part 2)
-      order.push_back({tm * tm / V + 1e-9, make_int2(i, t)});
-    }
+    small_tiles += (nISM + kTC - 1) / kTC;
     long long groups = (nS + 3) / 4 - nISM / 4;
     int nch = nISM < nS ? (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4)) : 0;
     for (int ch = 0; ch < nch; ch++) chunks.push_back(make_int2(i, ch));
+  }
+  const bool persistent = use_persistent(small_tiles, o.split, d);
+  const int tile_len = persistent ? kTCPersistent : kTC;
+  std::vector<std::pair<double, int2>> order;  // (estimated cost, (job, tile)) for heavy-first scheduling
+  for (int i = 0; i < n_rooms; i++) {
+    const BatchJob& J = jobs[i];
+    int nT = (J.nISM + tile_len - 1) / tile_len;
+    double V = (double)J.L[0] * J.L[1] * J.L[2];
+    for (int t = 0; t < nT; t++) {
+      double tm = (double)(t + 1) * tile_len / fs;  // image density ~ 4 pi c^3 t^2 / V (SURVEY §7 hard part 2)
+      order.push_back({tm * tm / V + 1e-9, make_int2(i, t)});
+    }
   }
   std::stable_sort(order.begin(), order.end(),
                    [](const std::pair<double, int2>& a, const std::pair<double, int2>& b) { return a.first > b.first; });
   tiles.reserve(order.size());
   for (auto& p : order) tiles.push_back(p.second);
-
-  int st = GPURIR_OK;
-  DeviceState* d = device_state(&st);
-  if (!d) return st;
-  cudaStream_t stream = (cudaStream_t)o.stream;
 
   size_t bj = jobs.size() * sizeof(BatchJob), bt = tiles.size() * sizeof(int2), bc = chunks.size() * sizeof(int2);
   size_t total = bj + bt + bc + 64;
@@ -413,7 +422,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     }
     long long nw = (long long)tiles.size();
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
-    if (use_persistent(nw, o.split, d)) e = launch_ism_ws(A, o.mode, nw, d->work_counter, d->num_sms, stream);
+    if (persistent) e = launch_ism_ws(A, o.mode, nw, d->work_counter, d->num_sms, stream);
     else e = launch_ism(A, o.mode, auto_split(nw, o.split), nw, stream);
     if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_ism(batch)"); }
     if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);

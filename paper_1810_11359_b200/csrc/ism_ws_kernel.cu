@@ -1,14 +1,14 @@
 // ism_ws_kernel.cu — persistent, warp-specialised ISM kernel for large batches
 // (hot-path rows a1-a5 of SURVEY.md §8(a); same mathematics as ism_kernel.cu).
 //
-// One CTA per SM loops over (RIR, 256-sample tile) work items taken heaviest-first
+// One CTA per SM loops over (RIR, 512-sample tile) work items taken heaviest-first
 // from a global counter.  Inside the CTA:
 //   producer warps (16): enumerate the shell images of a tile column by column
 //     (exact n_z ranges), compute each image's parameters in registers
 //     (Eqs. 1-4; fp64 delay), append compact records to a
 //     private window, stable-sort the window by delay bin and publish it into
 //     one of two shared buffers;
-//   consumer warps (16): wait for a published buffer, accumulate their two
+//   consumer warps (16): wait for a published buffer, accumulate their four
 //     8-sample sub-tiles from the contiguous record range of their bins
 //     (Eqs. 5-6), release the buffer, and write the tile when its last window
 //     has been consumed.
@@ -25,11 +25,12 @@ constexpr int kPW = 16;                      // producer warps
 constexpr int kCW = 16;                      // consumer warps
 constexpr int kPT = kPW * 32;                // producer threads
 constexpr int kWsThreads = (kPW + kCW) * 32; // 1024
-constexpr int kWsTC = kCW * 2 * kS;          // 256 samples per tile
+constexpr int kWsSub = 4;                    // 8-sample sub-tiles per consumer warp
+constexpr int kWsTC = kCW * kWsSub * kS;     // 512 samples per tile
 template <int MODE> struct WsCap { static constexpr int v = MODE == 1 ? 2048 : 4096; };  // records per window
 constexpr int kWsColBatch = kPT;             // columns per enumeration batch
 constexpr int kBzMax = 1024;                 // z-factor table entries
-static_assert(kWsTC == kTC, "tile size shared with the host planner");
+static_assert(kWsTC == kTCPersistent, "tile size shared with the host planner");
 
 constexpr int kNBuf = 3;       // published window buffers (producers may run kNBuf - 1 windows ahead)
 constexpr int kBarFull0 = 1;   // + buffer: producers arrive, consumers sync
@@ -445,11 +446,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
     // =========================== consumers ===========================
     const int cw = warp - kPW;
     const int grp = lane >> 3, li = lane & 7;
-    int kfs[2];
-    float2 acc[2];
+    int kfs[kWsSub];
+    float2 acc[kWsSub];
 #pragma unroll
-    for (int s = 0; s < 2; s++) {
-      kfs[s] = (cw * 2 + s) * kS + li - kWsTC / 2;  // sample relative to the tile centre
+    for (int s = 0; s < kWsSub; s++) {
+      kfs[s] = (cw * kWsSub + s) * kS + li - kWsTC / 2;  // sample relative to the tile centre
       acc[s] = make_float2(0.f, 0.f);
     }
     int win_i = 0;
@@ -463,8 +464,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
       }
       const float4* sorted = sm.sorted[buf];
 #pragma unroll
-      for (int s = 0; s < 2; s++) {
-        const int sub = cw * 2 + s;
+      for (int s = 0; s < kWsSub; s++) {
+        const int sub = cw * kWsSub + s;
         const int ra = sm.binstart[buf][sub], rb = sm.binstart[buf][min(sub + A.nbw, w.nbins)];
         if (MODE == 0) {
           const float kv = (float)kfs[s] * A.invHs;
@@ -552,13 +553,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
       bar_arrive(kBarEmpty0 + buf, kWsThreads);  // buffer consumed
       if (w.flags & kWinLast) {
 #pragma unroll
-        for (int s = 0; s < 2; s++) {
+        for (int s = 0; s < kWsSub; s++) {
           float a = acc[s].x + acc[s].y;
           a += __shfl_xor_sync(0xffffffffu, a, 8);
           a += __shfl_xor_sync(0xffffffffu, a, 16);
           if (MODE == 0) { if (kfs[s] & 1) a = -a; }
           else if (MODE == 2) { a *= (1.f / 1024.f); if (kfs[s] & 1) a = -a; }
-          const int k = w.t0 + (cw * 2 + s) * kS + li;
+          const int k = w.t0 + (cw * kWsSub + s) * kS + li;
           if (grp == 0 && k < w.te) A.out[w.row + k] = a;
           acc[s] = make_float2(0.f, 0.f);
         }
