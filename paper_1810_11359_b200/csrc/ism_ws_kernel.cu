@@ -366,8 +366,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
             }
             int j = lo;
             int before = j > 0 ? sm.colpre[j - 1] : 0;
+            int boundary = sm.colpre[j];
+#pragma unroll 2
             for (int gi = g0; gi < g1; gi++) {
-              while (sm.colpre[j] <= gi) { before = sm.colpre[j]; j++; }
+              while (gi >= boundary) { before = boundary; j++; boundary = sm.colpre[j]; }
               const WsColRec& cr = sm.col[j];
               const int l = gi - before;
               const int nz = l < cr.r1n ? cr.r1lo + l : cr.r2lo + (l - cr.r1n);
@@ -375,47 +377,43 @@ __global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long l
               const int odd = nz & 1;
               const double dz = fma((double)(nz + odd), g.L[2], odd ? T.offO : T.offE);
               const double x2 = fma(dz, dz, cr.rho2) * sc2;  // (d fs / c)^2
-              uint8_t b = kDiscard;
-              float2 rec = make_float2(0.f, 0.f);
+              if (x2 == 0.0) atomicOr(A.status, kStatusDegenerate);
+              // branch-free from here: culled records are computed and flagged with kDiscard
+              float x0f;
+              float xr = delay_rel(x2, T.tc, x0f);
+              const float xrel = xr + (float)(kWsTC / 2) + H;  // x - (t0 - H)
+              const bool keep = (x2 != 0.0) && (xrel > 0.f) && (xrel < T.xrel_max);
+              const uint8_t b = keep ? (uint8_t)(int)(xrel * (1.f / (float)kS)) : kDiscard;
+              const float rx = rcp_approx(x0f);          // 1/d = fs / (c x)
+              const float bz = T.use_bz ? sm.bz[min(max(nz - T.zl, 0), kBzMax - 1)] : z_factor(nz, g);
+              const float cth = fmaf((float)dz, g.o[2], cr.cdot) * ((float)fs_over_c * rx);
+              const float gain = g.a + (1.f - g.a) * cth;
+              const float amp = cr.bxy * bz * gain * rx * fs_over_c_4pi;  // Eq. 4
+              float2 rec;
               float recA = 0.f;
-              if (x2 == 0.0) {
-                atomicOr(A.status, kStatusDegenerate);
+              if (MODE == 1) {
+                float xq = xr * (float)A.lutQ;
+                float fiq = floorf(xq);
+                float phi = xq - fiq;
+                int iq1 = (int)fiq + 1;
+                int php = iq1 & (A.lutQ - 1);
+                int aa = (iq1 - php) / A.lutQ;
+                int ph = (A.lutQ - php) & (A.lutQ - 1);
+                int jsh = aa + (php > 0 ? 1 : 0);
+                rec = make_float2(__int_as_float(ph * A.lut_cols + A.lut_joff - jsh), phi);
+                recA = amp;
               } else {
-                float x0f;
-                float xr = delay_rel(x2, T.tc, x0f);
-                float xrel = xr + (float)(kWsTC / 2) + H;  // x - (t0 - H)
-                if (xrel > 0.f && xrel < T.xrel_max) {
-                  b = (uint8_t)(int)(xrel * (1.f / (float)kS));
-                  const float rx = rcp_approx(x0f);          // 1/d = fs / (c x)
-                  const float bz = T.use_bz ? sm.bz[nz - T.zl] : z_factor(nz, g);
-                  const float cth = fmaf((float)dz, g.o[2], cr.cdot) * ((float)fs_over_c * rx);
-                  const float gain = g.a + (1.f - g.a) * cth;
-                  const float amp = cr.bxy * bz * gain * rx * fs_over_c_4pi;  // Eq. 4
-                  if (MODE == 1) {
-                    float xq = xr * (float)A.lutQ;
-                    float fiq = floorf(xq);
-                    float phi = xq - fiq;
-                    int iq1 = (int)fiq + 1;
-                    int php = iq1 & (A.lutQ - 1);
-                    int aa = (iq1 - php) / A.lutQ;
-                    int ph = (A.lutQ - php) & (A.lutQ - 1);
-                    int jsh = aa + (php > 0 ? 1 : 0);
-                    rec = make_float2(__int_as_float(ph * A.lut_cols + A.lut_joff - jsh), phi);
-                    recA = amp;
-                  } else {
-                    float fj = floorf(xr);
-                    float f = xr - fj;
-                    if (f == 0.f) {  // reading R3
-                      xr = nextafterf(xr, 1e30f);
-                      fj = floorf(xr);
-                      f = xr - fj;
-                    }
-                    float cc = -amp * sinpi01(f) * 0.318309886183790672f;
-                    if ((int)fj & 1) cc = -cc;
-                    if (MODE == 0) rec = make_float2(-xr * A.invHs, cc * A.invHs);
-                    else rec = make_float2(-xr * (0.5f * A.invHs), cc * (0.5f * A.invHs) * 1024.f);
-                  }
+                float fj = floorf(xr);
+                float f = xr - fj;
+                if (f == 0.f) {  // exact integer delay (reading R3): move off the sinc zero by >= 1 ulp
+                  xr += fmaxf(fabsf(xr) * 1.1920929e-7f, 9.5367432e-7f);
+                  fj = floorf(xr);
+                  f = xr - fj;
                 }
+                float cc = -amp * sinpi01(f) * 0.318309886183790672f;
+                if ((int)fj & 1) cc = -cc;
+                if (MODE == 0) rec = make_float2(-xr * A.invHs, cc * A.invHs);
+                else rec = make_float2(-xr * (0.5f * A.invHs), cc * (0.5f * A.invHs) * 1024.f);
               }
               const int dst = filled + (gi - base);
               sm.rec[dst] = rec;
