@@ -14,7 +14,10 @@
  *     library.  Calls are stream-ordered on opts->stream and return without a
  *     device synchronisation unless GPURIR_FLAG_SYNC is set.
  *   - There is no global mutable state (the paper's global LUT / mixed-
- *     precision switches, become the per-call opts->mode).
+ *     precision switches, become the per-call opts->mode).  Per device
+ *     the library keeps a status word, a LUT cache and a ring of 256 work-
+ *     queue counters, so up to 256 calls may be in flight concurrently on
+ *     different streams of one device.
  *   - Validation runs on the host before any launch.  Conditions that can
  *     only be seen on the device (a zero orientation vector, an image source
  *     coinciding with a receiver) raise a per-device status word that is

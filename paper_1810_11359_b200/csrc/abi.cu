@@ -21,6 +21,7 @@ using namespace gpurir;
 namespace {
 
 thread_local char g_cuda_err[256] = "";
+constexpr unsigned kCounterRing = 256;
 
 int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
@@ -28,31 +29,36 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 // Per-device status word and LUT cache (lazily created, process lifetime).
+struct LutEntry {  // one uploaded Eq. 9 table; entries are never overwritten (kernels may still read them)
+  double Tw = 0, fs = 0;
+  int Q = 0, rows = 0, cols = 0, joff = 0;
+  float2* dev = nullptr;
+};
+
 struct DeviceState {
   int* status = nullptr;
-  int* work_counter = nullptr;  // persistent-kernel work queue head
+  std::vector<LutEntry> luts;
+  int* work_counter = nullptr;  // persistent-kernel work-queue heads, one per call in flight (ring)
+  unsigned next_counter = 0;
   int num_sms = 0;
-  float2* lut = nullptr;
-  size_t lut_cap = 0;
-  double lut_Tw = 0, lut_fs = 0;
-  int lut_Q = 0, lut_rows = 0, lut_cols = 0, lut_joff = 0;
 };
 std::mutex g_mu;
-std::vector<DeviceState> g_dev;
+constexpr int kMaxDevices = 64;
+DeviceState g_dev[kMaxDevices];  // stable addresses: callers keep pointers while other threads add devices
 
 DeviceState* device_state(int* err) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) { *err = cuda_fail(e, "cudaGetDevice"); return nullptr; }
+  if (dev < 0 || dev >= kMaxDevices) { *err = GPURIR_EINVAL; return nullptr; }
   std::lock_guard<std::mutex> lk(g_mu);
-  if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
   DeviceState& d = g_dev[dev];
   if (!d.status) {
     e = cudaMalloc(&d.status, sizeof(int));
     if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMalloc(status)"); return nullptr; }
     e = cudaMemset(d.status, 0, sizeof(int));
     if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMemset(status)"); return nullptr; }
-    e = cudaMalloc(&d.work_counter, sizeof(int));
+    e = cudaMalloc(&d.work_counter, kCounterRing * sizeof(int));
     if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMalloc(counter)"); return nullptr; }
     e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) { *err = cuda_fail(e, "num_sms"); return nullptr; }
@@ -75,33 +81,32 @@ long long lut_half(double Tw, double fs, int Q) { return (long long)ceil(Tw * Q 
 
 // Phase-major interpolation table for the LUT kernel:
 // TP[ph][jj + joff] = (T[Q jj + ph + 1], T[Q jj + ph] - T[Q jj + ph + 1]).
-int ensure_lut(DeviceState* d, double Tw, double fs, int Q, double H, cudaStream_t stream) {
-  if (d->lut && d->lut_Tw == Tw && d->lut_fs == fs && d->lut_Q == Q) return GPURIR_OK;
+const LutEntry* ensure_lut(DeviceState* d, double Tw, double fs, int Q, double H, cudaStream_t stream, int* err) {
+  *err = GPURIR_OK;
+  for (const LutEntry& L : d->luts)
+    if (L.Tw == Tw && L.fs == fs && L.Q == Q) return &L;
   long long half = lut_half(Tw, fs, Q);
-  int joff = (int)ceil(H) + kS + 2;
-  int cols = 2 * joff + 1;
-  int rows = Q;
-  std::vector<float2> tab((size_t)rows * cols);
-  for (int ph = 0; ph < rows; ph++)
-    for (int c = 0; c < cols; c++) {
-      long long jj = c - joff;
+  LutEntry L;
+  L.Tw = Tw; L.fs = fs; L.Q = Q;
+  L.joff = (int)ceil(H) + kS + 2;
+  L.cols = 2 * L.joff + 1;
+  L.rows = Q;
+  std::vector<float2> tab((size_t)L.rows * L.cols);
+  for (int ph = 0; ph < L.rows; ph++)
+    for (int c = 0; c < L.cols; c++) {
+      long long jj = c - L.joff;
       long long n = (long long)Q * jj + ph;
       double t0 = lut_entry(n, Tw, fs, Q, half), t1 = lut_entry(n + 1, Tw, fs, Q, half);
-      tab[(size_t)ph * cols + c] = make_float2((float)t1, (float)(t0 - t1));
+      tab[(size_t)ph * L.cols + c] = make_float2((float)t1, (float)(t0 - t1));
     }
   size_t bytes = tab.size() * sizeof(float2);
-  if (bytes > d->lut_cap) {
-    if (d->lut) cudaFree(d->lut);
-    cudaError_t e = cudaMalloc(&d->lut, bytes);
-    if (e != cudaSuccess) { d->lut = nullptr; d->lut_cap = 0; return cuda_fail(e, "cudaMalloc(lut)"); }
-    d->lut_cap = bytes;
-  }
-  cudaError_t e = cudaMemcpyAsync(d->lut, tab.data(), bytes, cudaMemcpyHostToDevice, stream);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(lut)");
-  e = cudaStreamSynchronize(stream);  // host vector goes out of scope
-  if (e != cudaSuccess) return cuda_fail(e, "sync(lut)");
-  d->lut_Tw = Tw; d->lut_fs = fs; d->lut_Q = Q; d->lut_rows = rows; d->lut_cols = cols; d->lut_joff = joff;
-  return GPURIR_OK;
+  cudaError_t e = cudaMalloc(&L.dev, bytes);
+  if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMalloc(lut)"); return nullptr; }
+  e = cudaMemcpyAsync(L.dev, tab.data(), bytes, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // host staging vector goes out of scope
+  if (e != cudaSuccess) { cudaFree(L.dev); *err = cuda_fail(e, "upload(lut)"); return nullptr; }
+  d->luts.push_back(L);
+  return &d->luts.back();
 }
 
 double sabine(const float L[3], const float b[6]) {
@@ -160,6 +165,13 @@ int auto_split(long long nclusters, int requested) {
   int s = 1;
   while (s < kMaxSplit && nclusters * s < 148LL * 4) s *= 2;
   return s;
+}
+
+// Work-queue head for one persistent launch: a ring of kCounterRing counters so that up to that many
+// calls can be in flight on different streams (each is zeroed on its stream right before its launch).
+int* take_counter(DeviceState* d) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return d->work_counter + (d->next_counter++ % kCounterRing);
 }
 
 // Persistent warp-specialised kernel when there are enough (RIR, tile) work items to keep one CTA per
@@ -291,16 +303,16 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
     A.status = d->status;
     if (o.mode == GPURIR_LUT) {
       std::lock_guard<std::mutex> lk(g_mu);
-      st = ensure_lut(d, o.Tw, fs, o.lut_Q, H, stream);
-      if (st) return st;
-      A.lut = d->lut; A.lut_rows = d->lut_rows; A.lut_cols = d->lut_cols; A.lut_joff = d->lut_joff;
+      const LutEntry* L = ensure_lut(d, o.Tw, fs, o.lut_Q, H, stream, &st);
+      if (!L) return st;
+      A.lut = L->dev; A.lut_rows = L->rows; A.lut_cols = L->cols; A.lut_joff = L->joff;
       A.lutQ = o.lut_Q;
     }
     long long nclusters = (long long)A.nTiles * M;
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
     if (persistent) {
-      e = launch_ism_ws(A, o.mode, nclusters, d->work_counter, d->num_sms, stream);
+      e = launch_ism_ws(A, o.mode, nclusters, take_counter(d), d->num_sms, stream);
     } else {
       int split = auto_split(nclusters, o.split);
       e = launch_ism(A, o.mode, split, nclusters, stream);
@@ -415,14 +427,14 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     A.status = d->status;
     if (o.mode == GPURIR_LUT) {
       std::lock_guard<std::mutex> lk(g_mu);
-      st = ensure_lut(d, o.Tw, fs, o.lut_Q, H, stream);
-      if (st) { cudaFreeAsync(ws, stream); return st; }
-      A.lut = d->lut; A.lut_rows = d->lut_rows; A.lut_cols = d->lut_cols; A.lut_joff = d->lut_joff;
+      const LutEntry* L = ensure_lut(d, o.Tw, fs, o.lut_Q, H, stream, &st);
+      if (!L) { cudaFreeAsync(ws, stream); return st; }
+      A.lut = L->dev; A.lut_rows = L->rows; A.lut_cols = L->cols; A.lut_joff = L->joff;
       A.lutQ = o.lut_Q;
     }
     long long nw = (long long)tiles.size();
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
-    if (persistent) e = launch_ism_ws(A, o.mode, nw, d->work_counter, d->num_sms, stream);
+    if (persistent) e = launch_ism_ws(A, o.mode, nw, take_counter(d), d->num_sms, stream);
     else e = launch_ism(A, o.mode, auto_split(nw, o.split), nw, stream);
     if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_ism(batch)"); }
     if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);
