@@ -389,20 +389,20 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
   }
   const bool persistent = use_persistent(small_tiles, o.split, d);
   const int tile_len = persistent ? kTCPersistent : kTC;
-  std::vector<std::pair<double, int2>> order;  // (estimated cost, (job, tile)) for heavy-first scheduling
+  // heavy-first schedule without a comparison sort: image density grows ~ t^2 (SURVEY §7 hard part 2), so
+  // emit all rooms' last tiles first, then the second-to-last, ... (a counting order over tile index)
+  int max_tiles = 0;
+  std::vector<int> ntile(n_rooms);
   for (int i = 0; i < n_rooms; i++) {
-    const BatchJob& J = jobs[i];
-    int nT = (J.nISM + tile_len - 1) / tile_len;
-    double V = (double)J.L[0] * J.L[1] * J.L[2];
-    for (int t = 0; t < nT; t++) {
-      double tm = (double)(t + 1) * tile_len / fs;  // image density ~ 4 pi c^3 t^2 / V (SURVEY §7 hard part 2)
-      order.push_back({tm * tm / V + 1e-9, make_int2(i, t)});
-    }
+    ntile[i] = (jobs[i].nISM + tile_len - 1) / tile_len;
+    max_tiles = std::max(max_tiles, ntile[i]);
   }
-  std::stable_sort(order.begin(), order.end(),
-                   [](const std::pair<double, int2>& a, const std::pair<double, int2>& b) { return a.first > b.first; });
-  tiles.reserve(order.size());
-  for (auto& p : order) tiles.push_back(p.second);
+  size_t total_tiles = 0;
+  for (int i = 0; i < n_rooms; i++) total_tiles += (size_t)ntile[i];
+  tiles.reserve(total_tiles);
+  for (int t = max_tiles - 1; t >= 0; t--)
+    for (int i = 0; i < n_rooms; i++)
+      if (ntile[i] > t) tiles.push_back(make_int2(i, t));
 
   size_t bj = jobs.size() * sizeof(BatchJob), bt = tiles.size() * sizeof(int2), bc = chunks.size() * sizeof(int2);
   size_t total = bj + bt + bc + 64;
