@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgpurir.so")
+LIB_PATH = os.environ.get("GPURIR_LIB", os.path.join(_HERE, "libgpurir.so"))  # override: A/B builds only
 
 OK, EINVAL, EDEGENERATE, EINFEASIBLE, ENOMEM, ECUDA = range(6)
 FLAG_SYNC = 1

@@ -21,13 +21,17 @@
 
 namespace gpurir {
 
-constexpr int kPW = 16;                      // producer warps
-constexpr int kCW = 16;                      // consumer warps
+#ifndef GPURIR_WS_CTAS_PER_SM
+#define GPURIR_WS_CTAS_PER_SM 2
+#endif
+constexpr int kWsCtasPerSm = GPURIR_WS_CTAS_PER_SM;  // persistent CTAs per SM (1: 16P+16C, 2: 8P+8C each)
+constexpr int kPW = 16 / kWsCtasPerSm;       // producer warps
+constexpr int kCW = 16 / kWsCtasPerSm;       // consumer warps
 constexpr int kPT = kPW * 32;                // producer threads
-constexpr int kWsThreads = (kPW + kCW) * 32; // 1024
-constexpr int kWsSub = 4;                    // 8-sample sub-tiles per consumer warp
+constexpr int kWsThreads = (kPW + kCW) * 32; // 1024 / kWsCtasPerSm
+constexpr int kWsSub = 4 * kWsCtasPerSm;     // 8-sample sub-tiles per consumer warp
 constexpr int kWsTC = kCW * kWsSub * kS;     // 512 samples per tile
-template <int MODE> struct WsCap { static constexpr int v = MODE == 1 ? 2048 : 4096; };  // records per window
+template <int MODE> struct WsCap { static constexpr int v = (MODE == 1 ? 2048 : 4096) / kWsCtasPerSm; };  // records per window
 constexpr int kWsColBatch = kPT;             // columns per enumeration batch
 constexpr int kBzMax = 1024;                 // z-factor table entries
 static_assert(kWsTC == kTCPersistent, "tile size shared with the host planner");
@@ -135,7 +139,7 @@ __device__ __forceinline__ float z_factor(int nz, const RirGeom& g) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kWsThreads, 1) ism_ws_kernel(IsmArgs A, long long n_work, int* work_counter) {
+__global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArgs A, long long n_work, int* work_counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WsSmem<MODE>& sm = *reinterpret_cast<WsSmem<MODE>*>(smem_raw);
   float2* lut = reinterpret_cast<float2*>(smem_raw + sizeof(WsSmem<MODE>));
@@ -588,7 +592,8 @@ cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* cou
                           cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
-  int grid = (int)(n_work < num_sms ? n_work : num_sms);
+  const long long slots = (long long)num_sms * kWsCtasPerSm;
+  int grid = (int)(n_work < slots ? n_work : slots);
   size_t smem = ism_ws_smem_bytes(mode, A.lut_rows, A.lut_cols);
   switch (mode) {
     case 0: return launch_ws_mode<0>(A, n_work, counter, grid, smem, stream);
