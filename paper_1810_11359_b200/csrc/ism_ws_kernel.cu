@@ -31,12 +31,18 @@ constexpr int kPT = kPW * 32;                // producer threads
 constexpr int kWsThreads = (kPW + kCW) * 32; // 1024 / kWsCtasPerSm
 constexpr int kWsSub = 4 * kWsCtasPerSm;     // 8-sample sub-tiles per consumer warp
 constexpr int kWsTC = kCW * kWsSub * kS;     // 512 samples per tile
-template <int MODE> struct WsCap { static constexpr int v = (MODE == 1 ? 2048 : 4096) / kWsCtasPerSm; };  // records per window
+#ifndef GPURIR_WS_CAP
+#define GPURIR_WS_CAP (4096 / GPURIR_WS_CTAS_PER_SM)
+#endif
+#ifndef GPURIR_WS_NBUF
+#define GPURIR_WS_NBUF 3
+#endif
+template <int MODE> struct WsCap { static constexpr int v = MODE == 1 ? GPURIR_WS_CAP / 2 : GPURIR_WS_CAP; };  // records per window
 constexpr int kWsColBatch = kPT;             // columns per enumeration batch
 constexpr int kBzMax = 1024;                 // z-factor table entries
 static_assert(kWsTC == kTCPersistent, "tile size shared with the host planner");
 
-constexpr int kNBuf = 3;       // published window buffers (producers may run kNBuf - 1 windows ahead)
+constexpr int kNBuf = GPURIR_WS_NBUF;  // published window buffers (producers may run kNBuf - 1 windows ahead)
 constexpr int kBarFull0 = 1;   // + buffer: producers arrive, consumers sync
 constexpr int kBarEmpty0 = kBarFull0 + kNBuf;   // + buffer: consumers arrive, producers sync
 constexpr int kBarProd = kBarEmpty0 + kNBuf;    // producer-internal
