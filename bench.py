@@ -258,10 +258,10 @@ def main():
     stream = torch.cuda.current_stream(dev)
     base = rank * M_PER_GPU
 
-    def step(ev=None):
+    def step(ev=None, ev_tail=None):
         P.simulate_rir(sc.room, beta, src, rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=orv,
                        mic_pattern=sc.pattern, mode=args.mode, seed=sc.seed, rir_index_base=base, out=out,
-                       stream=stream, ev_ism=ev)
+                       stream=stream, ev_ism=ev, ev_tail=ev_tail)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -273,6 +273,8 @@ def main():
     ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
     ism_s = [RawEvent() for _ in range(n_ev)]
     ism_e = [RawEvent() for _ in range(n_ev)]
+    tail_s = [RawEvent() for _ in range(n_ev)]
+    tail_e = [RawEvent() for _ in range(n_ev)]
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -280,13 +282,14 @@ def main():
         for i in range(args.steps):
             flush.zero_()                       # L2 flushed between timed steps (outside the events)
             ev_s[i].record(stream)
-            step((ism_s[i], ism_e[i]))
+            step((ism_s[i], ism_e[i]), (tail_s[i], tail_e[i]))
             ev_e[i].record(stream)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
     ism_ms = [a.elapsed_ms(b) for a, b in zip(ism_s, ism_e)]
+    tail_ms = [a.elapsed_ms(b) for a, b in zip(tail_s, tail_e)]
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
     if dist:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -359,6 +362,16 @@ def main():
     issue_peak = 148 * 128 * f_clk  # FP32 lane issue slots / s (B200_PROFILING.md unit counts)
     achieved = taps_launch * ISSUE_SLOTS_PER_TAP / ism_avg_s
     lattice = float(np.prod(nb.astype(np.float64)))
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ism_traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
+    except Exception:
+        pass
+    tail_bytes = M_PER_GPU * (nS - nISM) * 4
+    tail_avg_s = float(np.mean(tail_ms)) / 1000.0
+    hbm_peak = float(pk.get("hbm_gbs", 6650.0))
 
     line = {
         "metric": METRIC, "value": value, "unit": "RIRs/s", "n_gpus": world, "steps": args.steps,
@@ -372,11 +385,15 @@ def main():
         "taps_per_s": world * taps_launch / ism_avg_s if world == 1 else None,
         "ism_ms": float(np.mean(ism_ms)),
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": issue_peak / 1e12,
-                     "unit": "T FP32-lane-issue-slots/s", "frac": achieved / issue_peak, "traffic": None,
+                     "unit": "T FP32-lane-issue-slots/s", "frac": achieved / issue_peak, "traffic": traffic,
+                     "traffic_note": "DRAM bytes per launch from profiles/r01_ism_traffic.json (ncu --set full)",
                      "kernel": "ism_kernel<0>",
                      "basis": f"{ISSUE_SLOTS_PER_TAP} issue slots per in-window tap (SURVEY §8(d)) x {taps_launch:.4g} "
                               f"taps per launch (exact count on 256 sampled receivers x {M_PER_GPU}); peak = 148 SM x "
                               f"128 lanes x {f_clk / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)"},
+        "tail_kernel": {"ms": float(np.mean(tail_ms)), "bytes": tail_bytes, "GB_per_s": tail_bytes / tail_avg_s / 1e9,
+                        "frac_of_hbm": tail_bytes / tail_avg_s / 1e9 / hbm_peak, "bound": "hbm (write)",
+                        "peak_GB_per_s": hbm_peak},
         "e2e": {"value": e2e_value, "unit": "RIRs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "pipelining": "2 streams: D2H of step i overlaps the kernels of step i+1"},
         "gpu_launches": 2 * args.steps,
