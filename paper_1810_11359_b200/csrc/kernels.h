@@ -91,6 +91,6 @@ cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* cou
 cudaError_t launch_tail(const TailArgs& A, long long nblocks, cudaStream_t stream);
 
 constexpr int kTailThreads = 256;
-constexpr int kTailChunk = kTailThreads * 16;  // samples per tail CTA (4 Philox blocks per thread)
+constexpr int kTailChunk = kTailThreads * 64;  // samples per tail CTA (up to 16 Philox blocks per thread)
 
 }  // namespace gpurir

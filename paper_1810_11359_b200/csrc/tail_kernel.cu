@@ -69,10 +69,11 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A) {
   __syncthreads();
   const int w0 = s_w0;
   double sh = 0.0, se = 0.0;
+  const float kl2 = -kappa_fs * 1.4426950408889634f;  // exp(-kappa k / fs) = 2^(kl2 k)
   for (int k = w0 + tid; k < nISM; k += kTailThreads) {
     double v = (double)h[k];
     sh += v * v;
-    se += exp(-(double)kappa_fs * (double)k);
+    se += (double)ex2_fast(kl2 * (float)(k - w0));   // relative to w0; the common factor is restored below
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A) {
   if (tid == 0) {
     double th = 0.0, te = 0.0;
     for (int w = 0; w < kTailThreads / 32; w++) { th += red_h[w]; te += red_e[w]; }
+    te *= exp(-(double)kappa_fs * (double)w0);
     double Aenv = (w0 < nISM && te > 0.0) ? th / te : 0.0;
     // sqrt(P(k)) * sqrt(3)/pi * ln 2 = env0 * 2^(alpha (k - nISM)), alpha = -kappa_fs / (2 ln 2)
     s_env0 = (float)(sqrt(Aenv * exp(-(double)kappa_fs * nISM)) * 0.5513288954217920495 * 0.69314718055994530942);
@@ -98,10 +100,10 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A) {
   const long long qend = (long long)((nS + 3) >> 2);
   const uint2 key = make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32));
   const bool aligned = ((row & 3) == 0);
+  const long long qbeg = q0 + (long long)chunk * (kTailChunk / 4);
+  const long long qlim = min(qend, qbeg + (long long)(kTailChunk / 4));
 #pragma unroll 2
-  for (int it = 0; it < kTailChunk / (4 * kTailThreads); it++) {
-    const long long q = q0 + (long long)chunk * (kTailChunk / 4) + it * kTailThreads + tid;
-    if (q >= qend) break;
+  for (long long q = qbeg + tid; q < qlim; q += kTailThreads) {
     const uint4 ctr = make_uint4((uint32_t)q, (uint32_t)((unsigned long long)q >> 32), (uint32_t)rglob,
                                  (uint32_t)(rglob >> 32));
     const uint4 w = philox4x32_10(ctr, key);
