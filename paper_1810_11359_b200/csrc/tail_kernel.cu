@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A) {
   // ---- tail samples: Philox blocks of 4 samples, kTailChunk / 4 blocks per CTA ----------
   const long long q0 = (long long)(nISM >> 2);
   const long long qend = (long long)((nS + 3) >> 2);
-  const uint2 key = make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32));
+  const PhiloxKey key = philox_key(make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32)));
   const bool aligned = ((row & 3) == 0);
   const long long qbeg = q0 + (long long)chunk * (kTailChunk / 4);
   const long long qlim = min(qend, qbeg + (long long)(kTailChunk / 4));
@@ -113,9 +113,12 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A) {
     float vals[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      const float a = (float)(2u * (ws[j] >> 9) + 1u);  // u = a 2^-24, 1 - u = b 2^-24 (exact)
-      const float b = 16777216.f - a;
-      vals[j] = e * (lg2_approx(a) - lg2_approx(b));    // sqrt(P) (sqrt3/pi) ln(u/(1-u))
+      // u = (2 (w >> 9) + 1) 2^-24 built exactly without an int->float conversion:
+      // f = 1 + (w >> 9) 2^-23 in [1, 2), u = f - (1 - 2^-24), 1 - u = (2 - f) - 2^-24
+      const float f = __uint_as_float(0x3F800000u | (ws[j] >> 9));
+      const float u = f - 0.99999994039535522461f;
+      const float omu = (2.f - f) - 5.9604644775390625e-08f;
+      vals[j] = e * (lg2_approx(u) - lg2_approx(omu));  // sqrt(P) (sqrt3/pi) ln(u/(1-u))
       e *= rho;
     }
     float* o = A.out + row + k0;
