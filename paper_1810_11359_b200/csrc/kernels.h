@@ -88,7 +88,7 @@ cudaError_t launch_image_params(const IsmArgs& A, double* x_out, float* A_out, l
 size_t ism_ws_smem_bytes(int mode, int lut_rows, int lut_cols);
 cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* counter, int num_sms,
                           cudaStream_t stream);
-cudaError_t launch_tail(const TailArgs& A, long long nblocks, cudaStream_t stream);
+cudaError_t launch_tail(const TailArgs& A, long long n_items, cudaStream_t stream);  // one warp per item
 
 constexpr int kTailThreads = 256;
 constexpr int kTailChunk = kTailThreads * 64;  // samples per tail CTA (up to 16 Philox blocks per thread)

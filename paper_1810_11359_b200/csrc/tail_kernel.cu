@@ -7,11 +7,11 @@
 //   the direct-path sample (reading C15);
 //   h[k] = sqrt(P(k/fs)) * (sqrt(3)/pi) ln(u / (1 - u)),  nISM <= k < nS  (logistic noise),
 //   u from the stateless Philox4x32-10 stream (seed, global RIR index, k) (reading C16).
-// One CTA per (RIR, chunk of kTailChunk samples).  Each CTA re-reduces the
-// envelope window (<= 480 floats, L2 hits, fp64 sums, fixed tree) so the tail
-// needs no separate launch and no scratch; the RNG has no seeding kernel and
-// no noise buffer in HBM.  Output writes (4 B / sample, float4 stores) are the
-// only HBM traffic.
+// One warp per (RIR, chunk of kTailChunk samples).  Each warp re-reduces the
+// envelope window (<= 480 floats, L2 hits, fp64 sums, fixed butterfly) so the
+// tail needs no separate launch and no scratch; the RNG has no seeding kernel
+// and no noise buffer in HBM.  Output writes (4 B / sample, float4 stores) are
+// the only HBM traffic.
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -28,10 +28,12 @@ __device__ __forceinline__ float ex2_fast(float x) {
   return r;
 }
 
-__global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A) {
-  __shared__ double red_h[kTailThreads / 32], red_e[kTailThreads / 32];
-  __shared__ float s_env0, s_alpha;
-  __shared__ int s_w0;
+// One warp per (RIR, chunk of kTailChunk samples): the envelope window is reduced with warp shuffles
+// only (no block barriers), so the short prologue of one warp overlaps the streaming stores of others.
+__global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A, long long n_items) {
+  const int lane = threadIdx.x & 31;
+  const long long item = (long long)blockIdx.x * (kTailThreads / 32) + (threadIdx.x >> 5);
+  if (item >= n_items) return;
 
   int rir, chunk, nISM, nS;
   long long row;
@@ -40,62 +42,51 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A) {
   const float* ps;
   const float* pr;
   if (A.jobs) {
-    int2 jc = A.chunks[blockIdx.x];
+    int2 jc = A.chunks[item];
     rir = jc.x; chunk = jc.y;
     const BatchJob& J = A.jobs[rir];
     nISM = J.nISM; nS = J.nS; row = J.out_offset; kappa_fs = J.kappa_fs; rglob = J.rir_global;
     ps = J.src; pr = J.rcv;
   } else {
-    rir = blockIdx.x / A.chunks_per_rir;
-    chunk = blockIdx.x % A.chunks_per_rir;
+    rir = (int)(item / A.chunks_per_rir);
+    chunk = (int)(item % A.chunks_per_rir);
     nISM = A.nISM; nS = A.nS; row = (long long)rir * A.row_stride; kappa_fs = A.kappa_fs;
     rglob = A.rir_base + (unsigned long long)rir;
     ps = A.pos_src + 3 * (rir / A.M_rcv);
     pr = A.pos_rcv + 3 * (rir % A.M_rcv);
   }
   const float* h = A.out + row;
-  const int tid = threadIdx.x;
 
   // ---- envelope prediction (envPred; C15) -------------------------------
-  if (tid == 0) {
-    double ddx = (double)ps[0] - pr[0], ddy = (double)ps[1] - pr[1], ddz = (double)ps[2] - pr[2];
-    double x_dp = sqrt(ddx * ddx + ddy * ddy + ddz * ddz) * A.fs_over_c;  // direct-path delay (samples)
-    int w0 = nISM - A.win;
-    int wdp = (int)ceil(x_dp);
-    if (wdp > w0) w0 = wdp;
-    if (w0 < 0) w0 = 0;
-    s_w0 = w0;
-  }
-  __syncthreads();
-  const int w0 = s_w0;
+  const double ddx = (double)ps[0] - pr[0], ddy = (double)ps[1] - pr[1], ddz = (double)ps[2] - pr[2];
+  const double x_dp = sqrt(ddx * ddx + ddy * ddy + ddz * ddz) * A.fs_over_c;  // direct-path delay (samples)
+  int w0 = nISM - A.win;
+  const int wdp = (int)ceil(x_dp);
+  if (wdp > w0) w0 = wdp;
+  if (w0 < 0) w0 = 0;
   double sh = 0.0, se = 0.0;
   const float kl2 = -kappa_fs * 1.4426950408889634f;  // exp(-kappa k / fs) = 2^(kl2 k)
-  for (int k = w0 + tid; k < nISM; k += kTailThreads) {
-    double v = (double)h[k];
+  for (int k = w0 + lane; k < nISM; k += 32) {
+    const double v = (double)h[k];
     sh += v * v;
-    se += (double)ex2_fast(kl2 * (float)(k - w0));   // relative to w0; the common factor is restored below
+    se += (double)ex2_fast(kl2 * (float)(k - w0));    // relative to w0; the common factor is restored below
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = 16; o > 0; o >>= 1) {  // fixed butterfly, then lane 0's sums for everyone
     sh += __shfl_xor_sync(0xffffffffu, sh, o);
     se += __shfl_xor_sync(0xffffffffu, se, o);
   }
-  if ((tid & 31) == 0) { red_h[tid >> 5] = sh; red_e[tid >> 5] = se; }
-  __syncthreads();
-  if (tid == 0) {
-    double th = 0.0, te = 0.0;
-    for (int w = 0; w < kTailThreads / 32; w++) { th += red_h[w]; te += red_e[w]; }
-    te *= exp(-(double)kappa_fs * (double)w0);
-    double Aenv = (w0 < nISM && te > 0.0) ? th / te : 0.0;
-    // sqrt(P(k)) * sqrt(3)/pi * ln 2 = env0 * 2^(alpha (k - nISM)), alpha = -kappa_fs / (2 ln 2)
-    s_env0 = (float)(sqrt(Aenv * exp(-(double)kappa_fs * nISM)) * 0.5513288954217920495 * 0.69314718055994530942);
-    s_alpha = -kappa_fs * 0.72134752044448170368f;
-  }
-  __syncthreads();
-  const float env0 = s_env0, alpha = s_alpha;
+  sh = __shfl_sync(0xffffffffu, sh, 0);
+  se = __shfl_sync(0xffffffffu, se, 0);
+  se *= exp(-(double)kappa_fs * (double)w0);
+  const double Aenv = (w0 < nISM && se > 0.0) ? sh / se : 0.0;
+  // sqrt(P(k)) * sqrt(3)/pi * ln 2 = env0 * 2^(alpha (k - nISM)), alpha = -kappa_fs / (2 ln 2)
+  const float env0 = (float)(sqrt(Aenv * exp(-(double)kappa_fs * nISM)) * 0.5513288954217920495 *
+                             0.69314718055994530942);
+  const float alpha = -kappa_fs * 0.72134752044448170368f;
   const float rho = ex2_fast(alpha);  // envelope ratio between consecutive samples
 
-  // ---- tail samples: Philox blocks of 4 samples, kTailChunk / 4 blocks per CTA ----------
+  // ---- tail samples: Philox blocks of 4 samples ----------------------------------
   const long long q0 = (long long)(nISM >> 2);
   const long long qend = (long long)((nS + 3) >> 2);
   const PhiloxKey key = philox_key(make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32)));
@@ -103,7 +94,7 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A) {
   const long long qbeg = q0 + (long long)chunk * (kTailChunk / 4);
   const long long qlim = min(qend, qbeg + (long long)(kTailChunk / 4));
 #pragma unroll 2
-  for (long long q = qbeg + tid; q < qlim; q += kTailThreads) {
+  for (long long q = qbeg + lane; q < qlim; q += 32) {
     const uint4 ctr = make_uint4((uint32_t)q, (uint32_t)((unsigned long long)q >> 32), (uint32_t)rglob,
                                  (uint32_t)(rglob >> 32));
     const uint4 w = philox4x32_10(ctr, key);
@@ -134,9 +125,10 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A) {
   }
 }
 
-cudaError_t launch_tail(const TailArgs& A, long long nblocks, cudaStream_t stream) {
-  if (nblocks <= 0) return cudaSuccess;
-  tail_kernel<<<(unsigned)nblocks, kTailThreads, 0, stream>>>(A);
+cudaError_t launch_tail(const TailArgs& A, long long n_items, cudaStream_t stream) {
+  if (n_items <= 0) return cudaSuccess;
+  const long long per = kTailThreads / 32;
+  tail_kernel<<<(unsigned)((n_items + per - 1) / per), kTailThreads, 0, stream>>>(A, n_items);
   return cudaGetLastError();
 }
 
