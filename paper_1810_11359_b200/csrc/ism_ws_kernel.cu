@@ -72,17 +72,28 @@ struct WsStage {        // next work item's inputs, prefetched with cp.async by 
   int2 jt;               // (job, tile) of a batch work item
 };
 
+// Work order: items sorted heaviest-first are dealt from both ends (heavy, light, heavy, light, ...), so
+// each CTA alternates consumer-bound (many images) and producer-bound (few images, fixed per-tile cost)
+// tiles that its window buffers can smooth, while the last items handed out are medium-sized.
+__device__ __forceinline__ long long ws_order(long long wi, long long n) {
+#ifdef GPURIR_WS_HEAVY_FIRST
+  return wi;
+#else
+  return (wi & 1) ? n - 1 - (wi >> 1) : (wi >> 1);
+#endif
+}
+
 // Warp 0 of the producers: issue the asynchronous loads of work item wi's per-RIR inputs into stage.
 __device__ __forceinline__ void ws_prefetch(const IsmArgs& A, long long wi, long long n_work, WsStage& st, int lane) {
   if (lane == 0) st.wi = wi;
   if (wi >= n_work) return;
   if (A.jobs) {
-    int2 jt = A.tiles[wi];  // dependent: the job index selects the record to stage
+    int2 jt = A.tiles[ws_order(wi, n_work)];  // dependent: the job index selects the record to stage
     if (lane == 0) st.jt = jt;
     constexpr int n16 = (int)(sizeof(BatchJob) / 16);
     if (lane < n16) cp_async16(reinterpret_cast<char*>(&st.job) + 16 * lane, reinterpret_cast<const char*>(A.jobs + jt.x) + 16 * lane);
   } else {
-    const int m = (int)(wi % A.M);
+    const int m = (int)(ws_order(wi, n_work) % A.M);
     const int ms = m / A.M_rcv, mr = m % A.M_rcv;
     if (lane < 3) cp_async4(&st.pos[lane], A.pos_src + 3 * ms + lane);
     else if (lane < 6) cp_async4(&st.pos[lane], A.pos_rcv + 3 * mr + (lane - 3));
@@ -271,8 +282,9 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
               row = J.out_offset;
               geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.lb, J.neg, J.zero, T.g, A.status);
             } else {
-              tile = A.nTiles - 1 - (int)(wi / A.M);  // heaviest (latest) tiles first
-              m = (int)(wi % A.M);
+              const long long pos = ws_order(wi, n_work);
+              tile = A.nTiles - 1 - (int)(pos / A.M);  // position 0 = heaviest (latest) tile
+              m = (int)(pos % A.M);
               nISM = A.nISM;
               row = (long long)m * A.row_stride;
               geom_from(A.L, sm.stage.pos, sm.stage.pos + 3, A.orv ? sm.stage.pos + 6 : zero3, A.nb, A.pattern, A.lb,
