@@ -37,6 +37,12 @@ constexpr int kWsTC = kCW * kWsSub * kS;     // 512 samples per tile
 #ifndef GPURIR_WS_NBUF
 #define GPURIR_WS_NBUF 3
 #endif
+// setmaxnreg split of the per-CTA register pool (kPW, kCW warps; 0 disables):
+// kPW * PROD + kCW * CONS must equal (kPW + kCW) * 64.
+#ifndef GPURIR_WS_PROD_REGS
+#define GPURIR_WS_PROD_REGS 80
+#define GPURIR_WS_CONS_REGS 48
+#endif
 template <int MODE> struct WsCap { static constexpr int v = MODE == 1 ? GPURIR_WS_CAP / 2 : GPURIR_WS_CAP; };  // records per window
 constexpr int kWsColBatch = kPT;             // columns per enumeration batch
 constexpr int kBzMax = 1024;                 // z-factor table entries
@@ -171,6 +177,10 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
 
   if (warp < kPW) {
     // =========================== producers ===========================
+#if GPURIR_WS_PROD_REGS > 0
+    // rebalance the CTA's register pool: producers (fp64 image maths) up, consumers (FFMA2 loop) down
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(GPURIR_WS_PROD_REGS));
+#endif
     const int ptid = tid;
     const unsigned lt = (1u << lane) - 1u;
     const double fs_over_c = A.fs_over_c;
@@ -464,6 +474,9 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
     for (int w = max(0, win_i - kNBuf); w < win_i; w++) bar_sync(kBarEmpty0 + (w % kNBuf), kWsThreads);
   } else {
     // =========================== consumers ===========================
+#if GPURIR_WS_PROD_REGS > 0
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(GPURIR_WS_CONS_REGS));
+#endif
     const int cw = warp - kPW;
     const int grp = lane >> 3, li = lane & 7;
     int kfs[kWsSub];
