@@ -151,6 +151,7 @@ struct WsSmem {
   float4 sorted[kNBuf][MODE == 1 ? WsCap<MODE>::v + 8 : WsCap<MODE>::v / 2 + 8];
   int binstart[kNBuf][kMaxBins + 1];
   WinInfo win[kNBuf];
+  float2 cacc[kCW][kWsSub][32];  // consumer accumulators (kept in smem so the tap loop can unroll 4 pairs)
 };
 
 // z-axis factor of beta_n (C2): signed beta_z0^|floor(n/2)| beta_z1^|ceil(n/2)|
@@ -160,6 +161,38 @@ __device__ __forceinline__ float z_factor(int nz, const RirGeom& g) {
   float lz = axis_beta(nz, 2, g, sgn, zero);
   float v = zero ? 0.f : ex2_approx(lz);
   return sgn ? -v : v;
+}
+
+// Eqs. 5-6 for one lane over record pairs pp[0], pp[kG], ... < pend (see ism_kernel.cu for the derivation):
+// acc += C' w(u) / v, v = (k - x)/Hs, sigma = v^2 - rho^2 clamped <= 0, w = (sigma p(sigma))^2.
+struct TapConst {
+  float2 kv2, mr2, b3, b2, b1, b0;
+};
+__device__ __forceinline__ float2 tap_pair(const float4 p, const TapConst& K, float2 a2) {
+  float2 v = __fadd2_rn(K.kv2, make_float2(p.x, p.y));
+  float2 sg = __ffma2_rn(v, v, K.mr2);
+  sg.x = fminf(sg.x, 0.f); sg.y = fminf(sg.y, 0.f);
+  float2 q = __ffma2_rn(K.b3, sg, K.b2);
+  q = __ffma2_rn(q, sg, K.b1);
+  q = __ffma2_rn(q, sg, K.b0);
+  float2 c = __fmul2_rn(q, sg);
+  float2 w = __fmul2_rn(c, c);
+  float2 r = make_float2(rcp_approx(v.x), rcp_approx(v.y));
+  return __ffma2_rn(make_float2(p.z, p.w), __fmul2_rn(w, r), a2);
+}
+__device__ __forceinline__ float2 tap_loop(const float4* pp, const float4* pend, const TapConst& K, float2 a2) {
+  float2 a3 = make_float2(0.f, 0.f);  // second accumulator: two independent FFMA2 chains
+  for (; pp + 3 * kG < pend; pp += 4 * kG) {
+    const float4 p0 = pp[0], p1 = pp[kG], p2 = pp[2 * kG], p3 = pp[3 * kG];
+    a2 = tap_pair(p0, K, a2);
+    a3 = tap_pair(p1, K, a3);
+    a2 = tap_pair(p2, K, a2);
+    a3 = tap_pair(p3, K, a3);
+  }
+  for (; pp < pend; pp += kG) a2 = tap_pair(pp[0], K, a2);
+  a2.x += a3.x;
+  a2.y += a3.y;
+  return a2;
 }
 
 template <int MODE>
@@ -480,13 +513,9 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
 #endif
     const int cw = warp - kPW;
     const int grp = lane >> 3, li = lane & 7;
-    int kfs[kWsSub];
-    float2 acc[kWsSub];
+    float2 (*acc)[32] = sm.cacc[cw];
 #pragma unroll
-    for (int s = 0; s < kWsSub; s++) {
-      kfs[s] = (cw * kWsSub + s) * kS + li - kWsTC / 2;  // sample relative to the tile centre
-      acc[s] = make_float2(0.f, 0.f);
-    }
+    for (int s = 0; s < kWsSub; s++) acc[s][lane] = make_float2(0.f, 0.f);
     int win_i = 0;
     for (;;) {
       const int buf = win_i % kNBuf;
@@ -497,59 +526,29 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
         break;
       }
       const float4* sorted = sm.sorted[buf];
-#pragma unroll
+#pragma unroll 1
       for (int s = 0; s < kWsSub; s++) {
         const int sub = cw * kWsSub + s;
+        const int kf = sub * kS + li - kWsTC / 2;  // sample relative to the tile centre
         const int ra = sm.binstart[buf][sub], rb = sm.binstart[buf][min(sub + A.nbw, w.nbins)];
         if (MODE == 0) {
-          const float kv = (float)kfs[s] * A.invHs;
-          const float2 kv2 = make_float2(kv, kv);
-          const float2 mr2 = make_float2(-A.rho2, -A.rho2);
-          const float2 b3 = make_float2(A.wb[3], A.wb[3]), b2 = make_float2(A.wb[2], A.wb[2]);
-          const float2 b1 = make_float2(A.wb[1], A.wb[1]), b0 = make_float2(A.wb[0], A.wb[0]);
-          float2 a2 = acc[s];
-          int j = (ra & ~1) + 2 * grp;
-          for (; j + 2 * kG < rb; j += 4 * kG) {
-            float4 p0 = sorted[j >> 1];
-            float4 p1 = sorted[(j + 2 * kG) >> 1];
-            float2 v0 = __fadd2_rn(kv2, make_float2(p0.x, p0.y));
-            float2 v1 = __fadd2_rn(kv2, make_float2(p1.x, p1.y));
-            float2 s0 = __ffma2_rn(v0, v0, mr2);
-            float2 s1 = __ffma2_rn(v1, v1, mr2);
-            s0.x = fminf(s0.x, 0.f); s0.y = fminf(s0.y, 0.f);
-            s1.x = fminf(s1.x, 0.f); s1.y = fminf(s1.y, 0.f);
-            float2 q0 = __ffma2_rn(b3, s0, b2), q1 = __ffma2_rn(b3, s1, b2);
-            q0 = __ffma2_rn(q0, s0, b1); q1 = __ffma2_rn(q1, s1, b1);
-            q0 = __ffma2_rn(q0, s0, b0); q1 = __ffma2_rn(q1, s1, b0);
-            float2 c0 = __fmul2_rn(q0, s0), c1 = __fmul2_rn(q1, s1);
-            float2 w0 = __fmul2_rn(c0, c0), w1 = __fmul2_rn(c1, c1);
-            float2 r0 = make_float2(rcp_approx(v0.x), rcp_approx(v0.y));
-            float2 r1 = make_float2(rcp_approx(v1.x), rcp_approx(v1.y));
-            a2 = __ffma2_rn(make_float2(p0.z, p0.w), __fmul2_rn(w0, r0), a2);
-            a2 = __ffma2_rn(make_float2(p1.z, p1.w), __fmul2_rn(w1, r1), a2);
-          }
-          if (j < rb) {
-            float4 p0 = sorted[j >> 1];
-            float2 v0 = __fadd2_rn(kv2, make_float2(p0.x, p0.y));
-            float2 s0 = __ffma2_rn(v0, v0, mr2);
-            s0.x = fminf(s0.x, 0.f); s0.y = fminf(s0.y, 0.f);
-            float2 q0 = __ffma2_rn(b3, s0, b2);
-            q0 = __ffma2_rn(q0, s0, b1);
-            q0 = __ffma2_rn(q0, s0, b0);
-            float2 c0 = __fmul2_rn(q0, s0);
-            float2 w0 = __fmul2_rn(c0, c0);
-            float2 r0 = make_float2(rcp_approx(v0.x), rcp_approx(v0.y));
-            a2 = __ffma2_rn(make_float2(p0.z, p0.w), __fmul2_rn(w0, r0), a2);
-          }
-          acc[s] = a2;
+          TapConst K;
+          const float kv = (float)kf * A.invHs;
+          K.kv2 = make_float2(kv, kv);
+          K.mr2 = make_float2(-A.rho2, -A.rho2);
+          K.b3 = make_float2(A.wb[3], A.wb[3]); K.b2 = make_float2(A.wb[2], A.wb[2]);
+          K.b1 = make_float2(A.wb[1], A.wb[1]); K.b0 = make_float2(A.wb[0], A.wb[0]);
+          const float4* pp = sorted + ((ra & ~1) >> 1) + grp;  // record pairs, group grp, stride kG
+          const float4* pend = sorted + ((rb + 1) >> 1);
+          acc[s][lane] = tap_loop(pp, pend, K, acc[s][lane]);
         } else if (MODE == 2) {
-          const float kx = (float)kfs[s] * (0.5f * A.invHs);
+          const float kx = (float)kf * (0.5f * A.invHs);
           const float2 kx2 = make_float2(kx, kx);
           const __half2 c6 = __float2half2_rn(A.hc[2]), c4 = __float2half2_rn(A.hc[1]);
           const __half2 c2 = __float2half2_rn(A.hc[0]), c0 = __float2half2_rn(1.f);
           const __half2 xcl = __float2half2_rn(A.x2clamp);
           __half2 acch = __float2half2_rn(0.f);
-          float2 a2 = acc[s];
+          float2 a2 = acc[s][lane];
           int steps = 0;
           for (int j = (ra & ~1) + 2 * grp; j < rb; j += 2 * kG) {
             float4 pr = sorted[j >> 1];
@@ -572,30 +571,32 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
           }
           float2 f = __half22float2(acch);
           a2.x += f.x; a2.y += f.y;
-          acc[s] = a2;
+          acc[s][lane] = a2;
         } else {
-          float a = acc[s].x;
+          float a = acc[s][lane].x;
           for (int j = ra + grp; j < rb; j += kG) {
             float4 rc = sorted[j];
-            int idx = __float_as_int(rc.x) + kfs[s];
+            int idx = __float_as_int(rc.x) + kf;
             float2 d = lut[idx];
             a = fmaf(rc.z, fmaf(rc.y, d.y, d.x), a);
           }
-          acc[s].x = a;
+          acc[s][lane].x = a;
         }
       }
       bar_arrive(kBarEmpty0 + buf, kWsThreads);  // buffer consumed
       if (w.flags & kWinLast) {
 #pragma unroll
         for (int s = 0; s < kWsSub; s++) {
-          float a = acc[s].x + acc[s].y;
+          const float2 as = acc[s][lane];
+          float a = as.x + as.y;
           a += __shfl_xor_sync(0xffffffffu, a, 8);
           a += __shfl_xor_sync(0xffffffffu, a, 16);
-          if (MODE == 0) { if (kfs[s] & 1) a = -a; }
-          else if (MODE == 2) { a *= (1.f / 1024.f); if (kfs[s] & 1) a = -a; }
+          const int kf = (cw * kWsSub + s) * kS + li - kWsTC / 2;
+          if (MODE == 0) { if (kf & 1) a = -a; }
+          else if (MODE == 2) { a *= (1.f / 1024.f); if (kf & 1) a = -a; }
           const int k = w.t0 + (cw * kWsSub + s) * kS + li;
           if (grp == 0 && k < w.te) A.out[w.row + k] = a;
-          acc[s] = make_float2(0.f, 0.f);
+          acc[s][lane] = make_float2(0.f, 0.f);
         }
       }
       win_i++;
