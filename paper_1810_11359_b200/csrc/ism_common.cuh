@@ -86,4 +86,36 @@ __device__ __forceinline__ void z_range(const RirGeom& g, double invLz, double l
 }
 
 
+// Eqs. 5-6 for one lane over record pairs pp[0], pp[kG], ... < pend (see ism_kernel.cu for the derivation):
+// acc += C' w(u) / v, v = (k - x)/Hs, sigma = v^2 - rho^2 clamped <= 0, w = (sigma p(sigma))^2.
+struct TapConst {
+  float2 kv2, mr2, b3, b2, b1, b0;
+};
+__device__ __forceinline__ float2 tap_pair(const float4 p, const TapConst& K, float2 a2) {
+  float2 v = __fadd2_rn(K.kv2, make_float2(p.x, p.y));
+  float2 sg = __ffma2_rn(v, v, K.mr2);
+  sg.x = fminf(sg.x, 0.f); sg.y = fminf(sg.y, 0.f);
+  float2 q = __ffma2_rn(K.b3, sg, K.b2);
+  q = __ffma2_rn(q, sg, K.b1);
+  q = __ffma2_rn(q, sg, K.b0);
+  float2 c = __fmul2_rn(q, sg);
+  float2 w = __fmul2_rn(c, c);
+  float2 r = make_float2(rcp_approx(v.x), rcp_approx(v.y));
+  return __ffma2_rn(make_float2(p.z, p.w), __fmul2_rn(w, r), a2);
+}
+__device__ __forceinline__ float2 tap_loop(const float4* pp, const float4* pend, const TapConst& K, float2 a2) {
+  float2 a3 = make_float2(0.f, 0.f);  // second accumulator: two independent FFMA2 chains
+  for (; pp + 3 * kG < pend; pp += 4 * kG) {
+    const float4 p0 = pp[0], p1 = pp[kG], p2 = pp[2 * kG], p3 = pp[3 * kG];
+    a2 = tap_pair(p0, K, a2);
+    a3 = tap_pair(p1, K, a3);
+    a2 = tap_pair(p2, K, a2);
+    a3 = tap_pair(p3, K, a3);
+  }
+  for (; pp < pend; pp += kG) a2 = tap_pair(pp[0], K, a2);
+  a2.x += a3.x;
+  a2.y += a3.y;
+  return a2;
+}
+
 }  // namespace gpurir

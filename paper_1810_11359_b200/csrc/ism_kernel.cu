@@ -234,46 +234,15 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
       const int ra = sm.binstart[sub], rb = sm.binstart[min(sub + A.nbw, nbins)];
       if (MODE == 0) {
         // Eq. 5-6: acc += C' w(u) / v, v = (k - x)/Hs, w = Hann window (R5), C' = -A sin(pi f)/(pi Hs)
+        TapConst K;
         const float kv = (float)kfs[s] * A.invHs;
-        const float2 kv2 = make_float2(kv, kv);
-        const float2 mr2 = make_float2(-A.rho2, -A.rho2);
-        const float2 b3 = make_float2(A.wb[3], A.wb[3]), b2 = make_float2(A.wb[2], A.wb[2]);
-        const float2 b1 = make_float2(A.wb[1], A.wb[1]), b0 = make_float2(A.wb[0], A.wb[0]);
-        float2 a2 = acc[s];
-        int j = (ra & ~1) + 2 * grp;
-        for (; j + 2 * kG < rb; j += 4 * kG) {  // two independent pairs per iteration (ILP)
-          float4 p0 = sm.sorted[j >> 1];
-          float4 p1 = sm.sorted[(j + 2 * kG) >> 1];
-          float2 v0 = __fadd2_rn(kv2, make_float2(p0.x, p0.y));
-          float2 v1 = __fadd2_rn(kv2, make_float2(p1.x, p1.y));
-          float2 s0 = __ffma2_rn(v0, v0, mr2);
-          float2 s1 = __ffma2_rn(v1, v1, mr2);
-          s0.x = fminf(s0.x, 0.f); s0.y = fminf(s0.y, 0.f);
-          s1.x = fminf(s1.x, 0.f); s1.y = fminf(s1.y, 0.f);
-          float2 q0 = __ffma2_rn(b3, s0, b2), q1 = __ffma2_rn(b3, s1, b2);
-          q0 = __ffma2_rn(q0, s0, b1); q1 = __ffma2_rn(q1, s1, b1);
-          q0 = __ffma2_rn(q0, s0, b0); q1 = __ffma2_rn(q1, s1, b0);
-          float2 c0 = __fmul2_rn(q0, s0), c1 = __fmul2_rn(q1, s1);
-          float2 w0 = __fmul2_rn(c0, c0), w1 = __fmul2_rn(c1, c1);
-          float2 r0 = make_float2(rcp_approx(v0.x), rcp_approx(v0.y));
-          float2 r1 = make_float2(rcp_approx(v1.x), rcp_approx(v1.y));
-          a2 = __ffma2_rn(make_float2(p0.z, p0.w), __fmul2_rn(w0, r0), a2);
-          a2 = __ffma2_rn(make_float2(p1.z, p1.w), __fmul2_rn(w1, r1), a2);
-        }
-        if (j < rb) {
-          float4 p0 = sm.sorted[j >> 1];
-          float2 v0 = __fadd2_rn(kv2, make_float2(p0.x, p0.y));
-          float2 s0 = __ffma2_rn(v0, v0, mr2);
-          s0.x = fminf(s0.x, 0.f); s0.y = fminf(s0.y, 0.f);
-          float2 q0 = __ffma2_rn(b3, s0, b2);
-          q0 = __ffma2_rn(q0, s0, b1);
-          q0 = __ffma2_rn(q0, s0, b0);
-          float2 c0 = __fmul2_rn(q0, s0);
-          float2 w0 = __fmul2_rn(c0, c0);
-          float2 r0 = make_float2(rcp_approx(v0.x), rcp_approx(v0.y));
-          a2 = __ffma2_rn(make_float2(p0.z, p0.w), __fmul2_rn(w0, r0), a2);
-        }
-        acc[s] = a2;
+        K.kv2 = make_float2(kv, kv);
+        K.mr2 = make_float2(-A.rho2, -A.rho2);
+        K.b3 = make_float2(A.wb[3], A.wb[3]); K.b2 = make_float2(A.wb[2], A.wb[2]);
+        K.b1 = make_float2(A.wb[1], A.wb[1]); K.b0 = make_float2(A.wb[0], A.wb[0]);
+        const float4* pp = sm.sorted + ((ra & ~1) >> 1) + grp;  // record pairs, group grp, stride kG
+        const float4* pend = sm.sorted + ((rb + 1) >> 1);
+        acc[s] = tap_loop(pp, pend, K, acc[s]);
       } else if (MODE == 2) {
         // fp16 / half2: t - tau in fp32, window by the Eq. 11 polynomial
         // cos(pi x) at x = u / (2H) (reading C12), half2 Horner (Eq. 12), fp32 accumulation (C13).
