@@ -1,6 +1,8 @@
 // ism_common.cuh — device helpers shared by the ISM kernels (ism_kernel.cu, ism_ws_kernel.cu).
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -115,6 +117,47 @@ __device__ __forceinline__ float2 tap_loop(const float4* pp, const float4* pend,
   for (; pp < pend; pp += kG) a2 = tap_pair(pp[0], K, a2);
   a2.x += a3.x;
   a2.y += a3.y;
+  return a2;
+}
+
+// fp16 / half2 mode: t - tau in fp32, Hann window by the Eq. 11 polynomial cos(pi x)
+// at x = u / (2H) (reading C12) in half2 Horner (Eq. 12), the bounded product C/x in fp32 -> half2,
+// half2 partial sums flushed to fp32 every 4 unrolled iterations (reading C13).
+struct TapConstH {
+  float2 kx2;
+  __half2 c6, c4, c2, c0, xcl;
+};
+__device__ __forceinline__ __half2 tap_pair_h(const float4 p, const TapConstH& K, __half2 acch) {
+  const float2 x = __fadd2_rn(K.kx2, make_float2(p.x, p.y));  // x' = (k - tau fs) / (2 Hs), fp32
+  const __half2 hx = __float22half2_rn(x);
+  const __half2 x2 = __hmin2(__hmul2(hx, hx), K.xcl);         // clamp at the window edge |u/(2H)| = 1/2
+  __half2 q = __hfma2(K.c6, x2, K.c4);
+  q = __hfma2(q, x2, K.c2);
+  q = __hfma2(q, x2, K.c0);                                    // cos(pi x), Eq. 11
+  const __half2 w = __hmul2(q, q);                             // Hann window
+  const float2 r = make_float2(rcp_approx(x.x), rcp_approx(x.y));
+  const float2 cq = __fmul2_rn(make_float2(p.z, p.w), r);     // bounded by ~A (scaled 2^10)
+  return __hfma2(w, __float22half2_rn(cq), acch);
+}
+__device__ __forceinline__ float2 tap_loop_h(const float4* pp, const float4* pend, const TapConstH& K, float2 a2) {
+  const __half2 z = __float2half2_rn(0.f);
+  int it = 0;
+  __half2 h0 = z, h1 = z;
+  for (; pp + 3 * kG < pend; pp += 4 * kG) {
+    const float4 p0 = pp[0], p1 = pp[kG], p2 = pp[2 * kG], p3 = pp[3 * kG];
+    h0 = tap_pair_h(p0, K, h0);
+    h1 = tap_pair_h(p1, K, h1);
+    h0 = tap_pair_h(p2, K, h0);
+    h1 = tap_pair_h(p3, K, h1);
+    if (++it == 4) {  // at most 8 half2 products per partial sum
+      const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+      a2.x += f0.x + f1.x; a2.y += f0.y + f1.y;
+      h0 = z; h1 = z; it = 0;
+    }
+  }
+  for (; pp < pend; pp += kG) h0 = tap_pair_h(pp[0], K, h0);
+  const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+  a2.x += f0.x + f1.x; a2.y += f0.y + f1.y;
   return a2;
 }
 

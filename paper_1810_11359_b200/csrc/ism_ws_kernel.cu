@@ -510,36 +510,15 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
           const float4* pend = sorted + ((rb + 1) >> 1);
           acc[s][lane] = tap_loop(pp, pend, K, acc[s][lane]);
         } else if (MODE == 2) {
+          TapConstH K;
           const float kx = (float)kf * (0.5f * A.invHs);
-          const float2 kx2 = make_float2(kx, kx);
-          const __half2 c6 = __float2half2_rn(A.hc[2]), c4 = __float2half2_rn(A.hc[1]);
-          const __half2 c2 = __float2half2_rn(A.hc[0]), c0 = __float2half2_rn(1.f);
-          const __half2 xcl = __float2half2_rn(A.x2clamp);
-          __half2 acch = __float2half2_rn(0.f);
-          float2 a2 = acc[s][lane];
-          int steps = 0;
-          for (int j = (ra & ~1) + 2 * grp; j < rb; j += 2 * kG) {
-            float4 pr = sorted[j >> 1];
-            float2 x = __fadd2_rn(kx2, make_float2(pr.x, pr.y));
-            __half2 hx = __float22half2_rn(x);
-            __half2 x2 = __hmin2(__hmul2(hx, hx), xcl);
-            __half2 p = __hfma2(c6, x2, c4);
-            p = __hfma2(p, x2, c2);
-            p = __hfma2(p, x2, c0);
-            __half2 wv = __hmul2(p, p);
-            float2 r = make_float2(rcp_approx(x.x), rcp_approx(x.y));
-            float2 q = __fmul2_rn(make_float2(pr.z, pr.w), r);
-            acch = __hfma2(wv, __float22half2_rn(q), acch);
-            if (++steps == 8) {
-              float2 f = __half22float2(acch);
-              a2.x += f.x; a2.y += f.y;
-              acch = __float2half2_rn(0.f);
-              steps = 0;
-            }
-          }
-          float2 f = __half22float2(acch);
-          a2.x += f.x; a2.y += f.y;
-          acc[s][lane] = a2;
+          K.kx2 = make_float2(kx, kx);
+          K.c6 = __float2half2_rn(A.hc[2]); K.c4 = __float2half2_rn(A.hc[1]);
+          K.c2 = __float2half2_rn(A.hc[0]); K.c0 = __float2half2_rn(1.f);
+          K.xcl = __float2half2_rn(A.x2clamp);
+          const float4* pp = sorted + ((ra & ~1) >> 1) + grp;
+          const float4* pend = sorted + ((rb + 1) >> 1);
+          acc[s][lane] = tap_loop_h(pp, pend, K, acc[s][lane]);
         } else {
           float a = acc[s][lane].x;
           for (int j = ra + grp; j < rb; j += kG) {
