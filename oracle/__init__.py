@@ -84,6 +84,8 @@ def lib():
         L.oracle_lut_lookup.argtypes = [dp, C.c_long, C.c_int, C.c_double, C.c_double]
         L.oracle_logistic_stream.restype = None
         L.oracle_logistic_stream.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_long, dp]
+        L.oracle_simulate_trajectory.restype = C.c_int
+        L.oracle_simulate_trajectory.argtypes = [dp, C.c_long, dp, C.c_int, C.c_int, C.c_long, dp]
         L.oracle_sin_pi_poly.restype = C.c_double
         L.oracle_sin_pi_poly.argtypes = [C.c_double]
         L.oracle_cos_pi_poly.restype = C.c_double
@@ -206,6 +208,20 @@ def simulate_rir(room, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs=16000.0, 
                                    int(bool(dense)), int(nthreads), _dp(out))
     if st != 0:
         raise OracleError(st, "simulate_rir")
+    return out
+
+
+def simulate_trajectory(signal, rirs) -> np.ndarray:
+    """NEXT row f1: moving source through per-point RIR banks rirs [n_points][n_mics][L]."""
+    sig = _d(signal).reshape(-1)
+    R = _d(rirs)
+    if R.ndim != 3:
+        raise ValueError("rirs must be [n_points][n_mics][L]")
+    P_, M, L = R.shape
+    out = np.zeros((M, sig.size + L - 1))
+    st = lib().oracle_simulate_trajectory(_dp(sig), sig.size, _dp(R), P_, M, L, _dp(out))
+    if st != 0:
+        raise OracleError(st, "simulate_trajectory")
     return out
 
 

@@ -417,3 +417,32 @@ double oracle_cos_pi_poly(double x) {
 void oracle_logistic_stream(uint64_t seed, uint64_t r, uint64_t k0, long n, double* out) {
   for (long i = 0; i < n; i++) out[i] = oracle_logistic(oracle_uniform(seed, r, k0 + (uint64_t)i));
 }
+
+/* ------------------------------------------------------------------ */
+/* NEXT row f1 (§3.4): a moving */
+/* source recorded by a microphone array.  The source signal is split  */
+/* into n_points contiguous segments of floor(n_sig / n_points) samples */
+/* (the last takes the remainder; reading R7 = SPEC S:414); segment p   */
+/* is filtered by the RIRs of trajectory point p and the filtered       */
+/* segments are overlap-added at their offsets:                 */
+/*   out[m][t] = sum_j sig[j] rir[p(j)][m][t - j], 0 <= t - j < L,      */
+/*   0 <= t < n_sig + L - 1.  rirs: [n_points][n_mics][L].              */
+/* Direct time-domain convolution in double (the plain definition).    */
+/* ------------------------------------------------------------------ */
+int oracle_simulate_trajectory(const double* sig, long n_sig, const double* rirs, int n_points, int n_mics,
+                               long L, double* out) {
+  if (n_sig <= 0 || n_points <= 0 || n_mics <= 0 || L <= 0 || n_sig < n_points) return OR_EINVAL;
+  long seglen = n_sig / n_points;
+  long n_out = n_sig + L - 1;
+  for (long i = 0; i < (long)n_mics * n_out; i++) out[i] = 0.0;
+  for (int m = 0; m < n_mics; m++) {
+    double* o = out + (size_t)m * n_out;
+    for (long j = 0; j < n_sig; j++) {
+      long p = j / seglen;
+      if (p > n_points - 1) p = n_points - 1;
+      const double* h = rirs + ((size_t)p * n_mics + m) * L;
+      for (long tau = 0; tau < L; tau++) o[j + tau] += sig[j] * h[tau];
+    }
+  }
+  return OR_OK;
+}

@@ -396,3 +396,38 @@ def test_sin_cos_polynomials(oracle):
     # printed coefficients are exactly representable in fp16
     for c in (2.326171875, -5.14453125, 3.140625, -1.2294921875, 4.04296875, -4.93359375):
         assert float(np.float16(c)) == c
+
+
+# ---------------------------------------------------------------- NEXT f1: trajectory filtering
+
+def test_trajectory_single_point_equals_numpy_convolve(oracle):
+    """One trajectory point: plain filtering, pinned by numpy's convolution (library routine)."""
+    rng = np.random.default_rng(8)
+    sig = rng.standard_normal(1001)
+    rirs = rng.standard_normal((1, 3, 257))
+    out = oracle.simulate_trajectory(sig, rirs)
+    for m in range(3):
+        assert np.allclose(out[m], np.convolve(sig, rirs[0, m]), rtol=0, atol=1e-11)
+
+
+def test_trajectory_impulses_and_segments(oracle):
+    """S:396-397 impulse RIRs give identity / delay; S:406 identical RIRs on every point = single point;
+    S:407 scaled impulse scales the output; segment p uses point p's bank (remainder to the last)."""
+    rng = np.random.default_rng(9)
+    sig = rng.standard_normal(103)
+    L = 9
+    rir = np.zeros((1, 2, L)); rir[0, 0, 0] = 1.0; rir[0, 1, 4] = 0.5
+    out = oracle.simulate_trajectory(sig, rir)
+    assert np.array_equal(out[0, :103], sig) and np.all(out[0, 103:] == 0)
+    assert np.allclose(out[1, 4:107], 0.5 * sig, atol=0)
+    same = np.repeat(rng.standard_normal((1, 2, L)), 5, axis=0)
+    assert np.allclose(oracle.simulate_trajectory(sig, same), oracle.simulate_trajectory(sig, same[:1]), atol=1e-12)
+    # 103 samples, 5 points: segments of 20, last one 23 samples; point p = delta at delay p
+    rir5 = np.zeros((5, 1, L))
+    for p in range(5):
+        rir5[p, 0, p] = 1.0
+    out5 = oracle.simulate_trajectory(sig, rir5)[0]
+    ref = np.zeros(103 + L - 1)
+    for j in range(103):
+        ref[j + min(j // 20, 4)] += sig[j]
+    assert np.array_equal(out5, ref)
