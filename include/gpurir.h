@@ -126,6 +126,21 @@ typedef struct {
 int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, float* out,
                               const gpurir_opts* opts);
 
+/*
+ * gpurir_simulate_trajectory — a moving source recorded by a microphone array (§3.4,
+ * P:225-227; the trajectory-filtering function of P:276).
+ *   signal  device float[n_sig]                      mono source signal
+ *   rirs    device float[n_points][n_mics][rir_len]   RIR bank of every trajectory point (e.g. from
+ *                                                     gpurir_simulate_rir with the points as sources)
+ *   out     device float[n_mics][n_sig + rir_len - 1], caller-owned
+ * The signal is split into n_points contiguous segments of floor(n_sig / n_points) samples (the last one
+ * takes the remainder; reading R7); segment p is filtered by point p's RIRs and the filtered segments
+ * are overlap-added: out[m][t] = sum_j signal[j] rirs[p(j)][m][t - j].  Direct fp32 convolution,
+ * deterministic.  Errors: EINVAL (n_sig < n_points, sizes <= 0, NULL pointers).
+ */
+int gpurir_simulate_trajectory(const float* signal, long long n_sig, const float* rirs, int n_points, int n_mics,
+                               long long rir_len, float* out, const gpurir_opts* opts);
+
 /* Number of samples ceil(T fs) under reading C9 (a product within 1e-6 of an integer from above
  * counts as that integer). */
 long long gpurir_nsamples(double T, double fs);

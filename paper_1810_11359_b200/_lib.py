@@ -21,6 +21,7 @@ EXPORTS = [
     "gpurir_opts_default", "gpurir_simulate_rir", "gpurir_simulate_rir_batch", "gpurir_nsamples",
     "gpurir_sabine_t60", "gpurir_beta_sabine", "gpurir_att2t_sabine", "gpurir_t2n", "gpurir_image_params",
     "gpurir_lut_table", "gpurir_device_status", "gpurir_strerror", "gpurir_last_cuda_error", "gpurir_version",
+    "gpurir_simulate_trajectory",
 ]
 
 
@@ -64,6 +65,8 @@ def lib() -> C.CDLL:
                                       C.c_double, C.c_double, vp, C.POINTER(Opts)]
     L.gpurir_simulate_rir_batch.restype = C.c_int
     L.gpurir_simulate_rir_batch.argtypes = [C.c_int, C.POINTER(Room), C.c_double, C.c_double, vp, C.POINTER(Opts)]
+    L.gpurir_simulate_trajectory.restype = C.c_int
+    L.gpurir_simulate_trajectory.argtypes = [vp, C.c_longlong, vp, C.c_int, C.c_int, C.c_longlong, vp, C.POINTER(Opts)]
     L.gpurir_nsamples.restype = C.c_longlong
     L.gpurir_nsamples.argtypes = [C.c_double, C.c_double]
     L.gpurir_sabine_t60.restype = C.c_double

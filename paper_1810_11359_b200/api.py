@@ -139,6 +139,28 @@ def simulate_rir_batch(rooms, fs, out, c=343.0, mode="fp32", Tw=4e-3, lut_Q=16, 
     return out
 
 
+def simulate_trajectory(signal, rirs, out=None, stream=None, sync=False):
+    """gpurir_simulate_trajectory: filter a mono `signal` [n_sig] (CUDA float32) through the per-point RIR
+    banks `rirs` [n_points][n_mics][L] of a source trajectory; returns [n_mics][n_sig + L - 1]."""
+    import torch
+    signal = signal.reshape(-1)
+    if not (isinstance(signal, torch.Tensor) and signal.is_cuda and signal.dtype == torch.float32):
+        raise TypeError("signal must be a CUDA float32 tensor")
+    if not (isinstance(rirs, torch.Tensor) and rirs.is_cuda and rirs.dtype == torch.float32 and rirs.dim() == 3):
+        raise TypeError("rirs must be a CUDA float32 tensor [n_points, n_mics, L]")
+    signal = signal.contiguous()
+    rirs = rirs.contiguous()
+    n_points, n_mics, L = rirs.shape
+    n_out = signal.numel() + L - 1
+    if out is None:
+        out = torch.empty((n_mics, n_out), dtype=torch.float32, device=signal.device)
+    o = make_opts(stream=stream, sync=sync)
+    st = lib().gpurir_simulate_trajectory(signal.data_ptr(), signal.numel(), rirs.data_ptr(), n_points, n_mics, L,
+                                          out.data_ptr(), C.byref(o))
+    check(st, "gpurir_simulate_trajectory")
+    return out
+
+
 # ---- host helpers (P:276) ------------------------------------------------------------------
 
 def sabine_t60(room_sz, beta) -> float:

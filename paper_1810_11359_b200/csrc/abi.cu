@@ -458,6 +458,21 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
   return finish(o, stream, d);
 }
 
+int gpurir_simulate_trajectory(const float* signal, long long n_sig, const float* rirs, int n_points, int n_mics,
+                               long long rir_len, float* out, const gpurir_opts* opts) {
+  gpurir_opts o;
+  if (opts) o = *opts; else gpurir_opts_default(&o);
+  if (!signal || !rirs || !out || n_sig <= 0 || n_points <= 0 || n_mics <= 0 || rir_len <= 0) return GPURIR_EINVAL;
+  if (n_sig < n_points || n_mics > 65535 || n_sig + rir_len > (1LL << 40)) return GPURIR_EINVAL;
+  cudaStream_t stream = (cudaStream_t)o.stream;
+  cudaError_t e = launch_traj(signal, n_sig, rirs, n_points, n_mics, rir_len, out, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "launch_traj");
+  int st = GPURIR_OK;
+  DeviceState* d = device_state(&st);
+  if (!d) return st;
+  return finish(o, stream, d);
+}
+
 int gpurir_image_params(const float room_sz[3], const float beta[6], const float src[3], const float rcv[3],
                         const float orv[3], int mic_pattern, const int nb_img[3], double fs, double c,
                         double* x_out, float* A_out, void* stream_) {

@@ -90,6 +90,9 @@ cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* cou
                           cudaStream_t stream);
 cudaError_t launch_tail(const TailArgs& A, long long n_items, cudaStream_t stream);  // one warp per item
 
+cudaError_t launch_traj(const float* sig, long long n_sig, const float* rirs, int n_points, int n_mics, long long L,
+                        float* out, cudaStream_t stream);
+
 constexpr int kTailThreads = 256;
 constexpr int kTailChunk = kTailThreads * 64;  // samples per tail CTA (up to 16 Philox blocks per thread)
 

@@ -297,3 +297,55 @@ def test_batch_rooms_vs_oracle(P, oracle):
         g = o[off:off + r.size]
         off += r.size
         assert rel_err(g, r)[0] <= TOL["fp32"], i
+
+
+# ---------------------------------------------------------------- NEXT row f1: trajectory filtering
+
+TRAJ_TOL = 2e-5  # fp32 accumulation of up to L products per output sample (reading R8)
+
+
+@pytest.mark.parametrize("n_sig,n_points,n_mics,L", [(5003, 7, 3, 1337), (4096, 1, 2, 4096), (777, 777, 1, 64),
+                                                     (10007, 13, 4, 1), (2500, 3, 5, 5000)])
+def test_trajectory_vs_oracle(P, oracle, n_sig, n_points, n_mics, L):
+    import torch
+    rng = np.random.default_rng(n_sig + L)
+    sig = rng.standard_normal(n_sig).astype(np.float32)
+    rirs = (rng.standard_normal((n_points, n_mics, L)) * np.exp(-np.arange(L) / max(L / 4, 1))).astype(np.float32)
+    g = P.simulate_trajectory(torch.from_numpy(sig).cuda(), torch.from_numpy(rirs).cuda(), sync=True).cpu().numpy()
+    r = oracle.simulate_trajectory(sig, rirs)
+    assert g.shape == r.shape == (n_mics, n_sig + L - 1)
+    assert np.max(np.abs(g - r)) <= TRAJ_TOL * np.max(np.abs(r))
+
+
+def test_trajectory_moving_source_with_oracle_rirs(P, oracle):
+    """A source moving across a 3x4x2.5 room, 6 trajectory points x 4 mics, RIR banks from the oracle."""
+    import torch
+    room = np.float32([3, 4, 2.5])
+    beta, _ = oracle.beta_sabine(room, 0.4)
+    beta = beta.astype(np.float32)
+    pts = np.float32([[0.5 + 0.35 * i, 1.0 + 0.2 * i, 1.2] for i in range(6)])
+    mics = np.float32([[2.0, 2.5, 1.3], [2.1, 2.5, 1.3], [2.0, 2.6, 1.3], [2.1, 2.6, 1.3]])
+    nb = oracle.t2n(0.06, room)
+    rirs = oracle.simulate_rir(room, beta, pts, mics, nb, 0.06, 0.06).astype(np.float32)  # [6][4][960]
+    sig = np.random.default_rng(3).standard_normal(16000).astype(np.float32)
+    g = P.simulate_trajectory(torch.from_numpy(sig).cuda(), torch.from_numpy(rirs).cuda(), sync=True).cpu().numpy()
+    r = oracle.simulate_trajectory(sig, rirs)
+    assert np.max(np.abs(g - r)) <= TRAJ_TOL * np.max(np.abs(r))
+
+
+def test_trajectory_impulse_is_exact(P):
+    import torch
+    sig = torch.randn(3001, device="cuda")
+    rirs = torch.zeros((3, 2, 50), device="cuda")
+    rirs[:, 0, 0] = 1.0
+    rirs[:, 1, 7] = 1.0
+    out = P.simulate_trajectory(sig, rirs, sync=True)
+    assert torch.equal(out[0, :3001], sig)
+    assert torch.equal(out[1, 7:3008], sig)
+    assert torch.all(out[0, 3001:] == 0) and torch.all(out[1, :7] == 0)
+
+
+def test_trajectory_invalid(P):
+    import torch
+    with pytest.raises(P.GpurirError):
+        P.simulate_trajectory(torch.randn(3, device="cuda"), torch.zeros((5, 1, 4), device="cuda"))

@@ -126,6 +126,16 @@ def main():
                      samples=off, host_plan_s=plan_s,
                      note="time includes the call's host planning + job-table upload (batch API synchronises)"))
     emit(rows[-1])
+    # NEXT row f1: moving source, 1 s at 16 kHz, 100 trajectory points x 32 mics, 0.7 s RIRs (cfg3 length)
+    n_sig, n_pts, n_mics, L = 16000, 100, 32, 11200
+    sig = torch.randn(n_sig, device=dev)
+    rirs = torch.randn((n_pts, n_mics, L), device=dev) * 1e-2
+    outb = torch.empty((n_mics, n_sig + L - 1), device=dev)
+    ms = time_call(lambda: P.simulate_trajectory(sig, rirs, out=outb), reps=5, warm=2)
+    macs = n_sig * L * n_mics
+    rows.append(dict(cfg="traj_f1", n_sig=n_sig, points=n_pts, mics=n_mics, L=L, ms=ms, macs=macs,
+                     fma_per_s=macs / ms * 1e3, frac_fp32_fma_peak=macs / ms * 1e3 / (148 * 128 * 1.965e9)))
+    emit(rows[-1])
     emit({"summary": True, "device": torch.cuda.get_device_name(0), "rows": len(rows)})
 
 
