@@ -154,6 +154,8 @@ def simulate_trajectory(signal, rirs, out=None, stream=None, sync=False):
     n_out = signal.numel() + L - 1
     if out is None:
         out = torch.empty((n_mics, n_out), dtype=torch.float32, device=signal.device)
+    elif not (out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and tuple(out.shape) == (n_mics, n_out)):
+        raise TypeError(f"out must be a contiguous CUDA float32 tensor of shape {(n_mics, n_out)}")
     o = make_opts(stream=stream, sync=sync)
     st = lib().gpurir_simulate_trajectory(signal.data_ptr(), signal.numel(), rirs.data_ptr(), n_points, n_mics, L,
                                           out.data_ptr(), C.byref(o))

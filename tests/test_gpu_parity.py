@@ -305,7 +305,8 @@ TRAJ_TOL = 2e-5  # fp32 accumulation of up to L products per output sample (DESI
 
 
 @pytest.mark.parametrize("n_sig,n_points,n_mics,L", [(5003, 7, 3, 1337), (4096, 1, 2, 4096), (777, 777, 1, 64),
-                                                     (10007, 13, 4, 1), (2500, 3, 5, 5000)])
+                                                     (10007, 13, 4, 1), (2500, 3, 5, 5000),
+                                                     (20000, 9, 2, 9000), (30011, 31, 1, 2049)])
 def test_trajectory_vs_oracle(P, oracle, n_sig, n_points, n_mics, L):
     import torch
     rng = np.random.default_rng(n_sig + L)
