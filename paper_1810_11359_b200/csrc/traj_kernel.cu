@@ -76,11 +76,17 @@ __global__ void __launch_bounds__(kCvThreads) traj_kernel(const float* __restric
     const long long tmin = t0 - c.jend + 1;
     const int n = (int)(c.jend - c.jc);
     const int nslice = kCvTile + n - 1;
-    for (int i = tid; i < n; i += kCvThreads) cp_async4(&s_sig[buf][i], sig + (c.jend - 1 - i), true);
-    for (int e = tid; e < nslice; e += kCvThreads) {
-      const long long tau = tmin + e;
-      const bool ok = tau >= 0 && tau < L;
-      cp_async4(&s_rir[buf][cv_pad(e)], ok ? h + tau : h, ok);  // zero-fill outside the RIR
+    const float* sg = sig + (c.jend - 1);
+    for (int i = tid; i < n; i += kCvThreads) cp_async4(&s_sig[buf][i], sg - i, true);
+    // slice element e holds tau = tmin + e; valid taps are e in [elo, ehi), zero-filled elsewhere
+    const int elo = tmin < 0 ? (int)(-tmin) : 0;
+    const long long eh = L - tmin;
+    const int ehi = eh < nslice ? (int)eh : nslice;
+    const float* hb = h + tmin;  // only dereferenced for valid e
+    float* dst = &s_rir[buf][cv_pad(tid)];  // cv_pad(tid + 128 k) = cv_pad(tid) + 132 k
+    for (int e = tid; e < nslice; e += kCvThreads, dst += kCvThreads + kCvThreads / 32) {
+      const bool ok = e >= elo && e < ehi;
+      cp_async4(dst, ok ? hb + e : h, ok);
     }
     cp_async_commit();
   };
@@ -111,11 +117,13 @@ __global__ void __launch_bounds__(kCvThreads) traj_kernel(const float* __restric
       const float* ss = s_sig[buf];
       const int n = (int)(cur.jend - cur.jc);
       const int e0 = kCvPer * tid;
+      // for a base b that is a multiple of 16 and u < 16, cv_pad(b + u) = cv_pad(b) + u: one address per step
       float w[kCvPer];
 #pragma unroll
-      for (int i = 0; i < kCvPer; i++) w[i] = sr[cv_pad(e0 + i)];
+      for (int i = 0; i < kCvPer; i++) w[i] = sr[cv_pad(e0) + i];
       int d = 0;
       for (; d + kCvPer <= n; d += kCvPer) {
+        const float* rp = sr + cv_pad(e0 + d + kCvPer);
 #pragma unroll
         for (int u4 = 0; u4 < kCvPer; u4 += 4) {
           const float4 sv4 = *reinterpret_cast<const float4*>(&ss[d + u4]);  // broadcast
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(kCvThreads) traj_kernel(const float* __restric
             const int u = u4 + uu;  // window rotation is register renaming after unrolling
 #pragma unroll
             for (int i = 0; i < kCvPer; i++) acc[i] = fmaf(sv[uu], w[(i + u) % kCvPer], acc[i]);
-            w[u] = sr[cv_pad(e0 + d + u + kCvPer)];
+            w[u] = rp[u];
           }
         }
       }
