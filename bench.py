@@ -8,9 +8,14 @@ fp32 mode.  One step = one gpurir_simulate_rir call over the rank's 16384 receiv
 kernel).  Weak scaling: rank r owns receivers [16384 r, 16384 (r+1)) of the N*16384-receiver workload.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--mode fp32|lut|fp16]
+                  [--workload ism|trajectory]
 
 --impl reference times the CPU oracle (oracle/, test infrastructure) on the host cores: the paper's
 comparison arm for this tier.
+
+--workload trajectory (NEXT row f1, workloads.traj1): one step = one moving-source job: the 100 x 32
+RIRs of the trajectory (ISM + tail kernels) and the filtering of 1 s of signal through them
+(traj_kernel); value = trajectories/s.  Weak scaling: every rank runs its own trajectory.
 """
 from __future__ import annotations
 
@@ -31,6 +36,7 @@ import workloads as W  # noqa: E402
 
 M_PER_GPU = 16384
 METRIC = "RIRs/s and image contributions/s vs T60 and #RIRs at 1/2/4/8 B200"
+TRAJ_METRIC = "moving-source trajectories/s (RIR synthesis + trajectory filtering, NEXT row f1)"
 ISSUE_SLOTS_PER_TAP = 13  # algorithmic FP32-pipe issue slots per in-window tap
 
 
@@ -168,9 +174,58 @@ def cpu_baseline(sc, budget_s=15.0):
                       f"fp64 C oracle, -O2)"}
 
 
+def traj_oracle_times(sc, sig, n_rir, n_mic):
+    """Oracle seconds for n_rir of the trajectory's RIRs and for filtering n_mic microphones (random RIR
+    values of the right shape: the filter's cost does not depend on them)."""
+    import oracle
+    beta, _ = oracle.beta_sabine(sc.room, sc.T60)
+    beta = beta.astype(np.float32)
+    nb = oracle.t2n(sc.Tdiff, sc.room, sc.c)
+    L = oracle.nsamples(sc.Tmax, sc.fs)
+    n_src = max(1, n_rir // len(sc.pos_rcv))
+    t = time.perf_counter()
+    oracle.simulate_rir(sc.room, beta, sc.pos_src[:n_src], sc.pos_rcv[:max(1, n_rir // n_src)], nb, sc.Tdiff, sc.Tmax,
+                        fs=sc.fs, c=sc.c, pattern=sc.pattern, seed=sc.seed)
+    t_rir = time.perf_counter() - t
+    n_rir = n_src * max(1, n_rir // n_src)
+    rirs = np.random.default_rng(0).standard_normal((len(sc.pos_src), n_mic, L)) * 1e-2
+    t = time.perf_counter()
+    oracle.simulate_trajectory(sig, rirs)
+    t_f = time.perf_counter() - t
+    per_traj = t_rir * (len(sc.pos_src) * len(sc.pos_rcv)) / n_rir + t_f * len(sc.pos_rcv) / n_mic
+    return per_traj, n_rir, n_mic, t_rir + t_f
+
+
+def run_reference_trajectory(args):
+    import oracle
+    sc = W.traj1()
+    sig = W.traj_signal(sc.meta["n_sig"])
+    cores = oracle.max_threads()
+    times, nr, nm = [], cores, min(cores, len(sc.pos_rcv))
+    for i in range(args.warmup + args.steps):
+        per_traj, nr, nm, _ = traj_oracle_times(sc, sig, nr, nm)
+        if i >= args.warmup:
+            times.append(per_traj)
+    ms = 1000.0 * float(np.mean(times))
+    value = 1000.0 / ms
+    line = {"impl": "reference", "metric": TRAJ_METRIC, "value": value, "unit": "trajectories/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": sc.name, "reference_arm": "CPU oracle (oracle/oracle.c); each step times "
+                       f"{nr} of the {sc.M} RIRs and the filtering of {nm} of {len(sc.pos_rcv)} microphones and "
+                       "scales both to one trajectory"},
+            "cpu_baseline": {"value": value, "unit": "trajectories/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{nr} RIRs + {nm} microphones filtered per step"},
+            "e2e": {"value": value, "unit": "trajectories/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        return
+    if args.workload == "trajectory":
+        run_reference_trajectory(args)
         return
     import oracle
     sc = W.cfg3(M_PER_GPU, "diffuse")
@@ -219,6 +274,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 host path with several ranks on one GPU")
+    ap.add_argument("--workload", default="ism", choices=["ism", "trajectory"])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -243,6 +299,10 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
+
+    if args.workload == "trajectory":
+        run_trajectory(args, P, torch, dev, rank, world, dist, local_dev)
+        return
 
     # ---- workload (weak scaling: this rank's 16384 receivers of the N*16384 workload) ----
     sc = W.cfg3(M_PER_GPU * world, "diffuse")
@@ -387,7 +447,7 @@ def main():
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": issue_peak / 1e12,
                      "unit": "T FP32-lane-issue-slots/s", "frac": achieved / issue_peak, "traffic": traffic,
                      "traffic_note": "DRAM bytes per launch from profiles/r01_ism_traffic.json (ncu --set full)",
-                     "kernel": "ism_kernel<0>",
+                     "kernel": "ism_ws_kernel<0>" if args.mode == "fp32" else f"ism_ws_kernel ({args.mode})",
                      "basis": f"{ISSUE_SLOTS_PER_TAP} issue slots per in-window tap (SURVEY §8(d)) x {taps_launch:.4g} "
                               f"taps per launch (exact count on 256 sampled receivers x {M_PER_GPU}); peak = 148 SM x "
                               f"128 lanes x {f_clk / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)"},
@@ -403,6 +463,154 @@ def main():
     }
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(W.cfg3(M_PER_GPU, "diffuse"))
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev):
+    """--workload trajectory: one moving-source job per step (RIRs of all trajectory points + filtering)."""
+    sc = W.traj1()
+    n_sig = sc.meta["n_sig"]
+    sig_h = W.traj_signal(n_sig)
+    beta, _ = P.beta_sabine(sc.room, sc.T60)
+    nb = P.t2n(sc.Tdiff, sc.room, sc.c)
+    nS, nISM = P.nsamples(sc.Tmax, sc.fs), P.nsamples(sc.Tdiff, sc.fs)
+    n_pts, n_mic = len(sc.pos_src), len(sc.pos_rcv)
+    base = rank * n_pts * n_mic                # every rank's trajectory draws its own tail noise
+    src = torch.from_numpy(sc.pos_src).to(dev)
+    rcv = torch.from_numpy(sc.pos_rcv).to(dev)
+    sig = torch.from_numpy(sig_h).to(dev)
+    rirs = torch.empty((n_pts, n_mic, nS), dtype=torch.float32, device=dev)
+    out = torch.empty((n_mic, n_sig + nS - 1), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(s_src, s_rcv, s_sig, s_rirs, s_out, st, ev=None, ev_tail=None, ev_tr=None):
+        P.simulate_rir(sc.room, beta, s_src, s_rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, mic_pattern=sc.pattern,
+                       mode=args.mode, seed=sc.seed, rir_index_base=base, out=s_rirs, stream=st, ev_ism=ev,
+                       ev_tail=ev_tail)
+        if ev_tr is not None:
+            ev_tr[0].record(st)
+        P.simulate_trajectory(s_sig, s_rirs, out=s_out, stream=st)
+        if ev_tr is not None:
+            ev_tr[1].record(st)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(src, rcv, sig, rirs, out, stream)
+    torch.cuda.synchronize()
+    K = args.steps
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    tr = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    ism = [(RawEvent(), RawEvent()) for _ in range(K)]
+    tail = [(RawEvent(), RawEvent()) for _ in range(K)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_dev) as clk:
+        for i in range(K):
+            flush.zero_()
+            ev_s[i].record(stream)
+            step(src, rcv, sig, rirs, out, stream, ism[i], tail[i], tr[i])
+            ev_e[i].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
+    ism_ms = float(np.mean([a.elapsed_ms(b) for a, b in ism]))
+    tail_ms = float(np.mean([a.elapsed_ms(b) for a, b in tail]))
+    tr_ms = float(np.mean([a.elapsed_time(b) for a, b in tr]))
+    red_dev = dev if args.dist_backend == "nccl" else "cpu"
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=red_dev)
+    if dist:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    value = world * K / (total_ms / 1000.0)
+
+    # ---- e2e: signal + positions from pinned host memory, filtered output back, 2 streams ----
+    e2e_steps = max(2, args.e2e_steps)
+    h_src, h_rcv = torch.from_numpy(sc.pos_src).pin_memory(), torch.from_numpy(sc.pos_rcv).pin_memory()
+    h_sig = torch.from_numpy(sig_h).pin_memory()
+    h_out = [torch.empty(out.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+    d_rirs, d_out = [rirs, torch.empty_like(rirs)], [out, torch.empty_like(out)]
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for st_ in streams:
+        st_.wait_event(e0)
+    done = []
+    for i in range(e2e_steps):
+        st_ = streams[i % 2]
+        with torch.cuda.stream(st_):
+            step(h_src.to(dev, non_blocking=True), h_rcv.to(dev, non_blocking=True), h_sig.to(dev, non_blocking=True),
+                 d_rirs[i % 2], d_out[i % 2], st_)
+            h_out[i % 2].copy_(d_out[i % 2], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st_)
+            done.append(ev)
+    for ev in done[-2:]:
+        stream.wait_event(ev)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=red_dev)
+    if dist:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * e2e_steps / (float(e2e_ms.item()) / 1000.0)
+    assert torch.equal(h_out[(e2e_steps - 1) % 2][:, :64].to(dev), out[:, :64])
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    pk, pk_kind = peaks()
+    f_clk = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+    issue_peak = 148 * 128 * f_clk
+    H = 4e-3 * sc.fs / 2
+    pairs = [(p, m) for p in range(0, n_pts, 7) for m in range(0, n_mic, 5)]
+    taps = float(np.mean([count_taps(sc.room.astype(np.float64), sc.pos_src[p].astype(np.float64),
+                                     sc.pos_rcv[m].astype(np.float64), nb, nISM, sc.fs, sc.c, H) for p, m in pairs]))
+    taps_launch = taps * n_pts * n_mic
+    ism_ach = taps_launch * ISSUE_SLOTS_PER_TAP / (ism_ms / 1000.0)
+    macs = float(n_sig) * nS * n_mic
+    tr_ach = macs / (tr_ms / 1000.0)
+    kern = {"ism_ws_kernel": ism_ms, "traj_kernel": tr_ms, "tail_kernel": tail_ms}
+    dominant = max(kern, key=kern.get)
+    roof_ism = {"bound": "alu", "achieved": ism_ach / 1e12, "peak": issue_peak / 1e12,
+                "unit": "T FP32-lane-issue-slots/s", "frac": ism_ach / issue_peak, "traffic": None,
+                "kernel": "ism_ws_kernel<0>", "basis": f"{ISSUE_SLOTS_PER_TAP} issue slots per in-window tap x "
+                f"{taps_launch:.4g} taps per launch (exact count on {len(pairs)} sampled pairs)"}
+    roof_tr = {"bound": "alu", "achieved": tr_ach / 1e12, "peak": issue_peak / 1e12, "unit": "T FFMA/s",
+               "frac": tr_ach / issue_peak, "traffic": None, "kernel": "traj_kernel",
+               "basis": f"n_sig x L x n_mics = {macs:.4g} MACs per launch (one FFMA each); peak = 148 SM x 128 "
+                        f"lanes x {f_clk / 1e6:.0f} MHz ({pk_kind})"}
+    line = {
+        "metric": TRAJ_METRIC, "value": value, "unit": "trajectories/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": sc.name, "points": n_pts, "mics": n_mic, "n_sig": n_sig, "L": nS, "nISM": nISM,
+                   "room": [3, 4, 2.5], "T60": sc.T60, "fs": sc.fs, "nb_img": [int(v) for v in nb], "mode": args.mode,
+                   "l2": "256 MB buffer written between timed steps (L2 126 MB)"},
+        "kernel_ms": kern,
+        "roofline": roof_ism if dominant == "ism_ws_kernel" else roof_tr,
+        "traj_kernel": roof_tr,
+        "ism_kernel": roof_ism,
+        "e2e": {"value": e2e_value, "unit": "trajectories/s", "h2d_bytes_per_step": (h_src.numel() + h_rcv.numel() +
+                h_sig.numel()) * 4, "d2h_bytes_per_step": h_out[0].numel() * 4, "steps": e2e_steps},
+        "gpu_launches": 3 * K,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        import oracle
+        cores = oracle.max_threads()
+        per_traj, nr, nm, spent = traj_oracle_times(sc, sig_h, 4 * cores, min(cores, n_mic))
+        line["cpu_baseline"] = {"value": 1.0 / per_traj, "unit": "trajectories/s", "cores": cores, "kind": "oracle",
+                                "sample": f"{nr} of the {sc.M} RIRs + filtering of {nm} of {n_mic} microphones, "
+                                          f"scaled to one trajectory ({spent:.1f} s)"}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -435,7 +435,8 @@ int oracle_simulate_trajectory(const double* sig, long n_sig, const double* rirs
   long seglen = n_sig / n_points;
   long n_out = n_sig + L - 1;
   for (long i = 0; i < (long)n_mics * n_out; i++) out[i] = 0.0;
-  for (int m = 0; m < n_mics; m++) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int m = 0; m < n_mics; m++) {  /* microphones are independent (one thread each) */
     double* o = out + (size_t)m * n_out;
     for (long j = 0; j < n_sig; j++) {
       long p = j / seglen;

@@ -17,6 +17,9 @@ DESIGN.md §"Input recipe"):
         (a) Tdiff 0.25 / Tmax 1.0, (b) ISM to 0.5 s
   cfg5  n rooms (seed 5): L ~ U(3,10) x U(3,8) x U(2.5,4.5), T60 ~ U(0.2,1.5), src/rcv uniform with
         0.5 m wall margin, omni, 16 kHz, Tdiff = T60/4, Tmax = T60
+  traj1 (NEXT row f1) cfg3's room and T60, a source moving on a straight line (0.5,1.0,1.2) ->
+        (2.5,3.0,1.2) sampled at 100 trajectory points, 32-mic UCA r=0.10 m at (1.5,2.5,1.3), omni,
+        16 kHz, Tdiff 0.175 / Tmax 0.7 (L = 11200), 1 s of unit-variance white noise (seed 11)
 
 Positions, room sizes and orientations are float32 (the C ABI's type); the
 oracle receives the same float32 values widened to double.
@@ -107,6 +110,20 @@ def cfg4(variant: str = "a", n_mics: int = 32) -> Scene:
         raise ValueError(variant)
     return Scene(f"cfg4{variant}", _f32([3, 4, 2.5]), 1.0, _f32([[1.0, 1.0, 1.5]]), _f32(rcv), None,
                  PATTERN["omni"], Tdiff, Tmax, 48000.0, seed=SEED_BASE + 4)
+
+
+def traj1(n_points: int = 100, n_mics: int = 32, n_sig: int = 16000) -> Scene:
+    t = np.linspace(0.0, 1.0, n_points)
+    src = np.stack([0.5 + 2.0 * t, 1.0 + 2.0 * t, np.full(n_points, 1.2)], axis=1)
+    ang = 2.0 * np.pi * np.arange(n_mics) / n_mics
+    rcv = np.stack([1.5 + 0.10 * np.cos(ang), 2.5 + 0.10 * np.sin(ang), np.full(n_mics, 1.3)], axis=1)
+    return Scene(f"traj1_P{n_points}_M{n_mics}", _f32([3, 4, 2.5]), 0.7, _f32(src), _f32(rcv), None,
+                 PATTERN["omni"], 0.175, 0.7, 16000.0, seed=SEED_BASE + 11, meta={"n_sig": n_sig})
+
+
+def traj_signal(n_sig: int, seed: int = SEED_BASE + 11) -> np.ndarray:
+    """The source signal of a trajectory workload: unit-variance white noise, float32."""
+    return _f32(np.random.default_rng(seed).standard_normal(n_sig))
 
 
 @dataclass
