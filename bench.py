@@ -196,12 +196,22 @@ def traj_oracle_times(sc, sig, n_rir, n_mic):
     return per_traj, n_rir, n_mic, t_rir + t_f
 
 
+def traj_oracle_sample(sc, sig, cores, budget_s):
+    """Sample sizes (RIRs, microphones) so that one oracle pass over them takes about budget_s."""
+    per_traj, _, _, _ = traj_oracle_times(sc, sig, cores, 2)
+    f = min(1.0, budget_s / per_traj)
+    nr = int(min(sc.M, max(cores, round(f * sc.M / cores) * cores)))
+    nm = int(min(len(sc.pos_rcv), max(2, round(f * len(sc.pos_rcv)))))
+    return nr, nm
+
+
 def run_reference_trajectory(args):
     import oracle
     sc = W.traj1()
     sig = W.traj_signal(sc.meta["n_sig"])
     cores = oracle.max_threads()
-    times, nr, nm = [], cores, min(cores, len(sc.pos_rcv))
+    nr, nm = traj_oracle_sample(sc, sig, cores, 150.0 / max(1, args.steps + args.warmup))
+    times = []
     for i in range(args.warmup + args.steps):
         per_traj, nr, nm, _ = traj_oracle_times(sc, sig, nr, nm)
         if i >= args.warmup:
@@ -607,7 +617,8 @@ def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev):
     if not args.no_cpu_baseline and world == 1:
         import oracle
         cores = oracle.max_threads()
-        per_traj, nr, nm, spent = traj_oracle_times(sc, sig_h, 4 * cores, min(cores, n_mic))
+        nr, nm = traj_oracle_sample(sc, sig_h, cores, 15.0)
+        per_traj, nr, nm, spent = traj_oracle_times(sc, sig_h, nr, nm)
         line["cpu_baseline"] = {"value": 1.0 / per_traj, "unit": "trajectories/s", "cores": cores, "kind": "oracle",
                                 "sample": f"{nr} of the {sc.M} RIRs + filtering of {nm} of {n_mic} microphones, "
                                           f"scaled to one trajectory ({spent:.1f} s)"}

@@ -350,3 +350,19 @@ def test_trajectory_invalid(P):
     import torch
     with pytest.raises(P.GpurirError):
         P.simulate_trajectory(torch.randn(3, device="cuda"), torch.zeros((5, 1, 4), device="cuda"))
+
+
+def test_trajectory_full_size_sampled_mics(P, oracle):
+    """bench.py's trajectory launch (traj1: 1 s, 100 points, 32 mics, L = 11200) with seeded random banks;
+    the oracle filters 2 of the 32 microphones in full."""
+    import torch
+    import workloads as W
+    sc = W.traj1()
+    sig = W.traj_signal(sc.meta["n_sig"])
+    L = 11200
+    rirs = (np.random.default_rng(12).standard_normal((len(sc.pos_src), len(sc.pos_rcv), L)) *
+            np.exp(-np.arange(L) / 2000.0)).astype(np.float32)
+    g = P.simulate_trajectory(torch.from_numpy(sig).cuda(), torch.from_numpy(rirs).cuda(), sync=True).cpu().numpy()
+    for m in (0, 17):
+        r = oracle.simulate_trajectory(sig, rirs[:, m:m + 1])[0]
+        assert np.max(np.abs(g[m] - r)) <= TRAJ_TOL * np.max(np.abs(r))
