@@ -234,12 +234,7 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
       const int ra = sm.binstart[sub], rb = sm.binstart[min(sub + A.nbw, nbins)];
       if (MODE == 0) {
         // Eq. 5-6: acc += C' w(u) / v, v = (k - x)/Hs, w = Hann window (R5), C' = -A sin(pi f)/(pi Hs)
-        TapConst K;
-        const float kv = (float)kfs[s] * A.invHs;
-        K.kv2 = make_float2(kv, kv);
-        K.mr2 = make_float2(-A.rho2, -A.rho2);
-        K.b3 = make_float2(A.wb[3], A.wb[3]); K.b2 = make_float2(A.wb[2], A.wb[2]);
-        K.b1 = make_float2(A.wb[1], A.wb[1]); K.b0 = make_float2(A.wb[0], A.wb[0]);
+        const TapConst K = make_tap_const(A, (float)kfs[s] * A.invHs);
         const float4* pp = sm.sorted + ((ra & ~1) >> 1) + grp;  // record pairs, group grp, stride kG
         const float4* pend = sm.sorted + ((rb + 1) >> 1);
         acc[s] = tap_loop(pp, pend, K, acc[s]);

@@ -500,12 +500,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
         const int kf = sub * kS + li - kWsTC / 2;  // sample relative to the tile centre
         const int ra = sm.binstart[buf][sub], rb = sm.binstart[buf][min(sub + A.nbw, w.nbins)];
         if (MODE == 0) {
-          TapConst K;
-          const float kv = (float)kf * A.invHs;
-          K.kv2 = make_float2(kv, kv);
-          K.mr2 = make_float2(-A.rho2, -A.rho2);
-          K.b3 = make_float2(A.wb[3], A.wb[3]); K.b2 = make_float2(A.wb[2], A.wb[2]);
-          K.b1 = make_float2(A.wb[1], A.wb[1]); K.b0 = make_float2(A.wb[0], A.wb[0]);
+          const TapConst K = make_tap_const(A, (float)kf * A.invHs);
           const float4* pp = sorted + ((ra & ~1) >> 1) + grp;  // record pairs, group grp, stride kG
           const float4* pend = sorted + ((rb + 1) >> 1);
           acc[s][lane] = tap_loop(pp, pend, K, acc[s][lane]);
