@@ -118,6 +118,9 @@ __device__ __forceinline__ float2 tap_pair(const float4 p, const TapConst& K, fl
   return __ffma2_rn(make_float2(p.z, p.w), __fmul2_rn(w, r), a2);
 }
 __device__ __forceinline__ float2 tap_loop(const float4* pp, const float4* pend, const TapConst& K, float2 a2) {
+#ifdef GPURIR_EXPERIMENT_SKIP_TAPS  // profiling experiment only: producer-bound time
+  if (pend - pp < 1000000) return a2;
+#endif
   float2 a3 = make_float2(0.f, 0.f);  // second accumulator: two independent FFMA2 chains
   for (; pp + 3 * kG < pend; pp += 4 * kG) {
     const float4 p0 = pp[0], p1 = pp[kG], p2 = pp[2 * kG], p3 = pp[3 * kG];

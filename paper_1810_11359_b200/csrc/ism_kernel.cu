@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
   float2 acc[kSubPerWarp];
 #pragma unroll
   for (int s = 0; s < kSubPerWarp; s++) {
-    kfs[s] = T.t0 + (warp * kSubPerWarp + s) * kS + li - T.tc;  // sample relative to tc
+    kfs[s] = T.t0 + (s * kWarps + warp) * kS + li - T.tc;  // sample relative to tc
     acc[s] = make_float2(0.f, 0.f);
   }
 
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
 
 #pragma unroll
     for (int s = 0; s < kSubPerWarp; s++) {
-      const int sub = warp * kSubPerWarp + s;
+      const int sub = s * kWarps + warp;  // interleaved sub-tiles (balances the t^2 image density)
       const int ra = sm.binstart[sub], rb = sm.binstart[min(sub + A.nbw, nbins)];
       if (MODE == 0) {
         // Eq. 5-6: acc += C' w(u) / v, v = (k - x)/Hs, w = Hann window (R5), C' = -A sin(pi f)/(pi Hs)
@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
     a += __shfl_xor_sync(0xffffffffu, a, 16);
     if (MODE == 0) { if (kfs[s] & 1) a = -a; }
     else if (MODE == 2) { a *= (1.f / 1024.f); if (kfs[s] & 1) a = -a; }
-    if (grp == 0) sm.outtile[(warp * kSubPerWarp + s) * kS + li] = a;
+    if (grp == 0) sm.outtile[(s * kWarps + warp) * kS + li] = a;
   }
   if (P > 1) {
     cluster.sync();

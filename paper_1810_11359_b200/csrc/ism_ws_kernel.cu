@@ -56,6 +56,15 @@ constexpr int kBarProd = kBarEmpty0 + kNBuf;    // producer-internal
 
 constexpr int kWinLast = 1, kWinTerminate = 2;
 
+#ifdef GPURIR_WS_PROF  // profiling build only (tools/ws_prof.py): per-role cycle counters
+__device__ unsigned long long g_ws_prof[64];
+#define WS_T0(v) const long long v = clock64()
+#define WS_ADD(i, v) prof[i] += (unsigned long long)(clock64() - (v))
+#else
+#define WS_T0(v)
+#define WS_ADD(i, v)
+#endif
+
 __device__ __forceinline__ void bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -90,6 +99,18 @@ __device__ __forceinline__ long long ws_order(long long wi, long long n) {
 #endif
 }
 
+// Single-room call: work position -> (RIR, tile).
+#ifdef GPURIR_WS_RIR_MAJOR
+// RIR-major: the tiles of one RIR are consecutive positions, latest (heaviest) first, so every CTA sees a
+// mix of tile shapes (producer-heavy thin late shells, consumer-heavy middle tiles) at all times.
+__device__ __forceinline__ int ws_tile(long long pos, const IsmArgs& A) { return A.nTiles - 1 - (int)(pos % A.nTiles); }
+__device__ __forceinline__ int ws_rir(long long pos, const IsmArgs& A) { return (int)(pos / A.nTiles); }
+#else
+// tile-major: position 0..M-1 = the latest (heaviest) tile of every RIR, then the next tile, ...
+__device__ __forceinline__ int ws_tile(long long pos, const IsmArgs& A) { return A.nTiles - 1 - (int)(pos / A.M); }
+__device__ __forceinline__ int ws_rir(long long pos, const IsmArgs& A) { return (int)(pos % A.M); }
+#endif
+
 // Warp 0 of the producers: issue the asynchronous loads of work item wi's per-RIR inputs into stage.
 __device__ __forceinline__ void ws_prefetch(const IsmArgs& A, long long wi, long long n_work, WsStage& st, int lane) {
   if (lane == 0) st.wi = wi;
@@ -100,7 +121,7 @@ __device__ __forceinline__ void ws_prefetch(const IsmArgs& A, long long wi, long
     constexpr int n16 = (int)(sizeof(BatchJob) / 16);
     if (lane < n16) cp_async16(reinterpret_cast<char*>(&st.job) + 16 * lane, reinterpret_cast<const char*>(A.jobs + jt.x) + 16 * lane);
   } else {
-    const int m = (int)(ws_order(wi, n_work) % A.M);
+    const int m = ws_rir(ws_order(wi, n_work), A);
     const int ms = m / A.M_rcv, mr = m % A.M_rcv;
     if (lane < 3) cp_async4(&st.pos[lane], A.pos_src + 3 * ms + lane);
     else if (lane < 6) cp_async4(&st.pos[lane], A.pos_rcv + 3 * mr + (lane - 3));
@@ -191,7 +212,11 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
     int win_i = 0, filled = 0;
 
     // stable counting sort of rec[0, filled) by bin, then publish to buffer win_i % kNBuf
+#ifdef GPURIR_WS_PROF
+    unsigned long long prof[16] = {0};
+#endif
     auto publish = [&](int flags, int nbins) {
+      WS_T0(tp0);
       for (int i = ptid; i < kPW * kMaxBins; i += kPT) (&sm.warpcnt[0][0])[i] = 0;
       bar_sync(kBarProd, kPT);
       const int per_warp = (filled + kPW - 1) / kPW;
@@ -227,8 +252,10 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
         if (lane == 0) sm.pbinstart[nbins] = carry;
       }
       const int buf = win_i % kNBuf;
+      WS_T0(te0);
       if (win_i >= kNBuf) bar_sync(kBarEmpty0 + buf, kWsThreads);  // consumers released this buffer
       else bar_sync(kBarProd, kPT);
+      WS_ADD(1, te0);
       float4* sorted = sm.sorted[buf];
       for (int r = wbeg + lane; r < wend; r += 32) {  // pass 2: scatter (no warp collectives)
         const int b = (int)sm.bin[r];
@@ -265,6 +292,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
       bar_sync(kBarProd, kPT);                  // rec / warpcnt / pbinstart reusable
       win_i++;
       filled = 0;
+      WS_ADD(0, tp0);
     };
 
     long long wi_pending = 0;  // warp 0, lane 0: the atomicAdd result for the item after the current one
@@ -275,6 +303,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
       ws_prefetch(A, wi0, n_work, sm.stage, lane);
     }
     for (;;) {
+      WS_T0(ts0);
       if (warp == 0) {
         cp_async_wait_all();
         __syncwarp();
@@ -295,8 +324,8 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
               geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.lb, J.neg, J.zero, T.g, A.status);
             } else {
               const long long pos = ws_order(wi, n_work);
-              tile = A.nTiles - 1 - (int)(pos / A.M);  // position 0 = heaviest (latest) tile
-              m = (int)(pos % A.M);
+              tile = ws_tile(pos, A);
+              m = ws_rir(pos, A);
               nISM = A.nISM;
               row = (long long)m * A.row_stride;
               geom_from(A.L, sm.stage.pos, sm.stage.pos + 3, A.orv ? sm.stage.pos + 6 : zero3, A.nb, A.pattern, A.lb,
@@ -335,6 +364,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
       bar_sync(kBarProd, kPT);
       if ((long long)sm.next_work >= n_work) break;
       bar_sync(kBarProd, kPT);
+      WS_ADD(2, ts0);
       const WsTile& T = sm.ti;
       const RirGeom& g = T.g;
       const int nbins = (int)ceilf(((float)kWsTC + 2.f * H) / (float)kS) + 1;
@@ -343,6 +373,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
       // (the first column batch below syncs before any bz read)
 
       for (int qb = 0; qb < T.ncols; qb += kWsColBatch) {
+        WS_T0(tc0);
         int cnt = 0;
         {
           const int q = qb + ptid;
@@ -387,6 +418,8 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
         sm.colpre[ptid] = x + add;
         bar_sync(kBarProd, kPT);
         const int total = sm.colpre[kWsColBatch - 1];
+        WS_ADD(3, tc0);
+        WS_T0(ti0);
 
         for (int base = 0; base < total;) {
           const int take = min(WsCap<MODE>::v - filled, total - base);
@@ -401,58 +434,82 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
             int j = lo;
             int before = j > 0 ? sm.colpre[j - 1] : 0;
             int boundary = sm.colpre[j];
-#pragma unroll 2
-            for (int gi = g0; gi < g1; gi++) {
+            // tile constants in registers (shared-memory reads would be re-issued per image)
+            const double Lz = g.L[2], offE = T.offE, offO = T.offO;
+            const int tc = T.tc, zl = T.zl;
+            const bool use_bz = T.use_bz;
+            const float xmax = T.xrel_max, oz = g.o[2], ga = g.a, fsc = (float)fs_over_c;
+            // Two images per iteration: all shared loads first, then both images' arithmetic (independent,
+            // so the scheduler interleaves the two dependency chains), then the stores.
+            for (int gi = g0; gi < g1; gi += 2) {
               while (gi >= boundary) { before = boundary; j++; boundary = sm.colpre[j]; }
-              const WsColRec& cr = sm.col[j];
-              const int l = gi - before;
-              const int nz = l < cr.r1n ? cr.r1lo + l : cr.r2lo + (l - cr.r1n);
-              // Eq. 1 along z: even nz -> nz L + s, odd nz -> (nz + 1) L - s; Delta_z = z_n - z_r
-              const int odd = nz & 1;
-              const double dz = fma((double)(nz + odd), g.L[2], odd ? T.offO : T.offE);
-              const double x2 = fma(dz, dz, cr.rho2) * sc2;  // (d fs / c)^2
-              if (x2 == 0.0) atomicOr(A.status, kStatusDegenerate);
-              // branch-free from here: culled records are computed and flagged with kDiscard
-              float x0f;
-              float xr = delay_rel(x2, T.tc, x0f);
-              const float xrel = xr + (float)(kWsTC / 2) + H;  // x - (t0 - H)
-              const bool keep = (x2 != 0.0) && (xrel > 0.f) && (xrel < T.xrel_max);
-              const uint8_t b = keep ? (uint8_t)(int)(xrel * (1.f / (float)kS)) : kDiscard;
-              const float rx = rcp_approx(x0f);          // 1/d = fs / (c x)
-              const float bz = T.use_bz ? sm.bz[min(max(nz - T.zl, 0), kBzMax - 1)] : z_factor(nz, g);
-              const float cth = fmaf((float)dz, g.o[2], cr.cdot) * ((float)fs_over_c * rx);
-              const float gain = g.a + (1.f - g.a) * cth;
-              const float amp = cr.bxy * bz * gain * rx * fs_over_c_4pi;  // Eq. 4
-              float2 rec;
-              float recA = 0.f;
-              if (MODE == 1) {
-                float xq = xr * (float)A.lutQ;
-                float fiq = floorf(xq);
-                float phi = xq - fiq;
-                int iq1 = (int)fiq + 1;
-                int php = iq1 & (A.lutQ - 1);
-                int aa = (iq1 - php) / A.lutQ;
-                int ph = (A.lutQ - php) & (A.lutQ - 1);
-                int jsh = aa + (php > 0 ? 1 : 0);
-                rec = make_float2(__int_as_float(ph * A.lut_cols + A.lut_joff - jsh), phi);
-                recA = amp;
-              } else {
-                float fj = floorf(xr);
-                float f = xr - fj;
-                if (f == 0.f) {  // exact integer delay (reading R3): move off the sinc zero by >= 1 ulp
-                  xr += fmaxf(fabsf(xr) * 1.1920929e-7f, 9.5367432e-7f);
-                  fj = floorf(xr);
-                  f = xr - fj;
+              const int jA = j, lA = gi - before;
+              const bool hasB = gi + 1 < g1;
+              if (hasB) { while (gi + 1 >= boundary) { before = boundary; j++; boundary = sm.colpre[j]; } }
+              const int jB = j, lB = gi + 1 - before;
+              const WsColRec crA = sm.col[jA], crB = sm.col[jB];
+              int nz[2], odd[2];
+              nz[0] = lA < crA.r1n ? crA.r1lo + lA : crA.r2lo + (lA - crA.r1n);
+              nz[1] = lB < crB.r1n ? crB.r1lo + lB : crB.r2lo + (lB - crB.r1n);
+              float bz[2];
+#pragma unroll
+              for (int e = 0; e < 2; e++) {
+                odd[e] = nz[e] & 1;
+                bz[e] = use_bz ? sm.bz[min(max(nz[e] - zl, 0), kBzMax - 1)] : z_factor(nz[e], g);
+              }
+              float2 rec[2];
+              float recA[2];
+              uint8_t bb[2];
+#pragma unroll
+              for (int e = 0; e < 2; e++) {
+                const WsColRec& cr = e ? crB : crA;
+                // Eq. 1 along z: even nz -> nz L + s, odd nz -> (nz + 1) L - s; Delta_z = z_n - z_r
+                const double dz = fma((double)(nz[e] + odd[e]), Lz, odd[e] ? offO : offE);
+                const double x2 = fma(dz, dz, cr.rho2) * sc2;  // (d fs / c)^2
+                if (x2 == 0.0 && (e == 0 || hasB)) atomicOr(A.status, kStatusDegenerate);
+                // branch-free from here: culled records are computed and flagged with kDiscard
+                float x0f;
+                float xr = delay_rel(x2, tc, x0f);
+                const float xrel = xr + (float)(kWsTC / 2) + H;  // x - (t0 - H)
+                const bool keep = (x2 != 0.0) && (xrel > 0.f) && (xrel < xmax);
+                bb[e] = keep ? (uint8_t)(int)(xrel * (1.f / (float)kS)) : kDiscard;
+                const float rx = rcp_approx(x0f);          // 1/d = fs / (c x)
+                const float cth = fmaf((float)dz, oz, cr.cdot) * (fsc * rx);
+                const float gain = ga + (1.f - ga) * cth;
+                const float amp = cr.bxy * bz[e] * gain * rx * fs_over_c_4pi;  // Eq. 4
+                recA[e] = 0.f;
+                if (MODE == 1) {
+                  float xq = xr * (float)A.lutQ;
+                  float fiq = floorf(xq);
+                  float phi = xq - fiq;
+                  int iq1 = (int)fiq + 1;
+                  int php = iq1 & (A.lutQ - 1);
+                  int aa = (iq1 - php) / A.lutQ;
+                  int ph = (A.lutQ - php) & (A.lutQ - 1);
+                  int jsh = aa + (php > 0 ? 1 : 0);
+                  rec[e] = make_float2(__int_as_float(ph * A.lut_cols + A.lut_joff - jsh), phi);
+                  recA[e] = amp;
+                } else {
+                  // exact integer delay (reading R3): move off the sinc zero by >= 1 ulp (select, no branch)
+                  const float xr0 = xr;
+                  xr = (xr0 - floorf(xr0) == 0.f) ? xr0 + fmaxf(fabsf(xr0) * 1.1920929e-7f, 9.5367432e-7f) : xr0;
+                  const float fj = floorf(xr);
+                  const float f = xr - fj;
+                  float cc = -amp * sinpi01(f) * 0.318309886183790672f;
+                  if ((int)fj & 1) cc = -cc;
+                  if (MODE == 0) rec[e] = make_float2(-xr * A.invHs, cc * A.invHs);
+                  else rec[e] = make_float2(-xr * (0.5f * A.invHs), cc * (0.5f * A.invHs) * 1024.f);
                 }
-                float cc = -amp * sinpi01(f) * 0.318309886183790672f;
-                if ((int)fj & 1) cc = -cc;
-                if (MODE == 0) rec = make_float2(-xr * A.invHs, cc * A.invHs);
-                else rec = make_float2(-xr * (0.5f * A.invHs), cc * (0.5f * A.invHs) * 1024.f);
               }
               const int dst = filled + (gi - base);
-              sm.rec[dst] = rec;
-              if (MODE == 1) sm.recA[dst] = recA;
-              sm.bin[dst] = b;
+              sm.rec[dst] = rec[0];
+              if (MODE == 1) sm.recA[dst] = recA[0];
+              sm.bin[dst] = bb[0];
+              if (hasB) {
+                sm.rec[dst + 1] = rec[1];
+                if (MODE == 1) sm.recA[dst + 1] = recA[1];
+                sm.bin[dst + 1] = bb[1];
+              }
             }
           }
           filled += take;
@@ -463,6 +520,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
           }
         }
         bar_sync(kBarProd, kPT);  // column records are replaced by the next batch
+        WS_ADD(4, ti0);  // includes the publishes of full windows (also counted in [0])
       }
       if (warp == 0) {  // stage the next work item while the last window is sorted and published
         const long long wn = __shfl_sync(0xffffffffu, wi_pending, 0);
@@ -474,6 +532,10 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
     publish(kWinTerminate, 1);
     // match the consumers' releases of the last kNBuf buffers
     for (int w = max(0, win_i - kNBuf); w < win_i; w++) bar_sync(kBarEmpty0 + (w % kNBuf), kWsThreads);
+#ifdef GPURIR_WS_PROF
+    if (lane == 0)
+      for (int i = 0; i < 8; i++) atomicAdd(&g_ws_prof[i], prof[i]);
+#endif
   } else {
     // =========================== consumers ===========================
 #if GPURIR_WS_PROD_REGS > 0
@@ -485,10 +547,20 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
 #pragma unroll
     for (int s = 0; s < kWsSub; s++) acc[s][lane] = make_float2(0.f, 0.f);
     int win_i = 0;
+#ifdef GPURIR_WS_PROF
+    unsigned long long prof[32] = {0};
+#endif
     for (;;) {
       const int buf = win_i % kNBuf;
+      WS_T0(tf0);
       bar_sync(kBarFull0 + buf, kWsThreads);
       const WinInfo w = sm.win[buf];
+#ifdef GPURIR_WS_PROF
+      const int tb = min(w.t0 / kWsTC, 7);
+      prof[tb] += (unsigned long long)(clock64() - tf0);
+      prof[24 + tb] += 1;
+#endif
+      WS_T0(tw0);
       if (w.flags & kWinTerminate) {
         bar_arrive(kBarEmpty0 + buf, kWsThreads);
         break;
@@ -496,7 +568,8 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
       const float4* sorted = sm.sorted[buf];
 #pragma unroll 1
       for (int s = 0; s < kWsSub; s++) {
-        const int sub = cw * kWsSub + s;
+        const int sub = s * kCW + cw;  // interleaved: every warp gets early and late sub-tiles of the tile
+        if (sub * kS >= w.te - w.t0) break;  // past the end of a partial (last) tile
         const int kf = sub * kS + li - kWsTC / 2;  // sample relative to the tile centre
         const int ra = sm.binstart[buf][sub], rb = sm.binstart[buf][min(sub + A.nbw, w.nbins)];
         if (MODE == 0) {
@@ -533,18 +606,37 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
           float a = as.x + as.y;
           a += __shfl_xor_sync(0xffffffffu, a, 8);
           a += __shfl_xor_sync(0xffffffffu, a, 16);
-          const int kf = (cw * kWsSub + s) * kS + li - kWsTC / 2;
+          const int kf = (s * kCW + cw) * kS + li - kWsTC / 2;
           if (MODE == 0) { if (kf & 1) a = -a; }
           else if (MODE == 2) { a *= (1.f / 1024.f); if (kf & 1) a = -a; }
-          const int k = w.t0 + (cw * kWsSub + s) * kS + li;
+          const int k = w.t0 + (s * kCW + cw) * kS + li;
           if (grp == 0 && k < w.te) A.out[w.row + k] = a;
           acc[s][lane] = make_float2(0.f, 0.f);
         }
       }
+#ifdef GPURIR_WS_PROF
+      prof[8 + tb] += (unsigned long long)(clock64() - tw0);
+#endif
       win_i++;
     }
+#ifdef GPURIR_WS_PROF
+    if (lane == 0)
+      for (int i = 0; i < 32; i++) if (prof[i]) atomicAdd(&g_ws_prof[16 + i], prof[i]);
+#endif
   }
 }
+
+#ifdef GPURIR_WS_PROF
+extern "C" int gpurir_debug_ws_prof(unsigned long long* out64, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out64, g_ws_prof, sizeof(g_ws_prof)) != cudaSuccess) return 5;
+  if (reset) {
+    unsigned long long z[64] = {0};
+    cudaMemcpyToSymbol(g_ws_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 size_t ism_ws_smem_bytes(int mode, int lut_rows, int lut_cols) {
   switch (mode) {
