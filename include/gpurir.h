@@ -56,7 +56,11 @@ typedef enum {
 typedef enum {
   GPURIR_FP32 = 0, /* Eq. 6 evaluated in fp32 (the paper's "base" kernel)               */
   GPURIR_LUT = 1,  /* Eq. 9 windowed-sinc table, Q-times oversampled, linear interp.    */
-  GPURIR_FP16 = 2  /* half2 tap arithmetic with the Eq. 10-12 style polynomials */
+  GPURIR_FP16 = 2, /* half2 tap arithmetic with the Eq. 10-12 style polynomials */
+  GPURIR_LUT_TEX = 3 /* Eq. 9 table in texture memory, hardware linear interpolation (the paper's LUT
+                        placement).  Any Q >= 1 with 2 ceil(Tw Q fs / 2) + 1 <= the
+                        device's 1-D texture width (else EINVAL).  Interpolation weights have 8 fractional
+                        bits (texture hardware); tolerance as GPURIR_LUT. */
 } gpurir_mode;
 
 #define GPURIR_FLAG_SYNC 1u /* synchronise the stream before returning and report device-side status */

@@ -35,9 +35,18 @@ struct LutEntry {  // one uploaded Eq. 9 table; entries are never overwritten (k
   float2* dev = nullptr;
 };
 
+struct TexEntry {  // one Eq. 9 table as a filtered 1-D texture (texture-LUT mode, f2); never destroyed
+  double Tw = 0, fs = 0;
+  int Q = 0;
+  long long half = 0;
+  cudaArray_t arr = nullptr;
+  cudaTextureObject_t tex = 0;
+};
+
 struct DeviceState {
   int* status = nullptr;
   std::vector<LutEntry> luts;
+  std::vector<TexEntry> texs;
   int* work_counter = nullptr;  // persistent-kernel work-queue heads, one per call in flight (ring)
   unsigned next_counter = 0;
   int num_sms = 0;
@@ -107,6 +116,70 @@ const LutEntry* ensure_lut(DeviceState* d, double Tw, double fs, int Q, double H
   if (e != cudaSuccess) { cudaFree(L.dev); *err = cuda_fail(e, "upload(lut)"); return nullptr; }
   d->luts.push_back(L);
   return &d->luts.back();
+}
+
+// Texture-LUT mode ("texture memory ... hardware interpolation"): T[n], n = -half..half,
+// in a 1-D CUDA array, linear filtering, unnormalised coordinates, border addressing (0 outside the table).
+const TexEntry* ensure_tex(DeviceState* d, double Tw, double fs, int Q, cudaStream_t stream, int* err) {
+  *err = GPURIR_OK;
+  for (const TexEntry& T : d->texs)
+    if (T.Tw == Tw && T.fs == fs && T.Q == Q) return &T;
+  TexEntry T;
+  T.Tw = Tw; T.fs = fs; T.Q = Q;
+  T.half = lut_half(Tw, fs, Q);
+  const long long n = 2 * T.half + 1;
+  int dev = 0, maxw = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxTexture1DWidth, dev);
+  if (n > maxw) { *err = GPURIR_EINVAL; return nullptr; }
+  std::vector<float> tab((size_t)n);
+  for (long long i = -T.half; i <= T.half; i++) tab[(size_t)(i + T.half)] = (float)lut_entry(i, Tw, fs, Q, T.half);
+  cudaChannelFormatDesc cd = cudaCreateChannelDesc<float>();
+  cudaError_t e = cudaMallocArray(&T.arr, &cd, (size_t)n, 0);
+  if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMallocArray(lut tex)"); return nullptr; }
+  e = cudaMemcpy2DToArrayAsync(T.arr, 0, 0, tab.data(), n * sizeof(float), n * sizeof(float), 1,
+                               cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // the staging vector goes out of scope
+  if (e != cudaSuccess) { cudaFreeArray(T.arr); *err = cuda_fail(e, "upload(lut tex)"); return nullptr; }
+  cudaResourceDesc rd;
+  memset(&rd, 0, sizeof(rd));
+  rd.resType = cudaResourceTypeArray;
+  rd.res.array.array = T.arr;
+  cudaTextureDesc td;
+  memset(&td, 0, sizeof(td));
+  td.addressMode[0] = cudaAddressModeBorder;
+  td.filterMode = cudaFilterModeLinear;
+  td.readMode = cudaReadModeElementType;
+  td.normalizedCoords = 0;
+  e = cudaCreateTextureObject(&T.tex, &rd, &td, nullptr);
+  if (e != cudaSuccess) { cudaFreeArray(T.arr); *err = cuda_fail(e, "cudaCreateTextureObject"); return nullptr; }
+  d->texs.push_back(T);
+  return &d->texs.back();
+}
+
+// Mode tables of one call (LUT: phase-major smem table; texture LUT: filtered texture).
+int setup_mode(DeviceState* d, const gpurir_opts& o, double fs, double H, cudaStream_t stream, IsmArgs& A) {
+  int st = GPURIR_OK;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (o.mode == GPURIR_LUT) {
+    const LutEntry* L = ensure_lut(d, o.Tw, fs, o.lut_Q, H, stream, &st);
+    if (!L) return st;
+    A.lut = L->dev; A.lut_rows = L->rows; A.lut_cols = L->cols; A.lut_joff = L->joff;
+    A.lutQ = o.lut_Q;
+  } else if (o.mode == GPURIR_LUT_TEX) {
+    const TexEntry* T = ensure_tex(d, o.Tw, fs, o.lut_Q, stream, &st);
+    if (!T) return st;
+    A.tex = (unsigned long long)T->tex;
+    A.texQ = (float)o.lut_Q;
+    A.tex_off = (float)((double)T->half + 0.5);
+  }
+  return GPURIR_OK;
+}
+
+int validate_mode(const gpurir_opts& o) {
+  if (o.mode < GPURIR_FP32 || o.mode > GPURIR_LUT_TEX) return GPURIR_EINVAL;
+  if (o.mode == GPURIR_LUT && (o.lut_Q & (o.lut_Q - 1))) return GPURIR_EINVAL;  // power of two (R4)
+  return GPURIR_OK;
 }
 
 double sabine(const float L[3], const float b[6]) {
@@ -286,8 +359,7 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
   int st = validate_room(room_sz, beta, nb_img, mic_pattern);
   if (st) return st;
   if (mic_pattern != GPURIR_OMNI && !orV_rcv) return GPURIR_EINVAL;
-  if (o.mode < 0 || o.mode > 2) return GPURIR_EINVAL;
-  if (o.mode == GPURIR_LUT && (o.lut_Q & (o.lut_Q - 1))) return GPURIR_EINVAL;  // power of two
+  if (int em = validate_mode(o)) return em;
   double H = o.Tw * fs / 2.0;
   if ((int)ceil((kTCPersistent + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;  // window too long
   long long nS = gpurir_nsamples(Tmax, fs);
@@ -318,13 +390,7 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
     fill_common(A, fs, c, o.Tw);
     A.out = out;
     A.status = d->status;
-    if (o.mode == GPURIR_LUT) {
-      std::lock_guard<std::mutex> lk(g_mu);
-      const LutEntry* L = ensure_lut(d, o.Tw, fs, o.lut_Q, H, stream, &st);
-      if (!L) return st;
-      A.lut = L->dev; A.lut_rows = L->rows; A.lut_cols = L->cols; A.lut_joff = L->joff;
-      A.lutQ = o.lut_Q;
-    }
+    if ((st = setup_mode(d, o, fs, H, stream, A))) return st;
     long long nclusters = (long long)A.nTiles * M;
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
@@ -366,8 +432,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
   if (!(o.Tw > 0)) o.Tw = 4e-3;
   if (o.lut_Q <= 0) o.lut_Q = 16;
   if (n_rooms <= 0 || !rooms || !out || !(fs > 0) || !(c > 0)) return GPURIR_EINVAL;
-  if (o.mode < 0 || o.mode > 2) return GPURIR_EINVAL;
-  if (o.mode == GPURIR_LUT && (o.lut_Q & (o.lut_Q - 1))) return GPURIR_EINVAL;
+  if (int em = validate_mode(o)) return em;
   double H = o.Tw * fs / 2.0;
   if ((int)ceil((kTCPersistent + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;
 
@@ -442,13 +507,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     fill_common(A, fs, c, o.Tw);
     A.out = out;
     A.status = d->status;
-    if (o.mode == GPURIR_LUT) {
-      std::lock_guard<std::mutex> lk(g_mu);
-      const LutEntry* L = ensure_lut(d, o.Tw, fs, o.lut_Q, H, stream, &st);
-      if (!L) { cudaFreeAsync(ws, stream); return st; }
-      A.lut = L->dev; A.lut_rows = L->rows; A.lut_cols = L->cols; A.lut_joff = L->joff;
-      A.lutQ = o.lut_Q;
-    }
+    if ((st = setup_mode(d, o, fs, H, stream, A))) { cudaFreeAsync(ws, stream); return st; }
     long long nw = (long long)tiles.size();
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     if (persistent) e = launch_ism_ws(A, o.mode, nw, take_counter(d), d->num_sms, stream);

@@ -176,4 +176,29 @@ __device__ __forceinline__ float2 tap_loop_h(const float4* pp, const float4* pen
   return a2;
 }
 
+// Texture-LUT mode (the paper's own LUT design): record pairs (q_e, q_o, A_e, A_o) with
+// q = tex_off - x Q (x relative to the tile centre); per tap coordinate = kq + q (kq = k Q), the texture unit
+// interpolates T linearly (8-bit fractional weight) and returns 0 outside the table (border addressing).
+__device__ __forceinline__ float2 tap_pair_tex(const float4 p, cudaTextureObject_t tex, float2 kq2, float2 a2) {
+  const float2 q = __fadd2_rn(kq2, make_float2(p.x, p.y));
+  const float2 t = make_float2(tex1D<float>(tex, q.x), tex1D<float>(tex, q.y));
+  return __ffma2_rn(make_float2(p.z, p.w), t, a2);
+}
+__device__ __forceinline__ float2 tap_loop_tex(const float4* pp, const float4* pend, cudaTextureObject_t tex, float kq,
+                                               float2 a2) {
+  const float2 kq2 = make_float2(kq, kq);
+  float2 a3 = make_float2(0.f, 0.f);
+  for (; pp + 3 * kG < pend; pp += 4 * kG) {
+    const float4 p0 = pp[0], p1 = pp[kG], p2 = pp[2 * kG], p3 = pp[3 * kG];
+    a2 = tap_pair_tex(p0, tex, kq2, a2);
+    a3 = tap_pair_tex(p1, tex, kq2, a3);
+    a2 = tap_pair_tex(p2, tex, kq2, a2);
+    a3 = tap_pair_tex(p3, tex, kq2, a3);
+  }
+  for (; pp < pend; pp += kG) a2 = tap_pair_tex(pp[0], tex, kq2, a2);
+  a2.x += a3.x;
+  a2.y += a3.y;
+  return a2;
+}
+
 }  // namespace gpurir

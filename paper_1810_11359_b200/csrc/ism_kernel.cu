@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
         sm.sorted[pos] = make_float4(__int_as_float(0), 0.f, 0.f, 0.f);
       } else {
         float* pp = reinterpret_cast<float*>(&sm.sorted[pos >> 1]);
-        pp[pos & 1] = -1.0e4f;
+        pp[pos & 1] = MODE == 3 ? -1.0e6f : -1.0e4f;
         pp[2 + (pos & 1)] = 0.f;
       }
     }
@@ -271,6 +271,11 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
         float2 f = __half22float2(acch);
         a2.x += f.x; a2.y += f.y;
         acc[s] = a2;
+      } else if (MODE == 3) {
+        // texture LUT (f2): hardware linear interpolation of the Eq. 9 table
+        const float4* pp = sm.sorted + ((ra & ~1) >> 1) + grp;
+        const float4* pend = sm.sorted + ((rb + 1) >> 1);
+        acc[s] = tap_loop_tex(pp, pend, (cudaTextureObject_t)A.tex, (float)kfs[s] * A.texQ, acc[s]);
       } else {
         // LUT (Eq. 9): one table pair per tap, phase-major rows, linear interpolation
         float a = acc[s].x;
@@ -384,6 +389,8 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
                 int rowbase = ph * A.lut_cols + A.lut_joff - jsh;
                 rec = make_float2(__int_as_float(rowbase), phi);
                 recA = amp;
+              } else if (MODE == 3) {  // texture LUT: coordinate offset, amplitude
+                rec = make_float2(fmaf(-xr, A.texQ, A.tex_off), amp);
               } else {
                 // hoisted sinc numerator: sin(pi u) = -(-1)^(kf - j) sin(pi f), u = kf - xr, xr = j + f
                 float fj = floorf(xr);
@@ -508,6 +515,7 @@ cudaError_t launch_ism(const IsmArgs& A, int mode, int split, long long ncluster
   switch (mode) {
     case 0: return launch_mode<0>(cfg, A);
     case 1: return launch_mode<1>(cfg, A);
+    case 3: return launch_mode<3>(cfg, A);
     default: return launch_mode<2>(cfg, A);
   }
 }

@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
           sorted[pos] = make_float4(__int_as_float(0), 0.f, 0.f, 0.f);
         } else {
           float* pp = reinterpret_cast<float*>(&sorted[pos >> 1]);
-          pp[pos & 1] = -1.0e4f;
+          pp[pos & 1] = MODE == 3 ? -1.0e6f : -1.0e4f;  // outside every window / the texture
           pp[2 + (pos & 1)] = 0.f;
         }
       }
@@ -489,6 +489,8 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
                   int jsh = aa + (php > 0 ? 1 : 0);
                   rec[e] = make_float2(__int_as_float(ph * A.lut_cols + A.lut_joff - jsh), phi);
                   recA[e] = amp;
+                } else if (MODE == 3) {
+                  rec[e] = make_float2(fmaf(-xr, A.texQ, A.tex_off), amp);  // coordinate offset, amplitude
                 } else {
                   // exact integer delay (reading R3): move off the sinc zero by >= 1 ulp (select, no branch)
                   const float xr0 = xr;
@@ -587,6 +589,10 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
           const float4* pp = sorted + ((ra & ~1) >> 1) + grp;
           const float4* pend = sorted + ((rb + 1) >> 1);
           acc[s][lane] = tap_loop_h(pp, pend, K, acc[s][lane]);
+        } else if (MODE == 3) {
+          const float4* pp = sorted + ((ra & ~1) >> 1) + grp;
+          const float4* pend = sorted + ((rb + 1) >> 1);
+          acc[s][lane] = tap_loop_tex(pp, pend, (cudaTextureObject_t)A.tex, (float)kf * A.texQ, acc[s][lane]);
         } else {
           float a = acc[s][lane].x;
           for (int j = ra + grp; j < rb; j += kG) {
@@ -642,6 +648,7 @@ size_t ism_ws_smem_bytes(int mode, int lut_rows, int lut_cols) {
   switch (mode) {
     case 0: return sizeof(WsSmem<0>);
     case 1: return sizeof(WsSmem<1>) + (size_t)lut_rows * lut_cols * sizeof(float2);
+    case 3: return sizeof(WsSmem<3>);
     default: return sizeof(WsSmem<2>);
   }
 }
@@ -665,6 +672,7 @@ cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* cou
   switch (mode) {
     case 0: return launch_ws_mode<0>(A, n_work, counter, grid, smem, stream);
     case 1: return launch_ws_mode<1>(A, n_work, counter, grid, smem, stream);
+    case 3: return launch_ws_mode<3>(A, n_work, counter, grid, smem, stream);
     default: return launch_ws_mode<2>(A, n_work, counter, grid, smem, stream);
   }
 }

@@ -62,6 +62,10 @@ struct IsmArgs {
   // LUT mode
   const float2* lut;     // phase-major rows [Q][cols] of (T[n+1], T[n]-T[n+1])
   int lut_rows, lut_cols, lut_joff, lutQ;
+  // texture-LUT mode: the Eq. 9 table T[n], n = -half..half, in a 1-D CUDA array
+  // sampled with hardware linear filtering; a tap at offset u = k - x samples reads coordinate u Q + tex_off
+  unsigned long long tex;  // cudaTextureObject_t
+  float texQ, tex_off;     // Q and half + 0.5 (texel centres)
 };
 
 struct TailArgs {
