@@ -71,9 +71,12 @@ def lib():
         L.oracle_logistic.restype = C.c_double
         L.oracle_logistic.argtypes = [C.c_double]
         L.oracle_image_set.restype = C.c_long
-        L.oracle_image_set.argtypes = [dp, dp, dp, dp, dp, C.c_int, ip, C.c_double, C.c_double, ip, dp, dp, dp]
+        L.oracle_image_set.argtypes = [dp, dp, dp, dp, dp, C.c_int, dp, C.c_int, ip, C.c_double, C.c_double, ip,
+                                       dp, dp, dp]
+        L.oracle_beta_sabine_weighted.restype = C.c_int
+        L.oracle_beta_sabine_weighted.argtypes = [dp, C.c_double, dp, C.c_int, C.c_int, dp, ip]
         L.oracle_simulate_rir.restype = C.c_int
-        L.oracle_simulate_rir.argtypes = [dp, dp, dp, C.c_int, dp, C.c_int, dp, C.c_int, ip, C.c_double,
+        L.oracle_simulate_rir.argtypes = [dp, dp, dp, C.c_int, dp, C.c_int, dp, C.c_int, dp, C.c_int, ip, C.c_double,
                                           C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64,
                                           C.c_uint64, C.c_int, C.c_int, dp]
         L.oracle_max_threads.restype = C.c_int
@@ -139,6 +142,18 @@ def beta_sabine(room, T60: float, sign: int = -1, clamp: bool = False) -> tuple[
     return out, bool(cl.value)
 
 
+def beta_sabine_weighted(room, T60: float, weights, sign: int = -1, clamp: bool = False) -> tuple[np.ndarray, bool]:
+    """NEXT row f3 (reading R9): alpha_i = w_i alpha0 with Sabine's T60 (Eq. 7) met exactly."""
+    r, w = _d(room), _d(weights)
+    out = np.zeros(6)
+    cl = C.c_int(0)
+    st = lib().oracle_beta_sabine_weighted(_dp(r), float(T60), _dp(w), int(sign), int(bool(clamp)), _dp(out),
+                                           C.byref(cl))
+    if st != 0:
+        raise OracleError(st, "beta_sabine_weighted")
+    return out, bool(cl.value)
+
+
 def att2t(att_dB: float, T60: float) -> float:
     return lib().oracle_att2t(float(att_dB), float(T60))
 
@@ -174,7 +189,7 @@ def logistic_stream(seed: int, r: int, k0: int, n: int) -> np.ndarray:
     return out
 
 
-def image_set(room, beta, src, rcv, nb, fs=16000.0, c=343.0, pattern=0, orv=None):
+def image_set(room, beta, src, rcv, nb, fs=16000.0, c=343.0, pattern=0, orv=None, spkr_pattern=0, ors=None):
     """All lattice images of one (src, rcv): dict with n [N,3], x (delay in samples), A, beta."""
     nb = np.ascontiguousarray(np.asarray(nb, dtype=np.int32))
     N = int(np.prod(nb.astype(np.int64)))
@@ -184,15 +199,17 @@ def image_set(room, beta, src, rcv, nb, fs=16000.0, c=343.0, pattern=0, orv=None
     b_out = np.zeros(N)
     r, b, s, q = _d(room), _d(beta), _d(src), _d(rcv)
     o = _d(orv if orv is not None else [0.0, 0.0, 1.0])
-    cnt = lib().oracle_image_set(_dp(r), _dp(b), _dp(s), _dp(q), _dp(o), int(pattern), _ip(nb), float(fs),
-                                 float(c), _ip(n_out), _dp(x_out), _dp(A_out), _dp(b_out))
+    os_ = _d(ors if ors is not None else [0.0, 0.0, 1.0])
+    cnt = lib().oracle_image_set(_dp(r), _dp(b), _dp(s), _dp(q), _dp(o), int(pattern), _dp(os_), int(spkr_pattern),
+                                 _ip(nb), float(fs), float(c), _ip(n_out), _dp(x_out), _dp(A_out), _dp(b_out))
     if cnt < 0:
         raise OracleError(-cnt, "image_set")
     return {"n": n_out, "x": x_out, "A": A_out, "beta": b_out}
 
 
 def simulate_rir(room, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs=16000.0, c=343.0, pattern=0,
-                 orV_rcv=None, Tw=4e-3, seed=0, rir_index_base=0, dense=False, nthreads=0) -> np.ndarray:
+                 orV_rcv=None, Tw=4e-3, seed=0, rir_index_base=0, dense=False, nthreads=0, spkr_pattern=0,
+                 orV_src=None) -> np.ndarray:
     """Oracle RIRs [M_src][M_rcv][nSamples] in float64 (P:274 layout)."""
     src = _d(pos_src).reshape(-1, 3)
     rcv = _d(pos_rcv).reshape(-1, 3)
@@ -200,10 +217,12 @@ def simulate_rir(room, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs=16000.0, 
     nS = nsamples(Tmax, fs)
     out = np.zeros((Ms, Mr, nS))
     orv = None if orV_rcv is None else _d(orV_rcv).reshape(-1, 3)
+    ors = None if orV_src is None else _d(orV_src).reshape(-1, 3)
     nb = np.ascontiguousarray(np.asarray(nb_img, dtype=np.int32))
     r, b = _d(room), _d(beta)
     st = lib().oracle_simulate_rir(_dp(r), _dp(b), _dp(src), Ms, _dp(rcv), Mr,
-                                   _dp(orv) if orv is not None else None, int(pattern), _ip(nb), float(Tdiff),
+                                   _dp(orv) if orv is not None else None, int(pattern),
+                                   _dp(ors) if ors is not None else None, int(spkr_pattern), _ip(nb), float(Tdiff),
                                    float(Tmax), float(fs), float(c), float(Tw), int(seed), int(rir_index_base),
                                    int(bool(dense)), int(nthreads), _dp(out))
     if st != 0:

@@ -19,7 +19,10 @@
  * enumeration of the image set, reciprocity, lattice completeness, Sabine
  * helper values printed in SPEC.md, Philox4x32-10 known-answer vectors,
  * logistic-noise moments, energy-decay slope vs Sabine, the dense
- * formulation vs the support-restricted loop, cross-implementation goldens.
+ * formulation vs the support-restricted loop, cross-implementation goldens;
+ * for the f3 extensions: source directivity vs the mirror BFS's reflected
+ * orientation, vs the specular point of a first-order reflection, special
+ * angles, directional reciprocity; weighted beta vs Sabine's Eq. (7).
  * Functions without such a pin: none (oracle_lut_build and the Eq. 10/11
  * polynomials are pinned by the values the paper prints for their
  * coefficients and by their closed-form special points).
@@ -80,6 +83,33 @@ static double pattern_a(int pattern) {
   return -1.0;
 }
 
+/* Source directivity (NEXT row f3, reading R10; not in the paper, which  */
+/* gives only the receiver pattern): the image source n is the     */
+/* source mirrored along every axis on which Eq. (1) mirrors it (n odd),  */
+/* so it carries the source orientation o_s with those components negated */
+/* and radiates toward the receiver along p_r - p_n:                      */
+/* g_s = a_s + (1 - a_s) (M_n o_s) . (p_r - p_n) / d_n, M_n = diag((-1)^n). */
+static double source_gain(double a_s, const double os[3], const int n[3], const double p[3], const double rcv[3],
+                          double d) {
+  double c = 0.0;
+  for (int ax = 0; ax < 3; ax++) {
+    double o = (n[ax] % 2 != 0) ? -os[ax] : os[ax];
+    c += o * (rcv[ax] - p[ax]);
+  }
+  return a_s + (1.0 - a_s) * c / d;
+}
+
+/* Unit orientation of a directional pattern; EINVAL for a zero vector. */
+static int unit_orientation(int pattern, const double* v, double o[3]) {
+  o[0] = o[1] = o[2] = 0.0;
+  if (pattern == 0) return OR_OK;
+  if (!v) return OR_EINVAL;
+  double on = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  if (!(on > 0.0)) return OR_EINVAL;
+  for (int i = 0; i < 3; i++) o[i] = v[i] / on;
+  return OR_OK;
+}
+
 /* ------------------------------------------------------------------ */
 /* Eq. (6), P:127-134 with T_w = window length (s), f_c = fs/2 (C7):   */
 /* delta'(t) = 1/2 (1 + cos(2 pi t / T_w)) sinc(2 pi f_c t), |t|<T_w/2 */
@@ -126,6 +156,37 @@ int oracle_beta_sabine(const double room[3], double T60, int sign, int clamp, do
   }
   double b = sqrt(1.0 - alpha) * (sign < 0 ? -1.0 : 1.0);
   for (int i = 0; i < 6; i++) beta_out[i] = b;
+  return OR_OK;
+}
+
+/* NEXT row f3 (the helper of P:276 with non-uniform walls, reading R9): */
+/* alpha_i = w_i alpha0 with alpha0 fixed by Eq. (7), 0.161 V / sum_i S_i w_i alpha0   */
+/* = T60, i.e. alpha0 = 0.161 V / (T60 sum_i S_i w_i); beta_i = sign sqrt(1 - alpha_i). */
+/* Weights w_i >= 0, not all zero.  Some alpha_i > 1 -> EINFEASIBLE unless clamp (then  */
+/* beta = 0 everywhere, anechoic).                                                     */
+int oracle_beta_sabine_weighted(const double room[3], double T60, const double w[6], int sign, int clamp,
+                                double beta_out[6], int* clamped) {
+  if (clamped) *clamped = 0;
+  if (!(T60 > 0.0) || !(room[0] > 0 && room[1] > 0 && room[2] > 0)) return OR_EINVAL;
+  double V = room[0] * room[1] * room[2];
+  double S[6] = {room[1] * room[2], room[1] * room[2], room[0] * room[2],
+                 room[0] * room[2], room[0] * room[1], room[0] * room[1]};
+  double Sw = 0.0;
+  for (int i = 0; i < 6; i++) {
+    if (!(w[i] >= 0.0)) return OR_EINVAL;
+    Sw += S[i] * w[i];
+  }
+  if (!(Sw > 0.0)) return OR_EINVAL;
+  double alpha0 = 0.161 * V / (T60 * Sw);
+  for (int i = 0; i < 6; i++) {
+    if (w[i] * alpha0 > 1.0) {
+      if (!clamp) return OR_EINFEASIBLE;
+      if (clamped) *clamped = 1;
+      for (int j = 0; j < 6; j++) beta_out[j] = 0.0;
+      return OR_OK;
+    }
+  }
+  for (int i = 0; i < 6; i++) beta_out[i] = sqrt(1.0 - w[i] * alpha0) * (sign < 0 ? -1.0 : 1.0);
   return OR_OK;
 }
 
@@ -194,17 +255,13 @@ double oracle_logistic(double u) { return sqrt(3.0) / OR_PI * log(u / (1.0 - u))
 /* Returns the number of images, or -status on error.                  */
 /* ------------------------------------------------------------------ */
 long oracle_image_set(const double room[3], const double beta[6], const double src[3], const double rcv[3],
-                      const double orv[3], int pattern, const int nb[3], double fs, double c, int* n_out,
-                      double* x_out, double* A_out, double* beta_out) {
-  double a = pattern_a(pattern);
-  if (a < 0.0) return -OR_EINVAL;
-  double o[3] = {0, 0, 0};
-  if (pattern != 0) {
-    if (!orv) return -OR_EINVAL;
-    double on = sqrt(orv[0] * orv[0] + orv[1] * orv[1] + orv[2] * orv[2]);
-    if (!(on > 0.0)) return -OR_EINVAL;
-    for (int i = 0; i < 3; i++) o[i] = orv[i] / on;
-  }
+                      const double orv[3], int pattern, const double ors[3], int spkr_pattern, const int nb[3],
+                      double fs, double c, int* n_out, double* x_out, double* A_out, double* beta_out) {
+  double a = pattern_a(pattern), a_s = pattern_a(spkr_pattern);
+  if (a < 0.0 || a_s < 0.0) return -OR_EINVAL;
+  double o[3], os[3];
+  if (unit_orientation(pattern, orv, o) != OR_OK) return -OR_EINVAL;
+  if (unit_orientation(spkr_pattern, ors, os) != OR_OK) return -OR_EINVAL;
   long idx = 0;
   for (int nz = lattice_lo(nb[2]); nz < lattice_hi(nb[2]); nz++) {
     for (int ny = lattice_lo(nb[1]); ny < lattice_hi(nb[1]); ny++) {
@@ -223,9 +280,10 @@ long oracle_image_set(const double room[3], const double beta[6], const double s
         if (d == 0.0) return -OR_EDEGENERATE;
         double g = 1.0;
         if (pattern != 0) g = a + (1.0 - a) * (D[0] * o[0] + D[1] * o[1] + D[2] * o[2]) / d;
+        if (spkr_pattern != 0) g *= source_gain(a_s, os, n, p, rcv, d);
         if (n_out) { n_out[3 * idx] = nx; n_out[3 * idx + 1] = ny; n_out[3 * idx + 2] = nz; }
         if (x_out) x_out[idx] = d / c * fs;                   /* Eq. (3): tau = d / c */
-        if (A_out) A_out[idx] = bn * g / (4.0 * OR_PI * d);   /* Eq. (4) */
+        if (A_out) A_out[idx] = bn * g / (4.0 * OR_PI * d);   /* Eq. (4), g = receiver x source gain */
         if (beta_out) beta_out[idx] = bn;
         idx++;
       }
@@ -243,17 +301,14 @@ long oracle_image_set(const double room[3], const double beta[6], const double s
 /* support |k - x| < T_w fs / 2 (identical).                     */
 /* ------------------------------------------------------------------ */
 static int one_rir(const double room[3], const double beta[6], const double src[3], const double rcv[3],
-                   const double* orv, int pattern, const int nb[3], long nISM, long nS, double fs, double c,
-                   double Tw, uint64_t seed, uint64_t r_global, int dense, double* h) {
+                   const double* orv, int pattern, const double* ors, int spkr_pattern, const int nb[3], long nISM,
+                   long nS, double fs, double c, double Tw, uint64_t seed, uint64_t r_global, int dense, double* h) {
   for (long k = 0; k < nS; k++) h[k] = 0.0;
-  double a = pattern_a(pattern);
-  if (a < 0.0) return OR_EINVAL;
-  double o[3] = {0, 0, 0};
-  if (pattern != 0) {
-    double on = sqrt(orv[0] * orv[0] + orv[1] * orv[1] + orv[2] * orv[2]);
-    if (!(on > 0.0)) return OR_EINVAL;
-    for (int i = 0; i < 3; i++) o[i] = orv[i] / on;
-  }
+  double a = pattern_a(pattern), a_s = pattern_a(spkr_pattern);
+  if (a < 0.0 || a_s < 0.0) return OR_EINVAL;
+  double o[3], os[3];
+  if (unit_orientation(pattern, orv, o) != OR_OK) return OR_EINVAL;
+  if (unit_orientation(spkr_pattern, ors, os) != OR_OK) return OR_EINVAL;
   double H = Tw * fs / 2.0; /* half window in samples */
   long nI = nISM < nS ? nISM : nS;
   for (int nz = lattice_lo(nb[2]); nz < lattice_hi(nb[2]); nz++) {
@@ -272,6 +327,7 @@ static int one_rir(const double room[3], const double beta[6], const double src[
         if (d == 0.0) return OR_EDEGENERATE;
         double g = 1.0;
         if (pattern != 0) g = a + (1.0 - a) * (D[0] * o[0] + D[1] * o[1] + D[2] * o[2]) / d;
+        if (spkr_pattern != 0) g *= source_gain(a_s, os, n, p, rcv, d);
         double A = bn * g / (4.0 * OR_PI * d);
         double tau = d / c;
         if (dense) {
@@ -320,9 +376,11 @@ static int one_rir(const double room[3], const double beta[6], const double src[
 }
 
 /* Full call: RIR r = m_src * M_rcv + m_rcv, output [M_src][M_rcv][nSamples]. */
-/* src: M_src x 3, rcv: M_rcv x 3, orv: M_rcv x 3 or NULL (omni).                     */
+/* src: M_src x 3, rcv: M_rcv x 3, orv: M_rcv x 3 or NULL (omni receivers),          */
+/* ors: M_src x 3 or NULL (omni sources, reading R10).                                */
 int oracle_simulate_rir(const double room[3], const double beta[6], const double* src, int M_src,
-                        const double* rcv, int M_rcv, const double* orv, int pattern, const int nb[3],
+                        const double* rcv, int M_rcv, const double* orv, int pattern, const double* ors,
+                        int spkr_pattern, const int nb[3],
                         double Tdiff, double Tmax, double fs, double c, double Tw, uint64_t seed,
                         uint64_t rir_index_base, int dense, int nthreads, double* out) {
   if (M_src <= 0 || M_rcv <= 0 || !(fs > 0) || !(c > 0) || !(Tmax > 0) || Tdiff < 0) return OR_EINVAL;
@@ -331,6 +389,8 @@ int oracle_simulate_rir(const double room[3], const double beta[6], const double
     if (fabs(beta[i]) > 1.0) return OR_EINVAL;
   if (pattern < 0 || pattern > 4) return OR_EINVAL;
   if (pattern != 0 && !orv) return OR_EINVAL;
+  if (spkr_pattern < 0 || spkr_pattern > 4) return OR_EINVAL;
+  if (spkr_pattern != 0 && !ors) return OR_EINVAL;
   long nS = oracle_nsamples(Tmax, fs);
   long nISM = oracle_nsamples(Tdiff, fs);
   int M = M_src * M_rcv;
@@ -341,8 +401,9 @@ int oracle_simulate_rir(const double room[3], const double beta[6], const double
 #endif
   for (int r = 0; r < M; r++) {
     int ms = r / M_rcv, mr = r % M_rcv;
-    int st = one_rir(room, beta, src + 3 * ms, rcv + 3 * mr, orv ? orv + 3 * mr : NULL, pattern, nb, nISM, nS,
-                     fs, c, Tw, seed, rir_index_base + (uint64_t)r, dense, out + (size_t)r * nS);
+    int st = one_rir(room, beta, src + 3 * ms, rcv + 3 * mr, orv ? orv + 3 * mr : NULL, pattern,
+                     ors ? ors + 3 * ms : NULL, spkr_pattern, nb, nISM, nS, fs, c, Tw, seed,
+                     rir_index_base + (uint64_t)r, dense, out + (size_t)r * nS);
     if (st != OR_OK) {
 #ifdef _OPENMP
 #pragma omp critical

@@ -95,7 +95,7 @@ def _mirror_bfs(room, beta, src, order):
     ignored, while all shortest sequences to a room must agree."""
     L = np.asarray(room, float)
     start = (tuple(np.asarray(src, float)), (0, 0, 0), (False, False, False), 1.0)
-    seen = {(0, 0, 0): (np.asarray(src, float), 1.0, 0)}
+    seen = {(0, 0, 0): (np.asarray(src, float), 1.0, 0, (False, False, False))}
     frontier = [start]
     for depth in range(1, order + 1):
         nxt = []
@@ -119,7 +119,7 @@ def _mirror_bfs(room, beta, src, order):
                         if seen[key][2] == depth:
                             assert abs(seen[key][1] - nb) < 1e-12
                         continue
-                    seen[key] = (np.asarray(newpos), nb, depth)
+                    seen[key] = (np.asarray(newpos), nb, depth, tuple(nf))
                     nxt.append((tuple(newpos), key, tuple(nf), nb))
         frontier = nxt
     return seen
@@ -136,10 +136,113 @@ def test_image_set_vs_mirror_bfs(oracle, nb):
     bfs = _mirror_bfs(room, beta, src, order)
     assert len(imgs["x"]) == int(np.prod(nb))
     for n, x, bn in zip(imgs["n"], imgs["x"], imgs["beta"]):
-        pos, bprod, _ = bfs[tuple(int(v) for v in n)]
+        pos, bprod = bfs[tuple(int(v) for v in n)][:2]
         d = np.linalg.norm(pos - np.asarray(rcv))
         assert abs(x - d / c * fs) < 1e-9
         assert abs(bn - bprod) < 1e-12
+
+
+@pytest.mark.parametrize("spkr,mic", [(2, 0), (4, 3), (1, 2)])
+def test_source_directivity_vs_mirror_bfs(oracle, spkr, mic):
+    """f3 (reading R10): every image source carries the source orientation mirrored by the reflections that
+    produced it (tracked independently by the BFS as flipped axes) and radiates along p_r - p_n, so
+    A_n = beta_n g_r g_s / (4 pi d_n) with g_s = a_s + (1 - a_s) cos(theta_s)."""
+    room = [3.0, 4.0, 2.5]
+    beta = [-0.9, 0.8, -0.7, 0.95, 0.6, -0.85]
+    src, rcv = [0.7, 1.3, 0.9], [2.2, 3.1, 1.7]
+    os_, orv = np.array([0.3, -0.5, 0.8]), np.array([-0.6, 0.2, 0.4])
+    nb = (5, 4, 5)
+    a = {0: 1.0, 1: 0.75, 2: 0.5, 3: 0.25, 4: 0.0}
+    imgs = oracle.image_set(room, beta, src, rcv, nb, pattern=mic, orv=orv, spkr_pattern=spkr, ors=os_)
+    bfs = _mirror_bfs(room, beta, src, sum(int(math.ceil(N / 2)) for N in nb) + 3)
+    us, ur = os_ / np.linalg.norm(os_), orv / np.linalg.norm(orv)
+    for n, A in zip(imgs["n"], imgs["A"]):
+        pos, bprod, _, flipped = bfs[tuple(int(v) for v in n)]
+        o_img = np.where(flipped, -us, us)  # the orientation reflected with the source
+        d = np.linalg.norm(pos - np.asarray(rcv))
+        gs = a[spkr] + (1 - a[spkr]) * np.dot(o_img, np.asarray(rcv) - pos) / d
+        gr = a[mic] + (1 - a[mic]) * np.dot(ur, pos - np.asarray(rcv)) / d
+        assert abs(A - bprod * gs * gr / (4 * math.pi * d)) < 1e-13
+
+
+def test_source_directivity_reflection_point(oracle):
+    """f3: a first-order reflection off wall x0 leaves the source toward the specular point on x = 0, found
+    by intersecting the receiver -> image line with the wall plane (no image arithmetic involved)."""
+    room, src, rcv = [5.0, 4.0, 3.0], np.array([1.5, 1.2, 1.0]), np.array([3.5, 2.9, 1.8])
+    beta = [1.0, 0.0, 0.0, 0.0, 0.0, 0.0]  # only the direct path and the x0 reflection survive
+    o = np.array([-1.0, 0.2, 0.1])
+    im = oracle.image_set(room, beta, src, rcv, [3, 1, 1], spkr_pattern=2, ors=o)
+    uo = o / np.linalg.norm(o)
+    mirror = np.array([-src[0], src[1], src[2]])
+    t = rcv[0] / (rcv[0] - mirror[0])                  # receiver -> image line meets x = 0
+    q = rcv + t * (mirror - rcv)
+    dep = (q - src) / np.linalg.norm(q - src)
+    d = np.linalg.norm(rcv - mirror)
+    want = {(-1, 0, 0): (0.5 + 0.5 * np.dot(uo, dep)) / (4 * math.pi * d),
+            (0, 0, 0): (0.5 + 0.5 * np.dot(uo, (rcv - src) / np.linalg.norm(rcv - src)))
+            / (4 * math.pi * np.linalg.norm(rcv - src)),
+            (1, 0, 0): 0.0}
+    for n, A in zip(im["n"], im["A"]):
+        assert A == pytest.approx(want[tuple(int(v) for v in n)], abs=1e-15)
+
+
+def test_source_pattern_special_cases(oracle):
+    """f3, beta = 0: direct path only, g_s from the angle between the source axis and r - s (cardioid
+    1 toward / 0 away, bidirectional 0 broadside, hypercardioid a = 0.25 broadside)."""
+    room, src, rcv = [10.0, 10.0, 10.0], [2.0, 5.0, 5.0], [5.0, 5.0, 5.0]
+    cases = [(2, [1, 0, 0], 1.0), (2, [-1, 0, 0], 0.0), (4, [0, 0, 1], 0.0), (3, [0, 1, 0], 0.25),
+             (1, [-1, 0, 0], 0.5)]
+    for pat, o, g in cases:
+        im = oracle.image_set(room, [0.0] * 6, src, rcv, [1, 1, 1], spkr_pattern=pat, ors=o)
+        assert im["A"][0] == pytest.approx(g / (4 * math.pi * 3.0), abs=1e-15)
+
+
+def test_directional_reciprocity(oracle):
+    """f3: swapping source and receiver together with their patterns and orientations gives an identical
+    RIR (odd N, non-uniform walls): the arrival direction of one is the departure direction of the other."""
+    room = [3.0, 4.0, 2.5]
+    beta = np.array([-0.9, 0.8, -0.7, 0.95, 0.6, -0.85])
+    nb = oracle.t2n(0.05, room)
+    s, r = [1.2, 1.5, 1.1], [2.1, 2.9, 1.4]
+    oa, ob = [0.3, -0.5, 0.8], [-0.6, 0.2, 0.4]
+    h1 = oracle.simulate_rir(room, beta, [s], [r], nb, 0.05, 0.05, pattern=3, orV_rcv=[ob], spkr_pattern=2,
+                             orV_src=[oa])
+    h2 = oracle.simulate_rir(room, beta, [r], [s], nb, 0.05, 0.05, pattern=2, orV_rcv=[oa], spkr_pattern=3,
+                             orV_src=[ob])
+    h0 = oracle.simulate_rir(room, beta, [s], [r], nb, 0.05, 0.05)
+    assert np.max(np.abs(h1 - h2)) < 1e-12 * np.max(np.abs(h1))
+    assert np.max(np.abs(h1 - h0)) > 1e-2 * np.max(np.abs(h0))  # the patterns do change the RIR
+
+
+def test_weighted_beta_sabine(oracle):
+    """f3 (reading R9): non-uniform absorption weights meet Sabine's T60 exactly (Eq. 7), keep the
+    absorption ratios alpha_i / alpha_j = w_i / w_j, reduce to the uniform helper for equal weights, and
+    report infeasibility when a wall would need alpha > 1."""
+    rng = np.random.default_rng(9)
+    for _ in range(200):
+        room = rng.uniform(2, 10, 3)
+        w = rng.uniform(0.1, 1.0, 6)
+        T = rng.uniform(0.5, 3.0)
+        try:
+            b, _ = oracle.beta_sabine_weighted(room, T, w)
+        except oracle.OracleError as e:
+            assert e.status == 3
+            continue
+        assert abs(oracle.sabine_t60(room, b) - T) / T < 1e-12
+        al = 1 - b ** 2
+        assert np.allclose(al / al[0], w / w[0], rtol=1e-12)
+        assert np.all(b <= 0)
+    room = [3.0, 4.0, 2.5]
+    bu, _ = oracle.beta_sabine(room, 0.7)
+    bw, _ = oracle.beta_sabine_weighted(room, 0.7, [2.0] * 6)
+    assert np.allclose(bu, bw, rtol=0, atol=1e-15)
+    with pytest.raises(oracle.OracleError) as ei:
+        oracle.beta_sabine_weighted(room, 0.2, [1, 1, 1, 1, 1, 20])
+    assert ei.value.status == 3
+    b, cl = oracle.beta_sabine_weighted(room, 0.2, [1, 1, 1, 1, 1, 20], clamp=True)
+    assert cl and np.all(b == 0)
+    bz, _ = oracle.beta_sabine_weighted(room, 0.7, [1, 1, 0, 0, 1, 1])  # y walls reflect perfectly
+    assert bz[2] == -1.0 and bz[3] == -1.0
 
 
 def test_image_amp_example(oracle):
