@@ -104,6 +104,21 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
                         const float* pos_rcv, int M_rcv, const float* orV_rcv, int mic_pattern, const int nb_img[3],
                         double Tdiff, double Tmax, double fs, double c, float* out, const gpurir_opts* opts);
 
+/*
+ * gpurir_simulate_rir_dir — gpurir_simulate_rir with a directional source (reading
+ * R10 of DESIGN.md; the paper models only the receiver pattern).
+ *   orV_src      device float[M_src][3]  source orientations (normalised on the device), may be NULL only
+ *                                       when spkr_pattern == GPURIR_OMNI
+ *   spkr_pattern gpurir_pattern of every source: g_s = a + (1 - a) cos(theta_s), theta_s between the
+ *                image's mirrored source orientation diag((-1)^n) o_s and p_r - p_n.
+ * A_n = beta_n g_rcv g_src / (4 pi d_n).  Other arguments, layout and errors as gpurir_simulate_rir, which
+ * is this call with an omni source (bit-identical results).
+ */
+int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const float* pos_src, int M_src,
+                            const float* orV_src, int spkr_pattern, const float* pos_rcv, int M_rcv,
+                            const float* orV_rcv, int mic_pattern, const int nb_img[3], double Tdiff, double Tmax,
+                            double fs, double c, float* out, const gpurir_opts* opts);
+
 /* One independent room of a batch (config 5; a deviation from the paper's
  * same-room-only batching).  out_offset = element offset of this RIR's
  * row in the batch output buffer (ragged rows of ceil(Tmax fs) samples). */
@@ -118,6 +133,8 @@ typedef struct {
   double Tdiff;
   double Tmax;
   long long out_offset;
+  float orV_src[3]; /* source orientation (f3), ignored for an omni source */
+  int spkr_pattern; /* source gpurir_pattern (f3), GPURIR_OMNI = 0 for the paper's omni source */
 } gpurir_room;
 
 /*
@@ -159,6 +176,13 @@ double gpurir_sabine_t60(const float room_sz[3], const float beta[6]);
  * EINFEASIBLE unless clamp != 0, which returns beta = 0 (anechoic) and sets *clamped = 1. */
 int gpurir_beta_sabine(const float room_sz[3], double T60, int sign, int clamp, float beta_out[6], int* clamped);
 
+/* Non-uniform absorption (reading R9): alpha_i = weights[i] alpha0 with Sabine's Eq. 7
+ * met exactly, alpha0 = 0.161 V / (T60 sum_i S_i weights[i]); beta_i = sign sqrt(1 - alpha_i).  weights
+ * host float[6] >= 0, not all 0 (else EINVAL); some alpha_i > 1 returns EINFEASIBLE unless clamp != 0
+ * (then beta = 0, *clamped = 1).  Equal weights give gpurir_beta_sabine's result. */
+int gpurir_beta_sabine_weighted(const float room_sz[3], double T60, const float weights[6], int sign, int clamp,
+                                float beta_out[6], int* clamped);
+
 /* A18: time at which the exponential decay reaches att_dB: att_dB / 60 * T60. */
 double gpurir_att2t_sabine(double att_dB, double T60);
 
@@ -173,13 +197,14 @@ int gpurir_t2n(double T, const float room_sz[3], double c, int nb_img_out[3]);
  * one (source, receiver) pair for every lattice image, in lattice order (n_x fastest, then n_y,
  * then n_z), computed by the same device code the accumulation kernel inlines.
  *   src, rcv, orv  host float[3] (orv ignored for omni)
+ *   ors, spkr_pattern  source orientation host float[3] and pattern (f3; ors ignored / may be NULL for omni)
  *   x_out  device double[N]  delay in samples, tau_n * fs
- *   A_out  device float[N]   amplitude beta_n g / (4 pi d_n)
+ *   A_out  device float[N]   amplitude beta_n g_rcv g_src / (4 pi d_n)
  * Synchronises the stream.  Returns EDEGENERATE if some d_n = 0.
  */
 int gpurir_image_params(const float room_sz[3], const float beta[6], const float src[3], const float rcv[3],
-                        const float orv[3], int mic_pattern, const int nb_img[3], double fs, double c,
-                        double* x_out, float* A_out, void* stream);
+                        const float orv[3], int mic_pattern, const float ors[3], int spkr_pattern,
+                        const int nb_img[3], double fs, double c, double* x_out, float* A_out, void* stream);
 
 /* Windowed-sinc table of Eq. 9 (erratum C11) exactly as uploaded for GPURIR_LUT: entries
  * LUT[n], n = -half..half, written to host lut_out[0 .. 2 half] when lut_out != NULL and

@@ -21,7 +21,7 @@ EXPORTS = [
     "gpurir_opts_default", "gpurir_simulate_rir", "gpurir_simulate_rir_batch", "gpurir_nsamples",
     "gpurir_sabine_t60", "gpurir_beta_sabine", "gpurir_att2t_sabine", "gpurir_t2n", "gpurir_image_params",
     "gpurir_lut_table", "gpurir_device_status", "gpurir_strerror", "gpurir_last_cuda_error", "gpurir_version",
-    "gpurir_simulate_trajectory",
+    "gpurir_simulate_trajectory", "gpurir_simulate_rir_dir", "gpurir_beta_sabine_weighted",
 ]
 
 
@@ -34,7 +34,8 @@ class Opts(C.Structure):
 class Room(C.Structure):
     _fields_ = [("room_sz", C.c_float * 3), ("beta", C.c_float * 6), ("pos_src", C.c_float * 3),
                 ("pos_rcv", C.c_float * 3), ("orV_rcv", C.c_float * 3), ("mic_pattern", C.c_int),
-                ("nb_img", C.c_int * 3), ("Tdiff", C.c_double), ("Tmax", C.c_double), ("out_offset", C.c_longlong)]
+                ("nb_img", C.c_int * 3), ("Tdiff", C.c_double), ("Tmax", C.c_double), ("out_offset", C.c_longlong),
+                ("orV_src", C.c_float * 3), ("spkr_pattern", C.c_int)]
 
 
 class GpurirError(RuntimeError):
@@ -63,6 +64,11 @@ def lib() -> C.CDLL:
     L.gpurir_simulate_rir.restype = C.c_int
     L.gpurir_simulate_rir.argtypes = [fp, fp, vp, C.c_int, vp, C.c_int, vp, C.c_int, ip, C.c_double, C.c_double,
                                       C.c_double, C.c_double, vp, C.POINTER(Opts)]
+    L.gpurir_simulate_rir_dir.restype = C.c_int
+    L.gpurir_simulate_rir_dir.argtypes = [fp, fp, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, ip, C.c_double,
+                                          C.c_double, C.c_double, C.c_double, vp, C.POINTER(Opts)]
+    L.gpurir_beta_sabine_weighted.restype = C.c_int
+    L.gpurir_beta_sabine_weighted.argtypes = [fp, C.c_double, fp, C.c_int, C.c_int, fp, ip]
     L.gpurir_simulate_rir_batch.restype = C.c_int
     L.gpurir_simulate_rir_batch.argtypes = [C.c_int, C.POINTER(Room), C.c_double, C.c_double, vp, C.POINTER(Opts)]
     L.gpurir_simulate_trajectory.restype = C.c_int
@@ -78,7 +84,8 @@ def lib() -> C.CDLL:
     L.gpurir_t2n.restype = C.c_int
     L.gpurir_t2n.argtypes = [C.c_double, fp, C.c_double, ip]
     L.gpurir_image_params.restype = C.c_int
-    L.gpurir_image_params.argtypes = [fp, fp, fp, fp, fp, C.c_int, ip, C.c_double, C.c_double, vp, vp, vp]
+    L.gpurir_image_params.argtypes = [fp, fp, fp, fp, fp, C.c_int, fp, C.c_int, ip, C.c_double, C.c_double, vp, vp,
+                                      vp]
     L.gpurir_lut_table.restype = C.c_longlong
     L.gpurir_lut_table.argtypes = [C.c_double, C.c_double, C.c_int, fp, C.c_longlong]
     L.gpurir_device_status.restype = C.c_int

@@ -82,18 +82,22 @@ def _dev_f32(t, name, rows=None):
 
 def simulate_rir(room_sz, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs, c=343.0, orV_rcv=None,
                  mic_pattern="omni", mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0, out=None,
-                 stream=None, split=0, sync=False, ev_ism=None, ev_tail=None):
+                 stream=None, split=0, sync=False, ev_ism=None, ev_tail=None, orV_src=None, spkr_pattern="omni"):
     """gpurir_simulate_rir: RIRs [M_src][M_rcv][ceil(Tmax fs)] (float32, on pos_src's device).
 
     room_sz (3) and beta (6, wall order x0,x1,y0,y1,z0,z1) are host values; pos_src [M_src,3],
     pos_rcv [M_rcv,3] and orV_rcv [M_rcv,3] are CUDA float32 tensors.  Stream-ordered; returns `out`.
+    A directional source (orV_src [M_src,3], spkr_pattern; NEXT row f3) goes through gpurir_simulate_rir_dir.
     """
     import torch
     pos_src = _dev_f32(pos_src, "pos_src", rows=True)
     pos_rcv = _dev_f32(pos_rcv, "pos_rcv", rows=True)
     pat = _pattern(mic_pattern)
+    spat = _pattern(spkr_pattern)
     if orV_rcv is not None:
         orV_rcv = _dev_f32(orV_rcv, "orV_rcv", rows=True)
+    if orV_src is not None:
+        orV_src = _dev_f32(orV_src, "orV_src", rows=True)
     Ms, Mr = pos_src.shape[0], pos_rcv.shape[0]
     nS = nsamples(Tmax, fs)
     if out is None:
@@ -101,10 +105,18 @@ def simulate_rir(room_sz, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs, c=343
     elif out.dtype != torch.float32 or not out.is_contiguous() or out.numel() < Ms * Mr * nS:
         raise ValueError("out must be contiguous float32 with M_src*M_rcv*nSamples elements")
     o = make_opts(mode, Tw, lut_Q, seed, rir_index_base, stream, split, sync, ev_ism, ev_tail)
-    st = lib().gpurir_simulate_rir(_f3(room_sz), _f3(beta, 6), pos_src.data_ptr(), Ms, pos_rcv.data_ptr(), Mr,
-                                   orV_rcv.data_ptr() if orV_rcv is not None else None, pat, _i3(nb_img),
-                                   float(Tdiff), float(Tmax), float(fs), float(c), out.data_ptr(), C.byref(o))
-    check(st, "gpurir_simulate_rir")
+    ov = orV_rcv.data_ptr() if orV_rcv is not None else None
+    if spat == 0 and orV_src is None:
+        st = lib().gpurir_simulate_rir(_f3(room_sz), _f3(beta, 6), pos_src.data_ptr(), Ms, pos_rcv.data_ptr(), Mr,
+                                       ov, pat, _i3(nb_img), float(Tdiff), float(Tmax), float(fs), float(c),
+                                       out.data_ptr(), C.byref(o))
+        check(st, "gpurir_simulate_rir")
+    else:
+        st = lib().gpurir_simulate_rir_dir(_f3(room_sz), _f3(beta, 6), pos_src.data_ptr(), Ms,
+                                           orV_src.data_ptr() if orV_src is not None else None, spat,
+                                           pos_rcv.data_ptr(), Mr, ov, pat, _i3(nb_img), float(Tdiff), float(Tmax),
+                                           float(fs), float(c), out.data_ptr(), C.byref(o))
+        check(st, "gpurir_simulate_rir_dir")
     return out
 
 
@@ -119,6 +131,8 @@ def room_array(rooms) -> C.Array:
         R.pos_rcv[:] = [float(x) for x in r["pos_rcv"]]
         R.orV_rcv[:] = [float(x) for x in r.get("orV_rcv", (0.0, 0.0, 1.0))]
         R.mic_pattern = _pattern(r.get("mic_pattern", 0))
+        R.orV_src[:] = [float(x) for x in r.get("orV_src", (0.0, 0.0, 1.0))]
+        R.spkr_pattern = _pattern(r.get("spkr_pattern", 0))
         R.nb_img[:] = [int(x) for x in r["nb_img"]]
         R.Tdiff = float(r["Tdiff"])
         R.Tmax = float(r["Tmax"])
@@ -179,6 +193,16 @@ def beta_sabine(room_sz, T60: float, sign: int = -1, clamp: bool = False) -> tup
     return np.array(list(out), dtype=np.float32), bool(cl.value)
 
 
+def beta_sabine_weighted(room_sz, T60: float, weights, sign: int = -1, clamp: bool = False) -> tuple[np.ndarray, bool]:
+    """Non-uniform absorption (NEXT row f3, reading R9): alpha_i = w_i alpha0, Sabine's T60 met exactly."""
+    out = (C.c_float * 6)()
+    cl = C.c_int(0)
+    st = lib().gpurir_beta_sabine_weighted(_f3(room_sz), float(T60), _f3(weights, 6), int(sign), int(bool(clamp)),
+                                           out, C.byref(cl))
+    check(st, "gpurir_beta_sabine_weighted")
+    return np.array(list(out), dtype=np.float32), bool(cl.value)
+
+
 def att2t_sabine(att_dB: float, T60: float) -> float:
     return float(lib().gpurir_att2t_sabine(float(att_dB), float(T60)))
 
@@ -199,7 +223,8 @@ def lut_table(Tw: float = 4e-3, fs: float = 16000.0, Q: int = 16) -> tuple[np.nd
     return np.array(list(buf), dtype=np.float32), half
 
 
-def image_params(room_sz, beta, src, rcv, nb_img, fs, c=343.0, mic_pattern="omni", orv=None, device=None):
+def image_params(room_sz, beta, src, rcv, nb_img, fs, c=343.0, mic_pattern="omni", orv=None, device=None,
+                 spkr_pattern="omni", ors=None):
     """gpurir_image_params: (delay in samples float64 [N], amplitude float32 [N]) in lattice order."""
     import torch
     N = int(np.prod(np.asarray(nb_img, dtype=np.int64)))
@@ -207,8 +232,9 @@ def image_params(room_sz, beta, src, rcv, nb_img, fs, c=343.0, mic_pattern="omni
     x = torch.empty(N, dtype=torch.float64, device=dev)
     A = torch.empty(N, dtype=torch.float32, device=dev)
     o = _f3(orv) if orv is not None else None
-    st = lib().gpurir_image_params(_f3(room_sz), _f3(beta, 6), _f3(src), _f3(rcv), o, _pattern(mic_pattern),
-                                   _i3(nb_img), float(fs), float(c), x.data_ptr(), A.data_ptr(),
+    os_ = _f3(ors) if ors is not None else None
+    st = lib().gpurir_image_params(_f3(room_sz), _f3(beta, 6), _f3(src), _f3(rcv), o, _pattern(mic_pattern), os_,
+                                   _pattern(spkr_pattern), _i3(nb_img), float(fs), float(c), x.data_ptr(), A.data_ptr(),
                                    _stream_handle(None))
     check(st, "gpurir_image_params")
     return x, A

@@ -326,6 +326,37 @@ int gpurir_beta_sabine(const float room_sz[3], double T60, int sign, int clamp, 
   return GPURIR_OK;
 }
 
+int gpurir_beta_sabine_weighted(const float room_sz[3], double T60, const float weights[6], int sign, int clamp,
+                                float beta_out[6], int* clamped) {
+  if (clamped) *clamped = 0;
+  if (!(T60 > 0.0) || !weights) return GPURIR_EINVAL;
+  for (int i = 0; i < 3; i++)
+    if (!(room_sz[i] > 0.f)) return GPURIR_EINVAL;
+  double Lx = room_sz[0], Ly = room_sz[1], Lz = room_sz[2];
+  const double S[6] = {Ly * Lz, Ly * Lz, Lx * Lz, Lx * Lz, Lx * Ly, Lx * Ly};
+  double Sw = 0.0;
+  for (int i = 0; i < 6; i++) {
+    if (!(weights[i] >= 0.f)) return GPURIR_EINVAL;
+    Sw += S[i] * (double)weights[i];
+  }
+  if (!(Sw > 0.0)) return GPURIR_EINVAL;
+  const double alpha0 = 0.161 * Lx * Ly * Lz / (T60 * Sw);  // Eq. 7 met exactly (reading R9)
+  double alpha[6];
+  bool infeasible = false;
+  for (int i = 0; i < 6; i++) {
+    alpha[i] = (double)weights[i] * alpha0;
+    if (alpha[i] > 1.0) infeasible = true;
+  }
+  if (infeasible) {
+    if (!clamp) return GPURIR_EINFEASIBLE;
+    if (clamped) *clamped = 1;
+    for (int i = 0; i < 6; i++) beta_out[i] = 0.f;
+    return GPURIR_OK;
+  }
+  for (int i = 0; i < 6; i++) beta_out[i] = (float)(sqrt(1.0 - alpha[i]) * (sign < 0 ? -1.0 : 1.0));
+  return GPURIR_OK;
+}
+
 double gpurir_att2t_sabine(double att_dB, double T60) { return att_dB / 60.0 * T60; }
 
 int gpurir_t2n(double T, const float room_sz[3], double c, int nb_img_out[3]) {
@@ -350,6 +381,14 @@ long long gpurir_lut_table(double Tw, double fs, int Q, float* lut_out, long lon
 int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float* pos_src, int M_src,
                         const float* pos_rcv, int M_rcv, const float* orV_rcv, int mic_pattern, const int nb_img[3],
                         double Tdiff, double Tmax, double fs, double c, float* out, const gpurir_opts* opts) {
+  return gpurir_simulate_rir_dir(room_sz, beta, pos_src, M_src, nullptr, GPURIR_OMNI, pos_rcv, M_rcv, orV_rcv,
+                                 mic_pattern, nb_img, Tdiff, Tmax, fs, c, out, opts);
+}
+
+int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const float* pos_src, int M_src,
+                            const float* orV_src, int spkr_pattern, const float* pos_rcv, int M_rcv,
+                            const float* orV_rcv, int mic_pattern, const int nb_img[3], double Tdiff, double Tmax,
+                            double fs, double c, float* out, const gpurir_opts* opts) {
   gpurir_opts o;
   if (opts) o = *opts; else gpurir_opts_default(&o);
   if (!(o.Tw > 0)) o.Tw = 4e-3;
@@ -359,6 +398,7 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
   int st = validate_room(room_sz, beta, nb_img, mic_pattern);
   if (st) return st;
   if (mic_pattern != GPURIR_OMNI && !orV_rcv) return GPURIR_EINVAL;
+  if (spkr_pattern < 0 || spkr_pattern > 4 || (spkr_pattern != GPURIR_OMNI && !orV_src)) return GPURIR_EINVAL;
   if (int em = validate_mode(o)) return em;
   double H = o.Tw * fs / 2.0;
   if ((int)ceil((kTCPersistent + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;  // window too long
@@ -381,6 +421,8 @@ int gpurir_simulate_rir(const float room_sz[3], const float beta[6], const float
     beta_logs(beta, A.lb, &A.neg, &A.zero);
     A.pattern = mic_pattern;
     A.pos_src = pos_src; A.pos_rcv = pos_rcv; A.orv = mic_pattern == GPURIR_OMNI ? nullptr : orV_rcv;
+    A.ors = spkr_pattern == GPURIR_OMNI ? nullptr : orV_src;
+    A.spkr_pattern = spkr_pattern;
     A.M_src = M_src; A.M_rcv = M_rcv; A.M = (int)M;
     A.nISM = (int)nISM;
     A.row_stride = nS;
@@ -447,16 +489,19 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
   for (int i = 0; i < n_rooms; i++) {
     const gpurir_room& R = rooms[i];
     if (int e0 = validate_room(R.room_sz, R.beta, R.nb_img, R.mic_pattern)) return e0;
+    if (R.spkr_pattern < 0 || R.spkr_pattern > 4) return GPURIR_EINVAL;
     if (!(R.Tmax > 0) || !(R.Tdiff >= 0) || R.out_offset < 0) return GPURIR_EINVAL;
     BatchJob& J = jobs[i];
     memset(&J, 0, sizeof(J));
     for (int a = 0; a < 3; a++) {
       J.L[a] = R.room_sz[a]; J.src[a] = R.pos_src[a]; J.rcv[a] = R.pos_rcv[a]; J.orv[a] = R.orV_rcv[a];
+      J.ors[a] = R.orV_src[a];
       J.nb[a] = R.nb_img[a];
     }
     for (int w = 0; w < 6; w++) J.beta[w] = R.beta[w];
     beta_logs(R.beta, J.lb, &J.neg, &J.zero);
     J.pattern = R.mic_pattern;
+    J.spkr_pattern = R.spkr_pattern;
     long long nS = gpurir_nsamples(R.Tmax, fs), nISM = gpurir_nsamples(R.Tdiff, fs);
     if (nISM > nS) nISM = nS;
     if (nS > (1LL << 30)) return GPURIR_EINVAL;
@@ -550,10 +595,11 @@ int gpurir_simulate_trajectory(const float* signal, long long n_sig, const float
 }
 
 int gpurir_image_params(const float room_sz[3], const float beta[6], const float src[3], const float rcv[3],
-                        const float orv[3], int mic_pattern, const int nb_img[3], double fs, double c,
-                        double* x_out, float* A_out, void* stream_) {
+                        const float orv[3], int mic_pattern, const float ors[3], int spkr_pattern,
+                        const int nb_img[3], double fs, double c, double* x_out, float* A_out, void* stream_) {
   int st = validate_room(room_sz, beta, nb_img, mic_pattern);
   if (st) return st;
+  if (spkr_pattern < 0 || spkr_pattern > 4 || (spkr_pattern != GPURIR_OMNI && !ors)) return GPURIR_EINVAL;
   if (!(fs > 0) || !(c > 0) || !x_out || !A_out || !src || !rcv) return GPURIR_EINVAL;
   DeviceState* d = device_state(&st);
   if (!d) return st;
@@ -567,6 +613,8 @@ int gpurir_image_params(const float room_sz[3], const float beta[6], const float
   beta_logs(beta, J.lb, &J.neg, &J.zero);
   J.pattern = mic_pattern;
   if (mic_pattern != GPURIR_OMNI && !orv) return GPURIR_EINVAL;
+  for (int a = 0; a < 3; a++) J.ors[a] = ors ? ors[a] : 0.f;
+  J.spkr_pattern = spkr_pattern;
   BatchJob* dj = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&dj, sizeof(BatchJob), stream);
   if (e != cudaSuccess) return GPURIR_ENOMEM;

@@ -44,14 +44,24 @@ __device__ __forceinline__ float sinpi01(float f) {
 // ----------------------------------------------------------------------------
 // Per-RIR geometry (single-room call or batch job)
 // ----------------------------------------------------------------------------
-static __device__ void geom_from(const float* L, const float* src, const float* rcv, const float* orv, const int* nb,
-                                 int pattern, const float* lb, unsigned neg, unsigned zero, RirGeom& g, int* status) {
-  g.a = pattern == 0 ? 1.f : pattern == 1 ? 0.75f : pattern == 2 ? 0.5f : pattern == 3 ? 0.25f : 0.f;  // C4
-  float o0 = orv[0], o1 = orv[1], o2 = orv[2];
+__device__ __forceinline__ float pattern_const(int pattern) {  // C4
+  return pattern == 0 ? 1.f : pattern == 1 ? 0.75f : pattern == 2 ? 0.5f : pattern == 3 ? 0.25f : 0.f;
+}
+// unit orientation of a directional pattern (0 for omni); a zero vector raises the status word
+__device__ __forceinline__ void unit_orient(const float* v, int pattern, float* o, int* status) {
+  float o0 = v[0], o1 = v[1], o2 = v[2];
   float on2 = o0 * o0 + o1 * o1 + o2 * o2;
   if (pattern != 0 && !(on2 > 0.f)) { atomicOr(status, kStatusZeroOrient); on2 = 1.f; }
   const float inv = pattern != 0 ? rsqrtf(on2) : 0.f;
-  g.o[0] = o0 * inv; g.o[1] = o1 * inv; g.o[2] = o2 * inv;
+  o[0] = o0 * inv; o[1] = o1 * inv; o[2] = o2 * inv;
+}
+static __device__ void geom_from(const float* L, const float* src, const float* rcv, const float* orv, const int* nb,
+                                 int pattern, const float* ors, int spkr_pattern, const float* lb, unsigned neg,
+                                 unsigned zero, RirGeom& g, int* status) {
+  g.a = pattern_const(pattern);
+  unit_orient(orv, pattern, g.o, status);
+  g.as = pattern_const(spkr_pattern);  // source directivity (f3, reading R10)
+  unit_orient(ors, spkr_pattern, g.os, status);
   for (int i = 0; i < 3; i++) {
     g.L[i] = L[i]; g.s[i] = src[i]; g.r[i] = rcv[i];
     g.nlo[i] = -(nb[i] / 2);          // ceil(-N/2)
@@ -65,13 +75,26 @@ static __device__ void geom_from(const float* L, const float* src, const float* 
 static __device__ void load_geom(const IsmArgs& A, int m, RirGeom& g, int* status) {
   if (A.jobs) {
     const BatchJob& J = A.jobs[m];
-    geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.lb, J.neg, J.zero, g, status);
+    geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.ors, J.spkr_pattern, J.lb, J.neg, J.zero, g, status);
   } else {
     int ms = m / A.M_rcv, mr = m % A.M_rcv;
     const float zero3[3] = {0.f, 0.f, 0.f};
-    geom_from(A.L, A.pos_src + 3 * ms, A.pos_rcv + 3 * mr, A.orv ? A.orv + 3 * mr : zero3, A.nb, A.pattern, A.lb,
-              A.neg, A.zero, g, status);
+    geom_from(A.L, A.pos_src + 3 * ms, A.pos_rcv + 3 * mr, A.orv ? A.orv + 3 * mr : zero3, A.nb, A.pattern,
+              A.ors ? A.ors + 3 * ms : zero3, A.spkr_pattern, A.lb, A.neg, A.zero, g, status);
   }
+}
+
+// Source directivity (f3, reading R10): image n radiates along p_r - p_n with the source orientation mirrored on
+// the axes where n is odd.  Column part (x, y) of cos(theta_s) * d: -(sx dx os_x + sy dy os_y), s = (-1)^n,
+// d = p_n - p_r; the z part is added per image by src_gain.
+__device__ __forceinline__ float src_col_dot(int nx, int ny, float dx, float dy, const RirGeom& g) {
+  const float ox = (nx & 1) ? -g.os[0] : g.os[0], oy = (ny & 1) ? -g.os[1] : g.os[1];
+  return -fmaf(dy, oy, dx * ox);
+}
+// g_s = as + (1 - as) cos(theta_s); inv_d = 1 / d.  Exactly 1 for an omni source (as = 1, os = 0).
+__device__ __forceinline__ float src_gain(float sdot, int nz_odd, float dz, float inv_d, const RirGeom& g) {
+  const float oz = nz_odd ? -g.os[2] : g.os[2];
+  return fmaf(1.f - g.as, fmaf(-dz, oz, sdot) * inv_d, g.as);
 }
 
 // Exact n_z range of one side of a column: all n with lo <= Delta_z(n) <= hi, where

@@ -34,7 +34,7 @@ static_assert(kSubPerWarp * kWarps * kS == kTC, "tile geometry");
 // ----------------------------------------------------------------------------
 struct ColRec {         // one lattice column (n_x, n_y) of the current batch (32 B)
   double rho2;          // (x_n - x_r)^2 + (y_n - y_r)^2
-  float dx, dy;         // x_n - x_r, y_n - y_r (directivity)
+  float cdot, sdot;     // column parts of the receiver / source directivity (C4; f3)
   float lxy;            // log2 |beta product| of the x and y walls
   int r1lo, r2lo;       // n_z ranges [r1lo, r1lo + r1n) then [r2lo, ...)
   uint32_t r1n_flags;   // r1n | sign << 30 | zero << 31
@@ -307,7 +307,9 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
         double dx = image_coord(nx, g.L[0], g.s[0]) - g.r[0];
         double dy = image_coord(ny, g.L[1], g.s[1]) - g.r[1];
         double rho2 = dx * dx + dy * dy;
-        cr.rho2 = rho2; cr.dx = (float)dx; cr.dy = (float)dy;
+        cr.rho2 = rho2;
+        cr.cdot = (float)dx * g.o[0] + (float)dy * g.o[1];
+        cr.sdot = src_col_dot(nx, ny, (float)dx, (float)dy, g);
         uint32_t sgn = 0; bool zero = false;
         cr.lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
         fl = (sgn << 30) | (zero ? (1u << 31) : 0u);
@@ -373,8 +375,8 @@ __global__ void __launch_bounds__(kThreads, 2) ism_kernel(IsmArgs A) {
               const float lz = axis_beta(nz, 2, g, sgn, zero);
               float bn = zero ? 0.f : ex2_approx(cr.lxy + lz);
               if (sgn) bn = -bn;
-              const float cth = (cr.dx * g.o[0] + cr.dy * g.o[1] + (float)dz * g.o[2]) * ((float)fs_over_c * rx);
-              const float gain = g.a + (1.f - g.a) * cth;
+              const float cth = fmaf((float)dz, g.o[2], cr.cdot) * ((float)fs_over_c * rx);
+              const float gain = (g.a + (1.f - g.a) * cth) * src_gain(cr.sdot, nz & 1, (float)dz, (float)fs_over_c * rx, g);
               const float amp = bn * gain * rx * fs_over_c_4pi;
               if (MODE == 1) {
                 // Eq. 9 LUT: position u Q = kf Q - xq, xq = xr Q = iq + phi
@@ -479,7 +481,8 @@ __global__ void image_params_kernel(IsmArgs A, double* x_out, float* A_out) {
     float bn = zero ? 0.f : ex2_approx(lb);
     if (sgn) bn = -bn;
     float cth = ((float)dx * g.o[0] + (float)dy * g.o[1] + (float)dz * g.o[2]) * ((float)A.fs_over_c * rx);
-    float gain = g.a + (1.f - g.a) * cth;
+    float gain = (g.a + (1.f - g.a) * cth) *
+                 src_gain(src_col_dot(nx, ny, (float)dx, (float)dy, g), nz & 1, (float)dz, (float)A.fs_over_c * rx, g);
     x_out[i] = xfull;
     A_out[i] = bn * gain * rx * (float)A.fs_over_c * 0.0795774715459476679f;
   }

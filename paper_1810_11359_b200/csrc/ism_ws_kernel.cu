@@ -83,7 +83,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 struct WsStage {        // next work item's inputs, prefetched with cp.async by warp 0
   BatchJob job;          // batch call
-  float pos[12];         // single-room call: src[3], rcv[3], orv[3]
+  float pos[12];         // single-room call: src[3], rcv[3], orv[3], ors[3]
   long long wi;          // work index
   int2 jt;               // (job, tile) of a batch work item
 };
@@ -127,6 +127,8 @@ __device__ __forceinline__ void ws_prefetch(const IsmArgs& A, long long wi, long
     else if (lane < 6) cp_async4(&st.pos[lane], A.pos_rcv + 3 * mr + (lane - 3));
     else if (lane < 9 && A.orv) cp_async4(&st.pos[lane], A.orv + 3 * mr + (lane - 6));
     else if (lane < 9) st.pos[lane] = 0.f;
+    else if (lane < 12 && A.ors) cp_async4(&st.pos[lane], A.ors + 3 * ms + (lane - 9));
+    else if (lane < 12) st.pos[lane] = 0.f;
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -136,7 +138,8 @@ struct WsColRec {  // 32 B
   float bxy;       // signed beta product of the x and y walls (C2)
   float cdot;      // (x_n - x_r) o_x + (y_n - y_r) o_y (polar pattern, C4)
   int r1lo, r2lo;  // n_z ranges [r1lo, r1lo + r1n), [r2lo, ...)
-  int r1n, pad;
+  int r1n;
+  float sdot;      // column part of the source directivity (src_col_dot, f3)
 };
 
 struct WsTile {
@@ -321,15 +324,16 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
               m = sm.stage.jt.x; tile = sm.stage.jt.y;
               nISM = J.nISM;
               row = J.out_offset;
-              geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.lb, J.neg, J.zero, T.g, A.status);
+              geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.ors, J.spkr_pattern, J.lb, J.neg, J.zero, T.g,
+                        A.status);
             } else {
               const long long pos = ws_order(wi, n_work);
               tile = ws_tile(pos, A);
               m = ws_rir(pos, A);
               nISM = A.nISM;
               row = (long long)m * A.row_stride;
-              geom_from(A.L, sm.stage.pos, sm.stage.pos + 3, A.orv ? sm.stage.pos + 6 : zero3, A.nb, A.pattern, A.lb,
-                        A.neg, A.zero, T.g, A.status);
+              geom_from(A.L, sm.stage.pos, sm.stage.pos + 3, A.orv ? sm.stage.pos + 6 : zero3, A.nb, A.pattern,
+                        A.ors ? sm.stage.pos + 9 : zero3, A.spkr_pattern, A.lb, A.neg, A.zero, T.g, A.status);
             }
             T.m = m; T.row = row;
             T.t0 = tile * kWsTC;
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
         {
           const int q = qb + ptid;
           WsColRec cr;
-          cr.r1lo = 0; cr.r2lo = 0; cr.r1n = 0; cr.rho2 = 0.0; cr.bxy = 0.f; cr.cdot = 0.f; cr.pad = 0;
+          cr.r1lo = 0; cr.r2lo = 0; cr.r1n = 0; cr.rho2 = 0.0; cr.bxy = 0.f; cr.cdot = 0.f; cr.sdot = 0.f;
           if (q < T.ncols) {
             const int qy = (int)(((float)q + 0.5f) * T.invNX);  // q / NX, exact for q < 2^20
             const int nx = T.nx0 + (q - qy * T.NX), ny = T.ny0 + qy;
@@ -387,6 +391,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
             const double rho2 = dx * dx + dy * dy;
             cr.rho2 = rho2;
             cr.cdot = (float)dx * g.o[0] + (float)dy * g.o[1];
+            cr.sdot = src_col_dot(nx, ny, (float)dx, (float)dy, g);
             uint32_t sgn = 0; bool zero = false;
             float lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
             float bxy = zero ? 0.f : ex2_approx(lxy);
@@ -475,7 +480,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
                 bb[e] = keep ? (uint8_t)(int)(xrel * (1.f / (float)kS)) : kDiscard;
                 const float rx = rcp_approx(x0f);          // 1/d = fs / (c x)
                 const float cth = fmaf((float)dz, oz, cr.cdot) * (fsc * rx);
-                const float gain = ga + (1.f - ga) * cth;
+                const float gain = (ga + (1.f - ga) * cth) * src_gain(cr.sdot, odd[e], (float)dz, fsc * rx, g);
                 const float amp = cr.bxy * bz[e] * gain * rx * fs_over_c_4pi;  // Eq. 4
                 recA[e] = 0.f;
                 if (MODE == 1) {

@@ -24,6 +24,8 @@ struct alignas(16) BatchJob {
   unsigned long long rir_global;  // tail RNG stream id (C16)
   float lb[6];          // log2 |beta_w| (0 where beta_w == 0), precomputed on the host
   unsigned neg, zero;   // bit w: beta_w < 0 / beta_w == 0
+  float ors[3];         // source orientation (f3, reading R10; ignored for an omni source)
+  int spkr_pattern;     // source polar pattern (gpurir_pattern)
 };
 
 struct IsmArgs {
@@ -37,6 +39,8 @@ struct IsmArgs {
   const float* pos_src;
   const float* pos_rcv;
   const float* orv;
+  const float* ors;      // source orientations [M_src][3] or nullptr (omni source; f3)
+  int spkr_pattern;
   int M_src, M_rcv, M;
   int nISM;
   long long row_stride;  // nSamples

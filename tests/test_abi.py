@@ -78,3 +78,25 @@ def test_invalid_arguments_rejected_on_host(P):
     # host validation happens before any device work: EINVAL without touching CUDA
     assert P._lib.lib().gpurir_simulate_rir(None, None, None, 0, None, 0, None, 0, None, 0.1, 0.1, 16000.0, 343.0,
                                             None, None) == 1
+
+
+def test_weighted_beta_matches_oracle(P, oracle):
+    """f3 helper (reading R9): library and oracle agree, including infeasible and clamped cases."""
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        room = rng.uniform(2, 10, 3).astype(np.float32)
+        w = rng.uniform(0.0, 1.0, 6).astype(np.float32)
+        T60 = float(rng.uniform(0.2, 2.0))
+        try:
+            bo, _ = oracle.beta_sabine_weighted(room, T60, w)
+        except oracle.OracleError as e:
+            with pytest.raises(P.GpurirError) as ei:
+                P.beta_sabine_weighted(room, T60, w)
+            assert ei.value.status == e.status == 3
+            bg, cl = P.beta_sabine_weighted(room, T60, w, clamp=True)
+            assert cl and np.all(bg == 0)
+            continue
+        bg, cl = P.beta_sabine_weighted(room, T60, w)
+        assert not cl and np.allclose(bg, bo, rtol=1e-6, atol=1e-7)
+    with pytest.raises(P.GpurirError):
+        P.beta_sabine_weighted([3, 4, 2.5], 0.5, [0.0] * 6)

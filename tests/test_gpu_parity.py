@@ -366,3 +366,113 @@ def test_trajectory_full_size_sampled_mics(P, oracle):
     for m in (0, 17):
         r = oracle.simulate_trajectory(sig, rirs[:, m:m + 1])[0]
         assert np.max(np.abs(g[m] - r)) <= TRAJ_TOL * np.max(np.abs(r))
+
+
+# ---------------------------------------------------------------- NEXT row f3: source directivity, weighted walls
+
+@pytest.mark.parametrize("spkr,ors,mic,orv", [(2, [0.3, -0.5, 0.8], 0, None), (4, [1.0, 0.0, 0.0], 3, [0.0, 1.0, 0.0]),
+                                              (1, [-0.2, 0.7, 0.1], 2, [0.3, -0.2, 0.9])])
+def test_image_params_source_pattern(P, oracle, spkr, ors, mic, orv):
+    room = np.float32([3, 4, 2.5])
+    beta = np.float32([-0.9, 0.8, -0.7, 0.95, 0.6, -0.85])
+    src, rcv = np.float32([0.7, 1.3, 0.9]), np.float32([2.2, 3.1, 1.7])
+    nb = [9, 8, 7]
+    x, A = P.image_params(room, beta, src, rcv, nb, 16000.0, mic_pattern=mic, orv=orv, spkr_pattern=spkr, ors=ors)
+    ref = oracle.image_set(room, beta, src, rcv, nb, fs=16000.0, pattern=mic, orv=orv, spkr_pattern=spkr, ors=ors)
+    A = A.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(A - ref["A"])) < 2e-6 * np.max(np.abs(ref["A"]))
+
+
+def _dir_scene(rng, fs, Ms, Mr, T):
+    sc = W.random_small_scene(rng, fs=fs, max_src=Ms, max_rcv=Mr, T=T)
+    spkr = int(rng.integers(1, 5))
+    v = rng.standard_normal((sc.pos_src.shape[0], 3))
+    ors = (v / np.linalg.norm(v, axis=1, keepdims=True)).astype(np.float32)
+    return sc, spkr, ors
+
+
+def _run_dir(P, sc, beta, nb, spkr, ors, mode="fp32", split=0):
+    import torch
+    ov = torch.from_numpy(sc.orV_rcv).cuda() if sc.orV_rcv is not None else None
+    h = P.simulate_rir(sc.room, beta, torch.from_numpy(sc.pos_src).cuda(), torch.from_numpy(sc.pos_rcv).cuda(), nb,
+                       sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=ov, mic_pattern=sc.pattern, mode=mode, seed=sc.seed,
+                       split=split, sync=True, orV_src=torch.from_numpy(ors).cuda(), spkr_pattern=spkr)
+    return h.cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("kernel", ["auto", "persistent"])
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex"])
+def test_source_directivity_random_scenes(P, oracle, mode, kernel):
+    """f3 (reading R10): random rooms, all source and receiver patterns, 16 / 48 kHz, both ISM kernels."""
+    rng = np.random.default_rng(3310)
+    for i in range(12):
+        sc, spkr, ors = _dir_scene(rng, 16000.0 if i % 3 else 48000.0, 2, 3, None)
+        beta, nb = derive(oracle, sc)
+        g = _run_dir(P, sc, beta, nb, spkr, ors, mode=mode, split=-1 if kernel == "persistent" else 0)
+        r = oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv, nb, sc.Tdiff, sc.Tmax, fs=sc.fs, c=sc.c,
+                                pattern=sc.pattern, orV_rcv=sc.orV_rcv, seed=sc.seed, spkr_pattern=spkr, orV_src=ors)
+        assert rel_err(g, r).max() <= TOL[mode], (i, spkr, sc.pattern)
+
+
+def test_source_directivity_with_tail(P, oracle):
+    """Directional source + diffuse tail: the envelope is estimated from the directional ISM part."""
+    rng = np.random.default_rng(77)
+    sc, spkr, ors = _dir_scene(rng, 16000.0, 1, 4, 0.05)
+    sc.Tmax = 0.2
+    beta, nb = derive(oracle, sc)
+    g = _run_dir(P, sc, beta, nb, spkr, ors)
+    r = oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv, nb, sc.Tdiff, sc.Tmax, fs=sc.fs, c=sc.c,
+                            pattern=sc.pattern, orV_rcv=sc.orV_rcv, seed=sc.seed, spkr_pattern=spkr, orV_src=ors)
+    assert rel_err(g, r).max() <= TOL["fp32"]
+
+
+@pytest.mark.parametrize("split", [0, -1])
+def test_omni_source_dir_entry_bit_identical(P, oracle, split):
+    """gpurir_simulate_rir == gpurir_simulate_rir_dir with an omni source (g_s = 1 exactly)."""
+    sc = W.cfg3(16, "diffuse")
+    beta, nb = derive(oracle, sc)
+    a = run_gpu(P, sc, beta, nb, split=split)
+    b = _run_dir(P, sc, beta, nb, 0, np.float32([[0.0, 0.0, 1.0]]), split=split)
+    assert np.array_equal(a, b)
+
+
+def test_directional_reciprocity_gpu(P, oracle):
+    sc = W.cfg1()
+    beta, nb = derive(oracle, sc)
+    oa, ob = np.float32([[0.3, -0.5, 0.8]]), np.float32([[-0.6, 0.2, 0.4]])
+    s1 = W.Scene("d", sc.room, sc.T60, sc.pos_src, sc.pos_rcv, ob, 3, sc.Tdiff, sc.Tmax, sc.fs)
+    s2 = W.Scene("d", sc.room, sc.T60, sc.pos_rcv, sc.pos_src, oa, 2, sc.Tdiff, sc.Tmax, sc.fs)
+    a = _run_dir(P, s1, beta, nb, 2, oa)
+    b = _run_dir(P, s2, beta, nb, 3, ob)
+    assert rel_err(a, b)[0] <= 1e-5
+
+
+def test_batch_directional_weighted_rooms(P, oracle):
+    """Batch API with per-room source patterns and non-uniform wall weights (f3) vs the oracle."""
+    import torch
+    rb = W.cfg5(10)
+    rng = np.random.default_rng(5150)
+    rooms, refs, off = [], [], 0
+    for i in range(rb.n):
+        w = rng.uniform(0.3, 1.0, 6)
+        beta, _ = oracle.beta_sabine_weighted(rb.room[i], rb.T60[i], w, clamp=True)
+        beta = beta.astype(np.float32)
+        nb = oracle.t2n(rb.Tdiff[i], rb.room[i])
+        nS = oracle.nsamples(rb.Tmax[i], rb.fs)
+        spkr = i % 5
+        v = rng.standard_normal(3)
+        ors = (v / np.linalg.norm(v)).astype(np.float32)
+        rooms.append(dict(room_sz=rb.room[i], beta=beta, pos_src=rb.pos_src[i], pos_rcv=rb.pos_rcv[i], nb_img=nb,
+                          Tdiff=rb.Tdiff[i], Tmax=rb.Tmax[i], out_offset=off, orV_src=ors, spkr_pattern=spkr))
+        refs.append(oracle.simulate_rir(rb.room[i], beta, rb.pos_src[i:i + 1], rb.pos_rcv[i:i + 1], nb, rb.Tdiff[i],
+                                        rb.Tmax[i], fs=rb.fs, seed=rb.seed, rir_index_base=i, spkr_pattern=spkr,
+                                        orV_src=ors[None] if spkr else None)[0, 0])
+        off += nS
+    out = torch.full((off,), float("nan"), device="cuda")
+    P.simulate_rir_batch(rooms, rb.fs, out, seed=rb.seed, sync=True)
+    o = out.cpu().numpy().astype(np.float64)
+    off = 0
+    for i, r in enumerate(refs):
+        g = o[off:off + r.size]
+        off += r.size
+        assert rel_err(g, r)[0] <= TOL["fp32"], i
