@@ -224,21 +224,20 @@ void fill_common(IsmArgs& A, double fs, double c, double Tw) {
   double rho = H / Hs, r2 = rho * rho;
   A.invHs = (float)(1.0 / Hs);
   A.rho2 = (float)r2;
-  const double b[4] = {kWb0, kWb1, kWb2, kWb3};
-  for (int i = 0; i < 4; i++) A.wb[i] = (float)(b[i] / pow(r2, i + 1));
-  // c(sigma) = sigma (wb0 + wb1 sigma + wb2 sigma^2 + wb3 sigma^3) rewritten in u = 1 + sigma, which the
-  // kernel clamps to [0, 1] with FFMA.SAT (u = 1 <=> the window edge): a_j = sum_k wb_{k-1} C(k,j) (-1)^(k-j)
-  double a[5] = {0, 0, 0, 0, 0};
-  for (int k = 1; k <= 4; k++) {
+  const double b[3] = {kWb0, kWb1, kWb2};
+  for (int i = 0; i < 3; i++) A.wb[i] = (float)(b[i] / pow(r2, i + 1));
+  // c(sigma) = sigma (wb0 + wb1 sigma + wb2 sigma^2) rewritten in u = 1 + sigma, which the kernel clamps to
+  // [0, 1] with FFMA.SAT (u = 1 <=> the window edge): a_j = sum_k wb_{k-1} C(k,j) (-1)^(k-j)
+  double a[4] = {0, 0, 0, 0};
+  for (int k = 1; k <= 3; k++) {
     double ck = 1.0;  // C(k, j)
     for (int j = 0; j <= k; j++) {
       a[j] += (double)A.wb[k - 1] * ck * (((k - j) & 1) ? -1.0 : 1.0);
       ck = ck * (double)(k - j) / (double)(j + 1);
     }
   }
-  for (int j = 1; j <= 4; j++) A.wa[j] = (float)a[j];
-  float s = A.wa[4];  // Horner at u = 1 in fp32, so that c(1) = 0 exactly on the device
-  s = s + A.wa[3];
+  for (int j = 1; j <= 3; j++) A.wa[j] = (float)a[j];
+  float s = A.wa[3];  // Horner at u = 1 in fp32, so that c(1) = 0 exactly on the device
   s = s + A.wa[2];
   s = s + A.wa[1];
   A.wa[0] = -s;

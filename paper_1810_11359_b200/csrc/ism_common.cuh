@@ -114,16 +114,16 @@ __device__ __forceinline__ void z_range(const RirGeom& g, double invLz, double l
 // Eqs. 5-6 for one lane over record pairs pp[0], pp[kG], ... < pend (see ism_kernel.cu for the derivation):
 // acc += C' w(u) / v, v = (k - x)/Hs, sigma = v^2 - rho^2 clamped <= 0, w = (sigma p(sigma))^2.
 struct TapConst {
-  float2 kv2, a4, a3, a2, a1, a0;
+  float2 kv2, a3, a2, a1, a0;
   float up;
 };
 // Eq. 5-6 per pair of records: acc += C' w(v) / v with v = (k - x)/Hs.  The window is c(u)^2 where
 // u = min(max(v^2 + 1 - rho^2, 0), 1) (one FFMA.SAT per record: u = 1 at and beyond the window edge,
-// where c(1) = 0 exactly) and c is the degree-4 polynomial of fill_common (R5).
+// where c(1) = 0 exactly) and c is the degree-3 polynomial of fill_common (R5).
 __device__ __forceinline__ TapConst make_tap_const(const IsmArgs& A, float kv) {
   TapConst K;
   K.kv2 = make_float2(kv, kv);
-  K.a4 = make_float2(A.wa[4], A.wa[4]); K.a3 = make_float2(A.wa[3], A.wa[3]);
+  K.a3 = make_float2(A.wa[3], A.wa[3]);
   K.a2 = make_float2(A.wa[2], A.wa[2]); K.a1 = make_float2(A.wa[1], A.wa[1]);
   K.a0 = make_float2(A.wa[0], A.wa[0]);
   K.up = A.urho;
@@ -132,8 +132,7 @@ __device__ __forceinline__ TapConst make_tap_const(const IsmArgs& A, float kv) {
 __device__ __forceinline__ float2 tap_pair(const float4 p, const TapConst& K, float2 a2) {
   const float2 v = __fadd2_rn(K.kv2, make_float2(p.x, p.y));
   const float2 u = make_float2(__saturatef(fmaf(v.x, v.x, K.up)), __saturatef(fmaf(v.y, v.y, K.up)));
-  float2 c = __ffma2_rn(K.a4, u, K.a3);
-  c = __ffma2_rn(c, u, K.a2);
+  float2 c = __ffma2_rn(K.a3, u, K.a2);
   c = __ffma2_rn(c, u, K.a1);
   c = __ffma2_rn(c, u, K.a0);
   const float2 w = __fmul2_rn(c, c);

@@ -56,8 +56,8 @@ struct IsmArgs {
   // v = u / Hs, rho = H / Hs; window polynomial in sigma = v^2 - rho^2 with coefficients wb[i]
   float invHs;           // 1 / Hs
   float rho2;            // rho^2
-  float wb[4];           // b_i / rho^(2i+2)
-  float wa[5];           // the same window as a polynomial in u = 1 + sigma (sat-clamped form), wa[0] = -sum
+  float wb[3];           // b_i / rho^(2i+2)
+  float wa[4];           // the same window as a polynomial in u = 1 + sigma (sat-clamped form), wa[0] = -sum
   float urho;            // 1 - rho^2
   float hc[3];           // fp16 mode: Eq. 11 coefficients of x^2, x^4, x^6 divided by rho^2, rho^4, rho^6
   float x2clamp;         // fp16 mode: rho^2 / 4
