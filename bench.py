@@ -281,7 +281,7 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--mode", default="fp32", choices=["fp32", "lut", "fp16", "lut_tex"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 host path with several ranks on one GPU")
     ap.add_argument("--workload", default="ism", choices=["ism", "trajectory"])
@@ -369,38 +369,43 @@ def main():
 
     # ---- end to end through the public API with HOST buffers (H2D inputs, D2H RIRs in the region) ----
     # A dataset-generation loop: every step copies its inputs from pinned host memory, runs the call and
-    # copies the full RIR tensor back to pinned host memory.  Steps alternate between two streams (double-
-    # buffered device outputs), so the D2H of step i overlaps the kernels of step i+1.
+    # copies the full RIR tensor back to pinned host memory.  Kernels run in order on a compute stream; each
+    # step's 734 MB D2H runs on a copy stream while the next step computes into the other of two device
+    # output buffers (a buffer is reused only after its D2H has finished).
     e2e_steps = max(2, args.e2e_steps)
     h_src = torch.from_numpy(sc.pos_src).pin_memory()
     h_rcv = torch.from_numpy(np.ascontiguousarray(sc.pos_rcv[sl])).pin_memory()
     h_orv = torch.from_numpy(np.ascontiguousarray(sc.orV_rcv[sl])).pin_memory()
     h_out = [torch.empty((1, M_PER_GPU, nS), dtype=torch.float32).pin_memory() for _ in range(2)]
     d_out = [out, torch.empty_like(out)]
-    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    cs, xs = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for st_ in streams:
-        st_.wait_event(e0)
-    done = []
+    cs.wait_event(e0)
+    xs.wait_event(e0)
+    copied = []
     for i in range(e2e_steps):
-        st_ = streams[i % 2]
-        with torch.cuda.stream(st_):
+        with torch.cuda.stream(cs):
+            if i >= 2:
+                cs.wait_event(copied[i - 2])  # d_out[i % 2] is free once step i-2's D2H is done
             d_src = h_src.to(dev, non_blocking=True)
             d_rcv = h_rcv.to(dev, non_blocking=True)
             d_orv = h_orv.to(dev, non_blocking=True)
             P.simulate_rir(sc.room, beta, d_src, d_rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=d_orv,
                            mic_pattern=sc.pattern, mode=args.mode, seed=sc.seed, rir_index_base=base,
-                           out=d_out[i % 2], stream=st_)
+                           out=d_out[i % 2], stream=cs)
+            done = torch.cuda.Event()
+            done.record(cs)
+        xs.wait_event(done)
+        with torch.cuda.stream(xs):
             h_out[i % 2].copy_(d_out[i % 2], non_blocking=True)
             ev = torch.cuda.Event()
-            ev.record(st_)
-            done.append(ev)
-    for ev in done[-2:]:
-        stream.wait_event(ev)
+            ev.record(xs)
+            copied.append(ev)
+    stream.wait_event(copied[-1])
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64,
@@ -465,7 +470,7 @@ def main():
                         "frac_of_hbm": tail_bytes / tail_avg_s / 1e9 / hbm_peak, "bound": "hbm (write)",
                         "peak_GB_per_s": hbm_peak},
         "e2e": {"value": e2e_value, "unit": "RIRs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "steps": e2e_steps, "pipelining": "2 streams: D2H of step i overlaps the kernels of step i+1"},
+                "steps": e2e_steps, "pipelining": "compute stream + copy stream, 2 device output buffers: D2H of step i overlaps the kernels of step i+1"},
         "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
         "paper_context": "gpuRIR V100 fp32, 1024 RIRs, T60 0.7 s diffuse: 195.69 ms = 5,233 RIRs/s (P:362); "

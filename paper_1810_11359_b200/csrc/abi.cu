@@ -457,7 +457,11 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     T.seed = o.seed;
     T.out = out;
     long long groups = (nS + 3) / 4 - nISM / 4;
-    T.chunks_per_rir = (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4));
+    // One warp per tail chunk of up to kTailChunk samples (measured: splitting cfg3's 8400-sample tails into
+    // 3 warps to fill more waves was 10 % slower, the per-warp envelope reduction dominating)
+    const long long nch = (groups + kTailChunk / 4 - 1) / (kTailChunk / 4);
+    T.chunks_per_rir = (int)nch;
+    T.chunk_quads = (int)((groups + nch - 1) / nch);
     if (o.ev_tail[0]) cudaEventRecord((cudaEvent_t)o.ev_tail[0], stream);
     cudaError_t e = launch_tail(T, (long long)T.chunks_per_rir * M, stream);
     if (e != cudaSuccess) return cuda_fail(e, "launch_tail");
@@ -567,6 +571,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     T.win = (int)llround(0.010 * fs);
     T.seed = o.seed;
     T.out = out;
+    T.chunk_quads = kTailChunk / 4;
     if (o.ev_tail[0]) cudaEventRecord((cudaEvent_t)o.ev_tail[0], stream);
     e = launch_tail(T, (long long)chunks.size(), stream);
     if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_tail(batch)"); }

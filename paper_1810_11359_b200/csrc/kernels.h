@@ -90,6 +90,7 @@ struct TailArgs {
   unsigned long long seed;
   float* out;
   int chunks_per_rir;
+  int chunk_quads;       // Philox blocks (4 samples) per warp item
 };
 
 size_t ism_smem_bytes(int mode, int lut_rows, int lut_cols);

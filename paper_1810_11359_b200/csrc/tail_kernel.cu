@@ -7,7 +7,7 @@
 //   the direct-path sample (reading C15);
 //   h[k] = sqrt(P(k/fs)) * (sqrt(3)/pi) ln(u / (1 - u)),  nISM <= k < nS  (logistic noise),
 //   u from the stateless Philox4x32-10 stream (seed, global RIR index, k) (reading C16).
-// One warp per (RIR, chunk of kTailChunk samples).  Each warp re-reduces the
+// One warp per (RIR, chunk of chunk_quads Philox blocks).  Each warp re-reduces the
 // envelope window (<= 480 floats, L2 hits, fp64 sums, fixed butterfly) so the
 // tail needs no separate launch and no scratch; the RNG has no seeding kernel
 // and no noise buffer in HBM.  Output writes (4 B / sample, float4 stores) are
@@ -28,7 +28,7 @@ __device__ __forceinline__ float ex2_fast(float x) {
   return r;
 }
 
-// One warp per (RIR, chunk of kTailChunk samples): the envelope window is reduced with warp shuffles
+// One warp per (RIR, chunk): the envelope window is reduced with warp shuffles
 // only (no block barriers), so the short prologue of one warp overlaps the streaming stores of others.
 __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A, long long n_items) {
   const int lane = threadIdx.x & 31;
@@ -91,8 +91,8 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A, long lon
   const long long qend = (long long)((nS + 3) >> 2);
   const PhiloxKey key = philox_key(make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32)));
   const bool aligned = ((row & 3) == 0);
-  const long long qbeg = q0 + (long long)chunk * (kTailChunk / 4);
-  const long long qlim = min(qend, qbeg + (long long)(kTailChunk / 4));
+  const long long qbeg = q0 + (long long)chunk * A.chunk_quads;
+  const long long qlim = min(qend, qbeg + (long long)A.chunk_quads);
 #pragma unroll 2
   for (long long q = qbeg + lane; q < qlim; q += 32) {
     const uint4 ctr = make_uint4((uint32_t)q, (uint32_t)((unsigned long long)q >> 32), (uint32_t)rglob,
@@ -105,10 +105,11 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A, long lon
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       // u = (2 (w >> 9) + 1) 2^-24 built exactly without an int->float conversion:
-      // f = 1 + (w >> 9) 2^-23 in [1, 2), u = f - (1 - 2^-24), 1 - u = (2 - f) - 2^-24
+      // f = 1 + (w >> 9) 2^-23 in [1, 2), u = f - (1 - 2^-24); 1 - u is an odd multiple of 2^-24 below 1,
+      // so it is exact in fp32 too
       const float f = __uint_as_float(0x3F800000u | (ws[j] >> 9));
       const float u = f - 0.99999994039535522461f;
-      const float omu = (2.f - f) - 5.9604644775390625e-08f;
+      const float omu = 1.f - u;
       vals[j] = e * (lg2_approx(u) - lg2_approx(omu));  // sqrt(P) (sqrt3/pi) ln(u/(1-u))
       e *= rho;
     }
