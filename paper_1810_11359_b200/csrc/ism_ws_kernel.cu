@@ -441,6 +441,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
             int boundary = sm.colpre[j];
             // tile constants in registers (shared-memory reads would be re-issued per image)
             const double Lz = g.L[2], offE = T.offE, offO = T.offO;
+            const float Lzf = (float)Lz, offEf = (float)offE, offOf = (float)offO;
             const int tc = T.tc, zl = T.zl;
             const bool use_bz = T.use_bz;
             const float xmax = T.xrel_max, oz = g.o[2], ga = g.a, fsc = (float)fs_over_c;
@@ -469,18 +470,19 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
               for (int e = 0; e < 2; e++) {
                 const WsColRec& cr = e ? crB : crA;
                 // Eq. 1 along z: even nz -> nz L + s, odd nz -> (nz + 1) L - s; Delta_z = z_n - z_r
-                const double dz = fma((double)(nz[e] + odd[e]), Lz, odd[e] ? offO : offE);
+                const int nzo = nz[e] + odd[e];
+                const double dz = fma(int_to_double(nzo), Lz, odd[e] ? offO : offE);
                 const double x2 = fma(dz, dz, cr.rho2) * sc2;  // (d fs / c)^2
                 if (x2 == 0.0 && (e == 0 || hasB)) atomicOr(A.status, kStatusDegenerate);
                 // branch-free from here: culled records are computed and flagged with kDiscard
-                float x0f;
-                float xr = delay_rel(x2, tc, x0f);
+                float x0f, rx;                              // rx = rsqrt(x^2) = 1/x, so 1/d = fs rx / c
+                float xr = delay_rel(x2, tc, x0f, rx);
                 const float xrel = xr + (float)(kWsTC / 2) + H;  // x - (t0 - H)
                 const bool keep = (x2 != 0.0) && (xrel > 0.f) && (xrel < xmax);
-                bb[e] = keep ? (uint8_t)(int)(xrel * (1.f / (float)kS)) : kDiscard;
-                const float rx = rcp_approx(x0f);          // 1/d = fs / (c x)
-                const float cth = fmaf((float)dz, oz, cr.cdot) * (fsc * rx);
-                const float gain = (ga + (1.f - ga) * cth) * src_gain(cr.sdot, odd[e], (float)dz, fsc * rx, g);
+                bb[e] = keep ? (uint8_t)floor_div8(xrel) : kDiscard;
+                const float dzf = fmaf((float)nzo, Lzf, odd[e] ? offOf : offEf);  // fp32 Delta_z (directivity)
+                const float cth = fmaf(dzf, oz, cr.cdot) * (fsc * rx);
+                const float gain = (ga + (1.f - ga) * cth) * src_gain(cr.sdot, odd[e], dzf, fsc * rx, g);
                 const float amp = cr.bxy * bz[e] * gain * rx * fs_over_c_4pi;  // Eq. 4
                 recA[e] = 0.f;
                 if (MODE == 1) {
@@ -497,13 +499,13 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
                 } else if (MODE == 3) {
                   rec[e] = make_float2(fmaf(-xr, A.texQ, A.tex_off), amp);  // coordinate offset, amplitude
                 } else {
-                  // exact integer delay (reading R3): move off the sinc zero by >= 1 ulp (select, no branch)
-                  const float xr0 = xr;
-                  xr = (xr0 - floorf(xr0) == 0.f) ? xr0 + fmaxf(fabsf(xr0) * 1.1920929e-7f, 9.5367432e-7f) : xr0;
-                  const float fj = floorf(xr);
+                  int jodd;
+                  const float fj = floor_parity(xr, jodd);
+                  // exact integer delay (reading R3): move up by >= 1 ulp (floor unchanged; select, no branch)
+                  xr = (xr == fj) ? xr + fmaxf(fabsf(xr) * 1.1920929e-7f, 9.5367432e-7f) : xr;
                   const float f = xr - fj;
                   float cc = -amp * sinpi01(f) * 0.318309886183790672f;
-                  if ((int)fj & 1) cc = -cc;
+                  if (jodd) cc = -cc;
                   if (MODE == 0) rec[e] = make_float2(-xr * A.invHs, cc * A.invHs);
                   else rec[e] = make_float2(-xr * (0.5f * A.invHs), cc * (0.5f * A.invHs) * 1024.f);
                 }
