@@ -100,3 +100,35 @@ def test_weighted_beta_matches_oracle(P, oracle):
         assert not cl and np.allclose(bg, bo, rtol=1e-6, atol=1e-7)
     with pytest.raises(P.GpurirError):
         P.beta_sabine_weighted([3, 4, 2.5], 0.5, [0.0] * 6)
+
+
+def _dir_call(P, spkr, ors, mode=0, Q=16, buf=None):
+    """gpurir_simulate_rir_dir with dummy (never dereferenced on a rejected call) device pointers."""
+    L = P._lib.lib()
+    f3 = (ctypes.c_float * 3)(3.0, 4.0, 2.5)
+    b6 = (ctypes.c_float * 6)(*([0.5] * 6))
+    nb = (ctypes.c_int * 3)(3, 3, 3)
+    o = P._lib.Opts()
+    L.gpurir_opts_default(ctypes.byref(o))
+    o.mode, o.lut_Q = mode, Q
+    dummy = ctypes.c_void_p(16)
+    return L.gpurir_simulate_rir_dir(f3, b6, dummy, 1, ors, spkr, dummy, 1, None, 0, nb, 0.01, 0.01, 16000.0,
+                                     343.0, dummy, ctypes.byref(o))
+
+
+def test_directional_source_validated_on_host(P):
+    """f3: a directional source needs orientations; patterns outside 0..4 are rejected (EINVAL = 1)."""
+    assert _dir_call(P, 2, None) == 1
+    assert _dir_call(P, 5, ctypes.c_void_p(16)) == 1
+    assert _dir_call(P, -1, None) == 1
+
+
+def test_mode_validation_on_host(P):
+    """LUT needs a power-of-two Q (R4); the texture LUT (f2) does not; unknown modes are EINVAL.  A call
+    that passes host validation goes on to the device, which this container lacks (ECUDA = 5)."""
+    import torch
+    assert _dir_call(P, 0, None, mode=1, Q=10) == 1
+    assert _dir_call(P, 0, None, mode=4) == 1
+    if not torch.cuda.is_available():
+        assert _dir_call(P, 0, None, mode=3, Q=10) == 5
+        assert _dir_call(P, 0, None, mode=1, Q=16) == 5
