@@ -457,9 +457,14 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     T.seed = o.seed;
     T.out = out;
     long long groups = (nS + 3) / 4 - nISM / 4;
-    // One warp per tail chunk of up to kTailChunk samples (measured: splitting cfg3's 8400-sample tails into
-    // 3 warps to fill more waves was 10 % slower, the per-warp envelope reduction dominating)
-    const long long nch = (groups + kTailChunk / 4 - 1) / (kTailChunk / 4);
+    // One warp per tail chunk.  Large calls: one chunk (up to kTailChunk samples) per RIR — splitting cfg3's
+    // 8400-sample tails over 3 warps measured 10 % slower (the per-warp envelope reduction dominates).  Calls
+    // with fewer RIRs than resident warps: split each tail (>= 64 Philox blocks per warp) so that a single
+    // RIR's tail is not one warp's serial loop (latency of small calls, configs 1, 2 and 4).
+    const long long slots = (long long)d->num_sms * 48;  // resident tail warps (6 CTAs x 8 warps per SM)
+    long long nch = 1;
+    if (M < slots) nch = std::max(1LL, std::min((slots + M - 1) / M, groups / 64));
+    nch = std::max(nch, (groups + kTailChunk / 4 - 1) / (kTailChunk / 4));
     T.chunks_per_rir = (int)nch;
     T.chunk_quads = (int)((groups + nch - 1) / nch);
     if (o.ev_tail[0]) cudaEventRecord((cudaEvent_t)o.ev_tail[0], stream);

@@ -25,8 +25,11 @@ namespace gpurir {
 #define GPURIR_WS_CTAS_PER_SM 2
 #endif
 constexpr int kWsCtasPerSm = GPURIR_WS_CTAS_PER_SM;  // persistent CTAs per SM (1: 16P+16C, 2: 8P+8C each)
-constexpr int kPW = 16 / kWsCtasPerSm;       // producer warps
-constexpr int kCW = 16 / kWsCtasPerSm;       // consumer warps
+#ifndef GPURIR_WS_PW
+#define GPURIR_WS_PW (16 / GPURIR_WS_CTAS_PER_SM)
+#endif
+constexpr int kPW = GPURIR_WS_PW;            // producer warps
+constexpr int kCW = 32 / kWsCtasPerSm - kPW; // consumer warps
 constexpr int kPT = kPW * 32;                // producer threads
 constexpr int kWsThreads = (kPW + kCW) * 32; // 1024 / kWsCtasPerSm
 constexpr int kWsSub = 4 * kWsCtasPerSm;     // 8-sample sub-tiles per consumer warp
@@ -212,6 +215,11 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
     const double fs_over_c = A.fs_over_c;
     const double sc2 = fs_over_c * fs_over_c;
     const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f;
+    // per-mode record scale folded into each column's beta product: Eq. 4's fs/(4 pi c) and, for the fp32 /
+    // fp16 records, the hoisted sinc factor -1/pi and the tap-argument scale
+    const float rec_scale = MODE == 0   ? fs_over_c_4pi * -0.318309886183790672f * A.invHs
+                            : MODE == 2 ? fs_over_c_4pi * -0.318309886183790672f * (0.5f * A.invHs) * 1024.f
+                                        : fs_over_c_4pi;
     int win_i = 0, filled = 0;
 
     // stable counting sort of rec[0, filled) by bin, then publish to buffer win_i % kNBuf
@@ -395,7 +403,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
             uint32_t sgn = 0; bool zero = false;
             float lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
             float bxy = zero ? 0.f : ex2_approx(lxy);
-            cr.bxy = sgn ? -bxy : bxy;
+            cr.bxy = (sgn ? -bxy : bxy) * rec_scale;
             if (rho2 < T.dhi2) {
               // shell bounds along z: fp32 square roots suffice (an image misplaced by their rounding sits on the
               // shell edge, where its window weight is ~0); the ranges below are exact for these bounds
@@ -445,6 +453,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
             const int tc = T.tc, zl = T.zl;
             const bool use_bz = T.use_bz;
             const float xmax = T.xrel_max, oz = g.o[2], ga = g.a, fsc = (float)fs_over_c;
+            const bool dir_src = g.as != 1.f;  // directional source (f3): tile-uniform branch
             // Two images per iteration: all shared loads first, then both images' arithmetic (independent,
             // so the scheduler interleaves the two dependency chains), then the stores.
             for (int gi = g0; gi < g1; gi += 2) {
@@ -482,8 +491,9 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
                 bb[e] = keep ? (uint8_t)floor_div8(xrel) : kDiscard;
                 const float dzf = fmaf((float)nzo, Lzf, odd[e] ? offOf : offEf);  // fp32 Delta_z (directivity)
                 const float cth = fmaf(dzf, oz, cr.cdot) * (fsc * rx);
-                const float gain = (ga + (1.f - ga) * cth) * src_gain(cr.sdot, odd[e], dzf, fsc * rx, g);
-                const float amp = cr.bxy * bz[e] * gain * rx * fs_over_c_4pi;  // Eq. 4
+                float gain = ga + (1.f - ga) * cth;
+                if (dir_src) gain *= src_gain(cr.sdot, odd[e], dzf, fsc * rx, g);
+                const float amp = cr.bxy * bz[e] * gain * rx;  // Eq. 4 (times rec_scale)
                 recA[e] = 0.f;
                 if (MODE == 1) {
                   float xq = xr * (float)A.lutQ;
@@ -504,10 +514,9 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtasPerSm) ism_ws_kernel(IsmArg
                   // exact integer delay (reading R3): move up by >= 1 ulp (floor unchanged; select, no branch)
                   xr = (xr == fj) ? xr + fmaxf(fabsf(xr) * 1.1920929e-7f, 9.5367432e-7f) : xr;
                   const float f = xr - fj;
-                  float cc = -amp * sinpi01(f) * 0.318309886183790672f;
+                  float cc = amp * sinpi01(f);  // C' = -A sin(pi f) / pi (scaled), rec_scale
                   if (jodd) cc = -cc;
-                  if (MODE == 0) rec[e] = make_float2(-xr * A.invHs, cc * A.invHs);
-                  else rec[e] = make_float2(-xr * (0.5f * A.invHs), cc * (0.5f * A.invHs) * 1024.f);
+                  rec[e] = make_float2(-xr * (MODE == 0 ? A.invHs : 0.5f * A.invHs), cc);
                 }
               }
               const int dst = filled + (gi - base);
