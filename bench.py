@@ -279,7 +279,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--mode", default="fp32", choices=["fp32", "lut", "fp16", "lut_tex"])
+    ap.add_argument("--mode", default="fp32", choices=["fp32", "lut", "fp16", "lut_tex", "poly"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],

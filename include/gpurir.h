@@ -57,10 +57,15 @@ typedef enum {
   GPURIR_FP32 = 0, /* Eq. 6 evaluated in fp32 (the paper's "base" kernel)               */
   GPURIR_LUT = 1,  /* Eq. 9 windowed-sinc table, Q-times oversampled, linear interp.    */
   GPURIR_FP16 = 2, /* half2 tap arithmetic with the Eq. 10-12 style polynomials */
-  GPURIR_LUT_TEX = 3 /* Eq. 9 table in texture memory, hardware linear interpolation (the paper's LUT
+  GPURIR_LUT_TEX = 3, /* Eq. 9 table in texture memory, hardware linear interpolation (the paper's LUT
                         placement).  Any Q >= 1 with 2 ceil(Tw Q fs / 2) + 1 <= the
                         device's 1-D texture width (else EINVAL).  Interpolation weights have 8 fractional
                         bits (texture hardware); tolerance as GPURIR_LUT. */
+  GPURIR_POLY = 4     /* Eq. 6 by its polyphase expansion (reading R11): every image adds
+                        A_n T_d(2 phi_n - 1), d = 0..7, to the integer sample floor(x_n) (exact 64-bit
+                        fixed-point sums, deterministic), then an 8-channel FIR of 2H taps, whose
+                        coefficients expand delta'(m - phi) in Chebyshev polynomials (max error 4.3e-7),
+                        produces the RIR.  fp32 arithmetic; fp32 tolerance.  Requires Tw fs <= 1022. */
 } gpurir_mode;
 
 #define GPURIR_FLAG_SYNC 1u /* synchronise the stream before returning and report device-side status */

@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("GPURIR_LIB", os.path.join(_HERE, "libgpurir.so"))  # 
 
 OK, EINVAL, EDEGENERATE, EINFEASIBLE, ENOMEM, ECUDA = range(6)
 FLAG_SYNC = 1
-MODES = {"fp32": 0, "lut": 1, "fp16": 2, "lut_tex": 3}
+MODES = {"fp32": 0, "lut": 1, "fp16": 2, "lut_tex": 3, "poly": 4}
 PATTERNS = {"omni": 0, "subcardioid": 1, "cardioid": 2, "hypercardioid": 3, "bidirectional": 4}
 
 # Every symbol include/gpurir.h declares (checked by tests/test_abi.py).

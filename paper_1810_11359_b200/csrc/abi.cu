@@ -43,10 +43,17 @@ struct TexEntry {  // one Eq. 9 table as a filtered 1-D texture (texture-LUT mod
   cudaTextureObject_t tex = 0;
 };
 
+struct PolyEntry {  // polyphase table of one (Tw, fs) (mode GPURIR_POLY, reading R11); never overwritten
+  double Tw = 0, fs = 0;
+  int ntaps = 0, mlo = 0;
+  float* dev = nullptr;
+};
+
 struct DeviceState {
   int* status = nullptr;
   std::vector<LutEntry> luts;
   std::vector<TexEntry> texs;
+  std::vector<PolyEntry> polys;
   int* work_counter = nullptr;  // persistent-kernel work-queue heads, one per call in flight (ring)
   unsigned next_counter = 0;
   int num_sms = 0;
@@ -157,7 +164,49 @@ const TexEntry* ensure_tex(DeviceState* d, double Tw, double fs, int Q, cudaStre
   return &d->texs.back();
 }
 
-// Mode tables of one call (LUT: phase-major smem table; texture LUT: filtered texture).
+// Polyphase expansion of Eq. 6 (reading R11): for every integer tap m = k - floor(x) that the open support
+// |k - x| < H can reach (m_lo = floor(-H) + 1 .. m_hi), delta'(m - phi) ~= sum_{d<8} P[m][d] T_d(2 phi - 1),
+// phi in [0, 1), by the truncated Chebyshev series of the 64-node interpolant (max error 4.3e-7 for 16-96 kHz,
+// integer or fractional H).  Rows are the kernel's taps mi = m - m_lo.
+const int kPolyDeg = 8, kPolyNodes = 64, kPolyMaxTaps = 512;
+double eq6_samples(double u, double H) {
+  if (!(u > -H && u < H)) return 0.0;  // open support (C8)
+  const double w = 0.5 * (1.0 + cos(M_PI * u / H));
+  return w * (u == 0.0 ? 1.0 : sin(M_PI * u) / (M_PI * u));
+}
+const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t stream, int* err) {
+  *err = GPURIR_OK;
+  for (const PolyEntry& P : d->polys)
+    if (P.Tw == Tw && P.fs == fs) return &P;
+  const double H = Tw * fs / 2.0;
+  PolyEntry P;
+  P.Tw = Tw; P.fs = fs;
+  P.mlo = (int)floor(-H) + 1;
+  const int mhi = (H == floor(H)) ? (int)H : (int)floor(H) + 1;
+  P.ntaps = mhi - P.mlo + 1;
+  if (P.ntaps < 1 || P.ntaps > kPolyMaxTaps) { *err = GPURIR_EINVAL; return nullptr; }
+  std::vector<float> tab((size_t)P.ntaps * kPolyDeg);
+  for (int mi = 0; mi < P.ntaps; mi++) {
+    const int m = P.mlo + mi;
+    double c[kPolyDeg] = {0};
+    for (int i = 0; i < kPolyNodes; i++) {
+      const double th = M_PI * (i + 0.5) / kPolyNodes, y = cos(th), phi = 0.5 * (y + 1.0);
+      const double fv = eq6_samples((double)m - phi, H);
+      for (int k = 0; k < kPolyDeg; k++) c[k] += fv * cos(k * th);  // T_k(y) = cos(k theta)
+    }
+    for (int k = 0; k < kPolyDeg; k++) tab[(size_t)mi * kPolyDeg + k] = (float)(c[k] * (k ? 2.0 : 1.0) / kPolyNodes);
+  }
+  const size_t bytes = tab.size() * sizeof(float);
+  cudaError_t e = cudaMalloc(&P.dev, bytes);
+  if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMalloc(poly)"); return nullptr; }
+  e = cudaMemcpyAsync(P.dev, tab.data(), bytes, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // the staging vector goes out of scope
+  if (e != cudaSuccess) { cudaFree(P.dev); *err = cuda_fail(e, "upload(poly)"); return nullptr; }
+  d->polys.push_back(P);
+  return &d->polys.back();
+}
+
+// Mode tables of one call (LUT: phase-major smem table; texture LUT: filtered texture; polyphase table).
 int setup_mode(DeviceState* d, const gpurir_opts& o, double fs, double H, cudaStream_t stream, IsmArgs& A) {
   int st = GPURIR_OK;
   std::lock_guard<std::mutex> lk(g_mu);
@@ -172,12 +221,16 @@ int setup_mode(DeviceState* d, const gpurir_opts& o, double fs, double H, cudaSt
     A.tex = (unsigned long long)T->tex;
     A.texQ = (float)o.lut_Q;
     A.tex_off = (float)((double)T->half + 0.5);
+  } else if (o.mode == GPURIR_POLY) {
+    const PolyEntry* P = ensure_poly(d, o.Tw, fs, stream, &st);
+    if (!P) return st;
+    A.poly_P = P->dev; A.poly_ntaps = P->ntaps; A.poly_mlo = P->mlo;
   }
   return GPURIR_OK;
 }
 
 int validate_mode(const gpurir_opts& o) {
-  if (o.mode < GPURIR_FP32 || o.mode > GPURIR_LUT_TEX) return GPURIR_EINVAL;
+  if (o.mode < GPURIR_FP32 || o.mode > GPURIR_POLY) return GPURIR_EINVAL;
   if (o.mode == GPURIR_LUT && (o.lut_Q & (o.lut_Q - 1))) return GPURIR_EINVAL;  // power of two (R4)
   return GPURIR_OK;
 }
@@ -425,7 +478,8 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     A.M_src = M_src; A.M_rcv = M_rcv; A.M = (int)M;
     A.nISM = (int)nISM;
     A.row_stride = nS;
-    const bool persistent = use_persistent(((nISM + kTC - 1) / kTC) * M, o.split, d);
+    const bool poly = o.mode == GPURIR_POLY;
+    const bool persistent = poly || use_persistent(((nISM + kTC - 1) / kTC) * M, o.split, d);
     const int tile_len = persistent ? kTCPersistent : kTC;
     A.nTiles = (int)((nISM + tile_len - 1) / tile_len);
     fill_common(A, fs, c, o.Tw);
@@ -435,7 +489,9 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     long long nclusters = (long long)A.nTiles * M;
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
-    if (persistent) {
+    if (poly) {
+      e = launch_ism_poly(A, nclusters, take_counter(d), d->num_sms, stream);
+    } else if (persistent) {
       e = launch_ism_ws(A, o.mode, nclusters, take_counter(d), d->num_sms, stream);
     } else {
       int split = auto_split(nclusters, o.split);
@@ -522,7 +578,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     int nch = nISM < nS ? (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4)) : 0;
     for (int ch = 0; ch < nch; ch++) chunks.push_back(make_int2(i, ch));
   }
-  const bool persistent = use_persistent(small_tiles, o.split, d);
+  const bool persistent = o.mode == GPURIR_POLY || use_persistent(small_tiles, o.split, d);
   const int tile_len = persistent ? kTCPersistent : kTC;
   // heavy-first schedule without a comparison sort: image density grows ~ t^2 (SURVEY §7 hard part 2), so
   // emit all rooms' last tiles first, then the second-to-last, ... (a counting order over tile index)
@@ -563,7 +619,8 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     if ((st = setup_mode(d, o, fs, H, stream, A))) { cudaFreeAsync(ws, stream); return st; }
     long long nw = (long long)tiles.size();
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
-    if (persistent) e = launch_ism_ws(A, o.mode, nw, take_counter(d), d->num_sms, stream);
+    if (o.mode == GPURIR_POLY) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, stream);
+    else if (persistent) e = launch_ism_ws(A, o.mode, nw, take_counter(d), d->num_sms, stream);
     else e = launch_ism(A, o.mode, auto_split(nw, o.split), nw, stream);
     if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_ism(batch)"); }
     if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);

@@ -1,0 +1,328 @@
+// ism_poly_kernel.cu — polyphase ISM accumulation, "bin then filter" (mode GPURIR_POLY; hot-path rows
+// a1-a3 of SURVEY.md §8(a), reading R11 of DESIGN.md).
+//
+// Eq. 5 with the windowed sinc of Eq. 6 sums A_n delta'(k - x_n) over every image n and
+// sample k.  Writing x_n = j_n + phi_n (j_n = floor(x_n)) and expanding delta' on each integer tap
+// m = k - j_n in Chebyshev polynomials of the fractional delay,
+//     delta'(m - phi) = sum_d P_d[m] T_d(2 phi - 1),   d = 0..7   (max error 4.3e-7, host fit),
+// the RIR becomes a fixed 8-channel FIR filter applied to per-sample image aggregates:
+//     h[k] = sum_m sum_d P_d[m] G_d[k - m],   G_d[j] = sum_{n: j_n = j} A_n T_d(2 phi_n - 1).
+// Per work item (RIR, 512-sample tile) a CTA
+//   1. enumerates the tile's shell of images column by column (as ism_ws_kernel) and adds each image's
+//      8 channel values into G in shared memory — as 64-bit fixed point with integer atomics, so the sums
+//      are exact and independent of the order the images arrive in (deterministic, shard-invariant);
+//   2. converts G to fp32 and runs the 8-channel FIR (2H taps) for its 512 outputs, one per thread,
+//      writing the tile once, coalesced.
+// Work per output sample no longer grows with the image density (690 in-window taps per sample at config
+// 3 (i)): the filter costs 2H x 8 MACs, the aggregation 8 channel updates per image.
+#include "ism_common.cuh"
+
+namespace gpurir {
+
+constexpr int kPolyThreads = 512;
+constexpr int kPolyTC = kTCPersistent;  // 512 output samples per work item (the host planner's tile)
+constexpr int kPolyD = 8;               // Chebyshev channels T_0..T_7
+constexpr int kPolyCols = kPolyThreads; // lattice columns per enumeration batch
+constexpr int kPolyBz = 1024;           // z-factor table entries
+static_assert(kPolyTC == kPolyThreads, "one output sample per thread in the filter phase");
+
+struct PolyColRec {  // 32 B, as WsColRec
+  double rho2;
+  float bxy, cdot;
+  int r1lo, r2lo, r1n;
+  float sdot;
+};
+
+struct PolyTile {
+  RirGeom g;
+  double dlo2, dhi2, invLz, offE, offO, scale, inv_scale;
+  long long row;
+  int t0, te, tc, nx0, ny0, NX, ncols, zl, zh, use_bz, next;
+  float invNX;
+};
+
+struct PolySmem {
+  PolyTile ti;
+  PolyColRec col[kPolyCols];
+  int colpre[kPolyCols];
+  int scan_tmp[kPolyThreads / 32];
+  float bz[kPolyBz];
+};
+
+__device__ __forceinline__ int poly_block_scan(int v, int* tmp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = warp_incl_scan(v, lane);
+  if (lane == 31) tmp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < kPolyThreads / 32 ? tmp[lane] : 0;
+    t = warp_incl_scan(t, lane);
+    if (lane < kPolyThreads / 32) tmp[lane] = t;
+  }
+  __syncthreads();
+  return x + (w > 0 ? tmp[w - 1] : 0);
+}
+
+// z-axis factor of beta_n (C2)
+__device__ __forceinline__ float poly_z_factor(int nz, const RirGeom& g) {
+  uint32_t sgn = 0;
+  bool zero = false;
+  float lz = axis_beta(nz, 2, g, sgn, zero);
+  float v = zero ? 0.f : ex2_approx(lz);
+  return sgn ? -v : v;
+}
+
+// One image's 8 channel values A T_d(y), d = 0..7, added to G[.][p] as integers: v = round(A T_d 2^s) with
+// |v| <= 2^28 (the per-RIR scale bounds |A| by the direct path), split v = a 2^14 + b, b in [0, 2^14), and the
+// two parts accumulated in separate int32 planes with plain shared-memory reductions (no return value, no
+// carry).  Integer adds commute, so G does not depend on the order in which images arrive (deterministic,
+// shard-invariant); each plane holds 2^17 terms per position before it could overflow.
+__device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, float y, float amp, double scale) {
+  const double yd = (double)y, y2 = 2.0 * yd, ad = (double)amp * scale;
+  const double magic = 6755399441055744.0;  // 1.5 2^52: the low 32 bits of (v + magic) hold round(v)
+  double T[kPolyD];
+  T[0] = 1.0;
+  T[1] = yd;
+#pragma unroll
+  for (int d = 2; d < kPolyD; d++) T[d] = fma(y2, T[d - 1], -T[d - 2]);  // T_d = 2 y T_{d-1} - T_{d-2}
+#pragma unroll
+  for (int d = 0; d < kPolyD; d++) {
+    const int v = __double2loint(fma(ad, T[d], magic));
+    const int i = d * npos + p;  // channel-major planes: consecutive positions are consecutive words
+    atomicAdd(&Ga[i], v >> 14);
+    atomicAdd(&Gb[i], v & 0x3FFF);
+  }
+}
+
+__global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, long long n_work, int* work_counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PolySmem& sm = *reinterpret_cast<PolySmem*>(smem_raw);
+  const int ntaps = A.poly_ntaps, npos = kPolyTC + ntaps - 1;
+  int* Ga = reinterpret_cast<int*>(smem_raw + sizeof(PolySmem));  // coarse part of G (units 2^14)
+  int* Gb = Ga + kPolyD * npos;                                    // fine part of G
+  float* Pt = reinterpret_cast<float*>(Gb + kPolyD * npos);        // [ntaps][8], tap index mi = m - m_lo
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double fs_over_c = A.fs_over_c, sc2 = fs_over_c * fs_over_c;
+  const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f;
+  const int m_hi = A.poly_mlo + ntaps - 1;
+
+  for (int i = tid; i < ntaps * kPolyD; i += kPolyThreads) Pt[i] = A.poly_P[i];
+
+  for (;;) {
+    if (tid == 0) {
+      const long long wi = atomicAdd(work_counter, 1);
+      PolyTile& T = sm.ti;
+      T.next = wi < n_work;
+      if (wi < n_work) {
+        int m, tile, nISM;
+        long long row;
+        const float zero3[3] = {0.f, 0.f, 0.f};
+        if (A.jobs) {
+          const int2 jt = A.tiles[wi];
+          const BatchJob& J = A.jobs[jt.x];
+          m = jt.x; tile = jt.y; nISM = J.nISM; row = J.out_offset;
+          geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.ors, J.spkr_pattern, J.lb, J.neg, J.zero, T.g,
+                    A.status);
+        } else {
+          tile = A.nTiles - 1 - (int)(wi / A.M);  // heaviest (latest) tiles first
+          m = (int)(wi % A.M);
+          nISM = A.nISM;
+          row = (long long)m * A.row_stride;
+          const int ms = m / A.M_rcv, mr = m % A.M_rcv;
+          geom_from(A.L, A.pos_src + 3 * ms, A.pos_rcv + 3 * mr, A.orv ? A.orv + 3 * mr : zero3, A.nb, A.pattern,
+                    A.ors ? A.ors + 3 * ms : zero3, A.spkr_pattern, A.lb, A.neg, A.zero, T.g, A.status);
+        }
+        T.row = row;
+        T.t0 = tile * kPolyTC;
+        T.te = min(T.t0 + kPolyTC, nISM);
+        T.tc = T.t0 + kPolyTC / 2;
+        T.invLz = 1.0 / T.g.L[2];
+        T.offE = T.g.s[2] - T.g.r[2];
+        T.offO = -T.g.s[2] - T.g.r[2];
+        // images with floor(x) in [t0 - m_hi, te - 1 - m_lo] reach samples [t0, te)
+        const double xlo = (double)(T.t0 - m_hi), xhi = (double)(T.te - A.poly_mlo);
+        const double dlo = xlo > 0.0 ? xlo * A.c_over_fs : 0.0, dhi = xhi * A.c_over_fs;
+        T.dlo2 = dlo * dlo;
+        T.dhi2 = dhi * dhi;
+        int lo[2], hi[2];
+        for (int ax = 0; ax < 2; ax++) {
+          const double L = T.g.L[ax], r = T.g.r[ax];
+          const int a = (int)floor((r - dhi) / L) - 1, b = (int)floor((r + dhi) / L) + 1;
+          lo[ax] = max(a, T.g.nlo[ax]);
+          hi[ax] = min(b, T.g.nhi[ax] - 1);
+        }
+        T.nx0 = lo[0]; T.ny0 = lo[1];
+        T.NX = max(0, hi[0] - lo[0] + 1);
+        T.ncols = T.NX * max(0, hi[1] - lo[1] + 1);
+        T.invNX = T.NX > 0 ? 1.f / (float)T.NX : 0.f;
+        T.zl = T.g.nlo[2];
+        T.zh = T.g.nhi[2] - 1;
+        T.use_bz = (T.zh - T.zl + 1) <= kPolyBz;
+        // fixed-point scale: |A_n| <= 1 / (4 pi d_dp) (|beta|, |g| <= 1; the direct image is the closest) and
+        // |T_d| <= 1, so every channel value is at most 2^28 in units of 2^-s
+        const double ddx = T.g.s[0] - T.g.r[0], ddy = T.g.s[1] - T.g.r[1], ddz = T.g.s[2] - T.g.r[2];
+        const double abound = 0.0795774715459476679 / fmax(sqrt(ddx * ddx + ddy * ddy + ddz * ddz), 1e-30);
+        const int e = (int)ceil(log2(abound));
+        T.scale = ldexp(1.0, 28 - e);
+        T.inv_scale = ldexp(1.0, e - 28);
+      }
+    }
+    __syncthreads();
+    if (!sm.ti.next) break;
+    const PolyTile& T = sm.ti;
+    const RirGeom& g = T.g;
+    for (int i = tid; i < kPolyD * npos; i += kPolyThreads) { Ga[i] = 0; Gb[i] = 0; }
+    if (T.use_bz)
+      for (int i = tid; i <= T.zh - T.zl; i += kPolyThreads) sm.bz[i] = poly_z_factor(T.zl + i, g);
+
+    // ---- 1. image aggregation -------------------------------------------------------------
+    const float amp_scale = fs_over_c_4pi;
+    const int pofs = kPolyTC / 2 + m_hi;  // p = floor(x - tc) + pofs
+    for (int qb = 0; qb < T.ncols; qb += kPolyCols) {
+      int cnt = 0;
+      {
+        const int q = qb + tid;
+        PolyColRec cr;
+        cr.r1lo = 0; cr.r2lo = 0; cr.r1n = 0; cr.rho2 = 0.0; cr.bxy = 0.f; cr.cdot = 0.f; cr.sdot = 0.f;
+        if (q < T.ncols) {
+          const int qy = (int)(((float)q + 0.5f) * T.invNX);
+          const int nx = T.nx0 + (q - qy * T.NX), ny = T.ny0 + qy;
+          const double dx = image_coord(nx, g.L[0], g.s[0]) - g.r[0];
+          const double dy = image_coord(ny, g.L[1], g.s[1]) - g.r[1];
+          const double rho2 = dx * dx + dy * dy;
+          cr.rho2 = rho2;
+          cr.cdot = (float)dx * g.o[0] + (float)dy * g.o[1];
+          cr.sdot = src_col_dot(nx, ny, (float)dx, (float)dy, g);
+          uint32_t sgn = 0;
+          bool zero = false;
+          const float lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
+          const float bxy = zero ? 0.f : ex2_approx(lxy);
+          cr.bxy = (sgn ? -bxy : bxy) * amp_scale;
+          if (rho2 < T.dhi2) {
+            const double zhi = (double)sqrtf((float)(T.dhi2 - rho2));
+            const double zlo = T.dlo2 > rho2 ? (double)sqrtf((float)(T.dlo2 - rho2)) : 0.0;
+            int pa, pb, na, nbz;
+            z_range(g, T.invLz, zlo, zhi, pa, pb);
+            z_range(g, T.invLz, -zhi, -zlo, na, nbz);
+            if (nbz >= pa - 1) { pa = min(pa, na); na = 1; nbz = 0; }
+            pa = max(pa, T.zl); pb = min(pb, T.zh);
+            na = max(na, T.zl); nbz = min(nbz, T.zh);
+            const int n1 = max(0, pb - pa + 1), n2 = max(0, nbz - na + 1);
+            cr.r1lo = pa; cr.r1n = n1; cr.r2lo = na;
+            cnt = n1 + n2;
+          }
+        }
+        sm.col[tid] = cr;
+      }
+      sm.colpre[tid] = poly_block_scan(cnt, sm.scan_tmp);
+      __syncthreads();
+      const int total = sm.colpre[kPolyCols - 1];
+      const int R = (total + kPolyThreads - 1) / kPolyThreads;
+      const int g0 = tid * R, g1 = min(g0 + R, total);
+      if (g0 < g1) {
+        int lo = 0, hi = kPolyCols - 1;  // first column with colpre > g0
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (sm.colpre[mid] > g0) hi = mid; else lo = mid + 1;
+        }
+        int j = lo;
+        int before = j > 0 ? sm.colpre[j - 1] : 0;
+        int boundary = sm.colpre[j];
+        const double Lz = g.L[2], offE = T.offE, offO = T.offO;
+        const float Lzf = (float)Lz, offEf = (float)offE, offOf = (float)offO;
+        const int tc = T.tc, zl = T.zl;
+        const bool use_bz = T.use_bz, dir_src = g.as != 1.f;
+        const float oz = g.o[2], ga = g.a, fsc = (float)fs_over_c;
+        for (int gi = g0; gi < g1; gi++) {
+          while (gi >= boundary) { before = boundary; j++; boundary = sm.colpre[j]; }
+          const PolyColRec& cr = sm.col[j];
+          const int l = gi - before;
+          const int nz = l < cr.r1n ? cr.r1lo + l : cr.r2lo + (l - cr.r1n);
+          const int odd = nz & 1;
+          const float bz = use_bz ? sm.bz[min(max(nz - zl, 0), kPolyBz - 1)] : poly_z_factor(nz, g);
+          const int nzo = nz + odd;
+          const double dz = fma(int_to_double(nzo), Lz, odd ? offO : offE);  // Eq. 1 along z
+          const double x2 = fma(dz, dz, cr.rho2) * sc2;                       // (d fs / c)^2
+          if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); continue; }
+          float x0f, rx;
+          const float xr = delay_rel(x2, tc, x0f, rx);  // x - tc, fp64-corrected; rx = 1/x
+          int jodd;
+          const float fj = floor_parity(xr, jodd);
+          const int p = (int)fj + pofs;
+          if (p < 0 || p >= npos) continue;  // reaches no sample of this tile
+          const float dzf = fmaf((float)nzo, Lzf, odd ? offOf : offEf);
+          const float cth = fmaf(dzf, oz, cr.cdot) * (fsc * rx);
+          float gain = ga + (1.f - ga) * cth;
+          if (dir_src) gain *= src_gain(cr.sdot, odd, dzf, fsc * rx, g);
+          const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
+          const float y = fmaf(2.f, xr - fj, -1.f);        // 2 phi - 1 in [-1, 1)
+          poly_add(Ga, Gb, npos, p, y, amp, T.scale);
+        }
+      }
+      __syncthreads();  // column records are replaced by the next batch
+    }
+
+    // ---- 2. fixed point -> fp32, channel pairs interleaved: Gf[pair][p] = (G_2q, G_2q+1) ----
+    float2* Gf = reinterpret_cast<float2*>(Ga);  // in place over Ga / Gb
+    // convert into registers first (every thread reads its own words), then barrier, then write
+    float2 tmp[(kPolyD / 2) * 2];
+    int nmine = 0;
+    for (int p = tid; p < npos && nmine < 2; p += kPolyThreads, nmine++) {
+#pragma unroll
+      for (int q = 0; q < kPolyD / 2; q++) {
+        const int i0 = (2 * q) * npos + p, i1 = (2 * q + 1) * npos + p;
+        const long long v0 = (long long)Ga[i0] * 16384 + Gb[i0];
+        const long long v1 = (long long)Ga[i1] * 16384 + Gb[i1];
+        tmp[nmine * (kPolyD / 2) + q] =
+            make_float2((float)((double)v0 * T.inv_scale), (float)((double)v1 * T.inv_scale));
+      }
+    }
+    __syncthreads();
+    nmine = 0;
+    for (int p = tid; p < npos && nmine < 2; p += kPolyThreads, nmine++) {
+#pragma unroll
+      for (int q = 0; q < kPolyD / 2; q++) Gf[q * npos + p] = tmp[nmine * (kPolyD / 2) + q];
+    }
+    __syncthreads();
+
+    // ---- 3. 8-channel FIR: h[k] = sum_m sum_d P_d[m] G_d[k - m] --------------------------------
+    {
+      const int t = tid;
+      float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+      const float4* P4 = reinterpret_cast<const float4*>(Pt);
+      int p = t + ntaps - 1;  // position of tap mi = 0 (m = m_lo): j = k - m_lo
+#pragma unroll 4
+      for (int mi = 0; mi < ntaps; mi++, p--) {
+        const float4 pa = P4[2 * mi], pb = P4[2 * mi + 1];
+        const float2 g0 = Gf[p], g1 = Gf[npos + p], g2 = Gf[2 * npos + p], g3 = Gf[3 * npos + p];
+        a0 = __ffma2_rn(make_float2(pa.x, pa.y), g0, a0);
+        a1 = __ffma2_rn(make_float2(pa.z, pa.w), g1, a1);
+        a0 = __ffma2_rn(make_float2(pb.x, pb.y), g2, a0);
+        a1 = __ffma2_rn(make_float2(pb.z, pb.w), g3, a1);
+      }
+      const int k = T.t0 + t;
+      if (k < T.te) A.out[T.row + k] = (a0.x + a0.y) + (a1.x + a1.y);
+    }
+    __syncthreads();  // G and the tile record are reused by the next work item
+  }
+  (void)lane; (void)warp;
+}
+
+size_t ism_poly_smem_bytes(int ntaps) {
+  const size_t npos = (size_t)kPolyTC + ntaps - 1;
+  return sizeof(PolySmem) + 2 * kPolyD * npos * sizeof(unsigned) + (size_t)ntaps * kPolyD * sizeof(float);
+}
+
+cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  const size_t smem = ism_poly_smem_bytes(A.poly_ntaps);
+  e = cudaFuncSetAttribute(ism_poly_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long slots = 2LL * num_sms;
+  const int grid = (int)(n_work < slots ? n_work : slots);
+  ism_poly_kernel<<<grid, kPolyThreads, smem, stream>>>(A, n_work, counter);
+  return cudaGetLastError();
+}
+
+}  // namespace gpurir

@@ -70,6 +70,9 @@ struct IsmArgs {
   // sampled with hardware linear filtering; a tap at offset u = k - x samples reads coordinate u Q + tex_off
   unsigned long long tex;  // cudaTextureObject_t
   float texQ, tex_off;     // Q and half + 0.5 (texel centres)
+  // polyphase mode (reading R11): delta'(m - phi) = sum_d P[m - mlo][d] T_d(2 phi - 1), m = mlo .. mlo + ntaps - 1
+  const float* poly_P;     // device [ntaps][8]
+  int poly_ntaps, poly_mlo;
 };
 
 struct TailArgs {
@@ -99,6 +102,8 @@ cudaError_t launch_image_params(const IsmArgs& A, double* x_out, float* A_out, l
 size_t ism_ws_smem_bytes(int mode, int lut_rows, int lut_cols);
 cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* counter, int num_sms,
                           cudaStream_t stream);
+size_t ism_poly_smem_bytes(int ntaps);
+cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, cudaStream_t stream);
 cudaError_t launch_tail(const TailArgs& A, long long n_items, cudaStream_t stream);  // one warp per item
 
 cudaError_t launch_traj(const float* sig, long long n_sig, const float* rirs, int n_points, int n_mics, long long L,

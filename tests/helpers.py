@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import numpy as np
 
-TOL = {"fp32": 1e-4, "lut": 5e-3, "fp16": 2e-2, "lut_tex": 5e-3}  # north_star (lut_tex = LUT), per RIR, relative to max|h_oracle| (C20)
+TOL = {"fp32": 1e-4, "lut": 5e-3, "fp16": 2e-2, "lut_tex": 5e-3, "poly": 1e-4}  # north_star (lut_tex = LUT, poly = fp32), per RIR, relative to max|h_oracle| (C20)
 
 
 def derive(oracle, sc):

@@ -128,7 +128,7 @@ def test_mode_validation_on_host(P):
     that passes host validation goes on to the device, which this container lacks (ECUDA = 5)."""
     import torch
     assert _dir_call(P, 0, None, mode=1, Q=10) == 1
-    assert _dir_call(P, 0, None, mode=4) == 1
+    assert _dir_call(P, 0, None, mode=5) == 1
     if not torch.cuda.is_available():
         assert _dir_call(P, 0, None, mode=3, Q=10) == 5
         assert _dir_call(P, 0, None, mode=1, Q=16) == 5

@@ -55,7 +55,7 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden", "survey_appendix_b.json
 
 
 @pytest.mark.parametrize("case", ["G1", "G2", "G3", "G4"])
-@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex"])
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex", "poly"])
 def test_goldens(P, oracle, case, mode):
     import torch
     g = json.load(open(GOLD))["cases"][case]
@@ -76,7 +76,7 @@ def test_goldens(P, oracle, case, mode):
 
 
 @pytest.mark.parametrize("kernel", ["auto", "persistent"])
-@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex"])
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex", "poly"])
 def test_random_scenes(P, oracle, mode, kernel):
     """S:525 style: random rooms 2-8 m, T60 0.3-1.0, <=2 src x 3 rcv, all patterns, 16 and 48 kHz.
     kernel = persistent forces the warp-specialised kernel (split = -1) on these small calls."""
@@ -106,7 +106,7 @@ def test_cfg1_fp32(P, oracle):
     assert rel_err(g, r)[0] <= TOL["fp32"]
 
 
-@pytest.mark.parametrize("mode", ["lut", "fp16", "lut_tex"])
+@pytest.mark.parametrize("mode", ["lut", "fp16", "lut_tex", "poly"])
 def test_cfg1_modes(P, oracle, mode):
     sc = W.cfg1()
     beta, nb = derive(oracle, sc)
@@ -126,7 +126,7 @@ def test_cfg2_t60_sweep(P, oracle, T60):
 
 
 @pytest.mark.parametrize("kernel", ["auto", "persistent"])
-@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex"])
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex", "poly"])
 def test_cfg3_subset(P, oracle, mode, kernel):
     """#RIR sweep room, cardioid with random orientations, diffuse variant; first 24 receivers."""
     sc = W.cfg3(24, "diffuse")
@@ -150,7 +150,7 @@ def test_cfg3_full_size_sampled(P, oracle):
 
 
 @pytest.mark.parametrize("kernel", ["auto", "persistent"])
-@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex"])
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex", "poly"])
 def test_cfg4_48k_array(P, oracle, mode, kernel):
     sc = W.cfg4("a")
     sc.pos_rcv = sc.pos_rcv[:8]
@@ -401,7 +401,7 @@ def _run_dir(P, sc, beta, nb, spkr, ors, mode="fp32", split=0):
 
 
 @pytest.mark.parametrize("kernel", ["auto", "persistent"])
-@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex"])
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex", "poly"])
 def test_source_directivity_random_scenes(P, oracle, mode, kernel):
     """f3 (reading R10): random rooms, all source and receiver patterns, 16 / 48 kHz, both ISM kernels."""
     rng = np.random.default_rng(3310)

@@ -17,7 +17,7 @@ import workloads as W  # noqa: E402
 from helpers import TOL, derive, rel_err, run_gpu, run_oracle  # noqa: E402
 
 
-def report(name, sc, modes=("fp32", "lut", "fp16", "lut_tex"), kernels=(0, -1)):
+def report(name, sc, modes=("fp32", "lut", "fp16", "lut_tex", "poly"), kernels=(0, -1)):
     beta, nb = derive(oracle, sc)
     r = run_oracle(oracle, sc, beta, nb)
     for mode in modes:

@@ -67,7 +67,7 @@ def main():
     rows = []
 
     # config 1: latency of the single-RIR ISM-only call
-    for mode in ("fp32", "lut", "fp16", "lut_tex"):
+    for mode in ("fp32", "lut", "fp16", "lut_tex", "poly"):
         fn, nb = scene_call(W.cfg1(), mode)
         ms = time_call(fn, reps=20, warm=5)
         rows.append(dict(cfg="cfg1", mode=mode, M=1, ms=ms, rirs_per_s=1e3 / ms))
@@ -84,7 +84,7 @@ def main():
     # config 3: #RIR sweep (diffuse and full ISM), 3 modes
     Ms = [1, 16, 128, 1024, 4096, 16384]
     for variant in ("diffuse", "full"):
-        for mode in ("fp32", "lut", "fp16", "lut_tex"):
+        for mode in ("fp32", "lut", "fp16", "lut_tex", "poly"):
             for M in Ms:
                 if variant == "full" and M > 4096 and args.quick:
                     continue
@@ -97,7 +97,7 @@ def main():
 
     # config 4: 32-mic array at 48 kHz, three modes
     for variant in ("a", "b"):
-        for mode in ("fp32", "lut", "fp16", "lut_tex"):
+        for mode in ("fp32", "lut", "fp16", "lut_tex", "poly"):
             fn, nb = scene_call(W.cfg4(variant), mode)
             ms = time_call(fn, reps=reps, warm=2)
             rows.append(dict(cfg=f"cfg4{variant}", mode=mode, M=32, ms=ms, rirs_per_s=32 / ms * 1e3,
