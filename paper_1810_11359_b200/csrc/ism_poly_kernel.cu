@@ -33,6 +33,8 @@ struct PolyColRec {  // 32 B, as WsColRec
   float sdot;
 };
 
+static_assert(sizeof(PolyColRec) * kPolyCols >= 4 * kPolyTC * sizeof(float), "FIR partial sums reuse sm.col");
+
 struct PolyTile {
   RirGeom g;
   double dlo2, dhi2, invLz, offE, offO, scale, inv_scale;
@@ -262,9 +264,10 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
       __syncthreads();  // column records are replaced by the next batch
     }
 
-    // ---- 2. fixed point -> fp32, channel pairs interleaved: Gf[pair][p] = (G_2q, G_2q+1) ----
-    float2* Gf = reinterpret_cast<float2*>(Ga);  // in place over Ga / Gb
-    // convert into registers first (every thread reads its own words), then barrier, then write
+    // ---- 2. fixed point -> fp32 in 4 channel-pair planes, Gf[pair][pad(p)] = (G_2q, G_2q+1) ------------
+    // pad(p) = p + p/4: the filter's lanes read positions 4 apart, which the padding spreads over all banks
+    float2* Gf = reinterpret_cast<float2*>(Ga);  // in place over Ga / Gb (read everything, barrier, write)
+    const int plane = npos + (npos >> 2) + 1;
     float2 tmp[(kPolyD / 2) * 2];
     int nmine = 0;
     for (int p = tid; p < npos && nmine < 2; p += kPolyThreads, nmine++) {
@@ -281,27 +284,46 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
     nmine = 0;
     for (int p = tid; p < npos && nmine < 2; p += kPolyThreads, nmine++) {
 #pragma unroll
-      for (int q = 0; q < kPolyD / 2; q++) Gf[q * npos + p] = tmp[nmine * (kPolyD / 2) + q];
+      for (int q = 0; q < kPolyD / 2; q++) Gf[q * plane + p + (p >> 2)] = tmp[nmine * (kPolyD / 2) + q];
     }
     __syncthreads();
 
     // ---- 3. 8-channel FIR: h[k] = sum_m sum_d P_d[m] G_d[k - m] --------------------------------
+    // Thread group gq (128 threads) applies channel pair gq to 4 consecutive outputs per thread with a
+    // sliding register window (one new position per tap); the 4 groups' partial sums meet in shared memory.
     {
-      const int t = tid;
-      float2 a0 = make_float2(0.f, 0.f), a1 = a0;
-      const float4* P4 = reinterpret_cast<const float4*>(Pt);
-      int p = t + ntaps - 1;  // position of tap mi = 0 (m = m_lo): j = k - m_lo
-#pragma unroll 4
-      for (int mi = 0; mi < ntaps; mi++, p--) {
-        const float4 pa = P4[2 * mi], pb = P4[2 * mi + 1];
-        const float2 g0 = Gf[p], g1 = Gf[npos + p], g2 = Gf[2 * npos + p], g3 = Gf[3 * npos + p];
-        a0 = __ffma2_rn(make_float2(pa.x, pa.y), g0, a0);
-        a1 = __ffma2_rn(make_float2(pa.z, pa.w), g1, a1);
-        a0 = __ffma2_rn(make_float2(pb.x, pb.y), g2, a0);
-        a1 = __ffma2_rn(make_float2(pb.z, pb.w), g3, a1);
+      const int gq = tid >> 7, lt = tid & 127, t4 = 4 * lt;
+      const float2* G = Gf + gq * plane;
+      const float2* P2 = reinterpret_cast<const float2*>(Pt) + gq;  // (P_2gq, P_2gq+1)[mi] at P2[4 mi]
+      float2 acc[4], w[4];
+      int q = t4 + ntaps - 1;  // position of output t4 at tap mi = 0 (m = m_lo)
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        acc[r] = make_float2(0.f, 0.f);
+        w[r] = G[(q + r) + ((q + r) >> 2)];
       }
-      const int k = T.t0 + t;
-      if (k < T.te) A.out[T.row + k] = (a0.x + a0.y) + (a1.x + a1.y);
+      for (int mi = 0; mi < ntaps; mi += 4) {  // unrolled by 4 so the window shift is register renaming
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          if (mi + u < ntaps) {
+            const float2 pc = P2[4 * (mi + u)];
+#pragma unroll
+            for (int r = 0; r < 4; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 3], acc[r]);
+            const int qn = q - (mi + u) - 1;  // next tap's new (lowest) position
+            if (mi + u + 1 < ntaps) w[(3 - u) & 3] = G[qn + (qn >> 2)];
+          }
+        }
+      }
+      float* red = reinterpret_cast<float*>(sm.col);  // 4 x 512 partial sums (the column records are dead here)
+      reinterpret_cast<float4*>(red + gq * kPolyTC)[lt] =
+          make_float4(acc[0].x + acc[0].y, acc[1].x + acc[1].y, acc[2].x + acc[2].y, acc[3].x + acc[3].y);
+    }
+    __syncthreads();
+    {
+      const float* red = reinterpret_cast<const float*>(sm.col);
+      const int k = T.t0 + tid;
+      if (k < T.te)
+        A.out[T.row + k] = (red[tid] + red[kPolyTC + tid]) + (red[2 * kPolyTC + tid] + red[3 * kPolyTC + tid]);
     }
     __syncthreads();  // G and the tile record are reused by the next work item
   }
@@ -310,7 +332,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
 
 size_t ism_poly_smem_bytes(int ntaps) {
   const size_t npos = (size_t)kPolyTC + ntaps - 1;
-  return sizeof(PolySmem) + 2 * kPolyD * npos * sizeof(unsigned) + (size_t)ntaps * kPolyD * sizeof(float);
+  return sizeof(PolySmem) + 2 * kPolyD * npos * sizeof(int) + (size_t)ntaps * kPolyD * sizeof(float);
 }
 
 cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, cudaStream_t stream) {
