@@ -206,6 +206,18 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
   return &d->polys.back();
 }
 
+// Polyphase fixed-point width (ism_poly_kernel.cu, poly_add): a shoebox lattice holds one image per room
+// volume V, so about 4 pi d^2 (c / fs) / V images share one integer sample position at distance d.  With twice
+// that at the farthest ISM delay (+16) as the bound N, single-word accumulation with 2^bits N <= 2^30 is used
+// when it leaves bits >= 22 (N <= 256); otherwise 0 selects the two-word scheme (2^28 resolution).
+int poly_bits_for(const float L[3], long long nISM, double fs, double c, double Tw) {
+  const double V = (double)L[0] * L[1] * L[2];
+  const double dmax = ((double)nISM + Tw * fs / 2.0 + 1.0) * c / fs;
+  const double N = 2.0 * 4.0 * M_PI * dmax * dmax * (c / fs) / V + 16.0;
+  if (!(N <= 256.0)) return 0;
+  return 30 - (int)ceil(log2(N));
+}
+
 // Mode tables of one call (LUT: phase-major smem table; texture LUT: filtered texture; polyphase table).
 int setup_mode(DeviceState* d, const gpurir_opts& o, double fs, double H, cudaStream_t stream, IsmArgs& A) {
   int st = GPURIR_OK;
@@ -486,6 +498,7 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     A.out = out;
     A.status = d->status;
     if ((st = setup_mode(d, o, fs, H, stream, A))) return st;
+    A.poly_bits = poly_bits_for(room_sz, nISM, fs, c, o.Tw);
     long long nclusters = (long long)A.nTiles * M;
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
@@ -573,6 +586,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     double T60 = sabine(R.room_sz, R.beta);
     J.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);
     J.rir_global = o.rir_index_base + (unsigned long long)i;
+    J.poly_bits = poly_bits_for(R.room_sz, nISM, fs, c, o.Tw);
     small_tiles += (nISM + kTC - 1) / kTC;
     long long groups = (nS + 3) / 4 - nISM / 4;
     int nch = nISM < nS ? (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4)) : 0;

@@ -38,14 +38,15 @@ static_assert(sizeof(PolyColRec) * kPolyCols >= 4 * kPolyTC * sizeof(float), "FI
 struct PolyTile {
   RirGeom g;
   double dlo2, dhi2, invLz, offE, offO, scale, inv_scale;
+  int two_word;
   long long row;
   int t0, te, tc, nx0, ny0, NX, ncols, zl, zh, use_bz, next;
   float invNX;
 };
 
-struct PolySmem {
+struct alignas(16) PolySmem {
   PolyTile ti;
-  PolyColRec col[kPolyCols];
+  alignas(16) PolyColRec col[kPolyCols];  // 16-B aligned: reused as float4 partial sums by the FIR
   int colpre[kPolyCols];
   int scan_tmp[kPolyThreads / 32];
   float bz[kPolyBz];
@@ -74,12 +75,15 @@ __device__ __forceinline__ float poly_z_factor(int nz, const RirGeom& g) {
   return sgn ? -v : v;
 }
 
-// One image's 8 channel values A T_d(y), d = 0..7, added to G[.][p] as integers: v = round(A T_d 2^s) with
-// |v| <= 2^28 (the per-RIR scale bounds |A| by the direct path), split v = a 2^14 + b, b in [0, 2^14), and the
-// two parts accumulated in separate int32 planes with plain shared-memory reductions (no return value, no
-// carry).  Integer adds commute, so G does not depend on the order in which images arrive (deterministic,
-// shard-invariant); each plane holds 2^17 terms per position before it could overflow.
-__device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, float y, float amp, double scale) {
+// One image's 8 channel values A T_d(y), d = 0..7, added to G[.][p] as integers v = round(A T_d 2^s).  The
+// per-RIR scale bounds |A| by the direct path, so |v| <= 2^bits.  When the host's bound on the images per
+// sample position (2 x 4 pi d_max^2 (c / fs) / V + 16, from the lattice's one image per room volume) lets
+// 2^bits x that count fit an int32 with bits >= 22, one plain shared-memory reduction per channel suffices
+// (single word); otherwise bits = 28 and v = a 2^14 + b, b in [0, 2^14), goes to two int32 planes (2^17
+// terms per position before either could overflow).  Integer adds commute, so G does not depend on the order
+// in which images arrive (deterministic, shard-invariant).
+__device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, float y, float amp, double scale,
+                                         bool two_word) {
   const double yd = (double)y, y2 = 2.0 * yd, ad = (double)amp * scale;
   const double magic = 6755399441055744.0;  // 1.5 2^52: the low 32 bits of (v + magic) hold round(v)
   double T[kPolyD];
@@ -91,8 +95,12 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, floa
   for (int d = 0; d < kPolyD; d++) {
     const int v = __double2loint(fma(ad, T[d], magic));
     const int i = d * npos + p;  // channel-major planes: consecutive positions are consecutive words
-    atomicAdd(&Ga[i], v >> 14);
-    atomicAdd(&Gb[i], v & 0x3FFF);
+    if (two_word) {
+      atomicAdd(&Ga[i], v >> 14);
+      atomicAdd(&Gb[i], v & 0x3FFF);
+    } else {
+      atomicAdd(&Ga[i], v);
+    }
   }
 }
 
@@ -116,13 +124,14 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
       PolyTile& T = sm.ti;
       T.next = wi < n_work;
       if (wi < n_work) {
-        int m, tile, nISM;
+        int m, tile, nISM, bits = A.poly_bits;
         long long row;
         const float zero3[3] = {0.f, 0.f, 0.f};
         if (A.jobs) {
           const int2 jt = A.tiles[wi];
           const BatchJob& J = A.jobs[jt.x];
           m = jt.x; tile = jt.y; nISM = J.nISM; row = J.out_offset;
+          bits = J.poly_bits;
           geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.ors, J.spkr_pattern, J.lb, J.neg, J.zero, T.g,
                     A.status);
         } else {
@@ -161,12 +170,14 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
         T.zh = T.g.nhi[2] - 1;
         T.use_bz = (T.zh - T.zl + 1) <= kPolyBz;
         // fixed-point scale: |A_n| <= 1 / (4 pi d_dp) (|beta|, |g| <= 1; the direct image is the closest) and
-        // |T_d| <= 1, so every channel value is at most 2^28 in units of 2^-s
+        // |T_d| <= 1, so every channel value is at most 2^bits in units of 2^-s (see poly_add)
         const double ddx = T.g.s[0] - T.g.r[0], ddy = T.g.s[1] - T.g.r[1], ddz = T.g.s[2] - T.g.r[2];
         const double abound = 0.0795774715459476679 / fmax(sqrt(ddx * ddx + ddy * ddy + ddz * ddz), 1e-30);
         const int e = (int)ceil(log2(abound));
-        T.scale = ldexp(1.0, 28 - e);
-        T.inv_scale = ldexp(1.0, e - 28);
+        T.two_word = bits <= 0;
+        if (bits <= 0) bits = 28;
+        T.scale = ldexp(1.0, bits - e);
+        T.inv_scale = ldexp(1.0, e - bits);
       }
     }
     __syncthreads();
@@ -233,7 +244,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
         const double Lz = g.L[2], offE = T.offE, offO = T.offO;
         const float Lzf = (float)Lz, offEf = (float)offE, offOf = (float)offO;
         const int tc = T.tc, zl = T.zl;
-        const bool use_bz = T.use_bz, dir_src = g.as != 1.f;
+        const bool use_bz = T.use_bz, dir_src = g.as != 1.f, two_word = T.two_word;
         const float oz = g.o[2], ga = g.a, fsc = (float)fs_over_c;
         for (int gi = g0; gi < g1; gi++) {
           while (gi >= boundary) { before = boundary; j++; boundary = sm.colpre[j]; }
@@ -258,7 +269,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
           if (dir_src) gain *= src_gain(cr.sdot, odd, dzf, fsc * rx, g);
           const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
           const float y = fmaf(2.f, xr - fj, -1.f);        // 2 phi - 1 in [-1, 1)
-          poly_add(Ga, Gb, npos, p, y, amp, T.scale);
+          poly_add(Ga, Gb, npos, p, y, amp, T.scale, two_word);
         }
       }
       __syncthreads();  // column records are replaced by the next batch
@@ -274,8 +285,8 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
 #pragma unroll
       for (int q = 0; q < kPolyD / 2; q++) {
         const int i0 = (2 * q) * npos + p, i1 = (2 * q + 1) * npos + p;
-        const long long v0 = (long long)Ga[i0] * 16384 + Gb[i0];
-        const long long v1 = (long long)Ga[i1] * 16384 + Gb[i1];
+        const long long v0 = T.two_word ? (long long)Ga[i0] * 16384 + Gb[i0] : (long long)Ga[i0];
+        const long long v1 = T.two_word ? (long long)Ga[i1] * 16384 + Gb[i1] : (long long)Ga[i1];
         tmp[nmine * (kPolyD / 2) + q] =
             make_float2((float)((double)v0 * T.inv_scale), (float)((double)v1 * T.inv_scale));
       }
