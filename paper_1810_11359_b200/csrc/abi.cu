@@ -183,10 +183,11 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
   P.Tw = Tw; P.fs = fs;
   P.mlo = (int)floor(-H) + 1;
   const int mhi = (H == floor(H)) ? (int)H : (int)floor(H) + 1;
-  P.ntaps = mhi - P.mlo + 1;
-  if (P.ntaps < 1 || P.ntaps > kPolyMaxTaps) { *err = GPURIR_EINVAL; return nullptr; }
-  std::vector<float> tab((size_t)P.ntaps * kPolyDeg);
-  for (int mi = 0; mi < P.ntaps; mi++) {
+  const int ntaps = mhi - P.mlo + 1;
+  P.ntaps = (ntaps + 3) & ~3;  // zero taps appended: the kernel's FIR runs in groups of 4 taps
+  if (ntaps < 1 || P.ntaps > kPolyMaxTaps) { *err = GPURIR_EINVAL; return nullptr; }
+  std::vector<float> tab((size_t)P.ntaps * kPolyDeg, 0.f);
+  for (int mi = 0; mi < ntaps; mi++) {
     const int m = P.mlo + mi;
     double c[kPolyDeg] = {0};
     for (int i = 0; i < kPolyNodes; i++) {

@@ -302,28 +302,38 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
     // ---- 3. 8-channel FIR: h[k] = sum_m sum_d P_d[m] G_d[k - m] --------------------------------
     // Thread group gq (128 threads) applies channel pair gq to 4 consecutive outputs per thread with a
     // sliding register window (one new position per tap); the 4 groups' partial sums meet in shared memory.
+    // ntaps is padded to a multiple of 4 with zero taps, so in every unrolled group of 4 taps the new
+    // positions q - mi - 1 - u sit at fixed offsets 0, -1, -2, -4 of one padded address (q = 3 mod 4).
     {
       const int gq = tid >> 7, lt = tid & 127, t4 = 4 * lt;
-      const float2* G = Gf + gq * plane;
       const float2* P2 = reinterpret_cast<const float2*>(Pt) + gq;  // (P_2gq, P_2gq+1)[mi] at P2[4 mi]
       float2 acc[4], w[4];
-      int q = t4 + ntaps - 1;  // position of output t4 at tap mi = 0 (m = m_lo)
+      const int q = t4 + ntaps - 1;  // position of output t4 at tap mi = 0 (m = m_lo)
+      const float2* G = Gf + gq * plane;
 #pragma unroll
       for (int r = 0; r < 4; r++) {
         acc[r] = make_float2(0.f, 0.f);
         w[r] = G[(q + r) + ((q + r) >> 2)];
       }
-      for (int mi = 0; mi < ntaps; mi += 4) {  // unrolled by 4 so the window shift is register renaming
+      const float2* gn = G + (q - 1) + ((q - 1) >> 2);  // padded address of position q - 1 (= 2 mod 4)
+      for (int mi = 0; mi < ntaps; mi += 4, gn -= 5, P2 += 16) {
+        // tap mi + u uses window slot (r - u) & 3 for output r and refills slot (3 - u) & 3
+        float2 pc = P2[0];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          if (mi + u < ntaps) {
-            const float2 pc = P2[4 * (mi + u)];
+        for (int r = 0; r < 4; r++) acc[r] = __ffma2_rn(pc, w[r & 3], acc[r]);
+        w[3] = gn[0];
+        pc = P2[4];
 #pragma unroll
-            for (int r = 0; r < 4; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 3], acc[r]);
-            const int qn = q - (mi + u) - 1;  // next tap's new (lowest) position
-            if (mi + u + 1 < ntaps) w[(3 - u) & 3] = G[qn + (qn >> 2)];
-          }
-        }
+        for (int r = 0; r < 4; r++) acc[r] = __ffma2_rn(pc, w[(r + 3) & 3], acc[r]);
+        w[2] = gn[-1];
+        pc = P2[8];
+#pragma unroll
+        for (int r = 0; r < 4; r++) acc[r] = __ffma2_rn(pc, w[(r + 2) & 3], acc[r]);
+        w[1] = gn[-2];
+        pc = P2[12];
+#pragma unroll
+        for (int r = 0; r < 4; r++) acc[r] = __ffma2_rn(pc, w[(r + 1) & 3], acc[r]);
+        w[0] = gn[-4];  // the last group's refills read padding before the plane: never used
       }
       float* red = reinterpret_cast<float*>(sm.col);  // 4 x 512 partial sums (the column records are dead here)
       reinterpret_cast<float4*>(red + gq * kPolyTC)[lt] =
