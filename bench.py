@@ -4,10 +4,11 @@
 Workload (BASELINE.json config 3, the paper's #RIR sweep room): 3x4x2.5 m, T60 = 0.7 s
 (beta = -0.9397, Sabine), source (1.5, 1.0, 1.2), M = 16384 cardioid receivers per GPU uniform in the
 room (seed 3) with random orientations, fs = 16 kHz, ISM to Tdiff = 0.175 s + diffuse tail to 0.7 s,
-fp32 mode.  One step = one gpurir_simulate_rir call over the rank's 16384 receivers (ISM kernel + tail
-kernel).  Weak scaling: rank r owns receivers [16384 r, 16384 (r+1)) of the N*16384-receiver workload.
+polyphase mode by default (fp32 arithmetic and tolerance, reading R11; --mode fp32 selects the
+direct-tap kernel, which the line also reports as `direct_fp32`).  One step = one gpurir_simulate_rir call
+over the rank's 16384 receivers (ISM kernel + tail kernel).  Weak scaling: rank r owns receivers [16384 r, 16384 (r+1)) of the N*16384-receiver workload.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--mode fp32|lut|fp16]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--mode poly|fp32|lut|fp16|lut_tex]
                   [--workload ism|trajectory]
 
 --impl reference times the CPU oracle (oracle/, test infrastructure) on the host cores: the paper's
@@ -37,7 +38,11 @@ import workloads as W  # noqa: E402
 M_PER_GPU = 16384
 METRIC = "RIRs/s and image contributions/s vs T60 and #RIRs at 1/2/4/8 B200"
 TRAJ_METRIC = "moving-source trajectories/s (RIR synthesis + trajectory filtering, NEXT row f1)"
-ISSUE_SLOTS_PER_TAP = 13  # algorithmic FP32-pipe issue slots per in-window tap
+ISSUE_SLOTS_PER_TAP = 13  # algorithmic FP32-pipe issue slots per in-window tap (direct kernels)
+# Polyphase kernel (mode poly, reading R11 / §5.5): algorithmic lane-ops per in-range image (Eqs. 1-4:
+# 13, the 8 Chebyshev channel values: 14, their 8 deposits) and per output sample (the FIR: 2H taps x 8 MACs)
+POLY_OPS_PER_IMAGE = 35
+POLY_CHANNELS = 8
 
 
 def workload_name(mode="fp32"):
@@ -54,8 +59,9 @@ def peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def count_taps(room, src, rcv, nb, nISM, fs, c, H):
-    """Algorithmic work: in-window (image, sample) pairs for samples [0, nISM) (Eqs. 5-6 support)."""
+def count_taps(room, src, rcv, nb, nISM, fs, c, H, images=False):
+    """Algorithmic work: in-window (image, sample) pairs for samples [0, nISM) (Eqs. 5-6 support); with
+    images=True also the number of images with at least one such tap."""
     lo = [-(int(n) // 2) for n in nb]
     hi = [(int(n) + 1) // 2 for n in nb]
     ax = []
@@ -67,7 +73,8 @@ def count_taps(room, src, rcv, nb, nISM, fs, c, H):
     x = np.sqrt(d2).ravel() * fs / c
     k0 = np.maximum(np.floor(x - H) + 1, 0)
     k1 = np.minimum(np.ceil(x + H) - 1, nISM - 1)
-    return float(np.maximum(k1 - k0 + 1, 0).sum())
+    n = np.maximum(k1 - k0 + 1, 0)
+    return (float(n.sum()), float((n > 0).sum())) if images else float(n.sum())
 
 
 class RawEvent:
@@ -279,7 +286,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--mode", default="fp32", choices=["fp32", "lut", "fp16", "lut_tex", "poly"])
+    ap.add_argument("--mode", default="poly", choices=["fp32", "lut", "fp16", "lut_tex", "poly"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -427,15 +434,31 @@ def main():
     sample = np.linspace(0, M_PER_GPU - 1, 256).astype(int)
     H = 4e-3 * sc.fs / 2
     r64 = sc.pos_rcv[sl].astype(np.float64)
-    taps_sample = [count_taps(sc.room.astype(np.float64), sc.pos_src[0].astype(np.float64), r64[m], nb, nISM,
-                              sc.fs, sc.c, H) for m in sample]
-    taps_per_rir = float(np.mean(taps_sample))
+    ti_sample = [count_taps(sc.room.astype(np.float64), sc.pos_src[0].astype(np.float64), r64[m], nb, nISM,
+                            sc.fs, sc.c, H, images=True) for m in sample]
+    taps_per_rir = float(np.mean([t for t, _ in ti_sample]))
+    imgs_per_rir = float(np.mean([i for _, i in ti_sample]))
     taps_launch = taps_per_rir * M_PER_GPU
+    imgs_launch = imgs_per_rir * M_PER_GPU
     ism_avg_s = float(np.mean(ism_ms)) / 1000.0
     pk, pk_kind = peaks()
     f_clk = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
     issue_peak = 148 * 128 * f_clk  # FP32 lane issue slots / s (B200_PROFILING.md unit counts)
-    achieved = taps_launch * ISSUE_SLOTS_PER_TAP / ism_avg_s
+    ntaps_fir = int(round(2 * H))
+    poly_ops = imgs_launch * POLY_OPS_PER_IMAGE + M_PER_GPU * nISM * ntaps_fir * POLY_CHANNELS
+    if args.mode == "poly":
+        achieved = poly_ops / ism_avg_s
+        basis = (f"{POLY_OPS_PER_IMAGE} lane-ops per in-range image x {imgs_launch:.4g} images + {ntaps_fir} taps x "
+                 f"{POLY_CHANNELS} channels per output sample x {M_PER_GPU * nISM} samples per launch (exact image "
+                 f"count on 256 sampled receivers); peak = 148 SM x 128 lanes x {f_clk / 1e6:.0f} MHz "
+                 f"({pk_kind} sm_max_mhz)")
+        kname = "ism_poly_kernel"
+    else:
+        achieved = taps_launch * ISSUE_SLOTS_PER_TAP / ism_avg_s
+        basis = (f"{ISSUE_SLOTS_PER_TAP} issue slots per in-window tap (SURVEY §8(d)) x {taps_launch:.4g} taps per "
+                 f"launch (exact count on 256 sampled receivers x {M_PER_GPU}); peak = 148 SM x 128 lanes x "
+                 f"{f_clk / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)")
+        kname = "ism_ws_kernel<0>" if args.mode == "fp32" else f"ism_ws_kernel ({args.mode})"
     lattice = float(np.prod(nb.astype(np.float64)))
     traffic = None
     try:
@@ -462,10 +485,7 @@ def main():
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": issue_peak / 1e12,
                      "unit": "T FP32-lane-issue-slots/s", "frac": achieved / issue_peak, "traffic": traffic,
                      "traffic_note": "DRAM bytes per launch from profiles/r01_ism_traffic.json (ncu --set full)",
-                     "kernel": "ism_ws_kernel<0>" if args.mode == "fp32" else f"ism_ws_kernel ({args.mode})",
-                     "basis": f"{ISSUE_SLOTS_PER_TAP} issue slots per in-window tap (SURVEY §8(d)) x {taps_launch:.4g} "
-                              f"taps per launch (exact count on 256 sampled receivers x {M_PER_GPU}); peak = 148 SM x "
-                              f"128 lanes x {f_clk / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)"},
+                     "kernel": kname, "basis": basis},
         "tail_kernel": {"ms": float(np.mean(tail_ms)), "bytes": tail_bytes, "GB_per_s": tail_bytes / tail_avg_s / 1e9,
                         "frac_of_hbm": tail_bytes / tail_avg_s / 1e9 / hbm_peak, "bound": "hbm (write)",
                         "peak_GB_per_s": hbm_peak},
@@ -476,11 +496,36 @@ def main():
         "paper_context": "gpuRIR V100 fp32, 1024 RIRs, T60 0.7 s diffuse: 195.69 ms = 5,233 RIRs/s (P:362); "
                          "different fs/positions/pattern, context only",
     }
+    if args.mode == "poly":  # the direct-tap fp32 kernel on the same step, for the A/B (not part of `value`)
+        line["direct_fp32"] = direct_ab(P, torch, sc, beta, nb, src, rcv, orv, base, out, flush, stream,
+                                        taps_launch, issue_peak)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(W.cfg3(M_PER_GPU, "diffuse"))
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def direct_ab(P, torch, sc, beta, nb, src, rcv, orv, base, out, flush, stream, taps_launch, issue_peak, steps=5):
+    """The same step through the direct-tap fp32 kernel (ism_ws_kernel<0>): RIRs/s and its own roofline."""
+    ts, ism = [], []
+    for i in range(steps + 2):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = RawEvent(), RawEvent()
+        a.record(stream)
+        P.simulate_rir(sc.room, beta, src, rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=orv,
+                       mic_pattern=sc.pattern, mode="fp32", seed=sc.seed, rir_index_base=base, out=out,
+                       stream=stream, ev_ism=(e0, e1))
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i >= 2:
+            ts.append(a.elapsed_time(b))
+            ism.append(e0.elapsed_ms(e1))
+    ms, ism_ms = float(np.mean(ts)), float(np.mean(ism))
+    ach = taps_launch * ISSUE_SLOTS_PER_TAP / (ism_ms / 1000.0)
+    return {"value": M_PER_GPU / (ms / 1000.0), "unit": "RIRs/s", "ms_per_step": ms, "ism_ms": ism_ms,
+            "roofline_frac": ach / issue_peak, "kernel": "ism_ws_kernel<0>", "steps": steps}
 
 
 def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev):
@@ -587,18 +632,27 @@ def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev):
     issue_peak = 148 * 128 * f_clk
     H = 4e-3 * sc.fs / 2
     pairs = [(p, m) for p in range(0, n_pts, 7) for m in range(0, n_mic, 5)]
-    taps = float(np.mean([count_taps(sc.room.astype(np.float64), sc.pos_src[p].astype(np.float64),
-                                     sc.pos_rcv[m].astype(np.float64), nb, nISM, sc.fs, sc.c, H) for p, m in pairs]))
+    ti = [count_taps(sc.room.astype(np.float64), sc.pos_src[p].astype(np.float64), sc.pos_rcv[m].astype(np.float64),
+                     nb, nISM, sc.fs, sc.c, H, images=True) for p, m in pairs]
+    taps = float(np.mean([t for t, _ in ti]))
     taps_launch = taps * n_pts * n_mic
-    ism_ach = taps_launch * ISSUE_SLOTS_PER_TAP / (ism_ms / 1000.0)
+    if args.mode == "poly":
+        ism_work = (float(np.mean([i for _, i in ti])) * POLY_OPS_PER_IMAGE + nISM * round(2 * H) * POLY_CHANNELS) \
+            * n_pts * n_mic
+    else:
+        ism_work = taps_launch * ISSUE_SLOTS_PER_TAP
+    ism_ach = ism_work / (ism_ms / 1000.0)
     macs = float(n_sig) * nS * n_mic
     tr_ach = macs / (tr_ms / 1000.0)
-    kern = {"ism_ws_kernel": ism_ms, "traj_kernel": tr_ms, "tail_kernel": tail_ms}
+    kern = {"ism_kernel": ism_ms, "traj_kernel": tr_ms, "tail_kernel": tail_ms}
     dominant = max(kern, key=kern.get)
     roof_ism = {"bound": "alu", "achieved": ism_ach / 1e12, "peak": issue_peak / 1e12,
                 "unit": "T FP32-lane-issue-slots/s", "frac": ism_ach / issue_peak, "traffic": None,
-                "kernel": "ism_ws_kernel<0>", "basis": f"{ISSUE_SLOTS_PER_TAP} issue slots per in-window tap x "
-                f"{taps_launch:.4g} taps per launch (exact count on {len(pairs)} sampled pairs)"}
+                "kernel": "ism_poly_kernel" if args.mode == "poly" else "ism_ws_kernel<0>",
+                "basis": (f"{POLY_OPS_PER_IMAGE} lane-ops per in-range image + {round(2 * H)} taps x {POLY_CHANNELS} "
+                          f"channels per output sample" if args.mode == "poly" else
+                          f"{ISSUE_SLOTS_PER_TAP} issue slots per in-window tap x {taps_launch:.4g} taps per launch")
+                + f" (exact counts on {len(pairs)} sampled pairs)"}
     roof_tr = {"bound": "alu", "achieved": tr_ach / 1e12, "peak": issue_peak / 1e12, "unit": "T FFMA/s",
                "frac": tr_ach / issue_peak, "traffic": None, "kernel": "traj_kernel",
                "basis": f"n_sig x L x n_mics = {macs:.4g} MACs per launch (one FFMA each); peak = 148 SM x 128 "
@@ -611,7 +665,7 @@ def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev):
                    "room": [3, 4, 2.5], "T60": sc.T60, "fs": sc.fs, "nb_img": [int(v) for v in nb], "mode": args.mode,
                    "l2": "256 MB buffer written between timed steps (L2 126 MB)"},
         "kernel_ms": kern,
-        "roofline": roof_ism if dominant == "ism_ws_kernel" else roof_tr,
+        "roofline": roof_ism if dominant.startswith("ism") else roof_tr,
         "traj_kernel": roof_tr,
         "ism_kernel": roof_ism,
         "e2e": {"value": e2e_value, "unit": "trajectories/s", "h2d_bytes_per_step": (h_src.numel() + h_rcv.numel() +

@@ -476,3 +476,49 @@ def test_batch_directional_weighted_rooms(P, oracle):
         g = o[off:off + r.size]
         off += r.size
         assert rel_err(g, r)[0] <= TOL["fp32"], i
+
+
+# ---------------------------------------------------------------- polyphase mode (reading R11)
+
+def test_poly_deterministic_and_shard_invariant(P, oracle):
+    """Integer fixed-point aggregation: bitwise identical run to run and across receiver shards."""
+    sc = W.cfg3(64, "diffuse")
+    beta, nb = derive(oracle, sc)
+    a = run_gpu(P, sc, beta, nb, mode="poly")
+    b = run_gpu(P, sc, beta, nb, mode="poly")
+    assert np.array_equal(a, b)
+    parts = [run_gpu(P, sc, beta, nb, mode="poly", rir_index_base=16 * s, pos_rcv=sc.pos_rcv[16 * s:16 * (s + 1)],
+                     orv=sc.orV_rcv[16 * s:16 * (s + 1)]) for s in range(4)]
+    assert np.array_equal(a, np.concatenate(parts, axis=1))
+
+
+def test_poly_two_word_long_rir(P, oracle):
+    """Full ISM to 0.7 s (config 3 (ii)): the lattice-density bound exceeds the single-word range, so the
+    two-word accumulation runs; parity at the fp32 tolerance on 2 receivers."""
+    sc = W.cfg3(2, "full")
+    beta, nb = derive(oracle, sc)
+    g = run_gpu(P, sc, beta, nb, mode="poly")
+    r = run_oracle(oracle, sc, beta, nb)
+    assert rel_err(g, r).max() <= TOL["poly"]
+
+
+@pytest.mark.parametrize("fs", [8000.0, 22050.0, 44100.0, 96000.0])
+def test_poly_sampling_rates(P, oracle, fs):
+    """Integer and fractional half-windows H = Tw fs / 2 (16, 44.1, 88.2, 192 taps-half), zero-padded tap
+    groups; random scenes against the oracle."""
+    rng = np.random.default_rng(int(fs))
+    for i in range(3):
+        sc = W.random_small_scene(rng, fs=fs, T=0.03)
+        beta, nb = derive(oracle, sc)
+        g = run_gpu(P, sc, beta, nb, mode="poly")
+        r = run_oracle(oracle, sc, beta, nb)
+        assert rel_err(g, r).max() <= TOL["poly"], (fs, i)
+
+
+def test_poly_matches_direct_kernel(P, oracle):
+    """The two fp32 implementations of Eq. 5-6 (direct taps, polyphase) agree far inside the tolerance."""
+    sc = W.cfg3(32, "diffuse")
+    beta, nb = derive(oracle, sc)
+    a = run_gpu(P, sc, beta, nb, mode="fp32")
+    b = run_gpu(P, sc, beta, nb, mode="poly")
+    assert rel_err(b, a).max() <= 5e-5
