@@ -184,7 +184,7 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
   P.mlo = (int)floor(-H) + 1;
   const int mhi = (H == floor(H)) ? (int)H : (int)floor(H) + 1;
   const int ntaps = mhi - P.mlo + 1;
-  P.ntaps = (ntaps + 3) & ~3;  // zero taps appended: the kernel's FIR runs in groups of 4 taps
+  P.ntaps = (ntaps + 7) & ~7;  // zero taps appended: the kernel's FIR runs in groups of 8 taps
   if (ntaps < 1 || P.ntaps > kPolyMaxTaps) { *err = GPURIR_EINVAL; return nullptr; }
   std::vector<float> tab((size_t)P.ntaps * kPolyDeg, 0.f);
   for (int mi = 0; mi < ntaps; mi++) {
@@ -209,14 +209,13 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
 
 // Polyphase fixed-point width (ism_poly_kernel.cu, poly_add): a shoebox lattice holds one image per room
 // volume V, so about 4 pi d^2 (c / fs) / V images share one integer sample position at distance d.  With twice
-// that at the farthest ISM delay (+16) as the bound N, single-word accumulation with 2^bits N <= 2^30 is used
-// when it leaves bits >= 22 (N <= 256); otherwise 0 selects the two-word scheme (2^28 resolution).
+// that at the farthest ISM delay (+16) as the bound N, single-word accumulation with bits = 22 is used when
+// 2^22 N <= 2^30 (N <= 256); otherwise 0 selects the two-word scheme (2^28 resolution).
 int poly_bits_for(const float L[3], long long nISM, double fs, double c, double Tw) {
   const double V = (double)L[0] * L[1] * L[2];
   const double dmax = ((double)nISM + Tw * fs / 2.0 + 1.0) * c / fs;
   const double N = 2.0 * 4.0 * M_PI * dmax * dmax * (c / fs) / V + 16.0;
-  if (!(N <= 256.0)) return 0;
-  return 30 - (int)ceil(log2(N));
+  return N <= 256.0 ? 22 : 0;  // 2^22 x 256 = 2^30; the kernel's fp32 rounding is exact up to 2^22
 }
 
 // Mode tables of one call (LUT: phase-major smem table; texture LUT: filtered texture; polyphase table).
@@ -493,7 +492,7 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     A.row_stride = nS;
     const bool poly = o.mode == GPURIR_POLY;
     const bool persistent = poly || use_persistent(((nISM + kTC - 1) / kTC) * M, o.split, d);
-    const int tile_len = persistent ? kTCPersistent : kTC;
+    const int tile_len = poly ? kPolyTile : persistent ? kTCPersistent : kTC;
     A.nTiles = (int)((nISM + tile_len - 1) / tile_len);
     fill_common(A, fs, c, o.Tw);
     A.out = out;
@@ -594,7 +593,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     for (int ch = 0; ch < nch; ch++) chunks.push_back(make_int2(i, ch));
   }
   const bool persistent = o.mode == GPURIR_POLY || use_persistent(small_tiles, o.split, d);
-  const int tile_len = persistent ? kTCPersistent : kTC;
+  const int tile_len = o.mode == GPURIR_POLY ? kPolyTile : persistent ? kTCPersistent : kTC;
   // heavy-first schedule without a comparison sort: image density grows ~ t^2 (SURVEY §7 hard part 2), so
   // emit all rooms' last tiles first, then the second-to-last, ... (a counting order over tile index)
   int max_tiles = 0;

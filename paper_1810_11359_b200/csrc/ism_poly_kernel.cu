@@ -20,11 +20,11 @@
 namespace gpurir {
 
 constexpr int kPolyThreads = 512;
-constexpr int kPolyTC = kTCPersistent;  // 512 output samples per work item (the host planner's tile)
+constexpr int kPolyTC = kPolyTile;      // 1024 output samples per work item (the host planner's tile)
 constexpr int kPolyD = 8;               // Chebyshev channels T_0..T_7
 constexpr int kPolyCols = kPolyThreads; // lattice columns per enumeration batch
 constexpr int kPolyBz = 1024;           // z-factor table entries
-static_assert(kPolyTC == kPolyThreads, "one output sample per thread in the filter phase");
+static_assert(kPolyTC == 2 * kPolyThreads, "two output samples per thread in the filter's final sum");
 
 struct PolyColRec {  // 32 B, as WsColRec
   double rho2;
@@ -78,12 +78,28 @@ __device__ __forceinline__ float poly_z_factor(int nz, const RirGeom& g) {
 // One image's 8 channel values A T_d(y), d = 0..7, added to G[.][p] as integers v = round(A T_d 2^s).  The
 // per-RIR scale bounds |A| by the direct path, so |v| <= 2^bits.  When the host's bound on the images per
 // sample position (2 x 4 pi d_max^2 (c / fs) / V + 16, from the lattice's one image per room volume) lets
-// 2^bits x that count fit an int32 with bits >= 22, one plain shared-memory reduction per channel suffices
-// (single word); otherwise bits = 28 and v = a 2^14 + b, b in [0, 2^14), goes to two int32 planes (2^17
+// 2^bits x that count fit an int32 with bits = 22, one plain shared-memory reduction per channel suffices
+// (single word, fp32 arithmetic); otherwise bits = 28 and v = a 2^14 + b, b in [0, 2^14), goes to two int32 planes (2^17
 // terms per position before either could overflow).  Integer adds commute, so G does not depend on the order
 // in which images arrive (deterministic, shard-invariant).
 __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, float y, float amp, double scale,
                                          bool two_word) {
+  if (!two_word) {
+    // single word, bits <= 22: fp32 suffices — T_d by the recurrence in fp32 (|error| ~ 1e-7 d), and
+    // round(A T_d 2^s) from the low mantissa bits of A 2^s T_d + 1.5 2^23 (exact for |v| < 2^22)
+    const float as = (float)((double)amp * scale), y2 = 2.f * y, magic = 12582912.f;
+    float tm2 = 1.f, tm1 = y;
+    atomicAdd(&Ga[p], __float_as_int(fmaf(as, 1.f, magic)) - 0x4B400000);
+    atomicAdd(&Ga[npos + p], __float_as_int(fmaf(as, y, magic)) - 0x4B400000);
+#pragma unroll
+    for (int d = 2; d < kPolyD; d++) {
+      const float t = fmaf(y2, tm1, -tm2);  // T_d = 2 y T_{d-1} - T_{d-2}
+      atomicAdd(&Ga[d * npos + p], __float_as_int(fmaf(as, t, magic)) - 0x4B400000);
+      tm2 = tm1;
+      tm1 = t;
+    }
+    return;
+  }
   const double yd = (double)y, y2 = 2.0 * yd, ad = (double)amp * scale;
   const double magic = 6755399441055744.0;  // 1.5 2^52: the low 32 bits of (v + magic) hold round(v)
   double T[kPolyD];
@@ -95,12 +111,8 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, floa
   for (int d = 0; d < kPolyD; d++) {
     const int v = __double2loint(fma(ad, T[d], magic));
     const int i = d * npos + p;  // channel-major planes: consecutive positions are consecutive words
-    if (two_word) {
-      atomicAdd(&Ga[i], v >> 14);
-      atomicAdd(&Gb[i], v & 0x3FFF);
-    } else {
-      atomicAdd(&Ga[i], v);
-    }
+    atomicAdd(&Ga[i], v >> 14);
+    atomicAdd(&Gb[i], v & 0x3FFF);
   }
 }
 
@@ -276,12 +288,12 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
     }
 
     // ---- 2. fixed point -> fp32 in 4 channel-pair planes, Gf[pair][pad(p)] = (G_2q, G_2q+1) ------------
-    // pad(p) = p + p/4: the filter's lanes read positions 4 apart, which the padding spreads over all banks
+    // pad(p) = p + p/8: the filter's lanes read positions 8 apart, which the padding spreads over all banks
     float2* Gf = reinterpret_cast<float2*>(Ga);  // in place over Ga / Gb (read everything, barrier, write)
-    const int plane = npos + (npos >> 2) + 1;
-    float2 tmp[(kPolyD / 2) * 2];
+    const int plane = npos + (npos >> 3) + 1;
+    float2 tmp[(kPolyD / 2) * 3];  // npos <= 1024 + 511: at most 3 positions per thread
     int nmine = 0;
-    for (int p = tid; p < npos && nmine < 2; p += kPolyThreads, nmine++) {
+    for (int p = tid; p < npos && nmine < 3; p += kPolyThreads, nmine++) {
 #pragma unroll
       for (int q = 0; q < kPolyD / 2; q++) {
         const int i0 = (2 * q) * npos + p, i1 = (2 * q + 1) * npos + p;
@@ -293,58 +305,52 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
     }
     __syncthreads();
     nmine = 0;
-    for (int p = tid; p < npos && nmine < 2; p += kPolyThreads, nmine++) {
+    for (int p = tid; p < npos && nmine < 3; p += kPolyThreads, nmine++) {
 #pragma unroll
-      for (int q = 0; q < kPolyD / 2; q++) Gf[q * plane + p + (p >> 2)] = tmp[nmine * (kPolyD / 2) + q];
+      for (int q = 0; q < kPolyD / 2; q++) Gf[q * plane + p + (p >> 3)] = tmp[nmine * (kPolyD / 2) + q];
     }
     __syncthreads();
 
     // ---- 3. 8-channel FIR: h[k] = sum_m sum_d P_d[m] G_d[k - m] --------------------------------
-    // Thread group gq (128 threads) applies channel pair gq to 4 consecutive outputs per thread with a
+    // Thread group gq (128 threads) applies channel pair gq to 8 consecutive outputs per thread with a
     // sliding register window (one new position per tap); the 4 groups' partial sums meet in shared memory.
-    // ntaps is padded to a multiple of 4 with zero taps, so in every unrolled group of 4 taps the new
-    // positions q - mi - 1 - u sit at fixed offsets 0, -1, -2, -4 of one padded address (q = 3 mod 4).
+    // ntaps is padded to a multiple of 8 with zero taps, so in every unrolled group of 8 taps the new
+    // positions q - mi - 1 - u sit at fixed offsets 0 .. -6, -8 of one padded address (q = 7 mod 8).
     {
-      const int gq = tid >> 7, lt = tid & 127, t4 = 4 * lt;
+      const int gq = tid >> 7, lt = tid & 127, t8 = 8 * lt;
       const float2* P2 = reinterpret_cast<const float2*>(Pt) + gq;  // (P_2gq, P_2gq+1)[mi] at P2[4 mi]
-      float2 acc[4], w[4];
-      const int q = t4 + ntaps - 1;  // position of output t4 at tap mi = 0 (m = m_lo)
+      float2 acc[8], w[8];
+      const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (m = m_lo)
       const float2* G = Gf + gq * plane;
 #pragma unroll
-      for (int r = 0; r < 4; r++) {
+      for (int r = 0; r < 8; r++) {
         acc[r] = make_float2(0.f, 0.f);
-        w[r] = G[(q + r) + ((q + r) >> 2)];
+        w[r] = G[(q + r) + ((q + r) >> 3)];
       }
-      const float2* gn = G + (q - 1) + ((q - 1) >> 2);  // padded address of position q - 1 (= 2 mod 4)
-      for (int mi = 0; mi < ntaps; mi += 4, gn -= 5, P2 += 16) {
-        // tap mi + u uses window slot (r - u) & 3 for output r and refills slot (3 - u) & 3
-        float2 pc = P2[0];
+      const float2* gn = G + (q - 1) + ((q - 1) >> 3);  // padded address of position q - 1 (= 6 mod 8)
+      for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P2 += 32) {
 #pragma unroll
-        for (int r = 0; r < 4; r++) acc[r] = __ffma2_rn(pc, w[r & 3], acc[r]);
-        w[3] = gn[0];
-        pc = P2[4];
+        for (int u = 0; u < 8; u++) {  // tap mi + u: output r uses slot (r - u) & 7, then slot (7 - u) & 7 refills
+          const float2 pc = P2[4 * u];
 #pragma unroll
-        for (int r = 0; r < 4; r++) acc[r] = __ffma2_rn(pc, w[(r + 3) & 3], acc[r]);
-        w[2] = gn[-1];
-        pc = P2[8];
-#pragma unroll
-        for (int r = 0; r < 4; r++) acc[r] = __ffma2_rn(pc, w[(r + 2) & 3], acc[r]);
-        w[1] = gn[-2];
-        pc = P2[12];
-#pragma unroll
-        for (int r = 0; r < 4; r++) acc[r] = __ffma2_rn(pc, w[(r + 1) & 3], acc[r]);
-        w[0] = gn[-4];  // the last group's refills read padding before the plane: never used
+          for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 7], acc[r]);
+          w[(7 - u) & 7] = gn[u < 7 ? -u : -8];  // the last group's refills read padding: never used
+        }
       }
-      float* red = reinterpret_cast<float*>(sm.col);  // 4 x 512 partial sums (the column records are dead here)
-      reinterpret_cast<float4*>(red + gq * kPolyTC)[lt] =
-          make_float4(acc[0].x + acc[0].y, acc[1].x + acc[1].y, acc[2].x + acc[2].y, acc[3].x + acc[3].y);
+      float* red = reinterpret_cast<float*>(sm.col);  // 4 x 1024 partial sums (the column records are dead here)
+      float4* r4 = reinterpret_cast<float4*>(red + gq * kPolyTC + t8);
+      r4[0] = make_float4(acc[0].x + acc[0].y, acc[1].x + acc[1].y, acc[2].x + acc[2].y, acc[3].x + acc[3].y);
+      r4[1] = make_float4(acc[4].x + acc[4].y, acc[5].x + acc[5].y, acc[6].x + acc[6].y, acc[7].x + acc[7].y);
     }
     __syncthreads();
     {
       const float* red = reinterpret_cast<const float*>(sm.col);
-      const int k = T.t0 + tid;
-      if (k < T.te)
-        A.out[T.row + k] = (red[tid] + red[kPolyTC + tid]) + (red[2 * kPolyTC + tid] + red[3 * kPolyTC + tid]);
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int t = tid + h * kPolyThreads, k = T.t0 + t;
+        if (k < T.te)
+          A.out[T.row + k] = (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
+      }
     }
     __syncthreads();  // G and the tile record are reused by the next work item
   }
