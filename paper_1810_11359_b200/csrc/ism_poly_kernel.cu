@@ -37,7 +37,8 @@ static_assert(sizeof(PolyColRec) * kPolyCols >= 4 * kPolyTC * sizeof(float), "FI
 
 struct PolyTile {
   RirGeom g;
-  double dlo2, dhi2, invLz, offE, offO, scale, inv_scale;
+  double dlo2, dhi2, invLz, offE, offO, inv_scale;
+  float scalef;  // 2^(bits - e): a power of two, exact in fp32
   int two_word;
   long long row;
   int t0, te, tc, nx0, ny0, NX, ncols, zl, zh, use_bz, next;
@@ -82,12 +83,12 @@ __device__ __forceinline__ float poly_z_factor(int nz, const RirGeom& g) {
 // (single word, fp32 arithmetic); otherwise bits = 28 and v = a 2^14 + b, b in [0, 2^14), goes to two int32 planes (2^17
 // terms per position before either could overflow).  Integer adds commute, so G does not depend on the order
 // in which images arrive (deterministic, shard-invariant).
-__device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, float y, float amp, double scale,
+__device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, float y, float amp, float scale,
                                          bool two_word) {
   if (!two_word) {
     // single word, bits <= 22: fp32 suffices — T_d by the recurrence in fp32 (|error| ~ 1e-7 d), and
     // round(A T_d 2^s) from the low mantissa bits of A 2^s T_d + 1.5 2^23 (exact for |v| < 2^22)
-    const float as = (float)((double)amp * scale), y2 = 2.f * y, magic = 12582912.f;
+    const float as = amp * scale, y2 = 2.f * y, magic = 12582912.f;  // power-of-two scale: exact
     float tm2 = 1.f, tm1 = y;
     atomicAdd(&Ga[p], __float_as_int(fmaf(as, 1.f, magic)) - 0x4B400000);
     atomicAdd(&Ga[npos + p], __float_as_int(fmaf(as, y, magic)) - 0x4B400000);
@@ -100,7 +101,7 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, floa
     }
     return;
   }
-  const double yd = (double)y, y2 = 2.0 * yd, ad = (double)amp * scale;
+  const double yd = (double)y, y2 = 2.0 * yd, ad = (double)amp * (double)scale;
   const double magic = 6755399441055744.0;  // 1.5 2^52: the low 32 bits of (v + magic) hold round(v)
   double T[kPolyD];
   T[0] = 1.0;
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
         const int e = (int)ceil(log2(abound));
         T.two_word = bits <= 0;
         if (bits <= 0) bits = 28;
-        T.scale = ldexp(1.0, bits - e);
+        T.scalef = ldexpf(1.f, bits - e);
         T.inv_scale = ldexp(1.0, e - bits);
       }
     }
@@ -252,13 +253,13 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
         }
         int j = lo;
         int before = j > 0 ? sm.colpre[j - 1] : 0;
-        int boundary = sm.colpre[j];
         const double Lz = g.L[2], offE = T.offE, offO = T.offO;
         const float Lzf = (float)Lz, offEf = (float)offE, offOf = (float)offO;
         const int tc = T.tc, zl = T.zl;
         const bool use_bz = T.use_bz, dir_src = g.as != 1.f, two_word = T.two_word;
-        const float oz = g.o[2], ga = g.a, fsc = (float)fs_over_c;
-        for (int gi = g0; gi < g1; gi++) {
+        const float oz = g.o[2], ga = g.a, fsc = (float)fs_over_c, scalef = T.scalef;
+        int boundary = sm.colpre[j];
+        for (int gi = g0; gi < g1; gi++) {  // every lane runs R candidates: the walk keeps the warp converged
           while (gi >= boundary) { before = boundary; j++; boundary = sm.colpre[j]; }
           const PolyColRec& cr = sm.col[j];
           const int l = gi - before;
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
           if (dir_src) gain *= src_gain(cr.sdot, odd, dzf, fsc * rx, g);
           const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
           const float y = fmaf(2.f, xr - fj, -1.f);        // 2 phi - 1 in [-1, 1)
-          poly_add(Ga, Gb, npos, p, y, amp, T.scale, two_word);
+          poly_add(Ga, Gb, npos, p, y, amp, scalef, two_word);
         }
       }
       __syncthreads();  // column records are replaced by the next batch
