@@ -132,7 +132,9 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
   for (int i = tid; i < ntaps * kPolyD; i += kPolyThreads) Pt[i] = A.poly_P[i];
 
   for (;;) {
-    if (tid == 0) {
+    if (tid >= 32) {  // zero G while thread 0 sets the next work item up (G is free: the loop ends in a barrier)
+      for (int i = tid - 32; i < kPolyD * npos; i += kPolyThreads - 32) { Ga[i] = 0; Gb[i] = 0; }
+    } else if (tid == 0) {
       const long long wi = atomicAdd(work_counter, 1);
       PolyTile& T = sm.ti;
       T.next = wi < n_work;
@@ -186,7 +188,8 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
         // |T_d| <= 1, so every channel value is at most 2^bits in units of 2^-s (see poly_add)
         const double ddx = T.g.s[0] - T.g.r[0], ddy = T.g.s[1] - T.g.r[1], ddz = T.g.s[2] - T.g.r[2];
         const double abound = 0.0795774715459476679 / fmax(sqrt(ddx * ddx + ddy * ddy + ddz * ddz), 1e-30);
-        const int e = (int)ceil(log2(abound));
+        int e;
+        (void)frexp(abound, &e);  // abound < 2^e
         T.two_word = bits <= 0;
         if (bits <= 0) bits = 28;
         T.scalef = ldexpf(1.f, bits - e);
@@ -197,7 +200,6 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
     if (!sm.ti.next) break;
     const PolyTile& T = sm.ti;
     const RirGeom& g = T.g;
-    for (int i = tid; i < kPolyD * npos; i += kPolyThreads) { Ga[i] = 0; Gb[i] = 0; }
     if (T.use_bz)
       for (int i = tid; i <= T.zh - T.zl; i += kPolyThreads) sm.bz[i] = poly_z_factor(T.zl + i, g);
 
