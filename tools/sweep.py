@@ -120,12 +120,13 @@ def main():
     arr = P.room_array(rooms)
     plan_s = time.time() - t0
     out = torch.empty(off, dtype=torch.float32, device=dev)
-    fn = lambda: P.simulate_rir_batch(arr, rb.fs, out, seed=rb.seed)  # noqa: E731
-    ms = time_call(fn, reps=3, warm=1)
-    rows.append(dict(cfg="cfg5", mode="fp32", M=rb.n, ms=ms, rirs_per_s=rb.n / ms * 1e3, lattice_per_s=lattice / ms * 1e3,
-                     samples=off, host_plan_s=plan_s,
-                     note="time includes the call's host planning + job-table upload (batch API synchronises)"))
-    emit(rows[-1])
+    for mode in ("fp32", "poly"):
+        fn = lambda: P.simulate_rir_batch(arr, rb.fs, out, seed=rb.seed, mode=mode)  # noqa: E731
+        ms = time_call(fn, reps=3, warm=1)
+        rows.append(dict(cfg="cfg5", mode=mode, M=rb.n, ms=ms, rirs_per_s=rb.n / ms * 1e3,
+                         lattice_per_s=lattice / ms * 1e3, samples=off, host_plan_s=plan_s,
+                         note="time includes the call's host planning + job-table upload (batch API synchronises)"))
+        emit(rows[-1])
     # NEXT row f1: moving source, 1 s at 16 kHz, 100 trajectory points x 32 mics, 0.7 s RIRs (cfg3 length)
     n_sig, n_pts, n_mics, L = 16000, 100, 32, 11200
     sig = torch.randn(n_sig, device=dev)
