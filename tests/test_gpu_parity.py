@@ -274,7 +274,8 @@ def test_reciprocity_gpu(P, oracle):
     assert rel_err(a, b)[0] <= 1e-5
 
 
-def test_batch_rooms_vs_oracle(P, oracle):
+@pytest.mark.parametrize("mode", ["fp32", "poly"])
+def test_batch_rooms_vs_oracle(P, oracle, mode):
     """config 5 shape: independent rooms, ragged rows, tail streams rir_index_base + i."""
     import torch
     rb = W.cfg5(12)
@@ -290,13 +291,13 @@ def test_batch_rooms_vs_oracle(P, oracle):
                                         rb.Tmax[i], fs=rb.fs, seed=rb.seed, rir_index_base=1000 + i)[0, 0])
         off += nS
     out = torch.full((off,), float("nan"), device="cuda")
-    P.simulate_rir_batch(rooms, rb.fs, out, seed=rb.seed, rir_index_base=1000, sync=True)
+    P.simulate_rir_batch(rooms, rb.fs, out, seed=rb.seed, rir_index_base=1000, sync=True, mode=mode)
     o = out.cpu().numpy().astype(np.float64)
     off = 0
     for i, r in enumerate(refs):
         g = o[off:off + r.size]
         off += r.size
-        assert rel_err(g, r)[0] <= TOL["fp32"], i
+        assert rel_err(g, r)[0] <= TOL[mode], i
 
 
 # ---------------------------------------------------------------- NEXT row f1: trajectory filtering
