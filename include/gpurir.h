@@ -65,7 +65,9 @@ typedef enum {
                         A_n T_d(2 phi_n - 1), d = 0..7, to the integer sample floor(x_n) (exact 64-bit
                         fixed-point sums, deterministic), then an 8-channel FIR of 2H taps, whose
                         coefficients expand delta'(m - phi) in Chebyshev polynomials (max error 4.3e-7),
-                        produces the RIR.  fp32 arithmetic; fp32 tolerance.  Requires Tw fs <= 1022. */
+                        produces the RIR.  fp32 arithmetic; fp32 tolerance.  Requires Tw fs <= 1022.
+                        Calls with fewer than 32 work items of 1024 samples (a lone RIR) run the direct
+                        fp32 kernels instead, unless opts->split < 0 forces the polyphase kernel. */
 } gpurir_mode;
 
 #define GPURIR_FLAG_SYNC 1u /* synchronise the stream before returning and report device-side status */
@@ -77,7 +79,8 @@ typedef struct {
   uint64_t seed;            /* diffuse-tail RNG key (Philox4x32-10, reading C16), default 0         */
   uint64_t rir_index_base;  /* global index of this call's first RIR (tail RNG stream id), default 0 */
   void* stream;             /* cudaStream_t to launch on; NULL = the legacy default stream          */
-  int split;                /* CTAs cooperating on one time tile (thread-block cluster), 0 = auto   */
+  int split;                /* CTAs cooperating on one time tile (thread-block cluster), 0 = auto;
+                               < 0 forces the persistent kernel (fp32/LUT/fp16) or the polyphase kernel */
   unsigned flags;           /* GPURIR_FLAG_*                                                        */
   void* ev_ism[2];          /* optional cudaEvent_t pair recorded on `stream` around the ISM kernel  */
   void* ev_tail[2];         /* optional cudaEvent_t pair recorded around the diffuse-tail kernel     */

@@ -211,6 +211,8 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
 // volume V, so about 4 pi d^2 (c / fs) / V images share one integer sample position at distance d.  With twice
 // that at the farthest ISM delay (+16) as the bound N, single-word accumulation with bits = 22 is used when
 // 2^22 N <= 2^30 (N <= 256); otherwise 0 selects the two-word scheme (2^28 resolution).
+constexpr long long kPolyMinItems = 32;  // smaller polyphase calls take the direct fp32 kernels
+
 int poly_bits_for(const float L[3], long long nISM, double fs, double c, double Tw) {
   const double V = (double)L[0] * L[1] * L[2];
   const double dmax = ((double)nISM + Tw * fs / 2.0 + 1.0) * c / fs;
@@ -490,7 +492,11 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     A.M_src = M_src; A.M_rcv = M_rcv; A.M = (int)M;
     A.nISM = (int)nISM;
     A.row_stride = nS;
-    const bool poly = o.mode == GPURIR_POLY;
+    // polyphase mode on a call with fewer than kPolyMinItems 1024-sample work items (a lone RIR) runs the
+    // direct fp32 kernels instead: they spread one RIR's tiles over clusters of CTAs
+    const bool poly = o.mode == GPURIR_POLY &&
+                      (((nISM + kPolyTile - 1) / kPolyTile) * M >= kPolyMinItems || o.split < 0);  // split < 0 forces
+    const int kmode = o.mode == GPURIR_POLY ? (poly ? GPURIR_POLY : GPURIR_FP32) : o.mode;
     const bool persistent = poly || use_persistent(((nISM + kTC - 1) / kTC) * M, o.split, d);
     const int tile_len = poly ? kPolyTile : persistent ? kTCPersistent : kTC;
     A.nTiles = (int)((nISM + tile_len - 1) / tile_len);
@@ -505,10 +511,10 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     if (poly) {
       e = launch_ism_poly(A, nclusters, take_counter(d), d->num_sms, stream);
     } else if (persistent) {
-      e = launch_ism_ws(A, o.mode, nclusters, take_counter(d), d->num_sms, stream);
+      e = launch_ism_ws(A, kmode, nclusters, take_counter(d), d->num_sms, stream);
     } else {
       int split = auto_split(nclusters, o.split);
-      e = launch_ism(A, o.mode, split, nclusters, stream);
+      e = launch_ism(A, kmode, split, nclusters, stream);
     }
     if (e != cudaSuccess) return cuda_fail(e, "launch_ism");
     if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);
@@ -592,8 +598,12 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     int nch = nISM < nS ? (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4)) : 0;
     for (int ch = 0; ch < nch; ch++) chunks.push_back(make_int2(i, ch));
   }
-  const bool persistent = o.mode == GPURIR_POLY || use_persistent(small_tiles, o.split, d);
-  const int tile_len = o.mode == GPURIR_POLY ? kPolyTile : persistent ? kTCPersistent : kTC;
+  long long poly_tiles = 0;
+  for (int i = 0; i < n_rooms; i++) poly_tiles += (jobs[i].nISM + kPolyTile - 1) / kPolyTile;
+  const bool poly = o.mode == GPURIR_POLY && (poly_tiles >= kPolyMinItems || o.split < 0);  // as single-room
+  const int kmode = o.mode == GPURIR_POLY ? (poly ? GPURIR_POLY : GPURIR_FP32) : o.mode;
+  const bool persistent = poly || use_persistent(small_tiles, o.split, d);
+  const int tile_len = poly ? kPolyTile : persistent ? kTCPersistent : kTC;
   // heavy-first schedule without a comparison sort: image density grows ~ t^2 (SURVEY §7 hard part 2), so
   // emit all rooms' last tiles first, then the second-to-last, ... (a counting order over tile index)
   int max_tiles = 0;
@@ -633,9 +643,9 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     if ((st = setup_mode(d, o, fs, H, stream, A))) { cudaFreeAsync(ws, stream); return st; }
     long long nw = (long long)tiles.size();
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
-    if (o.mode == GPURIR_POLY) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, stream);
-    else if (persistent) e = launch_ism_ws(A, o.mode, nw, take_counter(d), d->num_sms, stream);
-    else e = launch_ism(A, o.mode, auto_split(nw, o.split), nw, stream);
+    if (poly) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, stream);
+    else if (persistent) e = launch_ism_ws(A, kmode, nw, take_counter(d), d->num_sms, stream);
+    else e = launch_ism(A, kmode, auto_split(nw, o.split), nw, stream);
     if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_ism(batch)"); }
     if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);
   }

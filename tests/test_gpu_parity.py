@@ -498,7 +498,7 @@ def test_poly_two_word_long_rir(P, oracle):
     two-word accumulation runs; parity at the fp32 tolerance on 2 receivers."""
     sc = W.cfg3(2, "full")
     beta, nb = derive(oracle, sc)
-    g = run_gpu(P, sc, beta, nb, mode="poly")
+    g = run_gpu(P, sc, beta, nb, mode="poly", split=-1)  # 22 work items: forced onto the polyphase kernel
     r = run_oracle(oracle, sc, beta, nb)
     assert rel_err(g, r).max() <= TOL["poly"]
 
@@ -511,7 +511,7 @@ def test_poly_sampling_rates(P, oracle, fs):
     for i in range(3):
         sc = W.random_small_scene(rng, fs=fs, T=0.03)
         beta, nb = derive(oracle, sc)
-        g = run_gpu(P, sc, beta, nb, mode="poly")
+        g = run_gpu(P, sc, beta, nb, mode="poly", split=-1)  # small call: forced onto the polyphase kernel
         r = run_oracle(oracle, sc, beta, nb)
         assert rel_err(g, r).max() <= TOL["poly"], (fs, i)
 
@@ -523,3 +523,16 @@ def test_poly_matches_direct_kernel(P, oracle):
     a = run_gpu(P, sc, beta, nb, mode="fp32")
     b = run_gpu(P, sc, beta, nb, mode="poly")
     assert rel_err(b, a).max() <= 5e-5
+
+
+def test_poly_small_calls_take_direct_kernel(P, oracle):
+    """Fewer than 32 polyphase work items (a lone RIR): the call runs the direct fp32 kernels (bitwise equal
+    to mode fp32); split = -1 still forces the polyphase kernel (different rounding, same tolerance)."""
+    sc = W.cfg1()
+    beta, nb = derive(oracle, sc)
+    a = run_gpu(P, sc, beta, nb, mode="fp32")
+    b = run_gpu(P, sc, beta, nb, mode="poly")
+    assert np.array_equal(a, b)
+    c = run_gpu(P, sc, beta, nb, mode="poly", split=-1)
+    assert not np.array_equal(a, c)
+    assert rel_err(c, run_oracle(oracle, sc, beta, nb))[0] <= TOL["poly"]
