@@ -261,9 +261,12 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
         const bool use_bz = T.use_bz, dir_src = g.as != 1.f, two_word = T.two_word;
         const float oz = g.o[2], ga = g.a, fsc = (float)fs_over_c, scalef = T.scalef;
         int boundary = sm.colpre[j];
+        PolyColRec cr = sm.col[j];  // the current column's record, in registers: reloaded on a column change
         for (int gi = g0; gi < g1; gi++) {  // every lane runs R candidates: the walk keeps the warp converged
-          while (gi >= boundary) { before = boundary; j++; boundary = sm.colpre[j]; }
-          const PolyColRec& cr = sm.col[j];
+          if (gi >= boundary) {
+            do { before = boundary; j++; boundary = sm.colpre[j]; } while (gi >= boundary);
+            cr = sm.col[j];
+          }
           const int l = gi - before;
           const int nz = l < cr.r1n ? cr.r1lo + l : cr.r2lo + (l - cr.r1n);
           const int odd = nz & 1;
