@@ -195,7 +195,9 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
       const double fv = eq6_samples((double)m - phi, H);
       for (int k = 0; k < kPolyDeg; k++) c[k] += fv * cos(k * th);  // T_k(y) = cos(k theta)
     }
-    for (int k = 0; k < kPolyDeg; k++) tab[(size_t)mi * kPolyDeg + k] = (float)(c[k] * (k ? 2.0 : 1.0) / kPolyNodes);
+    // layout [channel pair q][tap mi][2]: the kernel's FIR group for pair q streams its taps contiguously
+    for (int k = 0; k < kPolyDeg; k++)
+      tab[((size_t)(k >> 1) * P.ntaps + mi) * 2 + (k & 1)] = (float)(c[k] * (k ? 2.0 : 1.0) / kPolyNodes);
   }
   const size_t bytes = tab.size() * sizeof(float);
   cudaError_t e = cudaMalloc(&P.dev, bytes);

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
   const int ntaps = A.poly_ntaps, npos = kPolyTC + ntaps - 1;
   int* Ga = reinterpret_cast<int*>(smem_raw + sizeof(PolySmem));  // coarse part of G (units 2^14)
   int* Gb = Ga + kPolyD * npos;                                    // fine part of G
-  float* Pt = reinterpret_cast<float*>(Gb + kPolyD * npos);        // [ntaps][8], tap index mi = m - m_lo
+  float* Pt = reinterpret_cast<float*>(Gb + kPolyD * npos);        // [4 pairs][ntaps][2], mi = m - m_lo
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double fs_over_c = A.fs_over_c, sc2 = fs_over_c * fs_over_c;
   const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f;
@@ -133,7 +133,13 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
 
   for (;;) {
     if (tid >= 32) {  // zero G while thread 0 sets the next work item up (G is free: the loop ends in a barrier)
-      for (int i = tid - 32; i < kPolyD * npos; i += kPolyThreads - 32) { Ga[i] = 0; Gb[i] = 0; }
+      // 16-B stores (npos is odd, so the planes are zeroed as one block: 8 npos words per array)
+      const int n4 = (kPolyD * npos) >> 2;
+      int4* z = reinterpret_cast<int4*>(Ga);
+      const bool both = A.jobs || A.poly_bits <= 0;  // the fine plane Gb is only used by two-word items
+      for (int i = tid - 32; i < n4; i += kPolyThreads - 32) z[i] = make_int4(0, 0, 0, 0);
+      if (both)
+        for (int i = tid - 32; i < kPolyD * npos; i += kPolyThreads - 32) Gb[i] = 0;
     } else if (tid == 0) {
       const long long wi = atomicAdd(work_counter, 1);
       PolyTile& T = sm.ti;
@@ -303,10 +309,14 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
 #pragma unroll
       for (int q = 0; q < kPolyD / 2; q++) {
         const int i0 = (2 * q) * npos + p, i1 = (2 * q + 1) * npos + p;
-        const long long v0 = T.two_word ? (long long)Ga[i0] * 16384 + Gb[i0] : (long long)Ga[i0];
-        const long long v1 = T.two_word ? (long long)Ga[i1] * 16384 + Gb[i1] : (long long)Ga[i1];
-        tmp[nmine * (kPolyD / 2) + q] =
-            make_float2((float)((double)v0 * T.inv_scale), (float)((double)v1 * T.inv_scale));
+        if (T.two_word) {
+          const long long v0 = (long long)Ga[i0] * 16384 + Gb[i0], v1 = (long long)Ga[i1] * 16384 + Gb[i1];
+          tmp[nmine * (kPolyD / 2) + q] =
+              make_float2((float)((double)v0 * T.inv_scale), (float)((double)v1 * T.inv_scale));
+        } else {  // single word: |sum| < 2^30, exact in fp64; inv_scale is a power of two
+          tmp[nmine * (kPolyD / 2) + q] =
+              make_float2((float)((double)Ga[i0] * T.inv_scale), (float)((double)Ga[i1] * T.inv_scale));
+        }
       }
     }
     __syncthreads();
@@ -324,7 +334,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
     // positions q - mi - 1 - u sit at fixed offsets 0 .. -6, -8 of one padded address (q = 7 mod 8).
     {
       const int gq = tid >> 7, lt = tid & 127, t8 = 8 * lt;
-      const float2* P2 = reinterpret_cast<const float2*>(Pt) + gq;  // (P_2gq, P_2gq+1)[mi] at P2[4 mi]
+      const float4* P4 = reinterpret_cast<const float4*>(Pt) + gq * (ntaps >> 1);  // pair gq: taps (2i, 2i+1)
       float2 acc[8], w[8];
       const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (m = m_lo)
       const float2* G = Gf + gq * plane;
@@ -334,10 +344,11 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
         w[r] = G[(q + r) + ((q + r) >> 3)];
       }
       const float2* gn = G + (q - 1) + ((q - 1) >> 3);  // padded address of position q - 1 (= 6 mod 8)
-      for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P2 += 32) {
+      for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P4 += 4) {
+        const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};  // taps mi .. mi + 7 of channel pair gq
 #pragma unroll
         for (int u = 0; u < 8; u++) {  // tap mi + u: output r uses slot (r - u) & 7, then slot (7 - u) & 7 refills
-          const float2 pc = P2[4 * u];
+          const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
 #pragma unroll
           for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 7], acc[r]);
           w[(7 - u) & 7] = gn[u < 7 ? -u : -8];  // the last group's refills read padding: never used
