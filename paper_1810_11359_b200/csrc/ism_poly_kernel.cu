@@ -246,15 +246,21 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
             cnt = n1 + n2;
           }
         }
-        sm.col[tid] = cr;
+        // one scan of (candidates + 2^20 x nonempty) both prefixes the candidates and compacts the nonempty
+        // columns in order, so the run search and the walk below never visit an empty column
+        const int incl = poly_block_scan(cnt + (cnt > 0 ? (1 << 20) : 0), sm.scan_tmp);
+        if (cnt > 0) {
+          sm.col[(incl >> 20) - 1] = cr;
+          sm.colpre[(incl >> 20) - 1] = incl & 0xFFFFF;
+        }
       }
-      sm.colpre[tid] = poly_block_scan(cnt, sm.scan_tmp);
       __syncthreads();
-      const int total = sm.colpre[kPolyCols - 1];
+      const int tot = sm.scan_tmp[kPolyThreads / 32 - 1];
+      const int total = tot & 0xFFFFF, ncomp = tot >> 20;
       const int R = (total + kPolyThreads - 1) / kPolyThreads;
       const int g0 = tid * R, g1 = min(g0 + R, total);
       if (g0 < g1) {
-        int lo = 0, hi = kPolyCols - 1;  // first column with colpre > g0
+        int lo = 0, hi = ncomp - 1;  // first (compacted) column with colpre > g0
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
           if (sm.colpre[mid] > g0) hi = mid; else lo = mid + 1;
