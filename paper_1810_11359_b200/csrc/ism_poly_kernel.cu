@@ -83,7 +83,7 @@ __device__ __forceinline__ float poly_z_factor(int nz, const RirGeom& g) {
 // (single word, fp32 arithmetic); otherwise bits = 28 and v = a 2^14 + b, b in [0, 2^14), goes to two int32 planes (2^17
 // terms per position before either could overflow).  Integer adds commute, so G does not depend on the order
 // in which images arrive (deterministic, shard-invariant).
-__device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, float y, float amp, float scale,
+__device__ __forceinline__ void poly_add(int* Ga, int* Gb, int W, int p, float y, float amp, float scale,
                                          bool two_word) {
   if (!two_word) {
     // single word, bits <= 22: fp32 suffices — T_d by the recurrence in fp32 (|error| ~ 1e-7 d), and
@@ -91,11 +91,11 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, floa
     const float as = amp * scale, y2 = 2.f * y, magic = 12582912.f;  // power-of-two scale: exact
     float tm2 = 1.f, tm1 = y;
     atomicAdd(&Ga[p], __float_as_int(fmaf(as, 1.f, magic)) - 0x4B400000);
-    atomicAdd(&Ga[npos + p], __float_as_int(fmaf(as, y, magic)) - 0x4B400000);
+    atomicAdd(&Ga[W + p], __float_as_int(fmaf(as, y, magic)) - 0x4B400000);
 #pragma unroll
     for (int d = 2; d < kPolyD; d++) {
       const float t = fmaf(y2, tm1, -tm2);  // T_d = 2 y T_{d-1} - T_{d-2}
-      atomicAdd(&Ga[d * npos + p], __float_as_int(fmaf(as, t, magic)) - 0x4B400000);
+      atomicAdd(&Ga[d * W + p], __float_as_int(fmaf(as, t, magic)) - 0x4B400000);
       tm2 = tm1;
       tm1 = t;
     }
@@ -111,7 +111,7 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int npos, int p, floa
 #pragma unroll
   for (int d = 0; d < kPolyD; d++) {
     const int v = __double2loint(fma(ad, T[d], magic));
-    const int i = d * npos + p;  // channel-major planes: consecutive positions are consecutive words
+    const int i = d * W + p;  // channel-major planes: consecutive positions are consecutive words
     atomicAdd(&Ga[i], v >> 14);
     atomicAdd(&Gb[i], v & 0x3FFF);
   }
@@ -121,9 +121,12 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PolySmem& sm = *reinterpret_cast<PolySmem*>(smem_raw);
   const int ntaps = A.poly_ntaps, npos = kPolyTC + ntaps - 1;
+  // channel planes of W words, position p at p + p/8: the filter's lanes read positions 8 apart, which the
+  // padding spreads over all banks (stride 9 words)
+  const int W = npos + (npos >> 3) + 1;
   int* Ga = reinterpret_cast<int*>(smem_raw + sizeof(PolySmem));  // coarse part of G (units 2^14)
-  int* Gb = Ga + kPolyD * npos;                                    // fine part of G
-  float* Pt = reinterpret_cast<float*>(Gb + kPolyD * npos);        // [4 pairs][ntaps][2], mi = m - m_lo
+  int* Gb = Ga + kPolyD * W;                                       // fine part of G
+  float* Pt = reinterpret_cast<float*>(Gb + kPolyD * W);        // [4 pairs][ntaps][2], mi = m - m_lo
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double fs_over_c = A.fs_over_c, sc2 = fs_over_c * fs_over_c;
   const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f;
@@ -133,13 +136,12 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
 
   for (;;) {
     if (tid >= 32) {  // zero G while thread 0 sets the next work item up (G is free: the loop ends in a barrier)
-      // 16-B stores (npos is odd, so the planes are zeroed as one block: 8 npos words per array)
-      const int n4 = (kPolyD * npos) >> 2;
-      int4* z = reinterpret_cast<int4*>(Ga);
+      // 16-B stores over the 8 W words of each array
+      const int n4 = (kPolyD * W) >> 2;
       const bool both = A.jobs || A.poly_bits <= 0;  // the fine plane Gb is only used by two-word items
-      for (int i = tid - 32; i < n4; i += kPolyThreads - 32) z[i] = make_int4(0, 0, 0, 0);
+      for (int i = tid - 32; i < n4; i += kPolyThreads - 32) reinterpret_cast<int4*>(Ga)[i] = make_int4(0, 0, 0, 0);
       if (both)
-        for (int i = tid - 32; i < kPolyD * npos; i += kPolyThreads - 32) Gb[i] = 0;
+        for (int i = tid - 32; i < n4; i += kPolyThreads - 32) reinterpret_cast<int4*>(Gb)[i] = make_int4(0, 0, 0, 0);
     } else if (tid == 0) {
       const long long wi = atomicAdd(work_counter, 1);
       PolyTile& T = sm.ti;
@@ -299,37 +301,19 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
           if (dir_src) gain *= src_gain(cr.sdot, odd, dzf, fsc * rx, g);
           const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
           const float y = fmaf(2.f, xr - fj, -1.f);        // 2 phi - 1 in [-1, 1)
-          poly_add(Ga, Gb, npos, p, y, amp, scalef, two_word);
+          poly_add(Ga, Gb, W, p + (p >> 3), y, amp, scalef, two_word);
         }
       }
       __syncthreads();  // column records are replaced by the next batch
     }
 
-    // ---- 2. fixed point -> fp32 in 4 channel-pair planes, Gf[pair][pad(p)] = (G_2q, G_2q+1) ------------
-    // pad(p) = p + p/8: the filter's lanes read positions 8 apart, which the padding spreads over all banks
-    float2* Gf = reinterpret_cast<float2*>(Ga);  // in place over Ga / Gb (read everything, barrier, write)
-    const int plane = npos + (npos >> 3) + 1;
-    float2 tmp[(kPolyD / 2) * 3];  // npos <= 1024 + 511: at most 3 positions per thread
-    int nmine = 0;
-    for (int p = tid; p < npos && nmine < 3; p += kPolyThreads, nmine++) {
-#pragma unroll
-      for (int q = 0; q < kPolyD / 2; q++) {
-        const int i0 = (2 * q) * npos + p, i1 = (2 * q + 1) * npos + p;
-        if (T.two_word) {
-          const long long v0 = (long long)Ga[i0] * 16384 + Gb[i0], v1 = (long long)Ga[i1] * 16384 + Gb[i1];
-          tmp[nmine * (kPolyD / 2) + q] =
-              make_float2((float)((double)v0 * T.inv_scale), (float)((double)v1 * T.inv_scale));
-        } else {  // single word: |sum| < 2^30, exact in fp64; inv_scale is a power of two
-          tmp[nmine * (kPolyD / 2) + q] =
-              make_float2((float)((double)Ga[i0] * T.inv_scale), (float)((double)Ga[i1] * T.inv_scale));
-        }
-      }
-    }
-    __syncthreads();
-    nmine = 0;
-    for (int p = tid; p < npos && nmine < 3; p += kPolyThreads, nmine++) {
-#pragma unroll
-      for (int q = 0; q < kPolyD / 2; q++) Gf[q * plane + p + (p >> 3)] = tmp[nmine * (kPolyD / 2) + q];
+    // ---- 2. fixed point -> fp32, in place (every word converts itself: no staging, one barrier) ---------
+    float* Gf = reinterpret_cast<float*>(Ga);
+    if (T.two_word) {
+      for (int i = tid; i < kPolyD * W; i += kPolyThreads)
+        Gf[i] = (float)((double)((long long)Ga[i] * 16384 + Gb[i]) * T.inv_scale);
+    } else {  // single word: |sum| < 2^30 converts exactly; inv_scale is a power of two
+      for (int i = tid; i < kPolyD * W; i += kPolyThreads) Gf[i] = (float)((double)Ga[i] * T.inv_scale);
     }
     __syncthreads();
 
@@ -343,13 +327,14 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
       const float4* P4 = reinterpret_cast<const float4*>(Pt) + gq * (ntaps >> 1);  // pair gq: taps (2i, 2i+1)
       float2 acc[8], w[8];
       const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (m = m_lo)
-      const float2* G = Gf + gq * plane;
+      const float* G0 = Gf + (2 * gq) * W;  // channel 2 gq; channel 2 gq + 1 sits W words further
 #pragma unroll
       for (int r = 0; r < 8; r++) {
         acc[r] = make_float2(0.f, 0.f);
-        w[r] = G[(q + r) + ((q + r) >> 3)];
+        const int a = (q + r) + ((q + r) >> 3);
+        w[r] = make_float2(G0[a], G0[a + W]);
       }
-      const float2* gn = G + (q - 1) + ((q - 1) >> 3);  // padded address of position q - 1 (= 6 mod 8)
+      const float* gn = G0 + (q - 1) + ((q - 1) >> 3);  // padded address of position q - 1 (= 6 mod 8)
       for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P4 += 4) {
         const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};  // taps mi .. mi + 7 of channel pair gq
 #pragma unroll
@@ -357,7 +342,8 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
           const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
 #pragma unroll
           for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 7], acc[r]);
-          w[(7 - u) & 7] = gn[u < 7 ? -u : -8];  // the last group's refills read padding: never used
+          const int o = u < 7 ? -u : -8;  // the last group's refills read padding: never used
+          w[(7 - u) & 7] = make_float2(gn[o], gn[o + W]);
         }
       }
       float* red = reinterpret_cast<float*>(sm.col);  // 4 x 1024 partial sums (the column records are dead here)
@@ -382,7 +368,8 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
 
 size_t ism_poly_smem_bytes(int ntaps) {
   const size_t npos = (size_t)kPolyTC + ntaps - 1;
-  return sizeof(PolySmem) + 2 * kPolyD * npos * sizeof(int) + (size_t)ntaps * kPolyD * sizeof(float);
+  const size_t W = npos + (npos >> 3) + 1;
+  return sizeof(PolySmem) + 2 * kPolyD * W * sizeof(int) + (size_t)ntaps * kPolyD * sizeof(float);
 }
 
 cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, cudaStream_t stream) {
