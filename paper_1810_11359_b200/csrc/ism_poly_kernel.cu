@@ -289,10 +289,13 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
           const double dz = fma(int_to_double(nzo), Lz, odd ? offO : offE);  // Eq. 1 along z
           const double x2 = fma(dz, dz, cr.rho2) * sc2;                       // (d fs / c)^2
           if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); continue; }
-          float x0f, rx;
-          const float xr = delay_rel(x2, tc, x0f, rx);  // x - tc, fp64-corrected; rx = 1/x
+          float xa, xd, rx;  // x - tc = xa + xd (xa exact, xd the fp64 Newton correction); rx = 1/x
+          delay_split(x2, tc, xa, xd, rx);
           int jodd;
-          const float fj = floor_parity(xr, jodd);
+          float fj = floor_parity(xa, jodd);
+          float phi = (xa - fj) + xd;  // fraction of x to ~1e-7 samples, then renormalised to [0, 1)
+          if (phi < 0.f) { phi += 1.f; fj -= 1.f; }
+          else if (phi >= 1.f) { phi -= 1.f; fj += 1.f; }
           const int p = (int)fj + pofs;
           if (p < 0 || p >= npos) continue;  // reaches no sample of this tile
           const float dzf = fmaf((float)nzo, Lzf, odd ? offOf : offEf);
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
           float gain = ga + (1.f - ga) * cth;
           if (dir_src) gain *= src_gain(cr.sdot, odd, dzf, fsc * rx, g);
           const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
-          const float y = fmaf(2.f, xr - fj, -1.f);        // 2 phi - 1 in [-1, 1)
+          const float y = fmaf(2.f, phi, -1.f);            // 2 phi - 1 in [-1, 1)
           poly_add(Ga, Gb, W, p + (p >> 3), y, amp, scalef, two_word);
         }
       }
