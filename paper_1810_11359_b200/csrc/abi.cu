@@ -507,6 +507,7 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     A.status = d->status;
     if ((st = setup_mode(d, o, fs, H, stream, A))) return st;
     A.poly_bits = poly_bits_for(room_sz, nISM, fs, c, o.Tw);
+    A.poly_gb = A.poly_bits <= 0;
     long long nclusters = (long long)A.nTiles * M;
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
@@ -643,6 +644,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     A.out = out;
     A.status = d->status;
     if ((st = setup_mode(d, o, fs, H, stream, A))) { cudaFreeAsync(ws, stream); return st; }
+    for (int i = 0; i < n_rooms && !A.poly_gb; i++) A.poly_gb = jobs[i].poly_bits <= 0;
     long long nw = (long long)tiles.size();
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     if (poly) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, stream);

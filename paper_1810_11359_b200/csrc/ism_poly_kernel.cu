@@ -20,11 +20,12 @@
 namespace gpurir {
 
 constexpr int kPolyThreads = 512;
-constexpr int kPolyTC = kPolyTile;      // 1024 output samples per work item (the host planner's tile)
+constexpr int kPolyTC = kPolyTile;      // output samples per work item (the host planner's tile)
+constexpr int kPolyPasses = kPolyTC / 1024;  // FIR passes: 4 channel-pair groups x 128 threads x 8 outputs each
 constexpr int kPolyD = 8;               // Chebyshev channels T_0..T_7
 constexpr int kPolyCols = kPolyThreads; // lattice columns per enumeration batch
 constexpr int kPolyBz = 1024;           // z-factor table entries
-static_assert(kPolyTC == 2 * kPolyThreads, "two output samples per thread in the filter's final sum");
+static_assert(kPolyTC % 1024 == 0 && kPolyThreads == 512, "FIR passes of 4 x 128 threads x 8 outputs");
 
 struct PolyColRec {  // 32 B, as WsColRec
   double rho2;
@@ -33,7 +34,6 @@ struct PolyColRec {  // 32 B, as WsColRec
   float sdot;
 };
 
-static_assert(sizeof(PolyColRec) * kPolyCols >= 4 * kPolyTC * sizeof(float), "FIR partial sums reuse sm.col");
 
 struct PolyTile {
   RirGeom g;
@@ -125,8 +125,8 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
   // padding spreads over all banks (stride 9 words)
   const int W = npos + (npos >> 3) + 1;
   int* Ga = reinterpret_cast<int*>(smem_raw + sizeof(PolySmem));  // coarse part of G (units 2^14)
-  int* Gb = Ga + kPolyD * W;                                       // fine part of G
-  float* Pt = reinterpret_cast<float*>(Gb + kPolyD * W);        // [4 pairs][ntaps][2], mi = m - m_lo
+  int* Gb = Ga + kPolyD * W;                                       // fine part of G (two-word calls only)
+  float* Pt = reinterpret_cast<float*>(Gb + (A.poly_gb ? kPolyD * W : 0));        // [4 pairs][ntaps][2], mi = m - m_lo
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double fs_over_c = A.fs_over_c, sc2 = fs_over_c * fs_over_c;
   const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
     if (tid >= 32) {  // zero G while thread 0 sets the next work item up (G is free: the loop ends in a barrier)
       // 16-B stores over the 8 W words of each array
       const int n4 = (kPolyD * W) >> 2;
-      const bool both = A.jobs || A.poly_bits <= 0;  // the fine plane Gb is only used by two-word items
+      const bool both = A.poly_gb;  // the fine plane Gb exists (and is used) only for two-word items
       for (int i = tid - 32; i < n4; i += kPolyThreads - 32) reinterpret_cast<int4*>(Ga)[i] = make_int4(0, 0, 0, 0);
       if (both)
         for (int i = tid - 32; i < n4; i += kPolyThreads - 32) reinterpret_cast<int4*>(Gb)[i] = make_int4(0, 0, 0, 0);
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
 
     // ---- 1. image aggregation -------------------------------------------------------------
     const float amp_scale = fs_over_c_4pi;
-    const int pofs = kPolyTC / 2 + m_hi;  // p = floor(x - tc) + pofs
+    const int pbase = sm.ti.t0 - m_hi;  // p = floor(x) - pbase
     for (int qb = 0; qb < T.ncols; qb += kPolyCols) {
       int cnt = 0;
       {
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
         int before = j > 0 ? sm.colpre[j - 1] : 0;
         const double Lz = g.L[2], offE = T.offE, offO = T.offO;
         const float Lzf = (float)Lz, offEf = (float)offE, offOf = (float)offO;
-        const int tc = T.tc, zl = T.zl;
+        const int zl = T.zl;
         const bool use_bz = T.use_bz, dir_src = g.as != 1.f, two_word = T.two_word;
         const float oz = g.o[2], ga = g.a, fsc = (float)fs_over_c, scalef = T.scalef;
         int boundary = sm.colpre[j];
@@ -289,14 +289,14 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
           const double dz = fma(int_to_double(nzo), Lz, odd ? offO : offE);  // Eq. 1 along z
           const double x2 = fma(dz, dz, cr.rho2) * sc2;                       // (d fs / c)^2
           if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); continue; }
-          float xa, xd, rx;  // x - tc = xa + xd (xa exact, xd the fp64 Newton correction); rx = 1/x
-          delay_split(x2, tc, xa, xd, rx);
+          float x0f, xd, rx;  // x = x0f + xd (xd the fp64 Newton correction); rx = 1/x
+          delay_split(x2, x0f, xd, rx);
           int jodd;
-          float fj = floor_parity(xa, jodd);
-          float phi = (xa - fj) + xd;  // fraction of x to ~1e-7 samples, then renormalised to [0, 1)
+          float fj = floor_parity(x0f, jodd);  // floor and fraction of x0f are exact
+          float phi = (x0f - fj) + xd;          // fraction of x to ~1e-7 samples, renormalised to [0, 1)
           if (phi < 0.f) { phi += 1.f; fj -= 1.f; }
           else if (phi >= 1.f) { phi -= 1.f; fj += 1.f; }
-          const int p = (int)fj + pofs;
+          const int p = (int)fj - pbase;
           if (p < 0 || p >= npos) continue;  // reaches no sample of this tile
           const float dzf = fmaf((float)nzo, Lzf, odd ? offOf : offEf);
           const float cth = fmaf(dzf, oz, cr.cdot) * (fsc * rx);
@@ -326,39 +326,50 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
     // ntaps is padded to a multiple of 8 with zero taps, so in every unrolled group of 8 taps the new
     // positions q - mi - 1 - u sit at fixed offsets 0 .. -6, -8 of one padded address (q = 7 mod 8).
     {
-      const int gq = tid >> 7, lt = tid & 127, t8 = 8 * lt;
-      const float4* P4 = reinterpret_cast<const float4*>(Pt) + gq * (ntaps >> 1);  // pair gq: taps (2i, 2i+1)
-      float2 acc[8], w[8];
-      const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (m = m_lo)
+      const int gq = tid >> 7, lt = tid & 127;
       const float* G0 = Gf + (2 * gq) * W;  // channel 2 gq; channel 2 gq + 1 sits W words further
+      float part[kPolyPasses][8];
 #pragma unroll
-      for (int r = 0; r < 8; r++) {
-        acc[r] = make_float2(0.f, 0.f);
-        const int a = (q + r) + ((q + r) >> 3);
-        w[r] = make_float2(G0[a], G0[a + W]);
-      }
-      const float* gn = G0 + (q - 1) + ((q - 1) >> 3);  // padded address of position q - 1 (= 6 mod 8)
-      for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P4 += 4) {
-        const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};  // taps mi .. mi + 7 of channel pair gq
+      for (int pass = 0; pass < kPolyPasses; pass++) {
+        const int t8 = pass * 1024 + 8 * lt;
+        const float4* P4 = reinterpret_cast<const float4*>(Pt) + gq * (ntaps >> 1);  // pair gq: taps (2i, 2i+1)
+        float2 acc[8], w[8];
+        const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (m = m_lo)
 #pragma unroll
-        for (int u = 0; u < 8; u++) {  // tap mi + u: output r uses slot (r - u) & 7, then slot (7 - u) & 7 refills
-          const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
-#pragma unroll
-          for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 7], acc[r]);
-          const int o = u < 7 ? -u : -8;  // the last group's refills read padding: never used
-          w[(7 - u) & 7] = make_float2(gn[o], gn[o + W]);
+        for (int r = 0; r < 8; r++) {
+          acc[r] = make_float2(0.f, 0.f);
+          const int a = (q + r) + ((q + r) >> 3);
+          w[r] = make_float2(G0[a], G0[a + W]);
         }
+        const float* gn = G0 + (q - 1) + ((q - 1) >> 3);  // padded address of position q - 1 (= 6 mod 8)
+        for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P4 += 4) {
+          const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};  // taps mi .. mi + 7 of channel pair gq
+#pragma unroll
+          for (int u = 0; u < 8; u++) {  // tap mi + u: output r uses slot (r - u) & 7, then slot (7 - u) & 7 refills
+            const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
+#pragma unroll
+            for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 7], acc[r]);
+            const int o = u < 7 ? -u : -8;  // the last group's refills read padding: never used
+            w[(7 - u) & 7] = make_float2(gn[o], gn[o + W]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 8; r++) part[pass][r] = acc[r].x + acc[r].y;
       }
-      float* red = reinterpret_cast<float*>(sm.col);  // 4 x 1024 partial sums (the column records are dead here)
-      float4* r4 = reinterpret_cast<float4*>(red + gq * kPolyTC + t8);
-      r4[0] = make_float4(acc[0].x + acc[0].y, acc[1].x + acc[1].y, acc[2].x + acc[2].y, acc[3].x + acc[3].y);
-      r4[1] = make_float4(acc[4].x + acc[4].y, acc[5].x + acc[5].y, acc[6].x + acc[6].y, acc[7].x + acc[7].y);
+      __syncthreads();  // every group is done reading G: its planes take the 4 x kPolyTC partial sums
+      float* red = Gf;
+#pragma unroll
+      for (int pass = 0; pass < kPolyPasses; pass++) {
+        float4* r4 = reinterpret_cast<float4*>(red + gq * kPolyTC + pass * 1024 + 8 * lt);
+        r4[0] = make_float4(part[pass][0], part[pass][1], part[pass][2], part[pass][3]);
+        r4[1] = make_float4(part[pass][4], part[pass][5], part[pass][6], part[pass][7]);
+      }
     }
     __syncthreads();
     {
-      const float* red = reinterpret_cast<const float*>(sm.col);
+      const float* red = Gf;
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
+      for (int h = 0; h < kPolyTC / kPolyThreads; h++) {
         const int t = tid + h * kPolyThreads, k = T.t0 + t;
         if (k < T.te)
           A.out[T.row + k] = (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
@@ -369,16 +380,16 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
   (void)lane; (void)warp;
 }
 
-size_t ism_poly_smem_bytes(int ntaps) {
+size_t ism_poly_smem_bytes(int ntaps, bool two_word) {
   const size_t npos = (size_t)kPolyTC + ntaps - 1;
   const size_t W = npos + (npos >> 3) + 1;
-  return sizeof(PolySmem) + 2 * kPolyD * W * sizeof(int) + (size_t)ntaps * kPolyD * sizeof(float);
+  return sizeof(PolySmem) + (two_word ? 2 : 1) * kPolyD * W * sizeof(int) + (size_t)ntaps * kPolyD * sizeof(float);
 }
 
 cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
-  const size_t smem = ism_poly_smem_bytes(A.poly_ntaps);
+  const size_t smem = ism_poly_smem_bytes(A.poly_ntaps, A.poly_gb != 0);
   e = cudaFuncSetAttribute(ism_poly_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long slots = 2LL * num_sms;

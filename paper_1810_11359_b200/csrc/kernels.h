@@ -74,6 +74,7 @@ struct IsmArgs {
   const float* poly_P;     // device [ntaps][8]
   int poly_ntaps, poly_mlo;
   int poly_bits;           // single-room call: fixed-point bits of one channel value, or 0 (two-word scheme)
+  int poly_gb;             // the call has two-word items: allocate and use the fine plane Gb
 };
 
 struct TailArgs {
@@ -103,7 +104,7 @@ cudaError_t launch_image_params(const IsmArgs& A, double* x_out, float* A_out, l
 size_t ism_ws_smem_bytes(int mode, int lut_rows, int lut_cols);
 cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* counter, int num_sms,
                           cudaStream_t stream);
-size_t ism_poly_smem_bytes(int ntaps);
+size_t ism_poly_smem_bytes(int ntaps, bool two_word);
 cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, cudaStream_t stream);
 cudaError_t launch_tail(const TailArgs& A, long long n_items, cudaStream_t stream);  // one warp per item
 
