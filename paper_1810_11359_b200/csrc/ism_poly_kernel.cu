@@ -291,11 +291,12 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
           if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); continue; }
           float x0f, xd, rx;  // x = x0f + xd (xd the fp64 Newton correction); rx = 1/x
           delay_split(x2, x0f, xd, rx);
+          // floor of the fp32 sum x0f + xd, fraction from the exact difference x0f - floor plus xd: within 1e-7
+          // of an integer the rounded sum may pick the neighbouring floor, and the clamp moves phi by < 1e-7
+          // (delta' (m - phi) is continuous from tap m at phi = 1 to tap m + 1 at phi = 0)
           int jodd;
-          float fj = floor_parity(x0f, jodd);  // floor and fraction of x0f are exact
-          float phi = (x0f - fj) + xd;          // fraction of x to ~1e-7 samples, renormalised to [0, 1)
-          if (phi < 0.f) { phi += 1.f; fj -= 1.f; }
-          else if (phi >= 1.f) { phi -= 1.f; fj += 1.f; }
+          const float fj = floor_parity(x0f + xd, jodd);
+          const float phi = fminf(fmaxf((x0f - fj) + xd, 0.f), 0.99999994f);
           const int p = (int)fj - pbase;
           if (p < 0 || p >= npos) continue;  // reaches no sample of this tile
           const float dzf = fmaf((float)nzo, Lzf, odd ? offOf : offEf);
