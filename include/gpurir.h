@@ -219,6 +219,12 @@ int gpurir_image_params(const float room_sz[3], const float beta[6], const float
  * cap >= 2 half + 1.  Returns half (>= 0) or -GPURIR_EINVAL. */
 long long gpurir_lut_table(double Tw, double fs, int Q, float* lut_out, long long cap);
 
+/* Polyphase expansion of Eq. 6 exactly as uploaded for GPURIR_POLY (reading R11): delta'(m - phi) ~=
+ * sum_{d<8} P[m - mlo][d] T_d(2 phi - 1), phi in [0, 1), for taps m = mlo .. mlo + ntaps - 1 (the last
+ * taps are zero padding to a multiple of 8).  Writes *mlo and, when P_out != NULL and cap >= 8 ntaps, the
+ * host float[ntaps][8] table.  Returns ntaps, or -GPURIR_EINVAL (Tw fs > 1022 or not positive). */
+int gpurir_poly_table(double Tw, double fs, int* mlo, float* P_out, long long cap);
+
 /* Read and (if reset) clear the current device's status word (see file header). Synchronises. */
 int gpurir_device_status(int reset);
 

@@ -21,7 +21,7 @@ EXPORTS = [
     "gpurir_opts_default", "gpurir_simulate_rir", "gpurir_simulate_rir_batch", "gpurir_nsamples",
     "gpurir_sabine_t60", "gpurir_beta_sabine", "gpurir_att2t_sabine", "gpurir_t2n", "gpurir_image_params",
     "gpurir_lut_table", "gpurir_device_status", "gpurir_strerror", "gpurir_last_cuda_error", "gpurir_version",
-    "gpurir_simulate_trajectory", "gpurir_simulate_rir_dir", "gpurir_beta_sabine_weighted",
+    "gpurir_simulate_trajectory", "gpurir_simulate_rir_dir", "gpurir_beta_sabine_weighted", "gpurir_poly_table",
 ]
 
 
@@ -86,6 +86,8 @@ def lib() -> C.CDLL:
     L.gpurir_image_params.restype = C.c_int
     L.gpurir_image_params.argtypes = [fp, fp, fp, fp, fp, C.c_int, fp, C.c_int, ip, C.c_double, C.c_double, vp, vp,
                                       vp]
+    L.gpurir_poly_table.restype = C.c_int
+    L.gpurir_poly_table.argtypes = [C.c_double, C.c_double, ip, fp, C.c_longlong]
     L.gpurir_lut_table.restype = C.c_longlong
     L.gpurir_lut_table.argtypes = [C.c_double, C.c_double, C.c_int, fp, C.c_longlong]
     L.gpurir_device_status.restype = C.c_int

@@ -223,6 +223,17 @@ def lut_table(Tw: float = 4e-3, fs: float = 16000.0, Q: int = 16) -> tuple[np.nd
     return np.array(list(buf), dtype=np.float32), half
 
 
+def poly_table(Tw: float = 4e-3, fs: float = 16000.0) -> tuple[np.ndarray, int]:
+    """gpurir_poly_table: the polyphase coefficients P [ntaps, 8] of GPURIR_POLY and the first tap m_lo (R11)."""
+    mlo = C.c_int(0)
+    n = int(lib().gpurir_poly_table(float(Tw), float(fs), C.byref(mlo), None, 0))
+    if n < 0:
+        raise GpurirError(-n, "gpurir_poly_table")
+    buf = (C.c_float * (8 * n))()
+    lib().gpurir_poly_table(float(Tw), float(fs), C.byref(mlo), buf, 8 * n)
+    return np.array(list(buf), dtype=np.float32).reshape(n, 8), int(mlo.value)
+
+
 def image_params(room_sz, beta, src, rcv, nb_img, fs, c=343.0, mic_pattern="omni", orv=None, device=None,
                  spkr_pattern="omni", ors=None):
     """gpurir_image_params: (delay in samples float64 [N], amplitude float32 [N]) in lattice order."""

@@ -174,21 +174,18 @@ double eq6_samples(double u, double H) {
   const double w = 0.5 * (1.0 + cos(M_PI * u / H));
   return w * (u == 0.0 ? 1.0 : sin(M_PI * u) / (M_PI * u));
 }
-const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t stream, int* err) {
-  *err = GPURIR_OK;
-  for (const PolyEntry& P : d->polys)
-    if (P.Tw == Tw && P.fs == fs) return &P;
+// Host fit of R11: taps m_lo .. m_lo + ntaps - 1 (ntaps padded to a multiple of 8 with zero taps), table in
+// the kernel's layout [channel pair q][tap mi][2].  Returns the padded tap count, or -EINVAL.
+int poly_fit(double Tw, double fs, int* mlo_out, std::vector<float>& tab) {
   const double H = Tw * fs / 2.0;
-  PolyEntry P;
-  P.Tw = Tw; P.fs = fs;
-  P.mlo = (int)floor(-H) + 1;
+  const int mlo = (int)floor(-H) + 1;
   const int mhi = (H == floor(H)) ? (int)H : (int)floor(H) + 1;
-  const int ntaps = mhi - P.mlo + 1;
-  P.ntaps = (ntaps + 7) & ~7;  // zero taps appended: the kernel's FIR runs in groups of 8 taps
-  if (ntaps < 1 || P.ntaps > kPolyMaxTaps) { *err = GPURIR_EINVAL; return nullptr; }
-  std::vector<float> tab((size_t)P.ntaps * kPolyDeg, 0.f);
+  const int ntaps = mhi - mlo + 1;
+  const int npad = (ntaps + 7) & ~7;  // zero taps appended: the kernel's FIR runs in groups of 8 taps
+  if (!(H > 0) || ntaps < 1 || npad > kPolyMaxTaps) return -GPURIR_EINVAL;
+  tab.assign((size_t)npad * kPolyDeg, 0.f);
   for (int mi = 0; mi < ntaps; mi++) {
-    const int m = P.mlo + mi;
+    const int m = mlo + mi;
     double c[kPolyDeg] = {0};
     for (int i = 0; i < kPolyNodes; i++) {
       const double th = M_PI * (i + 0.5) / kPolyNodes, y = cos(th), phi = 0.5 * (y + 1.0);
@@ -197,8 +194,21 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
     }
     // layout [channel pair q][tap mi][2]: the kernel's FIR group for pair q streams its taps contiguously
     for (int k = 0; k < kPolyDeg; k++)
-      tab[((size_t)(k >> 1) * P.ntaps + mi) * 2 + (k & 1)] = (float)(c[k] * (k ? 2.0 : 1.0) / kPolyNodes);
+      tab[((size_t)(k >> 1) * npad + mi) * 2 + (k & 1)] = (float)(c[k] * (k ? 2.0 : 1.0) / kPolyNodes);
   }
+  *mlo_out = mlo;
+  return npad;
+}
+
+const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t stream, int* err) {
+  *err = GPURIR_OK;
+  for (const PolyEntry& P : d->polys)
+    if (P.Tw == Tw && P.fs == fs) return &P;
+  PolyEntry P;
+  P.Tw = Tw; P.fs = fs;
+  std::vector<float> tab;
+  P.ntaps = poly_fit(Tw, fs, &P.mlo, tab);
+  if (P.ntaps < 0) { *err = GPURIR_EINVAL; return nullptr; }
   const size_t bytes = tab.size() * sizeof(float);
   cudaError_t e = cudaMalloc(&P.dev, bytes);
   if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMalloc(poly)"); return nullptr; }
@@ -434,6 +444,20 @@ int gpurir_t2n(double T, const float room_sz[3], double c, int nb_img_out[3]) {
     nb_img_out[i] = 2 * ((int)ceil(c * T / (double)room_sz[i]) + 1) + 1;
   }
   return GPURIR_OK;
+}
+
+int gpurir_poly_table(double Tw, double fs, int* mlo, float* P_out, long long cap) {
+  std::vector<float> tab;
+  int m0 = 0;
+  const int ntaps = poly_fit(Tw, fs, &m0, tab);
+  if (ntaps < 0) return ntaps;
+  if (mlo) *mlo = m0;
+  if (P_out) {
+    if (cap < (long long)ntaps * kPolyDeg) return -GPURIR_EINVAL;
+    for (int mi = 0; mi < ntaps; mi++)  // [tap][channel] for the caller
+      for (int k = 0; k < kPolyDeg; k++) P_out[(size_t)mi * kPolyDeg + k] = tab[((size_t)(k >> 1) * ntaps + mi) * 2 + (k & 1)];
+  }
+  return ntaps;
 }
 
 long long gpurir_lut_table(double Tw, double fs, int Q, float* lut_out, long long cap) {

@@ -132,3 +132,26 @@ def test_mode_validation_on_host(P):
     if not torch.cuda.is_available():
         assert _dir_call(P, 0, None, mode=3, Q=10) == 5
         assert _dir_call(P, 0, None, mode=1, Q=16) == 5
+
+
+@pytest.mark.parametrize("fs", [8000.0, 16000.0, 22050.0, 44100.0, 48000.0, 96000.0])
+def test_poly_table_reproduces_eq6(P, oracle, fs):
+    """Reading R11: the host's Chebyshev expansion (exactly the table GPURIR_POLY uploads) reproduces the
+    oracle's Eq. 6 windowed sinc at every integer tap and fractional delay to < 1e-6 of its peak; taps past
+    the open support are zero."""
+    Tw = 4e-3
+    tab, mlo = P.poly_table(Tw, fs)
+    rng = np.random.default_rng(int(fs))
+    phi = np.concatenate([rng.random(200), [0.0, 1e-7, 0.5, 1 - 6e-8]])
+    T = np.cos(np.arange(8)[:, None] * np.arccos(2 * phi - 1)[None, :])  # T_d(2 phi - 1)
+    approx = tab.astype(np.float64) @ T                                     # [tap, phi]
+    worst = 0.0
+    for mi in range(tab.shape[0]):
+        m = mlo + mi
+        exact = np.array([oracle.windowed_sinc((m - f) / fs, Tw, fs / 2) for f in phi])
+        worst = max(worst, float(np.max(np.abs(approx[mi] - exact))))
+    assert worst < 1e-6, worst
+    H = Tw * fs / 2
+    assert mlo == int(np.floor(-H)) + 1 and tab.shape[0] % 8 == 0
+    with pytest.raises(P.GpurirError):
+        P.poly_table(Tw, 300000.0)  # Tw fs > 1022 taps
