@@ -46,7 +46,8 @@ POLY_CHANNELS = 8
 
 
 def workload_name(mode="fp32"):
-    return f"cfg3_diffuse_M{M_PER_GPU}perGPU_T60_0.7_fs16k_cardioid_{mode}"
+    """The workload (BASELINE.json config 3, diffuse variant); the evaluation mode is a separate config key."""
+    return f"cfg3_diffuse_M{M_PER_GPU}perGPU_T60_0.7_fs16k_cardioid"
 
 
 def peaks():
