@@ -7,12 +7,15 @@
 //     delta'(m - phi) = sum_d P_d[m] T_d(2 phi - 1),   d = 0..7   (max error 4.3e-7, host fit),
 // the RIR becomes a fixed 8-channel FIR filter applied to per-sample image aggregates:
 //     h[k] = sum_m sum_d P_d[m] G_d[k - m],   G_d[j] = sum_{n: j_n = j} A_n T_d(2 phi_n - 1).
-// Per work item (RIR, 512-sample tile) a CTA
-//   1. enumerates the tile's shell of images column by column (as ism_ws_kernel) and adds each image's
-//      8 channel values into G in shared memory — as 64-bit fixed point with integer atomics, so the sums
-//      are exact and independent of the order the images arrive in (deterministic, shard-invariant);
-//   2. converts G to fp32 and runs the 8-channel FIR (2H taps) for its 512 outputs, one per thread,
-//      writing the tile once, coalesced.
+// Per work item (RIR, 1024-sample tile) a CTA of 512 threads
+//   1. enumerates the tile's shell of images column by column (as ism_ws_kernel; nonempty columns
+//      compacted by the candidate scan) and adds each image's 8 channel values into G in shared memory —
+//      as fixed point with integer reductions (one int32 word per channel, or two for dense calls), so the
+//      sums are exact and independent of the order the images arrive in (deterministic, shard-invariant);
+//      the fraction of the delay comes from the exact floor of the fp32 estimate plus its fp64 correction;
+//   2. converts G to fp32 in place and runs the 8-channel FIR (2H taps): 4 channel-pair groups x 128
+//      threads x 8 consecutive outputs with a sliding register window, partial sums meeting in shared
+//      memory; the tile is written once, coalesced.
 // Work per output sample no longer grows with the image density (690 in-window taps per sample at config
 // 3 (i)): the filter costs 2H x 8 MACs, the aggregation 8 channel updates per image.
 #include "ism_common.cuh"
