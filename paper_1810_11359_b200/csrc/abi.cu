@@ -193,7 +193,7 @@ int poly_fit(double Tw, double fs, int* mlo_out, std::vector<float>& tab) {
       for (int k = 0; k < kPolyDeg; k++) c[k] += fv * cos(k * th);  // T_k(y) = cos(k theta)
     }
     // layout [channel pair q][tap mi][2]: the kernel's FIR group for pair q streams its taps contiguously
-    for (int k = 0; k < kPolyDeg; k++)
+    for (int k = 0; k < kPolyChannels; k++)  // channels past kPolyChannels stay 0 (a shorter expansion)
       tab[((size_t)(k >> 1) * npad + mi) * 2 + (k & 1)] = (float)(c[k] * (k ? 2.0 : 1.0) / kPolyNodes);
   }
   *mlo_out = mlo;

@@ -96,7 +96,7 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int W, int p, float y
     atomicAdd(&Ga[p], __float_as_int(fmaf(as, 1.f, magic)) - 0x4B400000);
     atomicAdd(&Ga[W + p], __float_as_int(fmaf(as, y, magic)) - 0x4B400000);
 #pragma unroll
-    for (int d = 2; d < kPolyD; d++) {
+    for (int d = 2; d < kPolyChannels; d++) {
       const float t = fmaf(y2, tm1, -tm2);  // T_d = 2 y T_{d-1} - T_{d-2}
       atomicAdd(&Ga[d * W + p], __float_as_int(fmaf(as, t, magic)) - 0x4B400000);
       tm2 = tm1;
@@ -112,7 +112,7 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int W, int p, float y
 #pragma unroll
   for (int d = 2; d < kPolyD; d++) T[d] = fma(y2, T[d - 1], -T[d - 2]);  // T_d = 2 y T_{d-1} - T_{d-2}
 #pragma unroll
-  for (int d = 0; d < kPolyD; d++) {
+  for (int d = 0; d < kPolyChannels; d++) {
     const int v = __double2loint(fma(ad, T[d], magic));
     const int i = d * W + p;  // channel-major planes: consecutive positions are consecutive words
     atomicAdd(&Ga[i], v >> 14);
