@@ -11,8 +11,8 @@
 // chunks that never straddle a segment boundary, so each chunk uses one RIR, whose needed slice is
 // staged in shared memory (cp.async, double-buffered so the next chunk's loads overlap this chunk's
 // FMAs) with a 1-in-32 padding (conflict-free stride-16 reads).  Every thread keeps 16
-// consecutive outputs in registers and a sliding 16-tap window of the RIR, so each input sample costs one
-// shared load of the RIR, a quarter of a float4 broadcast load of the signal and 16 FFMA.
+// consecutive outputs in registers (paired for FFMA2) and a sliding 16-tap window of the RIR, so each input
+// sample costs one shared load of the RIR, a quarter of a float4 broadcast load of the signal and 8 FFMA2.
 #include <cooperative_groups.h>
 
 #include "kernels.h"
@@ -66,9 +66,9 @@ __global__ void __launch_bounds__(kCvThreads) traj_kernel(const float* __restric
   const int cs = (int)cluster.num_blocks();
   const int crank = (int)cluster.block_rank();
   const long long t0 = (long long)(blockIdx.x / cs) * kCvTile;
-  float acc[kCvPer];
+  float2 acc2[kCvPer / 2];  // outputs (i, i + 8) of this thread's 16
 #pragma unroll
-  for (int i = 0; i < kCvPer; i++) acc[i] = 0.f;
+  for (int i = 0; i < kCvPer / 2; i++) acc2[i] = make_float2(0.f, 0.f);
 
   // stage chunk c: its signal and the RIR slice tau in [t0 - jend + 1, t0 + kCvTile - 1 - jc]
   auto stage = [&](const CvChunk& c, int buf) {
@@ -117,10 +117,17 @@ __global__ void __launch_bounds__(kCvThreads) traj_kernel(const float* __restric
       const float* ss = s_sig[buf];
       const int n = (int)(cur.jend - cur.jc);
       const int e0 = kCvPer * tid;
-      // for a base b that is a multiple of 16 and u < 16, cv_pad(b + u) = cv_pad(b) + u: one address per step
-      float w[kCvPer];
+      // for a base b that is a multiple of 16 and u < 16, cv_pad(b + u) = cv_pad(b) + u: one address per step.
+      // Outputs pair up as (i, i + 8) in float2 accumulators so that one FFMA2 serves two outputs; the
+      // 16-tap sliding window is kept twice as register pairs, W2[k] = (w[k], w[k + 8]) and its swap
+      // W2s[k] = (w[k + 8], w[k]): the taps (w[a], w[a + 8 mod 16]) a pair needs are W2[a] or W2s[a - 8].
+      float2 W2[8], W2s[8];
 #pragma unroll
-      for (int i = 0; i < kCvPer; i++) w[i] = sr[cv_pad(e0) + i];
+      for (int k = 0; k < 8; k++) {
+        const float lo = sr[cv_pad(e0) + k], hi = sr[cv_pad(e0) + k + 8];
+        W2[k] = make_float2(lo, hi);
+        W2s[k] = make_float2(hi, lo);
+      }
       int d = 0;
       for (; d + kCvPer <= n; d += kCvPer) {
         const float* rp = sr + cv_pad(e0 + d + kCvPer);
@@ -130,23 +137,33 @@ __global__ void __launch_bounds__(kCvThreads) traj_kernel(const float* __restric
           const float sv[4] = {sv4.x, sv4.y, sv4.z, sv4.w};
 #pragma unroll
           for (int uu = 0; uu < 4; uu++) {
-            const int u = u4 + uu;  // window rotation is register renaming after unrolling
+            const int u = u4 + uu;  // all indices below are compile-time after unrolling
+            const float2 s2 = make_float2(sv[uu], sv[uu]);
 #pragma unroll
-            for (int i = 0; i < kCvPer; i++) acc[i] = fmaf(sv[uu], w[(i + u) % kCvPer], acc[i]);
-            w[u] = rp[u];
+            for (int i = 0; i < 8; i++) {
+              const int a = (i + u) & 15;
+              acc2[i] = __ffma2_rn(s2, a < 8 ? W2[a] : W2s[a - 8], acc2[i]);
+            }
+            const float v = rp[u];  // the tap entering window slot u
+            if (u < 8) { W2[u].x = v; W2s[u].y = v; } else { W2[u - 8].y = v; W2s[u - 8].x = v; }
           }
         }
       }
       for (; d < n; d++) {
         const float sv = ss[d];
 #pragma unroll
-        for (int i = 0; i < kCvPer; i++) acc[i] = fmaf(sv, sr[cv_pad(e0 + i + d)], acc[i]);
+        for (int i = 0; i < 8; i++)
+          acc2[i] = __ffma2_rn(make_float2(sv, sv), make_float2(sr[cv_pad(e0 + i + d)], sr[cv_pad(e0 + i + 8 + d)]),
+                               acc2[i]);
       }
       __syncthreads();  // buffer consumed before the next iteration stages into it
       if (!more) break;
       cur = nxt;
     }
   }
+  float acc[kCvPer];
+#pragma unroll
+  for (int i = 0; i < kCvPer / 2; i++) { acc[i] = acc2[i].x; acc[i + 8] = acc2[i].y; }
   float* o = out + (long long)m * n_out;
   if (cs == 1) {
 #pragma unroll
