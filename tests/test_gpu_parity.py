@@ -182,16 +182,18 @@ def _scene(**kw):
                                                                                       [2.9, 3.9, 2.4]])),  # M_src > 1
     dict(T60=0.05, clamp=True),                      # infeasible T60 clamped -> beta = 0, direct path only
 ])
-def test_edge_cases(P, oracle, kw):
+@pytest.mark.parametrize("mode,split", [("fp32", 0), ("fp32", -1), ("poly", -1)])
+def test_edge_cases(P, oracle, kw, mode, split):
+    """Edge cases through the cluster-split (auto) and persistent direct kernels and the polyphase kernel."""
     sc = _scene(**kw)
     beta, nb = derive(oracle, sc)
-    g = run_gpu(P, sc, beta, nb)
+    g = run_gpu(P, sc, beta, nb, mode=mode, split=split)
     r = run_oracle(oracle, sc, beta, nb)
     assert g.shape == r.shape
     if np.max(np.abs(r)) == 0:
         assert np.max(np.abs(g)) == 0
     else:
-        assert rel_err(g, r).max() <= TOL["fp32"]
+        assert rel_err(g, r).max() <= TOL[mode]
 
 
 def test_nb_img_one(P, oracle):
@@ -206,9 +208,11 @@ def test_degenerate_and_invalid(P):
     import torch
     room = np.float32([3, 4, 2.5])
     s = torch.tensor([[1.0, 1.0, 1.0]], device="cuda")
-    with pytest.raises(P.GpurirError) as e:
-        P.simulate_rir(room, [0.9] * 6, s, s.clone(), [3, 3, 3], 0.02, 0.02, 16000.0, sync=True)
-    assert e.value.status == 2
+    for mode, split in (("fp32", 0), ("fp32", -1), ("poly", -1)):  # every accumulation kernel flags d_n = 0
+        with pytest.raises(P.GpurirError) as e:
+            P.simulate_rir(room, [0.9] * 6, s, s.clone(), [3, 3, 3], 0.02, 0.02, 16000.0, mode=mode, split=split,
+                           sync=True)
+        assert e.value.status == 2
     with pytest.raises(P.GpurirError) as e:
         P.simulate_rir(room, [1.1] + [0.9] * 5, s, s + 0.5, [3, 3, 3], 0.02, 0.02, 16000.0)
     assert e.value.status == 1
