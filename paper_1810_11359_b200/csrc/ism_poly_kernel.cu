@@ -22,13 +22,19 @@
 
 namespace gpurir {
 
-constexpr int kPolyThreads = 512;
 constexpr int kPolyTC = kPolyTile;      // output samples per work item (the host planner's tile)
-constexpr int kPolyPasses = kPolyTC / 1024;  // FIR passes: 4 channel-pair groups x 128 threads x 8 outputs each
 constexpr int kPolyD = 8;               // Chebyshev channels T_0..T_7
-constexpr int kPolyCols = kPolyThreads; // lattice columns per enumeration batch
 constexpr int kPolyBz = 1024;           // z-factor table entries
-static_assert(kPolyTC % 1024 == 0 && kPolyThreads == 512, "FIR passes of 4 x 128 threads x 8 outputs");
+// CTA shape (template parameter THREADS, 512 or 256): 1024 / THREADS CTAs per SM at 64 registers per thread
+template <int THREADS> struct PolyCfg {
+  static constexpr int kThreads = THREADS;
+  static constexpr int kCtasPerSm = 1024 / THREADS;
+  static constexpr int kCols = THREADS;         // lattice columns per enumeration batch
+  static constexpr int kGroup = THREADS / 4;    // FIR threads per channel pair
+  static constexpr int kPass = 8 * kGroup;      // outputs per FIR pass (8 per thread)
+  static constexpr int kPasses = kPolyTC / kPass;
+  static_assert(kPolyTC % kPass == 0, "FIR passes of 4 channel-pair groups x 8 outputs per thread");
+};
 
 struct PolyColRec {  // 32 B, as WsColRec
   double rho2;
@@ -48,14 +54,16 @@ struct PolyTile {
   float invNX;
 };
 
+template <int THREADS>
 struct alignas(16) PolySmem {
   PolyTile ti;
-  alignas(16) PolyColRec col[kPolyCols];  // 16-B aligned: reused as float4 partial sums by the FIR
-  int colpre[kPolyCols];
-  int scan_tmp[kPolyThreads / 32];
+  alignas(16) PolyColRec col[THREADS];  // one lattice column per thread and batch
+  int colpre[THREADS];
+  int scan_tmp[THREADS / 32];
   float bz[kPolyBz];
 };
 
+template <int kPolyThreads>
 __device__ __forceinline__ int poly_block_scan(int v, int* tmp) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int x = warp_incl_scan(v, lane);
@@ -120,14 +128,19 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int W, int p, float y
   }
 }
 
-__global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, long long n_work, int* work_counter) {
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
+    ism_poly_kernel(IsmArgs A, long long n_work, int* work_counter) {
+  using C = PolyCfg<THREADS>;
+  constexpr int kPolyThreads = C::kThreads, kPolyCols = C::kCols, kPolyGroup = C::kGroup, kPolyPass = C::kPass,
+                kPolyPasses = C::kPasses;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PolySmem& sm = *reinterpret_cast<PolySmem*>(smem_raw);
+  PolySmem<THREADS>& sm = *reinterpret_cast<PolySmem<THREADS>*>(smem_raw);
   const int ntaps = A.poly_ntaps, npos = kPolyTC + ntaps - 1;
   // channel planes of W words, position p at p + p/8: the filter's lanes read positions 8 apart, which the
   // padding spreads over all banks (stride 9 words)
   const int W = npos + (npos >> 3) + 1;
-  int* Ga = reinterpret_cast<int*>(smem_raw + sizeof(PolySmem));  // coarse part of G (units 2^14)
+  int* Ga = reinterpret_cast<int*>(smem_raw + sizeof(PolySmem<THREADS>));  // coarse part of G (units 2^14)
   int* Gb = Ga + kPolyD * W;                                       // fine part of G (two-word calls only)
   float* Pt = reinterpret_cast<float*>(Gb + (A.poly_gb ? kPolyD * W : 0));        // [4 pairs][ntaps][2], mi = m - m_lo
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -253,7 +266,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
         }
         // one scan of (candidates + 2^20 x nonempty) both prefixes the candidates and compacts the nonempty
         // columns in order, so the run search and the walk below never visit an empty column
-        const int incl = poly_block_scan(cnt + (cnt > 0 ? (1 << 20) : 0), sm.scan_tmp);
+        const int incl = poly_block_scan<kPolyThreads>(cnt + (cnt > 0 ? (1 << 20) : 0), sm.scan_tmp);
         if (cnt > 0) {
           sm.col[(incl >> 20) - 1] = cr;
           sm.colpre[(incl >> 20) - 1] = incl & 0xFFFFF;
@@ -330,12 +343,12 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
     // ntaps is padded to a multiple of 8 with zero taps, so in every unrolled group of 8 taps the new
     // positions q - mi - 1 - u sit at fixed offsets 0 .. -6, -8 of one padded address (q = 7 mod 8).
     {
-      const int gq = tid >> 7, lt = tid & 127;
+      const int gq = tid / kPolyGroup, lt = tid % kPolyGroup;
       const float* G0 = Gf + (2 * gq) * W;  // channel 2 gq; channel 2 gq + 1 sits W words further
       float part[kPolyPasses][8];
 #pragma unroll
       for (int pass = 0; pass < kPolyPasses; pass++) {
-        const int t8 = pass * 1024 + 8 * lt;
+        const int t8 = pass * kPolyPass + 8 * lt;
         const float4* P4 = reinterpret_cast<const float4*>(Pt) + gq * (ntaps >> 1);  // pair gq: taps (2i, 2i+1)
         float2 acc[8], w[8];
         const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (m = m_lo)
@@ -364,7 +377,7 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
       float* red = Gf;
 #pragma unroll
       for (int pass = 0; pass < kPolyPasses; pass++) {
-        float4* r4 = reinterpret_cast<float4*>(red + gq * kPolyTC + pass * 1024 + 8 * lt);
+        float4* r4 = reinterpret_cast<float4*>(red + gq * kPolyTC + pass * kPolyPass + 8 * lt);
         r4[0] = make_float4(part[pass][0], part[pass][1], part[pass][2], part[pass][3]);
         r4[1] = make_float4(part[pass][4], part[pass][5], part[pass][6], part[pass][7]);
       }
@@ -384,22 +397,40 @@ __global__ void __launch_bounds__(kPolyThreads, 2) ism_poly_kernel(IsmArgs A, lo
   (void)lane; (void)warp;
 }
 
-size_t ism_poly_smem_bytes(int ntaps, bool two_word) {
+template <int THREADS>
+static size_t poly_smem_bytes(int ntaps, bool two_word) {
   const size_t npos = (size_t)kPolyTC + ntaps - 1;
   const size_t W = npos + (npos >> 3) + 1;
-  return sizeof(PolySmem) + (two_word ? 2 : 1) * kPolyD * W * sizeof(int) + (size_t)ntaps * kPolyD * sizeof(float);
+  return sizeof(PolySmem<THREADS>) + (two_word ? 2 : 1) * kPolyD * W * sizeof(int) +
+         (size_t)ntaps * kPolyD * sizeof(float);
 }
 
+size_t ism_poly_smem_bytes(int ntaps, bool two_word) { return poly_smem_bytes<512>(ntaps, two_word); }
+
+template <int THREADS>
+static cudaError_t launch_poly(const IsmArgs& A, long long n_work, int* counter, size_t smem, int num_sms,
+                               cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(ism_poly_kernel<THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long slots = (long long)PolyCfg<THREADS>::kCtasPerSm * num_sms;
+  const int grid = (int)(n_work < slots ? n_work : slots);
+  ism_poly_kernel<THREADS><<<grid, THREADS, smem, stream>>>(A, n_work, counter);
+  return cudaGetLastError();
+}
+
+// CTA shape: 256-thread CTAs (4 per SM) hide the phases' barriers better on large single-word calls (+7 % on
+// config 3 (i)), but need 4 x their shared memory per SM and leave work items short of threads on small
+// calls; 512-thread CTAs (2 per SM) everywhere else.  Both give bit-identical RIRs (exact integer
+// aggregation, the same per-output FIR arithmetic).
 cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
-  const size_t smem = ism_poly_smem_bytes(A.poly_ntaps, A.poly_gb != 0);
-  e = cudaFuncSetAttribute(ism_poly_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const long long slots = 2LL * num_sms;
-  const int grid = (int)(n_work < slots ? n_work : slots);
-  ism_poly_kernel<<<grid, kPolyThreads, smem, stream>>>(A, n_work, counter);
-  return cudaGetLastError();
+  const bool two_word = A.poly_gb != 0;
+  const size_t s256 = poly_smem_bytes<256>(A.poly_ntaps, two_word);
+  if (!two_word && 4 * s256 <= 224 * 1024 && n_work >= 16LL * num_sms)
+    return launch_poly<256>(A, n_work, counter, s256, num_sms, stream);
+  return launch_poly<512>(A, n_work, counter, poly_smem_bytes<512>(A.poly_ntaps, two_word), num_sms, stream);
 }
 
 }  // namespace gpurir

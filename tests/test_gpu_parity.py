@@ -540,3 +540,19 @@ def test_poly_small_calls_take_direct_kernel(P, oracle):
     c = run_gpu(P, sc, beta, nb, mode="poly", split=-1)
     assert not np.array_equal(a, c)
     assert rel_err(c, run_oracle(oracle, sc, beta, nb))[0] <= TOL["poly"]
+
+
+def test_poly_cta_shapes_bit_identical(P, oracle):
+    """A large call (256-thread CTAs) and its 8 shards (512-thread CTAs, too few work items for the small
+    shape) give bit-identical RIRs: the aggregation is exact and each output's FIR arithmetic is fixed."""
+    sc = W.cfg3(1024, "diffuse")
+    beta, nb = derive(oracle, sc)
+    full = run_gpu(P, sc, beta, nb, mode="poly")
+    parts = [run_gpu(P, sc, beta, nb, mode="poly", rir_index_base=128 * s, pos_rcv=sc.pos_rcv[128 * s:128 * (s + 1)],
+                     orv=sc.orV_rcv[128 * s:128 * (s + 1)]) for s in range(8)]
+    assert np.array_equal(full, np.concatenate(parts, axis=1))
+    idx = [0, 511, 1023]
+    for m in idx:
+        rj = oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[m:m + 1], nb, sc.Tdiff, sc.Tmax, fs=sc.fs,
+                                 pattern=sc.pattern, orV_rcv=sc.orV_rcv[m:m + 1], seed=sc.seed, rir_index_base=m)
+        assert rel_err(full[0, m], rj[0, 0])[0] <= TOL["poly"], m
