@@ -101,6 +101,7 @@ void gpurir_opts_default(gpurir_opts* opts);
  *                                    only when mic_pattern == GPURIR_OMNI
  *   nb_img   host  int[3]     images per axis N_x, N_y, N_z >= 1; lattice ceil(-N/2) <= n < ceil(N/2)
  *   Tdiff    ISM / diffuse switch time (s) >= 0; nISM = ceil(Tdiff fs) samples (reading C9)
+ *            (at most 2^22 - 8192, the range the kernels' fp32 delay floor is exact on; else EINVAL)
  *   Tmax     RIR length (s) > 0; nSamples = ceil(Tmax fs) (C9); Tdiff >= Tmax means ISM only
  *   fs, c    sampling rate (Hz) and speed of sound (m/s), > 0
  *   out      device float[M_src][M_rcv][nSamples], caller-owned, row-major RIR r = m_src*M_rcv + m_rcv

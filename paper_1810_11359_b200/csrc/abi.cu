@@ -497,7 +497,7 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
   long long nS = gpurir_nsamples(Tmax, fs);
   long long nISM = gpurir_nsamples(Tdiff, fs);
   if (nISM > nS) nISM = nS;
-  if (nS > (1LL << 30)) return GPURIR_EINVAL;
+  if (nS > (1LL << 30) || nISM > kMaxIsmSamples) return GPURIR_EINVAL;
   long long M = (long long)M_src * M_rcv;
   if (M > (1LL << 30)) return GPURIR_EINVAL;
 
@@ -614,7 +614,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     J.spkr_pattern = R.spkr_pattern;
     long long nS = gpurir_nsamples(R.Tmax, fs), nISM = gpurir_nsamples(R.Tdiff, fs);
     if (nISM > nS) nISM = nS;
-    if (nS > (1LL << 30)) return GPURIR_EINVAL;
+    if (nS > (1LL << 30) || nISM > kMaxIsmSamples) return GPURIR_EINVAL;
     J.nISM = (int)nISM; J.nS = (int)nS; J.out_offset = R.out_offset;
     double T60 = sabine(R.room_sz, R.beta);
     J.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);

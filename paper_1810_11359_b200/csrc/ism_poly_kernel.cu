@@ -36,7 +36,7 @@ template <int THREADS> struct PolyCfg {
   static_assert(kPolyTC % kPass == 0, "FIR passes of 4 channel-pair groups x 8 outputs per thread");
 };
 
-struct PolyColRec {  // 32 B, as WsColRec
+struct PolyColRec {  // 32 B, as WsColRec; lengths in samples (x fs / c)
   double rho2;
   float bxy, cdot;
   int r1lo, r2lo, r1n;
@@ -46,7 +46,9 @@ struct PolyColRec {  // 32 B, as WsColRec
 
 struct PolyTile {
   RirGeom g;
-  double dlo2, dhi2, invLz, offE, offO, inv_scale;
+  double dlo2, dhi2, invLz, inv_scale;
+  double Lzs, offEs, offOs;     // Eq. 1 along z in samples: Delta_z fs / c = n Lz fs / c + off (even / odd n)
+  float Lzsf, offEsf, offOsf;   // the same in fp32 (amplitude and gain only)
   float scalef;  // 2^(bits - e): a power of two, exact in fp32
   int two_word;
   long long row;
@@ -128,7 +130,13 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int W, int p, float y
   }
 }
 
-template <int THREADS>
+// Plane stride W (words) fixed at compile time for ntaps <= 64 (fs <= 16 kHz at T_w = 4 ms): the 8 channel
+// updates of an image and the FIR's paired-channel loads then address G with immediate offsets
+__host__ __device__ constexpr int poly_plane_words(int ntaps) { return (kPolyTC + ntaps - 1) + ((kPolyTC + ntaps - 1) >> 3) + 1; }
+constexpr int kPolyWFixTaps = 64;
+constexpr int kPolyWFix = poly_plane_words(kPolyWFixTaps);
+
+template <int THREADS, int WFIX>
 __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     ism_poly_kernel(IsmArgs A, long long n_work, int* work_counter) {
   using C = PolyCfg<THREADS>;
@@ -139,13 +147,13 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
   const int ntaps = A.poly_ntaps, npos = kPolyTC + ntaps - 1;
   // channel planes of W words, position p at p + p/8: the filter's lanes read positions 8 apart, which the
   // padding spreads over all banks (stride 9 words)
-  const int W = npos + (npos >> 3) + 1;
+  const int W = WFIX > 0 ? WFIX : poly_plane_words(ntaps);
   int* Ga = reinterpret_cast<int*>(smem_raw + sizeof(PolySmem<THREADS>));  // coarse part of G (units 2^14)
   int* Gb = Ga + kPolyD * W;                                       // fine part of G (two-word calls only)
   float* Pt = reinterpret_cast<float*>(Gb + (A.poly_gb ? kPolyD * W : 0));        // [4 pairs][ntaps][2], mi = m - m_lo
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double fs_over_c = A.fs_over_c, sc2 = fs_over_c * fs_over_c;
-  const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f;
+  const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f, fsc = (float)fs_over_c;
   const int m_hi = A.poly_mlo + ntaps - 1;
 
   for (int i = tid; i < ntaps * kPolyD; i += kPolyThreads) Pt[i] = A.poly_P[i];
@@ -187,8 +195,10 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         T.te = min(T.t0 + kPolyTC, nISM);
         T.tc = T.t0 + kPolyTC / 2;
         T.invLz = 1.0 / T.g.L[2];
-        T.offE = T.g.s[2] - T.g.r[2];
-        T.offO = -T.g.s[2] - T.g.r[2];
+        T.Lzs = T.g.L[2] * A.fs_over_c;
+        T.offEs = (T.g.s[2] - T.g.r[2]) * A.fs_over_c;
+        T.offOs = (-T.g.s[2] - T.g.r[2]) * A.fs_over_c;
+        T.Lzsf = (float)T.Lzs; T.offEsf = (float)T.offEs; T.offOsf = (float)T.offOs;
         // images with floor(x) in [t0 - m_hi, te - 1 - m_lo] reach samples [t0, te)
         const double xlo = (double)(T.t0 - m_hi), xhi = (double)(T.te - A.poly_mlo);
         const double dlo = xlo > 0.0 ? xlo * A.c_over_fs : 0.0, dhi = xhi * A.c_over_fs;
@@ -242,9 +252,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           const double dx = image_coord(nx, g.L[0], g.s[0]) - g.r[0];
           const double dy = image_coord(ny, g.L[1], g.s[1]) - g.r[1];
           const double rho2 = dx * dx + dy * dy;
-          cr.rho2 = rho2;
-          cr.cdot = (float)dx * g.o[0] + (float)dy * g.o[1];
-          cr.sdot = src_col_dot(nx, ny, (float)dx, (float)dy, g);
+          cr.rho2 = rho2 * sc2;
+          cr.cdot = ((float)dx * g.o[0] + (float)dy * g.o[1]) * fsc;
+          cr.sdot = src_col_dot(nx, ny, (float)dx, (float)dy, g) * fsc;
           uint32_t sgn = 0;
           bool zero = false;
           const float lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
@@ -285,11 +295,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         }
         int j = lo;
         int before = j > 0 ? sm.colpre[j - 1] : 0;
-        const double Lz = g.L[2], offE = T.offE, offO = T.offO;
-        const float Lzf = (float)Lz, offEf = (float)offE, offOf = (float)offO;
         const int zl = T.zl;
         const bool use_bz = T.use_bz, dir_src = g.as != 1.f, two_word = T.two_word;
-        const float oz = g.o[2], ga = g.a, fsc = (float)fs_over_c, scalef = T.scalef;
+        const float oz = g.o[2], ga = g.a, scalef = T.scalef;
         int boundary = sm.colpre[j];
         PolyColRec cr = sm.col[j];  // the current column's record, in registers: reloaded on a column change
         for (int gi = g0; gi < g1; gi++) {  // every lane runs R candidates: the walk keeps the warp converged
@@ -302,23 +310,24 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           const int odd = nz & 1;
           const float bz = use_bz ? sm.bz[min(max(nz - zl, 0), kPolyBz - 1)] : poly_z_factor(nz, g);
           const int nzo = nz + odd;
-          const double dz = fma(int_to_double(nzo), Lz, odd ? offO : offE);  // Eq. 1 along z
-          const double x2 = fma(dz, dz, cr.rho2) * sc2;                       // (d fs / c)^2
+          // Eq. 1 along z, in samples (the tile's constants are read from shared memory: no conversions here)
+          const double dz = fma(int_to_double(nzo), T.Lzs, odd ? T.offOs : T.offEs);
+          const double x2 = fma(dz, dz, cr.rho2);                             // (d fs / c)^2
           if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); continue; }
           float x0f, xd, rx;  // x = x0f + xd (xd the fp64 Newton correction); rx = 1/x
           delay_split(x2, x0f, xd, rx);
           // floor of the fp32 sum x0f + xd, fraction from the exact difference x0f - floor plus xd: within 1e-7
           // of an integer the rounded sum may pick the neighbouring floor, and the clamp moves phi by < 1e-7
           // (delta' (m - phi) is continuous from tap m at phi = 1 to tap m + 1 at phi = 0)
-          int jodd;
-          const float fj = floor_parity(x0f + xd, jodd);
+          int jfl;
+          const float fj = floor_int(x0f + xd, jfl);
           const float phi = fminf(fmaxf((x0f - fj) + xd, 0.f), 0.99999994f);
-          const int p = (int)fj - pbase;
+          const int p = jfl - pbase;
           if (p < 0 || p >= npos) continue;  // reaches no sample of this tile
-          const float dzf = fmaf((float)nzo, Lzf, odd ? offOf : offEf);
-          const float cth = fmaf(dzf, oz, cr.cdot) * (fsc * rx);
+          const float dzf = fmaf((float)nzo, T.Lzsf, odd ? T.offOsf : T.offEsf);
+          const float cth = fmaf(dzf, oz, cr.cdot) * rx;
           float gain = ga + (1.f - ga) * cth;
-          if (dir_src) gain *= src_gain(cr.sdot, odd, dzf, fsc * rx, g);
+          if (dir_src) gain *= src_gain(cr.sdot, odd, dzf, rx, g);
           const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
           const float y = fmaf(2.f, phi, -1.f);            // 2 phi - 1 in [-1, 1)
           poly_add(Ga, Gb, W, p + (p >> 3), y, amp, scalef, two_word);
@@ -397,26 +406,33 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
   (void)lane; (void)warp;
 }
 
+static int poly_w(int ntaps) { return ntaps <= kPolyWFixTaps ? kPolyWFix : poly_plane_words(ntaps); }
+
 template <int THREADS>
 static size_t poly_smem_bytes(int ntaps, bool two_word) {
-  const size_t npos = (size_t)kPolyTC + ntaps - 1;
-  const size_t W = npos + (npos >> 3) + 1;
+  const size_t W = (size_t)poly_w(ntaps);
   return sizeof(PolySmem<THREADS>) + (two_word ? 2 : 1) * kPolyD * W * sizeof(int) +
          (size_t)ntaps * kPolyD * sizeof(float);
 }
 
 size_t ism_poly_smem_bytes(int ntaps, bool two_word) { return poly_smem_bytes<512>(ntaps, two_word); }
 
-template <int THREADS>
-static cudaError_t launch_poly(const IsmArgs& A, long long n_work, int* counter, size_t smem, int num_sms,
-                               cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(ism_poly_kernel<THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+template <int THREADS, int WFIX>
+static cudaError_t launch_poly_w(const IsmArgs& A, long long n_work, int* counter, size_t smem, int num_sms,
+                                 cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(ism_poly_kernel<THREADS, WFIX>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long slots = (long long)PolyCfg<THREADS>::kCtasPerSm * num_sms;
   const int grid = (int)(n_work < slots ? n_work : slots);
-  ism_poly_kernel<THREADS><<<grid, THREADS, smem, stream>>>(A, n_work, counter);
+  ism_poly_kernel<THREADS, WFIX><<<grid, THREADS, smem, stream>>>(A, n_work, counter);
   return cudaGetLastError();
+}
+template <int THREADS>
+static cudaError_t launch_poly(const IsmArgs& A, long long n_work, int* counter, size_t smem, int num_sms,
+                               cudaStream_t stream) {
+  return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_w<THREADS, kPolyWFix>(A, n_work, counter, smem, num_sms, stream)
+                                       : launch_poly_w<THREADS, 0>(A, n_work, counter, smem, num_sms, stream);
 }
 
 // CTA shape: 256-thread CTAs (4 per SM) hide the phases' barriers better on large single-word calls (+7 % on
