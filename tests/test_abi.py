@@ -102,7 +102,7 @@ def test_weighted_beta_matches_oracle(P, oracle):
         P.beta_sabine_weighted([3, 4, 2.5], 0.5, [0.0] * 6)
 
 
-def _dir_call(P, spkr, ors, mode=0, Q=16, buf=None):
+def _dir_call(P, spkr, ors, mode=0, Q=16, buf=None, Tdiff=0.01, Tmax=0.01, fs=16000.0):
     """gpurir_simulate_rir_dir with dummy (never dereferenced on a rejected call) device pointers."""
     L = P._lib.lib()
     f3 = (ctypes.c_float * 3)(3.0, 4.0, 2.5)
@@ -112,7 +112,7 @@ def _dir_call(P, spkr, ors, mode=0, Q=16, buf=None):
     L.gpurir_opts_default(ctypes.byref(o))
     o.mode, o.lut_Q = mode, Q
     dummy = ctypes.c_void_p(16)
-    return L.gpurir_simulate_rir_dir(f3, b6, dummy, 1, ors, spkr, dummy, 1, None, 0, nb, 0.01, 0.01, 16000.0,
+    return L.gpurir_simulate_rir_dir(f3, b6, dummy, 1, ors, spkr, dummy, 1, None, 0, nb, Tdiff, Tmax, fs,
                                      343.0, dummy, ctypes.byref(o))
 
 
@@ -132,6 +132,17 @@ def test_mode_validation_on_host(P):
     if not torch.cuda.is_available():
         assert _dir_call(P, 0, None, mode=3, Q=10) == 5
         assert _dir_call(P, 0, None, mode=1, Q=16) == 5
+
+
+def test_ism_length_cap(P):
+    """The kernels floor delays in fp32 with the 1.5 2^23 magic, exact below 2^22 samples: an ISM part
+    longer than 2^22 - 8192 samples (87 s at 48 kHz) is EINVAL on the host, for every mode; the diffuse
+    tail has no such limit."""
+    import torch
+    for mode in (0, 4):
+        assert _dir_call(P, 0, None, mode=mode, Tdiff=90.0, Tmax=90.0, fs=48000.0) == 1
+        if not torch.cuda.is_available():  # passes host validation, then needs the device
+            assert _dir_call(P, 0, None, mode=mode, Tdiff=80.0, Tmax=200.0, fs=48000.0) == 5
 
 
 @pytest.mark.parametrize("fs", [8000.0, 16000.0, 22050.0, 44100.0, 48000.0, 96000.0])
