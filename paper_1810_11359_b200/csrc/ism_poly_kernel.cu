@@ -49,7 +49,8 @@ struct PolyTile {
   double dlo2, dhi2, invLz, inv_scale;
   double Lzs, offEs, offOs;     // Eq. 1 along z in samples: Delta_z fs / c = n Lz fs / c + off (even / odd n)
   float Lzsf, offEsf, offOsf;   // the same in fp32 (amplitude and gain only)
-  float scalef;  // 2^(bits - e): a power of two, exact in fp32
+  float scalef;      // 2^(bits - e): a power of two, exact in fp32
+  float inv_scalef;  // 2^(e - bits), the same as inv_scale
   int two_word;
   long long row;
   int t0, te, tc, nx0, ny0, NX, ncols, zl, zh, use_bz, next;
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         if (bits <= 0) bits = 28;
         T.scalef = ldexpf(1.f, bits - e);
         T.inv_scale = ldexp(1.0, e - bits);
+        T.inv_scalef = ldexpf(1.f, e - bits);
       }
     }
     __syncthreads();
@@ -341,8 +343,13 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     if (T.two_word) {
       for (int i = tid; i < kPolyD * W; i += kPolyThreads)
         Gf[i] = (float)((double)((long long)Ga[i] * 16384 + Gb[i]) * T.inv_scale);
-    } else {  // single word: |sum| < 2^30 converts exactly; inv_scale is a power of two
-      for (int i = tid; i < kPolyD * W; i += kPolyThreads) Gf[i] = (float)((double)Ga[i] * T.inv_scale);
+    } else {  // single word, |sum| < 2^31: one rounding to fp32 (I2FP, ALU pipe), then an exact power-of-two scale
+      const float is = T.inv_scalef;
+      for (int i = tid; i < (kPolyD * W) >> 2; i += kPolyThreads) {
+        const int4 v = reinterpret_cast<const int4*>(Ga)[i];
+        reinterpret_cast<float4*>(Gf)[i] =
+            make_float4((float)v.x * is, (float)v.y * is, (float)v.z * is, (float)v.w * is);
+      }
     }
     __syncthreads();
 
