@@ -48,7 +48,6 @@ struct PolyTile {
   RirGeom g;
   double dlo2, dhi2, invLz, inv_scale;
   double Lzs, offEs, offOs;     // Eq. 1 along z in samples: Delta_z fs / c = n Lz fs / c + off (even / odd n)
-  float Lzsf, offEsf, offOsf;   // the same in fp32 (amplitude and gain only)
   float scalef;      // 2^(bits - e): a power of two, exact in fp32
   float inv_scalef;  // 2^(e - bits), the same as inv_scale
   int two_word;
@@ -199,7 +198,6 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         T.Lzs = T.g.L[2] * A.fs_over_c;
         T.offEs = (T.g.s[2] - T.g.r[2]) * A.fs_over_c;
         T.offOs = (-T.g.s[2] - T.g.r[2]) * A.fs_over_c;
-        T.Lzsf = (float)T.Lzs; T.offEsf = (float)T.offEs; T.offOsf = (float)T.offOs;
         // images with floor(x) in [t0 - m_hi, te - 1 - m_lo] reach samples [t0, te)
         const double xlo = (double)(T.t0 - m_hi), xhi = (double)(T.te - A.poly_mlo);
         const double dlo = xlo > 0.0 ? xlo * A.c_over_fs : 0.0, dhi = xhi * A.c_over_fs;
@@ -326,7 +324,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           const float phi = fminf(fmaxf((x0f - fj) + xd, 0.f), 0.99999994f);
           const int p = jfl - pbase;
           if (p < 0 || p >= npos) continue;  // reaches no sample of this tile
-          const float dzf = fmaf((float)nzo, T.Lzsf, odd ? T.offOsf : T.offEsf);
+          const float dzf = (float)dz;  // one XU conversion instead of shared-memory loads (the smem pipe binds)
           const float cth = fmaf(dzf, oz, cr.cdot) * rx;
           float gain = ga + (1.f - ga) * cth;
           if (dir_src) gain *= src_gain(cr.sdot, odd, dzf, rx, g);
