@@ -238,6 +238,14 @@ def run_reference_trajectory(args):
     print(json.dumps(line), flush=True)
 
 
+def cfg3_config(mode, sc, beta, nb, nS, nISM):
+    """The bench line's config for the cfg3 workload (both arms print the same dict)."""
+    return {"workload": workload_name(mode), "M_per_gpu": M_PER_GPU, "room": [3, 4, 2.5], "T60": 0.7,
+            "beta": float(beta[0]), "nb_img": [int(v) for v in nb], "fs": sc.fs, "Tdiff": sc.Tdiff,
+            "Tmax": sc.Tmax, "pattern": "cardioid", "mode": mode, "nSamples": nS, "nISM": nISM,
+            "l2": "256 MB buffer written between timed steps (L2 126 MB); step output 734 MB"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -271,8 +279,9 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "RIRs/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name("fp32"), "reference_arm": "CPU oracle (oracle/oracle.c), each step "
-                       f"{per_step} receivers of the workload"},
+            "config": dict(cfg3_config(args.mode, sc, beta, nb, oracle.nsamples(sc.Tmax, sc.fs),
+                                       oracle.nsamples(sc.Tdiff, sc.fs)),
+                           reference_arm=f"CPU oracle (oracle/oracle.c), each step {per_step} receivers of the workload"),
             "cpu_baseline": {"value": value, "unit": "RIRs/s", "cores": cores, "kind": "oracle",
                              "sample": f"{per_step} RIRs per step x {args.steps} steps"},
             "e2e": {"value": value, "unit": "RIRs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -476,10 +485,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "RIRs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if args.mode != "fp16" else "f16x2-taps/f32-acc", "data": "synthetic",
-        "config": {"workload": workload_name(args.mode), "M_per_gpu": M_PER_GPU, "room": [3, 4, 2.5], "T60": 0.7,
-                   "beta": float(beta[0]), "nb_img": [int(v) for v in nb], "fs": sc.fs, "Tdiff": sc.Tdiff,
-                   "Tmax": sc.Tmax, "pattern": "cardioid", "mode": args.mode, "nSamples": nS, "nISM": nISM,
-                   "l2": "256 MB buffer written between timed steps (L2 126 MB); step output 734 MB"},
+        "config": cfg3_config(args.mode, sc, beta, nb, nS, nISM),
         "image_contributions_per_s": value * lattice,
         "taps_per_s": world * taps_launch / ism_avg_s if world == 1 else None,
         "ism_ms": float(np.mean(ism_ms)),
