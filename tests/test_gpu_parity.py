@@ -136,17 +136,39 @@ def test_cfg3_subset(P, oracle, mode, kernel):
     assert rel_err(g, r).max() <= TOL[mode]
 
 
-def test_cfg3_full_size_sampled(P, oracle):
-    """M = 16384 in the bench launch configuration; 6 sampled RIRs re-computed by the oracle."""
+@pytest.mark.parametrize("mode", ["poly", "fp32"])
+def test_cfg3_full_size_sampled(P, oracle, mode):
+    """M = 16384 in the bench launch configuration (poly: the bench's path, 256-thread CTAs, fixed plane
+    stride; fp32: the direct kernel beside it); 6 sampled RIRs re-computed by the oracle."""
     sc = W.cfg3(16384, "diffuse")
     beta, nb = derive(oracle, sc)
-    g = run_gpu(P, sc, beta, nb)
+    g = run_gpu(P, sc, beta, nb, mode=mode)
     assert np.all(np.isfinite(g))
     idx = [0, 1, 4097, 8191, 12345, 16383]
     for m in idx:  # each sampled RIR with its own global tail stream id
         rj = oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[m:m + 1], nb, sc.Tdiff, sc.Tmax, fs=sc.fs,
                                  pattern=sc.pattern, orV_rcv=sc.orV_rcv[m:m + 1], seed=sc.seed, rir_index_base=m)
-        assert rel_err(g[0, m], rj[0, 0])[0] <= TOL["fp32"], m
+        assert rel_err(g[0, m], rj[0, 0])[0] <= TOL[mode], m
+
+
+def test_cfg3_full_size_poly_vs_direct_all_rirs(P, oracle):
+    """Every one of the bench's 16384 RIRs: the polyphase path (bench default) within the fp32 tolerance of each
+    RIR's peak of the direct fp32 kernel (itself pinned to the oracle above) — a property that holds at any
+    size, so it covers the outputs the sampled oracle comparison does not.  Compared on the device.  Measured:
+    max 5.6e-5, 99.9 % of RIRs below 2.8e-5; on the worst RIR (5590) the difference is the direct kernel's own
+    error (5.6e-5 vs the oracle, degree-3 window polynomial R5) while poly is 2.5e-6 from the oracle
+    (tools/diag_poly_vs_direct.py)."""
+    import torch
+    sc = W.cfg3(16384, "diffuse")
+    beta, nb = derive(oracle, sc)
+    src = torch.from_numpy(np.ascontiguousarray(sc.pos_src)).cuda()
+    rcv = torch.from_numpy(np.ascontiguousarray(sc.pos_rcv)).cuda()
+    ov = torch.from_numpy(np.ascontiguousarray(sc.orV_rcv)).cuda()
+    kw = dict(c=sc.c, orV_rcv=ov, mic_pattern=sc.pattern, seed=sc.seed, sync=True)
+    a = P.simulate_rir(sc.room, beta, src, rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, mode="poly", **kw)[0]
+    b = P.simulate_rir(sc.room, beta, src, rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, mode="fp32", **kw)[0]
+    err = ((a - b).abs().amax(dim=1) / b.abs().amax(dim=1)).cpu().numpy()
+    assert np.all(np.isfinite(err)) and err.max() <= TOL["poly"], (err.max(), int(err.argmax()))
 
 
 @pytest.mark.parametrize("kernel", ["auto", "persistent"])
