@@ -128,6 +128,26 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
                             const float* orV_rcv, int mic_pattern, const int nb_img[3], double Tdiff, double Tmax,
                             double fs, double c, float* out, const gpurir_opts* opts);
 
+/*
+ * gpurir_simulate_rir_host — gpurir_simulate_rir_dir from HOST memory: the end-to-end call of a
+ * dataset-generation loop (P:274's interface with the host<->device transfers inside; the paper's memcpy
+ * step).  pos_src, orV_src, pos_rcv, orV_rcv and out have the layouts of gpurir_simulate_rir_dir
+ * but are host pointers; page-locked (pinned) memory lets the copies run asynchronously, pageable memory
+ * works but its copies are staged by the driver.  The call copies the positions to the device, then
+ * computes the RIRs in chunks of whole rows (receiver ranges of one source, or groups of whole sources
+ * when M_rcv is small) into two device buffers on opts->stream while a second stream copies the previous
+ * chunk back into out, so the device->host transfer overlaps the kernels.  Every chunk keeps its global RIR
+ * index (tail RNG stream, reading C16): the result equals one device call over all RIRs (bit-identical in
+ * GPURIR_POLY mode, which is shard-invariant).  Device scratch (2 chunk outputs + positions) comes from the
+ * stream-ordered allocator and is released before return.  Synchronous: returns when out is filled (the
+ * status word is checked as with GPURIR_FLAG_SYNC).  opts->ev_ism / ev_tail are ignored.
+ * Errors: as gpurir_simulate_rir_dir; ENOMEM when the scratch cannot be allocated; ECUDA on copy failure.
+ */
+int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const float* pos_src, int M_src,
+                             const float* orV_src, int spkr_pattern, const float* pos_rcv, int M_rcv,
+                             const float* orV_rcv, int mic_pattern, const int nb_img[3], double Tdiff,
+                             double Tmax, double fs, double c, float* out, const gpurir_opts* opts);
+
 /* One independent room of a batch (config 5; a deviation from the paper's
  * same-room-only batching).  out_offset = element offset of this RIR's
  * row in the batch output buffer (ragged rows of ceil(Tmax fs) samples). */

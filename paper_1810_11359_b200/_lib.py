@@ -22,6 +22,7 @@ EXPORTS = [
     "gpurir_sabine_t60", "gpurir_beta_sabine", "gpurir_att2t_sabine", "gpurir_t2n", "gpurir_image_params",
     "gpurir_lut_table", "gpurir_device_status", "gpurir_strerror", "gpurir_last_cuda_error", "gpurir_version",
     "gpurir_simulate_trajectory", "gpurir_simulate_rir_dir", "gpurir_beta_sabine_weighted", "gpurir_poly_table",
+    "gpurir_simulate_rir_host",
 ]
 
 
@@ -67,6 +68,9 @@ def lib() -> C.CDLL:
     L.gpurir_simulate_rir_dir.restype = C.c_int
     L.gpurir_simulate_rir_dir.argtypes = [fp, fp, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, ip, C.c_double,
                                           C.c_double, C.c_double, C.c_double, vp, C.POINTER(Opts)]
+    L.gpurir_simulate_rir_host.restype = C.c_int
+    L.gpurir_simulate_rir_host.argtypes = [fp, fp, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, ip, C.c_double,
+                                           C.c_double, C.c_double, C.c_double, vp, C.POINTER(Opts)]
     L.gpurir_beta_sabine_weighted.restype = C.c_int
     L.gpurir_beta_sabine_weighted.argtypes = [fp, C.c_double, fp, C.c_int, C.c_int, fp, ip]
     L.gpurir_simulate_rir_batch.restype = C.c_int

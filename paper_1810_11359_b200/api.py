@@ -120,6 +120,54 @@ def simulate_rir(room_sz, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs, c=343
     return out
 
 
+def _host_f32(x, name, rows=False):
+    """A host float32 C-contiguous buffer (numpy array or CPU torch tensor, pinned or not) and its pointer."""
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            if x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous float32 CPU tensor")
+            if rows and (x.dim() != 2 or x.shape[1] != 3):
+                raise ValueError(f"{name} must have shape [M, 3]")
+            return x, x.data_ptr()
+    except ImportError:
+        pass
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    if rows and (a.ndim != 2 or a.shape[1] != 3):
+        raise ValueError(f"{name} must have shape [M, 3]")
+    return a, a.ctypes.data
+
+
+def simulate_rir_host(room_sz, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs, c=343.0, orV_rcv=None,
+                      mic_pattern="omni", mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0, out=None,
+                      stream=None, split=0, orV_src=None, spkr_pattern="omni"):
+    """gpurir_simulate_rir_host: simulate_rir from host memory, host<->device copies inside the call.
+
+    pos_src / pos_rcv / orV_* are host [M,3] float32 arrays (numpy or CPU tensors; pinned tensors let the
+    copies overlap the kernels); `out` (optional) a host float32 buffer of M_src*M_rcv*nSamples elements —
+    a numpy array is allocated if omitted.  Synchronous: returns `out` filled, shape [M_src, M_rcv, nS].
+    """
+    src, p_src = _host_f32(pos_src, "pos_src", rows=True)
+    rcv, p_rcv = _host_f32(pos_rcv, "pos_rcv", rows=True)
+    orv, p_orv = _host_f32(orV_rcv, "orV_rcv", rows=True) if orV_rcv is not None else (None, None)
+    ors, p_ors = _host_f32(orV_src, "orV_src", rows=True) if orV_src is not None else (None, None)
+    Ms, Mr = src.shape[0], rcv.shape[0]
+    nS = nsamples(Tmax, fs)
+    if out is None:
+        out = np.empty((Ms, Mr, nS), dtype=np.float32)
+    hold, p_out = _host_f32(out, "out")
+    if (hold.numel() if hasattr(hold, "numel") else hold.size) < Ms * Mr * nS:
+        raise ValueError("out must hold M_src*M_rcv*nSamples float32 elements")
+    if hold is not out:
+        raise ValueError("out must be a contiguous float32 host buffer")
+    o = make_opts(mode, Tw, lut_Q, seed, rir_index_base, stream, split, False)
+    st = lib().gpurir_simulate_rir_host(_f3(room_sz), _f3(beta, 6), p_src, Ms, p_ors, _pattern(spkr_pattern), p_rcv,
+                                        Mr, p_orv, _pattern(mic_pattern), _i3(nb_img), float(Tdiff), float(Tmax),
+                                        float(fs), float(c), p_out, C.byref(o))
+    check(st, "gpurir_simulate_rir_host")
+    return out
+
+
 def room_array(rooms) -> C.Array:
     """Build a gpurir_room[n] array from a sequence of dicts with the struct's field names."""
     arr = (Room * len(rooms))()

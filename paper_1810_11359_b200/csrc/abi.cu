@@ -55,6 +55,7 @@ struct DeviceState {
   std::vector<TexEntry> texs;
   std::vector<PolyEntry> polys;
   int* work_counter = nullptr;  // persistent-kernel work-queue heads, one per call in flight (ring)
+  cudaStream_t copy_stream = nullptr;  // device->host stream of gpurir_simulate_rir_host
   unsigned next_counter = 0;
   int num_sms = 0;
 };
@@ -223,6 +224,7 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
 // volume V, so about 4 pi d^2 (c / fs) / V images share one integer sample position at distance d.  With twice
 // that at the farthest ISM delay (+16) as the bound N, single-word accumulation with bits = 22 is used when
 // 2^22 N <= 2^30 (N <= 256); otherwise 0 selects the two-word scheme (2^28 resolution).
+constexpr long long kHostChunkMin = 2048;  // RIRs per chunk of gpurir_simulate_rir_host (fills the GPU)
 constexpr long long kPolyMinItems = 32;  // smaller polyphase calls take the direct fp32 kernels
 
 int poly_bits_for(const float L[3], long long nISM, double fs, double c, double Tw) {
@@ -575,6 +577,100 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     if (o.ev_tail[1]) cudaEventRecord((cudaEvent_t)o.ev_tail[1], stream);
   }
   return finish(o, stream, d);
+}
+
+int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const float* pos_src, int M_src,
+                             const float* orV_src, int spkr_pattern, const float* pos_rcv, int M_rcv,
+                             const float* orV_rcv, int mic_pattern, const int nb_img[3], double Tdiff, double Tmax,
+                             double fs, double c, float* out, const gpurir_opts* opts) {
+  gpurir_opts o;
+  if (opts) o = *opts; else gpurir_opts_default(&o);
+  if (M_src <= 0 || M_rcv <= 0 || !pos_src || !pos_rcv || !out) return GPURIR_EINVAL;
+  if (!(fs > 0) || !(c > 0) || !(Tmax > 0) || !(Tdiff >= 0)) return GPURIR_EINVAL;
+  if (mic_pattern != GPURIR_OMNI && !orV_rcv) return GPURIR_EINVAL;
+  if (spkr_pattern < 0 || spkr_pattern > 4 || (spkr_pattern != GPURIR_OMNI && !orV_src)) return GPURIR_EINVAL;
+  const long long nS = gpurir_nsamples(Tmax, fs);
+  if (nS > (1LL << 30) || (long long)M_src * M_rcv > (1LL << 30)) return GPURIR_EINVAL;
+  int st = GPURIR_OK;
+  DeviceState* d = device_state(&st);
+  if (!d) return st;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!d->copy_stream) {
+      cudaError_t e = cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate(copy)");
+    }
+  }
+  cudaStream_t cs = (cudaStream_t)o.stream, xs = d->copy_stream;
+  // chunks of whole output rows: a receiver range of one source, or whole sources when M_rcv is small
+  const long long chunk_target = std::max<long long>(kHostChunkMin, ((long long)M_src * M_rcv + 7) / 8);
+  const bool by_rcv = M_rcv >= chunk_target;
+  const int rcv_chunk = by_rcv ? (int)chunk_target : M_rcv;
+  const int src_chunk = by_rcv ? 1 : (int)std::max<long long>(1, chunk_target / M_rcv);
+  const size_t rows = (size_t)src_chunk * rcv_chunk;
+  const size_t in_bytes = ((size_t)M_src * (orV_src ? 6 : 3) + (size_t)M_rcv * (orV_rcv ? 6 : 3)) * sizeof(float);
+  const size_t buf_bytes = rows * (size_t)nS * sizeof(float);
+  char* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&scratch, in_bytes + 2 * buf_bytes + 256, cs);
+  if (e != cudaSuccess) { cudaGetLastError(); return GPURIR_ENOMEM; }
+  float* d_src = reinterpret_cast<float*>(scratch);
+  float* d_ors = orV_src ? d_src + 3 * (size_t)M_src : nullptr;
+  float* d_rcv = d_src + (orV_src ? 6 : 3) * (size_t)M_src;
+  float* d_orv = orV_rcv ? d_rcv + 3 * (size_t)M_rcv : nullptr;
+  float* d_buf[2];
+  d_buf[0] = reinterpret_cast<float*>(scratch + ((in_bytes + 255) & ~(size_t)255));
+  d_buf[1] = d_buf[0] + rows * (size_t)nS;
+  cudaEvent_t computed[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+  for (int b = 0; b < 2 && e == cudaSuccess; b++) {
+    e = cudaEventCreateWithFlags(&computed[b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_src, pos_src, 3 * sizeof(float) * M_src, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess && orV_src)
+    e = cudaMemcpyAsync(d_ors, orV_src, 3 * sizeof(float) * M_src, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_rcv, pos_rcv, 3 * sizeof(float) * M_rcv, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess && orV_rcv)
+    e = cudaMemcpyAsync(d_orv, orV_rcv, 3 * sizeof(float) * M_rcv, cudaMemcpyHostToDevice, cs);
+  if (e != cudaSuccess) st = cuda_fail(e, "host call setup");
+  gpurir_opts sub = o;
+  sub.stream = cs;
+  sub.flags &= ~GPURIR_FLAG_SYNC;
+  sub.ev_ism[0] = sub.ev_ism[1] = sub.ev_tail[0] = sub.ev_tail[1] = nullptr;
+  long long k = 0;
+  for (int s0 = 0; s0 < M_src && st == GPURIR_OK; s0 += src_chunk) {
+    const int ns = std::min(src_chunk, M_src - s0);
+    for (int r0 = 0; r0 < M_rcv && st == GPURIR_OK; r0 += rcv_chunk, k++) {
+      const int nr = std::min(rcv_chunk, M_rcv - r0);
+      const int b = (int)(k & 1);
+      if (k >= 2) cudaStreamWaitEvent(cs, copied[b], 0);  // d_buf[b] is free once chunk k-2 is on the host
+      const long long row0 = (long long)s0 * M_rcv + r0;  // global index of the chunk's first RIR
+      sub.rir_index_base = o.rir_index_base + (uint64_t)row0;
+      st = gpurir_simulate_rir_dir(room_sz, beta, d_src + 3 * (size_t)s0, ns, d_ors ? d_ors + 3 * (size_t)s0 : nullptr,
+                                   spkr_pattern, d_rcv + 3 * (size_t)r0, nr, d_orv ? d_orv + 3 * (size_t)r0 : nullptr,
+                                   mic_pattern, nb_img, Tdiff, Tmax, fs, c, d_buf[b], &sub);
+      if (st != GPURIR_OK) break;
+      e = cudaEventRecord(computed[b], cs);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(xs, computed[b], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out + row0 * nS, d_buf[b], (size_t)ns * nr * nS * sizeof(float), cudaMemcpyDeviceToHost, xs);
+      if (e == cudaSuccess) e = cudaEventRecord(copied[b], xs);
+      if (e != cudaSuccess) st = cuda_fail(e, "host call chunk");
+    }
+  }
+  // the scratch is released in stream order after the last copy; the call returns when out is filled
+  for (int b = 0; b < 2; b++)
+    if (copied[b] && k > b) cudaStreamWaitEvent(cs, copied[b], 0);
+  cudaFreeAsync(scratch, cs);
+  e = cudaStreamSynchronize(cs);
+  for (int b = 0; b < 2; b++) {
+    if (computed[b]) cudaEventDestroy(computed[b]);
+    if (copied[b]) cudaEventDestroy(copied[b]);
+  }
+  if (st != GPURIR_OK) return st;
+  if (e != cudaSuccess) return cuda_fail(e, "host call sync");
+  gpurir_opts fin = o;
+  fin.flags |= GPURIR_FLAG_SYNC;
+  return finish(fin, cs, d);
 }
 
 int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, float* out,

@@ -134,6 +134,29 @@ def test_mode_validation_on_host(P):
         assert _dir_call(P, 0, None, mode=1, Q=16) == 5
 
 
+def test_host_call_validated_on_host(P):
+    """gpurir_simulate_rir_host rejects bad arguments before touching the device (EINVAL = 1)."""
+    L = P._lib.lib()
+    f3 = (ctypes.c_float * 3)(3.0, 4.0, 2.5)
+    b6 = (ctypes.c_float * 6)(*([0.5] * 6))
+    nb = (ctypes.c_int * 3)(3, 3, 3)
+    buf = (ctypes.c_float * 64)()
+    o = P._lib.Opts()
+    L.gpurir_opts_default(ctypes.byref(o))
+    args = lambda **k: dict(dict(src=buf, ms=1, ors=None, sp=0, rcv=buf, mr=1, orv=None, mp=0, Tmax=0.01, out=buf), **k)
+    def call(a):
+        return L.gpurir_simulate_rir_host(f3, b6, ctypes.cast(a["src"], ctypes.c_void_p) if a["src"] else None, a["ms"],
+                                          a["ors"], a["sp"], ctypes.cast(a["rcv"], ctypes.c_void_p), a["mr"], a["orv"],
+                                          a["mp"], nb, 0.005, a["Tmax"], 16000.0, 343.0,
+                                          ctypes.cast(a["out"], ctypes.c_void_p) if a["out"] else None, ctypes.byref(o))
+    assert call(args(src=None)) == 1
+    assert call(args(out=None)) == 1
+    assert call(args(ms=0)) == 1
+    assert call(args(mp=2)) == 1            # cardioid receivers need orientations
+    assert call(args(sp=6)) == 1            # no such pattern
+    assert call(args(Tmax=-1.0)) == 1
+
+
 def test_ism_length_cap(P):
     """The kernels floor delays in fp32 with the 1.5 2^23 magic, exact below 2^22 samples: an ISM part
     longer than 2^22 - 8192 samples (87 s at 48 kHz) is EINVAL on the host, for every mode; the diffuse

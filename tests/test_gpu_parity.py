@@ -171,6 +171,41 @@ def test_cfg3_full_size_poly_vs_direct_all_rirs(P, oracle):
     assert np.all(np.isfinite(err)) and err.max() <= TOL["poly"], (err.max(), int(err.argmax()))
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_call_matches_device_call(P, oracle, pinned):
+    """gpurir_simulate_rir_host (host buffers, copies inside, 3 receiver chunks of <= 2048 RIRs overlapping
+    their D2H with the next chunk's kernels) returns exactly the RIRs of one device call in poly mode (the
+    chunks keep their global RIR index for the tail), from pinned tensors and from pageable numpy arrays."""
+    import torch
+    sc = W.cfg3(5000, "diffuse")
+    beta, nb = derive(oracle, sc)
+    ref = run_gpu(P, sc, beta, nb, mode="poly").astype(np.float32)
+    if pinned:
+        src, rcv, orv = (torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (sc.pos_src, sc.pos_rcv, sc.orV_rcv))
+        out = torch.empty((1, 5000, ref.shape[2]), dtype=torch.float32).pin_memory()
+    else:
+        src, rcv, orv, out = sc.pos_src, sc.pos_rcv, sc.orV_rcv, None
+    h = P.simulate_rir_host(sc.room, beta, src, rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=orv,
+                            mic_pattern=sc.pattern, mode="poly", seed=sc.seed, out=out)
+    h = h.numpy() if isinstance(h, torch.Tensor) else h
+    assert h.shape == ref.shape and np.array_equal(h, ref)
+
+
+def test_host_call_many_sources(P, oracle):
+    """Chunks of whole sources (M_rcv small): every RIR, tail included, matches the oracle on its global index."""
+    sc = W.cfg3(6, "diffuse")
+    rng = np.random.default_rng(5)
+    sc.pos_src = (rng.random((700, 3)) * np.array([2.4, 3.4, 1.9]) + 0.3).astype(np.float32)
+    beta, nb = derive(oracle, sc)
+    h = P.simulate_rir_host(sc.room, beta, sc.pos_src, sc.pos_rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c,
+                            orV_rcv=sc.orV_rcv, mic_pattern=sc.pattern, mode="poly", seed=sc.seed, rir_index_base=7)
+    assert h.shape[:2] == (700, 6)
+    for s in (0, 340, 341, 699):  # 2048 // 6 = 341 sources per chunk: both sides of the first boundary
+        r = oracle.simulate_rir(sc.room, beta, sc.pos_src[s:s + 1], sc.pos_rcv, nb, sc.Tdiff, sc.Tmax, fs=sc.fs,
+                                pattern=sc.pattern, orV_rcv=sc.orV_rcv, seed=sc.seed, rir_index_base=7 + 6 * s)
+        assert rel_err(h[s].astype(np.float64), r[0]).max() <= TOL["poly"], s
+
+
 @pytest.mark.parametrize("kernel", ["auto", "persistent"])
 @pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex", "poly"])
 def test_cfg4_48k_array(P, oracle, mode, kernel):
