@@ -384,25 +384,50 @@ def main():
     ms_per_step = total_ms / args.steps
     value = world * M_PER_GPU * args.steps / (total_ms / 1000.0)
 
-    # ---- end to end through the public API with HOST buffers (H2D inputs, D2H RIRs in the region) ----
-    # A dataset-generation loop: every step copies its inputs from pinned host memory, runs the call and
-    # copies the full RIR tensor back to pinned host memory.  Kernels run in order on a compute stream; each
-    # step's 734 MB D2H runs on a copy stream while the next step computes into the other of two device
-    # output buffers (a buffer is reused only after its D2H has finished).
+    # ---- end to end through the C ABI with HOST buffers: gpurir_simulate_rir_host ----
+    # A dataset-generation loop: every step is one call that takes the positions from pinned host memory and
+    # returns the full RIR tensor in pinned host memory (its H2D and D2H copies inside the call, the D2H of
+    # each 2048-RIR chunk overlapping the next chunk's kernels).  CUDA events on the call's stream bracket
+    # the K synchronous calls.
     e2e_steps = max(2, args.e2e_steps)
     h_src = torch.from_numpy(sc.pos_src).pin_memory()
     h_rcv = torch.from_numpy(np.ascontiguousarray(sc.pos_rcv[sl])).pin_memory()
     h_orv = torch.from_numpy(np.ascontiguousarray(sc.orV_rcv[sl])).pin_memory()
     h_out = [torch.empty((1, M_PER_GPU, nS), dtype=torch.float32).pin_memory() for _ in range(2)]
-    d_out = [out, torch.empty_like(out)]
-    cs, xs = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    # one untimed call first: it sizes the library's per-device scratch and creates its copy stream
+    P.simulate_rir_host(sc.room, beta, h_src, h_rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=h_orv,
+                        mic_pattern=sc.pattern, mode=args.mode, seed=sc.seed, rir_index_base=base,
+                        out=h_out[1], stream=stream)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    cs.wait_event(e0)
-    xs.wait_event(e0)
+    for i in range(e2e_steps):
+        P.simulate_rir_host(sc.room, beta, h_src, h_rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=h_orv,
+                            mic_pattern=sc.pattern, mode=args.mode, seed=sc.seed, rir_index_base=base,
+                            out=h_out[i % 2], stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64,
+                          device=dev if args.dist_backend == "nccl" else "cpu")
+    if dist:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * M_PER_GPU * e2e_steps / (float(e2e_ms.item()) / 1000.0)
+    h2d = (h_src.numel() + h_rcv.numel() + h_orv.numel()) * 4
+    d2h = h_out[0].numel() * 4
+    # the host copy of the last step equals the device-timed result (same inputs, deterministic kernels)
+    assert torch.equal(h_out[(e2e_steps - 1) % 2][0, :4].to(dev), out[0, :4])
+
+    # the same loop through the device API with torch copies, pipelined ACROSS steps (two device output
+    # buffers, D2H of step i on a copy stream while step i+1 computes): context for the host call's number
+    d_out = [out, torch.empty_like(out)]
+    cs, xs = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    cs.wait_event(p0)
+    xs.wait_event(p0)
     copied = []
     for i in range(e2e_steps):
         with torch.cuda.stream(cs):
@@ -423,17 +448,13 @@ def main():
             ev.record(xs)
             copied.append(ev)
     stream.wait_event(copied[-1])
-    e1.record(stream)
+    p1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64,
-                          device=dev if args.dist_backend == "nccl" else "cpu")
+    pipe_ms = torch.tensor([p0.elapsed_time(p1)], dtype=torch.float64,
+                           device=dev if args.dist_backend == "nccl" else "cpu")
     if dist:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = world * M_PER_GPU * e2e_steps / (float(e2e_ms.item()) / 1000.0)
-    h2d = (h_src.numel() + h_rcv.numel() + h_orv.numel()) * 4
-    d2h = h_out[0].numel() * 4
-    # the host copy of the last step equals the device-timed result (same inputs, deterministic kernels)
-    assert torch.equal(h_out[(e2e_steps - 1) % 2][0, :4].to(dev), out[0, :4])
+        dist.all_reduce(pipe_ms, op=dist.ReduceOp.MAX)
+    e2e_pipe_value = world * M_PER_GPU * e2e_steps / (float(pipe_ms.item()) / 1000.0)
 
     if rank != 0:
         if dist:
@@ -497,7 +518,10 @@ def main():
                         "frac_of_hbm": tail_bytes / tail_avg_s / 1e9 / hbm_peak, "bound": "hbm (write)",
                         "peak_GB_per_s": hbm_peak},
         "e2e": {"value": e2e_value, "unit": "RIRs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "steps": e2e_steps, "pipelining": "compute stream + copy stream, 2 device output buffers: D2H of step i overlaps the kernels of step i+1"},
+                "steps": e2e_steps, "call": "gpurir_simulate_rir_host (pinned host buffers; D2H of each 2048-RIR "
+                "chunk overlaps the next chunk's kernels)",
+                "stream_pipelined": {"value": e2e_pipe_value, "unit": "RIRs/s", "note": "device API + torch copies, "
+                                     "D2H of step i overlapping the kernels of step i+1 (context)"}},
         "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
         "paper_context": "gpuRIR V100 fp32, 1024 RIRs, T60 0.7 s diffuse: 195.69 ms = 5,233 RIRs/s (P:362); "

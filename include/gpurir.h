@@ -138,9 +138,10 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
  * when M_rcv is small) into two device buffers on opts->stream while a second stream copies the previous
  * chunk back into out, so the device->host transfer overlaps the kernels.  Every chunk keeps its global RIR
  * index (tail RNG stream, reading C16): the result equals one device call over all RIRs (bit-identical in
- * GPURIR_POLY mode, which is shard-invariant).  Device scratch (2 chunk outputs + positions) comes from the
- * stream-ordered allocator and is released before return.  Synchronous: returns when out is filled (the
- * status word is checked as with GPURIR_FLAG_SYNC).  opts->ev_ism / ev_tail are ignored.
+ * GPURIR_POLY mode, which is shard-invariant).  Device scratch (2 chunk outputs + positions) is a
+ * grow-only per-device buffer kept for later calls; host calls on one device are serialised by a lock.
+ * Synchronous: returns when out is filled (the status word is checked as with GPURIR_FLAG_SYNC).
+ * opts->ev_ism / ev_tail are ignored.
  * Errors: as gpurir_simulate_rir_dir; ENOMEM when the scratch cannot be allocated; ECUDA on copy failure.
  */
 int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const float* pos_src, int M_src,

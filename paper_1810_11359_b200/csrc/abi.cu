@@ -55,7 +55,13 @@ struct DeviceState {
   std::vector<TexEntry> texs;
   std::vector<PolyEntry> polys;
   int* work_counter = nullptr;  // persistent-kernel work-queue heads, one per call in flight (ring)
-  cudaStream_t copy_stream = nullptr;  // device->host stream of gpurir_simulate_rir_host
+  // gpurir_simulate_rir_host: copy stream, chunk events and a grow-only scratch buffer, owned by the device
+  // state and used under host_mu (host calls on one device run one at a time)
+  std::mutex host_mu;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t host_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // computed[2], copied[2]
+  char* host_scratch = nullptr;
+  size_t host_scratch_bytes = 0;
   unsigned next_counter = 0;
   int num_sms = 0;
 };
@@ -594,14 +600,16 @@ int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const 
   int st = GPURIR_OK;
   DeviceState* d = device_state(&st);
   if (!d) return st;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (!d->copy_stream) {
-      cudaError_t e = cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate(copy)");
-    }
+  std::lock_guard<std::mutex> hk(d->host_mu);
+  cudaError_t e = cudaSuccess;
+  if (!d->copy_stream) {
+    e = cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking);
+    for (int b = 0; b < 4 && e == cudaSuccess; b++) e = cudaEventCreateWithFlags(&d->host_ev[b], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "host call streams");
   }
   cudaStream_t cs = (cudaStream_t)o.stream, xs = d->copy_stream;
+  cudaEvent_t* computed = d->host_ev;
+  cudaEvent_t* copied = d->host_ev + 2;
   // chunks of whole output rows: a receiver range of one source, or whole sources when M_rcv is small
   const long long chunk_target = std::max<long long>(kHostChunkMin, ((long long)M_src * M_rcv + 7) / 8);
   const bool by_rcv = M_rcv >= chunk_target;
@@ -609,23 +617,27 @@ int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const 
   const int src_chunk = by_rcv ? 1 : (int)std::max<long long>(1, chunk_target / M_rcv);
   const size_t rows = (size_t)src_chunk * rcv_chunk;
   const size_t in_bytes = ((size_t)M_src * (orV_src ? 6 : 3) + (size_t)M_rcv * (orV_rcv ? 6 : 3)) * sizeof(float);
-  const size_t buf_bytes = rows * (size_t)nS * sizeof(float);
-  char* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&scratch, in_bytes + 2 * buf_bytes + 256, cs);
-  if (e != cudaSuccess) { cudaGetLastError(); return GPURIR_ENOMEM; }
+  const size_t in_pad = (in_bytes + 255) & ~(size_t)255;
+  const size_t need = in_pad + 2 * rows * (size_t)nS * sizeof(float);
+  if (need > d->host_scratch_bytes) {  // grow-only: later calls of this size reuse it (no allocator traffic)
+    if (d->host_scratch) {
+      cudaFree(d->host_scratch);  // private to host calls, which return only after their work has finished
+      d->host_scratch = nullptr;
+      d->host_scratch_bytes = 0;
+    }
+    e = cudaMalloc((void**)&d->host_scratch, need);
+    if (e != cudaSuccess) { cudaGetLastError(); d->host_scratch = nullptr; return GPURIR_ENOMEM; }
+    d->host_scratch_bytes = need;
+  }
+  char* scratch = d->host_scratch;
   float* d_src = reinterpret_cast<float*>(scratch);
   float* d_ors = orV_src ? d_src + 3 * (size_t)M_src : nullptr;
   float* d_rcv = d_src + (orV_src ? 6 : 3) * (size_t)M_src;
   float* d_orv = orV_rcv ? d_rcv + 3 * (size_t)M_rcv : nullptr;
   float* d_buf[2];
-  d_buf[0] = reinterpret_cast<float*>(scratch + ((in_bytes + 255) & ~(size_t)255));
+  d_buf[0] = reinterpret_cast<float*>(scratch + in_pad);
   d_buf[1] = d_buf[0] + rows * (size_t)nS;
-  cudaEvent_t computed[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
-  for (int b = 0; b < 2 && e == cudaSuccess; b++) {
-    e = cudaEventCreateWithFlags(&computed[b], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
-  }
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_src, pos_src, 3 * sizeof(float) * M_src, cudaMemcpyHostToDevice, cs);
+  e = cudaMemcpyAsync(d_src, pos_src, 3 * sizeof(float) * M_src, cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess && orV_src)
     e = cudaMemcpyAsync(d_ors, orV_src, 3 * sizeof(float) * M_src, cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_rcv, pos_rcv, 3 * sizeof(float) * M_rcv, cudaMemcpyHostToDevice, cs);
@@ -639,7 +651,7 @@ int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const 
   long long k = 0;
   for (int s0 = 0; s0 < M_src && st == GPURIR_OK; s0 += src_chunk) {
     const int ns = std::min(src_chunk, M_src - s0);
-    for (int r0 = 0; r0 < M_rcv && st == GPURIR_OK; r0 += rcv_chunk, k++) {
+    for (int r0 = 0; r0 < M_rcv && st == GPURIR_OK; r0 += rcv_chunk) {
       const int nr = std::min(rcv_chunk, M_rcv - r0);
       const int b = (int)(k & 1);
       if (k >= 2) cudaStreamWaitEvent(cs, copied[b], 0);  // d_buf[b] is free once chunk k-2 is on the host
@@ -655,17 +667,13 @@ int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const 
         e = cudaMemcpyAsync(out + row0 * nS, d_buf[b], (size_t)ns * nr * nS * sizeof(float), cudaMemcpyDeviceToHost, xs);
       if (e == cudaSuccess) e = cudaEventRecord(copied[b], xs);
       if (e != cudaSuccess) st = cuda_fail(e, "host call chunk");
+      k++;
     }
   }
-  // the scratch is released in stream order after the last copy; the call returns when out is filled
+  // the caller's stream resumes after the last copy; the call returns when out is filled
   for (int b = 0; b < 2; b++)
-    if (copied[b] && k > b) cudaStreamWaitEvent(cs, copied[b], 0);
-  cudaFreeAsync(scratch, cs);
+    if (k > b) cudaStreamWaitEvent(cs, copied[b], 0);
   e = cudaStreamSynchronize(cs);
-  for (int b = 0; b < 2; b++) {
-    if (computed[b]) cudaEventDestroy(computed[b]);
-    if (copied[b]) cudaEventDestroy(copied[b]);
-  }
   if (st != GPURIR_OK) return st;
   if (e != cudaSuccess) return cuda_fail(e, "host call sync");
   gpurir_opts fin = o;
