@@ -62,8 +62,10 @@ typedef enum {
                         device's 1-D texture width (else EINVAL).  Interpolation weights have 8 fractional
                         bits (texture hardware); tolerance as GPURIR_LUT. */
   GPURIR_POLY = 4     /* Eq. 6 by its polyphase expansion (reading R11): every image adds
-                        A_n T_d(2 phi_n - 1), d = 0..7, to the integer sample floor(x_n) (exact 64-bit
-                        fixed-point sums, deterministic), then an 8-channel FIR of 2H taps, whose
+                        A_n T_d(2 phi_n - 1), d = 0..7, to the integer sample floor(x_n) (exact
+                        fixed-point sums with a per-tile scale: one int32 word per channel, two for tiles
+                        with more than 2^14 possible images per sample; deterministic), then an
+                        8-channel FIR of 2H taps, whose
                         coefficients expand delta'(m - phi) in Chebyshev polynomials (max error 4.3e-7),
                         produces the RIR.  fp32 arithmetic; fp32 tolerance.  Requires Tw fs <= 1022.
                         Calls with fewer than 32 work items of 1024 samples (a lone RIR) run the direct
@@ -80,7 +82,8 @@ typedef struct {
   uint64_t rir_index_base;  /* global index of this call's first RIR (tail RNG stream id), default 0 */
   void* stream;             /* cudaStream_t to launch on; NULL = the legacy default stream          */
   int split;                /* CTAs cooperating on one time tile (thread-block cluster), 0 = auto;
-                               < 0 forces the persistent kernel (fp32/LUT/fp16) or the polyphase kernel */
+                               < 0 forces the persistent kernel (fp32/LUT/fp16) or the polyphase kernel;
+                               -2 also forces the polyphase two-word scheme on every tile (test hook) */
   unsigned flags;           /* GPURIR_FLAG_*                                                        */
   void* ev_ism[2];          /* optional cudaEvent_t pair recorded on `stream` around the ISM kernel  */
   void* ev_tail[2];         /* optional cudaEvent_t pair recorded around the diffuse-tail kernel     */

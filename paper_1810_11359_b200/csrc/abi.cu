@@ -233,11 +233,13 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
 constexpr long long kHostChunkMin = 2048;  // RIRs per chunk of gpurir_simulate_rir_host (fills the GPU)
 constexpr long long kPolyMinItems = 32;  // smaller polyphase calls take the direct fp32 kernels
 
-int poly_bits_for(const float L[3], long long nISM, double fs, double c, double Tw) {
-  const double V = (double)L[0] * L[1] * L[2];
-  const double dmax = ((double)nISM + Tw * fs / 2.0 + 1.0) * c / fs;
-  const double N = 2.0 * 4.0 * M_PI * dmax * dmax * (c / fs) / V + 16.0;
-  return N <= 256.0 ? 22 : 0;  // 2^22 x 256 = 2^30; the kernel's fp32 rounding is exact up to 2^22
+// Polyphase fixed point (ism_poly_kernel.cu, poly_tile_scale): a tile needs the two-word scheme when its
+// bound on the images per sample position, N = 8 pi x_hi^2 / V_s + 16 (x_hi the tile's largest delay and V_s
+// the room volume, both in samples), exceeds 2^14.  The call allocates the fine plane when its last tile could.
+bool poly_two_word_for(const float L[3], long long nISM, double fs, double c, double Tw) {
+  const double Vs = (double)L[0] * L[1] * L[2] * pow(fs / c, 3.0);
+  const double xhi = (double)nISM + Tw * fs / 2.0 + 1.0;
+  return 8.0 * M_PI * xhi * xhi / Vs + 16.0 >= 16384.0;  // the kernel's lb >= 15
 }
 
 // Mode tables of one call (LUT: phase-major smem table; texture LUT: filtered texture; polyphase table).
@@ -538,8 +540,8 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     A.out = out;
     A.status = d->status;
     if ((st = setup_mode(d, o, fs, H, stream, A))) return st;
-    A.poly_bits = poly_bits_for(room_sz, nISM, fs, c, o.Tw);
-    A.poly_gb = A.poly_bits <= 0;
+    A.poly_force2 = o.split == -2;
+    A.poly_gb = A.poly_force2 || poly_two_word_for(room_sz, nISM, fs, c, o.Tw);
     long long nclusters = (long long)A.nTiles * M;
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
@@ -700,6 +702,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
   std::vector<BatchJob> jobs(n_rooms);
   std::vector<int2> tiles, chunks;
   long long small_tiles = 0;  // work items at the cluster kernel's tile length (kernel choice)
+  bool any_two_word = false;  // polyphase: some job's last tile may need the two-word scheme
   for (int i = 0; i < n_rooms; i++) {
     const gpurir_room& R = rooms[i];
     if (int e0 = validate_room(R.room_sz, R.beta, R.nb_img, R.mic_pattern)) return e0;
@@ -723,7 +726,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     double T60 = sabine(R.room_sz, R.beta);
     J.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);
     J.rir_global = o.rir_index_base + (unsigned long long)i;
-    J.poly_bits = poly_bits_for(R.room_sz, nISM, fs, c, o.Tw);
+    any_two_word = any_two_word || poly_two_word_for(R.room_sz, nISM, fs, c, o.Tw);
     small_tiles += (nISM + kTC - 1) / kTC;
     long long groups = (nS + 3) / 4 - nISM / 4;
     int nch = nISM < nS ? (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4)) : 0;
@@ -772,7 +775,8 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     A.out = out;
     A.status = d->status;
     if ((st = setup_mode(d, o, fs, H, stream, A))) { cudaFreeAsync(ws, stream); return st; }
-    for (int i = 0; i < n_rooms && !A.poly_gb; i++) A.poly_gb = jobs[i].poly_bits <= 0;
+    A.poly_force2 = o.split == -2;
+    A.poly_gb = A.poly_force2 || any_two_word;
     long long nw = (long long)tiles.size();
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     if (poly) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, stream);

@@ -90,12 +90,11 @@ __device__ __forceinline__ float poly_z_factor(int nz, const RirGeom& g) {
 }
 
 // One image's 8 channel values A T_d(y), d = 0..7, added to G[.][p] as integers v = round(A T_d 2^s).  The
-// per-RIR scale bounds |A| by the direct path, so |v| <= 2^bits.  When the host's bound on the images per
-// sample position (2 x 4 pi d_max^2 (c / fs) / V + 16, from the lattice's one image per room volume) lets
-// 2^bits x that count fit an int32 with bits = 22, one plain shared-memory reduction per channel suffices
-// (single word, fp32 arithmetic); otherwise bits = 28 and v = a 2^14 + b, b in [0, 2^14), goes to two int32 planes (2^17
-// terms per position before either could overflow).  Integer adds commute, so G does not depend on the order
-// in which images arrive (deterministic, shard-invariant).
+// tile's scale bounds |A| by its closest possible image, so |v| <= 2^bits, and its bound N on the images per
+// sample position sets bits (tile setup): single word (bits <= 22, fp32 arithmetic, one plain shared-memory
+// reduction per channel) while N 2^bits <= 2^30 leaves bits >= 16; otherwise bits = 28 and v = a 2^14 + b,
+// b in [0, 2^14), goes to two int32 planes (2^17 terms per position before either could overflow).  Integer
+// adds commute, so G does not depend on the order in which images arrive (deterministic, shard-invariant).
 __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int W, int p, float y, float amp, float scale,
                                          bool two_word) {
   if (!two_word) {
@@ -171,14 +170,13 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       PolyTile& T = sm.ti;
       T.next = wi < n_work;
       if (wi < n_work) {
-        int m, tile, nISM, bits = A.poly_bits;
+        int m, tile, nISM;
         long long row;
         const float zero3[3] = {0.f, 0.f, 0.f};
         if (A.jobs) {
           const int2 jt = A.tiles[wi];
           const BatchJob& J = A.jobs[jt.x];
           m = jt.x; tile = jt.y; nISM = J.nISM; row = J.out_offset;
-          bits = J.poly_bits;
           geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.ors, J.spkr_pattern, J.lb, J.neg, J.zero, T.g,
                     A.status);
         } else {
@@ -217,14 +215,25 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         T.zl = T.g.nlo[2];
         T.zh = T.g.nhi[2] - 1;
         T.use_bz = (T.zh - T.zl + 1) <= kPolyBz;
-        // fixed-point scale: |A_n| <= 1 / (4 pi d_dp) (|beta|, |g| <= 1; the direct image is the closest) and
-        // |T_d| <= 1, so every channel value is at most 2^bits in units of 2^-s (see poly_add)
+        // per-tile fixed point (see poly_add).  Images depositing into this tile have x >= x_lo =
+        // max(t0 - m_hi, x_dp) samples (the direct path is the closest image), so |A_n| <= 1 / (4 pi d_lo)
+        // (|beta|, |g| <= 1); at most N = 8 pi x_hi^2 / V_s + 16 of them share a sample position (a shoebox
+        // lattice holds one image per room volume V_s; x_hi the tile's largest delay; x2 margin + 16).  With
+        // |v| <= 2^bits and N 2^bits <= 2^30 one int32 word per channel holds every sum: bits = min(22,
+        // 30 - ceil(log2 N)); below 16 bits (N > 2^14) the tile takes the two-word scheme (bits = 28).
         const double ddx = T.g.s[0] - T.g.r[0], ddy = T.g.s[1] - T.g.r[1], ddz = T.g.s[2] - T.g.r[2];
-        const double abound = 0.0795774715459476679 / fmax(sqrt(ddx * ddx + ddy * ddy + ddz * ddz), 1e-30);
+        const double x_dp = sqrt(ddx * ddx + ddy * ddy + ddz * ddz) * A.fs_over_c;
+        const double x_lo = fmax(fmax((double)(T.t0 - m_hi), x_dp), 1e-30);
+        const double x_hi = (double)(T.te - A.poly_mlo);
+        const double Vs = T.g.L[0] * T.g.L[1] * T.g.L[2] * A.fs_over_c * A.fs_over_c * A.fs_over_c;
+        int lb;
+        (void)frexp(25.132741228718345 * x_hi * x_hi / Vs + 16.0, &lb);  // N < 2^lb
+        int bits = min(22, 30 - lb);
+        T.two_word = bits < 16 || A.poly_force2;
+        if (T.two_word) bits = 28;
+        const double abound = 0.0795774715459476679 * A.fs_over_c / x_lo;
         int e;
         (void)frexp(abound, &e);  // abound < 2^e
-        T.two_word = bits <= 0;
-        if (bits <= 0) bits = 28;
         T.scalef = ldexpf(1.f, bits - e);
         T.inv_scale = ldexp(1.0, e - bits);
         T.inv_scalef = ldexpf(1.f, e - bits);

@@ -20,7 +20,6 @@ struct alignas(16) BatchJob {
   int nS;               // total samples of this RIR
   long long out_offset; // element offset of the RIR row in the output
   float kappa_fs;       // kappa / fs (1/sample) of the Sabine envelope (Eq. 8, C14)
-  int poly_bits;        // polyphase mode: fixed-point bits of one channel value, or 0 for the two-word scheme
   unsigned long long rir_global;  // tail RNG stream id (C16)
   float lb[6];          // log2 |beta_w| (0 where beta_w == 0), precomputed on the host
   unsigned neg, zero;   // bit w: beta_w < 0 / beta_w == 0
@@ -73,8 +72,8 @@ struct IsmArgs {
   // polyphase mode (reading R11): delta'(m - phi) = sum_d P[m - mlo][d] T_d(2 phi - 1), m = mlo .. mlo + ntaps - 1
   const float* poly_P;     // device [ntaps][8]
   int poly_ntaps, poly_mlo;
-  int poly_bits;           // single-room call: fixed-point bits of one channel value, or 0 (two-word scheme)
-  int poly_gb;             // the call has two-word items: allocate and use the fine plane Gb
+  int poly_gb;             // some tile of the call may need the two-word scheme: allocate the fine plane Gb
+  int poly_force2;         // test hook (opts.split == -2): every tile uses the two-word scheme
 };
 
 struct TailArgs {

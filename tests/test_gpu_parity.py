@@ -554,12 +554,14 @@ def test_poly_deterministic_and_shard_invariant(P, oracle):
     assert np.array_equal(a, np.concatenate(parts, axis=1))
 
 
-def test_poly_two_word_long_rir(P, oracle):
-    """Full ISM to 0.7 s (config 3 (ii)): the lattice-density bound exceeds the single-word range, so the
-    two-word accumulation runs; parity at the fp32 tolerance on 2 receivers."""
+@pytest.mark.parametrize("split", [-1, -2])
+def test_poly_long_rir_per_tile_scale(P, oracle, split):
+    """Full ISM to 0.7 s (config 3 (ii)): the per-tile fixed point keeps every tile single-word (split -1; the
+    late tiles' scale follows their closest image) and the two-word scheme forced on every tile (split -2,
+    the test hook) must agree with the oracle too; parity at the fp32 tolerance on 2 receivers."""
     sc = W.cfg3(2, "full")
     beta, nb = derive(oracle, sc)
-    g = run_gpu(P, sc, beta, nb, mode="poly", split=-1)  # 22 work items: forced onto the polyphase kernel
+    g = run_gpu(P, sc, beta, nb, mode="poly", split=split)  # 22 work items: forced onto the polyphase kernel
     r = run_oracle(oracle, sc, beta, nb)
     assert rel_err(g, r).max() <= TOL["poly"]
 
