@@ -64,7 +64,7 @@ typedef enum {
   GPURIR_POLY = 4     /* Eq. 6 by its polyphase expansion (reading R11): every image adds
                         A_n T_d(2 phi_n - 1), d = 0..7, to the integer sample floor(x_n) (exact
                         fixed-point sums with a per-tile scale: one int32 word per channel, two for tiles
-                        with more than 2^14 possible images per sample; deterministic), then an
+                        whose bound on images per sample reaches 2^14; deterministic), then an
                         8-channel FIR of 2H taps, whose
                         coefficients expand delta'(m - phi) in Chebyshev polynomials (max error 4.3e-7),
                         produces the RIR.  fp32 arithmetic; fp32 tolerance.  Requires Tw fs <= 1022.

@@ -233,13 +233,16 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
 constexpr long long kHostChunkMin = 2048;  // RIRs per chunk of gpurir_simulate_rir_host (fills the GPU)
 constexpr long long kPolyMinItems = 32;  // smaller polyphase calls take the direct fp32 kernels
 
-// Polyphase fixed point (ism_poly_kernel.cu, poly_tile_scale): a tile needs the two-word scheme when its
-// bound on the images per sample position, N = 8 pi x_hi^2 / V_s + 16 (x_hi the tile's largest delay and V_s
-// the room volume, both in samples), exceeds 2^14.  The call allocates the fine plane when its last tile could.
+// Polyphase fixed point (ism_poly_kernel.cu, tile setup): a tile needs the two-word scheme when its bound on
+// the images per sample position, N = 8 pi x_hi^2 / V_s + 24 x_hi / L_min + 16 (x_hi the tile's largest delay,
+// V_s the room volume and L_min its shortest side, all in samples), reaches 2^14.  The call allocates the
+// fine plane when its last tile could.
 bool poly_two_word_for(const float L[3], long long nISM, double fs, double c, double Tw) {
-  const double Vs = (double)L[0] * L[1] * L[2] * pow(fs / c, 3.0);
+  const double k = fs / c;
+  const double Vs = (double)L[0] * L[1] * L[2] * k * k * k;
+  const double Lmin = std::min(std::min((double)L[0], (double)L[1]), (double)L[2]) * k;
   const double xhi = (double)nISM + Tw * fs / 2.0 + 1.0;
-  return 8.0 * M_PI * xhi * xhi / Vs + 16.0 >= 16384.0;  // the kernel's lb >= 15
+  return 8.0 * M_PI * xhi * xhi / Vs + 24.0 * xhi / Lmin + 16.0 >= 16384.0;  // the kernel's lb >= 15: bits < 16
 }
 
 // Mode tables of one call (LUT: phase-major smem table; texture LUT: filtered texture; polyphase table).

@@ -217,17 +217,22 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         T.use_bz = (T.zh - T.zl + 1) <= kPolyBz;
         // per-tile fixed point (see poly_add).  Images depositing into this tile have x >= x_lo =
         // max(t0 - m_hi, x_dp) samples (the direct path is the closest image), so |A_n| <= 1 / (4 pi d_lo)
-        // (|beta|, |g| <= 1); at most N = 8 pi x_hi^2 / V_s + 16 of them share a sample position (a shoebox
-        // lattice holds one image per room volume V_s; x_hi the tile's largest delay; x2 margin + 16).  With
-        // |v| <= 2^bits and N 2^bits <= 2^30 one int32 word per channel holds every sum: bits = min(22,
-        // 30 - ceil(log2 N)); below 16 bits (N > 2^14) the tile takes the two-word scheme (bits = 28).
+        // (|beta|, |g| <= 1) and every channel value is |v| <= 2^bits.  N bounds the images that can share one
+        // sample position at delays <= x_hi (the tile's largest): twice the mean count 4 pi x_hi^2 / V_s (one
+        // image per room volume V_s, in samples), plus 24 x_hi / (L_min fs / c) for images stacked on equal
+        // distances by symmetric or commensurate geometry (a cube with source and receiver at its centre puts
+        // r3(n) <= 24 sqrt(n) images on |k|^2 = n, |k| = d / L), plus 16.  bits = min(22, 30 - ceil(log2 N))
+        // leaves room for 2N full-amplitude images per position before an int32 sum could overflow
+        // (brute-force counts fill <= 1/3 of it: tests/test_poly_headroom.py).  Below 16 bits (N >= 2^14)
+        // the tile takes the two-word scheme.
         const double ddx = T.g.s[0] - T.g.r[0], ddy = T.g.s[1] - T.g.r[1], ddz = T.g.s[2] - T.g.r[2];
         const double x_dp = sqrt(ddx * ddx + ddy * ddy + ddz * ddz) * A.fs_over_c;
         const double x_lo = fmax(fmax((double)(T.t0 - m_hi), x_dp), 1e-30);
         const double x_hi = (double)(T.te - A.poly_mlo);
         const double Vs = T.g.L[0] * T.g.L[1] * T.g.L[2] * A.fs_over_c * A.fs_over_c * A.fs_over_c;
+        const double Lmin_s = fmin(fmin(T.g.L[0], T.g.L[1]), T.g.L[2]) * A.fs_over_c;
         int lb;
-        (void)frexp(25.132741228718345 * x_hi * x_hi / Vs + 16.0, &lb);  // N < 2^lb
+        (void)frexp(25.132741228718345 * x_hi * x_hi / Vs + 24.0 * x_hi / Lmin_s + 16.0, &lb);  // N < 2^lb
         int bits = min(22, 30 - lb);
         T.two_word = bits < 16 || A.poly_force2;
         if (T.two_word) bits = 28;

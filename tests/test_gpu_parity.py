@@ -566,6 +566,26 @@ def test_poly_long_rir_per_tile_scale(P, oracle, split):
     assert rel_err(g, r).max() <= TOL["poly"]
 
 
+@pytest.mark.parametrize("fs", [16000.0, 48000.0])
+def test_poly_rigid_centred_cube(P, oracle, fs):
+    """The fixed point's worst case: rigid walls (beta = 1: every image at full amplitude, all of one sign)
+    in a cube with the source at its centre and receivers on its symmetry axes, where the image lattice
+    stacks up to r3(n) images on one delay (tests/test_poly_headroom.py).  Polyphase vs oracle at the fp32
+    tolerance, plus the other sign pattern (beta = -1)."""
+    room = np.array([2.0, 2.0, 2.0], np.float32)
+    src = np.array([[1.0, 1.0, 1.0]], np.float32)
+    rcv = np.array([[1.0, 1.0, 1.5], [1.0, 1.5, 1.5], [0.5, 1.0, 1.0], [1.25, 1.25, 1.25]], np.float32)
+    T = 0.05
+    nb = oracle.t2n(T, room, 343.0)
+    for b in (1.0, -1.0):
+        beta = np.full(6, b, np.float32)
+        import torch
+        g = P.simulate_rir(room, beta, torch.from_numpy(src).cuda(), torch.from_numpy(rcv).cuda(), nb, T, T, fs,
+                           mode="poly", split=-1, sync=True).cpu().numpy().astype(np.float64)
+        r = oracle.simulate_rir(room, beta, src, rcv, nb, T, T, fs=fs)
+        assert rel_err(g, r).max() <= TOL["poly"], (b, rel_err(g, r).max())
+
+
 @pytest.mark.parametrize("fs", [8000.0, 22050.0, 44100.0, 96000.0])
 def test_poly_sampling_rates(P, oracle, fs):
     """Integer and fractional half-windows H = Tw fs / 2 (16, 44.1, 88.2, 192 taps-half), zero-padded tap
