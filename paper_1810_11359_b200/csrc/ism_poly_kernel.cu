@@ -18,6 +18,8 @@
 //      memory; the tile is written once, coalesced.
 // Work per output sample no longer grows with the image density (690 in-window taps per sample at config
 // 3 (i)): the filter costs 2H x 8 MACs, the aggregation 8 channel updates per image.
+#include <type_traits>
+
 #include "ism_common.cuh"
 
 namespace gpurir {
@@ -310,10 +312,15 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         int j = lo;
         int before = j > 0 ? sm.colpre[j - 1] : 0;
         const int zl = T.zl;
-        const bool use_bz = T.use_bz, dir_src = g.as != 1.f, two_word = T.two_word;
         const float oz = g.o[2], ga = g.a, scalef = T.scalef;
         int boundary = sm.colpre[j];
         PolyColRec cr = sm.col[j];  // the current column's record, in registers: reloaded on a column change
+        // the walk, compiled twice: the common case (single word, omni source, z factors from the table) with
+        // its flags as constants — fewer live registers, so fewer loop constants re-read from shared memory —
+        // and the general case with runtime flags
+        auto walk = [&](auto fast) {
+        constexpr bool kFast = decltype(fast)::value;
+        const bool use_bz = kFast || T.use_bz, dir_src = !kFast && g.as != 1.f, two_word = !kFast && T.two_word;
         for (int gi = g0; gi < g1; gi++) {  // every lane runs R candidates: the walk keeps the warp converged
           if (gi >= boundary) {
             do { before = boundary; j++; boundary = sm.colpre[j]; } while (gi >= boundary);
@@ -346,6 +353,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           const float y = fmaf(2.f, phi, -1.f);            // 2 phi - 1 in [-1, 1)
           poly_add(Ga, Gb, W, p + (p >> 3), y, amp, scalef, two_word);
         }
+        };
+        if (T.use_bz && !T.two_word && g.as == 1.f) walk(std::true_type());
+        else walk(std::false_type());
       }
       __syncthreads();  // column records are replaced by the next batch
     }
