@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         auto walk = [&](auto fast) {
         constexpr bool kFast = decltype(fast)::value;
         const bool use_bz = kFast || T.use_bz, dir_src = !kFast && g.as != 1.f, two_word = !kFast && T.two_word;
+        const double Lzs = T.Lzs, offEs = T.offEs, offOs = T.offOs;
         for (int gi = g0; gi < g1; gi++) {  // every lane runs R candidates: the walk keeps the warp converged
           if (gi >= boundary) {
             do { before = boundary; j++; boundary = sm.colpre[j]; } while (gi >= boundary);
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           const float bz = use_bz ? sm.bz[min(max(nz - zl, 0), kPolyBz - 1)] : poly_z_factor(nz, g);
           const int nzo = nz + odd;
           // Eq. 1 along z, in samples (the tile's constants are read from shared memory: no conversions here)
-          const double dz = fma(int_to_double(nzo), T.Lzs, odd ? T.offOs : T.offEs);
+          const double dz = fma(int_to_double(nzo), Lzs, odd ? offOs : offEs);
           const double x2 = fma(dz, dz, cr.rho2);                             // (d fs / c)^2
           if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); continue; }
           float x0f, xd, rx;  // x = x0f + xd (xd the fp64 Newton correction); rx = 1/x
