@@ -38,12 +38,24 @@ template <int THREADS> struct PolyCfg {
   static_assert(kPolyTC % kPass == 0, "FIR passes of 4 channel-pair groups x 8 outputs per thread");
 };
 
-struct PolyColRec {  // 32 B, as WsColRec; lengths in samples (x fs / c)
+// One nonempty lattice column of a batch (32 B, two 16-B loads; lengths in samples, x fs / c).  Its
+// candidates are the global indices [start, end) of the batch's candidate list; candidate gi is the image
+// n_z = gi + (gi < b ? a1 : a2) (the two n_z runs of the column, see the walk).
+struct PolyColRec {
   double rho2;
   float bxy, cdot;
-  int r1lo, r2lo, r1n;
-  float sdot;
+  int a1, a2, b, end;
 };
+__device__ __forceinline__ PolyColRec load_col(const PolyColRec* c) {
+  const int4* p = reinterpret_cast<const int4*>(c);
+  const int4 u = p[0], v = p[1];
+  PolyColRec r;
+  r.rho2 = __hiloint2double(u.y, u.x);
+  r.bxy = __int_as_float(u.z);
+  r.cdot = __int_as_float(u.w);
+  r.a1 = v.x; r.a2 = v.y; r.b = v.z; r.end = v.w;
+  return r;
+}
 
 
 struct PolyTile {
@@ -62,7 +74,8 @@ template <int THREADS>
 struct alignas(16) PolySmem {
   PolyTile ti;
   alignas(16) PolyColRec col[THREADS];  // one lattice column per thread and batch
-  int colpre[THREADS];
+  int colpre[THREADS];                  // inclusive candidate prefix (= col[].end), for the run search
+  float colsdot[THREADS];               // directional source: the column's part of cos(theta_s) (general walk)
   int scan_tmp[THREADS / 32];
   float bz[kPolyBz];
 };
@@ -261,7 +274,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       {
         const int q = qb + tid;
         PolyColRec cr;
-        cr.r1lo = 0; cr.r2lo = 0; cr.r1n = 0; cr.rho2 = 0.0; cr.bxy = 0.f; cr.cdot = 0.f; cr.sdot = 0.f;
+        cr.a1 = 0; cr.a2 = 0; cr.b = 0; cr.end = 0; cr.rho2 = 0.0; cr.bxy = 0.f; cr.cdot = 0.f;
+        float sdot = 0.f;
+        int r1lo = 0, r2lo = 0, r1n = 0;
         if (q < T.ncols) {
           const int qy = (int)(((float)q + 0.5f) * T.invNX);
           const int nx = T.nx0 + (q - qy * T.NX), ny = T.ny0 + qy;
@@ -270,7 +285,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           const double rho2 = dx * dx + dy * dy;
           cr.rho2 = rho2 * sc2;
           cr.cdot = ((float)dx * g.o[0] + (float)dy * g.o[1]) * fsc;
-          cr.sdot = src_col_dot(nx, ny, (float)dx, (float)dy, g) * fsc;
+          sdot = src_col_dot(nx, ny, (float)dx, (float)dy, g) * fsc;
           uint32_t sgn = 0;
           bool zero = false;
           const float lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
@@ -286,7 +301,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             pa = max(pa, T.zl); pb = min(pb, T.zh);
             na = max(na, T.zl); nbz = min(nbz, T.zh);
             const int n1 = max(0, pb - pa + 1), n2 = max(0, nbz - na + 1);
-            cr.r1lo = pa; cr.r1n = n1; cr.r2lo = na;
+            r1lo = pa; r1n = n1; r2lo = na;
             cnt = n1 + n2;
           }
         }
@@ -294,8 +309,14 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         // columns in order, so the run search and the walk below never visit an empty column
         const int incl = poly_block_scan<kPolyThreads>(cnt + (cnt > 0 ? (1 << 20) : 0), sm.scan_tmp);
         if (cnt > 0) {
-          sm.col[(incl >> 20) - 1] = cr;
-          sm.colpre[(incl >> 20) - 1] = incl & 0xFFFFF;
+          const int end = incl & 0xFFFFF, start = end - cnt, k = (incl >> 20) - 1;
+          cr.end = end;
+          cr.b = start + r1n;          // first candidate of the second n_z run
+          cr.a1 = r1lo - start;        // n_z = gi + a1 on the first run
+          cr.a2 = r2lo - r1n - start;  // n_z = gi + a2 on the second
+          sm.col[k] = cr;
+          sm.colpre[k] = end;
+          sm.colsdot[k] = sdot;
         }
       }
       __syncthreads();
@@ -310,11 +331,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           if (sm.colpre[mid] > g0) hi = mid; else lo = mid + 1;
         }
         int j = lo;
-        int before = j > 0 ? sm.colpre[j - 1] : 0;
         const int zl = T.zl;
         const float oz = g.o[2], ga = g.a, scalef = T.scalef;
-        int boundary = sm.colpre[j];
-        PolyColRec cr = sm.col[j];  // the current column's record, in registers: reloaded on a column change
+        PolyColRec cr = load_col(&sm.col[j]);  // the current column's record, in registers
         // the walk, compiled twice: the common case (single word, omni source, z factors from the table) with
         // its flags as constants — fewer live registers, so fewer loop constants re-read from shared memory —
         // and the general case with runtime flags
@@ -323,12 +342,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         const bool use_bz = kFast || T.use_bz, dir_src = !kFast && g.as != 1.f, two_word = !kFast && T.two_word;
         const double Lzs = T.Lzs, offEs = T.offEs, offOs = T.offOs;
         for (int gi = g0; gi < g1; gi++) {  // every lane runs R candidates: the walk keeps the warp converged
-          if (gi >= boundary) {
-            do { before = boundary; j++; boundary = sm.colpre[j]; } while (gi >= boundary);
-            cr = sm.col[j];
-          }
-          const int l = gi - before;
-          const int nz = l < cr.r1n ? cr.r1lo + l : cr.r2lo + (l - cr.r1n);
+          // compacted columns are nonempty and gi advances by one: a change moves exactly one column on
+          if (gi >= cr.end) cr = load_col(&sm.col[++j]);
+          const int nz = gi + (gi < cr.b ? cr.a1 : cr.a2);
           const int odd = nz & 1;
           const float bz = use_bz ? sm.bz[min(max(nz - zl, 0), kPolyBz - 1)] : poly_z_factor(nz, g);
           const int nzo = nz + odd;
@@ -349,7 +365,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           const float dzf = (float)dz;  // one XU conversion instead of shared-memory loads (the smem pipe binds)
           const float cth = fmaf(dzf, oz, cr.cdot) * rx;
           float gain = ga + (1.f - ga) * cth;
-          if (dir_src) gain *= src_gain(cr.sdot, odd, dzf, rx, g);
+          if (dir_src) gain *= src_gain(sm.colsdot[j], odd, dzf, rx, g);
           const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
           const float y = fmaf(2.f, phi, -1.f);            // 2 phi - 1 in [-1, 1)
           poly_add(Ga, Gb, W, p + (p >> 3), y, amp, scalef, two_word);
