@@ -191,6 +191,22 @@ def test_host_call_matches_device_call(P, oracle, pinned):
     assert h.shape == ref.shape and np.array_equal(h, ref)
 
 
+def test_host_call_directional_source(P, oracle):
+    """The host call with a directional (cardioid) source and receivers: equal to the device call (poly)."""
+    import torch
+    sc = W.cfg3(3000, "diffuse")
+    beta, nb = derive(oracle, sc)
+    ors = np.array([[0.6, -0.8, 0.0]], np.float32)
+    ref = P.simulate_rir(sc.room, beta, torch.from_numpy(sc.pos_src).cuda(), torch.from_numpy(sc.pos_rcv).cuda(), nb,
+                         sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=torch.from_numpy(sc.orV_rcv).cuda(),
+                         mic_pattern=sc.pattern, mode="poly", seed=sc.seed, orV_src=torch.from_numpy(ors).cuda(),
+                         spkr_pattern="cardioid", sync=True).cpu().numpy()
+    h = P.simulate_rir_host(sc.room, beta, sc.pos_src, sc.pos_rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c,
+                            orV_rcv=sc.orV_rcv, mic_pattern=sc.pattern, mode="poly", seed=sc.seed, orV_src=ors,
+                            spkr_pattern="cardioid")
+    assert np.array_equal(h, ref)
+
+
 def test_host_call_many_sources(P, oracle):
     """Chunks of whole sources (M_rcv small): every RIR, tail included, matches the oracle on its global index."""
     sc = W.cfg3(6, "diffuse")
