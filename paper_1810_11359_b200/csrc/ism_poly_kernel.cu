@@ -7,15 +7,20 @@
 //     delta'(m - phi) = sum_d P_d[m] T_d(2 phi - 1),   d = 0..7   (max error 4.3e-7, host fit),
 // the RIR becomes a fixed 8-channel FIR filter applied to per-sample image aggregates:
 //     h[k] = sum_m sum_d P_d[m] G_d[k - m],   G_d[j] = sum_{n: j_n = j} A_n T_d(2 phi_n - 1).
-// Per work item (RIR, 1024-sample tile) a CTA of 512 threads
+// Persistent CTAs (THREADS = 256 x 4 per SM for large single-word calls, else 512 x 2) take (RIR,
+// 1024-sample tile) work items from a global counter; per item the CTA
 //   1. enumerates the tile's shell of images column by column (as ism_ws_kernel; nonempty columns
 //      compacted by the candidate scan) and adds each image's 8 channel values into G in shared memory —
-//      as fixed point with integer reductions (one int32 word per channel, or two for dense calls), so the
-//      sums are exact and independent of the order the images arrive in (deterministic, shard-invariant);
-//      the fraction of the delay comes from the exact floor of the fp32 estimate plus its fp64 correction;
-//   2. converts G to fp32 in place and runs the 8-channel FIR (2H taps): 4 channel-pair groups x 128
+//      as fixed point with integer reductions (one int32 word per channel, or two for tiles dense enough to
+//      need them; the scale is per tile), so the sums are exact and independent of the order the images
+//      arrive in (deterministic, shard-invariant); the fraction of the delay comes from the exact floor of
+//      the fp32 estimate plus its fp64 correction;
+//   2. converts G to fp32 in place and runs the 8-channel FIR (2H taps): 4 channel-pair groups x THREADS/4
 //      threads x 8 consecutive outputs with a sliding register window, partial sums meeting in shared
 //      memory; the tile is written once, coalesced.
+// The kernel is bound by shared-memory wavefronts (80 % of peak: the random-position reductions and the
+// FIR's loads), so the loops keep their constants in registers rather than re-reading them from shared
+// memory.
 // Work per output sample no longer grows with the image density (690 in-window taps per sample at config
 // 3 (i)): the filter costs 2H x 8 MACs, the aggregation 8 channel updates per image.
 #include <type_traits>
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     __syncthreads();
 
     // ---- 3. 8-channel FIR: h[k] = sum_m sum_d P_d[m] G_d[k - m] --------------------------------
-    // Thread group gq (128 threads) applies channel pair gq to 8 consecutive outputs per thread with a
+    // Thread group gq (THREADS/4 threads) applies channel pair gq to 8 consecutive outputs per thread with a
     // sliding register window (one new position per tap); the 4 groups' partial sums meet in shared memory.
     // ntaps is padded to a multiple of 8 with zero taps, so in every unrolled group of 8 taps the new
     // positions q - mi - 1 - u sit at fixed offsets 0 .. -6, -8 of one padded address (q = 7 mod 8).
