@@ -518,6 +518,7 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
   if (!d) return st;
   cudaStream_t stream = (cudaStream_t)o.stream;
 
+  bool fused_tail = false;
   if (nISM > 0) {
     IsmArgs A;
     memset(&A, 0, sizeof(A));
@@ -545,6 +546,19 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     if ((st = setup_mode(d, o, fs, H, stream, A))) return st;
     A.poly_force2 = o.split == -2;
     A.poly_gb = A.poly_force2 || poly_two_word_for(room_sz, nISM, fs, c, o.Tw);
+    // polyphase: the diffuse tail runs inside the ISM kernel when the envelope window (10 ms) fits the last
+    // 1024-sample tile; the separate tail kernel otherwise
+    const int win = (int)llround(0.010 * fs);
+    fused_tail = poly && nISM < nS && win <= kPolyTile;
+    if (fused_tail) {
+      A.poly_tail = 1;
+      A.tail_win = win;
+      A.tail_nS = (int)nS;
+      const double T60 = sabine(room_sz, beta);
+      A.tail_kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);  // Eq. 8, reading C14
+      A.tail_seed = o.seed;
+      A.tail_rir_base = o.rir_index_base;
+    }
     long long nclusters = (long long)A.nTiles * M;
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
@@ -559,7 +573,10 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     if (e != cudaSuccess) return cuda_fail(e, "launch_ism");
     if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);
   }
-  if (nISM < nS) {
+  if (nISM < nS && fused_tail) {  // the tail was written by the polyphase kernel: the events bracket nothing
+    if (o.ev_tail[0]) cudaEventRecord((cudaEvent_t)o.ev_tail[0], stream);
+    if (o.ev_tail[1]) cudaEventRecord((cudaEvent_t)o.ev_tail[1], stream);
+  } else if (nISM < nS) {
     TailArgs T;
     memset(&T, 0, sizeof(T));
     T.pos_src = pos_src; T.pos_rcv = pos_rcv; T.M_rcv = M_rcv; T.M = (int)M;

@@ -26,6 +26,7 @@
 #include <type_traits>
 
 #include "ism_common.cuh"
+#include "tail_common.cuh"
 
 namespace gpurir {
 
@@ -72,8 +73,39 @@ struct PolyTile {
   int two_word;
   long long row;
   int t0, te, tc, nx0, ny0, NX, ncols, zl, zh, use_bz, next;
+  int rir, tail;     // the RIR; this tile ends its ISM part and the call fuses the tail
+  double x_dp;       // direct-path delay (samples)
+  float tenv[3];     // fused tail: env0, alpha, rho of the RIR (tail_envelope)
   float invNX;
 };
+
+// The diffuse tail of RIR T.rir, by the CTA that just wrote its last ISM tile (output partial sums still in
+// red): warp 0 reduces the envelope window from shared memory exactly as tail_kernel does from global memory,
+// then every thread writes Philox blocks of the tail.  Not inlined: the tail's registers (Philox round keys)
+// stay out of the image loop's allocation.
+__device__ __noinline__ void poly_fused_tail(PolyTile& T, const float* red, int tid, int nthreads, float* out,
+                                             int nS, int win, float kappa_fs, unsigned long long seed,
+                                             unsigned long long rir_base) {
+  const int nISM = T.te;
+  if (tid < 32) {
+    float env0, alpha, rho;
+    const int t0 = T.t0;
+    tail_envelope([&](int k) {
+                    const int t = k - t0;
+                    return (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
+                  },
+                  nISM, win, T.x_dp, kappa_fs, tid, env0, alpha, rho);
+    if (tid == 0) { T.tenv[0] = env0; T.tenv[1] = alpha; T.tenv[2] = rho; }
+  }
+  __syncthreads();
+  const float env0 = T.tenv[0], alpha = T.tenv[1], rho = T.tenv[2];
+  const PhiloxKey key = philox_key(make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  const unsigned long long rglob = rir_base + (unsigned long long)T.rir;
+  const bool aligned = ((T.row & 3) == 0);
+  const long long qend = (long long)((nS + 3) >> 2);
+  for (long long q = (long long)(nISM >> 2) + tid; q < qend; q += nthreads)
+    tail_quad(q, nISM, nS, env0, alpha, rho, key, rglob, out + T.row, aligned);
+}
 
 template <int THREADS>
 struct alignas(16) PolySmem {
@@ -209,8 +241,15 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
                     A.ors ? A.ors + 3 * ms : zero3, A.spkr_pattern, A.lb, A.neg, A.zero, T.g, A.status);
         }
         T.row = row;
-        T.t0 = tile * kPolyTC;
-        T.te = min(T.t0 + kPolyTC, nISM);
+        T.rir = m;
+        if (A.jobs) {
+          T.t0 = tile * kPolyTC;
+          T.te = min(T.t0 + kPolyTC, nISM);
+        } else {  // single-room calls: tiles end-aligned, so the last one holds the whole envelope window
+          T.te = nISM - (A.nTiles - 1 - tile) * kPolyTC;
+          T.t0 = max(0, T.te - kPolyTC);
+        }
+        T.tail = A.poly_tail && !A.jobs && tile == A.nTiles - 1;
         T.tc = T.t0 + kPolyTC / 2;
         T.invLz = 1.0 / T.g.L[2];
         T.Lzs = T.g.L[2] * A.fs_over_c;
@@ -247,6 +286,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         // the tile takes the two-word scheme.
         const double ddx = T.g.s[0] - T.g.r[0], ddy = T.g.s[1] - T.g.r[1], ddz = T.g.s[2] - T.g.r[2];
         const double x_dp = sqrt(ddx * ddx + ddy * ddy + ddz * ddz) * A.fs_over_c;
+        T.x_dp = x_dp;
         const double x_lo = fmax(fmax((double)(T.t0 - m_hi), x_dp), 1e-30);
         const double x_hi = (double)(T.te - A.poly_mlo);
         const double Vs = T.g.L[0] * T.g.L[1] * T.g.L[2] * A.fs_over_c * A.fs_over_c * A.fs_over_c;
@@ -451,6 +491,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         if (k < T.te)
           A.out[T.row + k] = (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
       }
+      if (T.tail)
+        poly_fused_tail(sm.ti, red, tid, kPolyThreads, A.out, A.tail_nS, A.tail_win, A.tail_kappa_fs, A.tail_seed,
+                        A.tail_rir_base);
     }
     __syncthreads();  // G and the tile record are reused by the next work item
   }

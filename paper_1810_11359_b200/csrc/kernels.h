@@ -74,6 +74,12 @@ struct IsmArgs {
   int poly_ntaps, poly_mlo;
   int poly_gb;             // some tile of the call may need the two-word scheme: allocate the fine plane Gb
   int poly_force2;         // test hook (opts.split == -2): every tile uses the two-word scheme
+  // polyphase single-room calls: the diffuse tail fused into the kernel — the CTA that finishes a RIR's last
+  // (end-aligned) ISM tile, which holds the whole envelope window, writes that RIR's tail (tail_common.cuh)
+  int poly_tail;
+  int tail_win, tail_nS;
+  float tail_kappa_fs;
+  unsigned long long tail_seed, tail_rir_base;
 };
 
 struct TailArgs {
