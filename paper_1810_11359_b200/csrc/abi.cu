@@ -547,9 +547,10 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     A.poly_force2 = o.split == -2;
     A.poly_gb = A.poly_force2 || poly_two_word_for(room_sz, nISM, fs, c, o.Tw);
     // polyphase: the diffuse tail runs inside the ISM kernel when the envelope window (10 ms) fits the last
-    // 1024-sample tile; the separate tail kernel otherwise
+    // 1024-sample tile and the call has enough RIRs to spread the tails over the GPU (one CTA writes a whole
+    // tail); small calls keep the separate tail kernel, which splits each tail over many warps
     const int win = (int)llround(0.010 * fs);
-    fused_tail = poly && nISM < nS && win <= kPolyTile;
+    fused_tail = poly && nISM < nS && win <= kPolyTile && M >= 4LL * d->num_sms;
     if (fused_tail) {
       A.poly_tail = 1;
       A.tail_win = win;

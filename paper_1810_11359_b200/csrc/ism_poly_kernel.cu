@@ -242,10 +242,10 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         }
         T.row = row;
         T.rir = m;
-        if (A.jobs) {
+        if (A.jobs || !A.poly_tail) {
           T.t0 = tile * kPolyTC;
           T.te = min(T.t0 + kPolyTC, nISM);
-        } else {  // single-room calls: tiles end-aligned, so the last one holds the whole envelope window
+        } else {  // fused tail: tiles end-aligned, so the last one holds the whole envelope window
           T.te = nISM - (A.nTiles - 1 - tile) * kPolyTC;
           T.t0 = max(0, T.te - kPolyTC);
         }
