@@ -242,10 +242,12 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         }
         T.row = row;
         T.rir = m;
-        if (A.jobs || !A.poly_tail) {
+        if (A.jobs) {
           T.t0 = tile * kPolyTC;
           T.te = min(T.t0 + kPolyTC, nISM);
-        } else {  // fused tail: tiles end-aligned, so the last one holds the whole envelope window
+        } else {  // single-room calls: tiles end-aligned, so the last one holds the whole envelope window when
+                  // the tail is fused; also when it is not, because the fixed-point scale is per tile and a call
+                  // must give the same bits whether or not its tail is fused (shards of one call fuse or not by size)
           T.te = nISM - (A.nTiles - 1 - tile) * kPolyTC;
           T.t0 = max(0, T.te - kPolyTC);
         }

@@ -639,7 +639,9 @@ def test_poly_small_calls_take_direct_kernel(P, oracle):
 
 def test_poly_cta_shapes_bit_identical(P, oracle):
     """A large call (256-thread CTAs) and its 8 shards (512-thread CTAs, too few work items for the small
-    shape) give bit-identical RIRs: the aggregation is exact and each output's FIR arithmetic is fixed."""
+    shape) give bit-identical RIRs: the aggregation is exact and each output's FIR arithmetic is fixed.  The
+    large call also fuses the diffuse tail into the polyphase kernel (end-aligned tiles, M >= 4 x SMs) while
+    the shards use tail_kernel (start-aligned tiles), so this pins the fused tail to the separate one."""
     sc = W.cfg3(1024, "diffuse")
     beta, nb = derive(oracle, sc)
     full = run_gpu(P, sc, beta, nb, mode="poly")
