@@ -191,6 +191,29 @@ def test_host_call_matches_device_call(P, oracle, pinned):
     assert h.shape == ref.shape and np.array_equal(h, ref)
 
 
+@pytest.mark.parametrize("M", [591, 592, 2600])
+def test_fused_tail_threshold_bit_identical(P, oracle, M):
+    """The diffuse tail is fused into the polyphase kernel only for calls of >= 4 x 148 RIRs; on either side
+    of that threshold (591 / 592) and for a host call whose chunks straddle it (2600 = 2048 fused + 552 with
+    tail_kernel), the RIRs equal those of one device call bit for bit; sampled RIRs checked against the oracle."""
+    sc = W.cfg3(M, "diffuse")
+    beta, nb = derive(oracle, sc)
+    ref = run_gpu(P, sc, beta, nb, mode="poly").astype(np.float32)
+    if M == 2600:
+        got = P.simulate_rir_host(sc.room, beta, sc.pos_src, sc.pos_rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c,
+                                  orV_rcv=sc.orV_rcv, mic_pattern=sc.pattern, mode="poly", seed=sc.seed)
+        assert got.shape == ref.shape and np.array_equal(got, ref)
+    else:
+        half = M // 2  # two calls below the threshold: tail_kernel, and the same bits as the whole call
+        parts = [run_gpu(P, sc, beta, nb, mode="poly", rir_index_base=a, pos_rcv=sc.pos_rcv[a:b], orv=sc.orV_rcv[a:b])
+                 for a, b in ((0, half), (half, M))]
+        assert np.array_equal(ref, np.concatenate(parts, axis=1).astype(np.float32))
+    for m in (0, M - 1):
+        rj = oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[m:m + 1], nb, sc.Tdiff, sc.Tmax, fs=sc.fs,
+                                 pattern=sc.pattern, orV_rcv=sc.orV_rcv[m:m + 1], seed=sc.seed, rir_index_base=m)
+        assert rel_err(ref[0, m], rj[0, 0])[0] <= TOL["poly"], m
+
+
 def test_host_call_directional_source(P, oracle):
     """The host call with a directional (cardioid) source and receivers: equal to the device call (poly)."""
     import torch
