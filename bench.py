@@ -501,7 +501,7 @@ def main():
     tail_bytes = M_PER_GPU * (nS - nISM) * 4
     # polyphase mode writes the diffuse tail inside the ISM kernel (fs <= 102.4 kHz: the 10 ms envelope
     # window fits the last 1024-sample tile); the tail events then bracket nothing
-    fused_tail = args.mode == "poly" and round(0.010 * sc.fs) <= 1024 and M_PER_GPU >= 4 * 148
+    fused_tail = args.mode == "poly" and round(0.010 * sc.fs) <= 1024  # GPURIR_FUSE_MIN_PER_SM = 0 (abi.cu)
     tail_avg_s = max(float(np.mean(tail_ms)), 1e-9) / 1000.0
     hbm_peak = float(pk.get("hbm_gbs", 6650.0))
 
@@ -707,8 +707,8 @@ def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev):
         "ism_kernel": roof_ism,
         "e2e": {"value": e2e_value, "unit": "trajectories/s", "h2d_bytes_per_step": (h_src.numel() + h_rcv.numel() +
                 h_sig.numel()) * 4, "d2h_bytes_per_step": h_out[0].numel() * 4, "steps": e2e_steps},
-        # ISM, tail (fused into the polyphase ISM kernel on calls of >= 4 x 148 RIRs), trajectory filtering
-        "gpu_launches": (2 if (args.mode == "poly" and n_pts * n_mic >= 4 * 148 and round(0.010 * sc.fs) <= 1024)
+        # ISM, tail (fused into the polyphase ISM kernel), trajectory filtering
+        "gpu_launches": (2 if (args.mode == "poly" and round(0.010 * sc.fs) <= 1024)
                          else 3) * K,
         "clocks": clk.summary(),
     }

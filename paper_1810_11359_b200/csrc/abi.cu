@@ -230,6 +230,10 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
 // volume V, so about 4 pi d^2 (c / fs) / V images share one integer sample position at distance d.  With twice
 // that at the farthest ISM delay (+16) as the bound N, single-word accumulation with bits = 22 is used when
 // 2^22 N <= 2^30 (N <= 256); otherwise 0 selects the two-word scheme (2^28 resolution).
+#ifndef GPURIR_FUSE_MIN_PER_SM
+#define GPURIR_FUSE_MIN_PER_SM 0  // RIRs per SM from which the polyphase kernel writes the diffuse tail itself
+                                  // (A/B: fusing is faster at every M from 12 to 2048, so always)
+#endif
 constexpr long long kHostChunkMin = 2048;  // RIRs per chunk of gpurir_simulate_rir_host (fills the GPU)
 constexpr long long kPolyMinItems = 32;  // smaller polyphase calls take the direct fp32 kernels
 
@@ -547,10 +551,9 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     A.poly_force2 = o.split == -2;
     A.poly_gb = A.poly_force2 || poly_two_word_for(room_sz, nISM, fs, c, o.Tw);
     // polyphase: the diffuse tail runs inside the ISM kernel when the envelope window (10 ms) fits the last
-    // 1024-sample tile and the call has enough RIRs to spread the tails over the GPU (one CTA writes a whole
-    // tail); small calls keep the separate tail kernel, which splits each tail over many warps
+    // 1024-sample tile (and the call has GPURIR_FUSE_MIN_PER_SM RIRs per SM: 0, measured faster at every size)
     const int win = (int)llround(0.010 * fs);
-    fused_tail = poly && nISM < nS && win <= kPolyTile && M >= 4LL * d->num_sms;
+    fused_tail = poly && nISM < nS && win <= kPolyTile && M >= (long long)GPURIR_FUSE_MIN_PER_SM * d->num_sms;
     if (fused_tail) {
       A.poly_tail = 1;
       A.tail_win = win;

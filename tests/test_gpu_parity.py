@@ -193,9 +193,10 @@ def test_host_call_matches_device_call(P, oracle, pinned):
 
 @pytest.mark.parametrize("M", [591, 592, 2600])
 def test_fused_tail_threshold_bit_identical(P, oracle, M):
-    """The diffuse tail is fused into the polyphase kernel only for calls of >= 4 x 148 RIRs; on either side
-    of that threshold (591 / 592) and for a host call whose chunks straddle it (2600 = 2048 fused + 552 with
-    tail_kernel), the RIRs equal those of one device call bit for bit; sampled RIRs checked against the oracle."""
+    """Shards of a call and the chunks of a host call (2600 = 2048 + 552) give the bits of one device call, the
+    diffuse tail fused into the polyphase kernel or not: the fusion threshold GPURIR_FUSE_MIN_PER_SM is 0 (always
+    fused); an A/B build with 4 puts 591 / 592 and the host call's chunks on either side of it.
+    Sampled RIRs checked against the oracle."""
     sc = W.cfg3(M, "diffuse")
     beta, nb = derive(oracle, sc)
     ref = run_gpu(P, sc, beta, nb, mode="poly").astype(np.float32)
@@ -662,9 +663,8 @@ def test_poly_small_calls_take_direct_kernel(P, oracle):
 
 def test_poly_cta_shapes_bit_identical(P, oracle):
     """A large call (256-thread CTAs) and its 8 shards (512-thread CTAs, too few work items for the small
-    shape) give bit-identical RIRs: the aggregation is exact and each output's FIR arithmetic is fixed.  The
-    large call also fuses the diffuse tail into the polyphase kernel (end-aligned tiles, M >= 4 x SMs) while
-    the shards use tail_kernel (start-aligned tiles), so this pins the fused tail to the separate one."""
+    shape) give bit-identical RIRs: the aggregation is exact and each output's FIR arithmetic is fixed.  Both
+    fuse the diffuse tail into the polyphase kernel (tiles end-aligned for every single-room call)."""
     sc = W.cfg3(1024, "diffuse")
     beta, nb = derive(oracle, sc)
     full = run_gpu(P, sc, beta, nb, mode="poly")
