@@ -9,7 +9,15 @@ direct-tap kernel, which the line also reports as `direct_fp32`).  One step = on
 over the rank's 16384 receivers (ISM kernel + tail kernel).  Weak scaling: rank r owns receivers [16384 r, 16384 (r+1)) of the N*16384-receiver workload.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--mode poly|fp32|lut|fp16|lut_tex]
-                  [--workload ism|trajectory]
+                  [--workload ism|trajectory|cfg5] [--no-sweep] [--no-cpu-baseline]
+
+The default line also carries `sweep`: the points behind the metric's axes (the cfg3 #RIR sweep 1-16384 in
+both variants, the cfg2 T60 sweep, cfg4 (a/b) in every mode, the cfg1 single-RIR latency, config 5's 100 000
+rooms in one batch call, the trajectory job), device-timed in the same run, and `parity`: the timed step's
+output checked against the oracle RIRs that cpu_baseline computes.
+
+--workload cfg5 (BASELINE.json config 5, dataset generation): 100 000 random rooms LPT-sharded over the ranks
+(SURVEY §8(e)), one gpurir_simulate_rir_batch call per rank per step, no collective; strong scaling.
 
 --impl reference times the CPU oracle (oracle/, test infrastructure) on the host cores: the paper's
 comparison arm for this tier.
@@ -155,31 +163,67 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def lib_record(P, allow_override):
+    """Which libgpurir.so this run timed: path, sha256 prefix, version.  A GPURIR_LIB override (A/B variant
+    builds, tools/build_variant.sh) or a variant build is refused unless --ab-lib is given."""
+    import hashlib
+    path = os.path.abspath(P.LIB_PATH)
+    with open(path, "rb") as f:
+        sha = hashlib.sha256(f.read()).hexdigest()[:16]
+    ver = P.version()
+    default = os.path.abspath(os.path.join(ROOT, "paper_1810_11359_b200", "libgpurir.so"))
+    overridden = path != default or "variant" in ver
+    if overridden and not allow_override:
+        raise SystemExit(f"bench.py: refusing to time {path} ({ver}): not the in-tree build (pass --ab-lib for A/B)")
+    return {"path": os.path.relpath(path, ROOT), "sha256_16": sha, "version": ver, "override": overridden}
+
+
 # ----------------------------------------------------------------------------- oracle arms
 
-def oracle_rate(sc, beta, nb, n_rir, base_index=0):
-    """Time the CPU oracle (as it stands) on the first n_rir receivers of the workload; RIRs/s."""
+def oracle_rate(sc, beta, nb, n_rir, base_index=0, nthreads=0):
+    """Time the CPU oracle (as it stands) on the first n_rir receivers of the workload; (RIRs/s, s, RIRs)."""
     import oracle
     t = time.perf_counter()
-    oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[:n_rir], nb, sc.Tdiff, sc.Tmax, fs=sc.fs, c=sc.c,
-                        pattern=sc.pattern, orV_rcv=sc.orV_rcv[:n_rir], seed=sc.seed, rir_index_base=base_index)
+    h = oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[:n_rir], nb, sc.Tdiff, sc.Tmax, fs=sc.fs, c=sc.c,
+                            pattern=sc.pattern, orV_rcv=sc.orV_rcv[:n_rir], seed=sc.seed, rir_index_base=base_index,
+                            nthreads=nthreads)
     dt = time.perf_counter() - t
-    return n_rir / dt, dt
+    return n_rir / dt, dt, h
 
 
-def cpu_baseline(sc, budget_s=15.0):
+def cpu_baseline(sc, gpu_rows=None, budget_s=15.0):
+    """The oracle (oracle/, -O3 -march=native built on this host) on the host cores, on a bounded sample of the
+    workload: all cores, then one thread.  With gpu_rows (the timed step's output rows [M, nS] as a host array)
+    it also returns the step's parity against the oracle RIRs it just computed (reading C20)."""
     import oracle
+    oracle.use_native()
     beta, _ = oracle.beta_sabine(sc.room, sc.T60)
     beta = beta.astype(np.float32)
     nb = oracle.t2n(sc.Tdiff, sc.room, sc.c)
     cores = oracle.max_threads()
     n0 = max(cores, 8)
-    r0, dt0 = oracle_rate(sc, beta, nb, n0)
+    r0, dt0, _ = oracle_rate(sc, beta, nb, n0, nthreads=cores)
     n = int(min(len(sc.pos_rcv), max(n0, round(r0 * budget_s / cores) * cores)))
-    r, dt = oracle_rate(sc, beta, nb, n)
-    return {"value": r, "unit": "RIRs/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {n} of the {len(sc.pos_rcv)} receivers of the workload ({dt:.1f} s, OpenMP over RIRs, "
-                      f"fp64 C oracle, -O2)"}
+    if gpu_rows is not None:
+        n = min(n, len(gpu_rows))
+    r, dt, h = oracle_rate(sc, beta, nb, n, nthreads=cores)
+    n1 = max(1, int(round(r / cores * 3.0)))  # about 3 s on one thread
+    r1, dt1, _ = oracle_rate(sc, beta, nb, n1, nthreads=1)
+    out = {"value": r, "unit": "RIRs/s", "cores": cores, "kind": "oracle",
+           "sample": f"first {n} of the {len(sc.pos_rcv)} receivers of the workload ({dt:.1f} s, OpenMP over RIRs, "
+                     f"fp64 C oracle, {oracle.build_flags()})",
+           "single_thread": {"value": r1, "unit": "RIRs/s", "sample": f"first {n1} receivers, 1 thread ({dt1:.1f} s)"},
+           "cpu_model": oracle.cpu_model(), "build": oracle.build_flags()}
+    parity = None
+    if gpu_rows is not None:
+        g = gpu_rows[:n].astype(np.float64)
+        r_ = h.reshape(n, -1)
+        peak = np.abs(r_).max(axis=1)
+        err = np.abs(g - r_).max(axis=1) / np.where(peak > 0, peak, 1.0)
+        parity = {"max_err_over_peak": float(err.max()), "median_err_over_peak": float(np.median(err)), "n": n,
+                  "tol": 1e-4, "ok": bool(err.max() <= 1e-4),
+                  "what": f"the timed step's RIRs 0..{n - 1} (all samples, tail included) vs the oracle's (C20)"}
+    return out, parity
 
 
 def traj_oracle_times(sc, sig, n_rir, n_mic):
@@ -254,13 +298,14 @@ def run_reference(args):
         run_reference_trajectory(args)
         return
     import oracle
+    oracle.use_native()
     sc = W.cfg3(M_PER_GPU, "diffuse")
     beta, _ = oracle.beta_sabine(sc.room, sc.T60)
     beta = beta.astype(np.float32)
     nb = oracle.t2n(sc.Tdiff, sc.room, sc.c)
     cores = oracle.max_threads()
     per_step = max(cores, 16)
-    r0, dt0 = oracle_rate(sc, beta, nb, per_step)
+    r0, dt0, _ = oracle_rate(sc, beta, nb, per_step, nthreads=cores)
     # size each step so warmup + steps finish in ~2-3 minutes
     target = 150.0 / max(1, args.steps + args.warmup)
     per_step = int(min(M_PER_GPU, max(cores, round(r0 * target / cores) * cores)))
@@ -283,7 +328,8 @@ def run_reference(args):
                                        oracle.nsamples(sc.Tdiff, sc.fs)),
                            reference_arm=f"CPU oracle (oracle/oracle.c), each step {per_step} receivers of the workload"),
             "cpu_baseline": {"value": value, "unit": "RIRs/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{per_step} RIRs per step x {args.steps} steps"},
+                             "sample": f"{per_step} RIRs per step x {args.steps} steps",
+                             "build": oracle.build_flags(), "cpu_model": oracle.cpu_model()},
             "e2e": {"value": value, "unit": "RIRs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -301,7 +347,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 host path with several ranks on one GPU")
-    ap.add_argument("--workload", default="ism", choices=["ism", "trajectory"])
+    ap.add_argument("--workload", default="ism", choices=["ism", "trajectory", "cfg5"])
+    ap.add_argument("--no-sweep", action="store_true", help="skip the `sweep` points (configs 1-5)")
+    ap.add_argument("--ab-lib", action="store_true", help="allow timing a GPURIR_LIB override / variant build")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -327,8 +375,12 @@ def main():
         else:
             dist.init_process_group("gloo")
 
+    lib = lib_record(P, args.ab_lib)
     if args.workload == "trajectory":
-        run_trajectory(args, P, torch, dev, rank, world, dist, local_dev)
+        run_trajectory(args, P, torch, dev, rank, world, dist, local_dev, lib)
+        return
+    if args.workload == "cfg5":
+        run_cfg5(args, P, torch, dev, rank, world, dist, local_dev, lib)
         return
 
     # ---- workload (weak scaling: this rank's 16384 receivers of the N*16384 workload) ----
@@ -491,13 +543,13 @@ def main():
                  f"{f_clk / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)")
         kname = "ism_ws_kernel<0>" if args.mode == "fp32" else f"ism_ws_kernel ({args.mode})"
     lattice = float(np.prod(nb.astype(np.float64)))
-    traffic = None
+    prof = {}
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ism_traffic.json")) as f:
-            tj = json.load(f)
-        traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
+        with open(os.path.join(ROOT, "profiles", "r02_ism_profile.json")) as f:
+            prof = json.load(f)
     except Exception:
         pass
+    traffic = (prof["dram_read_bytes"] + prof["dram_write_bytes"]) if prof else None
     tail_bytes = M_PER_GPU * (nS - nISM) * 4
     # polyphase mode writes the diffuse tail inside the ISM kernel (fs <= 102.4 kHz: the 10 ms envelope
     # window fits the last 1024-sample tile); the tail events then bracket nothing
@@ -505,6 +557,26 @@ def main():
     tail_avg_s = max(float(np.mean(tail_ms)), 1e-9) / 1000.0
     hbm_peak = float(pk.get("hbm_gbs", 6650.0))
 
+    # the polyphase kernel's binding resource is the shared-memory pipe: its roofline counts
+    # shared-memory wavefronts per launch (one per SM per clock), the bank-conflict-free count as the
+    # algorithmic figure and the measured one (conflict replays included) as the traffic, both from the ncu
+    # capture of this step's launch (profiles/r02_ism_profile.json), over the live kernel time
+    wf_peak = 148 * f_clk
+    if args.mode == "poly" and prof.get("smem_wavefronts"):
+        roof_main = {"bound": "smem", "achieved": prof["smem_wavefronts_ideal"] / ism_avg_s / 1e9,
+                     "peak": wf_peak / 1e9, "unit": "G shared-memory wavefronts/s",
+                     "frac": prof["smem_wavefronts_ideal"] / ism_avg_s / wf_peak,
+                     "traffic": prof["smem_wavefronts"], "traffic_unit": "wavefronts per launch (measured)",
+                     "frac_measured": prof["smem_wavefronts"] / ism_avg_s / wf_peak,
+                     "kernel": kname, "dram_traffic": traffic,
+                     "basis": f"bank-conflict-free wavefronts per launch {prof['smem_wavefronts_ideal']:.4g} "
+                              f"(measured {prof['smem_wavefronts']:.4g}, {prof['smem_bank_conflicts']:.3g} of them "
+                              f"conflict replays; ncu, profiles/r02_ism_profile.json) / live ism_ms; peak = 148 SM x 1 "
+                              f"wavefront/clk x {f_clk / 1e6:.0f} MHz ({pk_kind} sm_max_mhz)"}
+    else:
+        roof_main = {"bound": "alu", "achieved": achieved / 1e12, "peak": issue_peak / 1e12,
+                     "unit": "T FP32-lane-issue-slots/s", "frac": achieved / issue_peak, "traffic": traffic,
+                     "kernel": kname, "basis": basis}
     line = {
         "metric": METRIC, "value": value, "unit": "RIRs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -513,10 +585,11 @@ def main():
         "image_contributions_per_s": value * lattice,
         "taps_per_s": world * taps_launch / ism_avg_s if world == 1 else None,
         "ism_ms": float(np.mean(ism_ms)),
-        "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": issue_peak / 1e12,
-                     "unit": "T FP32-lane-issue-slots/s", "frac": achieved / issue_peak, "traffic": traffic,
-                     "traffic_note": "DRAM bytes per launch from profiles/r01_ism_traffic.json (ncu --set full)",
-                     "kernel": kname, "basis": basis},
+        "roofline": roof_main,
+        "roofline_alu": {"bound": "alu", "achieved": achieved / 1e12, "peak": issue_peak / 1e12,
+                         "unit": "T FP32-lane-issue-slots/s", "frac": achieved / issue_peak, "traffic": traffic,
+                         "traffic_note": "DRAM bytes per launch from profiles/r02_ism_profile.json (ncu --set full)",
+                         "kernel": kname, "basis": basis},
         "tail_kernel": ({"fused_into": "ism_poly_kernel", "bytes": tail_bytes,
                          "note": "the CTA that finishes a RIR's last (end-aligned) ISM tile writes its diffuse tail; "
                                  "its time is inside ism_ms"} if fused_tail else
@@ -536,11 +609,130 @@ def main():
     if args.mode == "poly":  # the direct-tap fp32 kernel on the same step, for the A/B (not part of `value`)
         line["direct_fp32"] = direct_ab(P, torch, sc, beta, nb, src, rcv, orv, base, out, flush, stream,
                                         taps_launch, issue_peak)
+    line["lib"] = lib
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(W.cfg3(M_PER_GPU, "diffuse"))
+        rows = out[0, :8192].cpu().numpy()
+        line["cpu_baseline"], line["parity"] = cpu_baseline(W.cfg3(M_PER_GPU, "diffuse"), gpu_rows=rows)
+    if not args.no_sweep and world == 1:
+        line["sweep"] = sweep(P, torch, dev, flush)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def _time_calls(torch, fn, flush, reps=5, warm=2, events=None):
+    """Median device ms of fn() over reps calls (CUDA events on the current stream, L2 flushed between calls
+    outside the events).  With events=(start, end) RawEvent pairs from fn, those bracket the device work."""
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        ev = fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(ev[0].elapsed_ms(ev[1]) if isinstance(ev, tuple) else a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def _latency_us(torch, fn, n=50):
+    """Back-to-back calls (no flush): device µs per call, the small-call latency of configs 1, 2, 4."""
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(n):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1000.0 / n
+
+
+def sweep(P, torch, dev, flush):
+    """The points behind the metric's axes (BASELINE.json configs 1-5: #RIRs and T60), device-timed in this run:
+    median ms per call, RIRs/s and lattice image contributions/s (the paper's work unit)."""
+    rows = []
+
+    def scene(sc, mode):
+        beta, _ = P.beta_sabine(sc.room, sc.T60, clamp=sc.clamp)
+        nb = P.t2n(sc.nb_time if sc.nb_time is not None else max(sc.Tdiff, 1e-6), sc.room, sc.c)
+        src = torch.from_numpy(sc.pos_src).to(dev)
+        rcv = torch.from_numpy(np.ascontiguousarray(sc.pos_rcv)).to(dev)
+        orv = torch.from_numpy(np.ascontiguousarray(sc.orV_rcv)).to(dev) if sc.orV_rcv is not None else None
+        out = torch.empty((src.shape[0], rcv.shape[0], P.nsamples(sc.Tmax, sc.fs)), dtype=torch.float32, device=dev)
+
+        def fn():
+            P.simulate_rir(sc.room, beta, src, rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=orv,
+                           mic_pattern=sc.pattern, mode=mode, seed=sc.seed, out=out)
+        return fn, float(np.prod(nb.astype(np.float64))), src.shape[0] * rcv.shape[0]
+
+    def point(cfg, sc, mode, reps=5, warm=2, **kw):
+        fn, lat, M = scene(sc, mode)
+        ms = _time_calls(torch, fn, flush, reps, warm)
+        rows.append(dict(cfg=cfg, mode=mode, M=M, ms=ms, rirs_per_s=M / ms * 1e3, lattice_per_s=M * lat / ms * 1e3, **kw))
+        return fn
+
+    t0 = time.time()
+    for mode in ("poly", "fp32", "lut", "fp16", "lut_tex"):  # config 1: one RIR, ISM only — latency
+        fn = point("cfg1", W.cfg1(), mode, reps=10, warm=3)
+        rows[-1]["us_per_call_back_to_back"] = _latency_us(torch, fn)
+    for T60 in W.CFG2_T60:  # config 2: T60 sweep, one RIR, ISM + tail
+        fn = point("cfg2", W.cfg2(T60), "poly", reps=7, warm=3, T60=T60)
+        rows[-1]["us_per_call_back_to_back"] = _latency_us(torch, fn, 20)
+    for M in (1, 4, 16, 64, 256, 1024, 4096, 16384):  # config 3 (i): #RIR sweep, diffuse
+        point("cfg3_diffuse", W.cfg3(M, "diffuse"), "poly", reps=5 if M < 4096 else 3)
+    for mode in ("fp32", "lut", "fp16", "lut_tex"):
+        point("cfg3_diffuse", W.cfg3(4096, "diffuse"), mode, reps=3, warm=1)
+    for M in (1, 16, 128, 1024):  # config 3 (ii): #RIR sweep, full ISM to 0.7 s
+        point("cfg3_full", W.cfg3(M, "full"), "poly", reps=3, warm=1)
+    point("cfg3_full", W.cfg3(128, "full"), "fp32", reps=3, warm=1)
+    for variant in ("a", "b"):  # config 4: 32-mic array at 48 kHz, every mode
+        for mode in ("poly", "fp32", "lut", "fp16", "lut_tex"):
+            point(f"cfg4{variant}", W.cfg4(variant), mode, reps=5, warm=2)
+    # config 5: 100 000 rooms in one batch call (device time between the call's first and last kernel events;
+    # the host planning of the call is reported beside it)
+    rb = W.cfg5(100_000)
+    th = time.time()
+    rooms, off, lattice = [], 0, 0.0
+    for i in range(rb.n):
+        beta, _ = P.beta_sabine(rb.room[i], rb.T60[i])
+        nb = P.t2n(rb.Tdiff[i], rb.room[i])
+        lattice += float(np.prod(nb.astype(np.float64)))
+        rooms.append(dict(room_sz=rb.room[i], beta=beta, pos_src=rb.pos_src[i], pos_rcv=rb.pos_rcv[i], nb_img=nb,
+                          Tdiff=rb.Tdiff[i], Tmax=rb.Tmax[i], out_offset=off))
+        off += P.nsamples(rb.Tmax[i], rb.fs)
+    arr = P.room_array(rooms)
+    build_s = time.time() - th
+    outb = torch.empty(off, dtype=torch.float32, device=dev)
+    for mode in ("poly", "fp32"):
+        def fn5(mode=mode):
+            e = (RawEvent(), RawEvent()), (RawEvent(), RawEvent())
+            P.simulate_rir_batch(arr, rb.fs, outb, seed=rb.seed, mode=mode, ev_ism=e[0], ev_tail=e[1])
+            return e[0][0], e[1][1]
+        tc = time.time()
+        ms = _time_calls(torch, fn5, flush, reps=3, warm=1, events=True)
+        call_s = (time.time() - tc) / 4
+        rows.append(dict(cfg="cfg5", mode=mode, M=rb.n, ms=ms, rirs_per_s=rb.n / ms * 1e3,
+                         lattice_per_s=lattice / ms * 1e3, samples=off, host_call_ms=call_s * 1e3,
+                         note="device time from the ISM kernel's start event to the tail's end event; the call's "
+                              "host planning + staging (host_call_ms) precedes it"))
+    del outb
+    # NEXT row f1: the trajectory filter alone, 1 s at 16 kHz, 100 points x 32 mics, 0.7 s RIRs
+    n_sig, n_pts, n_mics, L = 16000, 100, 32, 11200
+    g = torch.Generator(device=dev).manual_seed(11)
+    sig = torch.randn(n_sig, device=dev, generator=g)
+    rirs = torch.randn((n_pts, n_mics, L), device=dev, generator=g) * 1e-2
+    outt = torch.empty((n_mics, n_sig + L - 1), device=dev)
+    ms = _time_calls(torch, lambda: P.simulate_trajectory(sig, rirs, out=outt), flush, reps=5, warm=2)
+    rows.append(dict(cfg="traj_f1", n_sig=n_sig, points=n_pts, mics=n_mics, L=L, ms=ms,
+                     macs_per_s=n_sig * L * n_mics / ms * 1e3))
+    return {"rows": rows, "seconds": time.time() - t0, "cfg5_room_list_build_s": build_s,
+            "timing": "median device ms per call (CUDA events, inputs resident, 256 MB L2 flush between calls); "
+                      "us_per_call_back_to_back = device time of 20-50 back-to-back calls / n"}
 
 
 def direct_ab(P, torch, sc, beta, nb, src, rcv, orv, base, out, flush, stream, taps_launch, issue_peak, steps=5):
@@ -565,7 +757,7 @@ def direct_ab(P, torch, sc, beta, nb, src, rcv, orv, base, out, flush, stream, t
             "roofline_frac": ach / issue_peak, "kernel": "ism_ws_kernel<0>", "steps": steps}
 
 
-def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev):
+def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev, lib):
     """--workload trajectory: one moving-source job per step (RIRs of all trajectory points + filtering)."""
     sc = W.traj1()
     n_sig = sc.meta["n_sig"]
@@ -711,15 +903,144 @@ def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev):
         "gpu_launches": (2 if (args.mode == "poly" and round(0.010 * sc.fs) <= 1024)
                          else 3) * K,
         "clocks": clk.summary(),
+        "lib": lib,
     }
     if not args.no_cpu_baseline and world == 1:
         import oracle
+        oracle.use_native()
         cores = oracle.max_threads()
         nr, nm = traj_oracle_sample(sc, sig_h, cores, 15.0)
         per_traj, nr, nm, spent = traj_oracle_times(sc, sig_h, nr, nm)
         line["cpu_baseline"] = {"value": 1.0 / per_traj, "unit": "trajectories/s", "cores": cores, "kind": "oracle",
                                 "sample": f"{nr} of the {sc.M} RIRs + filtering of {nm} of {n_mic} microphones, "
                                           f"scaled to one trajectory ({spent:.1f} s)"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_cfg5(args, P, torch, dev, rank, world, dist, local_dev, lib):
+    """--workload cfg5 (BASELINE.json config 5): dataset generation, 100 000 random rooms LPT-sharded over the
+    ranks (no collective on the path, every room keeps its global rir_index), one batch call per
+    rank per step.  value = 100 000 rooms / (max over ranks of the step's device time): strong scaling."""
+    from paper_1810_11359_b200 import shard
+    rb = W.cfg5(100_000)
+    rooms, costs, ns, lattice = [], [], [], 0.0
+    for i in range(rb.n):
+        beta, _ = P.beta_sabine(rb.room[i], rb.T60[i])
+        nb = P.t2n(rb.Tdiff[i], rb.room[i])
+        n_i = P.nsamples(rb.Tmax[i], rb.fs)
+        lattice += float(np.prod(nb.astype(np.float64)))
+        rooms.append(dict(room_sz=rb.room[i], beta=beta, pos_src=rb.pos_src[i], pos_rcv=rb.pos_rcv[i], nb_img=nb,
+                          Tdiff=rb.Tdiff[i], Tmax=rb.Tmax[i], rir_index=i, n=n_i))
+        costs.append(shard.room_cost(rb.room[i], rb.Tdiff[i], rb.Tmax[i], rb.fs))
+        ns.append(n_i)
+    plan = shard.lpt_plan(costs, world)
+    idx, mine, tot = shard.batch_shard(rooms, costs, world, rank)
+    arr = P.room_array(mine)
+    out = torch.empty((tot,), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        P.simulate_rir_batch(arr, rb.fs, out, seed=rb.seed, mode=args.mode, stream=stream,
+                             ev_ism=ev[0] if ev else None, ev_tail=ev[1] if ev else None)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    K = args.steps
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    kev = [((RawEvent(), RawEvent()), (RawEvent(), RawEvent())) for _ in range(K)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_dev) as clk:
+        for i in range(K):
+            flush.zero_()
+            ev_s[i].record(stream)
+            step(kev[i])
+            ev_e[i].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
+    dev_ms = [k[0][0].elapsed_ms(k[1][1]) for k in kev]
+    red_dev = dev if args.dist_backend == "nccl" else "cpu"
+    tot_t = torch.tensor([sum(step_ms), sum(dev_ms)], dtype=torch.float64, device=red_dev)
+    if dist:
+        dist.all_reduce(tot_t, op=dist.ReduceOp.MAX)
+    total_ms, total_dev_ms = float(tot_t[0].item()), float(tot_t[1].item())
+    value = rb.n * K / (total_ms / 1000.0)
+
+    # e2e through the public API from host memory: the room list in, every RIR of this rank back into pinned
+    # host memory (D2H inside the timed region)
+    e2e_steps = max(2, min(args.e2e_steps, 3))
+    h_out = torch.empty((tot,), dtype=torch.float32).pin_memory()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        step()
+        h_out.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=red_dev)
+    if dist:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = rb.n * e2e_steps / (float(e2e_t.item()) / 1000.0)
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "RIRs/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "cfg5_100k_random_rooms_T60_0.2-1.5_fs16k", "rooms": rb.n, "rooms_rank0": len(idx),
+                   "plan": "LPT on estimated room cost (shard.lpt_plan)",
+                   "imbalance": shard.plan_imbalance(costs, plan), "mode": args.mode, "fs": rb.fs,
+                   "samples_total": int(sum(ns)), "samples_rank0": tot,
+                   "l2": "256 MB buffer written between timed steps (L2 126 MB); step output 5.4 GB"},
+        "device_ms_per_step": total_dev_ms / K,
+        "image_contributions_per_s": lattice * K / (total_ms / 1000.0),
+        "e2e": {"value": e2e_value, "unit": "RIRs/s", "h2d_bytes_per_step": len(idx) * 160,
+                "d2h_bytes_per_step": tot * 4, "steps": e2e_steps,
+                "call": "gpurir_simulate_rir_batch (host room list, job table staged + uploaded inside the call) + "
+                        "D2H of every RIR of the rank into pinned host memory"},
+        "gpu_launches": K * (1 if args.mode == "poly" else 2),
+        "clocks": clk.summary(), "lib": lib,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        import oracle
+        oracle.use_native()
+        cores = oracle.max_threads()
+        t = time.perf_counter()
+        n_done, errs = 0, []
+        starts = np.concatenate([[0], np.cumsum([r["n"] for r in (rooms[i] for i in idx)])])
+        sample = list(range(0, len(idx), max(1, len(idx) // 2000)))
+        for j in sample:  # rooms spread over the shard until ~15 s of oracle time
+            i = idx[j]
+            r = rooms[i]
+            h = oracle.simulate_rir(r["room_sz"], r["beta"], np.asarray(r["pos_src"], np.float32)[None],
+                                    np.asarray(r["pos_rcv"], np.float32)[None], r["nb_img"], r["Tdiff"], r["Tmax"],
+                                    fs=rb.fs, seed=rb.seed, rir_index_base=i)[0, 0]
+            g = out[int(starts[j]):int(starts[j]) + h.size].cpu().numpy().astype(np.float64)
+            errs.append(float(np.abs(g - h).max() / max(np.abs(h).max(), 1e-300)))
+            n_done += 1
+            if time.perf_counter() - t > 15.0:
+                break
+        dt = time.perf_counter() - t
+        line["cpu_baseline"] = {"value": n_done / dt, "unit": "RIRs/s", "cores": 1, "kind": "oracle",
+                                "sample": f"{n_done} rooms spread over the workload, one oracle call each ({dt:.1f} s; "
+                                          f"a single-RIR call runs on one thread)", "build": oracle.build_flags(),
+                                "cpu_model": oracle.cpu_model(), "host_cores": cores}
+        line["parity"] = {"max_err_over_peak": max(errs), "n": n_done, "tol": 1e-4, "ok": max(errs) <= 1e-4,
+                          "what": "the timed step's RIRs of the sampled rooms vs the oracle (C20)"}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

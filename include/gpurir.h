@@ -40,7 +40,11 @@ typedef enum {
   GPURIR_EDEGENERATE = 2,  /* an image source coincides with a receiver, d_n = 0 */
   GPURIR_EINFEASIBLE = 3,  /* Sabine target T60 below the room's minimum */
   GPURIR_ENOMEM = 4,       /* device allocation failed */
-  GPURIR_ECUDA = 5         /* CUDA runtime error; see gpurir_last_cuda_error() */
+  GPURIR_ECUDA = 5,        /* CUDA runtime error; see gpurir_last_cuda_error() */
+  GPURIR_ECAPACITY = 6     /* capacity: GPURIR_POLY found more images on one sample position of a tile
+                              than its exact integer sums can hold (2^17 in the two-word format; 2^(31 - bits)
+                              in the single-word one when the call's CTAs have no room for the two-word redo)
+                              — reported instead of a wrapped sum; re-run with opts->split = -2 */
 } gpurir_status;
 
 /* Receiver polar patterns, g = a + (1 - a) cos(theta) (reading C4). */
@@ -64,8 +68,9 @@ typedef enum {
   GPURIR_POLY = 4     /* Eq. 6 by its polyphase expansion (reading R11): every image adds
                         A_n T_d(2 phi_n - 1), d = 0..7, to the integer sample floor(x_n) (exact
                         fixed-point sums with a per-tile scale: one int32 word per channel, two for tiles
-                        whose bound on images per sample reaches 2^14; deterministic), then an
-                        8-channel FIR of 2H taps, whose
+                        whose estimate of images per sample reaches 2^12; deterministic; a tile whose exact
+                        per-sample image count reaches its word's capacity is redone wider, never wrapped —
+                        GPURIR_ECAPACITY past 2^17), then an 8-channel FIR of 2H taps, whose
                         coefficients expand delta'(m - phi) in Chebyshev polynomials (max error 4.3e-7),
                         produces the RIR.  fp32 arithmetic; fp32 tolerance.  Requires Tw fs <= 1022.
                         Calls with fewer than 32 work items of 1024 samples (a lone RIR) run the direct
@@ -83,10 +88,20 @@ typedef struct {
   void* stream;             /* cudaStream_t to launch on; NULL = the legacy default stream          */
   int split;                /* CTAs cooperating on one time tile (thread-block cluster), 0 = auto;
                                < 0 forces the persistent kernel (fp32/LUT/fp16) or the polyphase kernel;
-                               -2 also forces the polyphase two-word scheme on every tile (test hook) */
+                               test hooks of GPURIR_POLY: -2 two-word scheme on every tile; -3 a count capacity
+                               of 4 images per sample position on the first pass (exercises the overflow
+                               guard: redo in two words, or GPURIR_ECAPACITY for a call launched without the
+                               fine plane); -5 two-word tiles with that capacity (GPURIR_ECAPACITY) */
   unsigned flags;           /* GPURIR_FLAG_*                                                        */
   void* ev_ism[2];          /* optional cudaEvent_t pair recorded on `stream` around the ISM kernel  */
   void* ev_tail[2];         /* optional cudaEvent_t pair recorded around the diffuse-tail kernel     */
+  void* workspace;          /* optional caller-owned device scratch of gpurir_simulate_rir_batch, 256-B
+                               aligned, >= gpurir_workspace_bytes() bytes (EINVAL otherwise); NULL = the
+                               stream-ordered pool (cudaMallocAsync / cudaFreeAsync on `stream`)          */
+  size_t workspace_bytes;   /* its size                                                               */
+  int* status;              /* optional caller-owned device int, zero-initialised: this call's status
+                               word (device-side errors, read with GPURIR_FLAG_SYNC) instead of the
+                               device's shared one — calls in flight on several streams stay separate    */
 } gpurir_opts;
 
 /* Fill *opts with the defaults above. */
@@ -168,17 +183,31 @@ typedef struct {
   long long out_offset;
   float orV_src[3]; /* source orientation (f3), ignored for an omni source */
   int spkr_pattern; /* source gpurir_pattern (f3), GPURIR_OMNI = 0 for the paper's omni source */
+  unsigned long long rir_index; /* this RIR's index in the whole job: its tail RNG stream is
+                                   opts->rir_index_base + rir_index (reading C16), so a shard of rooms in any
+                                   order reproduces the unsharded bits */
 } gpurir_room;
 
 /*
- * gpurir_simulate_rir_batch — one RIR per room for n_rooms independent rooms.
- *   rooms  host gpurir_room[n_rooms] (copied to the device inside the call, stream-ordered)
+ * gpurir_simulate_rir_batch — one RIR per room for n_rooms independent rooms (config 5: dataset generation;
+ * P:167 batches only RIRs of one room, the rooms of a dataset are as independent).
+ *   rooms  host gpurir_room[n_rooms], read before return (planned on the host: a job table and a heavy-first
+ *          tile list, uploaded through a pinned staging buffer by an asynchronous copy on opts->stream)
  *   out    device float buffer; room i writes out[rooms[i].out_offset + k], 0 <= k < ceil(Tmax_i fs)
- *   The tail RNG stream of room i is rir_index_base + i.
- * Errors as gpurir_simulate_rir; ENOMEM if the internal job table cannot be allocated.
+ *   The tail RNG stream of room i is opts->rir_index_base + rooms[i].rir_index.
+ * Stream-ordered: returns without synchronising (unless GPURIR_FLAG_SYNC); device scratch from
+ * opts->workspace or the stream-ordered pool.  In GPURIR_POLY mode a room's RIR equals, bit for bit, the same
+ * room simulated alone by gpurir_simulate_rir_dir (the tiles are end-aligned per room in both), and the
+ * diffuse tail is written by the polyphase kernel (one launch per call).
+ * Errors as gpurir_simulate_rir; ENOMEM if the workspace or the staging buffer cannot be allocated; EINVAL
+ * for a caller workspace below gpurir_workspace_bytes() or not 256-B aligned.
  */
 int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, float* out,
                               const gpurir_opts* opts);
+
+/* Device workspace (bytes) gpurir_simulate_rir_batch needs for these rooms and options (job table, tile and
+ * chunk lists: about 100 B per room); 0 for invalid arguments.  Single-room calls need no workspace. */
+size_t gpurir_workspace_bytes(int n_rooms, const gpurir_room* rooms, double fs, double c, const gpurir_opts* opts);
 
 /*
  * gpurir_simulate_trajectory — a moving source recorded by a microphone array (§3.4,

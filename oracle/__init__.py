@@ -32,6 +32,42 @@ def build(force: bool = False) -> str:
     return LIB_PATH
 
 
+_native_path = None
+
+
+def use_native() -> str:
+    """Switch this process to an -O3 -march=native build of oracle.c (bench.py's timed oracle arms only; the
+    arithmetic is the same source).  Built where it runs, in the temp directory, because -march=native code
+    from another host may not execute on this one.  Call before the first oracle function."""
+    global _native_path, _lib
+    import tempfile
+    tag = f"{int(os.path.getmtime(SRC_PATH))}_{os.uname().nodename}"
+    path = os.path.join(tempfile.gettempdir(), f"liboracle_native_{tag}.so")
+    if not os.path.exists(path):
+        tmp = path + f".{os.getpid()}"
+        subprocess.run(["gcc", "-O3", "-march=native", "-fopenmp", "-fPIC", "-shared", "-o", tmp, SRC_PATH, "-lm"],
+                       check=True)
+        os.replace(tmp, path)
+    _native_path = path
+    _lib = None
+    return path
+
+
+def build_flags() -> str:
+    return "-O3 -march=native" if _native_path else "-O2"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 class OracleError(RuntimeError):
     def __init__(self, status: int, where: str):
         super().__init__(f"{where}: oracle status {status} ({STATUS.get(status, '?')})")
@@ -44,8 +80,9 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(LIB_PATH)
+        if _native_path is None:
+            build()
+        L = C.CDLL(_native_path or LIB_PATH)
         dp = C.POINTER(C.c_double)
         ip = C.POINTER(C.c_int)
         L.oracle_nsamples.restype = C.c_long

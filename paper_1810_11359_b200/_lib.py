@@ -11,7 +11,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GPURIR_LIB", os.path.join(_HERE, "libgpurir.so"))  # override: A/B builds only
 
-OK, EINVAL, EDEGENERATE, EINFEASIBLE, ENOMEM, ECUDA = range(6)
+OK, EINVAL, EDEGENERATE, EINFEASIBLE, ENOMEM, ECUDA, ECAPACITY = range(7)
 FLAG_SYNC = 1
 MODES = {"fp32": 0, "lut": 1, "fp16": 2, "lut_tex": 3, "poly": 4}
 PATTERNS = {"omni": 0, "subcardioid": 1, "cardioid": 2, "hypercardioid": 3, "bidirectional": 4}
@@ -22,21 +22,22 @@ EXPORTS = [
     "gpurir_sabine_t60", "gpurir_beta_sabine", "gpurir_att2t_sabine", "gpurir_t2n", "gpurir_image_params",
     "gpurir_lut_table", "gpurir_device_status", "gpurir_strerror", "gpurir_last_cuda_error", "gpurir_version",
     "gpurir_simulate_trajectory", "gpurir_simulate_rir_dir", "gpurir_beta_sabine_weighted", "gpurir_poly_table",
-    "gpurir_simulate_rir_host",
+    "gpurir_simulate_rir_host", "gpurir_workspace_bytes",
 ]
 
 
 class Opts(C.Structure):
     _fields_ = [("mode", C.c_int), ("Tw", C.c_double), ("lut_Q", C.c_int), ("seed", C.c_uint64),
                 ("rir_index_base", C.c_uint64), ("stream", C.c_void_p), ("split", C.c_int), ("flags", C.c_uint),
-                ("ev_ism", C.c_void_p * 2), ("ev_tail", C.c_void_p * 2)]
+                ("ev_ism", C.c_void_p * 2), ("ev_tail", C.c_void_p * 2), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t), ("status", C.c_void_p)]
 
 
 class Room(C.Structure):
     _fields_ = [("room_sz", C.c_float * 3), ("beta", C.c_float * 6), ("pos_src", C.c_float * 3),
                 ("pos_rcv", C.c_float * 3), ("orV_rcv", C.c_float * 3), ("mic_pattern", C.c_int),
                 ("nb_img", C.c_int * 3), ("Tdiff", C.c_double), ("Tmax", C.c_double), ("out_offset", C.c_longlong),
-                ("orV_src", C.c_float * 3), ("spkr_pattern", C.c_int)]
+                ("orV_src", C.c_float * 3), ("spkr_pattern", C.c_int), ("rir_index", C.c_ulonglong)]
 
 
 class GpurirError(RuntimeError):
@@ -75,6 +76,8 @@ def lib() -> C.CDLL:
     L.gpurir_beta_sabine_weighted.argtypes = [fp, C.c_double, fp, C.c_int, C.c_int, fp, ip]
     L.gpurir_simulate_rir_batch.restype = C.c_int
     L.gpurir_simulate_rir_batch.argtypes = [C.c_int, C.POINTER(Room), C.c_double, C.c_double, vp, C.POINTER(Opts)]
+    L.gpurir_workspace_bytes.restype = C.c_size_t
+    L.gpurir_workspace_bytes.argtypes = [C.c_int, C.POINTER(Room), C.c_double, C.c_double, C.POINTER(Opts)]
     L.gpurir_simulate_trajectory.restype = C.c_int
     L.gpurir_simulate_trajectory.argtypes = [vp, C.c_longlong, vp, C.c_int, C.c_int, C.c_longlong, vp, C.POINTER(Opts)]
     L.gpurir_nsamples.restype = C.c_longlong

@@ -46,7 +46,7 @@ def _stream_handle(stream) -> int | None:
 
 
 def make_opts(mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0, stream=None, split=0, sync=False,
-              ev_ism=None, ev_tail=None) -> Opts:
+              ev_ism=None, ev_tail=None, workspace=None, status=None) -> Opts:
     o = Opts()
     lib().gpurir_opts_default(C.byref(o))
     o.mode = _mode(mode)
@@ -61,7 +61,18 @@ def make_opts(mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0, stream=N
         o.ev_ism[0], o.ev_ism[1] = ev_ism[0].cuda_event, ev_ism[1].cuda_event
     if ev_tail is not None:
         o.ev_tail[0], o.ev_tail[1] = ev_tail[0].cuda_event, ev_tail[1].cuda_event
+    if workspace is not None:  # caller-owned device scratch (uint8 CUDA tensor) of the batch call
+        o.workspace = workspace.data_ptr()
+        o.workspace_bytes = workspace.numel() * workspace.element_size()
+    if status is not None:  # caller-owned device int32 status word of this call
+        o.status = status.data_ptr()
     return o
+
+
+def _on_device(t):
+    """The calling thread's current device is the library's device (gpurir.h conventions): switch to t's."""
+    import torch
+    return torch.cuda.device(t.device)
 
 
 def nsamples(T: float, fs: float) -> int:
@@ -104,6 +115,17 @@ def simulate_rir(room_sz, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs, c=343
         out = torch.empty((Ms, Mr, nS), dtype=torch.float32, device=pos_src.device)
     elif out.dtype != torch.float32 or not out.is_contiguous() or out.numel() < Ms * Mr * nS:
         raise ValueError("out must be contiguous float32 with M_src*M_rcv*nSamples elements")
+    for t, nm in ((pos_rcv, "pos_rcv"), (orV_rcv, "orV_rcv"), (orV_src, "orV_src"), (out, "out")):
+        if t is not None and t.device != pos_src.device:
+            raise ValueError(f"{nm} must be on {pos_src.device}")
+    with _on_device(pos_src):
+        return _simulate_rir(room_sz, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs, c, orV_rcv, pat, mode, Tw,
+                             lut_Q, seed, rir_index_base, out, stream, split, sync, ev_ism, ev_tail, orV_src, spat,
+                             Ms, Mr)
+
+
+def _simulate_rir(room_sz, beta, pos_src, pos_rcv, nb_img, Tdiff, Tmax, fs, c, orV_rcv, pat, mode, Tw, lut_Q, seed,
+                  rir_index_base, out, stream, split, sync, ev_ism, ev_tail, orV_src, spat, Ms, Mr):
     o = make_opts(mode, Tw, lut_Q, seed, rir_index_base, stream, split, sync, ev_ism, ev_tail)
     ov = orV_rcv.data_ptr() if orV_rcv is not None else None
     if spat == 0 and orV_src is None:
@@ -185,18 +207,38 @@ def room_array(rooms) -> C.Array:
         R.Tdiff = float(r["Tdiff"])
         R.Tmax = float(r["Tmax"])
         R.out_offset = int(r["out_offset"])
+        R.rir_index = int(r.get("rir_index", i))  # tail RNG stream: rir_index_base + rir_index (reading C16)
     return arr
 
 
+def _batch_need(arr, fs) -> int:
+    """Elements of `out` the rooms write: max(out_offset + ceil(Tmax fs))."""
+    return max((R.out_offset + nsamples(R.Tmax, fs) for R in arr), default=0)
+
+
+def workspace_bytes(rooms, fs, c=343.0, mode="fp32", Tw=4e-3, lut_Q=16, split=0) -> int:
+    """gpurir_workspace_bytes: device scratch the batch call needs for these rooms (opts.workspace)."""
+    arr = rooms if isinstance(rooms, C.Array) else room_array(rooms)
+    o = make_opts(mode, Tw, lut_Q, split=split, stream=0)
+    return int(lib().gpurir_workspace_bytes(len(arr), arr, float(fs), float(c), C.byref(o)))
+
+
 def simulate_rir_batch(rooms, fs, out, c=343.0, mode="fp32", Tw=4e-3, lut_Q=16, seed=0, rir_index_base=0,
-                       stream=None, split=0, sync=False):
+                       stream=None, split=0, sync=False, workspace=None, status=None, ev_ism=None, ev_tail=None):
     """gpurir_simulate_rir_batch: one RIR per independent room into ragged rows of `out` (CUDA float32).
 
-    `rooms` is a ctypes gpurir_room array (see room_array) or a sequence of dicts.
+    `rooms` is a ctypes gpurir_room array (see room_array) or a sequence of dicts; room i's tail stream is
+    rir_index_base + its rir_index (default i).  Stream-ordered (no host synchronisation unless sync).
     """
+    import torch
     arr = rooms if isinstance(rooms, C.Array) else room_array(rooms)
-    o = make_opts(mode, Tw, lut_Q, seed, rir_index_base, stream, split, sync)
-    st = lib().gpurir_simulate_rir_batch(len(arr), arr, float(fs), float(c), out.data_ptr(), C.byref(o))
+    if not (isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.float32 and out.is_contiguous()):
+        raise TypeError("out must be a contiguous CUDA float32 tensor")
+    if out.numel() < _batch_need(arr, fs):
+        raise ValueError(f"out holds {out.numel()} elements; the rooms write up to {_batch_need(arr, fs)}")
+    with _on_device(out):
+        o = make_opts(mode, Tw, lut_Q, seed, rir_index_base, stream, split, sync, ev_ism, ev_tail, workspace, status)
+        st = lib().gpurir_simulate_rir_batch(len(arr), arr, float(fs), float(c), out.data_ptr(), C.byref(o))
     check(st, "gpurir_simulate_rir_batch")
     return out
 
@@ -218,9 +260,12 @@ def simulate_trajectory(signal, rirs, out=None, stream=None, sync=False):
         out = torch.empty((n_mics, n_out), dtype=torch.float32, device=signal.device)
     elif not (out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and tuple(out.shape) == (n_mics, n_out)):
         raise TypeError(f"out must be a contiguous CUDA float32 tensor of shape {(n_mics, n_out)}")
-    o = make_opts(stream=stream, sync=sync)
-    st = lib().gpurir_simulate_trajectory(signal.data_ptr(), signal.numel(), rirs.data_ptr(), n_points, n_mics, L,
-                                          out.data_ptr(), C.byref(o))
+    if rirs.device != signal.device or out.device != signal.device:
+        raise ValueError("signal, rirs and out must be on one device")
+    with _on_device(signal):
+        o = make_opts(stream=stream, sync=sync)
+        st = lib().gpurir_simulate_trajectory(signal.data_ptr(), signal.numel(), rirs.data_ptr(), n_points, n_mics,
+                                              L, out.data_ptr(), C.byref(o))
     check(st, "gpurir_simulate_trajectory")
     return out
 

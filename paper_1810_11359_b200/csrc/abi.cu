@@ -5,6 +5,7 @@
 // tail_kernel.cu; this file only validates, sizes and launches.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -64,6 +65,14 @@ struct DeviceState {
   size_t host_scratch_bytes = 0;
   unsigned next_counter = 0;
   int num_sms = 0;
+  // gpurir_simulate_rir_batch: a ring of two grow-only pinned staging buffers for the job table, so the upload
+  // is an asynchronous copy and the call returns without synchronising (a slot is reused once the copy that
+  // last read it has executed: its event)
+  std::mutex stage_mu;
+  char* stage_host[2] = {nullptr, nullptr};
+  size_t stage_bytes[2] = {0, 0};
+  cudaEvent_t stage_done[2] = {nullptr, nullptr};
+  unsigned stage_next = 0;
 };
 std::mutex g_mu;
 constexpr int kMaxDevices = 64;
@@ -239,14 +248,14 @@ constexpr long long kPolyMinItems = 32;  // smaller polyphase calls take the dir
 
 // Polyphase fixed point (ism_poly_kernel.cu, tile setup): a tile needs the two-word scheme when its bound on
 // the images per sample position, N = 8 pi x_hi^2 / V_s + 24 x_hi / L_min + 16 (x_hi the tile's largest delay,
-// V_s the room volume and L_min its shortest side, all in samples), reaches 2^14.  The call allocates the
+// V_s the room volume and L_min its shortest side, all in samples), reaches 2^12.  The call allocates the
 // fine plane when its last tile could.
 bool poly_two_word_for(const float L[3], long long nISM, double fs, double c, double Tw) {
   const double k = fs / c;
   const double Vs = (double)L[0] * L[1] * L[2] * k * k * k;
   const double Lmin = std::min(std::min((double)L[0], (double)L[1]), (double)L[2]) * k;
   const double xhi = (double)nISM + Tw * fs / 2.0 + 1.0;
-  return 8.0 * M_PI * xhi * xhi / Vs + 24.0 * xhi / Lmin + 16.0 >= 16384.0;  // the kernel's lb >= 15: bits < 16
+  return 8.0 * M_PI * xhi * xhi / Vs + 24.0 * xhi / Lmin + 16.0 >= 4096.0;  // the kernel's lb >= 13: bits < 18
 }
 
 // Mode tables of one call (LUT: phase-major smem table; texture LUT: filtered texture; polyphase table).
@@ -361,26 +370,139 @@ int* take_counter(DeviceState* d) {
 
 // Persistent warp-specialised kernel when there are enough (RIR, tile) work items to keep one CTA per
 // SM busy; the cluster-split kernel otherwise (latency-bound small calls).  split < 0 forces persistent.
-bool use_persistent(long long n_work, int split, const DeviceState* d) {
+bool use_persistent(long long n_work, int split, int num_sms) {
   if (split < 0) return true;
   if (split > 0) return false;
-  return n_work >= 4LL * d->num_sms;
+  return n_work >= 4LL * num_sms;
 }
+
+// The polyphase kernel writes the diffuse tail of the RIRs it finishes; GPURIR_FUSE_TAIL=0 in the
+// environment keeps tail_kernel instead (A/B measurements only)
+bool fuse_tail_enabled() {
+  static const int v = [] {
+    const char* e = getenv("GPURIR_FUSE_TAIL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v != 0;
+}
+
+int status_code(int s) {
+  if (s & kStatusDegenerate) return GPURIR_EDEGENERATE;
+  if (s & kStatusCapacity) return GPURIR_ECAPACITY;
+  return GPURIR_EINVAL;
+}
+
+int* status_ptr(const gpurir_opts& o, DeviceState* d) { return o.status ? o.status : d->status; }
 
 int finish(const gpurir_opts& o, cudaStream_t st, DeviceState* d) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "launch");
   if (o.flags & GPURIR_FLAG_SYNC) {
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(e, "sync");
+    int* sp = status_ptr(o, d);
     int s = 0;
-    e = cudaMemcpy(&s, d->status, sizeof(int), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_fail(e, "status");
+    e = cudaMemcpyAsync(&s, sp, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "sync");
     if (s) {
-      cudaMemset(d->status, 0, sizeof(int));
-      return (s & kStatusDegenerate) ? GPURIR_EDEGENERATE : GPURIR_EINVAL;
+      cudaMemsetAsync(sp, 0, sizeof(int), st);
+      return status_code(s);
     }
   }
+  return GPURIR_OK;
+}
+
+// Host plan of a multi-room batch (gpurir_simulate_rir_batch, gpurir_workspace_bytes): the device job table, the
+// heavy-first tile list of the ISM kernel and the chunk list of the tail kernel.
+struct BatchPlan {
+  std::vector<BatchJob> jobs;
+  std::vector<int2> tiles, chunks;
+  bool poly = false, persistent = false, any_two_word = false, fused = false;
+  int kmode = 0;
+  size_t off_tiles = 0, off_chunks = 0, bytes = 0;  // device workspace layout
+};
+
+int plan_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, const gpurir_opts& o, int num_sms,
+               BatchPlan& P) {
+  if (n_rooms <= 0 || !rooms || !(fs > 0) || !(c > 0)) return GPURIR_EINVAL;
+  if (int em = validate_mode(o)) return em;
+  const double H = o.Tw * fs / 2.0;
+  if ((int)ceil((kTCPersistent + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;
+  P.jobs.resize(n_rooms);
+  long long small_tiles = 0, poly_tiles = 0;  // work items at the cluster kernel's / polyphase tile length
+  for (int i = 0; i < n_rooms; i++) {
+    const gpurir_room& R = rooms[i];
+    if (int e0 = validate_room(R.room_sz, R.beta, R.nb_img, R.mic_pattern)) return e0;
+    if (R.spkr_pattern < 0 || R.spkr_pattern > 4) return GPURIR_EINVAL;
+    if (!(R.Tmax > 0) || !(R.Tdiff >= 0) || R.out_offset < 0) return GPURIR_EINVAL;
+    BatchJob& J = P.jobs[i];
+    memset(&J, 0, sizeof(J));
+    for (int a = 0; a < 3; a++) {
+      J.L[a] = R.room_sz[a]; J.src[a] = R.pos_src[a]; J.rcv[a] = R.pos_rcv[a]; J.orv[a] = R.orV_rcv[a];
+      J.ors[a] = R.orV_src[a];
+      J.nb[a] = R.nb_img[a];
+    }
+    for (int w = 0; w < 6; w++) J.beta[w] = R.beta[w];
+    beta_logs(R.beta, J.lb, &J.neg, &J.zero);
+    J.pattern = R.mic_pattern;
+    J.spkr_pattern = R.spkr_pattern;
+    long long nS = gpurir_nsamples(R.Tmax, fs), nISM = gpurir_nsamples(R.Tdiff, fs);
+    if (nISM > nS) nISM = nS;
+    if (nS > (1LL << 30) || nISM > kMaxIsmSamples) return GPURIR_EINVAL;
+    J.nISM = (int)nISM; J.nS = (int)nS; J.out_offset = R.out_offset;
+    const double T60 = sabine(R.room_sz, R.beta);
+    J.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);  // Eq. 8, reading C14
+    J.rir_global = o.rir_index_base + R.rir_index;                        // reading C16: global stream id
+    P.any_two_word = P.any_two_word || poly_two_word_for(R.room_sz, nISM, fs, c, o.Tw);
+    small_tiles += (nISM + kTC - 1) / kTC;
+    poly_tiles += (nISM + kPolyTile - 1) / kPolyTile;
+  }
+  P.poly = o.mode == GPURIR_POLY && (poly_tiles >= kPolyMinItems || o.split < 0);  // as single-room calls
+  P.kmode = o.mode == GPURIR_POLY ? (P.poly ? GPURIR_POLY : GPURIR_FP32) : o.mode;
+  P.persistent = P.poly || use_persistent(small_tiles, o.split, num_sms);
+  // polyphase: every room's diffuse tail is written by the CTA that finishes its last (end-aligned) ISM tile,
+  // which holds the whole 10 ms envelope window (fs <= 102.4 kHz); rooms without ISM samples keep tail_kernel
+  P.fused = P.poly && llround(0.010 * fs) <= kPolyTile && fuse_tail_enabled();
+  for (int i = 0; i < n_rooms; i++) {
+    const BatchJob& J = P.jobs[i];
+    if (J.nISM >= J.nS || (P.fused && J.nISM > 0)) continue;
+    const long long groups = (J.nS + 3) / 4 - J.nISM / 4;
+    const int nch = (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4));
+    for (int ch = 0; ch < nch; ch++) P.chunks.push_back(make_int2(i, ch));
+  }
+  const int tile_len = P.poly ? kPolyTile : P.persistent ? kTCPersistent : kTC;
+  std::vector<int> ntile(n_rooms);
+  int max_tiles = 0;
+  size_t total_tiles = 0;
+  for (int i = 0; i < n_rooms; i++) {
+    ntile[i] = (P.jobs[i].nISM + tile_len - 1) / tile_len;
+    max_tiles = std::max(max_tiles, ntile[i]);
+    total_tiles += (size_t)ntile[i];
+  }
+  P.tiles.reserve(total_tiles);
+  // heavy-first without a comparison sort: image density grows ~ t^2 (SURVEY §7 hard part 2), so emit the tiles
+  // by decreasing end sample (a counting order over tile-length buckets).  The polyphase kernel's tiles are
+  // end-aligned per room (tile t of n ends at nISM - (n - 1 - t) 1024); the other kernels' start at t tile_len.
+  if (P.poly) {
+    std::vector<size_t> start(max_tiles + 1, 0);  // bucket = ceil(te / tile_len) - 1, emitted in decreasing order
+    auto bucket = [&](int i, int t) {
+      const int te = P.jobs[i].nISM - (ntile[i] - 1 - t) * tile_len;
+      return max_tiles - 1 - ((te + tile_len - 1) / tile_len - 1);  // 0 = the latest end
+    };
+    for (int i = 0; i < n_rooms; i++)
+      for (int t = 0; t < ntile[i]; t++) start[bucket(i, t) + 1]++;
+    for (int b = 0; b < max_tiles; b++) start[b + 1] += start[b];
+    P.tiles.resize(total_tiles);
+    for (int i = 0; i < n_rooms; i++)
+      for (int t = ntile[i] - 1; t >= 0; t--) P.tiles[start[bucket(i, t)]++] = make_int2(i, t);
+  } else {
+    for (int t = max_tiles - 1; t >= 0; t--)
+      for (int i = 0; i < n_rooms; i++)
+        if (ntile[i] > t) P.tiles.push_back(make_int2(i, t));
+  }
+  const size_t bj = P.jobs.size() * sizeof(BatchJob), bt = P.tiles.size() * sizeof(int2);
+  P.off_tiles = (bj + 255) & ~(size_t)255;
+  P.off_chunks = P.off_tiles + ((bt + 255) & ~(size_t)255);
+  P.bytes = P.off_chunks + P.chunks.size() * sizeof(int2) + 256;
   return GPURIR_OK;
 }
 
@@ -541,19 +663,21 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     const bool poly = o.mode == GPURIR_POLY &&
                       (((nISM + kPolyTile - 1) / kPolyTile) * M >= kPolyMinItems || o.split < 0);  // split < 0 forces
     const int kmode = o.mode == GPURIR_POLY ? (poly ? GPURIR_POLY : GPURIR_FP32) : o.mode;
-    const bool persistent = poly || use_persistent(((nISM + kTC - 1) / kTC) * M, o.split, d);
+    const bool persistent = poly || use_persistent(((nISM + kTC - 1) / kTC) * M, o.split, d->num_sms);
     const int tile_len = poly ? kPolyTile : persistent ? kTCPersistent : kTC;
     A.nTiles = (int)((nISM + tile_len - 1) / tile_len);
     fill_common(A, fs, c, o.Tw);
     A.out = out;
-    A.status = d->status;
+    A.status = status_ptr(o, d);
     if ((st = setup_mode(d, o, fs, H, stream, A))) return st;
     A.poly_force2 = o.split == -2;
-    A.poly_gb = A.poly_force2 || poly_two_word_for(room_sz, nISM, fs, c, o.Tw);
+    A.poly_hook = o.split == -3 ? 2 : o.split == -5 ? 3 : 0;
+    A.poly_gbz = A.poly_force2 || A.poly_hook == 3 || poly_two_word_for(room_sz, nISM, fs, c, o.Tw);
     // polyphase: the diffuse tail runs inside the ISM kernel when the envelope window (10 ms) fits the last
     // 1024-sample tile (and the call has GPURIR_FUSE_MIN_PER_SM RIRs per SM: 0, measured faster at every size)
     const int win = (int)llround(0.010 * fs);
-    fused_tail = poly && nISM < nS && win <= kPolyTile && M >= (long long)GPURIR_FUSE_MIN_PER_SM * d->num_sms;
+    fused_tail = poly && nISM < nS && win <= kPolyTile && M >= (long long)GPURIR_FUSE_MIN_PER_SM * d->num_sms &&
+                 fuse_tail_enabled();
     if (fused_tail) {
       A.poly_tail = 1;
       A.tail_win = win;
@@ -673,6 +797,12 @@ int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const 
   gpurir_opts sub = o;
   sub.stream = cs;
   sub.flags &= ~GPURIR_FLAG_SYNC;
+  // polyphase: every chunk takes the kernel the whole call would (a small last chunk would otherwise fall back to
+  // the direct kernels, whose rounding differs), so the result equals one device call bit for bit
+  if (o.mode == GPURIR_POLY && o.split == 0 &&
+      ((gpurir_nsamples(std::min(Tdiff, Tmax), fs) + kPolyTile - 1) / kPolyTile) * M_src * (long long)M_rcv >=
+          kPolyMinItems)
+    sub.split = -1;
   sub.ev_ism[0] = sub.ev_ism[1] = sub.ev_tail[0] = sub.ev_tail[1] = nullptr;
   long long k = 0;
   for (int s0 = 0; s0 < M_src && st == GPURIR_OK; s0 += src_chunk) {
@@ -707,109 +837,106 @@ int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const 
   return finish(fin, cs, d);
 }
 
+size_t gpurir_workspace_bytes(int n_rooms, const gpurir_room* rooms, double fs, double c, const gpurir_opts* opts) {
+  gpurir_opts o;
+  if (opts) o = *opts; else gpurir_opts_default(&o);
+  if (!(o.Tw > 0)) o.Tw = 4e-3;
+  int st = GPURIR_OK;
+  DeviceState* d = device_state(&st);
+  if (!d) return 0;
+  BatchPlan P;
+  if (plan_batch(n_rooms, rooms, fs, c, o, d->num_sms, P) != GPURIR_OK) return 0;
+  return P.bytes;
+}
+
 int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, float* out,
                               const gpurir_opts* opts) {
   gpurir_opts o;
   if (opts) o = *opts; else gpurir_opts_default(&o);
   if (!(o.Tw > 0)) o.Tw = 4e-3;
   if (o.lut_Q <= 0) o.lut_Q = 16;
-  if (n_rooms <= 0 || !rooms || !out || !(fs > 0) || !(c > 0)) return GPURIR_EINVAL;
-  if (int em = validate_mode(o)) return em;
-  double H = o.Tw * fs / 2.0;
-  if ((int)ceil((kTCPersistent + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;
-
+  if (!out) return GPURIR_EINVAL;
   int st = GPURIR_OK;
   DeviceState* d = device_state(&st);
   if (!d) return st;
+  BatchPlan P;
+  if ((st = plan_batch(n_rooms, rooms, fs, c, o, d->num_sms, P))) return st;
+  const double H = o.Tw * fs / 2.0;
   cudaStream_t stream = (cudaStream_t)o.stream;
+  if (o.workspace && o.workspace_bytes < P.bytes) return GPURIR_EINVAL;
+  if (o.workspace && (reinterpret_cast<uintptr_t>(o.workspace) & 255)) return GPURIR_EINVAL;
 
-  std::vector<BatchJob> jobs(n_rooms);
-  std::vector<int2> tiles, chunks;
-  long long small_tiles = 0;  // work items at the cluster kernel's tile length (kernel choice)
-  bool any_two_word = false;  // polyphase: some job's last tile may need the two-word scheme
-  for (int i = 0; i < n_rooms; i++) {
-    const gpurir_room& R = rooms[i];
-    if (int e0 = validate_room(R.room_sz, R.beta, R.nb_img, R.mic_pattern)) return e0;
-    if (R.spkr_pattern < 0 || R.spkr_pattern > 4) return GPURIR_EINVAL;
-    if (!(R.Tmax > 0) || !(R.Tdiff >= 0) || R.out_offset < 0) return GPURIR_EINVAL;
-    BatchJob& J = jobs[i];
-    memset(&J, 0, sizeof(J));
-    for (int a = 0; a < 3; a++) {
-      J.L[a] = R.room_sz[a]; J.src[a] = R.pos_src[a]; J.rcv[a] = R.pos_rcv[a]; J.orv[a] = R.orV_rcv[a];
-      J.ors[a] = R.orV_src[a];
-      J.nb[a] = R.nb_img[a];
+  // device workspace: the caller's, else the stream-ordered pool
+  unsigned char* ws = reinterpret_cast<unsigned char*>(o.workspace);
+  cudaError_t e = cudaSuccess;
+  if (!ws) {
+    e = cudaMallocAsync((void**)&ws, P.bytes, stream);
+    if (e != cudaSuccess) { cudaGetLastError(); return GPURIR_ENOMEM; }
+  }
+  auto release = [&] {
+    if (!o.workspace) cudaFreeAsync(ws, stream);
+  };
+  BatchJob* djobs = reinterpret_cast<BatchJob*>(ws);
+  int2* dtiles = reinterpret_cast<int2*>(ws + P.off_tiles);
+  int2* dchunks = reinterpret_cast<int2*>(ws + P.off_chunks);
+  const size_t bj = P.jobs.size() * sizeof(BatchJob), bt = P.tiles.size() * sizeof(int2),
+               bc = P.chunks.size() * sizeof(int2);
+  {
+    // upload through a pinned staging slot: an asynchronous copy, no host synchronisation (the slot's previous
+    // copy is waited for only if it has not executed yet, i.e. two batch calls are still queued before it)
+    std::lock_guard<std::mutex> lk(d->stage_mu);
+    const unsigned k = d->stage_next++ & 1u;
+    if (!d->stage_done[k]) {
+      e = cudaEventCreateWithFlags(&d->stage_done[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) { release(); return cuda_fail(e, "batch staging event"); }
+    } else {
+      e = cudaEventSynchronize(d->stage_done[k]);
+      if (e != cudaSuccess) { release(); return cuda_fail(e, "batch staging wait"); }
     }
-    for (int w = 0; w < 6; w++) J.beta[w] = R.beta[w];
-    beta_logs(R.beta, J.lb, &J.neg, &J.zero);
-    J.pattern = R.mic_pattern;
-    J.spkr_pattern = R.spkr_pattern;
-    long long nS = gpurir_nsamples(R.Tmax, fs), nISM = gpurir_nsamples(R.Tdiff, fs);
-    if (nISM > nS) nISM = nS;
-    if (nS > (1LL << 30) || nISM > kMaxIsmSamples) return GPURIR_EINVAL;
-    J.nISM = (int)nISM; J.nS = (int)nS; J.out_offset = R.out_offset;
-    double T60 = sabine(R.room_sz, R.beta);
-    J.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);
-    J.rir_global = o.rir_index_base + (unsigned long long)i;
-    any_two_word = any_two_word || poly_two_word_for(R.room_sz, nISM, fs, c, o.Tw);
-    small_tiles += (nISM + kTC - 1) / kTC;
-    long long groups = (nS + 3) / 4 - nISM / 4;
-    int nch = nISM < nS ? (int)((groups + kTailChunk / 4 - 1) / (kTailChunk / 4)) : 0;
-    for (int ch = 0; ch < nch; ch++) chunks.push_back(make_int2(i, ch));
+    if (d->stage_bytes[k] < P.bytes) {
+      if (d->stage_host[k]) cudaFreeHost(d->stage_host[k]);
+      d->stage_host[k] = nullptr;
+      d->stage_bytes[k] = 0;
+      const size_t want = P.bytes + P.bytes / 4;
+      e = cudaMallocHost((void**)&d->stage_host[k], want);
+      if (e != cudaSuccess) { cudaGetLastError(); release(); return GPURIR_ENOMEM; }
+      d->stage_bytes[k] = want;
+    }
+    char* h = d->stage_host[k];
+    memcpy(h, P.jobs.data(), bj);
+    if (bt) memcpy(h + P.off_tiles, P.tiles.data(), bt);
+    if (bc) memcpy(h + P.off_chunks, P.chunks.data(), bc);
+    e = cudaMemcpyAsync(ws, h, P.off_chunks + bc, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaEventRecord(d->stage_done[k], stream);
+    if (e != cudaSuccess) { release(); return cuda_fail(e, "batch upload"); }
   }
-  long long poly_tiles = 0;
-  for (int i = 0; i < n_rooms; i++) poly_tiles += (jobs[i].nISM + kPolyTile - 1) / kPolyTile;
-  const bool poly = o.mode == GPURIR_POLY && (poly_tiles >= kPolyMinItems || o.split < 0);  // as single-room
-  const int kmode = o.mode == GPURIR_POLY ? (poly ? GPURIR_POLY : GPURIR_FP32) : o.mode;
-  const bool persistent = poly || use_persistent(small_tiles, o.split, d);
-  const int tile_len = poly ? kPolyTile : persistent ? kTCPersistent : kTC;
-  // heavy-first schedule without a comparison sort: image density grows ~ t^2 (SURVEY §7 hard part 2), so
-  // emit all rooms' last tiles first, then the second-to-last, ... (a counting order over tile index)
-  int max_tiles = 0;
-  std::vector<int> ntile(n_rooms);
-  for (int i = 0; i < n_rooms; i++) {
-    ntile[i] = (jobs[i].nISM + tile_len - 1) / tile_len;
-    max_tiles = std::max(max_tiles, ntile[i]);
-  }
-  size_t total_tiles = 0;
-  for (int i = 0; i < n_rooms; i++) total_tiles += (size_t)ntile[i];
-  tiles.reserve(total_tiles);
-  for (int t = max_tiles - 1; t >= 0; t--)
-    for (int i = 0; i < n_rooms; i++)
-      if (ntile[i] > t) tiles.push_back(make_int2(i, t));
 
-  size_t bj = jobs.size() * sizeof(BatchJob), bt = tiles.size() * sizeof(int2), bc = chunks.size() * sizeof(int2);
-  size_t total = bj + bt + bc + 64;
-  unsigned char* ws = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&ws, total, stream);
-  if (e != cudaSuccess) return GPURIR_ENOMEM;
-  BatchJob* djobs = (BatchJob*)ws;
-  int2* dtiles = (int2*)(ws + ((bj + 15) & ~(size_t)15));
-  int2* dchunks = dtiles + tiles.size();
-  // the host vectors must outlive the async copies: copy, then synchronise before returning
-  e = cudaMemcpyAsync(djobs, jobs.data(), bj, cudaMemcpyHostToDevice, stream);
-  if (e == cudaSuccess && bt) e = cudaMemcpyAsync(dtiles, tiles.data(), bt, cudaMemcpyHostToDevice, stream);
-  if (e == cudaSuccess && bc) e = cudaMemcpyAsync(dchunks, chunks.data(), bc, cudaMemcpyHostToDevice, stream);
-  if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "batch upload"); }
-
-  if (!tiles.empty()) {
+  if (!P.tiles.empty()) {
     IsmArgs A;
     memset(&A, 0, sizeof(A));
     A.jobs = djobs; A.tiles = dtiles;
     fill_common(A, fs, c, o.Tw);
     A.out = out;
-    A.status = d->status;
-    if ((st = setup_mode(d, o, fs, H, stream, A))) { cudaFreeAsync(ws, stream); return st; }
+    A.status = status_ptr(o, d);
+    if ((st = setup_mode(d, o, fs, H, stream, A))) { release(); return st; }
     A.poly_force2 = o.split == -2;
-    A.poly_gb = A.poly_force2 || any_two_word;
-    long long nw = (long long)tiles.size();
+    A.poly_hook = o.split == -3 ? 2 : o.split == -5 ? 3 : 0;
+    A.poly_gbz = A.poly_force2 || A.poly_hook == 3 || P.any_two_word;
+    if (P.fused) {
+      A.poly_tail = 1;
+      A.tail_win = (int)llround(0.010 * fs);
+      A.tail_seed = o.seed;
+    }
+    const long long nw = (long long)P.tiles.size();
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
-    if (poly) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, stream);
-    else if (persistent) e = launch_ism_ws(A, kmode, nw, take_counter(d), d->num_sms, stream);
-    else e = launch_ism(A, kmode, auto_split(nw, o.split), nw, stream);
-    if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_ism(batch)"); }
+    if (P.poly) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, stream);
+    else if (P.persistent) e = launch_ism_ws(A, P.kmode, nw, take_counter(d), d->num_sms, stream);
+    else e = launch_ism(A, P.kmode, auto_split(nw, o.split), nw, stream);
+    if (e != cudaSuccess) { release(); return cuda_fail(e, "launch_ism(batch)"); }
     if (o.ev_ism[1]) cudaEventRecord((cudaEvent_t)o.ev_ism[1], stream);
   }
-  if (!chunks.empty()) {
+  if (o.ev_tail[0]) cudaEventRecord((cudaEvent_t)o.ev_tail[0], stream);
+  if (!P.chunks.empty()) {
     TailArgs T;
     memset(&T, 0, sizeof(T));
     T.jobs = djobs; T.chunks = dchunks;
@@ -818,14 +945,11 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     T.seed = o.seed;
     T.out = out;
     T.chunk_quads = kTailChunk / 4;
-    if (o.ev_tail[0]) cudaEventRecord((cudaEvent_t)o.ev_tail[0], stream);
-    e = launch_tail(T, (long long)chunks.size(), stream);
-    if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return cuda_fail(e, "launch_tail(batch)"); }
-    if (o.ev_tail[1]) cudaEventRecord((cudaEvent_t)o.ev_tail[1], stream);
+    e = launch_tail(T, (long long)P.chunks.size(), stream);
+    if (e != cudaSuccess) { release(); return cuda_fail(e, "launch_tail(batch)"); }
   }
-  cudaFreeAsync(ws, stream);
-  e = cudaStreamSynchronize(stream);  // host staging vectors are released on return
-  if (e != cudaSuccess) return cuda_fail(e, "batch sync");
+  if (o.ev_tail[1]) cudaEventRecord((cudaEvent_t)o.ev_tail[1], stream);
+  release();
   return finish(o, stream, d);
 }
 
@@ -894,7 +1018,7 @@ int gpurir_device_status(int reset) {
   if (e != cudaSuccess) return cuda_fail(e, "status");
   if (reset) cudaMemset(d->status, 0, sizeof(int));
   if (!s) return GPURIR_OK;
-  return (s & kStatusDegenerate) ? GPURIR_EDEGENERATE : GPURIR_EINVAL;
+  return status_code(s);
 }
 
 const char* gpurir_strerror(int status) {
@@ -905,12 +1029,17 @@ const char* gpurir_strerror(int status) {
     case GPURIR_EINFEASIBLE: return "infeasible target T60";
     case GPURIR_ENOMEM: return "out of device memory";
     case GPURIR_ECUDA: return "CUDA error";
+    case GPURIR_ECAPACITY: return "capacity: more than 2^17 images on one sample of a polyphase tile";
   }
   return "unknown status";
 }
 
 const char* gpurir_last_cuda_error(void) { return g_cuda_err; }
 
-const char* gpurir_version(void) { return "gpurir-b200 0.1.0 (sm_100a)"; }
+#ifdef GPURIR_VARIANT  // A/B builds (tools/build_variant.sh); bench.py refuses to time them without --ab-lib
+const char* gpurir_version(void) { return "gpurir-b200 0.2.0 (sm_100a) variant:" GPURIR_VARIANT; }
+#else
+const char* gpurir_version(void) { return "gpurir-b200 0.2.0 (sm_100a)"; }
+#endif
 
 }  // extern "C"

@@ -70,10 +70,18 @@ struct PolyTile {
   double Lzs, offEs, offOs;     // Eq. 1 along z in samples: Delta_z fs / c = n Lz fs / c + off (even / odd n)
   float scalef;      // 2^(bits - e): a power of two, exact in fp32
   float inv_scalef;  // 2^(e - bits), the same as inv_scale
+  float scale_lf;    // single word: the last channel's scale 2^(bits - e - J)
   int two_word;
+  int e, bits;       // amplitude bound |A| < 2^e (in 1/(fs/c 4 pi) units, see setup); channel resolution bits
+  int J;             // the last channel's word counts its deposits in its low J bits (capacity 2^J per position)
+  unsigned cnt_mask; // 2^J - 1
+  int ovf, redo;     // some position's count reached 2^J / the aggregation is redone at a wider format
   long long row;
   int t0, te, tc, nx0, ny0, NX, ncols, zl, zh, use_bz, next;
   int rir, tail;     // the RIR; this tile ends its ISM part and the call fuses the tail
+  int tail_nS;       // fused tail: the RIR's samples, its Philox stream (global RIR index) and decay
+  float tail_kappa;
+  unsigned long long tail_rglob;
   double x_dp;       // direct-path delay (samples)
   float tenv[3];     // fused tail: env0, alpha, rho of the RIR (tail_envelope)
   float invNX;
@@ -84,9 +92,8 @@ struct PolyTile {
 // then every thread writes Philox blocks of the tail.  Not inlined: the tail's registers (Philox round keys)
 // stay out of the image loop's allocation.
 __device__ __noinline__ void poly_fused_tail(PolyTile& T, const float* red, int tid, int nthreads, float* out,
-                                             int nS, int win, float kappa_fs, unsigned long long seed,
-                                             unsigned long long rir_base) {
-  const int nISM = T.te;
+                                             int win, unsigned long long seed) {
+  const int nISM = T.te, nS = T.tail_nS;
   if (tid < 32) {
     float env0, alpha, rho;
     const int t0 = T.t0;
@@ -94,17 +101,17 @@ __device__ __noinline__ void poly_fused_tail(PolyTile& T, const float* red, int 
                     const int t = k - t0;
                     return (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
                   },
-                  nISM, win, T.x_dp, kappa_fs, tid, env0, alpha, rho);
+                  nISM, win, T.x_dp, T.tail_kappa, tid, env0, alpha, rho);
     if (tid == 0) { T.tenv[0] = env0; T.tenv[1] = alpha; T.tenv[2] = rho; }
   }
   __syncthreads();
   const float env0 = T.tenv[0], alpha = T.tenv[1], rho = T.tenv[2];
   const PhiloxKey key = philox_key(make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-  const unsigned long long rglob = rir_base + (unsigned long long)T.rir;
-  const bool aligned = ((T.row & 3) == 0);
+  float* row = out + T.row;
+  const bool aligned = (reinterpret_cast<uintptr_t>(row) & 15) == 0;  // float4 stores need a 16-B row start
   const long long qend = (long long)((nS + 3) >> 2);
   for (long long q = (long long)(nISM >> 2) + tid; q < qend; q += nthreads)
-    tail_quad(q, nISM, nS, env0, alpha, rho, key, rglob, out + T.row, aligned);
+    tail_quad(q, nISM, nS, env0, alpha, rho, key, T.tail_rglob, row, aligned);
 }
 
 template <int THREADS>
@@ -142,24 +149,39 @@ __device__ __forceinline__ float poly_z_factor(int nz, const RirGeom& g) {
 }
 
 // One image's 8 channel values A T_d(y), d = 0..7, added to G[.][p] as integers v = round(A T_d 2^s).  The
-// tile's scale bounds |A| by its closest possible image, so |v| <= 2^bits, and its bound N on the images per
-// sample position sets bits (tile setup): single word (bits <= 22, fp32 arithmetic, one plain shared-memory
-// reduction per channel) while N 2^bits <= 2^30 leaves bits >= 16; otherwise bits = 28 and v = a 2^14 + b,
-// b in [0, 2^14), goes to two int32 planes (2^17 terms per position before either could overflow).  Integer
-// adds commute, so G does not depend on the order in which images arrive (deterministic, shard-invariant).
+// tile's scale bounds |A| by its closest possible image, so |v| <= 2^bits; sums of integers commute, so G does
+// not depend on the order in which images arrive (deterministic, shard-invariant).
+// Overflow guard (exact, no assumption on how many images share a sample position): the last channel's word
+// also COUNTS its deposits, in its low J bits — the channel value goes in shifted left by J (its resolution
+// is 2^-J of the others'; its coefficients are <= 8.5e-6, R11) plus 1 — and every deposit reads the word's
+// old value.  The deposit that takes a position's count to 2^J sees the count field all ones, so `acc`
+// (min over this thread's deposits of ~old & mask) reaches 0 exactly when some position holds 2^J images;
+// below that, sum |v| <= (2^J - 1) 2^bits < 2^31 on every channel and no partial sum can wrap.  The tile is
+// then redone in a wider format (ism_poly_kernel, after the aggregation).
+//   single word (bits <= 22, J = 31 - bits): fp32 arithmetic — T_d by the recurrence in fp32 (|error| ~ 1e-7
+//     d), round(A T_d 2^s) from the low mantissa bits of A 2^s T_d + 1.5 2^23 (exact for |v| < 2^22);
+//   two words (bits = 28): v = a 2^14 + b, b in [0, 2^14), into two int32 planes (2^17 terms of headroom); the
+//     last channel puts round(v 2^-14) in its coarse plane and counts in its fine plane (J = 17).
 __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int W, int p, float y, float amp, float scale,
-                                         bool two_word) {
+                                         float scale_l, int J, unsigned mask, bool two_word, unsigned& acc) {
+  constexpr int kLast = kPolyChannels - 1;
   if (!two_word) {
-    // single word, bits <= 22: fp32 suffices — T_d by the recurrence in fp32 (|error| ~ 1e-7 d), and
-    // round(A T_d 2^s) from the low mantissa bits of A 2^s T_d + 1.5 2^23 (exact for |v| < 2^22)
-    const float as = amp * scale, y2 = 2.f * y, magic = 12582912.f;  // power-of-two scale: exact
+    // the deposits are the raw bit patterns 0x4B400000 + v of A 2^s T_d + 1.5 2^23: the sums carry count x
+    // 0x4B400000 (mod 2^32), removed at the conversion with the exact count of the last channel's low bits
+    const float as = amp * scale, y2 = 2.f * y, magic = 12582912.f;  // power-of-two scales: exact
     float tm2 = 1.f, tm1 = y;
-    atomicAdd(&Ga[p], __float_as_int(fmaf(as, 1.f, magic)) - 0x4B400000);
-    atomicAdd(&Ga[W + p], __float_as_int(fmaf(as, y, magic)) - 0x4B400000);
+    atomicAdd(&Ga[p], __float_as_int(fmaf(as, 1.f, magic)));
+    atomicAdd(&Ga[W + p], __float_as_int(fmaf(as, y, magic)));
 #pragma unroll
     for (int d = 2; d < kPolyChannels; d++) {
       const float t = fmaf(y2, tm1, -tm2);  // T_d = 2 y T_{d-1} - T_{d-2}
-      atomicAdd(&Ga[d * W + p], __float_as_int(fmaf(as, t, magic)) - 0x4B400000);
+      if (d < kLast) {
+        atomicAdd(&Ga[d * W + p], __float_as_int(fmaf(as, t, magic)));
+      } else {
+        const unsigned raw = __float_as_uint(fmaf(amp * scale_l, t, magic));
+        const unsigned old = atomicAdd(reinterpret_cast<unsigned*>(&Ga[d * W + p]), raw * (1u << J) + 1u);
+        acc = min(acc, ~old & mask);
+      }
       tm2 = tm1;
       tm1 = t;
     }
@@ -173,17 +195,38 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int W, int p, float y
 #pragma unroll
   for (int d = 2; d < kPolyD; d++) T[d] = fma(y2, T[d - 1], -T[d - 2]);  // T_d = 2 y T_{d-1} - T_{d-2}
 #pragma unroll
-  for (int d = 0; d < kPolyChannels; d++) {
+  for (int d = 0; d < kLast; d++) {
     const int v = __double2loint(fma(ad, T[d], magic));
     const int i = d * W + p;  // channel-major planes: consecutive positions are consecutive words
     atomicAdd(&Ga[i], v >> 14);
     atomicAdd(&Gb[i], v & 0x3FFF);
   }
+  const int i = kLast * W + p;
+  atomicAdd(&Ga[i], __double2loint(fma(ad * 6.103515625e-05, T[kLast], magic)));  // round(v 2^-14)
+  const unsigned old = atomicAdd(reinterpret_cast<unsigned*>(&Gb[i]), 1u);
+  acc = min(acc, ~old & mask);
+}
+
+// Tile format: channel resolution `bits`, one or two words, count capacity 2^J per position (jcap > 0 lowers J:
+// a test hook that makes the guard fire).
+__device__ __forceinline__ void poly_set_format(PolyTile& T, int bits, int two_word, int jcap) {
+  T.bits = bits;
+  T.two_word = two_word;
+  T.scalef = ldexpf(1.f, bits - T.e);
+  T.inv_scale = ldexp(1.0, T.e - bits);
+  T.inv_scalef = ldexpf(1.f, T.e - bits);
+  int J = two_word ? 17 : 31 - bits;
+  if (jcap > 0 && jcap < J) J = jcap;
+  T.J = J;
+  T.cnt_mask = (1u << J) - 1u;
+  T.scale_lf = ldexpf(1.f, bits - T.e - J);
 }
 
 // Plane stride W (words) fixed at compile time for ntaps <= 64 (fs <= 16 kHz at T_w = 4 ms): the 8 channel
 // updates of an image and the FIR's paired-channel loads then address G with immediate offsets
-__host__ __device__ constexpr int poly_plane_words(int ntaps) { return (kPolyTC + ntaps - 1) + ((kPolyTC + ntaps - 1) >> 3) + 1; }
+__host__ __device__ constexpr int poly_plane_words(int ntaps) {
+  return ((kPolyTC + ntaps - 1) + ((kPolyTC + ntaps - 1) >> 3) + 1 + 3) & ~3;  // 16-B aligned planes
+}
 constexpr int kPolyWFixTaps = 64;
 constexpr int kPolyWFix = poly_plane_words(kPolyWFixTaps);
 
@@ -213,7 +256,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     if (tid >= 32) {  // zero G while thread 0 sets the next work item up (G is free: the loop ends in a barrier)
       // 16-B stores over the 8 W words of each array
       const int n4 = (kPolyD * W) >> 2;
-      const bool both = A.poly_gb;  // the fine plane Gb exists (and is used) only for two-word items
+      const bool both = A.poly_gbz;  // the call has two-word tiles: zero the fine plane with the coarse one
       for (int i = tid - 32; i < n4; i += kPolyThreads - 32) reinterpret_cast<int4*>(Ga)[i] = make_int4(0, 0, 0, 0);
       if (both)
         for (int i = tid - 32; i < n4; i += kPolyThreads - 32) reinterpret_cast<int4*>(Gb)[i] = make_int4(0, 0, 0, 0);
@@ -242,16 +285,25 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         }
         T.row = row;
         T.rir = m;
+        // tiles end-aligned ([nISM - 1024 (k + 1), nISM - 1024 k)), so the last one holds the whole envelope
+        // window when the tail is fused; also when it is not, because the fixed-point scale is per tile and a RIR
+        // must give the same bits whether or not its tail is fused (shards of one call fuse or not by size), and
+        // the same bits in a batch of rooms as alone
+        const int ntile = (nISM + kPolyTC - 1) / kPolyTC;
+        T.te = nISM - (ntile - 1 - tile) * kPolyTC;
+        T.t0 = max(0, T.te - kPolyTC);
         if (A.jobs) {
-          T.t0 = tile * kPolyTC;
-          T.te = min(T.t0 + kPolyTC, nISM);
-        } else {  // single-room calls: tiles end-aligned, so the last one holds the whole envelope window when
-                  // the tail is fused; also when it is not, because the fixed-point scale is per tile and a call
-                  // must give the same bits whether or not its tail is fused (shards of one call fuse or not by size)
-          T.te = nISM - (A.nTiles - 1 - tile) * kPolyTC;
-          T.t0 = max(0, T.te - kPolyTC);
+          const BatchJob& J = A.jobs[m];
+          T.tail = A.poly_tail && tile == ntile - 1 && J.nISM < J.nS;
+          T.tail_nS = J.nS;
+          T.tail_kappa = J.kappa_fs;
+          T.tail_rglob = J.rir_global;
+        } else {
+          T.tail = A.poly_tail && tile == ntile - 1;
+          T.tail_nS = A.tail_nS;
+          T.tail_kappa = A.tail_kappa_fs;
+          T.tail_rglob = A.tail_rir_base + (unsigned long long)m;
         }
-        T.tail = A.poly_tail && !A.jobs && tile == A.nTiles - 1;
         T.tc = T.t0 + kPolyTC / 2;
         T.invLz = 1.0 / T.g.L[2];
         T.Lzs = T.g.L[2] * A.fs_over_c;
@@ -278,14 +330,15 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         T.use_bz = (T.zh - T.zl + 1) <= kPolyBz;
         // per-tile fixed point (see poly_add).  Images depositing into this tile have x >= x_lo =
         // max(t0 - m_hi, x_dp) samples (the direct path is the closest image), so |A_n| <= 1 / (4 pi d_lo)
-        // (|beta|, |g| <= 1) and every channel value is |v| <= 2^bits.  N bounds the images that can share one
-        // sample position at delays <= x_hi (the tile's largest): twice the mean count 4 pi x_hi^2 / V_s (one
-        // image per room volume V_s, in samples), plus 24 x_hi / (L_min fs / c) for images stacked on equal
-        // distances by symmetric or commensurate geometry (a cube with source and receiver at its centre puts
-        // r3(n) <= 24 sqrt(n) images on |k|^2 = n, |k| = d / L), plus 16.  bits = min(22, 30 - ceil(log2 N))
-        // leaves room for 2N full-amplitude images per position before an int32 sum could overflow
-        // (brute-force counts fill <= 1/3 of it: tests/test_poly_headroom.py).  Below 16 bits (N >= 2^14)
-        // the tile takes the two-word scheme.
+        // (|beta|, |g| <= 1) and every channel value is |v| <= 2^bits.  The resolution is chosen from an
+        // ESTIMATE N of the images sharing one sample position at delays <= x_hi (the tile's largest): twice the
+        // mean count 4 pi x_hi^2 / V_s (one image per room volume V_s, in samples), plus 24 x_hi / (L_min fs / c)
+        // for images stacked on equal distances by symmetric or commensurate geometry, plus 16;
+        // bits = min(22, 30 - ceil(log2 N)), i.e. a count capacity 2^(31 - bits) > 2N.  N is a heuristic (the
+        // number of lattice points on a sphere is not bounded by any fixed multiple of the mean: DESIGN.md
+        // §5.5); correctness rests on the exact count guard of poly_add, which redoes a tile whose capacity is
+        // reached.  Below 18 bits (N >= 2^12) the tile takes the two-word scheme: single-word tiles keep
+        // 2 bits - 31 >= 5 bits for the counting channel (poly_add).
         const double ddx = T.g.s[0] - T.g.r[0], ddy = T.g.s[1] - T.g.r[1], ddz = T.g.s[2] - T.g.r[2];
         const double x_dp = sqrt(ddx * ddx + ddy * ddy + ddz * ddz) * A.fs_over_c;
         T.x_dp = x_dp;
@@ -296,14 +349,12 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         int lb;
         (void)frexp(25.132741228718345 * x_hi * x_hi / Vs + 24.0 * x_hi / Lmin_s + 16.0, &lb);  // N < 2^lb
         int bits = min(22, 30 - lb);
-        T.two_word = bits < 16 || A.poly_force2;
-        if (T.two_word) bits = 28;
+        const int two_word = bits < 18 || A.poly_force2 || A.poly_hook == 3;
+        if (two_word) bits = 28;
         const double abound = 0.0795774715459476679 * A.fs_over_c / x_lo;
-        int e;
-        (void)frexp(abound, &e);  // abound < 2^e
-        T.scalef = ldexpf(1.f, bits - e);
-        T.inv_scale = ldexp(1.0, e - bits);
-        T.inv_scalef = ldexpf(1.f, e - bits);
+        (void)frexp(abound, &T.e);  // abound < 2^e
+        poly_set_format(T, bits, two_word, A.poly_hook >= 2 ? 2 : 0);
+        T.ovf = 0;
       }
     }
     __syncthreads();
@@ -314,127 +365,174 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       for (int i = tid; i <= T.zh - T.zl; i += kPolyThreads) sm.bz[i] = poly_z_factor(T.zl + i, g);
 
     // ---- 1. image aggregation -------------------------------------------------------------
-    const float amp_scale = fs_over_c_4pi;
-    const int pbase = sm.ti.t0 - m_hi;  // p = floor(x) - pbase
-    for (int qb = 0; qb < T.ncols; qb += kPolyCols) {
-      int cnt = 0;
-      {
-        const int q = qb + tid;
-        PolyColRec cr;
-        cr.a1 = 0; cr.a2 = 0; cr.b = 0; cr.end = 0; cr.rho2 = 0.0; cr.bxy = 0.f; cr.cdot = 0.f;
-        float sdot = 0.f;
-        int r1lo = 0, r2lo = 0, r1n = 0;
-        if (q < T.ncols) {
-          const int qy = (int)(((float)q + 0.5f) * T.invNX);
-          const int nx = T.nx0 + (q - qy * T.NX), ny = T.ny0 + qy;
-          const double dx = image_coord(nx, g.L[0], g.s[0]) - g.r[0];
-          const double dy = image_coord(ny, g.L[1], g.s[1]) - g.r[1];
-          const double rho2 = dx * dx + dy * dy;
-          cr.rho2 = rho2 * sc2;
-          cr.cdot = ((float)dx * g.o[0] + (float)dy * g.o[1]) * fsc;
-          sdot = src_col_dot(nx, ny, (float)dx, (float)dy, g) * fsc;
-          uint32_t sgn = 0;
-          bool zero = false;
-          const float lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
-          const float bxy = zero ? 0.f : ex2_approx(lxy);
-          cr.bxy = (sgn ? -bxy : bxy) * amp_scale;
-          if (rho2 < T.dhi2) {
-            const double zhi = (double)sqrtf((float)(T.dhi2 - rho2));
-            const double zlo = T.dlo2 > rho2 ? (double)sqrtf((float)(T.dlo2 - rho2)) : 0.0;
-            int pa, pb, na, nbz;
-            z_range(g, T.invLz, zlo, zhi, pa, pb);
-            z_range(g, T.invLz, -zhi, -zlo, na, nbz);
-            if (nbz >= pa - 1) { pa = min(pa, na); na = 1; nbz = 0; }
-            pa = max(pa, T.zl); pb = min(pb, T.zh);
-            na = max(na, T.zl); nbz = min(nbz, T.zh);
-            const int n1 = max(0, pb - pa + 1), n2 = max(0, nbz - na + 1);
-            r1lo = pa; r1n = n1; r2lo = na;
-            cnt = n1 + n2;
+    // Redone (once) when the count guard fires: a single-word tile goes to the two-word format (capacity 2^17
+    // images per position) if the call's shared memory holds the fine plane; otherwise — and for a two-word
+    // tile that fires — the capacity status is set instead of returning a wrapped sum.  The format
+    // depends only on this tile's own images (deterministic, shard-invariant; a call launched without the fine
+    // plane, i.e. 256-thread CTAs, reports the capacity status where a 512-thread call would go on).
+    for (;;) {
+      const float amp_scale = fs_over_c_4pi;
+      const int pbase = sm.ti.t0 - m_hi;  // p = floor(x) - pbase
+      for (int qb = 0; qb < T.ncols; qb += kPolyCols) {
+        int cnt = 0;
+        {
+          const int q = qb + tid;
+          PolyColRec cr;
+          cr.a1 = 0; cr.a2 = 0; cr.b = 0; cr.end = 0; cr.rho2 = 0.0; cr.bxy = 0.f; cr.cdot = 0.f;
+          float sdot = 0.f;
+          int r1lo = 0, r2lo = 0, r1n = 0;
+          if (q < T.ncols) {
+            const int qy = (int)(((float)q + 0.5f) * T.invNX);
+            const int nx = T.nx0 + (q - qy * T.NX), ny = T.ny0 + qy;
+            const double dx = image_coord(nx, g.L[0], g.s[0]) - g.r[0];
+            const double dy = image_coord(ny, g.L[1], g.s[1]) - g.r[1];
+            const double rho2 = dx * dx + dy * dy;
+            cr.rho2 = rho2 * sc2;
+            cr.cdot = ((float)dx * g.o[0] + (float)dy * g.o[1]) * fsc;
+            sdot = src_col_dot(nx, ny, (float)dx, (float)dy, g) * fsc;
+            uint32_t sgn = 0;
+            bool zero = false;
+            const float lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
+            const float bxy = zero ? 0.f : ex2_approx(lxy);
+            cr.bxy = (sgn ? -bxy : bxy) * amp_scale;
+            if (rho2 < T.dhi2) {
+              const double zhi = (double)sqrtf((float)(T.dhi2 - rho2));
+              const double zlo = T.dlo2 > rho2 ? (double)sqrtf((float)(T.dlo2 - rho2)) : 0.0;
+              int pa, pb, na, nbz;
+              z_range(g, T.invLz, zlo, zhi, pa, pb);
+              z_range(g, T.invLz, -zhi, -zlo, na, nbz);
+              if (nbz >= pa - 1) { pa = min(pa, na); na = 1; nbz = 0; }
+              pa = max(pa, T.zl); pb = min(pb, T.zh);
+              na = max(na, T.zl); nbz = min(nbz, T.zh);
+              const int n1 = max(0, pb - pa + 1), n2 = max(0, nbz - na + 1);
+              r1lo = pa; r1n = n1; r2lo = na;
+              cnt = n1 + n2;
+            }
+          }
+          // one scan of (candidates + 2^20 x nonempty) both prefixes the candidates and compacts the nonempty
+          // columns in order, so the run search and the walk below never visit an empty column
+          const int incl = poly_block_scan<kPolyThreads>(cnt + (cnt > 0 ? (1 << 20) : 0), sm.scan_tmp);
+          if (cnt > 0) {
+            const int end = incl & 0xFFFFF, start = end - cnt, k = (incl >> 20) - 1;
+            cr.end = end;
+            cr.b = start + r1n;          // first candidate of the second n_z run
+            cr.a1 = r1lo - start;        // n_z = gi + a1 on the first run
+            cr.a2 = r2lo - r1n - start;  // n_z = gi + a2 on the second
+            sm.col[k] = cr;
+            sm.colpre[k] = end;
+            sm.colsdot[k] = sdot;
           }
         }
-        // one scan of (candidates + 2^20 x nonempty) both prefixes the candidates and compacts the nonempty
-        // columns in order, so the run search and the walk below never visit an empty column
-        const int incl = poly_block_scan<kPolyThreads>(cnt + (cnt > 0 ? (1 << 20) : 0), sm.scan_tmp);
-        if (cnt > 0) {
-          const int end = incl & 0xFFFFF, start = end - cnt, k = (incl >> 20) - 1;
-          cr.end = end;
-          cr.b = start + r1n;          // first candidate of the second n_z run
-          cr.a1 = r1lo - start;        // n_z = gi + a1 on the first run
-          cr.a2 = r2lo - r1n - start;  // n_z = gi + a2 on the second
-          sm.col[k] = cr;
-          sm.colpre[k] = end;
-          sm.colsdot[k] = sdot;
+        __syncthreads();
+        const int tot = sm.scan_tmp[kPolyThreads / 32 - 1];
+        const int total = tot & 0xFFFFF, ncomp = tot >> 20;
+        const int R = (total + kPolyThreads - 1) / kPolyThreads;
+        const int g0 = tid * R, g1 = min(g0 + R, total);
+        if (g0 < g1) {
+          int lo = 0, hi = ncomp - 1;  // first (compacted) column with colpre > g0
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sm.colpre[mid] > g0) hi = mid; else lo = mid + 1;
+          }
+          int j = lo;
+          const int zl = T.zl;
+          const float oz = g.o[2], ga = g.a, scalef = T.scalef, scale_lf = T.scale_lf;
+          const int J = T.J;
+          const unsigned cmask = T.cnt_mask;
+          unsigned acc = 0xFFFFFFFFu;  // min of ~old & mask over this thread's last-channel deposits (poly_add)
+          PolyColRec cr = load_col(&sm.col[j]);  // the current column's record, in registers
+          // the walk, compiled twice: the common case (single word, omni source, z factors from the table) with
+          // its flags as constants — fewer live registers, so fewer loop constants re-read from shared memory —
+          // and the general case with runtime flags
+          auto walk = [&](auto fast) {
+          constexpr bool kFast = decltype(fast)::value;
+          const bool use_bz = kFast || T.use_bz, dir_src = !kFast && g.as != 1.f, two_word = !kFast && T.two_word;
+          const double Lzs = T.Lzs, offEs = T.offEs, offOs = T.offOs;
+          for (int gi = g0; gi < g1; gi++) {  // every lane runs R candidates: the walk keeps the warp converged
+            // compacted columns are nonempty and gi advances by one: a change moves exactly one column on
+            if (gi >= cr.end) cr = load_col(&sm.col[++j]);
+            const int nz = gi + (gi < cr.b ? cr.a1 : cr.a2);
+            const int odd = nz & 1;
+            const float bz = use_bz ? sm.bz[min(max(nz - zl, 0), kPolyBz - 1)] : poly_z_factor(nz, g);
+            const int nzo = nz + odd;
+            // Eq. 1 along z, in samples (the tile's constants are read from shared memory: no conversions here)
+            const double dz = fma(int_to_double(nzo), Lzs, odd ? offOs : offEs);
+            const double x2 = fma(dz, dz, cr.rho2);                             // (d fs / c)^2
+            if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); continue; }
+            float x0f, xd, rx;  // x = x0f + xd (xd the fp64 Newton correction); rx = 1/x
+            delay_split(x2, x0f, xd, rx);
+            // floor of the fp32 sum x0f + xd, fraction from the exact difference x0f - floor plus xd: within 1e-7
+            // of an integer the rounded sum may pick the neighbouring floor, and the clamp moves phi by < 1e-7
+            // (delta' (m - phi) is continuous from tap m at phi = 1 to tap m + 1 at phi = 0)
+            int jfl;
+            const float fj = floor_int(x0f + xd, jfl);
+            const float phi = fminf(fmaxf((x0f - fj) + xd, 0.f), 0.99999994f);
+            const int p = jfl - pbase;
+            if (p < 0 || p >= npos) continue;  // reaches no sample of this tile
+            const float dzf = (float)dz;  // one XU conversion instead of shared-memory loads (the smem pipe binds)
+            const float cth = fmaf(dzf, oz, cr.cdot) * rx;
+            float gain = ga + (1.f - ga) * cth;
+            if (dir_src) gain *= src_gain(sm.colsdot[j], odd, dzf, rx, g);
+            const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
+            const float y = fmaf(2.f, phi, -1.f);            // 2 phi - 1 in [-1, 1)
+            poly_add(Ga, Gb, W, p + (p >> 3), y, amp, scalef, scale_lf, J, cmask, two_word, acc);
+          }
+          };
+          if (T.use_bz && !T.two_word && g.as == 1.f) walk(std::true_type());
+          else walk(std::false_type());
+          if (acc == 0u) sm.ti.ovf = 1;  // a position of this tile reached its count capacity
+        }
+        __syncthreads();  // column records are replaced by the next batch
+      }
+      const int ovf = sm.ti.ovf;  // read after the last batch's barrier; uniform
+      if (!ovf) break;
+      __syncthreads();  // everyone has read the flag before thread 0 changes the format
+      if (tid == 0) {
+        PolyTile& Tw = sm.ti;
+        Tw.ovf = 0;
+        Tw.redo = 1;
+        if (!Tw.two_word && A.poly_gb) {
+          poly_set_format(Tw, 28, 1, 0);
+        } else {
+          atomicOr(A.status, kStatusCapacity);
+          Tw.redo = 0;
         }
       }
       __syncthreads();
-      const int tot = sm.scan_tmp[kPolyThreads / 32 - 1];
-      const int total = tot & 0xFFFFF, ncomp = tot >> 20;
-      const int R = (total + kPolyThreads - 1) / kPolyThreads;
-      const int g0 = tid * R, g1 = min(g0 + R, total);
-      if (g0 < g1) {
-        int lo = 0, hi = ncomp - 1;  // first (compacted) column with colpre > g0
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (sm.colpre[mid] > g0) hi = mid; else lo = mid + 1;
-        }
-        int j = lo;
-        const int zl = T.zl;
-        const float oz = g.o[2], ga = g.a, scalef = T.scalef;
-        PolyColRec cr = load_col(&sm.col[j]);  // the current column's record, in registers
-        // the walk, compiled twice: the common case (single word, omni source, z factors from the table) with
-        // its flags as constants — fewer live registers, so fewer loop constants re-read from shared memory —
-        // and the general case with runtime flags
-        auto walk = [&](auto fast) {
-        constexpr bool kFast = decltype(fast)::value;
-        const bool use_bz = kFast || T.use_bz, dir_src = !kFast && g.as != 1.f, two_word = !kFast && T.two_word;
-        const double Lzs = T.Lzs, offEs = T.offEs, offOs = T.offOs;
-        for (int gi = g0; gi < g1; gi++) {  // every lane runs R candidates: the walk keeps the warp converged
-          // compacted columns are nonempty and gi advances by one: a change moves exactly one column on
-          if (gi >= cr.end) cr = load_col(&sm.col[++j]);
-          const int nz = gi + (gi < cr.b ? cr.a1 : cr.a2);
-          const int odd = nz & 1;
-          const float bz = use_bz ? sm.bz[min(max(nz - zl, 0), kPolyBz - 1)] : poly_z_factor(nz, g);
-          const int nzo = nz + odd;
-          // Eq. 1 along z, in samples (the tile's constants are read from shared memory: no conversions here)
-          const double dz = fma(int_to_double(nzo), Lzs, odd ? offOs : offEs);
-          const double x2 = fma(dz, dz, cr.rho2);                             // (d fs / c)^2
-          if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); continue; }
-          float x0f, xd, rx;  // x = x0f + xd (xd the fp64 Newton correction); rx = 1/x
-          delay_split(x2, x0f, xd, rx);
-          // floor of the fp32 sum x0f + xd, fraction from the exact difference x0f - floor plus xd: within 1e-7
-          // of an integer the rounded sum may pick the neighbouring floor, and the clamp moves phi by < 1e-7
-          // (delta' (m - phi) is continuous from tap m at phi = 1 to tap m + 1 at phi = 0)
-          int jfl;
-          const float fj = floor_int(x0f + xd, jfl);
-          const float phi = fminf(fmaxf((x0f - fj) + xd, 0.f), 0.99999994f);
-          const int p = jfl - pbase;
-          if (p < 0 || p >= npos) continue;  // reaches no sample of this tile
-          const float dzf = (float)dz;  // one XU conversion instead of shared-memory loads (the smem pipe binds)
-          const float cth = fmaf(dzf, oz, cr.cdot) * rx;
-          float gain = ga + (1.f - ga) * cth;
-          if (dir_src) gain *= src_gain(sm.colsdot[j], odd, dzf, rx, g);
-          const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
-          const float y = fmaf(2.f, phi, -1.f);            // 2 phi - 1 in [-1, 1)
-          poly_add(Ga, Gb, W, p + (p >> 3), y, amp, scalef, two_word);
-        }
-        };
-        if (T.use_bz && !T.two_word && g.as == 1.f) walk(std::true_type());
-        else walk(std::false_type());
+      if (!sm.ti.redo) break;
+      {
+        const int n4 = (kPolyD * W) >> 2;
+        for (int i = tid; i < n4; i += kPolyThreads) reinterpret_cast<int4*>(Ga)[i] = make_int4(0, 0, 0, 0);
+        if (sm.ti.two_word)
+          for (int i = tid; i < n4; i += kPolyThreads) reinterpret_cast<int4*>(Gb)[i] = make_int4(0, 0, 0, 0);
       }
-      __syncthreads();  // column records are replaced by the next batch
+      __syncthreads();
     }
 
     // ---- 2. fixed point -> fp32, in place (every word converts itself: no staging, one barrier) ---------
     float* Gf = reinterpret_cast<float*>(Ga);
+    constexpr int kLast = kPolyChannels - 1;  // the channel whose word also counts (poly_add)
     if (T.two_word) {
       for (int i = tid; i < kPolyD * W; i += kPolyThreads)
-        Gf[i] = (float)((double)((long long)Ga[i] * 16384 + Gb[i]) * T.inv_scale);
+        Gf[i] = (i >= kLast * W && i < (kLast + 1) * W) ? (float)((double)Ga[i] * 16384.0 * T.inv_scale)
+                                                        : (float)((double)((long long)Ga[i] * 16384 + Gb[i]) * T.inv_scale);
     } else {  // single word, |sum| < 2^31: one rounding to fp32 (I2FP, ALU pipe), then an exact power-of-two scale
+      // each thread owns 4 positions of every plane: it reads their counts from the last channel's low bits
+      // and removes count x 0x4B400000 (the raw-bit deposits of poly_add) from every channel
       const float is = T.inv_scalef;
-      for (int i = tid; i < (kPolyD * W) >> 2; i += kPolyThreads) {
-        const int4 v = reinterpret_cast<const int4*>(Ga)[i];
-        reinterpret_cast<float4*>(Gf)[i] =
-            make_float4((float)v.x * is, (float)v.y * is, (float)v.z * is, (float)v.w * is);
+      const unsigned mask = T.cnt_mask, kLastOff = 1u + (0x4B400000u << T.J);
+      const int w4 = W >> 2;  // W is a multiple of 4
+      for (int q = tid; q < w4; q += kPolyThreads) {
+        const uint4 c = reinterpret_cast<const uint4*>(Ga)[kLast * w4 + q];
+        const uint4 n = make_uint4(c.x & mask, c.y & mask, c.z & mask, c.w & mask);
+#pragma unroll
+        for (int d = 0; d < kPolyD; d++) {
+          const unsigned off = d < kLast ? 0x4B400000u : d == kLast ? kLastOff : 0u;  // planes past kLast stay 0
+          const uint4 v = d == kLast ? c : reinterpret_cast<const uint4*>(Ga)[d * w4 + q];
+          reinterpret_cast<float4*>(Gf)[d * w4 + q] =
+              make_float4((float)(int)(v.x - n.x * off) * is, (float)(int)(v.y - n.y * off) * is,
+                          (float)(int)(v.z - n.z * off) * is, (float)(int)(v.w - n.w * off) * is);
+        }
       }
     }
     __syncthreads();
@@ -494,8 +592,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           A.out[T.row + k] = (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
       }
       if (T.tail)
-        poly_fused_tail(sm.ti, red, tid, kPolyThreads, A.out, A.tail_nS, A.tail_win, A.tail_kappa_fs, A.tail_seed,
-                        A.tail_rir_base);
+        poly_fused_tail(sm.ti, red, tid, kPolyThreads, A.out, A.tail_win, A.tail_seed);
     }
     __syncthreads();  // G and the tile record are reused by the next work item
   }
@@ -538,11 +635,17 @@ static cudaError_t launch_poly(const IsmArgs& A, long long n_work, int* counter,
 cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
-  const bool two_word = A.poly_gb != 0;
-  const size_t s256 = poly_smem_bytes<256>(A.poly_ntaps, two_word);
-  if (!two_word && 4 * s256 <= 224 * 1024 && n_work >= 16LL * num_sms)
-    return launch_poly<256>(A, n_work, counter, s256, num_sms, stream);
-  return launch_poly<512>(A, n_work, counter, poly_smem_bytes<512>(A.poly_ntaps, two_word), num_sms, stream);
+  const bool two_word = A.poly_gbz != 0;  // some tile starts in the two-word format
+  const size_t s256 = poly_smem_bytes<256>(A.poly_ntaps, false);
+  IsmArgs B = A;
+  if (!two_word && 4 * s256 <= 224 * 1024 && n_work >= 16LL * num_sms) {
+    B.poly_gb = 0;
+    return launch_poly<256>(B, n_work, counter, s256, num_sms, stream);
+  }
+  // 512-thread CTAs carry the fine plane whenever two of them still fit an SM with it (the guard's last rung)
+  const size_t s1 = poly_smem_bytes<512>(A.poly_ntaps, false), s2 = poly_smem_bytes<512>(A.poly_ntaps, true);
+  B.poly_gb = two_word || 2 * (s2 + 1024) <= 228 * 1024;
+  return launch_poly<512>(B, n_work, counter, B.poly_gb ? s2 : s1, num_sms, stream);
 }
 
 }  // namespace gpurir

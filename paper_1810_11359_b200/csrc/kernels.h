@@ -72,8 +72,12 @@ struct IsmArgs {
   // polyphase mode (reading R11): delta'(m - phi) = sum_d P[m - mlo][d] T_d(2 phi - 1), m = mlo .. mlo + ntaps - 1
   const float* poly_P;     // device [ntaps][8]
   int poly_ntaps, poly_mlo;
-  int poly_gb;             // some tile of the call may need the two-word scheme: allocate the fine plane Gb
+  int poly_gbz;            // some tile of the call starts in the two-word scheme: zero the fine plane Gb per tile
+  int poly_gb;             // set by the launcher: the fine plane Gb is allocated (two-word tiles, guard's last rung)
   int poly_force2;         // test hook (opts.split == -2): every tile uses the two-word scheme
+  int poly_hook;           // test hooks of the count guard (capacity 4 images per position): 2 (split -3) on the
+                           // first pass (-> redo in two words, or the capacity status without the fine plane);
+                           // 3 (split -5) two words on every tile (-> the capacity status)
   // polyphase single-room calls: the diffuse tail fused into the kernel — the CTA that finishes a RIR's last
   // (end-aligned) ISM tile, which holds the whole envelope window, writes that RIR's tail (tail_common.cuh)
   int poly_tail;

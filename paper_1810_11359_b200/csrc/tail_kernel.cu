@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(TailArgs A, long lon
   const long long q0 = (long long)(nISM >> 2);
   const long long qend = (long long)((nS + 3) >> 2);
   const PhiloxKey key = philox_key(make_uint2((uint32_t)A.seed, (uint32_t)(A.seed >> 32)));
-  const bool aligned = ((row & 3) == 0);
+  const bool aligned = (reinterpret_cast<uintptr_t>(A.out + row) & 15) == 0;  // float4 stores: 16-B row start
   const long long qbeg = q0 + (long long)chunk * A.chunk_quads;
   const long long qlim = min(qend, qbeg + (long long)A.chunk_quads);
 #pragma unroll 2

@@ -84,3 +84,55 @@ def gather_rows(local, M_total: int, world: int, rank: int):
     if rank != 0:
         return None
     return torch.cat([bufs[r][: sizes[r][1] - sizes[r][0]] for r in range(world)], dim=0)
+
+
+def batch_shard(rooms: Sequence[dict], costs: Sequence[float], world: int, rank: int):
+    """The rooms of `rank` under the LPT plan (config 5 over `world` GPUs): (global indices, rooms with their
+    global `rir_index` kept — so each tail RNG stream, reading C16, is the unsharded one — and compact ragged
+    `out_offset`s, total samples).  `rooms` are gpurir_room dicts whose `out_offset` is ignored here; the
+    samples of room i are `n_samples[i]` = ceil(Tmax_i fs), passed in as the dicts' 'n' key."""
+    plan = lpt_plan(costs, world)
+    idx = plan[rank]
+    mine, off = [], 0
+    for i in idx:
+        r = dict(rooms[i])
+        r["rir_index"] = int(rooms[i].get("rir_index", i))
+        r["out_offset"] = off
+        off += int(r.pop("n"))
+        mine.append(r)
+    return idx, mine, off
+
+
+def gather_ragged(local, idx, n_samples: Sequence[int], world: int, rank: int):
+    """Gather every rank's compact batch output (1-D, rooms in `idx` order) to rank 0 as one ragged buffer in
+    global room order (None on other ranks).  Host-side (gloo or nccl), outside any timed region."""
+    import torch
+    import torch.distributed as dist
+    n_samples = np.asarray(n_samples, dtype=np.int64)
+    starts = np.concatenate([[0], np.cumsum(n_samples)])
+    if not dist.is_initialized() or world == 1:
+        out = torch.empty(int(starts[-1]), dtype=local.dtype, device=local.device)
+        pos = 0
+        for i in idx:
+            out[starts[i]:starts[i + 1]] = local[pos:pos + n_samples[i]]
+            pos += int(n_samples[i])
+        return out
+    sizes = torch.tensor([local.numel()], dtype=torch.int64, device=local.device)
+    all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes)
+    mx = int(max(s.item() for s in all_sizes))
+    pad = torch.zeros((mx,), dtype=local.dtype, device=local.device)
+    pad[: local.numel()] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
+    dist.gather(pad, gather_list=bufs, dst=0)
+    idxs = [None] * world
+    dist.all_gather_object(idxs, [int(i) for i in idx])
+    if rank != 0:
+        return None
+    out = torch.empty(int(starts[-1]), dtype=local.dtype, device=local.device)
+    for r in range(world):
+        pos = 0
+        for i in idxs[r]:
+            out[starts[i]:starts[i + 1]] = bufs[r][pos:pos + n_samples[i]]
+            pos += int(n_samples[i])
+    return out

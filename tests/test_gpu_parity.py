@@ -115,14 +115,20 @@ def test_cfg1_modes(P, oracle, mode):
     assert rel_err(g, r)[0] <= TOL[mode]
 
 
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex", "poly"])
 @pytest.mark.parametrize("T60", [0.1, 0.2, 0.5, 0.9, 1.4, 2.0])
-def test_cfg2_t60_sweep(P, oracle, T60):
-    """ISM to T60/4 + diffuse tail to T60 (tail RNG is bit-reproducible, so parity covers every sample)."""
+def test_cfg2_t60_sweep(P, oracle, T60, mode):
+    """ISM to T60/4 + diffuse tail to T60 (tail RNG is bit-reproducible, so parity covers every sample), in
+    every mode (north_star: fp32 and fp16 across all five configs).  The lone RIR's poly call is forced onto
+    the polyphase kernel too (split = -1) besides the default (direct kernels below 32 work items)."""
     sc = W.cfg2(T60)
     beta, nb = derive(oracle, sc)
-    g = run_gpu(P, sc, beta, nb)
     r = run_oracle(oracle, sc, beta, nb)
-    assert rel_err(g, r)[0] <= TOL["fp32"], T60
+    g = run_gpu(P, sc, beta, nb, mode=mode)
+    assert rel_err(g, r)[0] <= TOL[mode], T60
+    if mode == "poly":
+        g = run_gpu(P, sc, beta, nb, mode=mode, split=-1)
+        assert rel_err(g, r)[0] <= TOL[mode], T60
 
 
 @pytest.mark.parametrize("kernel", ["auto", "persistent"])
@@ -375,30 +381,170 @@ def test_reciprocity_gpu(P, oracle):
     assert rel_err(a, b)[0] <= 1e-5
 
 
-@pytest.mark.parametrize("mode", ["fp32", "poly"])
+def _batch(oracle, rb, idx, base_off=0, rir_index=None):
+    """gpurir_room dicts of rooms idx of a workloads.RoomBatch (beta, nb_img from the oracle's helpers), packed
+    into ragged rows from base_off; returns (rooms, row offsets, total samples)."""
+    rooms, offs, off = [], [], base_off
+    for k, i in enumerate(idx):
+        beta, _ = oracle.beta_sabine(rb.room[i], rb.T60[i])
+        nb = oracle.t2n(rb.Tdiff[i], rb.room[i])
+        rooms.append(dict(room_sz=rb.room[i], beta=beta.astype(np.float32), pos_src=rb.pos_src[i],
+                          pos_rcv=rb.pos_rcv[i], nb_img=nb, Tdiff=rb.Tdiff[i], Tmax=rb.Tmax[i], out_offset=off,
+                          rir_index=int(i if rir_index is None else rir_index[k])))
+        offs.append(off)
+        off += oracle.nsamples(rb.Tmax[i], rb.fs)
+    return rooms, offs, off
+
+
+def _oracle_room(oracle, rb, room, base):
+    src = np.asarray(room["pos_src"], np.float32)[None]
+    rcv = np.asarray(room["pos_rcv"], np.float32)[None]
+    return oracle.simulate_rir(room["room_sz"], room["beta"], src, rcv, room["nb_img"], room["Tdiff"], room["Tmax"],
+                               fs=rb.fs, seed=rb.seed, rir_index_base=base + room["rir_index"])[0, 0]
+
+
+@pytest.mark.parametrize("mode", ["fp32", "lut", "fp16", "lut_tex", "poly"])
 def test_batch_rooms_vs_oracle(P, oracle, mode):
-    """config 5 shape: independent rooms, ragged rows, tail streams rir_index_base + i."""
+    """config 5 shape in every mode: independent rooms, ragged rows, tail streams rir_index_base + rir_index."""
     import torch
     rb = W.cfg5(12)
-    rooms, refs, off = [], [], 0
-    for i in range(rb.n):
-        beta, _ = oracle.beta_sabine(rb.room[i], rb.T60[i])
-        beta = beta.astype(np.float32)
-        nb = oracle.t2n(rb.Tdiff[i], rb.room[i])
-        nS = oracle.nsamples(rb.Tmax[i], rb.fs)
-        rooms.append(dict(room_sz=rb.room[i], beta=beta, pos_src=rb.pos_src[i], pos_rcv=rb.pos_rcv[i], nb_img=nb,
-                          Tdiff=rb.Tdiff[i], Tmax=rb.Tmax[i], out_offset=off))
-        refs.append(oracle.simulate_rir(rb.room[i], beta, rb.pos_src[i:i + 1], rb.pos_rcv[i:i + 1], nb, rb.Tdiff[i],
-                                        rb.Tmax[i], fs=rb.fs, seed=rb.seed, rir_index_base=1000 + i)[0, 0])
-        off += nS
-    out = torch.full((off,), float("nan"), device="cuda")
+    rooms, offs, tot = _batch(oracle, rb, range(rb.n))
+    out = torch.full((tot,), float("nan"), device="cuda")
     P.simulate_rir_batch(rooms, rb.fs, out, seed=rb.seed, rir_index_base=1000, sync=True, mode=mode)
     o = out.cpu().numpy().astype(np.float64)
-    off = 0
-    for i, r in enumerate(refs):
-        g = o[off:off + r.size]
-        off += r.size
-        assert rel_err(g, r)[0] <= TOL[mode], i
+    for i, room in enumerate(rooms):
+        r = _oracle_room(oracle, rb, room, 1000)
+        assert rel_err(o[offs[i]:offs[i] + r.size], r)[0] <= TOL[mode], i
+
+
+def test_batch_room_equals_single_room_call(P, oracle):
+    """Polyphase: a room's RIR in a batch is bit-identical to the same room simulated alone (end-aligned
+    tiles and per-tile fixed point in both; the batch fuses the diffuse tail like the single-room call)."""
+    import torch
+    rb = W.cfg5(40)
+    rooms, offs, tot = _batch(oracle, rb, range(rb.n))
+    out = torch.empty((tot,), device="cuda")
+    P.simulate_rir_batch(rooms, rb.fs, out, seed=rb.seed, rir_index_base=5, sync=True, mode="poly")
+    o = out.cpu().numpy()
+    for i in (0, 17, 39):
+        rm = rooms[i]
+        h = P.simulate_rir(rm["room_sz"], rm["beta"], torch.tensor([rm["pos_src"]], device="cuda"),
+                           torch.tensor([rm["pos_rcv"]], device="cuda"), rm["nb_img"], rm["Tdiff"], rm["Tmax"], rb.fs,
+                           mode="poly", split=-1, seed=rb.seed, rir_index_base=5 + i, sync=True).cpu().numpy()[0, 0]
+        assert np.array_equal(o[offs[i]:offs[i] + h.size], h), i
+
+
+@pytest.mark.parametrize("mode", ["poly", "fp32"])
+def test_batch_lpt_shards_reproduce_unsharded(P, oracle, mode):
+    """SURVEY §8(e) / P:167: an 8-way LPT shard of a 2000-room batch (rooms in LPT order, not contiguous), each
+    shard one batch call with the rooms' global rir_index, reproduces the unsharded call — bit for bit in
+    polyphase mode (a RIR's bits depend only on its own room), within the fp32 tolerance of each other in
+    direct mode (shards may take the other direct kernel)."""
+    import torch
+    from paper_1810_11359_b200 import shard
+    rb = W.cfg5(2000)
+    rooms, offs, tot = _batch(oracle, rb, range(rb.n))
+    full = torch.empty((tot,), device="cuda")
+    P.simulate_rir_batch(rooms, rb.fs, full, seed=rb.seed, mode=mode)
+    costs = [shard.room_cost(rb.room[i], rb.Tdiff[i], rb.Tmax[i], rb.fs) for i in range(rb.n)]
+    plan = shard.lpt_plan(costs, 8)
+    assert shard.plan_imbalance(costs, plan) < 1.01
+    got = torch.full((tot,), float("nan"), device="cuda")
+    for ranks in plan:
+        idx = list(ranks)
+        sub, soff, stot = _batch(oracle, rb, idx)
+        buf = torch.empty((stot,), device="cuda")
+        P.simulate_rir_batch(sub, rb.fs, buf, seed=rb.seed, mode=mode)
+        for k, i in enumerate(idx):
+            n = oracle.nsamples(rb.Tmax[i], rb.fs)
+            got[offs[i]:offs[i] + n] = buf[soff[k]:soff[k] + n]
+    torch.cuda.synchronize()
+    if mode == "poly":
+        assert torch.equal(got, full)
+    else:
+        f, g = full.cpu().numpy(), got.cpu().numpy()
+        for i in range(0, rb.n, 97):
+            n = oracle.nsamples(rb.Tmax[i], rb.fs)
+            assert rel_err(g[offs[i]:offs[i] + n], f[offs[i]:offs[i] + n])[0] <= TOL["fp32"], i
+
+
+def test_batch_full_size_cfg5_sampled(P, oracle):
+    """config 5 at full size: 100 000 random rooms in ONE batch call (polyphase, the bench's path), 64 rooms
+    sampled across the batch checked against the oracle, tail included."""
+    import torch
+    rb = W.cfg5(100_000)
+    rooms, offs, tot = _batch(oracle, rb, range(rb.n))
+    out = torch.empty((tot,), device="cuda")
+    P.simulate_rir_batch(rooms, rb.fs, out, seed=rb.seed, sync=True, mode="poly")
+    for i in np.linspace(0, rb.n - 1, 64).astype(int):
+        r = _oracle_room(oracle, rb, rooms[i], 0)
+        g = out[offs[i]:offs[i] + r.size].cpu().numpy().astype(np.float64)
+        assert rel_err(g, r)[0] <= TOL["poly"], i
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_batch_stream_ordered_workspace_and_status(P, oracle):
+    """The batch call is stream-ordered: two calls on two streams without synchronisation, one with a caller
+    workspace of exactly gpurir_workspace_bytes(), both correct after the streams drain; a workspace one byte
+    short is EINVAL; a degenerate room (source on the receiver) raises the CALLER's status word (opts.status),
+    not the device's shared one."""
+    import torch
+    rb = W.cfg5(300)
+    rooms, offs, tot = _batch(oracle, rb, range(rb.n))
+    need = P.workspace_bytes(rooms, rb.fs, mode="poly")
+    assert need > 0
+    ws = torch.empty((need,), dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    a, b = torch.empty((tot,), device="cuda"), torch.empty((tot,), device="cuda")
+    P.simulate_rir_batch(rooms, rb.fs, a, seed=rb.seed, mode="poly", stream=s1, workspace=ws)
+    P.simulate_rir_batch(rooms, rb.fs, b, seed=rb.seed, mode="poly", stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    for i in (0, 299):
+        r = _oracle_room(oracle, rb, rooms[i], 0)
+        assert rel_err(a[offs[i]:offs[i] + r.size].cpu().numpy().astype(np.float64), r)[0] <= TOL["poly"]
+    with pytest.raises(P.GpurirError) as e:
+        P.simulate_rir_batch(rooms, rb.fs, a, mode="poly", workspace=ws[:need - 1])
+    assert e.value.status == P._lib.EINVAL
+    bad = [dict(rooms[0], pos_rcv=rooms[0]["pos_src"])]
+    st = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    P.simulate_rir_batch(bad, rb.fs, a, mode="poly", split=-1, status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) != 0 and P.device_status(reset=True) == 0
+    st.zero_()
+    with pytest.raises(P.GpurirError) as e:
+        P.simulate_rir_batch(bad, rb.fs, a, mode="poly", split=-1, status=st, sync=True)
+    assert e.value.status == P._lib.EDEGENERATE and int(st.item()) == 0
+
+
+@pytest.mark.parametrize("mode", ["poly", "fp32"])
+def test_misaligned_output_rows(P, oracle, mode):
+    """an output view starting 4 bytes into an allocation (contiguous, not 16-B aligned) — the tail's
+    float4 stores must fall back to scalar stores (fused polyphase tail and tail_kernel alike)."""
+    import torch
+    sc = W.cfg3(64, "diffuse")
+    beta, nb = derive(oracle, sc)
+    ref = run_gpu(P, sc, beta, nb, mode=mode).astype(np.float32)
+    nS = ref.shape[-1]
+    buf = torch.empty((64 * nS + 1,), device="cuda")
+    out = buf[1:]
+    src = torch.from_numpy(sc.pos_src).cuda()
+    rcv, orv = torch.from_numpy(sc.pos_rcv).cuda(), torch.from_numpy(sc.orV_rcv).cuda()
+    P.simulate_rir(sc.room, beta, src, rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, orV_rcv=orv, mic_pattern=sc.pattern,
+                   mode=mode, seed=sc.seed, out=out, sync=True)
+    assert np.array_equal(out.cpu().numpy().reshape(ref.shape), ref)
+
+
+def test_host_call_small_last_chunk_bit_identical(P, oracle):
+    """a host call whose last chunk has 10 receivers (2058 = 2048 + 10; 30 polyphase work items,
+    below the kernel's 32) still runs every chunk on the polyphase kernel: the bits of one device call."""
+    sc = W.cfg3(2058, "diffuse")
+    beta, nb = derive(oracle, sc)
+    ref = run_gpu(P, sc, beta, nb, mode="poly").astype(np.float32)
+    got = P.simulate_rir_host(sc.room, beta, sc.pos_src, sc.pos_rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c,
+                              orV_rcv=sc.orV_rcv, mic_pattern=sc.pattern, mode="poly", seed=sc.seed)
+    assert np.array_equal(got, ref)
 
 
 # ---------------------------------------------------------------- NEXT row f1: trajectory filtering
@@ -676,3 +822,114 @@ def test_poly_cta_shapes_bit_identical(P, oracle):
         rj = oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[m:m + 1], nb, sc.Tdiff, sc.Tmax, fs=sc.fs,
                                  pattern=sc.pattern, orV_rcv=sc.orV_rcv[m:m + 1], seed=sc.seed, rir_index_base=m)
         assert rel_err(full[0, m], rj[0, 0])[0] <= TOL["poly"], m
+
+
+def test_poly_count_guard_redo(P, oracle):
+    """The polyphase overflow guard (poly_add): with the test hook split = -3 every tile's first pass has a
+    count capacity of 4 images per sample position, so the guard fires on nearly every tile; a call whose
+    512-thread CTAs hold the fine plane (64 receivers) redoes those tiles in the two-word format and must match
+    the oracle at the fp32 tolerance, and its shards the whole call bit for bit (the format depends only on the
+    tile's own images)."""
+    sc = W.cfg3(64, "diffuse")
+    beta, nb = derive(oracle, sc)
+    g = run_gpu(P, sc, beta, nb, mode="poly", split=-3)
+    for m in (0, 32, 63):  # each RIR keeps its global index (tail stream, reading C16)
+        r = oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[m:m + 1], nb, sc.Tdiff, sc.Tmax, fs=sc.fs,
+                                pattern=sc.pattern, orV_rcv=sc.orV_rcv[m:m + 1], seed=sc.seed, rir_index_base=m)
+        assert rel_err(g[:, m], r[:, 0]).max() <= TOL["poly"], m
+    part = run_gpu(P, sc, beta, nb, mode="poly", split=-3, rir_index_base=16, pos_rcv=sc.pos_rcv[16:48],
+                   orv=sc.orV_rcv[16:48])
+    assert np.array_equal(g[:, 16:48], part)
+
+
+def test_poly_count_guard_capacity_status(P, oracle):
+    """Where the redo has no room — 256-thread CTAs without the fine plane (1024 receivers, split = -3), or a
+    two-word tile that fires (split = -5) — the call must fail loudly with GPURIR_ECAPACITY, never return a
+    wrapped sum as a result; the status word is cleared afterwards."""
+    beta = None
+    for split, M in ((-3, 1024), (-5, 64)):
+        sc = W.cfg3(M, "diffuse")
+        beta, nb = derive(oracle, sc)
+        with pytest.raises(P.GpurirError) as ei:
+            run_gpu(P, sc, beta, nb, mode="poly", split=split)
+        assert ei.value.status == P._lib.ECAPACITY, split
+    assert P.device_status(reset=True) == 0
+
+
+@pytest.mark.parametrize("fs,T", [(16000.0, 0.6), (48000.0, 0.3)])
+def test_poly_worst_geometry_found(P, oracle, fs, T):
+    """The geometry tests/test_poly_headroom.py's brute force found closest to the single-word capacity (35 %
+    of it at 48 kHz): a 2 m cube, source at the centre, receiver 1 mm above it, rigid walls (beta = +-1: every
+    image at full amplitude).  Polyphase (default path, no hooks) vs the oracle at the fp32 tolerance."""
+    import torch
+    room = np.array([2.0, 2.0, 2.0], np.float32)
+    src = np.array([[1.0, 1.0, 1.0]], np.float32)
+    rcv = np.array([[1.0, 1.0, 1.0 + 2.0 ** -10], [1.0, 1.0, 1.5]], np.float32)
+    nb = oracle.t2n(T, room, 343.0)
+    for b in (1.0, -1.0):
+        beta = np.full(6, b, np.float32)
+        g = P.simulate_rir(room, beta, torch.from_numpy(src).cuda(), torch.from_numpy(rcv).cuda(), nb, T, T, fs,
+                           mode="poly", split=-1, sync=True).cpu().numpy().astype(np.float64)
+        r = oracle.simulate_rir(room, beta, src, rcv, nb, T, T, fs=fs)
+        assert rel_err(g, r).max() <= TOL["poly"], (b, rel_err(g, r).max())
+
+
+@pytest.fixture(scope="module")
+def curand_lib(tmp_path_factory):
+    import ctypes
+    import subprocess
+    d = tmp_path_factory.mktemp("curand")
+    so = str(d / "libcurand_stream.so")
+    src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "curand_stream.cu")
+    subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-shared",
+                    "-Xcompiler", "-fPIC", "-o", so, src], check=True)
+    L = ctypes.CDLL(so)
+    L.curand_words.restype = ctypes.c_int
+    L.curand_words.argtypes = [ctypes.c_ulonglong, ctypes.c_ulonglong, ctypes.c_ulonglong, ctypes.c_int,
+                               ctypes.c_void_p]
+    return L
+
+
+@pytest.mark.parametrize("seed,r,k0", [(0, 0, 0), (0x5EED0003, 5, 8400), (0xFFFFFFFF12345678, 2**33 + 7, 2**32 - 6),
+                                       (12345, 99999, 1)])
+def test_tail_rng_is_curand_philox_stream(oracle, curand_lib, seed, r, k0):
+    """The library special case of SURVEY §8(c)'s RNG row: the oracle's uniform u(seed, r, k) = (2 (w >> 9) + 1)
+    2^-24 takes w = the k-th word of cuRAND's device API after curand_init(seed, subsequence = r, offset = 0)
+    — pinning the counter layout (k >> 2 in the low, r in the high counter words), the key and the word order
+    (x, y, z, w) against an implementation that is not ours.  Offsets k0 straddle a 2^32 counter carry."""
+    import torch
+    n = 64
+    buf = torch.zeros((n,), dtype=torch.int32, device="cuda")
+    assert curand_lib.curand_words(seed, r, k0, n, buf.data_ptr()) == 0
+    w = buf.cpu().numpy().view(np.uint32).astype(np.uint64)
+    u_curand = (2.0 * (w >> np.uint64(9)).astype(np.float64) + 1.0) / 16777216.0
+    u_oracle = np.array([oracle.uniform(seed, r, k0 + i) for i in range(n)])
+    assert np.array_equal(u_curand, u_oracle)
+
+
+def test_cfg5_two_ranks_through_the_library(P, tmp_path):
+    """SURVEY §8(e) through the library, not the oracle: config-5 rooms LPT-sharded over 2 ranks (two processes
+    on cuda:0, torch.distributed gloo, one batch call per rank) and gathered to rank 0 equal the 1-rank call
+    bit for bit (polyphase; every room keeps its global rir_index)."""
+    import socket
+    import subprocess
+    import sys
+    import torch
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import shard_worker
+    rb, rooms, costs, ns = shard_worker.rooms_of(P, W, 600)
+    one = [dict(r, out_offset=int(sum(ns[:i]))) for i, r in enumerate(rooms)]
+    for r in one:
+        r.pop("n")
+    ref = torch.empty((int(sum(ns)),), device="cuda")
+    P.simulate_rir_batch(one, rb.fs, ref, seed=rb.seed, mode="poly", sync=True)
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    out = str(tmp_path / "two_ranks.npy")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                                  "shard_worker.py"), "--out", out]
+    subprocess.run(cmd, check=True, timeout=600)
+    got = np.load(out)
+    assert np.array_equal(got, ref.cpu().numpy())

@@ -459,6 +459,19 @@ def test_uniform_open_interval(oracle):
         assert m == int(m) and int(m) % 2 == 1
 
 
+def test_uniform_is_curand_device_stream(oracle):
+    """The counter / key / word layout of oracle_uniform (reading C16) against cuRAND itself: P:223 draws the
+    tail noise with cuRAND, and tests/golden/curand_philox4x32_10.txt holds words of cuRAND's device-API stream
+    (curand_init(seed, subsequence = r, offset = k0), then curand()) written on a B200 box by
+    tools/gen_curand_golden.py, which calls only cuRAND.  A swapped (k, r) counter, a reversed word order or a
+    wrong key half fails here; offsets straddle a 2^32 counter carry (r = 2^33 + 7, k near 2^32)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "curand_philox4x32_10.txt")
+    rows = [tuple(int(v) for v in line.split()) for line in open(path) if line.strip() and not line.startswith("#")]
+    assert len(rows) >= 60
+    for seed, r, k, w in rows:
+        assert oracle.uniform(seed, r, k) == (2.0 * (w >> 9) + 1.0) / 16777216.0, (seed, r, k)
+
+
 def test_logistic_moments(oracle):
     """1e6 unit-variance logistic draws: mean within +-0.005, variance 1 +- 0.05."""
     x = oracle.logistic_stream(0x5EED0002, 9, 0, 10 ** 6)

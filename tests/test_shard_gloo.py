@@ -82,3 +82,45 @@ def test_two_rank_gloo_shard_gather_bitwise():
     same, t = q.get(timeout=10)
     assert same
     assert t == 2.0
+
+
+def _batch_worker(rank, world, port, q):
+    """config 5 host path: batch_shard + gather_ragged over gloo, with synthetic per-room rows standing in for
+    the batch call's output (each room's row encodes its global index and sample, so any misplacement shows)."""
+    import torch.distributed as dist
+
+    import workloads as W
+    from paper_1810_11359_b200.shard import batch_shard, gather_ragged, room_cost
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rb = W.cfg5(300)
+    ns = [int(np.ceil(rb.Tmax[i] * rb.fs - 1e-6)) for i in range(rb.n)]
+    rooms = [dict(rir_index=i, n=ns[i], Tmax=rb.Tmax[i]) for i in range(rb.n)]
+    costs = [room_cost(rb.room[i], rb.Tdiff[i], rb.Tmax[i], rb.fs) for i in range(rb.n)]
+    idx, mine, tot = batch_shard(rooms, costs, world, rank)
+    local = torch.empty((tot,), dtype=torch.float64)
+    for r in mine:  # the "RIR" of room i: 1e6 i + k at sample k
+        n = int(np.ceil(r["Tmax"] * rb.fs - 1e-6))
+        local[r["out_offset"]:r["out_offset"] + n] = torch.arange(n, dtype=torch.float64) + 1e6 * r["rir_index"]
+    full = gather_ragged(local, idx, ns, world, rank)
+    if rank == 0:
+        ref = np.concatenate([np.arange(ns[i], dtype=np.float64) + 1e6 * i for i in range(rb.n)])
+        q.put(bool(np.array_equal(full.numpy(), ref)) and sorted(int(i) for i in idx) != list(range(rb.n)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_batch_shard_gather():
+    """LPT shards of rooms (non-contiguous global indices) gathered back to rank 0 in
+    global room order, world_size 2 over gloo."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert q.get(timeout=10)

@@ -7,4 +7,4 @@ cd "$(dirname "$0")/.."
 NAME=$1; shift
 mkdir -p build
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
-  -I include "$@" -o build/${NAME}.so paper_1810_11359_b200/csrc/*.cu
+  -I include -DGPURIR_VARIANT=\"${NAME}\" "$@" -o build/${NAME}.so paper_1810_11359_b200/csrc/*.cu
