@@ -244,7 +244,6 @@ const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t 
                                   // (A/B: fusing is faster at every M from 12 to 2048, so always)
 #endif
 constexpr long long kHostChunkMin = 2048;  // RIRs per chunk of gpurir_simulate_rir_host (fills the GPU)
-constexpr long long kPolyMinItems = 32;  // smaller polyphase calls take the direct fp32 kernels
 
 // Polyphase fixed point (ism_poly_kernel.cu, tile setup): a tile needs the two-word scheme when its bound on
 // the images per sample position, N = 8 pi x_hi^2 / V_s + 24 x_hi / L_min + 16 (x_hi the tile's largest delay,
@@ -428,7 +427,7 @@ int plan_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, const
   const double H = o.Tw * fs / 2.0;
   if ((int)ceil((kTCPersistent + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;
   P.jobs.resize(n_rooms);
-  long long small_tiles = 0, poly_tiles = 0;  // work items at the cluster kernel's / polyphase tile length
+  long long small_tiles = 0;  // work items at the cluster kernel's tile length (kernel choice)
   for (int i = 0; i < n_rooms; i++) {
     const gpurir_room& R = rooms[i];
     if (int e0 = validate_room(R.room_sz, R.beta, R.nb_img, R.mic_pattern)) return e0;
@@ -454,9 +453,8 @@ int plan_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, const
     J.rir_global = o.rir_index_base + R.rir_index;                        // reading C16: global stream id
     P.any_two_word = P.any_two_word || poly_two_word_for(R.room_sz, nISM, fs, c, o.Tw);
     small_tiles += (nISM + kTC - 1) / kTC;
-    poly_tiles += (nISM + kPolyTile - 1) / kPolyTile;
   }
-  P.poly = o.mode == GPURIR_POLY && (poly_tiles >= kPolyMinItems || o.split < 0);  // as single-room calls
+  P.poly = o.mode == GPURIR_POLY;
   P.kmode = o.mode == GPURIR_POLY ? (P.poly ? GPURIR_POLY : GPURIR_FP32) : o.mode;
   P.persistent = P.poly || use_persistent(small_tiles, o.split, num_sms);
   // polyphase: every room's diffuse tail is written by the CTA that finishes its last (end-aligned) ISM tile,
@@ -658,10 +656,9 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     A.M_src = M_src; A.M_rcv = M_rcv; A.M = (int)M;
     A.nISM = (int)nISM;
     A.row_stride = nS;
-    // polyphase mode on a call with fewer than kPolyMinItems 1024-sample work items (a lone RIR) runs the
-    // direct fp32 kernels instead: they spread one RIR's tiles over clusters of CTAs
-    const bool poly = o.mode == GPURIR_POLY &&
-                      (((nISM + kPolyTile - 1) / kPolyTile) * M >= kPolyMinItems || o.split < 0);  // split < 0 forces
+    // polyphase mode runs the polyphase kernel at every call size: small calls split each tile's columns over a
+    // thread-block cluster (ism_poly_kernel.cu), with the same bits as the persistent kernel
+    const bool poly = o.mode == GPURIR_POLY;
     const int kmode = o.mode == GPURIR_POLY ? (poly ? GPURIR_POLY : GPURIR_FP32) : o.mode;
     const bool persistent = poly || use_persistent(((nISM + kTC - 1) / kTC) * M, o.split, d->num_sms);
     const int tile_len = poly ? kPolyTile : persistent ? kTCPersistent : kTC;
@@ -691,7 +688,7 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
     if (poly) {
-      e = launch_ism_poly(A, nclusters, take_counter(d), d->num_sms, stream);
+      e = launch_ism_poly(A, nclusters, take_counter(d), d->num_sms, o.split, stream);
     } else if (persistent) {
       e = launch_ism_ws(A, kmode, nclusters, take_counter(d), d->num_sms, stream);
     } else {
@@ -797,13 +794,6 @@ int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const 
   gpurir_opts sub = o;
   sub.stream = cs;
   sub.flags &= ~GPURIR_FLAG_SYNC;
-  // polyphase: every chunk takes the kernel the whole call would (a small last chunk would otherwise fall back to
-  // the direct kernels, whose rounding differs), so the result equals one device call bit for bit
-  if (o.mode == GPURIR_POLY && o.split == 0 &&
-      ((gpurir_nsamples(std::min(Tdiff, Tmax), fs) + kPolyTile - 1) / kPolyTile) * M_src * (long long)M_rcv >=
-          kPolyMinItems)
-    sub.split = -1;
-  sub.ev_ism[0] = sub.ev_ism[1] = sub.ev_tail[0] = sub.ev_tail[1] = nullptr;
   long long k = 0;
   for (int s0 = 0; s0 < M_src && st == GPURIR_OK; s0 += src_chunk) {
     const int ns = std::min(src_chunk, M_src - s0);
@@ -929,7 +919,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     }
     const long long nw = (long long)P.tiles.size();
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
-    if (P.poly) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, stream);
+    if (P.poly) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, o.split, stream);
     else if (P.persistent) e = launch_ism_ws(A, P.kmode, nw, take_counter(d), d->num_sms, stream);
     else e = launch_ism(A, P.kmode, auto_split(nw, o.split), nw, stream);
     if (e != cudaSuccess) { release(); return cuda_fail(e, "launch_ism(batch)"); }

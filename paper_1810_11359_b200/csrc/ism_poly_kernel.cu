@@ -23,10 +23,13 @@
 // memory.
 // Work per output sample no longer grows with the image density (690 in-window taps per sample at config
 // 3 (i)): the filter costs 2H x 8 MACs, the aggregation 8 channel updates per image.
+#include <cooperative_groups.h>
 #include <type_traits>
 
 #include "ism_common.cuh"
 #include "tail_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gpurir {
 
@@ -91,17 +94,25 @@ struct PolyTile {
 // red): warp 0 reduces the envelope window from shared memory exactly as tail_kernel does from global memory,
 // then every thread writes Philox blocks of the tail.  Not inlined: the tail's registers (Philox round keys)
 // stay out of the image loop's allocation.
-__device__ __noinline__ void poly_fused_tail(PolyTile& T, const float* red, int tid, int nthreads, float* out,
-                                             int win, unsigned long long seed) {
+// The diffuse tail of the tile's RIR (tail_common.cuh, bit-identical to tail_kernel): warp 0 reduces the envelope
+// window — from the output partial sums still in shared memory (`red`, single-CTA items) or from the samples just
+// written to global memory (`hg`, cluster items) — then this CTA writes Philox blocks q0 + tid, + stride, ...
+// Not inlined: the tail's registers (Philox round keys) stay out of the image loop's allocation.
+__device__ __noinline__ void poly_fused_tail(PolyTile& T, const float* red, const float* hg, int tid, int nthreads,
+                                             float* out, int win, unsigned long long seed, int q_first,
+                                             int q_stride) {
   const int nISM = T.te, nS = T.tail_nS;
   if (tid < 32) {
     float env0, alpha, rho;
     const int t0 = T.t0;
-    tail_envelope([&](int k) {
-                    const int t = k - t0;
-                    return (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
-                  },
-                  nISM, win, T.x_dp, T.tail_kappa, tid, env0, alpha, rho);
+    if (hg)
+      tail_envelope([&](int k) { return hg[k]; }, nISM, win, T.x_dp, T.tail_kappa, tid, env0, alpha, rho);
+    else
+      tail_envelope([&](int k) {
+                      const int t = k - t0;
+                      return (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
+                    },
+                    nISM, win, T.x_dp, T.tail_kappa, tid, env0, alpha, rho);
     if (tid == 0) { T.tenv[0] = env0; T.tenv[1] = alpha; T.tenv[2] = rho; }
   }
   __syncthreads();
@@ -110,8 +121,9 @@ __device__ __noinline__ void poly_fused_tail(PolyTile& T, const float* red, int 
   float* row = out + T.row;
   const bool aligned = (reinterpret_cast<uintptr_t>(row) & 15) == 0;  // float4 stores need a 16-B row start
   const long long qend = (long long)((nS + 3) >> 2);
-  for (long long q = (long long)(nISM >> 2) + tid; q < qend; q += nthreads)
+  for (long long q = (long long)(nISM >> 2) + q_first + tid; q < qend; q += q_stride)
     tail_quad(q, nISM, nS, env0, alpha, rho, key, T.tail_rglob, row, aligned);
+  (void)nthreads;
 }
 
 template <int THREADS>
@@ -230,10 +242,20 @@ __host__ __device__ constexpr int poly_plane_words(int ntaps) {
 constexpr int kPolyWFixTaps = 64;
 constexpr int kPolyWFix = poly_plane_words(kPolyWFixTaps);
 
-template <int THREADS, int WFIX>
+// CL = false: persistent CTAs taking (RIR, tile) items from a queue (large calls).  CL = true (small calls): a
+// thread-block cluster of S CTAs per item — rank r aggregates the tile's columns r, r + S, ... into its own G,
+// the ranks' integer G planes are summed through distributed shared memory (exactly the single CTA's sums), and
+// rank r filters outputs [r 1024/S, (r + 1) 1024/S) with the same per-output arithmetic: bit-identical RIRs for
+// any call size.
+template <int THREADS, int WFIX, bool CL>
 __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     ism_poly_kernel(IsmArgs A, long long n_work, int* work_counter) {
   using C = PolyCfg<THREADS>;
+  int S = 1, rank = 0;
+  if constexpr (CL) {
+    S = (int)cg::this_cluster().num_blocks();
+    rank = (int)cg::this_cluster().block_rank();
+  }
   constexpr int kPolyThreads = C::kThreads, kPolyCols = C::kCols, kPolyGroup = C::kGroup, kPolyPass = C::kPass,
                 kPolyPasses = C::kPasses;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -249,6 +271,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
   const double fs_over_c = A.fs_over_c, sc2 = fs_over_c * fs_over_c;
   const float fs_over_c_4pi = (float)fs_over_c * 0.0795774715459476679f, fsc = (float)fs_over_c;
   const int m_hi = A.poly_mlo + ntaps - 1;
+  constexpr int kLast = kPolyChannels - 1;  // the channel whose word also counts (poly_add)
 
   for (int i = tid; i < ntaps * kPolyD; i += kPolyThreads) Pt[i] = A.poly_P[i];
 
@@ -261,7 +284,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       if (both)
         for (int i = tid - 32; i < n4; i += kPolyThreads - 32) reinterpret_cast<int4*>(Gb)[i] = make_int4(0, 0, 0, 0);
     } else if (tid == 0) {
-      const long long wi = atomicAdd(work_counter, 1);
+      const long long wi = CL ? (long long)(blockIdx.x / S) : atomicAdd(work_counter, 1);
       PolyTile& T = sm.ti;
       T.next = wi < n_work;
       if (wi < n_work) {
@@ -373,10 +396,11 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     for (;;) {
       const float amp_scale = fs_over_c_4pi;
       const int pbase = sm.ti.t0 - m_hi;  // p = floor(x) - pbase
-      for (int qb = 0; qb < T.ncols; qb += kPolyCols) {
+      const int ncl = CL ? (T.ncols - rank + S - 1) / S : T.ncols;  // this rank's columns: rank, rank + S, ...
+      for (int qb = 0; qb < ncl; qb += kPolyCols) {
         int cnt = 0;
         {
-          const int q = qb + tid;
+          const int q = CL ? (qb + tid) * S + rank : qb + tid;
           PolyColRec cr;
           cr.a1 = 0; cr.a2 = 0; cr.b = 0; cr.end = 0; cr.rho2 = 0.0; cr.bxy = 0.f; cr.cdot = 0.f;
           float sdot = 0.f;
@@ -461,12 +485,17 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             if (x2 == 0.0) { atomicOr(A.status, kStatusDegenerate); continue; }
             float x0f, xd, rx;  // x = x0f + xd (xd the fp64 Newton correction); rx = 1/x
             delay_split(x2, x0f, xd, rx);
-            // floor of the fp32 sum x0f + xd, fraction from the exact difference x0f - floor plus xd: within 1e-7
-            // of an integer the rounded sum may pick the neighbouring floor, and the clamp moves phi by < 1e-7
-            // (delta' (m - phi) is continuous from tap m at phi = 1 to tap m + 1 at phi = 0)
+            // floor of x0f (exact: x0f is a float), fraction (x0f - floor) + xd, then one step back or forward when
+            // xd carries the fraction out of [0, 1) (|xd| <= 2.4e-7 x).  Flooring the fp32 SUM x0f + xd instead
+            // picks the wrong integer within half an fp32 ulp of x (5e-4 samples at x ~ 1.3e4) and the clamp then
+            // moves phi by that much: harmless for one image, 1.7e-4 of peak for the ~500 images a rigid centred
+            // cube stacks on one delay at 48 kHz (tests/test_gpu_parity.py::test_poly_worst_geometry_found)
             int jfl;
-            const float fj = floor_int(x0f + xd, jfl);
-            const float phi = fminf(fmaxf((x0f - fj) + xd, 0.f), 0.99999994f);
+            const float fj = floor_int(x0f, jfl);
+            float phi = (x0f - fj) + xd;
+            if (phi < 0.f) { phi += 1.f; jfl -= 1; }
+            else if (phi >= 1.f) { phi -= 1.f; jfl += 1; }
+            phi = fminf(phi, 0.99999994f);  // phi + 1 rounds to 1 for phi > -3e-8
             const int p = jfl - pbase;
             if (p < 0 || p >= npos) continue;  // reaches no sample of this tile
             const float dzf = (float)dz;  // one XU conversion instead of shared-memory loads (the smem pipe binds)
@@ -485,7 +514,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         __syncthreads();  // column records are replaced by the next batch
       }
       const int ovf = sm.ti.ovf;  // read after the last batch's barrier; uniform
-      if (!ovf) break;
+      if (CL || !ovf) break;      // cluster items check the summed counts below (no redo: capacity status)
       __syncthreads();  // everyone has read the flag before thread 0 changes the format
       if (tid == 0) {
         PolyTile& Tw = sm.ti;
@@ -509,90 +538,170 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       __syncthreads();
     }
 
-    // ---- 2. fixed point -> fp32, in place (every word converts itself: no staging, one barrier) ---------
-    float* Gf = reinterpret_cast<float*>(Ga);
-    constexpr int kLast = kPolyChannels - 1;  // the channel whose word also counts (poly_add)
-    if (T.two_word) {
-      for (int i = tid; i < kPolyD * W; i += kPolyThreads)
-        Gf[i] = (i >= kLast * W && i < (kLast + 1) * W) ? (float)((double)Ga[i] * 16384.0 * T.inv_scale)
-                                                        : (float)((double)((long long)Ga[i] * 16384 + Gb[i]) * T.inv_scale);
-    } else {  // single word, |sum| < 2^31: one rounding to fp32 (I2FP, ALU pipe), then an exact power-of-two scale
-      // each thread owns 4 positions of every plane: it reads their counts from the last channel's low bits
-      // and removes count x 0x4B400000 (the raw-bit deposits of poly_add) from every channel
-      const float is = T.inv_scalef;
-      const unsigned mask = T.cnt_mask, kLastOff = 1u + (0x4B400000u << T.J);
-      const int w4 = W >> 2;  // W is a multiple of 4
-      for (int q = tid; q < w4; q += kPolyThreads) {
-        const uint4 c = reinterpret_cast<const uint4*>(Ga)[kLast * w4 + q];
-        const uint4 n = make_uint4(c.x & mask, c.y & mask, c.z & mask, c.w & mask);
+    if constexpr (CL) {
+      // ---- 2'. cluster: sum the ranks' integer planes over DSMEM for this rank's positions, fp32, FIR -------
+      cg::cluster_group cl = cg::this_cluster();
+      const int R = kPolyTC / S, o0 = rank * R, npp = R + ntaps - 1;  // outputs and positions of this rank
+      cl.sync();  // every rank's G is complete
+      float v[kPolyD];
+      bool bad = tid == 0 && T.ovf;  // this rank's own guard fired
+      const bool have = tid < npp;
+      if (have) {
+        const int p = o0 + tid, a = p + (p >> 3);
+        if (!T.two_word) {
+          unsigned w[kPolyD], n = 0;
 #pragma unroll
-        for (int d = 0; d < kPolyD; d++) {
-          const unsigned off = d < kLast ? 0x4B400000u : d == kLast ? kLastOff : 0u;  // planes past kLast stay 0
-          const uint4 v = d == kLast ? c : reinterpret_cast<const uint4*>(Ga)[d * w4 + q];
-          reinterpret_cast<float4*>(Gf)[d * w4 + q] =
-              make_float4((float)(int)(v.x - n.x * off) * is, (float)(int)(v.y - n.y * off) * is,
-                          (float)(int)(v.z - n.z * off) * is, (float)(int)(v.w - n.w * off) * is);
+          for (int d = 0; d < kPolyD; d++) w[d] = 0u;
+          for (int r = 0; r < S; r++) {
+            const unsigned* Gr = reinterpret_cast<const unsigned*>(cl.map_shared_rank(Ga, r));
+#pragma unroll
+            for (int d = 0; d < kPolyD; d++) w[d] += Gr[d * W + a];
+            n += Gr[kLast * W + a] & T.cnt_mask;  // the ranks' counts, summed without wrapping
+          }
+          bad = bad || n > T.cnt_mask;            // 2^J images on this position in all: as the guard
+          const unsigned kLastOff = 1u + (0x4B400000u << T.J);
+#pragma unroll
+          for (int d = 0; d < kPolyD; d++) {
+            const unsigned off = d < kLast ? 0x4B400000u : d == kLast ? kLastOff : 0u;
+            v[d] = (float)(int)(w[d] - n * off) * T.inv_scalef;
+          }
+        } else {
+          int ca[kPolyD], fb[kPolyD];
+#pragma unroll
+          for (int d = 0; d < kPolyD; d++) { ca[d] = 0; fb[d] = 0; }
+          for (int r = 0; r < S; r++) {
+            const int* Gar = cl.map_shared_rank(Ga, r);
+            const int* Gbr = cl.map_shared_rank(Gb, r);
+#pragma unroll
+            for (int d = 0; d < kPolyD; d++) { ca[d] += Gar[d * W + a]; fb[d] += Gbr[d * W + a]; }
+          }
+          bad = bad || (unsigned)fb[kLast] > T.cnt_mask;
+#pragma unroll
+          for (int d = 0; d < kPolyD; d++)
+            v[d] = d == kLast ? (float)((double)ca[d] * 16384.0 * T.inv_scale)
+                              : (float)((double)((long long)ca[d] * 16384 + fb[d]) * T.inv_scale);
         }
       }
-    }
-    __syncthreads();
-
-    // ---- 3. 8-channel FIR: h[k] = sum_m sum_d P_d[m] G_d[k - m] --------------------------------
-    // Thread group gq (THREADS/4 threads) applies channel pair gq to 8 consecutive outputs per thread with a
-    // sliding register window (one new position per tap); the 4 groups' partial sums meet in shared memory.
-    // ntaps is padded to a multiple of 8 with zero taps, so in every unrolled group of 8 taps the new
-    // positions q - mi - 1 - u sit at fixed offsets 0 .. -6, -8 of one padded address (q = 7 mod 8).
-    {
-      const int gq = tid / kPolyGroup, lt = tid % kPolyGroup;
-      const float* G0 = Gf + (2 * gq) * W;  // channel 2 gq; channel 2 gq + 1 sits W words further
-      float part[kPolyPasses][8];
+      cl.sync();  // every rank has read the remote planes: this rank's planes take its fp32 values
+      if (bad) atomicOr(A.status, kStatusCapacity);
+      float* Gf = reinterpret_cast<float*>(Ga);
+      if (have) {
+        const int a = tid + (tid >> 3);
 #pragma unroll
-      for (int pass = 0; pass < kPolyPasses; pass++) {
-        const int t8 = pass * kPolyPass + 8 * lt;
-        const float4* P4 = reinterpret_cast<const float4*>(Pt) + gq * (ntaps >> 1);  // pair gq: taps (2i, 2i+1)
-        float2 acc[8], w[8];
-        const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (m = m_lo)
-#pragma unroll
-        for (int r = 0; r < 8; r++) {
-          acc[r] = make_float2(0.f, 0.f);
-          const int a = (q + r) + ((q + r) >> 3);
-          w[r] = make_float2(G0[a], G0[a + W]);
+        for (int d = 0; d < kPolyD; d++) Gf[d * W + a] = v[d];
+      }
+      __syncthreads();
+      // FIR: one (output, channel) per thread and step; each channel's taps in the order of the single-CTA
+      // filter (fma chain over m = m_lo .. m_lo + ntaps - 1), then ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7))
+      // — the single-CTA path's pair sums and their combination: the same bits
+      for (int i = tid; i < R * kPolyD; i += kPolyThreads) {
+        const int o = i >> 3, d = i & 7;
+        const float* Gd = Gf + d * W;
+        const float* Pd = Pt + (d >> 1) * ntaps * 2 + (d & 1);
+        float acc = 0.f;
+        for (int mi = 0; mi < ntaps; mi++) {
+          const int pl = o + ntaps - 1 - mi;
+          acc = fmaf(Pd[2 * mi], Gd[pl + (pl >> 3)], acc);
         }
-        const float* gn = G0 + (q - 1) + ((q - 1) >> 3);  // padded address of position q - 1 (= 6 mod 8)
-        for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P4 += 4) {
-          const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};  // taps mi .. mi + 7 of channel pair gq
-#pragma unroll
-          for (int u = 0; u < 8; u++) {  // tap mi + u: output r uses slot (r - u) & 7, then slot (7 - u) & 7 refills
-            const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
-#pragma unroll
-            for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 7], acc[r]);
-            const int o = u < 7 ? -u : -8;  // the last group's refills read padding: never used
-            w[(7 - u) & 7] = make_float2(gn[o], gn[o + W]);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        const int k = T.t0 + o0 + o;
+        if (d == 0 && k < T.te) A.out[T.row + k] = acc;
+      }
+      if (T.tail) {  // uniform over the cluster: the tile's samples are in global memory once every rank is here
+        __threadfence();
+        cl.sync();
+        poly_fused_tail(sm.ti, nullptr, A.out + T.row, tid, kPolyThreads, A.out, A.tail_win, A.tail_seed,
+                        rank * kPolyThreads, S * kPolyThreads);
+      }
+      cl.sync();  // no rank leaves while another may still read its shared memory
+      break;      // one item per cluster
+    } else {
+      // ---- 2. fixed point -> fp32, in place (every word converts itself: no staging, one barrier) ---------
+      float* Gf = reinterpret_cast<float*>(Ga);
+      if (T.two_word) {
+        for (int i = tid; i < kPolyD * W; i += kPolyThreads)
+          Gf[i] = (i >= kLast * W && i < (kLast + 1) * W) ? (float)((double)Ga[i] * 16384.0 * T.inv_scale)
+                                                          : (float)((double)((long long)Ga[i] * 16384 + Gb[i]) * T.inv_scale);
+      } else {  // single word, |sum| < 2^31: one rounding to fp32 (I2FP, ALU pipe), then an exact power-of-two scale
+        // each thread owns 4 positions of every plane: it reads their counts from the last channel's low bits
+        // and removes count x 0x4B400000 (the raw-bit deposits of poly_add) from every channel
+        const float is = T.inv_scalef;
+        const unsigned mask = T.cnt_mask, kLastOff = 1u + (0x4B400000u << T.J);
+        const int w4 = W >> 2;  // W is a multiple of 4
+        for (int q = tid; q < w4; q += kPolyThreads) {
+          const uint4 c = reinterpret_cast<const uint4*>(Ga)[kLast * w4 + q];
+          const uint4 n = make_uint4(c.x & mask, c.y & mask, c.z & mask, c.w & mask);
+  #pragma unroll
+          for (int d = 0; d < kPolyD; d++) {
+            const unsigned off = d < kLast ? 0x4B400000u : d == kLast ? kLastOff : 0u;  // planes past kLast stay 0
+            const uint4 v = d == kLast ? c : reinterpret_cast<const uint4*>(Ga)[d * w4 + q];
+            reinterpret_cast<float4*>(Gf)[d * w4 + q] =
+                make_float4((float)(int)(v.x - n.x * off) * is, (float)(int)(v.y - n.y * off) * is,
+                            (float)(int)(v.z - n.z * off) * is, (float)(int)(v.w - n.w * off) * is);
           }
         }
-#pragma unroll
-        for (int r = 0; r < 8; r++) part[pass][r] = acc[r].x + acc[r].y;
       }
-      __syncthreads();  // every group is done reading G: its planes take the 4 x kPolyTC partial sums
-      float* red = Gf;
-#pragma unroll
-      for (int pass = 0; pass < kPolyPasses; pass++) {
-        float4* r4 = reinterpret_cast<float4*>(red + gq * kPolyTC + pass * kPolyPass + 8 * lt);
-        r4[0] = make_float4(part[pass][0], part[pass][1], part[pass][2], part[pass][3]);
-        r4[1] = make_float4(part[pass][4], part[pass][5], part[pass][6], part[pass][7]);
+      __syncthreads();
+
+      // ---- 3. 8-channel FIR: h[k] = sum_m sum_d P_d[m] G_d[k - m] --------------------------------
+      // Thread group gq (THREADS/4 threads) applies channel pair gq to 8 consecutive outputs per thread with a
+      // sliding register window (one new position per tap); the 4 groups' partial sums meet in shared memory.
+      // ntaps is padded to a multiple of 8 with zero taps, so in every unrolled group of 8 taps the new
+      // positions q - mi - 1 - u sit at fixed offsets 0 .. -6, -8 of one padded address (q = 7 mod 8).
+      {
+        const int gq = tid / kPolyGroup, lt = tid % kPolyGroup;
+        const float* G0 = Gf + (2 * gq) * W;  // channel 2 gq; channel 2 gq + 1 sits W words further
+        float part[kPolyPasses][8];
+  #pragma unroll
+        for (int pass = 0; pass < kPolyPasses; pass++) {
+          const int t8 = pass * kPolyPass + 8 * lt;
+          const float4* P4 = reinterpret_cast<const float4*>(Pt) + gq * (ntaps >> 1);  // pair gq: taps (2i, 2i+1)
+          float2 acc[8], w[8];
+          const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (m = m_lo)
+  #pragma unroll
+          for (int r = 0; r < 8; r++) {
+            acc[r] = make_float2(0.f, 0.f);
+            const int a = (q + r) + ((q + r) >> 3);
+            w[r] = make_float2(G0[a], G0[a + W]);
+          }
+          const float* gn = G0 + (q - 1) + ((q - 1) >> 3);  // padded address of position q - 1 (= 6 mod 8)
+          for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P4 += 4) {
+            const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};  // taps mi .. mi + 7 of channel pair gq
+  #pragma unroll
+            for (int u = 0; u < 8; u++) {  // tap mi + u: output r uses slot (r - u) & 7, then slot (7 - u) & 7 refills
+              const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
+  #pragma unroll
+              for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 7], acc[r]);
+              const int o = u < 7 ? -u : -8;  // the last group's refills read padding: never used
+              w[(7 - u) & 7] = make_float2(gn[o], gn[o + W]);
+            }
+          }
+  #pragma unroll
+          for (int r = 0; r < 8; r++) part[pass][r] = acc[r].x + acc[r].y;
+        }
+        __syncthreads();  // every group is done reading G: its planes take the 4 x kPolyTC partial sums
+        float* red = Gf;
+  #pragma unroll
+        for (int pass = 0; pass < kPolyPasses; pass++) {
+          float4* r4 = reinterpret_cast<float4*>(red + gq * kPolyTC + pass * kPolyPass + 8 * lt);
+          r4[0] = make_float4(part[pass][0], part[pass][1], part[pass][2], part[pass][3]);
+          r4[1] = make_float4(part[pass][4], part[pass][5], part[pass][6], part[pass][7]);
+        }
       }
-    }
-    __syncthreads();
-    {
-      const float* red = Gf;
-#pragma unroll
-      for (int h = 0; h < kPolyTC / kPolyThreads; h++) {
-        const int t = tid + h * kPolyThreads, k = T.t0 + t;
-        if (k < T.te)
-          A.out[T.row + k] = (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
+      __syncthreads();
+      {
+        const float* red = Gf;
+  #pragma unroll
+        for (int h = 0; h < kPolyTC / kPolyThreads; h++) {
+          const int t = tid + h * kPolyThreads, k = T.t0 + t;
+          if (k < T.te)
+            A.out[T.row + k] = (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
+        }
+        if (T.tail)
+          poly_fused_tail(sm.ti, red, nullptr, tid, kPolyThreads, A.out, A.tail_win, A.tail_seed, 0, kPolyThreads);
       }
-      if (T.tail)
-        poly_fused_tail(sm.ti, red, tid, kPolyThreads, A.out, A.tail_win, A.tail_seed);
     }
     __syncthreads();  // G and the tile record are reused by the next work item
   }
@@ -610,15 +719,29 @@ static size_t poly_smem_bytes(int ntaps, bool two_word) {
 
 size_t ism_poly_smem_bytes(int ntaps, bool two_word) { return poly_smem_bytes<512>(ntaps, two_word); }
 
+// cudaFuncSetAttribute is a driver call per launch otherwise (small calls are latency-bound): set the kernel's
+// dynamic shared-memory limit (and the non-portable cluster size) once per device, to the most any call uses
+template <class F>
+static cudaError_t ensure_attrs(F* kernel, bool cluster) {
+  static unsigned long long done = 0;  // bit per device
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev >= 64) return e;
+  if (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & (1ull << dev)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess && cluster) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) __atomic_fetch_or(&done, 1ull << dev, __ATOMIC_RELEASE);
+  return e;
+}
+
 template <int THREADS, int WFIX>
 static cudaError_t launch_poly_w(const IsmArgs& A, long long n_work, int* counter, size_t smem, int num_sms,
                                  cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(ism_poly_kernel<THREADS, WFIX>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_attrs(ism_poly_kernel<THREADS, WFIX, false>, false);
   if (e != cudaSuccess) return e;
   const long long slots = (long long)PolyCfg<THREADS>::kCtasPerSm * num_sms;
   const int grid = (int)(n_work < slots ? n_work : slots);
-  ism_poly_kernel<THREADS, WFIX><<<grid, THREADS, smem, stream>>>(A, n_work, counter);
+  ism_poly_kernel<THREADS, WFIX, false><<<grid, THREADS, smem, stream>>>(A, n_work, counter);
   return cudaGetLastError();
 }
 template <int THREADS>
@@ -628,21 +751,54 @@ static cudaError_t launch_poly(const IsmArgs& A, long long n_work, int* counter,
                                        : launch_poly_w<THREADS, 0>(A, n_work, counter, smem, num_sms, stream);
 }
 
-// CTA shape: 256-thread CTAs (4 per SM) hide the phases' barriers better on large single-word calls (+7 % on
-// config 3 (i)), but need 4 x their shared memory per SM and leave work items short of threads on small
-// calls; 512-thread CTAs (2 per SM) everywhere else.  Both give bit-identical RIRs (exact integer
-// aggregation, the same per-output FIR arithmetic).
-cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, cudaStream_t stream) {
+template <int WFIX>
+static cudaError_t launch_poly_cluster(const IsmArgs& A, long long n_work, int S, size_t smem, cudaStream_t stream) {
+  cudaError_t e = ensure_attrs(ism_poly_kernel<512, WFIX, true>, true);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_work * S), 1, 1);
+  cfg.blockDim = dim3(512, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ism_poly_kernel<512, WFIX, true>, A, n_work, (int*)nullptr);
+}
+
+// Kernel shape.  Small calls (fewer than 2 work items per SM): thread-block clusters of S = 4..16 CTAs per item
+// (split > 0 forces S), so a lone RIR's few tiles still spread over the GPU.  Large calls: persistent CTAs —
+// 256 threads (4 per SM) hide the phases' barriers better on large single-word calls (+7 % on config 3 (i)) but
+// need 4 x their shared memory per SM; 512 threads (2 per SM) otherwise (split < 0 forces persistent CTAs).
+// Every shape gives bit-identical RIRs (exact integer aggregation, the same per-output FIR arithmetic).
+cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, int split,
+                            cudaStream_t stream) {
+  const bool two_word = A.poly_gbz != 0;  // some tile starts in the two-word format
+  IsmArgs B = A;
+  int S = split > 0 ? split : 0;
+  if (split == 0 && n_work < 2LL * num_sms) {
+    S = 4;
+    while (S < 16 && n_work * S < 2LL * num_sms) S *= 2;
+  }
+  if (S > 0) {  // cluster items: no redo, so the fine plane only for two-word tiles
+    if (S != 4 && S != 8 && S != 16) return cudaErrorInvalidValue;
+    B.poly_gb = two_word;
+    const size_t smem = poly_smem_bytes<512>(A.poly_ntaps, two_word);
+    return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_cluster<kPolyWFix>(B, n_work, S, smem, stream)
+                                         : launch_poly_cluster<0>(B, n_work, S, smem, stream);
+  }
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
-  const bool two_word = A.poly_gbz != 0;  // some tile starts in the two-word format
   const size_t s256 = poly_smem_bytes<256>(A.poly_ntaps, false);
-  IsmArgs B = A;
   if (!two_word && 4 * s256 <= 224 * 1024 && n_work >= 16LL * num_sms) {
     B.poly_gb = 0;
     return launch_poly<256>(B, n_work, counter, s256, num_sms, stream);
   }
-  // 512-thread CTAs carry the fine plane whenever two of them still fit an SM with it (the guard's last rung)
+  // 512-thread CTAs carry the fine plane whenever two of them still fit an SM with it (the guard's redo)
   const size_t s1 = poly_smem_bytes<512>(A.poly_ntaps, false), s2 = poly_smem_bytes<512>(A.poly_ntaps, true);
   B.poly_gb = two_word || 2 * (s2 + 1024) <= 228 * 1024;
   return launch_poly<512>(B, n_work, counter, B.poly_gb ? s2 : s1, num_sms, stream);

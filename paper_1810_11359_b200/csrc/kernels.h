@@ -114,7 +114,8 @@ size_t ism_ws_smem_bytes(int mode, int lut_rows, int lut_cols);
 cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* counter, int num_sms,
                           cudaStream_t stream);
 size_t ism_poly_smem_bytes(int ntaps, bool two_word);
-cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, cudaStream_t stream);
+cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, int split,
+                            cudaStream_t stream);
 cudaError_t launch_tail(const TailArgs& A, long long n_items, cudaStream_t stream);  // one warp per item
 
 cudaError_t launch_traj(const float* sig, long long n_sig, const float* rirs, int n_points, int n_mics, long long L,

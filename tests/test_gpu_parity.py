@@ -120,7 +120,7 @@ def test_cfg1_modes(P, oracle, mode):
 def test_cfg2_t60_sweep(P, oracle, T60, mode):
     """ISM to T60/4 + diffuse tail to T60 (tail RNG is bit-reproducible, so parity covers every sample), in
     every mode (north_star: fp32 and fp16 across all five configs).  The lone RIR's poly call is forced onto
-    the polyphase kernel too (split = -1) besides the default (direct kernels below 32 work items)."""
+    the persistent polyphase kernel too (split = -1) besides the default (cluster items for a lone RIR)."""
     sc = W.cfg2(T60)
     beta, nb = derive(oracle, sc)
     r = run_oracle(oracle, sc, beta, nb)
@@ -285,9 +285,10 @@ def _scene(**kw):
                                                                                       [2.9, 3.9, 2.4]])),  # M_src > 1
     dict(T60=0.05, clamp=True),                      # infeasible T60 clamped -> beta = 0, direct path only
 ])
-@pytest.mark.parametrize("mode,split", [("fp32", 0), ("fp32", -1), ("poly", -1)])
+@pytest.mark.parametrize("mode,split", [("fp32", 0), ("fp32", -1), ("poly", -1), ("poly", 0)])
 def test_edge_cases(P, oracle, kw, mode, split):
-    """Edge cases through the cluster-split (auto) and persistent direct kernels and the polyphase kernel."""
+    """Edge cases through the cluster-split (auto) and persistent direct kernels and the polyphase kernel
+    (persistent and cluster items)."""
     sc = _scene(**kw)
     beta, nb = derive(oracle, sc)
     g = run_gpu(P, sc, beta, nb, mode=mode, split=split)
@@ -794,17 +795,41 @@ def test_poly_matches_direct_kernel(P, oracle):
     assert rel_err(b, a).max() <= 5e-5
 
 
-def test_poly_small_calls_take_direct_kernel(P, oracle):
-    """Fewer than 32 polyphase work items (a lone RIR): the call runs the direct fp32 kernels (bitwise equal
-    to mode fp32); split = -1 still forces the polyphase kernel (different rounding, same tolerance)."""
+def test_poly_small_calls_cluster_kernel(P, oracle):
+    """A lone RIR (config 1: 5 tiles) runs the polyphase kernel with each tile's columns split over a cluster of
+    S CTAs (auto S = 16; forced 4 and 8 through opts.split), whose summed integer planes and per-output FIR
+    reproduce the persistent kernel (split = -1) bit for bit; the oracle at the fp32 tolerance."""
     sc = W.cfg1()
     beta, nb = derive(oracle, sc)
-    a = run_gpu(P, sc, beta, nb, mode="fp32")
-    b = run_gpu(P, sc, beta, nb, mode="poly")
-    assert np.array_equal(a, b)
-    c = run_gpu(P, sc, beta, nb, mode="poly", split=-1)
-    assert not np.array_equal(a, c)
-    assert rel_err(c, run_oracle(oracle, sc, beta, nb))[0] <= TOL["poly"]
+    ref = run_gpu(P, sc, beta, nb, mode="poly", split=-1)
+    for split in (0, 4, 8, 16):
+        assert np.array_equal(run_gpu(P, sc, beta, nb, mode="poly", split=split), ref), split
+    assert not np.array_equal(run_gpu(P, sc, beta, nb, mode="fp32"), ref)
+    assert rel_err(ref, run_oracle(oracle, sc, beta, nb))[0] <= TOL["poly"]
+
+
+@pytest.mark.parametrize("case", ["cfg2_2.0", "cfg4a", "cfg3_16", "two_word_48k"])
+def test_poly_cluster_matches_persistent(P, oracle, case):
+    """Cluster items (small calls) and persistent items give the same bits: a tail-fused lone RIR (config 2,
+    T60 = 2 s), the 48 kHz array (config 4 (a): 192 taps, runtime plane stride), 16 cardioid receivers, and a
+    2 m cube at 48 kHz to 0.8 s whose late tiles take the two-word format (N >= 2^12)."""
+    import torch
+    if case == "two_word_48k":
+        room = np.array([2.0, 2.0, 2.0], np.float32)
+        src = torch.tensor([[0.7, 1.1, 0.9]], device="cuda")
+        rcv = torch.tensor([[1.3, 0.6, 1.45]], device="cuda")
+        T = 0.8
+        nb = oracle.t2n(T, room, 343.0)
+        beta = np.full(6, -0.95, np.float32)
+        a, b = (P.simulate_rir(room, beta, src, rcv, nb, T, T, 48000.0, mode="poly", split=sp, sync=True).cpu().numpy()
+                for sp in (-1, 8))
+        assert np.array_equal(a, b)
+        return
+    sc = {"cfg2_2.0": lambda: W.cfg2(2.0), "cfg4a": lambda: W.cfg4("a"), "cfg3_16": lambda: W.cfg3(16, "diffuse")}[case]()
+    beta, nb = derive(oracle, sc)
+    ref = run_gpu(P, sc, beta, nb, mode="poly", split=-1)
+    for split in (0, 4, 16):
+        assert np.array_equal(run_gpu(P, sc, beta, nb, mode="poly", split=split), ref), split
 
 
 def test_poly_cta_shapes_bit_identical(P, oracle):
