@@ -720,16 +720,19 @@ static size_t poly_smem_bytes(int ntaps, bool two_word) {
 size_t ism_poly_smem_bytes(int ntaps, bool two_word) { return poly_smem_bytes<512>(ntaps, two_word); }
 
 // cudaFuncSetAttribute is a driver call per launch otherwise (small calls are latency-bound): set the kernel's
-// dynamic shared-memory limit (and the non-portable cluster size) once per device, to the most any call uses
-template <class F>
-static cudaError_t ensure_attrs(F* kernel, bool cluster) {
+// dynamic shared-memory limit (and the non-portable cluster size) once per device, to the most any call uses.
+// The cache is per kernel INSTANTIATION (template parameters), not per function type: every variant of
+// ism_poly_kernel has the same signature, and a cache keyed on the type set only the first one launched.
+template <int THREADS, int WFIX, bool CL>
+static cudaError_t ensure_attrs() {
   static unsigned long long done = 0;  // bit per device
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess || dev >= 64) return e;
   if (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & (1ull << dev)) return cudaSuccess;
+  auto* kernel = ism_poly_kernel<THREADS, WFIX, CL>;
   e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (e == cudaSuccess && cluster) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess && CL) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess) __atomic_fetch_or(&done, 1ull << dev, __ATOMIC_RELEASE);
   return e;
 }
@@ -737,7 +740,7 @@ static cudaError_t ensure_attrs(F* kernel, bool cluster) {
 template <int THREADS, int WFIX>
 static cudaError_t launch_poly_w(const IsmArgs& A, long long n_work, int* counter, size_t smem, int num_sms,
                                  cudaStream_t stream) {
-  cudaError_t e = ensure_attrs(ism_poly_kernel<THREADS, WFIX, false>, false);
+  cudaError_t e = ensure_attrs<THREADS, WFIX, false>();
   if (e != cudaSuccess) return e;
   const long long slots = (long long)PolyCfg<THREADS>::kCtasPerSm * num_sms;
   const int grid = (int)(n_work < slots ? n_work : slots);
@@ -753,7 +756,7 @@ static cudaError_t launch_poly(const IsmArgs& A, long long n_work, int* counter,
 
 template <int WFIX>
 static cudaError_t launch_poly_cluster(const IsmArgs& A, long long n_work, int S, size_t smem, cudaStream_t stream) {
-  cudaError_t e = ensure_attrs(ism_poly_kernel<512, WFIX, true>, true);
+  cudaError_t e = ensure_attrs<512, WFIX, true>();
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(n_work * S), 1, 1);
