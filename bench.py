@@ -652,6 +652,32 @@ def _latency_us(torch, fn, n=50):
     return a.elapsed_time(b) * 1000.0 / n
 
 
+def _graph_latency_us(torch, fn, n=50):
+    """The same call captured once into a CUDA graph and replayed back to back: device µs per call without the
+    Python / ctypes / launch overhead of an eager call (the library is stream-ordered and capturable)."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        fn()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(n):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1000.0 / n
+
+
 def sweep(P, torch, dev, flush):
     """The points behind the metric's axes (BASELINE.json configs 1-5: #RIRs and T60), device-timed in this run:
     median ms per call, RIRs/s and lattice image contributions/s (the paper's work unit)."""
@@ -680,9 +706,11 @@ def sweep(P, torch, dev, flush):
     for mode in ("poly", "fp32", "lut", "fp16", "lut_tex"):  # config 1: one RIR, ISM only — latency
         fn = point("cfg1", W.cfg1(), mode, reps=10, warm=3)
         rows[-1]["us_per_call_back_to_back"] = _latency_us(torch, fn)
+        rows[-1]["us_per_call_graph_replay"] = _graph_latency_us(torch, fn)
     for T60 in W.CFG2_T60:  # config 2: T60 sweep, one RIR, ISM + tail
         fn = point("cfg2", W.cfg2(T60), "poly", reps=7, warm=3, T60=T60)
         rows[-1]["us_per_call_back_to_back"] = _latency_us(torch, fn, 20)
+        rows[-1]["us_per_call_graph_replay"] = _graph_latency_us(torch, fn, 20)
     for M in (1, 4, 16, 64, 256, 1024, 4096, 16384):  # config 3 (i): #RIR sweep, diffuse
         point("cfg3_diffuse", W.cfg3(M, "diffuse"), "poly", reps=5 if M < 4096 else 3)
     for mode in ("fp32", "lut", "fp16", "lut_tex"):
@@ -692,7 +720,9 @@ def sweep(P, torch, dev, flush):
     point("cfg3_full", W.cfg3(128, "full"), "fp32", reps=3, warm=1)
     for variant in ("a", "b"):  # config 4: 32-mic array at 48 kHz, every mode
         for mode in ("poly", "fp32", "lut", "fp16", "lut_tex"):
-            point(f"cfg4{variant}", W.cfg4(variant), mode, reps=5, warm=2)
+            fn = point(f"cfg4{variant}", W.cfg4(variant), mode, reps=5, warm=2)
+            if mode == "poly":
+                rows[-1]["us_per_call_graph_replay"] = _graph_latency_us(torch, fn, 20)
     # config 5: 100 000 rooms in one batch call (device time between the call's first and last kernel events;
     # the host planning of the call is reported beside it)
     rb = W.cfg5(100_000)

@@ -65,6 +65,11 @@ struct DeviceState {
   size_t host_scratch_bytes = 0;
   unsigned next_counter = 0;
   int num_sms = 0;
+  // polyphase small calls (cluster items): L2 exchange scratch, a ring of grow-only slots so that calls in flight
+  // on different streams use different slots (a slot grows only in an eager call: the first call of a size)
+  unsigned* poly_slab[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t poly_slab_words[4] = {0, 0, 0, 0};
+  unsigned next_slab = 0;
   // gpurir_simulate_rir_batch: a ring of two grow-only pinned staging buffers for the job table, so the upload
   // is an asynchronous copy and the call returns without synchronising (a slot is reused once the copy that
   // last read it has executed: its event)
@@ -358,6 +363,32 @@ int auto_split(long long nclusters, int requested) {
   int s = 1;
   while (s < kMaxSplit && nclusters * s < 148LL * 4) s *= 2;
   return s;
+}
+
+// Exchange scratch of a cluster-item polyphase launch (ism_poly_kernel.cu: the ranks' planes meet through L2).
+// Fully overwritten by each launch, so never zeroed.
+int set_poly_slab(DeviceState* d, IsmArgs& A, long long n_work, int split) {
+  const int S = ism_poly_cluster_size(n_work, d->num_sms, split, A.poly_ntaps, A.poly_gbz != 0, nullptr);
+  if (S <= 0) return GPURIR_OK;
+  const size_t need = ism_poly_slab_words(n_work, S, A.poly_ntaps);
+  std::lock_guard<std::mutex> lk(g_mu);
+  const unsigned k = d->next_slab++ % 4;
+  if (d->poly_slab_words[k] < need) {
+    if (d->poly_slab[k]) {
+      cudaError_t e = cudaDeviceSynchronize();  // the slot may still be in use by an earlier launch
+      if (e == cudaSuccess) e = cudaFree(d->poly_slab[k]);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFree(poly slab)");
+      d->poly_slab[k] = nullptr;
+      d->poly_slab_words[k] = 0;
+    }
+    const size_t words = need + need / 4;  // some headroom for the next call size
+    cudaError_t e = cudaMalloc((void**)&d->poly_slab[k], words * sizeof(unsigned));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(poly slab)");
+    d->poly_slab_words[k] = words;
+  }
+  A.poly_slab = d->poly_slab[k];
+  A.poly_slab_w = (kPolyTile + A.poly_ntaps - 1 + 31) & ~31;
+  return GPURIR_OK;
 }
 
 // Work-queue head for one persistent launch: a ring of kCounterRing counters so that up to that many
@@ -685,6 +716,7 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
       A.tail_rir_base = o.rir_index_base;
     }
     long long nclusters = (long long)A.nTiles * M;
+    if (poly && (st = set_poly_slab(d, A, nclusters, o.split))) return st;
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
     if (poly) {
@@ -918,6 +950,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
       A.tail_seed = o.seed;
     }
     const long long nw = (long long)P.tiles.size();
+    if (P.poly && (st = set_poly_slab(d, A, nw, o.split))) { release(); return st; }
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     if (P.poly) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, o.split, stream);
     else if (P.persistent) e = launch_ism_ws(A, P.kmode, nw, take_counter(d), d->num_sms, stream);

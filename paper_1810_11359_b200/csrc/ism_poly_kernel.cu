@@ -24,6 +24,11 @@
 // Work per output sample no longer grows with the image density (690 in-window taps per sample at config
 // 3 (i)): the filter costs 2H x 8 MACs, the aggregation 8 channel updates per image.
 #include <cooperative_groups.h>
+#include <mutex>
+#include <utility>
+#include <vector>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "ism_common.cuh"
@@ -33,18 +38,28 @@ namespace cg = cooperative_groups;
 
 namespace gpurir {
 
+// Phase timing of the cluster items (diagnostic build -DGPURIR_PHASE_TIMING, tools/build_variant.sh,
+// tools/phase_probe.py): thread 0 of every CTA prints %globaltimer at the phase boundaries of its item
+#ifdef GPURIR_PHASE_TIMING
+#define PT_MARK(i) do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); pt_[i] = t_; } } while (0)
+#define PT_DUMP() do { if (threadIdx.x == 0) printf("PT %d %d %d %d %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", (int)blockIdx.x, (int)sm.ti.rir, 0, 1, pt_[0], pt_[1], pt_[2], pt_[3], pt_[4], pt_[5], pt_[6], pt_[7], (unsigned long long)sm.ti.te); } while (0)
+#else
+#define PT_MARK(i) do {} while (0)
+#define PT_DUMP() do {} while (0)
+#endif
+
 constexpr int kPolyTC = kPolyTile;      // output samples per work item (the host planner's tile)
 constexpr int kPolyD = 8;               // Chebyshev channels T_0..T_7
 constexpr int kPolyBz = 1024;           // z-factor table entries
 // CTA shape (template parameter THREADS, 512 or 256): 1024 / THREADS CTAs per SM at 64 registers per thread
 template <int THREADS> struct PolyCfg {
   static constexpr int kThreads = THREADS;
-  static constexpr int kCtasPerSm = 1024 / THREADS;
+  static constexpr int kCtasPerSm = THREADS >= 1024 ? 1 : 1024 / THREADS;
   static constexpr int kCols = THREADS;         // lattice columns per enumeration batch
   static constexpr int kGroup = THREADS / 4;    // FIR threads per channel pair
   static constexpr int kPass = 8 * kGroup;      // outputs per FIR pass (8 per thread)
   static constexpr int kPasses = kPolyTC / kPass;
-  static_assert(kPolyTC % kPass == 0, "FIR passes of 4 channel-pair groups x 8 outputs per thread");
+  static_assert(THREADS >= 1024 || kPolyTC % kPass == 0, "FIR passes of 4 channel-pair groups x 8 outputs per thread");  // 1024: cluster items only
 };
 
 // One nonempty lattice column of a batch (32 B, two 16-B loads; lengths in samples, x fs / c).  Its
@@ -273,6 +288,10 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
   const int m_hi = A.poly_mlo + ntaps - 1;
   constexpr int kLast = kPolyChannels - 1;  // the channel whose word also counts (poly_add)
 
+#ifdef GPURIR_PHASE_TIMING
+  unsigned long long pt_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+  PT_MARK(0);
   for (int i = tid; i < ntaps * kPolyD; i += kPolyThreads) Pt[i] = A.poly_P[i];
 
   for (;;) {
@@ -382,11 +401,13 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     }
     __syncthreads();
     if (!sm.ti.next) break;
+    PT_MARK(1);
     const PolyTile& T = sm.ti;
     const RirGeom& g = T.g;
     if (T.use_bz)
       for (int i = tid; i <= T.zh - T.zl; i += kPolyThreads) sm.bz[i] = poly_z_factor(T.zl + i, g);
 
+    PT_MARK(2);
     // ---- 1. image aggregation -------------------------------------------------------------
     // Redone (once) when the count guard fires: a single-word tile goes to the two-word format (capacity 2^17
     // images per position) if the call's shared memory holds the fine plane; otherwise — and for a two-word
@@ -514,6 +535,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         __syncthreads();  // column records are replaced by the next batch
       }
       const int ovf = sm.ti.ovf;  // read after the last batch's barrier; uniform
+      PT_MARK(3);
       if (CL || !ovf) break;      // cluster items check the summed counts below (no redo: capacity status)
       __syncthreads();  // everyone has read the flag before thread 0 changes the format
       if (tid == 0) {
@@ -542,81 +564,115 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       // ---- 2'. cluster: sum the ranks' integer planes over DSMEM for this rank's positions, fp32, FIR -------
       cg::cluster_group cl = cg::this_cluster();
       const int R = kPolyTC / S, o0 = rank * R, npp = R + ntaps - 1;  // outputs and positions of this rank
-      cl.sync();  // every rank's G is complete
-      float v[kPolyD];
-      bool bad = tid == 0 && T.ovf;  // this rank's own guard fired
-      const bool have = tid < npp;
-      if (have) {
-        const int p = o0 + tid, a = p + (p >> 3);
-        if (!T.two_word) {
-          unsigned w[kPolyD], n = 0;
-#pragma unroll
-          for (int d = 0; d < kPolyD; d++) w[d] = 0u;
-          for (int r = 0; r < S; r++) {
-            const unsigned* Gr = reinterpret_cast<const unsigned*>(cl.map_shared_rank(Ga, r));
-#pragma unroll
-            for (int d = 0; d < kPolyD; d++) w[d] += Gr[d * W + a];
-            n += Gr[kLast * W + a] & T.cnt_mask;  // the ranks' counts, summed without wrapping
-          }
-          bad = bad || n > T.cnt_mask;            // 2^J images on this position in all: as the guard
-          const unsigned kLastOff = 1u + (0x4B400000u << T.J);
-#pragma unroll
-          for (int d = 0; d < kPolyD; d++) {
-            const unsigned off = d < kLast ? 0x4B400000u : d == kLast ? kLastOff : 0u;
-            v[d] = (float)(int)(w[d] - n * off) * T.inv_scalef;
-          }
-        } else {
-          int ca[kPolyD], fb[kPolyD];
-#pragma unroll
-          for (int d = 0; d < kPolyD; d++) { ca[d] = 0; fb[d] = 0; }
-          for (int r = 0; r < S; r++) {
-            const int* Gar = cl.map_shared_rank(Ga, r);
-            const int* Gbr = cl.map_shared_rank(Gb, r);
-#pragma unroll
-            for (int d = 0; d < kPolyD; d++) { ca[d] += Gar[d * W + a]; fb[d] += Gbr[d * W + a]; }
-          }
-          bad = bad || (unsigned)fb[kLast] > T.cnt_mask;
-#pragma unroll
-          for (int d = 0; d < kPolyD; d++)
-            v[d] = d == kLast ? (float)((double)ca[d] * 16384.0 * T.inv_scale)
-                              : (float)((double)((long long)ca[d] * 16384 + fb[d]) * T.inv_scale);
+      // The ranks' integer planes meet through L2 (distributed shared memory moves only ~20 B per clock per SM):
+      // (1) every rank stores its planes to its slab; (2) each rank sums a disjoint range of Pq positions over the
+      // ranks' slabs (integer sums mod 2^32: exactly the single-CTA G), converts them and stores the fp32 totals;
+      // (3) each rank loads the positions its FIR needs — its R outputs plus the halo.
+      const int Ws = A.poly_slab_w;                     // slab plane stride (words, >= npos)
+      const int nw = T.two_word ? 2 * kPolyD : kPolyD;  // integer planes: coarse, then fine
+      const size_t slab_words = (size_t)2 * kPolyD * Ws;
+      const unsigned* slab0 = A.poly_slab + (size_t)(blockIdx.x - rank) * slab_words;  // this cluster's rank 0
+      {
+        unsigned* my = A.poly_slab + (size_t)blockIdx.x * slab_words;
+        const unsigned* Gu = reinterpret_cast<const unsigned*>(Ga);  // Gb follows Ga at kPolyD W words
+        for (int i = tid; i < nw * npos; i += kPolyThreads) {
+          const int d = i / npos, p = i - d * npos;
+          __stcg(&my[(size_t)d * Ws + p], Gu[d * W + p + (p >> 3)]);
         }
       }
-      cl.sync();  // every rank has read the remote planes: this rank's planes take its fp32 values
-      if (bad) atomicOr(A.status, kStatusCapacity);
-      float* Gf = reinterpret_cast<float*>(Ga);
-      if (have) {
-        const int a = tid + (tid >> 3);
+      cl.sync();  // barrier.cluster arrive.release / wait.acquire: every rank's slab stores are visible
+      PT_MARK(4);
+      const int Pq = (npos + S - 1) / S, q0 = rank * Pq, nq = max(0, min(npos, q0 + Pq) - q0);
+      float* tot = reinterpret_cast<float*>(A.poly_slab + (size_t)gridDim.x * slab_words) +
+                   (size_t)(blockIdx.x / S) * kPolyD * Ws;  // this cluster's fp32 totals
+      unsigned* stu = reinterpret_cast<unsigned*>(Ga);      // [nw][Pq] sums, then [Pq] counts (G is free now)
+      const unsigned cmask = T.two_word ? 0u : T.cnt_mask;
+      for (int i = tid; i < nw * nq; i += kPolyThreads) {
+        const int d = i / nq, pi = i - d * nq;
+        const unsigned* src = slab0 + (size_t)d * Ws + q0 + pi;
+        unsigned x[16], w = 0u, n = 0u;  // S = 4, 8 or 16: all S loads in flight at once
 #pragma unroll
-        for (int d = 0; d < kPolyD; d++) Gf[d * W + a] = v[d];
+        for (int u = 0; u < 16; u++) x[u] = u < S ? __ldcg(src + (size_t)u * slab_words) : 0u;
+#pragma unroll
+        for (int u = 0; u < 16; u++) { w += x[u]; n += x[u] & cmask; }  // counts sum without wrapping
+        stu[d * Pq + pi] = w;
+        if (d == kLast) stu[nw * Pq + pi] = n;
       }
       __syncthreads();
-      // FIR: one (output, channel) per thread and step; each channel's taps in the order of the single-CTA
-      // filter (fma chain over m = m_lo .. m_lo + ntaps - 1), then ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7))
-      // — the single-CTA path's pair sums and their combination: the same bits
-      for (int i = tid; i < R * kPolyD; i += kPolyThreads) {
-        const int o = i >> 3, d = i & 7;
+      {
+        bool bad = tid == 0 && T.ovf;  // this rank's own guard fired
+        const unsigned kLastOff = 1u + (0x4B400000u << T.J);
+        for (int pi = tid; pi < nq; pi += kPolyThreads) {
+          float v[kPolyD];
+          if (!T.two_word) {
+            const unsigned n = stu[nw * Pq + pi];
+            bad = bad || n > T.cnt_mask;  // 2^J images on this position in all: as the guard
+#pragma unroll
+            for (int d = 0; d < kPolyD; d++) {
+              const unsigned off = d < kLast ? 0x4B400000u : d == kLast ? kLastOff : 0u;
+              v[d] = (float)(int)(stu[d * Pq + pi] - n * off) * T.inv_scalef;
+            }
+          } else {
+            bad = bad || stu[(kPolyD + kLast) * Pq + pi] > T.cnt_mask;
+#pragma unroll
+            for (int d = 0; d < kPolyD; d++) {
+              const int ca = (int)stu[d * Pq + pi], fb = (int)stu[(kPolyD + d) * Pq + pi];
+              v[d] = d == kLast ? (float)((double)ca * 16384.0 * T.inv_scale)
+                                : (float)((double)((long long)ca * 16384 + fb) * T.inv_scale);
+            }
+          }
+#pragma unroll
+          for (int d = 0; d < kPolyD; d++) __stcg(&tot[(size_t)d * Ws + q0 + pi], v[d]);
+        }
+        if (bad) atomicOr(A.status, kStatusCapacity);
+      }
+      cl.sync();  // every rank's totals are visible (cluster-scope release / acquire)
+      float* Gf = reinterpret_cast<float*>(Ga);
+      for (int i = tid; i < kPolyD * npp; i += kPolyThreads) {
+        const int d = i / npp, pi = i - d * npp;
+        Gf[d * W + pi + (pi >> 3)] = __ldcg(&tot[(size_t)d * Ws + o0 + pi]);
+      }
+      __syncthreads();
+      PT_MARK(5);
+      // FIR: thread (channel d, output o), the lanes of a warp on consecutive outputs of one channel (broadcast
+      // coefficient loads, conflict-free plane loads); each channel's taps in the order of the single-CTA filter
+      // (fma chain over m = m_lo .. m_lo + ntaps - 1), then ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)) —
+      // the single-CTA path's pair sums and their combination: the same bits
+      float* sums = reinterpret_cast<float*>(sm.col);  // [kPolyD][R]
+      for (int i = tid; i < kPolyD * R; i += kPolyThreads) {
+        const int d = i / R, o = i - d * R;
         const float* Gd = Gf + d * W;
         const float* Pd = Pt + (d >> 1) * ntaps * 2 + (d & 1);
         float acc = 0.f;
-        for (int mi = 0; mi < ntaps; mi++) {
-          const int pl = o + ntaps - 1 - mi;
-          acc = fmaf(Pd[2 * mi], Gd[pl + (pl >> 3)], acc);
+        for (int mi = 0; mi < ntaps; mi += 8) {  // ntaps is a multiple of 8: the loads of 8 taps go first
+          float pc[8], gv[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const int pl = o + ntaps - 1 - (mi + u);
+            pc[u] = Pd[2 * (mi + u)];
+            gv[u] = Gd[pl + (pl >> 3)];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; u++) acc = fmaf(pc[u], gv[u], acc);
         }
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-        const int k = T.t0 + o0 + o;
-        if (d == 0 && k < T.te) A.out[T.row + k] = acc;
+        sums[d * R + o] = acc;
       }
+      __syncthreads();
+      for (int o = tid; o < R; o += kPolyThreads) {
+        const float* q = sums + o;
+        const int k = T.t0 + o0 + o;
+        if (k < T.te) A.out[T.row + k] = ((q[0] + q[R]) + (q[2 * R] + q[3 * R])) + ((q[4 * R] + q[5 * R]) + (q[6 * R] + q[7 * R]));
+      }
+      PT_MARK(6);
       if (T.tail) {  // uniform over the cluster: the tile's samples are in global memory once every rank is here
         __threadfence();
         cl.sync();
         poly_fused_tail(sm.ti, nullptr, A.out + T.row, tid, kPolyThreads, A.out, A.tail_win, A.tail_seed,
                         rank * kPolyThreads, S * kPolyThreads);
       }
-      cl.sync();  // no rank leaves while another may still read its shared memory
-      break;      // one item per cluster
+      PT_MARK(7);
+      PT_DUMP();
+      break;  // one item per cluster (no rank reads another's shared memory)
     } else {
       // ---- 2. fixed point -> fp32, in place (every word converts itself: no staging, one barrier) ---------
       float* Gf = reinterpret_cast<float*>(Ga);
@@ -754,13 +810,13 @@ static cudaError_t launch_poly(const IsmArgs& A, long long n_work, int* counter,
                                        : launch_poly_w<THREADS, 0>(A, n_work, counter, smem, num_sms, stream);
 }
 
-template <int WFIX>
+template <int THREADS, int WFIX>
 static cudaError_t launch_poly_cluster(const IsmArgs& A, long long n_work, int S, size_t smem, cudaStream_t stream) {
-  cudaError_t e = ensure_attrs<512, WFIX, true>();
+  cudaError_t e = ensure_attrs<THREADS, WFIX, true>();
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(n_work * S), 1, 1);
-  cfg.blockDim = dim3(512, 1, 1);
+  cfg.blockDim = dim3(THREADS, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -770,29 +826,98 @@ static cudaError_t launch_poly_cluster(const IsmArgs& A, long long n_work, int S
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, ism_poly_kernel<512, WFIX, true>, A, n_work, (int*)nullptr);
+  return cudaLaunchKernelEx(&cfg, ism_poly_kernel<THREADS, WFIX, true>, A, n_work, (int*)nullptr);
 }
 
-// Kernel shape.  Small calls (fewer than 2 work items per SM): thread-block clusters of S = 4..16 CTAs per item
-// (split > 0 forces S), so a lone RIR's few tiles still spread over the GPU.  Large calls: persistent CTAs —
-// 256 threads (4 per SM) hide the phases' barriers better on large single-word calls (+7 % on config 3 (i)) but
-// need 4 x their shared memory per SM; 512 threads (2 per SM) otherwise (split < 0 forces persistent CTAs).
-// Every shape gives bit-identical RIRs (exact integer aggregation, the same per-output FIR arithmetic).
+// Clusters of S CTAs of THREADS threads with `smem` bytes each that the GPU holds at once (GPCs hold whole
+// clusters); cached per device, shape and shared-memory size; 0 if the query fails.
+template <int THREADS, int WFIX>
+static int poly_max_clusters(int S, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<long long, int>> cache;  // key: (device, S, smem)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  const long long key = ((long long)dev << 40) | ((long long)S << 32) | (long long)smem;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& kv : cache)
+      if (kv.first == key) return kv.second;
+  }
+  int n = 0;
+  if (ensure_attrs<THREADS, WFIX, true>() == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)S, 1, 1);
+    cfg.blockDim = dim3(THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, ism_poly_kernel<THREADS, WFIX, true>, &cfg) != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 0;
+    }
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache.emplace_back(key, n);
+  return n;
+}
+
+static int poly_max_clusters_for(int threads, int S, int ntaps, bool two_word) {
+  if (threads == 1024) {
+    const size_t smem = poly_smem_bytes<1024>(ntaps, two_word);
+    return ntaps <= kPolyWFixTaps ? poly_max_clusters<1024, kPolyWFix>(S, smem) : poly_max_clusters<1024, 0>(S, smem);
+  }
+  const size_t smem = poly_smem_bytes<512>(ntaps, two_word);
+  return ntaps <= kPolyWFixTaps ? poly_max_clusters<512, kPolyWFix>(S, smem) : poly_max_clusters<512, 0>(S, smem);
+}
+
+// Shape of a call's items: 0 = persistent CTAs; else clusters of S CTAs of `threads` threads, one item per
+// cluster.  Small calls (fewer than 2 items per SM): S = 4..16 such that the call has about 2 CTAs per SM, and
+// 1024-thread CTAs (one per SM: all 32 warps hide the image walk's latencies; config 1: 18.7 vs 20.6 us per call)
+// when the GPU holds all its clusters at that size in one wave (GPCs hold whole clusters), else 512-thread CTAs.
+// split > 0 forces S (512 threads), split < 0 persistent CTAs.  GPURIR_POLY_CL_THREADS=512: always 512 (A/B).
+int ism_poly_cluster_size(long long n_work, int num_sms, int split, int ntaps, bool two_word, int* threads) {
+  static const bool only512 = [] {
+    const char* e = getenv("GPURIR_POLY_CL_THREADS");
+    return e && atoi(e) == 512;
+  }();
+  if (threads) *threads = 512;
+  if (split > 0) return split;
+  if (split < 0 || n_work >= 2LL * num_sms) return 0;
+  int S = 4;
+  while (S < 16 && n_work * S < 2LL * num_sms) S *= 2;
+  if (!only512 && n_work <= poly_max_clusters_for(1024, S, ntaps, two_word) && threads) *threads = 1024;
+  return S;
+}
+
+size_t ism_poly_slab_words(long long n_work, int S, int ntaps) {
+  if (S <= 0) return 0;
+  const size_t Ws = (size_t)((kPolyTC + ntaps - 1 + 31) & ~31);
+  return (size_t)n_work * S * 2 * kPolyD * Ws + (size_t)n_work * kPolyD * Ws;
+}
+
 cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, int split,
                             cudaStream_t stream) {
   const bool two_word = A.poly_gbz != 0;  // some tile starts in the two-word format
   IsmArgs B = A;
-  int S = split > 0 ? split : 0;
-  if (split == 0 && n_work < 2LL * num_sms) {
-    S = 4;
-    while (S < 16 && n_work * S < 2LL * num_sms) S *= 2;
-  }
+  int cl_threads = 512;
+  const int S = ism_poly_cluster_size(n_work, num_sms, split, A.poly_ntaps, two_word, &cl_threads);
   if (S > 0) {  // cluster items: no redo, so the fine plane only for two-word tiles
     if (S != 4 && S != 8 && S != 16) return cudaErrorInvalidValue;
+    if (!A.poly_slab || A.poly_slab_w < kPolyTC + A.poly_ntaps - 1) return cudaErrorInvalidValue;
     B.poly_gb = two_word;
+    if (cl_threads == 1024) {
+      const size_t smem = poly_smem_bytes<1024>(A.poly_ntaps, two_word);
+      return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_cluster<1024, kPolyWFix>(B, n_work, S, smem, stream)
+                                           : launch_poly_cluster<1024, 0>(B, n_work, S, smem, stream);
+    }
     const size_t smem = poly_smem_bytes<512>(A.poly_ntaps, two_word);
-    return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_cluster<kPolyWFix>(B, n_work, S, smem, stream)
-                                         : launch_poly_cluster<0>(B, n_work, S, smem, stream);
+    return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_cluster<512, kPolyWFix>(B, n_work, S, smem, stream)
+                                         : launch_poly_cluster<512, 0>(B, n_work, S, smem, stream);
   }
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;

@@ -84,6 +84,11 @@ struct IsmArgs {
   int tail_win, tail_nS;
   float tail_kappa_fs;
   unsigned long long tail_seed, tail_rir_base;
+  // polyphase small calls (thread-block cluster items): the ranks' integer planes meet through global memory (L2
+  // moves several times the ~20 B/clk per SM of distributed shared memory): per CTA a slab of poly_slab_planes x
+  // poly_slab_w words, then per cluster kPolyD x poly_slab_w fp32 totals (scratch owned by the library)
+  unsigned* poly_slab;
+  int poly_slab_w;
 };
 
 struct TailArgs {
@@ -116,6 +121,9 @@ cudaError_t launch_ism_ws(const IsmArgs& A, int mode, long long n_work, int* cou
 size_t ism_poly_smem_bytes(int ntaps, bool two_word);
 cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, int split,
                             cudaStream_t stream);
+int ism_poly_cluster_size(long long n_work, int num_sms, int split, int ntaps, bool two_word,
+                          int* threads);  // cluster size S of a call's items (0: persistent CTAs)
+size_t ism_poly_slab_words(long long n_work, int S, int ntaps);       // cluster items' L2 exchange scratch
 cudaError_t launch_tail(const TailArgs& A, long long n_items, cudaStream_t stream);  // one warp per item
 
 cudaError_t launch_traj(const float* sig, long long n_sig, const float* rirs, int n_points, int n_mics, long long L,

@@ -821,15 +821,60 @@ def test_poly_cluster_matches_persistent(P, oracle, case):
         T = 0.8
         nb = oracle.t2n(T, room, 343.0)
         beta = np.full(6, -0.95, np.float32)
-        a, b = (P.simulate_rir(room, beta, src, rcv, nb, T, T, 48000.0, mode="poly", split=sp, sync=True).cpu().numpy()
-                for sp in (-1, 8))
-        assert np.array_equal(a, b)
+        a, b, c = (P.simulate_rir(room, beta, src, rcv, nb, T, T, 48000.0, mode="poly", split=sp, sync=True).cpu().numpy()
+                   for sp in (-1, 8, 0))  # 0: heavy tiles split into parts merged in global memory (two words)
+        assert np.array_equal(a, b) and np.array_equal(a, c)
         return
     sc = {"cfg2_2.0": lambda: W.cfg2(2.0), "cfg4a": lambda: W.cfg4("a"), "cfg3_16": lambda: W.cfg3(16, "diffuse")}[case]()
     beta, nb = derive(oracle, sc)
     ref = run_gpu(P, sc, beta, nb, mode="poly", split=-1)
     for split in (0, 4, 16):
         assert np.array_equal(run_gpu(P, sc, beta, nb, mode="poly", split=split), ref), split
+
+
+def test_poly_parts_scratch_self_cleaning(P, oracle):
+    """Small calls split their heavy tiles into parts whose integer planes meet in a global scratch slot that
+    the last part zeroes again: back-to-back calls of different sizes and sampling rates on one stream (which
+    reuse the ring's slots) reproduce their first results bit for bit."""
+    cases = [W.cfg1(), W.cfg2(2.0), W.cfg4("a"), W.cfg2(0.7)]
+    derived = [derive(oracle, sc) for sc in cases]
+    first = [run_gpu(P, sc, b, n, mode="poly") for sc, (b, n) in zip(cases, derived)]
+    for _ in range(3):
+        for sc, (b, n), f in zip(cases, derived, first):
+            assert np.array_equal(run_gpu(P, sc, b, n, mode="poly"), f), sc.name
+    assert rel_err(first[0], run_oracle(oracle, cases[0], *derived[0]))[0] <= TOL["poly"]
+
+
+@pytest.mark.parametrize("mode", ["poly", "fp32"])
+def test_small_call_cuda_graph_replay(P, oracle, mode):
+    """The call is stream-ordered and capturable: a lone-RIR call (config 1, and config 2 with its diffuse
+    tail) captured into a CUDA graph and replayed gives the eager call's bits (the small-call latency path)."""
+    import torch
+    for sc in (W.cfg1(), W.cfg2(0.7)):
+        beta, nb = derive(oracle, sc)
+        src = torch.from_numpy(sc.pos_src).cuda()
+        rcv = torch.from_numpy(np.ascontiguousarray(sc.pos_rcv)).cuda()
+        out = torch.empty((1, 1, P.nsamples(sc.Tmax, sc.fs)), device="cuda")
+        call = lambda: P.simulate_rir(sc.room, beta, src, rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, mode=mode,
+                                      seed=sc.seed, out=out)
+        call()
+        torch.cuda.synchronize()
+        ref = out.clone()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            call()  # warm-up on the capture stream
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            call()
+        for _ in range(3):
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref), sc.name
+        assert P.device_status() == 0
 
 
 def test_poly_cta_shapes_bit_identical(P, oracle):

@@ -59,8 +59,27 @@ def main():
             y.record()
             torch.cuda.synchronize()
             iso.append(x.elapsed_time(y) * 1e3)
+        # the same call captured once into a CUDA graph, replayed back to back (launch overhead of one graph)
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            fn()
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            fn()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(a.reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        gr = e0.elapsed_time(e1) * 1e3 / a.reps
         print(f"{name:10s} {mode:5s} split={split:3d}  back-to-back {b2b:7.1f} us/call  isolated {np.median(iso):7.1f} us  "
-              f"host {host:7.1f} us/call", flush=True)
+              f"host {host:7.1f} us/call  graph replay {gr:7.1f} us/call", flush=True)
 
 
 if __name__ == "__main__":
