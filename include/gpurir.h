@@ -218,8 +218,14 @@ size_t gpurir_workspace_bytes(int n_rooms, const gpurir_room* rooms, double fs, 
  *   out     device float[n_mics][n_sig + rir_len - 1], caller-owned
  * The signal is split into n_points contiguous segments of floor(n_sig / n_points) samples (the last one
  * takes the remainder; reading R7); segment p is filtered by point p's RIRs and the filtered segments
- * are overlap-added: out[m][t] = sum_j signal[j] rirs[p(j)][m][t - j].  Direct fp32 convolution,
- * deterministic.  Errors: EINVAL (n_sig < n_points, sizes <= 0, NULL pointers).
+ * are overlap-added: out[m][t] = sum_j signal[j] rirs[p(j)][m][t - j].  When rir_len is a multiple of 4 and
+ * rirs 16-B aligned, the sum runs on the tensor cores (tcgen05, 3xTF32: fp32 accuracy, ~2^-22 per product): per
+ * segment a banded Toeplitz matrix of the signal times windows of the RIRs, 128 outputs x 256 (block, mic)
+ * columns per tile, K-split partial tiles summed in a fixed order; otherwise a direct fp32 convolution on the
+ * CUDA cores.  Deterministic either way.  opts->split: 0 automatic, -1 forces the CUDA-core kernel, k > 0 the
+ * tensor-core kernel with a K split of k (test hooks).  Device scratch for the K-split partials is owned by the
+ * library (grow-only, allocated by the first call of a size).
+ * Errors: EINVAL (n_sig < n_points, sizes <= 0, NULL pointers).
  */
 int gpurir_simulate_trajectory(const float* signal, long long n_sig, const float* rirs, int n_points, int n_mics,
                                long long rir_len, float* out, const gpurir_opts* opts);

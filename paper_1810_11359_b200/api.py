@@ -243,9 +243,11 @@ def simulate_rir_batch(rooms, fs, out, c=343.0, mode="fp32", Tw=4e-3, lut_Q=16, 
     return out
 
 
-def simulate_trajectory(signal, rirs, out=None, stream=None, sync=False):
+def simulate_trajectory(signal, rirs, out=None, stream=None, sync=False, split=0):
     """gpurir_simulate_trajectory: filter a mono `signal` [n_sig] (CUDA float32) through the per-point RIR
-    banks `rirs` [n_points][n_mics][L] of a source trajectory; returns [n_mics][n_sig + L - 1]."""
+    banks `rirs` [n_points][n_mics][L] of a source trajectory; returns [n_mics][n_sig + L - 1].
+    split: 0 automatic (tensor-core kernel when L % 4 == 0), -1 the CUDA-core kernel, > 0 the tensor-core
+    kernel with that K split (test hooks)."""
     import torch
     signal = signal.reshape(-1)
     if not (isinstance(signal, torch.Tensor) and signal.is_cuda and signal.dtype == torch.float32):
@@ -263,7 +265,7 @@ def simulate_trajectory(signal, rirs, out=None, stream=None, sync=False):
     if rirs.device != signal.device or out.device != signal.device:
         raise ValueError("signal, rirs and out must be on one device")
     with _on_device(signal):
-        o = make_opts(stream=stream, sync=sync)
+        o = make_opts(stream=stream, sync=sync, split=split)
         st = lib().gpurir_simulate_trajectory(signal.data_ptr(), signal.numel(), rirs.data_ptr(), n_points, n_mics,
                                               L, out.data_ptr(), C.byref(o))
     check(st, "gpurir_simulate_trajectory")

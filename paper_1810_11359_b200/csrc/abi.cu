@@ -68,6 +68,10 @@ struct DeviceState {
   // polyphase small calls (cluster items): L2 exchange scratch, a ring of grow-only slots so that calls in flight
   // on different streams use different slots (a slot grows only in an eager call: the first call of a size)
   unsigned* poly_slab[4] = {nullptr, nullptr, nullptr, nullptr};
+  // tensor-core trajectory filter: K-split partial sums, a ring of two grow-only slots
+  float* traj_part[2] = {nullptr, nullptr};
+  size_t traj_part_words[2] = {0, 0};
+  unsigned next_traj = 0;
   size_t poly_slab_words[4] = {0, 0, 0, 0};
   unsigned next_slab = 0;
   // gpurir_simulate_rir_batch: a ring of two grow-only pinned staging buffers for the job table, so the upload
@@ -983,11 +987,39 @@ int gpurir_simulate_trajectory(const float* signal, long long n_sig, const float
   if (!signal || !rirs || !out || n_sig <= 0 || n_points <= 0 || n_mics <= 0 || rir_len <= 0) return GPURIR_EINVAL;
   if (n_sig < n_points || n_mics > 65535 || n_sig + rir_len > (1LL << 40)) return GPURIR_EINVAL;
   cudaStream_t stream = (cudaStream_t)o.stream;
-  cudaError_t e = launch_traj(signal, n_sig, rirs, n_points, n_mics, rir_len, out, stream);
-  if (e != cudaSuccess) return cuda_fail(e, "launch_traj");
   int st = GPURIR_OK;
   DeviceState* d = device_state(&st);
   if (!d) return st;
+  cudaError_t e;
+  // the tcgen05 kernel (traj_tc_kernel.cu) when the RIR bank allows 16-B loads; opts.split = -1 forces the
+  // CUDA-core kernel (traj_kernel.cu), split > 0 the tensor-core kernel's K split (test hooks)
+  const size_t pw = o.split >= 0 && traj_tc_supported(rirs, rir_len)
+                        ? traj_tc_part_words(signal, n_sig, rirs, n_points, n_mics, rir_len, d->num_sms, o.split)
+                        : 0;
+  if (pw > 0) {
+    float* part = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      const unsigned k = d->next_traj++ % 2;
+      if (d->traj_part_words[k] < pw) {
+        if (d->traj_part[k]) {
+          e = cudaDeviceSynchronize();  // the slot may still be in use by an earlier call
+          if (e == cudaSuccess) e = cudaFree(d->traj_part[k]);
+          if (e != cudaSuccess) return cuda_fail(e, "cudaFree(traj partials)");
+          d->traj_part[k] = nullptr;
+          d->traj_part_words[k] = 0;
+        }
+        e = cudaMalloc((void**)&d->traj_part[k], pw * sizeof(float));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(traj partials)");
+        d->traj_part_words[k] = pw;
+      }
+      part = d->traj_part[k];
+    }
+    e = launch_traj_tc(signal, n_sig, rirs, n_points, n_mics, rir_len, out, part, d->num_sms, o.split, stream);
+  } else {
+    e = launch_traj(signal, n_sig, rirs, n_points, n_mics, rir_len, out, stream);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "launch_traj");
   return finish(o, stream, d);
 }
 

@@ -128,6 +128,12 @@ cudaError_t launch_tail(const TailArgs& A, long long n_items, cudaStream_t strea
 
 cudaError_t launch_traj(const float* sig, long long n_sig, const float* rirs, int n_points, int n_mics, long long L,
                         float* out, cudaStream_t stream);
+// tensor-core trajectory filter (traj_tc_kernel.cu): RIR length a multiple of 4 and a 16-B aligned RIR bank
+bool traj_tc_supported(const float* rirs, long long L);
+size_t traj_tc_part_words(const float* sig, long long n_sig, const float* rirs, int n_points, int n_mics, long long L,
+                          int num_sms, int force);  // K-split partial scratch (0: the tensor-core kernel cannot run)
+cudaError_t launch_traj_tc(const float* sig, long long n_sig, const float* rirs, int n_points, int n_mics, long long L,
+                           float* out, float* partial, int num_sms, int force, cudaStream_t stream);
 
 constexpr int kTailThreads = 256;
 constexpr int kTailChunk = kTailThreads * 64;  // samples per tail CTA (up to 16 Philox blocks per thread)

@@ -1,0 +1,133 @@
+// tc_common.cuh — the sm_100a tensor-core primitives of the trajectory filter (traj_tc_kernel.cu): tcgen05.mma
+// (kind::tf32, cta_group::1) with operands in shared memory and the accumulator in tensor memory (TMEM),
+// mbarrier hand-offs, TMEM allocation and 32x32b loads.  Raw PTX, no CUTLASS.
+//
+// Operand layout (both operands K-major, no swizzle, the canonical "interleave" layout of the UMMA smem
+// descriptor): a [rows x 32] fp32 tile is stored as core matrices of 8 rows x 16 B (4 elements along K);
+// element (row, kk) sits at byte (row / 8) * 1024 + (kk / 4) * 128 + (row % 8) * 16 + (kk % 4) * 4, i.e. the
+// leading-dimension byte offset (between the K-adjacent core matrices) is 128 B and the stride byte offset
+// (between 8-row groups) 1024 B.  One MMA consumes K = 8 tf32 (32 B = two core matrices): the k-th step of a
+// 32-wide tile starts 256 B further.
+#pragma once
+
+#include <cstdint>
+
+namespace gpurir {
+namespace tc {
+
+constexpr uint32_t kLBO = 128, kSBO = 1024;
+
+__host__ __device__ constexpr int canon_off(int row, int kk) {
+  return (row >> 3) * (int)kSBO + (kk >> 2) * (int)kLBO + (row & 7) * 16 + (kk & 3) * 4;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// UMMA shared-memory descriptor: start >> 4 in bits [0,14), LBO >> 4 in [16,30), SBO >> 4 in [32,46),
+// version 1 (Blackwell) in [46,48), base offset 0, layout SWIZZLE_NONE (0) in [61,64)
+__device__ __forceinline__ uint64_t smem_desc(const void* p) {
+  return (uint64_t)((smem_u32(p) >> 4) & 0x3FFFu) | ((uint64_t)(kLBO >> 4) << 16) | ((uint64_t)(kSBO >> 4) << 32) |
+         (1ull << 46);
+}
+
+// The same for the SWIZZLE_128B K-major layout (rows of 128 B in 8-row atoms of 1024 B, 16-B chunk j of row r
+// stored at chunk j ^ (r % 8); SBO = 1024 B between atoms, LBO unused (1)); the k-th K step of 8 tf32 starts
+// 32 k bytes further (descriptor + 2 k: the start address is in 16-B units)
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+  return (uint64_t)((smem_u32(p) >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+// Instruction descriptor of kind::tf32: D fp32 (bits [4,6) = 1), A and B tf32 ([7,10) = [10,13) = 2), both
+// K-major (bits 15, 16 = 0), N >> 3 in [17,23), M >> 4 in [24,29)
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// D[tmem] (+)= A[smem] B[smem]; accumulate = false overwrites D
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, bool accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"((uint32_t)accumulate));
+}
+
+// The mbarrier receives one arrival when every tcgen05.mma this thread issued before has completed (and their
+// shared-memory operands may be overwritten).  Implies tcgen05.fence::before_thread_sync.
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// one arrival that also announces `bytes` of asynchronous (TMA) transfers completing on this barrier
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+// TMA: a 2-D box of the tensor map at coordinates (x, y) (elements; out-of-range parts are zero-filled) into
+// shared memory, completing `bytes` on the mbarrier
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// byte offset of element (row, kk) of a [rows x 32] fp32 tile in the SWIZZLE_128B K-major layout
+__host__ __device__ constexpr int sw128_off(int row, int kk) {
+  return (row >> 3) * 1024 + (row & 7) * 128 + ((((kk >> 2) ^ row) & 7) << 4) + (kk & 3) * 4;
+}
+
+// generic-proxy shared-memory writes become visible to the tensor cores (async proxy)
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// one full warp: allocate ncols (power of two >= 32) TMEM columns, base address written to *dst (shared)
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// warp q (q = warp % 4) reads TMEM lanes 32 q .. 32 q + 31 (lane = row of D), 16 consecutive columns from taddr;
+// the load and its wait are one asm block, so no use of the registers can be scheduled before the data lands
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int j = 0; j < 16; j++) v[j] = __uint_as_float(r[j]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+}  // namespace tc
+}  // namespace gpurir
