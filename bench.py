@@ -758,8 +758,12 @@ def sweep(P, torch, dev, flush):
     rirs = torch.randn((n_pts, n_mics, L), device=dev, generator=g) * 1e-2
     outt = torch.empty((n_mics, n_sig + L - 1), device=dev)
     ms = _time_calls(torch, lambda: P.simulate_trajectory(sig, rirs, out=outt), flush, reps=5, warm=2)
-    rows.append(dict(cfg="traj_f1", n_sig=n_sig, points=n_pts, mics=n_mics, L=L, ms=ms,
-                     macs_per_s=n_sig * L * n_mics / ms * 1e3))
+    ms_fma = _time_calls(torch, lambda: P.simulate_trajectory(sig, rirs, out=outt, split=-1), flush, reps=5, warm=2)
+    pk, pk_kind = peaks()
+    rows.append(dict(cfg="traj_f1", kernel="traj_tc_kernel (tcgen05)", n_sig=n_sig, points=n_pts, mics=n_mics, L=L,
+                     ms=ms, macs_per_s=n_sig * L * n_mics / ms * 1e3,
+                     roofline=traj_roofline(n_sig, n_pts, n_mics, L, ms, pk, pk_kind),
+                     cuda_core_kernel_ms=ms_fma))
     return {"rows": rows, "seconds": time.time() - t0, "cfg5_room_list_build_s": build_s,
             "timing": "median device ms per call (CUDA events, inputs resident, 256 MB L2 flush between calls); "
                       "us_per_call_back_to_back = device time of 20-50 back-to-back calls / n"}
@@ -785,6 +789,57 @@ def direct_ab(P, torch, sc, beta, nb, src, rcv, orv, base, out, flush, stream, t
     ach = taps_launch * ISSUE_SLOTS_PER_TAP / (ism_ms / 1000.0)
     return {"value": M_PER_GPU / (ms / 1000.0), "unit": "RIRs/s", "ms_per_step": ms, "ism_ms": ism_ms,
             "roofline_frac": ach / issue_peak, "kernel": "ism_ws_kernel<0>", "steps": steps}
+
+
+def traj_tc_chunks(n_sig, n_points, n_mics, L):
+    """K chunks (128 outputs x 256 columns x 32) the tensor-core trajectory kernel issues per launch: the same integer
+    walk as tc_tile_chunks in csrc/traj_tc_kernel.cu (segments padded to U = 4 ceil((e - j0) / 4) + 1 from the
+    32-aligned start j0; chunk c of segment p touches a tile's blocks [a_lo, a_hi] when its RIR window overlaps [0, L))."""
+    seglen = n_sig // n_points
+    n_out = n_sig + L - 1
+    nA = -(-n_out // 128)
+    n_cols = nA * n_mics
+    total = 0
+    for tile in range(-(-n_cols // 256)):
+        col0 = tile * 256
+        a_lo, a_hi = col0 // n_mics, min(nA - 1, (col0 + 255) // n_mics)
+        tlo, thi = 128 * a_lo, 128 * (a_hi + 1) - 1
+        for p in range(n_points):
+            jp = p * seglen
+            ep = n_sig if p == n_points - 1 else jp + seglen
+            if ep + L - 2 < tlo or jp > thi:
+                continue
+            j0 = jp - jp % 32
+            U = 4 * ((ep - j0 + 3) // 4) + 1
+            nC = (127 + U + 31) // 32
+            off = -j0 - (U - 1)
+            klo, khi = -(128 * a_hi + off), L - (128 * a_lo + off)
+            lo = klo // 32 if klo > 0 else 0
+            hi = min(nC - 1, (khi - 1) // 32) if khi > 0 else -1
+            total += max(0, hi - lo + 1)
+    return total
+
+
+def traj_roofline(n_sig, n_pts, n_mics, L, ms, pk, pk_kind):
+    """Roofline of the trajectory filter.  Tensor-core kernel (L % 4 == 0): bound "tensor" against the dense tf32
+    peak (the measured bf16 cuBLAS peak x 0.5, the nominal tf32 : bf16 ratio); achieved = tf32 flops the kernel
+    issues (3 products of the 3xTF32 split x 128 x 256 x 32 per chunk); useful = 2 n_sig L n_mics (the fp32 filter).
+    CUDA-core kernel: FP32 FFMA issue (148 SMs x 128 lanes x clock)."""
+    macs = float(n_sig) * L * n_mics
+    if L % 4 == 0:
+        peak = float(pk.get("bf16_tflops", 2250.0)) * 0.5e12
+        issued = traj_tc_chunks(n_sig, n_pts, n_mics, L) * 3 * 128 * 256 * 32 * 2.0
+        return {"bound": "tensor", "achieved": issued / (ms / 1e3) / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+                "frac": issued / (ms / 1e3) / peak, "useful_frac": 2 * macs / (ms / 1e3) / peak, "traffic": None,
+                "kernel": "traj_tc_kernel",
+                "basis": f"{issued:.4g} tf32 flops issued per launch (3xTF32 over the signal's banded Toeplitz chunks), "
+                         f"{2 * macs:.4g} useful; peak = measured bf16 {pk.get('bf16_tflops')} TF/s x 0.5 ({pk_kind})"}
+    f_clk = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+    issue_peak = 148 * 128 * f_clk
+    return {"bound": "alu", "achieved": macs / (ms / 1e3) / 1e12, "peak": issue_peak / 1e12, "unit": "T FFMA/s",
+            "frac": macs / (ms / 1e3) / issue_peak, "traffic": None, "kernel": "traj_kernel",
+            "basis": f"n_sig x L x n_mics = {macs:.4g} MACs per launch (one FFMA each); peak = 148 SM x 128 lanes x "
+                     f"{f_clk / 1e6:.0f} MHz ({pk_kind})"}
 
 
 def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev, lib):
@@ -912,10 +967,7 @@ def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev, lib):
                           f"channels per output sample" if args.mode == "poly" else
                           f"{ISSUE_SLOTS_PER_TAP} issue slots per in-window tap x {taps_launch:.4g} taps per launch")
                 + f" (exact counts on {len(pairs)} sampled pairs)"}
-    roof_tr = {"bound": "alu", "achieved": tr_ach / 1e12, "peak": issue_peak / 1e12, "unit": "T FFMA/s",
-               "frac": tr_ach / issue_peak, "traffic": None, "kernel": "traj_kernel",
-               "basis": f"n_sig x L x n_mics = {macs:.4g} MACs per launch (one FFMA each); peak = 148 SM x 128 "
-                        f"lanes x {f_clk / 1e6:.0f} MHz ({pk_kind})"}
+    roof_tr = traj_roofline(n_sig, n_pts, n_mic, nS, tr_ms, pk, pk_kind)
     line = {
         "metric": TRAJ_METRIC, "value": value, "unit": "trajectories/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
@@ -929,9 +981,10 @@ def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev, lib):
         "ism_kernel": roof_ism,
         "e2e": {"value": e2e_value, "unit": "trajectories/s", "h2d_bytes_per_step": (h_src.numel() + h_rcv.numel() +
                 h_sig.numel()) * 4, "d2h_bytes_per_step": h_out[0].numel() * 4, "steps": e2e_steps},
-        # ISM, tail (fused into the polyphase ISM kernel), trajectory filtering
-        "gpu_launches": (2 if (args.mode == "poly" and round(0.010 * sc.fs) <= 1024)
-                         else 3) * K,
+        # ISM, tail (fused into the polyphase ISM kernel), trajectory filtering (tensor-core kernel + the ordered
+        # sum of its K-share partials)
+        "gpu_launches": ((1 if (args.mode == "poly" and round(0.010 * sc.fs) <= 1024) else 2) +
+                         (2 if nS % 4 == 0 else 1)) * K,
         "clocks": clk.summary(),
         "lib": lib,
     }

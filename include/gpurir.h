@@ -209,6 +209,12 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
  * chunk lists: about 100 B per room); 0 for invalid arguments.  Single-room calls need no workspace. */
 size_t gpurir_workspace_bytes(int n_rooms, const gpurir_room* rooms, double fs, double c, const gpurir_opts* opts);
 
+/* Elements of `out` a gpurir_simulate_rir_batch call with these rooms writes: max over i of
+ * rooms[i].out_offset + ceil(Tmax_i fs) (reading C9, the same count as gpurir_nsamples).  Host only, no device
+ * work; the caller sizes (or checks) its output buffer with it.  -1 for invalid arguments (n_rooms < 0, NULL
+ * rooms with n_rooms > 0, fs <= 0). */
+long long gpurir_batch_extent(int n_rooms, const gpurir_room* rooms, double fs);
+
 /*
  * gpurir_simulate_trajectory — a moving source recorded by a microphone array (§3.4,
  * P:225-227; the trajectory-filtering function of P:276).

@@ -22,7 +22,7 @@ EXPORTS = [
     "gpurir_sabine_t60", "gpurir_beta_sabine", "gpurir_att2t_sabine", "gpurir_t2n", "gpurir_image_params",
     "gpurir_lut_table", "gpurir_device_status", "gpurir_strerror", "gpurir_last_cuda_error", "gpurir_version",
     "gpurir_simulate_trajectory", "gpurir_simulate_rir_dir", "gpurir_beta_sabine_weighted", "gpurir_poly_table",
-    "gpurir_simulate_rir_host", "gpurir_workspace_bytes",
+    "gpurir_simulate_rir_host", "gpurir_workspace_bytes", "gpurir_batch_extent",
 ]
 
 
@@ -77,6 +77,8 @@ def lib() -> C.CDLL:
     L.gpurir_simulate_rir_batch.restype = C.c_int
     L.gpurir_simulate_rir_batch.argtypes = [C.c_int, C.POINTER(Room), C.c_double, C.c_double, vp, C.POINTER(Opts)]
     L.gpurir_workspace_bytes.restype = C.c_size_t
+    L.gpurir_batch_extent.restype = C.c_longlong
+    L.gpurir_batch_extent.argtypes = [C.c_int, C.POINTER(Room), C.c_double]
     L.gpurir_workspace_bytes.argtypes = [C.c_int, C.POINTER(Room), C.c_double, C.c_double, C.POINTER(Opts)]
     L.gpurir_simulate_trajectory.restype = C.c_int
     L.gpurir_simulate_trajectory.argtypes = [vp, C.c_longlong, vp, C.c_int, C.c_int, C.c_longlong, vp, C.POINTER(Opts)]

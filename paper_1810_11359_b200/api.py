@@ -212,8 +212,11 @@ def room_array(rooms) -> C.Array:
 
 
 def _batch_need(arr, fs) -> int:
-    """Elements of `out` the rooms write: max(out_offset + ceil(Tmax fs))."""
-    return max((R.out_offset + nsamples(R.Tmax, fs) for R in arr), default=0)
+    """Elements of `out` the rooms write: max(out_offset + ceil(Tmax fs)) (gpurir_batch_extent, one C call)."""
+    n = int(lib().gpurir_batch_extent(len(arr), arr, float(fs)))
+    if n < 0:
+        raise ValueError("invalid rooms / fs")
+    return n
 
 
 def workspace_bytes(rooms, fs, c=343.0, mode="fp32", Tw=4e-3, lut_Q=16, split=0) -> int:

@@ -863,6 +863,13 @@ int gpurir_simulate_rir_host(const float room_sz[3], const float beta[6], const 
   return finish(fin, cs, d);
 }
 
+long long gpurir_batch_extent(int n_rooms, const gpurir_room* rooms, double fs) {
+  if (n_rooms < 0 || (n_rooms > 0 && !rooms) || !(fs > 0)) return -1;
+  long long need = 0;
+  for (int i = 0; i < n_rooms; i++) need = std::max(need, rooms[i].out_offset + gpurir_nsamples(rooms[i].Tmax, fs));
+  return need;
+}
+
 size_t gpurir_workspace_bytes(int n_rooms, const gpurir_room* rooms, double fs, double c, const gpurir_opts* opts) {
   gpurir_opts o;
   if (opts) o = *opts; else gpurir_opts_default(&o);

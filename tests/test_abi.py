@@ -189,3 +189,16 @@ def test_poly_table_reproduces_eq6(P, oracle, fs):
     assert mlo == int(np.floor(-H)) + 1 and tab.shape[0] % 8 == 0
     with pytest.raises(P.GpurirError):
         P.poly_table(Tw, 300000.0)  # Tw fs > 1022 taps
+
+
+def test_batch_extent_on_host(P):
+    """gpurir_batch_extent (the binding's output-size check of a batch call): max(out_offset + ceil(Tmax fs)),
+    reading C9 / R1, computed on the host without a device; -1 for invalid arguments."""
+    rooms = [dict(room_sz=[3, 4, 2.5], beta=[-0.9] * 6, pos_src=[1, 1, 1], pos_rcv=[2, 2, 1], nb_img=[5, 5, 5],
+                  Tdiff=0.05, Tmax=T, out_offset=off) for T, off in ((0.3, 0), (0.1, 4800), (0.2, 6400), (0.05, 100))]
+    arr = P.room_array(rooms)
+    want = max(r["out_offset"] + P.nsamples(r["Tmax"], 16000.0) for r in rooms)
+    assert want == 9600
+    assert P._lib.lib().gpurir_batch_extent(len(arr), arr, 16000.0) == want
+    assert P._lib.lib().gpurir_batch_extent(0, arr, 16000.0) == 0
+    assert P._lib.lib().gpurir_batch_extent(1, arr, 0.0) == -1
