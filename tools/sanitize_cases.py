@@ -1,7 +1,8 @@
 """Tiny calls of every kernel for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 cluster-split direct kernel (cfg1-like, fp32 / lut / fp16 / lut_tex), persistent warp-specialised kernel
 (split -1), polyphase kernel (split -1, single- and two-word, fused tail, the count guard's redo), tail
-kernel, batch call (polyphase with fused tail; fp32 with tail_kernel), trajectory filter.  Small sizes:
+kernel, batch call (polyphase with fused tail; fp32 with tail_kernel), the polyphase cluster items of small calls,
+trajectory filter (tcgen05 kernel with TMA- and register-fed B, K shares; CUDA-core kernel).  Small sizes:
 racecheck tracks every shared-memory access."""
 import os
 import sys
@@ -52,11 +53,17 @@ def main():
         P.simulate_rir_batch(rooms, rb.fs, out, seed=rb.seed, mode=mode, split=split, sync=True)
         assert torch.isfinite(out).all()
         print(f"ok batch {mode}", flush=True)
+    run(small, "poly")                    # lone RIR: cluster items (1024-thread CTAs, L2 slab exchange), fused tail
+    run(small, "poly", split=8)           # forced cluster of 8 (512-thread CTAs)
+    run(W.cfg4("a"), "poly", M=4)         # 48 kHz cluster items (runtime plane stride)
     sig = torch.randn(777, device="cuda")
-    rirs = torch.randn((3, 2, 300), device="cuda")
-    y = P.simulate_trajectory(sig, rirs, sync=True)
-    assert torch.isfinite(y).all()
-    print("ok trajectory", flush=True)
+    for shape, split in (((3, 2, 301), 0), ((3, 2, 300), 0), ((3, 8, 300), 0), ((3, 8, 300), 3), ((3, 8, 300), -1)):
+        # L % 4 != 0: CUDA-core kernel; 2 mics: tensor cores, B through registers; 8 mics: TMA-fed B; 3 K shares
+        # (the ordered partial sum); -1: the CUDA-core kernel
+        rirs = torch.randn(shape, device="cuda")
+        y = P.simulate_trajectory(sig, rirs, sync=True, split=split)
+        assert torch.isfinite(y).all()
+        print(f"ok trajectory {shape} split={split}", flush=True)
 
 
 if __name__ == "__main__":
