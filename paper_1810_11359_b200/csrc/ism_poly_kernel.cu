@@ -564,10 +564,11 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       // ---- 2'. cluster: sum the ranks' integer planes over DSMEM for this rank's positions, fp32, FIR -------
       cg::cluster_group cl = cg::this_cluster();
       const int R = kPolyTC / S, o0 = rank * R, npp = R + ntaps - 1;  // outputs and positions of this rank
-      // The ranks' integer planes meet through L2 (distributed shared memory moves only ~20 B per clock per SM):
+      // The ranks' integer planes meet through L2 (distributed shared memory moves only ~20 B per clock per SM: a
+      // pull of the ranks' planes, or a push of their words by DSMEM reductions into the owners, measured 2x slower):
       // (1) every rank stores its planes to its slab; (2) each rank sums a disjoint range of Pq positions over the
-      // ranks' slabs (integer sums mod 2^32: exactly the single-CTA G), converts them and stores the fp32 totals;
-      // (3) each rank loads the positions its FIR needs — its R outputs plus the halo.
+      // ranks' slabs (integer sums mod 2^32: exactly the single-CTA G) and converts them to fp32 in its staging area;
+      // (3) each rank gathers the positions its FIR needs — its R outputs plus the halo — from the owners (DSMEM).
       const int Ws = A.poly_slab_w;                     // slab plane stride (words, >= npos)
       const int nw = T.two_word ? 2 * kPolyD : kPolyD;  // integer planes: coarse, then fine
       const size_t slab_words = (size_t)2 * kPolyD * Ws;
@@ -583,9 +584,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       cl.sync();  // barrier.cluster arrive.release / wait.acquire: every rank's slab stores are visible
       PT_MARK(4);
       const int Pq = (npos + S - 1) / S, q0 = rank * Pq, nq = max(0, min(npos, q0 + Pq) - q0);
-      float* tot = reinterpret_cast<float*>(A.poly_slab + (size_t)gridDim.x * slab_words) +
-                   (size_t)(blockIdx.x / S) * kPolyD * Ws;  // this cluster's fp32 totals
       unsigned* stu = reinterpret_cast<unsigned*>(Ga);      // [nw][Pq] sums, then [Pq] counts (G is free now)
+      float* stf = reinterpret_cast<float*>(sm.col);        // [kPolyD][Pq] fp32 totals, read by the other ranks
       const unsigned cmask = T.two_word ? 0u : T.cnt_mask;
       for (int i = tid; i < nw * nq; i += kPolyThreads) {
         const int d = i / nq, pi = i - d * nq;
@@ -622,46 +622,54 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             }
           }
 #pragma unroll
-          for (int d = 0; d < kPolyD; d++) __stcg(&tot[(size_t)d * Ws + q0 + pi], v[d]);
+          for (int d = 0; d < kPolyD; d++) stf[d * Pq + pi] = v[d];
         }
         if (bad) atomicOr(A.status, kStatusCapacity);
       }
-      cl.sync();  // every rank's totals are visible (cluster-scope release / acquire)
+      cl.sync();  // every rank's totals are staged
+      // the positions this rank's FIR needs, [o0, o0 + npp): its own and the halo, from the owners over DSMEM
       float* Gf = reinterpret_cast<float*>(Ga);
       for (int i = tid; i < kPolyD * npp; i += kPolyThreads) {
-        const int d = i / npp, pi = i - d * npp;
-        Gf[d * W + pi + (pi >> 3)] = __ldcg(&tot[(size_t)d * Ws + o0 + pi]);
+        const int d = i / npp, pi = i - d * npp, p = o0 + pi, own = p / Pq;
+        Gf[d * W + pi + (pi >> 3)] = cl.map_shared_rank(stf, own)[d * Pq + (p - own * Pq)];
       }
-      __syncthreads();
+      cl.sync();  // every rank has gathered: the staging areas are free
       PT_MARK(5);
-      // FIR: thread (channel d, output o), the lanes of a warp on consecutive outputs of one channel (broadcast
-      // coefficient loads, conflict-free plane loads); each channel's taps in the order of the single-CTA filter
-      // (fma chain over m = m_lo .. m_lo + ntaps - 1), then ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)) —
-      // the single-CTA path's pair sums and their combination: the same bits
-      float* sums = reinterpret_cast<float*>(sm.col);  // [kPolyD][R]
-      for (int i = tid; i < kPolyD * R; i += kPolyThreads) {
-        const int d = i / R, o = i - d * R;
-        const float* Gd = Gf + d * W;
-        const float* Pd = Pt + (d >> 1) * ntaps * 2 + (d & 1);
-        float acc = 0.f;
-        for (int mi = 0; mi < ntaps; mi += 8) {  // ntaps is a multiple of 8: the loads of 8 taps go first
-          float pc[8], gv[8];
+      // FIR over this rank's R outputs with the persistent path's arithmetic (so the same bits): item (channel pair
+      // gq, 8 consecutive outputs) — a sliding register window, FFMA2 over the taps in order — then per output the
+      // pairs' partials ((p0 + p1) + (p2 + p3)); all positions are local to the rank (o0 is its first output)
+      float* red = reinterpret_cast<float*>(sm.col);  // [4 pairs][R]
+      for (int it = tid; it < 4 * (R >> 3); it += kPolyThreads) {
+        const int gq = it / (R >> 3), t8 = 8 * (it - gq * (R >> 3));
+        const float* G0 = Gf + (2 * gq) * W;  // channel 2 gq; channel 2 gq + 1 sits W words further
+        const float4* P4 = reinterpret_cast<const float4*>(Pt) + gq * (ntaps >> 1);  // pair gq: taps (2i, 2i+1)
+        float2 acc[8], wv[8];
+        const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (q = 7 mod 8)
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+          acc[r] = make_float2(0.f, 0.f);
+          const int a = (q + r) + ((q + r) >> 3);
+          wv[r] = make_float2(G0[a], G0[a + W]);
+        }
+        const float* gn = G0 + (q - 1) + ((q - 1) >> 3);
+        for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P4 += 4) {
+          const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};
 #pragma unroll
           for (int u = 0; u < 8; u++) {
-            const int pl = o + ntaps - 1 - (mi + u);
-            pc[u] = Pd[2 * (mi + u)];
-            gv[u] = Gd[pl + (pl >> 3)];
-          }
+            const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
 #pragma unroll
-          for (int u = 0; u < 8; u++) acc = fmaf(pc[u], gv[u], acc);
+            for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, wv[(r - u) & 7], acc[r]);
+            const int o = u < 7 ? -u : -8;  // the last group's refills read padding: never used
+            wv[(7 - u) & 7] = make_float2(gn[o], gn[o + W]);
+          }
         }
-        sums[d * R + o] = acc;
+#pragma unroll
+        for (int r = 0; r < 8; r++) red[gq * R + t8 + r] = acc[r].x + acc[r].y;
       }
       __syncthreads();
       for (int o = tid; o < R; o += kPolyThreads) {
-        const float* q = sums + o;
         const int k = T.t0 + o0 + o;
-        if (k < T.te) A.out[T.row + k] = ((q[0] + q[R]) + (q[2 * R] + q[3 * R])) + ((q[4 * R] + q[5 * R]) + (q[6 * R] + q[7 * R]));
+        if (k < T.te) A.out[T.row + k] = (red[o] + red[R + o]) + (red[2 * R + o] + red[3 * R + o]);
       }
       PT_MARK(6);
       if (T.tail) {  // uniform over the cluster: the tile's samples are in global memory once every rank is here
@@ -767,7 +775,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
 static int poly_w(int ntaps) { return ntaps <= kPolyWFixTaps ? kPolyWFix : poly_plane_words(ntaps); }
 
 template <int THREADS>
-static size_t poly_smem_bytes(int ntaps, bool two_word) {
+static size_t poly_smem_bytes(int ntaps, bool two_word, bool cluster = false) {
+  (void)cluster;
   const size_t W = (size_t)poly_w(ntaps);
   return sizeof(PolySmem<THREADS>) + (two_word ? 2 : 1) * kPolyD * W * sizeof(int) +
          (size_t)ntaps * kPolyD * sizeof(float);
@@ -868,10 +877,10 @@ static int poly_max_clusters(int S, size_t smem) {
 
 static int poly_max_clusters_for(int threads, int S, int ntaps, bool two_word) {
   if (threads == 1024) {
-    const size_t smem = poly_smem_bytes<1024>(ntaps, two_word);
+    const size_t smem = poly_smem_bytes<1024>(ntaps, two_word, true);
     return ntaps <= kPolyWFixTaps ? poly_max_clusters<1024, kPolyWFix>(S, smem) : poly_max_clusters<1024, 0>(S, smem);
   }
-  const size_t smem = poly_smem_bytes<512>(ntaps, two_word);
+  const size_t smem = poly_smem_bytes<512>(ntaps, two_word, true);
   return ntaps <= kPolyWFixTaps ? poly_max_clusters<512, kPolyWFix>(S, smem) : poly_max_clusters<512, 0>(S, smem);
 }
 
@@ -911,11 +920,11 @@ cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, in
     if (!A.poly_slab || A.poly_slab_w < kPolyTC + A.poly_ntaps - 1) return cudaErrorInvalidValue;
     B.poly_gb = two_word;
     if (cl_threads == 1024) {
-      const size_t smem = poly_smem_bytes<1024>(A.poly_ntaps, two_word);
+      const size_t smem = poly_smem_bytes<1024>(A.poly_ntaps, two_word, true);
       return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_cluster<1024, kPolyWFix>(B, n_work, S, smem, stream)
                                            : launch_poly_cluster<1024, 0>(B, n_work, S, smem, stream);
     }
-    const size_t smem = poly_smem_bytes<512>(A.poly_ntaps, two_word);
+    const size_t smem = poly_smem_bytes<512>(A.poly_ntaps, two_word, true);
     return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_cluster<512, kPolyWFix>(B, n_work, S, smem, stream)
                                          : launch_poly_cluster<512, 0>(B, n_work, S, smem, stream);
   }
