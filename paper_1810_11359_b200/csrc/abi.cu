@@ -374,7 +374,7 @@ int auto_split(long long nclusters, int requested) {
 int set_poly_slab(DeviceState* d, IsmArgs& A, long long n_work, int split) {
   const int S = ism_poly_cluster_size(n_work, d->num_sms, split, A.poly_ntaps, A.poly_gbz != 0, nullptr);
   if (S <= 0) return GPURIR_OK;
-  const size_t need = ism_poly_slab_words(n_work, S, A.poly_ntaps);
+  const size_t need = ism_poly_slab_words(n_work, S, A.poly_ntaps, d->num_sms);
   std::lock_guard<std::mutex> lk(g_mu);
   const unsigned k = d->next_slab++ % 4;
   if (d->poly_slab_words[k] < need) {

@@ -24,6 +24,7 @@
 // Work per output sample no longer grows with the image density (690 in-window taps per sample at config
 // 3 (i)): the filter costs 2H x 8 MACs, the aggregation 8 channel updates per image.
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -103,6 +104,7 @@ struct PolyTile {
   double x_dp;       // direct-path delay (samples)
   float tenv[3];     // fused tail: env0, alpha, rho of the RIR (tail_envelope)
   float invNX;
+  int ot0, ote, npos_i;  // this item's outputs [ot0, ote) and positions (sub-range of the tile; cluster items)
 };
 
 // The diffuse tail of RIR T.rir, by the CTA that just wrote its last ISM tile (output partial sums still in
@@ -303,7 +305,25 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       if (both)
         for (int i = tid - 32; i < n4; i += kPolyThreads - 32) reinterpret_cast<int4*>(Gb)[i] = make_int4(0, 0, 0, 0);
     } else if (tid == 0) {
-      const long long wi = CL ? (long long)(blockIdx.x / S) : atomicAdd(work_counter, 1);
+      long long wi;
+      int sub = 0, nsub = 1;  // this cluster's output sub-range of the item, of nsub
+      if (CL) {
+        const int ci = (int)(blockIdx.x / S);
+        if (A.poly_nitems > 0) {  // the last item i with poly_first[i] <= ci
+          int lo = 0, hi = A.poly_nitems - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((int)A.poly_first[mid] <= ci) lo = mid; else hi = mid - 1;
+          }
+          wi = lo;
+          sub = ci - (int)A.poly_first[lo];
+          nsub = (int)A.poly_first[lo + 1] - (int)A.poly_first[lo];
+        } else {
+          wi = ci;
+        }
+      } else {
+        wi = atomicAdd(work_counter, 1);
+      }
       PolyTile& T = sm.ti;
       T.next = wi < n_work;
       if (wi < n_work) {
@@ -334,6 +354,14 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         const int ntile = (nISM + kPolyTC - 1) / kPolyTC;
         T.te = nISM - (ntile - 1 - tile) * kPolyTC;
         T.t0 = max(0, T.te - kPolyTC);
+        // the item's outputs: sub-range `sub` of nsub equal end-aligned parts (nsub > 1 only for full tiles; the
+        // fixed-point format below stays the whole tile's); positions cover the nominal part + the halo
+        {
+          const int Ls = kPolyTC / nsub;
+          T.ote = T.te - (nsub - 1 - sub) * Ls;
+          T.ot0 = nsub > 1 ? T.ote - Ls : T.t0;
+          T.npos_i = Ls + ntaps - 1;
+        }
         if (A.jobs) {
           const BatchJob& J = A.jobs[m];
           T.tail = A.poly_tail && tile == ntile - 1 && J.nISM < J.nS;
@@ -341,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           T.tail_kappa = J.kappa_fs;
           T.tail_rglob = J.rir_global;
         } else {
-          T.tail = A.poly_tail && tile == ntile - 1;
+          T.tail = A.poly_tail && tile == ntile - 1 && sub == nsub - 1;
           T.tail_nS = A.tail_nS;
           T.tail_kappa = A.tail_kappa_fs;
           T.tail_rglob = A.tail_rir_base + (unsigned long long)m;
@@ -352,7 +380,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         T.offEs = (T.g.s[2] - T.g.r[2]) * A.fs_over_c;
         T.offOs = (-T.g.s[2] - T.g.r[2]) * A.fs_over_c;
         // images with floor(x) in [t0 - m_hi, te - 1 - m_lo] reach samples [t0, te)
-        const double xlo = (double)(T.t0 - m_hi), xhi = (double)(T.te - A.poly_mlo);
+        const double xlo = (double)(T.ot0 - m_hi), xhi = (double)(T.ote - A.poly_mlo);  // this item's shell
         const double dlo = xlo > 0.0 ? xlo * A.c_over_fs : 0.0, dhi = xhi * A.c_over_fs;
         T.dlo2 = dlo * dlo;
         T.dhi2 = dhi * dhi;
@@ -416,7 +444,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     // plane, i.e. 256-thread CTAs, reports the capacity status where a 512-thread call would go on).
     for (;;) {
       const float amp_scale = fs_over_c_4pi;
-      const int pbase = sm.ti.t0 - m_hi;  // p = floor(x) - pbase
+      const int pbase = sm.ti.ot0 - m_hi;  // p = floor(x) - pbase
+      const int npos_i = sm.ti.npos_i;
       const int ncl = CL ? (T.ncols - rank + S - 1) / S : T.ncols;  // this rank's columns: rank, rank + S, ...
       for (int qb = 0; qb < ncl; qb += kPolyCols) {
         int cnt = 0;
@@ -518,7 +547,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             else if (phi >= 1.f) { phi -= 1.f; jfl += 1; }
             phi = fminf(phi, 0.99999994f);  // phi + 1 rounds to 1 for phi > -3e-8
             const int p = jfl - pbase;
-            if (p < 0 || p >= npos) continue;  // reaches no sample of this tile
+            if (p < 0 || p >= npos_i) continue;  // reaches no sample of this item
             const float dzf = (float)dz;  // one XU conversion instead of shared-memory loads (the smem pipe binds)
             const float cth = fmaf(dzf, oz, cr.cdot) * rx;
             float gain = ga + (1.f - ga) * cth;
@@ -563,7 +592,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     if constexpr (CL) {
       // ---- 2'. cluster: sum the ranks' integer planes over DSMEM for this rank's positions, fp32, FIR -------
       cg::cluster_group cl = cg::this_cluster();
-      const int R = kPolyTC / S, o0 = rank * R, npp = R + ntaps - 1;  // outputs and positions of this rank
+      const int npos = T.npos_i;  // this item's positions (its nominal outputs + the halo)
+      const int R = (npos - ntaps + 1) / S, o0 = rank * R, npp = R + ntaps - 1;  // outputs and positions of this rank
       // The ranks' integer planes meet through L2 (distributed shared memory moves only ~20 B per clock per SM: a
       // pull of the ranks' planes, or a push of their words by DSMEM reductions into the owners, measured 2x slower):
       // (1) every rank stores its planes to its slab; (2) each rank sums a disjoint range of Pq positions over the
@@ -668,8 +698,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       }
       __syncthreads();
       for (int o = tid; o < R; o += kPolyThreads) {
-        const int k = T.t0 + o0 + o;
-        if (k < T.te) A.out[T.row + k] = (red[o] + red[R + o]) + (red[2 * R + o] + red[3 * R + o]);
+        const int k = T.ot0 + o0 + o;
+        if (k < T.ote) A.out[T.row + k] = (red[o] + red[R + o]) + (red[2 * R + o] + red[3 * R + o]);
       }
       PT_MARK(6);
       if (T.tail) {  // uniform over the cluster: the tile's samples are in global memory once every rank is here
@@ -820,11 +850,12 @@ static cudaError_t launch_poly(const IsmArgs& A, long long n_work, int* counter,
 }
 
 template <int THREADS, int WFIX>
-static cudaError_t launch_poly_cluster(const IsmArgs& A, long long n_work, int S, size_t smem, cudaStream_t stream) {
+static cudaError_t launch_poly_cluster(const IsmArgs& A, long long n_work, long long n_clusters, int S, size_t smem,
+                                       cudaStream_t stream) {
   cudaError_t e = ensure_attrs<THREADS, WFIX, true>();
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(n_work * S), 1, 1);
+  cfg.gridDim = dim3((unsigned)(n_clusters * S), 1, 1);
   cfg.blockDim = dim3(THREADS, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -899,14 +930,68 @@ int ism_poly_cluster_size(long long n_work, int num_sms, int split, int ntaps, b
   if (split < 0 || n_work >= 2LL * num_sms) return 0;
   int S = 4;
   while (S < 16 && n_work * S < 2LL * num_sms) S *= 2;
+  // items whose output ranges the planner may split (poly_plan_subs) get clusters of 8: sub-ranges add the
+  // clusters; measured best at 8 with 1024-thread CTAs (config 2 at T60 = 2 s: 18.6 vs 20.7 us per call at 16)
+  if (n_work <= kPolyMaxItems) S = 8;
+  static const int force_s = [] {
+    const char* e = getenv("GPURIR_POLY_CL_S");  // A/B of the cluster size of small calls
+    const int x = e ? atoi(e) : 0;
+    return (x == 4 || x == 8 || x == 16) ? x : 0;
+  }();
+  if (force_s) S = force_s;
   if (!only512 && n_work <= poly_max_clusters_for(1024, S, ntaps, two_word) && threads) *threads = 1024;
   return S;
 }
 
-size_t ism_poly_slab_words(long long n_work, int S, int ntaps) {
+// L2 exchange scratch of a cluster-item launch: a slab of 2 kPolyD planes per CTA, for at most max(items x S,
+// 2 x SMs) CTAs (output sub-ranges add clusters only up to one wave)
+size_t ism_poly_slab_words(long long n_work, int S, int ntaps, int num_sms) {
   if (S <= 0) return 0;
   const size_t Ws = (size_t)((kPolyTC + ntaps - 1 + 31) & ~31);
-  return (size_t)n_work * S * 2 * kPolyD * Ws + (size_t)n_work * kPolyD * Ws;
+  const long long ctas = std::max(n_work * S, 2LL * num_sms + S);
+  return (size_t)ctas * 2 * kPolyD * Ws;
+}
+
+// Output sub-ranges of a small single-room call's items (IsmArgs::poly_first): item wi is tile nTiles - 1 - wi / M
+// of RIR wi % M (end-aligned 1024-sample tiles); its images lie in the shell of delays (t0 - H, te + H), about
+// (te + H)^3 - (t0 - H)^3 of them.  Starting from one cluster per item, the full tile with the most images per
+// cluster is split in two (then four) while the GPU holds all clusters in one wave (cmax) — the last tile only while
+// its last part still holds the fused tail's envelope window.  Returns the cluster count.
+static long long poly_plan_subs(IsmArgs& B, long long n_work, long long cmax) {
+  const double H = 0.5 * B.poly_ntaps;
+  std::vector<double> w((size_t)n_work);
+  std::vector<int> ns((size_t)n_work, 1);
+  std::vector<char> full((size_t)n_work), last((size_t)n_work);
+  for (long long wi = 0; wi < n_work; wi++) {
+    const int tile = B.nTiles - 1 - (int)(wi / B.M);
+    const long long te = B.nISM - (long long)(B.nTiles - 1 - tile) * kPolyTC, t0 = std::max(0LL, te - kPolyTC);
+    const double lo = std::max(0.0, (double)t0 - H), hi = (double)te + H;
+    w[(size_t)wi] = hi * hi * hi - lo * lo * lo;
+    full[(size_t)wi] = te - t0 == kPolyTC;
+    last[(size_t)wi] = tile == B.nTiles - 1;
+  }
+  long long total = n_work;
+  for (;;) {
+    long long best = -1;
+    double worst = 0.0;
+    for (long long wi = 0; wi < n_work; wi++) {
+      const int k = ns[(size_t)wi];
+      if (!full[(size_t)wi] || k >= 4) continue;
+      if (last[(size_t)wi] && B.poly_tail && kPolyTC / (2 * k) < B.tail_win) continue;
+      if (w[(size_t)wi] / k > worst) { worst = w[(size_t)wi] / k; best = wi; }
+    }
+    if (best < 0 || total + ns[(size_t)best] > cmax) break;
+    total += ns[(size_t)best];
+    ns[(size_t)best] *= 2;
+  }
+  int first = 0;
+  for (long long wi = 0; wi < n_work; wi++) {
+    B.poly_first[wi] = (unsigned short)first;
+    first += ns[(size_t)wi];
+  }
+  B.poly_first[n_work] = (unsigned short)first;
+  B.poly_nitems = (int)n_work;
+  return total;
 }
 
 cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, int num_sms, int split,
@@ -919,14 +1004,21 @@ cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, in
     if (S != 4 && S != 8 && S != 16) return cudaErrorInvalidValue;
     if (!A.poly_slab || A.poly_slab_w < kPolyTC + A.poly_ntaps - 1) return cudaErrorInvalidValue;
     B.poly_gb = two_word;
+    B.poly_nitems = 0;
+    long long n_clusters = n_work;
+    if (split == 0 && !A.jobs && n_work <= kPolyMaxItems) {  // heavy tiles' output ranges over more clusters
+      const long long cmax = poly_max_clusters_for(cl_threads, S, A.poly_ntaps, two_word);
+      const long long cap = std::min(cmax, (2LL * num_sms + S) / S);  // the exchange scratch is sized for this
+      if (cap > n_work) n_clusters = poly_plan_subs(B, n_work, cap);
+    }
     if (cl_threads == 1024) {
       const size_t smem = poly_smem_bytes<1024>(A.poly_ntaps, two_word, true);
-      return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_cluster<1024, kPolyWFix>(B, n_work, S, smem, stream)
-                                           : launch_poly_cluster<1024, 0>(B, n_work, S, smem, stream);
+      return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_cluster<1024, kPolyWFix>(B, n_work, n_clusters, S, smem, stream)
+                                           : launch_poly_cluster<1024, 0>(B, n_work, n_clusters, S, smem, stream);
     }
     const size_t smem = poly_smem_bytes<512>(A.poly_ntaps, two_word, true);
-    return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_cluster<512, kPolyWFix>(B, n_work, S, smem, stream)
-                                         : launch_poly_cluster<512, 0>(B, n_work, S, smem, stream);
+    return A.poly_ntaps <= kPolyWFixTaps ? launch_poly_cluster<512, kPolyWFix>(B, n_work, n_clusters, S, smem, stream)
+                                         : launch_poly_cluster<512, 0>(B, n_work, n_clusters, S, smem, stream);
   }
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;

@@ -7,6 +7,8 @@
 
 namespace gpurir {
 
+constexpr int kPolyMaxItems = 64;  // polyphase small calls: work items whose output range may be split
+
 // One RIR of a multi-room batch (device copy built by the host planner).
 struct alignas(16) BatchJob {
   float L[3];
@@ -89,6 +91,11 @@ struct IsmArgs {
   // poly_slab_w words, then per cluster kPolyD x poly_slab_w fp32 totals (scratch owned by the library)
   unsigned* poly_slab;
   int poly_slab_w;
+  // polyphase small single-room calls: a heavy tile's OUTPUT range split into 2 or 4 sub-ranges, each a cluster
+  // item of its own (the tile's fixed-point format is kept, so its G and every output are the same bits); item i
+  // (= tile x RIR work item) owns clusters [poly_first[i], poly_first[i + 1]); poly_nitems = 0: one cluster each
+  int poly_nitems;
+  unsigned short poly_first[kPolyMaxItems + 1];
 };
 
 struct TailArgs {
@@ -123,7 +130,7 @@ cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, in
                             cudaStream_t stream);
 int ism_poly_cluster_size(long long n_work, int num_sms, int split, int ntaps, bool two_word,
                           int* threads);  // cluster size S of a call's items (0: persistent CTAs)
-size_t ism_poly_slab_words(long long n_work, int S, int ntaps);       // cluster items' L2 exchange scratch
+size_t ism_poly_slab_words(long long n_work, int S, int ntaps, int num_sms);  // cluster items' L2 exchange scratch
 cudaError_t launch_tail(const TailArgs& A, long long n_items, cudaStream_t stream);  // one warp per item
 
 cudaError_t launch_traj(const float* sig, long long n_sig, const float* rirs, int n_points, int n_mics, long long L,
