@@ -312,7 +312,8 @@ def test_degenerate_and_invalid(P):
     import torch
     room = np.float32([3, 4, 2.5])
     s = torch.tensor([[1.0, 1.0, 1.0]], device="cuda")
-    for mode, split in (("fp32", 0), ("fp32", -1), ("poly", -1)):  # every accumulation kernel flags d_n = 0
+    # every accumulation kernel flags d_n = 0 (the polyphase kernel per lattice column: persistent and cluster items)
+    for mode, split in (("fp32", 0), ("fp32", -1), ("poly", -1), ("poly", 0), ("poly", 8)):
         with pytest.raises(P.GpurirError) as e:
             P.simulate_rir(room, [0.9] * 6, s, s.clone(), [3, 3, 3], 0.02, 0.02, 16000.0, mode=mode, split=split,
                            sync=True)
