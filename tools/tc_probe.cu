@@ -65,7 +65,9 @@ __global__ void probe(const float* A, const float* B, float* D) {
 
 int rate_main();
 int sw_main();
+int pair_main();
 int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'p') return pair_main();
   if (argc > 1 && argv[1][0] == 'r') return rate_main();
   if (argc > 1 && argv[1][0] == 's') return sw_main();
   std::vector<float> A(M * K), B(K * N), D(M * N), R(M * N, 0.f);
@@ -216,5 +218,71 @@ int sw_main() {
     }
   printf("sw128: %d mismatches; tf32(1 + 2^-11 + 2^-20) = %.10f (truncation: 1, round to nearest: 1.0009765625)\n",
          bad, D[0]);
+  return bad != 0;
+}
+
+// ---- CTA pair: cluster of 2, M = 256 (128 rows per CTA), N = 256 (128 columns of B per CTA), K = 32, SW128 ----
+__global__ void __cluster_dims__(2, 1, 1) probe_pair(const float* A, const float* B, float* D) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* sA = reinterpret_cast<float*>(smem);            // this CTA's 128 rows x 32
+  float* sB = sA + 128 * 32;                              // this CTA's 128 columns x 32
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  for (int i = tid; i < 128 * 32; i += blockDim.x) {
+    sA[sw_off(i / 32, i % 32) / 4] = A[(128 * rank + i / 32) * 32 + i % 32];
+    sB[sw_off(i / 32, i % 32) / 4] = B[(i % 32) * 256 + 128 * rank + i / 32];
+  }
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc_pair(&tmem_base, 256);
+  if (tid == 0) mbar_init(&bar, 1);
+  fence_mbar_init();
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  if (rank == 0 && tid == 0) {
+    const uint32_t idesc = idesc_tf32(256, 256);
+    for (int k = 0; k < 4; k++)
+      mma_tf32_pair(tmem, smem_desc_sw128(sA) + 2 * k, smem_desc_sw128(sB) + 2 * k, idesc, k != 0);
+    mma_commit_pair(&bar, 3);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  if (warp < 4)
+    for (int c0 = 0; c0 < 256; c0 += 16) {
+      float v[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0, v);
+      for (int j = 0; j < 16; j++) D[(128 * rank + 32 * warp + (tid & 31)) * 256 + c0 + j] = v[j];
+    }
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) tmem_dealloc_pair(tmem, 256);
+}
+
+int pair_main() {
+  std::vector<float> A(256 * 32), B(32 * 256), D(256 * 256);
+  srand(3);
+  for (auto& x : A) x = (float)(rand() % 17 - 8);
+  for (auto& x : B) x = (float)(rand() % 17 - 8);
+  float *dA, *dB, *dD;
+  cudaMalloc(&dA, A.size() * 4); cudaMalloc(&dB, B.size() * 4); cudaMalloc(&dD, D.size() * 4);
+  cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemset(dD, 0, D.size() * 4);
+  cudaFuncSetAttribute(probe_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  probe_pair<<<2, 128, 64 * 1024>>>(dA, dB, dD);
+  printf("pair kernel: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+  int bad = 0;
+  for (int i = 0; i < 256; i++)
+    for (int n = 0; n < 256; n++) {
+      double s = 0;
+      for (int k = 0; k < 32; k++) s += (double)A[i * 32 + k] * B[k * 256 + n];
+      if (D[i * 256 + n] != (float)s) { if (bad < 5) printf("pair mismatch %d %d: %g vs %g\n", i, n, D[i * 256 + n], s); bad++; }
+    }
+  printf("pair: %d mismatches of %d\n", bad, 256 * 256);
   return bad != 0;
 }
