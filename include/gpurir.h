@@ -17,7 +17,13 @@
  *     precision switches, become the per-call opts->mode).  Per device
  *     the library keeps a status word, a LUT cache and a ring of 256 work-
  *     queue counters, so up to 256 calls may be in flight concurrently on
- *     different streams of one device.
+ *     different streams of one device; the scratch of small polyphase calls
+ *     (4 slots) and of the trajectory filter's partial sums (2 slots) is
+ *     reused in stream order (an event per slot), so more concurrent calls
+ *     than slots wait for the slot on the device, not on the host.  A call
+ *     captured into a CUDA graph takes its slot at capture time; replays of
+ *     one graph are ordered by their stream, concurrent replays of several
+ *     graphs that captured the same slot are not.
  *   - Validation runs on the host before any launch.  Conditions that can
  *     only be seen on the device (a zero orientation vector, an image source
  *     coinciding with a receiver) raise a per-device status word that is

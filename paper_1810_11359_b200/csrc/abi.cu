@@ -65,15 +65,18 @@ struct DeviceState {
   size_t host_scratch_bytes = 0;
   unsigned next_counter = 0;
   int num_sms = 0;
-  // polyphase small calls (cluster items): L2 exchange scratch, a ring of grow-only slots so that calls in flight
-  // on different streams use different slots (a slot grows only in an eager call: the first call of a size)
+  // polyphase small calls (cluster items): L2 exchange scratch, a ring of grow-only slots (a slot grows only in an
+  // eager call: the first call of a size); tensor-core trajectory filter: K-split partial sums, two slots.  A slot
+  // is reused after the launch that used it last (its event, SlotGuard); take and record happen under slot_mu.
   unsigned* poly_slab[4] = {nullptr, nullptr, nullptr, nullptr};
-  // tensor-core trajectory filter: K-split partial sums, a ring of two grow-only slots
+  size_t poly_slab_words[4] = {0, 0, 0, 0};
+  unsigned next_slab = 0;
   float* traj_part[2] = {nullptr, nullptr};
   size_t traj_part_words[2] = {0, 0};
   unsigned next_traj = 0;
-  size_t poly_slab_words[4] = {0, 0, 0, 0};
-  unsigned next_slab = 0;
+  std::mutex slot_mu;
+  cudaEvent_t slab_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t traj_ev[2] = {nullptr, nullptr};
   // gpurir_simulate_rir_batch: a ring of two grow-only pinned staging buffers for the job table, so the upload
   // is an asynchronous copy and the call returns without synchronising (a slot is reused once the copy that
   // last read it has executed: its event)
@@ -369,14 +372,42 @@ int auto_split(long long nclusters, int requested) {
   return s;
 }
 
+// Stream order for a scratch slot shared round-robin by calls on any stream: the call that takes the slot waits
+// (on its stream) for the event its previous user recorded after its launch, and records the slot's event after its
+// own launch (SlotGuard's destructor); the device's slot_mu is held from take to record, so no two calls interleave.
+// A stream being captured into a CUDA graph neither waits nor records (a graph replays its nodes in order).
+struct SlotGuard {
+  std::unique_lock<std::mutex> lk;
+  cudaEvent_t* ev = nullptr;  // the slot's event (created on first use)
+  cudaStream_t stream = nullptr;
+  bool capturing = false;
+  void take(std::mutex& mu, cudaEvent_t* slot_ev, cudaStream_t s) {
+    lk = std::unique_lock<std::mutex>(mu);
+    ev = slot_ev;
+    stream = s;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    capturing = cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+    if (!capturing && *ev) cudaStreamWaitEvent(s, *ev, 0);
+  }
+  ~SlotGuard() {
+    if (!ev || capturing) return;
+    if (!*ev && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess) { *ev = nullptr; return; }
+    cudaEventRecord(*ev, stream);
+  }
+};
+
 // Exchange scratch of a cluster-item polyphase launch (ism_poly_kernel.cu: the ranks' planes meet through L2).
 // Fully overwritten by each launch, so never zeroed.
-int set_poly_slab(DeviceState* d, IsmArgs& A, long long n_work, int split) {
+int set_poly_slab(DeviceState* d, IsmArgs& A, long long n_work, int split, cudaStream_t stream, SlotGuard& guard) {
   const int S = ism_poly_cluster_size(n_work, d->num_sms, split, A.poly_ntaps, A.poly_gbz != 0, nullptr);
   if (S <= 0) return GPURIR_OK;
   const size_t need = ism_poly_slab_words(n_work, S, A.poly_ntaps, d->num_sms);
-  std::lock_guard<std::mutex> lk(g_mu);
-  const unsigned k = d->next_slab++ % 4;
+  unsigned k;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    k = d->next_slab++ % 4;
+  }
+  guard.take(d->slot_mu, &d->slab_ev[k], stream);
   if (d->poly_slab_words[k] < need) {
     if (d->poly_slab[k]) {
       cudaError_t e = cudaDeviceSynchronize();  // the slot may still be in use by an earlier launch
@@ -720,7 +751,8 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
       A.tail_rir_base = o.rir_index_base;
     }
     long long nclusters = (long long)A.nTiles * M;
-    if (poly && (st = set_poly_slab(d, A, nclusters, o.split))) return st;
+    SlotGuard slab_guard;  // records the slab slot's event after the launch below (end of this scope)
+    if (poly && (st = set_poly_slab(d, A, nclusters, o.split, stream, slab_guard))) return st;
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     cudaError_t e;
     if (poly) {
@@ -961,7 +993,8 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
       A.tail_seed = o.seed;
     }
     const long long nw = (long long)P.tiles.size();
-    if (P.poly && (st = set_poly_slab(d, A, nw, o.split))) { release(); return st; }
+    SlotGuard slab_guard;
+    if (P.poly && (st = set_poly_slab(d, A, nw, o.split, stream, slab_guard))) { release(); return st; }
     if (o.ev_ism[0]) cudaEventRecord((cudaEvent_t)o.ev_ism[0], stream);
     if (P.poly) e = launch_ism_poly(A, nw, take_counter(d), d->num_sms, o.split, stream);
     else if (P.persistent) e = launch_ism_ws(A, P.kmode, nw, take_counter(d), d->num_sms, stream);
@@ -1003,11 +1036,16 @@ int gpurir_simulate_trajectory(const float* signal, long long n_sig, const float
   const size_t pw = o.split >= 0 && traj_tc_supported(rirs, rir_len)
                         ? traj_tc_part_words(signal, n_sig, rirs, n_points, n_mics, rir_len, d->num_sms, o.split)
                         : 0;
+  SlotGuard part_guard;  // records the partials slot's event after the launch (end of this function)
   if (pw > 0) {
     float* part = nullptr;
     {
-      std::lock_guard<std::mutex> lk(g_mu);
-      const unsigned k = d->next_traj++ % 2;
+      unsigned k;
+      {
+        std::lock_guard<std::mutex> lk(g_mu);
+        k = d->next_traj++ % 2;
+      }
+      part_guard.take(d->slot_mu, &d->traj_ev[k], stream);
       if (d->traj_part_words[k] < pw) {
         if (d->traj_part[k]) {
           e = cudaDeviceSynchronize();  // the slot may still be in use by an earlier call

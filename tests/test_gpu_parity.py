@@ -893,6 +893,39 @@ def test_small_call_cuda_graph_replay(P, oracle, mode):
         assert P.device_status() == 0
 
 
+def test_concurrent_calls_on_many_streams(P, oracle):
+    """Calls in flight on more streams than the library's scratch slots (4 for small polyphase calls' exchange,
+    2 for the trajectory filter's partials): slot reuse is ordered by events, so every call equals its serial result."""
+    import torch
+    cases = [W.cfg1(), W.cfg2(2.0), W.cfg2(0.7), W.cfg1()]
+    ref = []
+    for sc in cases:
+        b, n = derive(oracle, sc)
+        ref.append(run_gpu(P, sc, b, n, mode="poly"))
+    g = torch.Generator(device="cuda").manual_seed(5)
+    sig = torch.randn(5000, device="cuda", generator=g)
+    rirs = torch.randn((10, 8, 1200), device="cuda", generator=g)
+    tref = P.simulate_trajectory(sig, rirs, sync=True).clone()
+    streams = [torch.cuda.Stream() for _ in range(8)]
+    outs, touts = [], []
+    for rep in range(2):
+        for i, st in enumerate(streams):
+            sc = cases[i % len(cases)]
+            b, n = derive(oracle, sc)
+            with torch.cuda.stream(st):
+                src = torch.from_numpy(sc.pos_src).cuda()
+                rcv = torch.from_numpy(np.ascontiguousarray(sc.pos_rcv)).cuda()
+                outs.append((i % len(cases), P.simulate_rir(sc.room, b, src, rcv, n, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c,
+                                                             mode="poly", seed=sc.seed, stream=st)))
+                touts.append(P.simulate_trajectory(sig, rirs, stream=st))
+    torch.cuda.synchronize()
+    for k, h in outs:
+        assert np.array_equal(h.cpu().numpy().astype(np.float64), ref[k])
+    for y in touts:
+        assert torch.equal(y, tref)
+    assert P.device_status() == 0
+
+
 def test_poly_cta_shapes_bit_identical(P, oracle):
     """A large call (256-thread CTAs) and its 8 shards (512-thread CTAs, too few work items for the small
     shape) give bit-identical RIRs: the aggregation is exact and each output's FIR arithmetic is fixed.  Both
