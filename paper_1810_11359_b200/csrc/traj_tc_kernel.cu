@@ -453,9 +453,12 @@ static void traj_tc_args(TrajTcArgs& P, const float* sig, long long n_sig, const
   P.sig = sig; P.n_sig = n_sig; P.rirs = rirs; P.n_points = n_points; P.n_mics = n_mics; P.L = L;
   P.n_out = n_sig + L - 1;
   P.seglen = n_sig / n_points;
-  P.nA = (int)((P.n_out + kTcM - 1) / kTcM);
-  P.n_cols = P.nA * n_mics;
-  P.n_tiles = (P.n_cols + kTcN - 1) / kTcN;
+  // counts in 64 bits first: a call whose tiles do not fit the CTA table (or int) runs the CUDA-core kernel
+  const long long nA = (P.n_out + kTcM - 1) / kTcM, n_cols = nA * n_mics, n_tiles = (n_cols + kTcN - 1) / kTcN;
+  const bool fits = n_tiles <= kTcMaxTiles;
+  P.nA = fits ? (int)nA : 0;
+  P.n_cols = fits ? (int)n_cols : 0;
+  P.n_tiles = fits ? (int)n_tiles : kTcMaxTiles + 1;
 }
 
 // K shares per tile: about one CTA per SM in all, each with ~the same number of chunks (tiles at the ends of the
