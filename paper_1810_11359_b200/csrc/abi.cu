@@ -329,6 +329,16 @@ int validate_room(const float L[3], const float b[6], const int nb[3], int patte
   return GPURIR_OK;
 }
 
+// Reciprocals the polyphase tile setup multiplies by (device divisions are long fp64 sequences on one thread):
+// 1/L[0..2] (m^-1), 1/V_s with V_s the room volume in samples^3, 1/L_min,s (the shortest side in samples)
+void poly_geo_consts(const float L[3], double fs_over_c, double geo[5]) {
+  for (int i = 0; i < 3; i++) geo[i] = 1.0 / (double)L[i];
+  const double Vs = (double)L[0] * (double)L[1] * (double)L[2] * fs_over_c * fs_over_c * fs_over_c;
+  const double Lmin_s = fmin(fmin((double)L[0], (double)L[1]), (double)L[2]) * fs_over_c;
+  geo[3] = 1.0 / Vs;
+  geo[4] = 1.0 / Lmin_s;
+}
+
 void fill_common(IsmArgs& A, double fs, double c, double Tw) {
   A.fs_over_c = fs / c;
   A.c_over_fs = c / fs;
@@ -517,6 +527,7 @@ int plan_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, const
     const double T60 = sabine(R.room_sz, R.beta);
     J.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);  // Eq. 8, reading C14
     J.rir_global = o.rir_index_base + R.rir_index;                        // reading C16: global stream id
+    poly_geo_consts(R.room_sz, fs / c, J.geo);
     P.any_two_word = P.any_two_word || poly_two_word_for(R.room_sz, nISM, fs, c, o.Tw);
     small_tiles += (nISM + kTC - 1) / kTC;
   }
@@ -720,8 +731,11 @@ int gpurir_simulate_rir_dir(const float room_sz[3], const float beta[6], const f
     A.ors = spkr_pattern == GPURIR_OMNI ? nullptr : orV_src;
     A.spkr_pattern = spkr_pattern;
     A.M_src = M_src; A.M_rcv = M_rcv; A.M = (int)M;
+    A.invM = 1.0 / (double)M;
+    A.invMrcv = 1.0 / (double)M_rcv;
     A.nISM = (int)nISM;
     A.row_stride = nS;
+    poly_geo_consts(room_sz, fs / c, A.poly_geo);
     // polyphase mode runs the polyphase kernel at every call size: small calls split each tile's columns over a
     // thread-block cluster (ism_poly_kernel.cu), with the same bits as the persistent kernel
     const bool poly = o.mode == GPURIR_POLY;

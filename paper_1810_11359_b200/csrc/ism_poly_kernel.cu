@@ -48,6 +48,16 @@ namespace gpurir {
 #define PT_MARK(i) do {} while (0)
 #define PT_DUMP() do {} while (0)
 #endif
+// persistent items (the same build): per-phase time summed over the items of CTAs 0..7, printed at their exit
+#ifdef GPURIR_PHASE_TIMING
+#define PTL_MARK(i) do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); ptl_[i] = t_; } } while (0)
+#define PTL_ACC() do { if (threadIdx.x == 0) { for (int i_ = 1; i_ < 7; i_++) pta_[i_] += ptl_[i_] - ptl_[i_ - 1]; pta_[0]++; } } while (0)
+#define PTL_DUMP() do { if (threadIdx.x == 0 && blockIdx.x < 8) printf("PTL %d items %llu setup %llu bz %llu aggr %llu conv %llu fir %llu end %llu\n", (int)blockIdx.x, pta_[0], pta_[1], pta_[2], pta_[3], pta_[4], pta_[5], pta_[6]); } while (0)
+#else
+#define PTL_MARK(i) do {} while (0)
+#define PTL_ACC() do {} while (0)
+#define PTL_DUMP() do {} while (0)
+#endif
 
 constexpr int kPolyTC = kPolyTile;      // output samples per work item (the host planner's tile)
 constexpr int kPolyD = 8;               // Chebyshev channels T_0..T_7
@@ -151,7 +161,24 @@ struct alignas(16) PolySmem {
   float colsdot[THREADS];               // directional source: the column's part of cos(theta_s) (general walk)
   int scan_tmp[THREADS / 32];
   float bz[kPolyBz];
+  // persistent single-room items: the next item's queue index and inputs (src, rcv, rcv orientation, src
+  // orientation), fetched by thread 0 with cp.async while the current item filters
+  long long pf_wi;
+  int pf_valid;
+  float pf_in[12];
 };
+
+// exact q = n / d, r = n % d (0 <= n < 2^53, d >= 1) from a host reciprocal: the fp64 estimate is off by at most one
+__device__ __forceinline__ long long poly_divmod(long long n, long long d, double inv_d, long long& r) {
+  long long q = (long long)((double)n * inv_d);
+  r = n - q * d;
+  if (r < 0) { q--; r += d; } else if (r >= d) { q++; r -= d; }
+  return q;
+}
+__device__ __forceinline__ void poly_cp4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
 
 template <int kPolyThreads>
 __device__ __forceinline__ int poly_block_scan(int v, int* tmp) {
@@ -293,11 +320,15 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
 
 #ifdef GPURIR_PHASE_TIMING
   unsigned long long pt_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long ptl_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pta_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
   PT_MARK(0);
   for (int i = tid; i < ntaps * kPolyD; i += kPolyThreads) Pt[i] = A.poly_P[i];
+  if (tid == 0) sm.pf_valid = 0;  // read by thread 0 only, after the loop top's barrier
+  bool bz_ready = false;          // sm.bz holds this call's z factors (single-room calls)
 
   for (;;) {
+    PTL_MARK(0);
     if (tid >= 32) {  // zero G while thread 0 sets the next work item up (G is free: the loop ends in a barrier)
       // 16-B stores over the 8 W words of each array
       const int n4 = (kPolyD * W) >> 2;
@@ -322,6 +353,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         } else {
           wi = ci;
         }
+      } else if (sm.pf_valid) {  // prefetched during the previous item's filter
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        wi = sm.pf_wi;
       } else {
         wi = atomicAdd(work_counter, 1);
       }
@@ -338,13 +372,19 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           geom_from(J.L, J.src, J.rcv, J.orv, J.nb, J.pattern, J.ors, J.spkr_pattern, J.lb, J.neg, J.zero, T.g,
                     A.status);
         } else {
-          tile = A.nTiles - 1 - (int)(wi / A.M);  // heaviest (latest) tiles first
-          m = (int)(wi % A.M);
+          long long rm;
+          tile = A.nTiles - 1 - (int)poly_divmod(wi, A.M, A.invM, rm);  // heaviest (latest) tiles first
+          m = (int)rm;
           nISM = A.nISM;
           row = (long long)m * A.row_stride;
-          const int ms = m / A.M_rcv, mr = m % A.M_rcv;
-          geom_from(A.L, A.pos_src + 3 * ms, A.pos_rcv + 3 * mr, A.orv ? A.orv + 3 * mr : zero3, A.nb, A.pattern,
-                    A.ors ? A.ors + 3 * ms : zero3, A.spkr_pattern, A.lb, A.neg, A.zero, T.g, A.status);
+          long long mr;
+          const int ms = (int)poly_divmod(m, A.M_rcv, A.invMrcv, mr);
+          if (!CL && sm.pf_valid)  // the inputs were fetched with the index
+            geom_from(A.L, sm.pf_in, sm.pf_in + 3, A.orv ? sm.pf_in + 6 : zero3, A.nb, A.pattern,
+                      A.ors ? sm.pf_in + 9 : zero3, A.spkr_pattern, A.lb, A.neg, A.zero, T.g, A.status);
+          else
+            geom_from(A.L, A.pos_src + 3 * ms, A.pos_rcv + 3 * mr, A.orv ? A.orv + 3 * mr : zero3, A.nb, A.pattern,
+                      A.ors ? A.ors + 3 * ms : zero3, A.spkr_pattern, A.lb, A.neg, A.zero, T.g, A.status);
         }
         T.row = row;
         T.rir = m;
@@ -376,7 +416,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           T.tail_rglob = A.tail_rir_base + (unsigned long long)m;
         }
         T.tc = T.t0 + kPolyTC / 2;
-        T.invLz = 1.0 / T.g.L[2];
+        const double* geo = A.jobs ? A.jobs[m].geo : A.poly_geo;  // 1/L, 1/V_s, 1/L_min,s (host reciprocals)
+        T.invLz = geo[2];
         T.Lzs = T.g.L[2] * A.fs_over_c;
         T.offEs = (T.g.s[2] - T.g.r[2]) * A.fs_over_c;
         T.offOs = (-T.g.s[2] - T.g.r[2]) * A.fs_over_c;
@@ -387,8 +428,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         T.dhi2 = dhi * dhi;
         int lo[2], hi[2];
         for (int ax = 0; ax < 2; ax++) {
-          const double L = T.g.L[ax], r = T.g.r[ax];
-          const int a = (int)floor((r - dhi) / L) - 1, b = (int)floor((r + dhi) / L) + 1;
+          const double iL = geo[ax], r = T.g.r[ax];  // the -1 / +1 margins cover the reciprocal's rounding
+          const int a = (int)floor((r - dhi) * iL) - 1, b = (int)floor((r + dhi) * iL) + 1;
           lo[ax] = max(a, T.g.nlo[ax]);
           hi[ax] = min(b, T.g.nhi[ax] - 1);
         }
@@ -415,10 +456,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         T.x_dp = x_dp;
         const double x_lo = fmax(fmax((double)(T.t0 - m_hi), x_dp), 1e-30);
         const double x_hi = (double)(T.te - A.poly_mlo);
-        const double Vs = T.g.L[0] * T.g.L[1] * T.g.L[2] * A.fs_over_c * A.fs_over_c * A.fs_over_c;
-        const double Lmin_s = fmin(fmin(T.g.L[0], T.g.L[1]), T.g.L[2]) * A.fs_over_c;
         int lb;
-        (void)frexp(25.132741228718345 * x_hi * x_hi / Vs + 24.0 * x_hi / Lmin_s + 16.0, &lb);  // N < 2^lb
+        (void)frexp(25.132741228718345 * x_hi * x_hi * geo[3] + 24.0 * x_hi * geo[4] + 16.0, &lb);  // N < 2^lb
         int bits = min(22, 30 - lb);
         const int two_word = bits < 18 || A.poly_force2 || A.poly_hook == 3;
         if (two_word) bits = 28;
@@ -429,14 +468,18 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       }
     }
     __syncthreads();
-    if (!sm.ti.next) break;
+    if (!sm.ti.next) { PTL_DUMP(); break; }
     PT_MARK(1);
+    PTL_MARK(1);
     const PolyTile& T = sm.ti;
     const RirGeom& g = T.g;
-    if (T.use_bz)
+    // the z factors depend only on the room: once per CTA for a single-room call, per item for a batch of rooms
+    if (T.use_bz && (A.jobs || !bz_ready))
       for (int i = tid; i <= T.zh - T.zl; i += kPolyThreads) sm.bz[i] = poly_z_factor(T.zl + i, g);
+    bz_ready = true;
 
     PT_MARK(2);
+    PTL_MARK(2);
     // ---- 1. image aggregation -------------------------------------------------------------
     // Redone (once) when the count guard fires: a single-word tile goes to the two-word format (capacity 2^17
     // images per position) if the call's shared memory holds the fine plane; otherwise — and for a two-word
@@ -580,6 +623,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       }
       const int ovf = sm.ti.ovf;  // read after the last batch's barrier; uniform
       PT_MARK(3);
+      PTL_MARK(3);
       if (CL || !ovf) break;      // cluster items check the summed counts below (no redo: capacity status)
       __syncthreads();  // everyone has read the flag before thread 0 changes the format
       if (tid == 0) {
@@ -729,6 +773,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     } else {
       // ---- 2. fixed point -> fp32, in place (every word converts itself: no staging, one barrier) ---------
       float* Gf = reinterpret_cast<float*>(Ga);
+      long long wi_next = 0;
+      if (tid == 0) wi_next = atomicAdd(work_counter, 1);  // the next item's index; its latency hides under the work
       if (T.two_word) {
         for (int i = tid; i < kPolyD * W; i += kPolyThreads)
           Gf[i] = (i >= kLast * W && i < (kLast + 1) * W) ? (float)((double)Ga[i] * 16384.0 * T.inv_scale)
@@ -753,6 +799,23 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         }
       }
       __syncthreads();
+      PTL_MARK(4);
+      if (tid == 0) {  // the next item's inputs, asynchronously into shared memory (single-room calls)
+        sm.pf_wi = wi_next;
+        sm.pf_valid = 1;
+        if (!A.jobs && wi_next < n_work) {
+          long long rm, mr;
+          (void)poly_divmod(wi_next, A.M, A.invM, rm);
+          const int ms = (int)poly_divmod(rm, A.M_rcv, A.invMrcv, mr);
+          for (int k = 0; k < 3; k++) {
+            poly_cp4(&sm.pf_in[k], A.pos_src + 3 * ms + k);
+            poly_cp4(&sm.pf_in[3 + k], A.pos_rcv + 3 * mr + k);
+            if (A.orv) poly_cp4(&sm.pf_in[6 + k], A.orv + 3 * mr + k);
+            if (A.ors) poly_cp4(&sm.pf_in[9 + k], A.ors + 3 * ms + k);
+          }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      }
 
       // ---- 3. 8-channel FIR: h[k] = sum_m sum_d P_d[m] G_d[k - m] --------------------------------
       // Thread group gq (THREADS/4 threads) applies channel pair gq to 8 consecutive outputs per thread with a
@@ -812,7 +875,10 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           poly_fused_tail(sm.ti, red, nullptr, tid, kPolyThreads, A.out, A.tail_win, A.tail_seed, 0, kPolyThreads);
       }
     }
+    PTL_MARK(5);
     __syncthreads();  // G and the tile record are reused by the next work item
+    PTL_MARK(6);
+    PTL_ACC();
   }
   (void)lane; (void)warp;
 }

@@ -27,6 +27,8 @@ struct alignas(16) BatchJob {
   unsigned neg, zero;   // bit w: beta_w < 0 / beta_w == 0
   float ors[3];         // source orientation (f3, reading R10; ignored for an omni source)
   int spkr_pattern;     // source polar pattern (gpurir_pattern)
+  double geo[5];        // host-computed reciprocals for the polyphase tile setup: 1/L[0..2] (m^-1), 1/V_s (samples^-3),
+                        // 1/L_min,s (samples^-1) — see IsmArgs::poly_geo
 };
 
 struct IsmArgs {
@@ -51,6 +53,10 @@ struct IsmArgs {
   const int2* tiles;     // per cluster: (job, tile)
   // common
   double fs_over_c, c_over_fs;
+  // polyphase tile setup without divisions (single-room calls; batch jobs carry their own BatchJob::geo):
+  // 1/L[0..2], 1/V_s, 1/L_min,s as in BatchJob::geo, and 1/M, 1/M_rcv for the work-item decode (exact, fix-up)
+  double poly_geo[5];
+  double invM, invMrcv;
   float H, invH;         // half window (samples) and 1/H
   int nbw;               // delay bins touching one warp sub-tile
   // exact power-of-two scaling of the tap argument: Hs = 2^ceil(log2 H),
