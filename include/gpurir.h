@@ -23,7 +23,10 @@
  *     than slots wait for the slot on the device, not on the host.  A call
  *     captured into a CUDA graph takes its slot at capture time; replays of
  *     one graph are ordered by their stream, concurrent replays of several
- *     graphs that captured the same slot are not.
+ *     graphs that captured the same slot are not.  Scratch grows only in an
+ *     eager call (growing synchronises the device), so make one eager call of
+ *     a size before capturing it — every call is otherwise capturable (no
+ *     host synchronisation, allocation or pageable copy on the call path).
  *   - Validation runs on the host before any launch.  Conditions that can
  *     only be seen on the device (a zero orientation vector, an image source
  *     coinciding with a receiver) raise a per-device status word that is
