@@ -25,8 +25,9 @@
  *     one graph are ordered by their stream, concurrent replays of several
  *     graphs that captured the same slot are not.  Scratch grows only in an
  *     eager call (growing synchronises the device), so make one eager call of
- *     a size before capturing it — every call is otherwise capturable (no
- *     host synchronisation, allocation or pageable copy on the call path).
+ *     a size before capturing it; after that, gpurir_simulate_rir(_dir) and
+ *     gpurir_simulate_trajectory are capturable (no host synchronisation,
+ *     allocation or pageable copy on their path; tested for configs 1 and 2).
  *   - Validation runs on the host before any launch.  Conditions that can
  *     only be seen on the device (a zero orientation vector, an image source
  *     coinciding with a receiver) raise a per-device status word that is
