@@ -893,6 +893,35 @@ def test_small_call_cuda_graph_replay(P, oracle, mode):
         assert P.device_status() == 0
 
 
+def test_trajectory_cuda_graph_replay(P):
+    """The trajectory filter (tensor-core kernel with K shares and the ordered partial sum; CUDA-core kernel) is
+    capturable after one eager call of its size: graph replays give the eager bits."""
+    import torch
+    g0 = torch.Generator(device="cuda").manual_seed(7)
+    sig = torch.randn(6000, device="cuda", generator=g0)
+    for shape, split in (((12, 32, 2000), 0), ((12, 32, 2001), 0), ((12, 32, 2000), -1)):
+        rirs = torch.randn(shape, device="cuda", generator=g0)
+        out = torch.empty((shape[1], 6000 + shape[2] - 1), device="cuda")
+        call = lambda: P.simulate_trajectory(sig, rirs, out=out, split=split)
+        call()
+        torch.cuda.synchronize()
+        ref = out.clone()
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            call()
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            call()
+        for _ in range(2):
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref), (shape, split)
+
+
 def test_concurrent_calls_on_many_streams(P, oracle):
     """Calls in flight on more streams than the library's scratch slots (4 for small polyphase calls' exchange,
     2 for the trajectory filter's partials): slot reuse is ordered by events, so every call equals its serial result."""
