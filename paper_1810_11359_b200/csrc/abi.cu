@@ -406,6 +406,42 @@ struct SlotGuard {
   }
 };
 
+// Grows every slot of a round-robin scratch ring to at least `need` elements (with headroom for the next call
+// size) when the one about to be taken is short, so that after one eager call of a size every later call of that
+// size — whichever slot it draws, on whichever stream, captured or not — allocates nothing.  Slots may still be in
+// use by earlier launches on other streams: the device is synchronised before any is freed.  A stream being
+// captured cannot allocate or synchronise: the call fails with GPURIR_ECUDA and a message instead of invalidating
+// the capture (gpurir.h: capture after one eager call of the same size).
+template <class T>
+int grow_ring(T** slot, size_t* words, int n, size_t need, bool capturing, const char* what) {
+  bool short_any = false, held = false;
+  for (int i = 0; i < n; i++) { short_any |= words[i] < need; held |= slot[i] != nullptr; }
+  if (!short_any) return GPURIR_OK;
+  if (capturing) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: scratch must grow during stream capture; make one eager call "
+             "of this size first", what);
+    return GPURIR_ECUDA;
+  }
+  if (held) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, what);
+  }
+  const size_t w = need + need / 4;
+  for (int i = 0; i < n; i++) {
+    if (words[i] >= need) continue;
+    if (slot[i]) {
+      cudaError_t e = cudaFree(slot[i]);
+      if (e != cudaSuccess) return cuda_fail(e, what);
+      slot[i] = nullptr;
+      words[i] = 0;
+    }
+    cudaError_t e = cudaMalloc((void**)&slot[i], w * sizeof(T));
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    words[i] = w;
+  }
+  return GPURIR_OK;
+}
+
 // Exchange scratch of a cluster-item polyphase launch (ism_poly_kernel.cu: the ranks' planes meet through L2).
 // Fully overwritten by each launch, so never zeroed.
 int set_poly_slab(DeviceState* d, IsmArgs& A, long long n_work, int split, cudaStream_t stream, SlotGuard& guard) {
@@ -418,19 +454,7 @@ int set_poly_slab(DeviceState* d, IsmArgs& A, long long n_work, int split, cudaS
     k = d->next_slab++ % 4;
   }
   guard.take(d->slot_mu, &d->slab_ev[k], stream);
-  if (d->poly_slab_words[k] < need) {
-    if (d->poly_slab[k]) {
-      cudaError_t e = cudaDeviceSynchronize();  // the slot may still be in use by an earlier launch
-      if (e == cudaSuccess) e = cudaFree(d->poly_slab[k]);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaFree(poly slab)");
-      d->poly_slab[k] = nullptr;
-      d->poly_slab_words[k] = 0;
-    }
-    const size_t words = need + need / 4;  // some headroom for the next call size
-    cudaError_t e = cudaMalloc((void**)&d->poly_slab[k], words * sizeof(unsigned));
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(poly slab)");
-    d->poly_slab_words[k] = words;
-  }
+  if (int st = grow_ring(d->poly_slab, d->poly_slab_words, 4, need, guard.capturing, "poly slab")) return st;
   A.poly_slab = d->poly_slab[k];
   A.poly_slab_w = (kPolyTile + A.poly_ntaps - 1 + 31) & ~31;
   return GPURIR_OK;
@@ -1060,18 +1084,8 @@ int gpurir_simulate_trajectory(const float* signal, long long n_sig, const float
         k = d->next_traj++ % 2;
       }
       part_guard.take(d->slot_mu, &d->traj_ev[k], stream);
-      if (d->traj_part_words[k] < pw) {
-        if (d->traj_part[k]) {
-          e = cudaDeviceSynchronize();  // the slot may still be in use by an earlier call
-          if (e == cudaSuccess) e = cudaFree(d->traj_part[k]);
-          if (e != cudaSuccess) return cuda_fail(e, "cudaFree(traj partials)");
-          d->traj_part[k] = nullptr;
-          d->traj_part_words[k] = 0;
-        }
-        e = cudaMalloc((void**)&d->traj_part[k], pw * sizeof(float));
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(traj partials)");
-        d->traj_part_words[k] = pw;
-      }
+      if (int st = grow_ring(d->traj_part, d->traj_part_words, 2, pw, part_guard.capturing, "traj partials"))
+        return st;
       part = d->traj_part[k];
     }
     e = launch_traj_tc(signal, n_sig, rirs, n_points, n_mics, rir_len, out, part, d->num_sms, o.split, stream);

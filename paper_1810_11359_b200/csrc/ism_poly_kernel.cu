@@ -43,9 +43,13 @@ namespace gpurir {
 // tools/phase_probe.py): thread 0 of every CTA prints %globaltimer at the phase boundaries of its item
 #ifdef GPURIR_PHASE_TIMING
 #define PT_MARK(i) do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); pt_[i] = t_; } } while (0)
-#define PT_DUMP() do { if (threadIdx.x == 0) printf("PT %d %d %d %d %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", (int)blockIdx.x, (int)sm.ti.rir, 0, 1, pt_[0], pt_[1], pt_[2], pt_[3], pt_[4], pt_[5], pt_[6], pt_[7], (unsigned long long)sm.ti.te); } while (0)
+#define PT_DUMP() do { if (threadIdx.x == 0) printf("PT %d %d %d %d %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", (int)blockIdx.x, (int)sm.ti.rir, 0, 1, pt_[0], pt_[1], pt_[2], pt_[3], pt_[4], pt_[5], pt_[6], pt_[7], (unsigned long long)sm.ti.te, pts_[0], pts_[1], pts_[2], pts_[3], pts_[4]); } while (0)
+// setup sub-steps of thread 0 (SM clock, for differences within the CTA): kernel entry, after the P table load,
+// after the item decode, after geom_from; the PT line also prints the clock at the end of the setup
+#define PS_MARK(i) do { if (threadIdx.x == 0) pts_[i] = clock64(); } while (0)
 #else
 #define PT_MARK(i) do {} while (0)
+#define PS_MARK(i) do {} while (0)
 #define PT_DUMP() do {} while (0)
 #endif
 // persistent items (the same build): per-phase time summed over the items of CTAs 0..7, printed at their exit
@@ -319,11 +323,13 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
   constexpr int kLast = kPolyChannels - 1;  // the channel whose word also counts (poly_add)
 
 #ifdef GPURIR_PHASE_TIMING
-  unsigned long long pt_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long pt_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pts_[5] = {0, 0, 0, 0, 0};
   unsigned long long ptl_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pta_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
   PT_MARK(0);
+  PS_MARK(0);
   for (int i = tid; i < ntaps * kPolyD; i += kPolyThreads) Pt[i] = A.poly_P[i];
+  PS_MARK(1);
   if (tid == 0) sm.pf_valid = 0;  // read by thread 0 only, after the loop top's barrier
   bool bz_ready = false;          // sm.bz holds this call's z factors (single-room calls)
 
@@ -361,6 +367,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       }
       PolyTile& T = sm.ti;
       T.next = wi < n_work;
+      PS_MARK(2);
       if (wi < n_work) {
         int m, tile, nISM;
         long long row;
@@ -388,6 +395,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         }
         T.row = row;
         T.rir = m;
+        PS_MARK(3);
         // tiles end-aligned ([nISM - 1024 (k + 1), nISM - 1024 k)), so the last one holds the whole envelope
         // window when the tail is fused; also when it is not, because the fixed-point scale is per tile and a RIR
         // must give the same bits whether or not its tail is fused (shards of one call fuse or not by size), and
@@ -467,6 +475,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         T.ovf = 0;
       }
     }
+    PS_MARK(4);
     __syncthreads();
     if (!sm.ti.next) { PTL_DUMP(); break; }
     PT_MARK(1);

@@ -34,6 +34,10 @@ def parse(path):
     for te in sorted(set(a[:, 12].astype(int))):
         s = a[:, 12] == te
         print(f"  tile te={te:6d}: {s.sum():4d} CTAs  aggr done max {t[s, 3].max():7.2f}  end max {t[s, 7].max():7.2f}")
+    if a.shape[1] >= 18:  # thread-0 setup sub-steps in SM clocks from entry (1.965 GHz)
+        u = (a[:, 14:18] - a[:, 13:14]) / 1965.0
+        for i, n in enumerate(["P loaded", "decoded", "geom", "set up"]):
+            print(f"  setup {n:9s} min {u[:, i].min():7.2f}  median {np.median(u[:, i]):7.2f}  max {u[:, i].max():7.2f}")
 
 
 if __name__ == "__main__":
