@@ -126,7 +126,13 @@ class ClockSampler:
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "100"], stdout=open(self.path, "w"),
                 stderr=subprocess.DEVNULL)
-            time.sleep(0.3)
+            # nvidia-smi's NVML start-up can take longer than a fixed sleep and stalls the driver meanwhile (a cfg5
+            # step that plans on the host saw its first timed call take 117 ms instead of 40): wait for its first
+            # sample before the timed region starts
+            t_end = time.time() + 5.0
+            while time.time() < t_end and os.path.getsize(self.path) == 0:
+                time.sleep(0.02)
+            time.sleep(0.1)
         except Exception:
             self.proc = None
         return self
@@ -1051,6 +1057,9 @@ def run_cfg5(args, P, torch, dev, rank, world, dist, local_dev, lib):
             dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
     dev_ms = [k[0][0].elapsed_ms(k[1][1]) for k in kev]
+    if os.environ.get("GPURIR_BENCH_DEBUG"):
+        print("cfg5 step ms", " ".join(f"{x:.1f}" for x in step_ms), "device ms", " ".join(f"{x:.1f}" for x in dev_ms),
+              file=sys.stderr, flush=True)
     red_dev = dev if args.dist_backend == "nccl" else "cpu"
     tot_t = torch.tensor([sum(step_ms), sum(dev_ms)], dtype=torch.float64, device=red_dev)
     if dist:

@@ -10,7 +10,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/gpurir.h"
@@ -510,6 +512,18 @@ int finish(const gpurir_opts& o, cudaStream_t st, DeviceState* d) {
   return GPURIR_OK;
 }
 
+// GPURIR_PLAN_TIMING=1: the batch call prints its host phases (plan, workspace, staging, launch) to stderr
+bool plan_timing() {
+  static const bool on = [] {
+    const char* e = getenv("GPURIR_PLAN_TIMING");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 // Host plan of a multi-room batch (gpurir_simulate_rir_batch, gpurir_workspace_bytes): the device job table, the
 // heavy-first tile list of the ISM kernel and the chunk list of the tail kernel.
 struct BatchPlan {
@@ -518,6 +532,15 @@ struct BatchPlan {
   bool poly = false, persistent = false, any_two_word = false, fused = false;
   int kmode = 0;
   size_t off_tiles = 0, off_chunks = 0, bytes = 0;  // device workspace layout
+  std::vector<int> ntile;                            // scratch: tiles per room
+  // a plan is reused by the next call on the same host thread (thread_local in the callers): its vectors keep
+  // their capacity, so a large batch does not map and zero-fill ~24 MB of fresh pages on every call
+  void reset() {
+    tiles.clear(); chunks.clear();
+    poly = persistent = any_two_word = fused = false;
+    kmode = 0;
+    off_tiles = off_chunks = bytes = 0;
+  }
 };
 
 int plan_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, const gpurir_opts& o, int num_sms,
@@ -527,33 +550,73 @@ int plan_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, const
   const double H = o.Tw * fs / 2.0;
   if ((int)ceil((kTCPersistent + 2.0 * H) / kS) + 1 > kMaxBins) return GPURIR_EINVAL;
   P.jobs.resize(n_rooms);
-  long long small_tiles = 0;  // work items at the cluster kernel's tile length (kernel choice)
-  for (int i = 0; i < n_rooms; i++) {
-    const gpurir_room& R = rooms[i];
-    if (int e0 = validate_room(R.room_sz, R.beta, R.nb_img, R.mic_pattern)) return e0;
-    if (R.spkr_pattern < 0 || R.spkr_pattern > 4) return GPURIR_EINVAL;
-    if (!(R.Tmax > 0) || !(R.Tdiff >= 0) || R.out_offset < 0) return GPURIR_EINVAL;
-    BatchJob& J = P.jobs[i];
-    memset(&J, 0, sizeof(J));
-    for (int a = 0; a < 3; a++) {
-      J.L[a] = R.room_sz[a]; J.src[a] = R.pos_src[a]; J.rcv[a] = R.pos_rcv[a]; J.orv[a] = R.orV_rcv[a];
-      J.ors[a] = R.orV_src[a];
-      J.nb[a] = R.nb_img[a];
+  // rooms [lo, hi): validation and the job record of each (independent per room); the first invalid room's code
+  struct Part {
+    int err = GPURIR_OK, err_room = 0;
+    bool two_word = false;
+    long long small_tiles = 0;  // work items at the cluster kernel's tile length (kernel choice)
+  };
+  auto plan_rooms = [&](int lo, int hi, Part& out) {
+    for (int i = lo; i < hi; i++) {
+      const gpurir_room& R = rooms[i];
+      int e0 = validate_room(R.room_sz, R.beta, R.nb_img, R.mic_pattern);
+      if (!e0 && (R.spkr_pattern < 0 || R.spkr_pattern > 4)) e0 = GPURIR_EINVAL;
+      if (!e0 && (!(R.Tmax > 0) || !(R.Tdiff >= 0) || R.out_offset < 0)) e0 = GPURIR_EINVAL;
+      long long nS = 0, nISM = 0;
+      if (!e0) {
+        nS = gpurir_nsamples(R.Tmax, fs);
+        nISM = std::min(gpurir_nsamples(R.Tdiff, fs), nS);
+        if (nS > (1LL << 30) || nISM > kMaxIsmSamples) e0 = GPURIR_EINVAL;
+      }
+      if (e0) { out.err = e0; out.err_room = i; return; }
+      BatchJob& J = P.jobs[i];
+      memset(&J, 0, sizeof(J));
+      for (int a = 0; a < 3; a++) {
+        J.L[a] = R.room_sz[a]; J.src[a] = R.pos_src[a]; J.rcv[a] = R.pos_rcv[a]; J.orv[a] = R.orV_rcv[a];
+        J.ors[a] = R.orV_src[a];
+        J.nb[a] = R.nb_img[a];
+      }
+      for (int w = 0; w < 6; w++) J.beta[w] = R.beta[w];
+      beta_logs(R.beta, J.lb, &J.neg, &J.zero);
+      J.pattern = R.mic_pattern;
+      J.spkr_pattern = R.spkr_pattern;
+      J.nISM = (int)nISM; J.nS = (int)nS; J.out_offset = R.out_offset;
+      const double T60 = sabine(R.room_sz, R.beta);
+      J.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);  // Eq. 8, reading C14
+      J.rir_global = o.rir_index_base + R.rir_index;                        // reading C16: global stream id
+      poly_geo_consts(R.room_sz, fs / c, J.geo);
+      out.two_word = out.two_word || poly_two_word_for(R.room_sz, nISM, fs, c, o.Tw);
+      out.small_tiles += (nISM + kTC - 1) / kTC;
     }
-    for (int w = 0; w < 6; w++) J.beta[w] = R.beta[w];
-    beta_logs(R.beta, J.lb, &J.neg, &J.zero);
-    J.pattern = R.mic_pattern;
-    J.spkr_pattern = R.spkr_pattern;
-    long long nS = gpurir_nsamples(R.Tmax, fs), nISM = gpurir_nsamples(R.Tdiff, fs);
-    if (nISM > nS) nISM = nS;
-    if (nS > (1LL << 30) || nISM > kMaxIsmSamples) return GPURIR_EINVAL;
-    J.nISM = (int)nISM; J.nS = (int)nS; J.out_offset = R.out_offset;
-    const double T60 = sabine(R.room_sz, R.beta);
-    J.kappa_fs = isinf(T60) ? 0.f : (float)(6.0 * log(10.0) / T60 / fs);  // Eq. 8, reading C14
-    J.rir_global = o.rir_index_base + R.rir_index;                        // reading C16: global stream id
-    poly_geo_consts(R.room_sz, fs / c, J.geo);
-    P.any_two_word = P.any_two_word || poly_two_word_for(R.room_sz, nISM, fs, c, o.Tw);
-    small_tiles += (nISM + kTC - 1) / kTC;
+  };
+  // large batches (dataset generation, config 5) over host threads: the plan of 100 000 rooms is ~11 ms on one
+  // core, which a slower or busier host turns into the step's bottleneck (the kernel takes ~25 ms); small calls
+  // stay on the calling thread.  GPURIR_PLAN_THREADS caps the count (1 = serial).
+  static const int max_threads = [] {
+    const char* e = getenv("GPURIR_PLAN_THREADS");
+    const int hw = (int)std::thread::hardware_concurrency();
+    const int x = e ? atoi(e) : std::min(8, std::max(1, hw));
+    return std::max(1, x);
+  }();
+  const int nt = std::max(1, std::min(max_threads, n_rooms / 4096));
+  std::vector<Part> parts((size_t)nt);
+  if (nt == 1) {
+    plan_rooms(0, n_rooms, parts[0]);
+  } else {
+    std::vector<std::thread> th;
+    th.reserve((size_t)nt - 1);
+    const int per = (n_rooms + nt - 1) / nt;
+    for (int t = 1; t < nt; t++)
+      th.emplace_back(plan_rooms, t * per, std::min(n_rooms, (t + 1) * per), std::ref(parts[(size_t)t]));
+    plan_rooms(0, std::min(n_rooms, per), parts[0]);
+    for (auto& x : th) x.join();
+  }
+  long long small_tiles = 0;
+  for (const Part& pt : parts)  // in room order: the first invalid room decides the code, as serially
+    if (pt.err) return pt.err;
+  for (const Part& pt : parts) {
+    P.any_two_word = P.any_two_word || pt.two_word;
+    small_tiles += pt.small_tiles;
   }
   P.poly = o.mode == GPURIR_POLY;
   P.kmode = o.mode == GPURIR_POLY ? (P.poly ? GPURIR_POLY : GPURIR_FP32) : o.mode;
@@ -569,7 +632,8 @@ int plan_batch(int n_rooms, const gpurir_room* rooms, double fs, double c, const
     for (int ch = 0; ch < nch; ch++) P.chunks.push_back(make_int2(i, ch));
   }
   const int tile_len = P.poly ? kPolyTile : P.persistent ? kTCPersistent : kTC;
-  std::vector<int> ntile(n_rooms);
+  std::vector<int>& ntile = P.ntile;
+  ntile.resize(n_rooms);
   int max_tiles = 0;
   size_t total_tiles = 0;
   for (int i = 0; i < n_rooms; i++) {
@@ -947,7 +1011,9 @@ size_t gpurir_workspace_bytes(int n_rooms, const gpurir_room* rooms, double fs, 
   int st = GPURIR_OK;
   DeviceState* d = device_state(&st);
   if (!d) return 0;
-  BatchPlan P;
+  thread_local BatchPlan plan;
+  BatchPlan& P = plan;
+  P.reset();
   if (plan_batch(n_rooms, rooms, fs, c, o, d->num_sms, P) != GPURIR_OK) return 0;
   return P.bytes;
 }
@@ -962,8 +1028,12 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
   int st = GPURIR_OK;
   DeviceState* d = device_state(&st);
   if (!d) return st;
-  BatchPlan P;
+  thread_local BatchPlan plan;
+  BatchPlan& P = plan;
+  P.reset();
+  const double t_start = plan_timing() ? now_ms() : 0.0;
   if ((st = plan_batch(n_rooms, rooms, fs, c, o, d->num_sms, P))) return st;
+  const double t_plan = plan_timing() ? now_ms() : 0.0;
   const double H = o.Tw * fs / 2.0;
   cudaStream_t stream = (cudaStream_t)o.stream;
   if (o.workspace && o.workspace_bytes < P.bytes) return GPURIR_EINVAL;
@@ -979,6 +1049,7 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
   auto release = [&] {
     if (!o.workspace) cudaFreeAsync(ws, stream);
   };
+  const double t_alloc = plan_timing() ? now_ms() : 0.0;
   BatchJob* djobs = reinterpret_cast<BatchJob*>(ws);
   int2* dtiles = reinterpret_cast<int2*>(ws + P.off_tiles);
   int2* dchunks = reinterpret_cast<int2*>(ws + P.off_chunks);
@@ -1013,6 +1084,16 @@ int gpurir_simulate_rir_batch(int n_rooms, const gpurir_room* rooms, double fs, 
     if (e == cudaSuccess) e = cudaEventRecord(d->stage_done[k], stream);
     if (e != cudaSuccess) { release(); return cuda_fail(e, "batch upload"); }
   }
+  const double t_stage = plan_timing() ? now_ms() : 0.0;
+  struct TimingPrint {  // at return: the launch phase ends with the call
+    double t0, t1, t2, t3;
+    int n;
+    ~TimingPrint() {
+      if (!plan_timing()) return;
+      fprintf(stderr, "gpurir batch %d rooms: plan %.2f ms, workspace %.2f ms, staging %.2f ms, launch %.2f ms\n", n,
+              t1 - t0, t2 - t1, t3 - t2, now_ms() - t3);
+    }
+  } timing_print{t_start, t_plan, t_alloc, t_stage, n_rooms};
 
   if (!P.tiles.empty()) {
     IsmArgs A;
