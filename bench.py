@@ -658,9 +658,11 @@ def _latency_us(torch, fn, n=50):
     return a.elapsed_time(b) * 1000.0 / n
 
 
-def _graph_latency_us(torch, fn, n=50):
-    """The same call captured once into a CUDA graph and replayed back to back: device µs per call without the
-    Python / ctypes / launch overhead of an eager call (the library is stream-ordered and capturable)."""
+def _graph_latency_us(torch, fn, n=50, calls=1):
+    """The same call captured into a CUDA graph (`calls` times back to back) and replayed: device µs per call without
+    the Python / ctypes / launch overhead of an eager call (the library is stream-ordered and capturable).  A graph
+    replay costs a whole number of ~2.05 µs steps (tools/replay_quantum.py: any kernel, cluster or not), so one call
+    per graph rounds the kernel up; with several calls per graph only the kernels and their gaps remain."""
     fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
@@ -671,7 +673,8 @@ def _graph_latency_us(torch, fn, n=50):
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
     with torch.cuda.graph(g):
-        fn()
+        for _ in range(calls):
+            fn()
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
@@ -681,7 +684,7 @@ def _graph_latency_us(torch, fn, n=50):
         g.replay()
     b.record()
     torch.cuda.synchronize()
-    return a.elapsed_time(b) * 1000.0 / n
+    return a.elapsed_time(b) * 1000.0 / (n * calls)
 
 
 def sweep(P, torch, dev, flush):
@@ -713,10 +716,13 @@ def sweep(P, torch, dev, flush):
         fn = point("cfg1", W.cfg1(), mode, reps=10, warm=3)
         rows[-1]["us_per_call_back_to_back"] = _latency_us(torch, fn)
         rows[-1]["us_per_call_graph_replay"] = _graph_latency_us(torch, fn)
+        if mode == "poly":
+            rows[-1]["us_per_call_graph_10_calls"] = _graph_latency_us(torch, fn, 10, calls=10)
     for T60 in W.CFG2_T60:  # config 2: T60 sweep, one RIR, ISM + tail
         fn = point("cfg2", W.cfg2(T60), "poly", reps=7, warm=3, T60=T60)
         rows[-1]["us_per_call_back_to_back"] = _latency_us(torch, fn, 20)
         rows[-1]["us_per_call_graph_replay"] = _graph_latency_us(torch, fn, 20)
+        rows[-1]["us_per_call_graph_10_calls"] = _graph_latency_us(torch, fn, 5, calls=10)
     for M in (1, 4, 16, 64, 256, 1024, 4096, 16384):  # config 3 (i): #RIR sweep, diffuse
         point("cfg3_diffuse", W.cfg3(M, "diffuse"), "poly", reps=5 if M < 4096 else 3)
     for mode in ("fp32", "lut", "fp16", "lut_tex"):
