@@ -890,6 +890,20 @@ def test_small_call_cuda_graph_replay(P, oracle, mode):
             g.replay()
             torch.cuda.synchronize()
             assert torch.equal(out, ref), sc.name
+        # several calls in one graph (how small calls amortise the graph launch): the scratch ring's slots are
+        # taken in turn inside the capture; every call writes the same bits
+        outs = [torch.empty_like(out) for _ in range(6)]
+        g6 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g6):
+            for o in outs:
+                P.simulate_rir(sc.room, beta, src, rcv, nb, sc.Tdiff, sc.Tmax, sc.fs, c=sc.c, mode=mode,
+                               seed=sc.seed, out=o)
+        for o in outs:
+            o.zero_()
+        g6.replay()
+        torch.cuda.synchronize()
+        for o in outs:
+            assert torch.equal(o, ref), sc.name
         assert P.device_status() == 0
 
 
