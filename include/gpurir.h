@@ -301,6 +301,16 @@ long long gpurir_lut_table(double Tw, double fs, int Q, float* lut_out, long lon
  * host float[ntaps][8] table.  Returns ntaps, or -GPURIR_EINVAL (Tw fs > 1022 or not positive). */
 int gpurir_poly_table(double Tw, double fs, int* mlo, float* P_out, long long cap);
 
+/* The FIR form of that expansion exactly as GPURIR_POLY uploads it (reading R13): the channels
+ * rotated per parity, G' = Q G (Q orthogonal, block diagonal over even / odd d, rows the eigenvectors of the
+ * Gram matrix of the taps outside the window below), so that rotated channels 0..3 keep all ntaps taps and
+ * channels 4..7 only the nn taps mi = nmi0 .. nmi0 + nn - 1 around m = 0, 1: delta'(m - phi) ~=
+ * sum_r P'_r[m] (Q T(2 phi - 1))_r.  Writes *mlo, *nmi0, *nn and, when out != NULL and cap >= 4 ntaps + 4 nn + 32,
+ * the host float table [far: 2 pairs][ntaps][2] (channels (0,1), (2,3)), [near: 2 pairs][nn][2] (channels (4,5),
+ * (6,7)), Q [parity][k][i] (rotated channel 2k + parity = sum_i Q G_{2i + parity}).  Returns ntaps, or
+ * -GPURIR_EINVAL. */
+int gpurir_poly_fir_table(double Tw, double fs, int* mlo, int* nmi0, int* nn, float* out, long long cap);
+
 /* Read and (if reset) clear the current device's status word (see file header). Synchronises. */
 int gpurir_device_status(int reset);
 

@@ -22,7 +22,7 @@ EXPORTS = [
     "gpurir_sabine_t60", "gpurir_beta_sabine", "gpurir_att2t_sabine", "gpurir_t2n", "gpurir_image_params",
     "gpurir_lut_table", "gpurir_device_status", "gpurir_strerror", "gpurir_last_cuda_error", "gpurir_version",
     "gpurir_simulate_trajectory", "gpurir_simulate_rir_dir", "gpurir_beta_sabine_weighted", "gpurir_poly_table",
-    "gpurir_simulate_rir_host", "gpurir_workspace_bytes", "gpurir_batch_extent",
+    "gpurir_simulate_rir_host", "gpurir_workspace_bytes", "gpurir_batch_extent", "gpurir_poly_fir_table",
 ]
 
 
@@ -97,6 +97,8 @@ def lib() -> C.CDLL:
                                       vp]
     L.gpurir_poly_table.restype = C.c_int
     L.gpurir_poly_table.argtypes = [C.c_double, C.c_double, ip, fp, C.c_longlong]
+    L.gpurir_poly_fir_table.restype = C.c_int
+    L.gpurir_poly_fir_table.argtypes = [C.c_double, C.c_double, ip, ip, ip, fp, C.c_longlong]
     L.gpurir_lut_table.restype = C.c_longlong
     L.gpurir_lut_table.argtypes = [C.c_double, C.c_double, C.c_int, fp, C.c_longlong]
     L.gpurir_device_status.restype = C.c_int

@@ -332,6 +332,22 @@ def poly_table(Tw: float = 4e-3, fs: float = 16000.0) -> tuple[np.ndarray, int]:
     return np.array(list(buf), dtype=np.float32).reshape(n, 8), int(mlo.value)
 
 
+def poly_fir_table(Tw: float = 4e-3, fs: float = 16000.0) -> dict:
+    """gpurir_poly_fir_table: the rotated low-rank FIR form of GPURIR_POLY (reading R13) — far [2, ntaps, 2],
+    near [2, nn, 2], Q [2, 4, 4], m_lo, nmi0, nn."""
+    mlo, nmi0, nn = C.c_int(0), C.c_int(0), C.c_int(0)
+    n = int(lib().gpurir_poly_fir_table(float(Tw), float(fs), C.byref(mlo), C.byref(nmi0), C.byref(nn), None, 0))
+    if n < 0:
+        raise GpurirError(-n, "gpurir_poly_fir_table")
+    k = nn.value
+    cap = 4 * n + 4 * k + 32
+    buf = (C.c_float * cap)()
+    lib().gpurir_poly_fir_table(float(Tw), float(fs), C.byref(mlo), C.byref(nmi0), C.byref(nn), buf, cap)
+    a = np.array(list(buf), dtype=np.float32)
+    return {"far": a[:4 * n].reshape(2, n, 2), "near": a[4 * n:4 * n + 4 * k].reshape(2, k, 2),
+            "Q": a[4 * n + 4 * k:].reshape(2, 4, 4), "mlo": int(mlo.value), "nmi0": int(nmi0.value), "nn": k}
+
+
 def image_params(room_sz, beta, src, rcv, nb_img, fs, c=343.0, mic_pattern="omni", orv=None, device=None,
                  spkr_pattern="omni", ors=None):
     """gpurir_image_params: (delay in samples float64 [N], amplitude float32 [N]) in lattice order."""

@@ -49,6 +49,7 @@ struct TexEntry {  // one Eq. 9 table as a filtered 1-D texture (texture-LUT mod
 struct PolyEntry {  // polyphase table of one (Tw, fs) (mode GPURIR_POLY, reading R11); never overwritten
   double Tw = 0, fs = 0;
   int ntaps = 0, mlo = 0;
+  int nmi0 = 0, nn = 0;  // the rotated near channels' tap window (poly_fir_tables)
   float* dev = nullptr;
 };
 
@@ -230,15 +231,102 @@ int poly_fit(double Tw, double fs, int* mlo_out, std::vector<float>& tab) {
   return npad;
 }
 
+// Eigen-decomposition of a symmetric 4 x 4 matrix by cyclic Jacobi rotations (fp64, to convergence): a = V
+// diag(w) V^T, eigenvector k in column k of v.
+static void jacobi4(double a[4][4], double w[4], double v[4][4]) {
+  for (int i = 0; i < 4; i++)
+    for (int j = 0; j < 4; j++) v[i][j] = i == j;
+  for (int sweep = 0; sweep < 64; sweep++) {
+    double off = 0.0;
+    for (int p = 0; p < 4; p++)
+      for (int q = p + 1; q < 4; q++) off += a[p][q] * a[p][q];
+    if (off == 0.0) break;
+    for (int p = 0; p < 4; p++)
+      for (int q = p + 1; q < 4; q++) {
+        if (a[p][q] == 0.0) continue;
+        const double th = 0.5 * atan2(2.0 * a[p][q], a[q][q] - a[p][p]), c = cos(th), s = sin(th);
+        for (int k = 0; k < 4; k++) {  // a <- a J (columns p, q), then J^T a (rows p, q)
+          const double akp = a[k][p], akq = a[k][q];
+          a[k][p] = c * akp - s * akq;
+          a[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < 4; k++) {
+          const double apk = a[p][k], aqk = a[q][k];
+          a[p][k] = c * apk - s * aqk;
+          a[q][k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < 4; k++) {
+          const double vkp = v[k][p], vkq = v[k][q];
+          v[k][p] = c * vkp - s * vkq;
+          v[k][q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  for (int i = 0; i < 4; i++) w[i] = a[i][i];
+}
+
+// Low-rank FIR of R11 (reading R13): the 8 channel filters P_d[m] restricted to the taps away from
+// the centre have numerical rank 4 (the windowed sinc there is sin(pi phi) times a function of phi that varies
+// slowly with m), so after an orthogonal change of channel basis G' = Q G — per parity (P_d[1 - m] =
+// (-1)^d P_d[m], Eq. 6 is even, so Q is block diagonal over even / odd d), rows the eigenvectors of the far taps'
+// Gram matrix sum_m P[m] P[m]^T by decreasing eigenvalue — only the rotated channels 0..3 need the whole support;
+// channels 4..7 keep an aligned window of nn = 16 (or 24) taps around m = 0, 1 (the far-tap coefficients dropped
+// there are < 1e-8: their eigenvalues).  The kernel converts G, rotates it by Q and runs the FIR on
+// 4 ntaps + 4 nn taps per output instead of 8 ntaps.  Device table: far [2 pairs][ntaps][2] (rotated channels
+// (0, 1), (2, 3)), near [2 pairs][nn][2] (channels (4, 5), (6, 7)) for taps mi = nmi0 .. nmi0 + nn - 1, then
+// Q [parity][k][i] (32 floats): rotated channel 2 k + par = sum_i Q[par][k][i] G_{2 i + par}, the k-th
+// eigenvector of that parity.
+void poly_fir_tables(const std::vector<float>& tab, int npad, int mlo, std::vector<float>& out, int* nmi0_out,
+                     int* nn_out) {
+  auto Pd = [&](int mi, int d) { return (double)tab[((size_t)(d >> 1) * npad + mi) * 2 + (d & 1)]; };
+  const int mc = -mlo;                         // tap index of m = 0
+  const int nmi0 = std::max(0, ((mc - 6) / 8) * 8);  // the window covers m = -6 .. 7 (mi = mc - 6 .. mc + 7)
+  const int nn = std::min(npad - nmi0, ((mc + 8 - nmi0 + 7) / 8) * 8);
+  double Q[8][8] = {};
+  for (int par = 0; par < 2; par++) {
+    double a[4][4] = {}, w[4], v[4][4];
+    for (int mi = 0; mi < npad; mi++) {
+      if (mi >= nmi0 && mi < nmi0 + nn) continue;
+      for (int i = 0; i < 4; i++)
+        for (int j = 0; j < 4; j++) a[i][j] += Pd(mi, 2 * i + par) * Pd(mi, 2 * j + par);
+    }
+    jacobi4(a, w, v);
+    int ord[4] = {0, 1, 2, 3};
+    std::sort(ord, ord + 4, [&](int x, int y) { return w[x] > w[y]; });
+    for (int k = 0; k < 4; k++)
+      for (int i = 0; i < 4; i++) Q[2 * k + par][2 * i + par] = v[i][ord[k]];
+  }
+  auto Pr = [&](int mi, int r) {  // rotated coefficient P'_r[mi] = sum_d Q[r][d] P_d[mi]
+    double s = 0.0;
+    for (int d = 0; d < 8; d++) s += Q[r][d] * Pd(mi, d);
+    return (float)s;
+  };
+  out.assign((size_t)4 * npad + (size_t)4 * nn + 32, 0.f);
+  for (int q = 0; q < 2; q++)
+    for (int mi = 0; mi < npad; mi++)
+      for (int c = 0; c < 2; c++) out[((size_t)q * npad + mi) * 2 + c] = Pr(mi, 2 * q + c);
+  float* near = out.data() + (size_t)4 * npad;
+  for (int q = 0; q < 2; q++)
+    for (int i = 0; i < nn; i++)
+      for (int c = 0; c < 2; c++) near[((size_t)q * nn + i) * 2 + c] = Pr(nmi0 + i, 4 + 2 * q + c);
+  float* Qo = near + (size_t)4 * nn;  // [parity][k][i]: rotated channel 2 k + par = sum_i Q G_{2 i + par}
+  for (int par = 0; par < 2; par++)
+    for (int k = 0; k < 4; k++)
+      for (int i = 0; i < 4; i++) Qo[(par * 4 + k) * 4 + i] = (float)Q[2 * k + par][2 * i + par];
+  *nmi0_out = nmi0;
+  *nn_out = nn;
+}
+
 const PolyEntry* ensure_poly(DeviceState* d, double Tw, double fs, cudaStream_t stream, int* err) {
   *err = GPURIR_OK;
   for (const PolyEntry& P : d->polys)
     if (P.Tw == Tw && P.fs == fs) return &P;
   PolyEntry P;
   P.Tw = Tw; P.fs = fs;
-  std::vector<float> tab;
-  P.ntaps = poly_fit(Tw, fs, &P.mlo, tab);
+  std::vector<float> tab0, tab;
+  P.ntaps = poly_fit(Tw, fs, &P.mlo, tab0);
   if (P.ntaps < 0) { *err = GPURIR_EINVAL; return nullptr; }
+  poly_fir_tables(tab0, P.ntaps, P.mlo, tab, &P.nmi0, &P.nn);
   const size_t bytes = tab.size() * sizeof(float);
   cudaError_t e = cudaMalloc(&P.dev, bytes);
   if (e != cudaSuccess) { *err = cuda_fail(e, "cudaMalloc(poly)"); return nullptr; }
@@ -289,7 +377,7 @@ int setup_mode(DeviceState* d, const gpurir_opts& o, double fs, double H, cudaSt
   } else if (o.mode == GPURIR_POLY) {
     const PolyEntry* P = ensure_poly(d, o.Tw, fs, stream, &st);
     if (!P) return st;
-    A.poly_P = P->dev; A.poly_ntaps = P->ntaps; A.poly_mlo = P->mlo;
+    A.poly_P = P->dev; A.poly_ntaps = P->ntaps; A.poly_mlo = P->mlo; A.poly_nmi0 = P->nmi0; A.poly_nn = P->nn;
   }
   return GPURIR_OK;
 }
@@ -758,6 +846,22 @@ int gpurir_poly_table(double Tw, double fs, int* mlo, float* P_out, long long ca
     if (cap < (long long)ntaps * kPolyDeg) return -GPURIR_EINVAL;
     for (int mi = 0; mi < ntaps; mi++)  // [tap][channel] for the caller
       for (int k = 0; k < kPolyDeg; k++) P_out[(size_t)mi * kPolyDeg + k] = tab[((size_t)(k >> 1) * ntaps + mi) * 2 + (k & 1)];
+  }
+  return ntaps;
+}
+
+int gpurir_poly_fir_table(double Tw, double fs, int* mlo, int* nmi0, int* nn, float* out, long long cap) {
+  std::vector<float> tab0, tab;
+  int m0 = 0, a = 0, b = 0;
+  const int ntaps = poly_fit(Tw, fs, &m0, tab0);
+  if (ntaps < 0) return ntaps;
+  poly_fir_tables(tab0, ntaps, m0, tab, &a, &b);
+  if (mlo) *mlo = m0;
+  if (nmi0) *nmi0 = a;
+  if (nn) *nn = b;
+  if (out) {
+    if (cap < (long long)tab.size()) return -GPURIR_EINVAL;
+    memcpy(out, tab.data(), tab.size() * sizeof(float));
   }
   return ntaps;
 }

@@ -289,6 +289,61 @@ __host__ __device__ constexpr int poly_plane_words(int ntaps) {
 }
 constexpr int kPolyWFixTaps = 64;
 constexpr int kPolyWFix = poly_plane_words(kPolyWFixTaps);
+constexpr int kPolyMaxNear = 24;  // rotated near channels' tap window (abi.cu poly_fir_tables: 16 or 24)
+// floats of the FIR tables in shared memory (reading R13): far [2][ntaps][2], near [2][nn][2], Q [2][4][4]
+__host__ __device__ constexpr int poly_tab_floats(int ntaps, int nn) { return 4 * ntaps + 4 * nn + 32; }
+
+// Channel rotation of reading R13 (G' = Q G, per parity): one rotated value from the four same-parity channel
+// values a, b, c, d (channels par, 2 + par, 4 + par, 6 + par) — one fixed FMA order, shared by every path that
+// converts G (persistent and cluster items give the same bits)
+__device__ __forceinline__ float poly_rot1(const float* q, float a, float b, float c, float d) {
+  return fmaf(q[3], d, fmaf(q[2], c, fmaf(q[1], b, q[0] * a)));
+}
+
+// One FIR item (reading R13): outputs t8 .. t8 + 7 of partial pi = 2 s + h — the far channel pair s (rotated
+// channels 2 s, 2 s + 1) over tap half h of its ntaps taps, then the near pair s (channels 4 + 2 s, 5 + 2 s) over
+// half h of its nn taps — with a sliding register window, FFMA2 over the taps in order.  Gf: fp32 rotated planes
+// of stride W, position p at p + p / 8, the item's first output at position ntaps - 1 (t8 relative to it).
+__device__ __forceinline__ void poly_fir_range(const float* G0, int W, const float4* P4, int q, int ngroups,
+                                               float2 (&acc)[8]) {
+  float2 w[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const int a = (q + r) + ((q + r) >> 3);
+    w[r] = make_float2(G0[a], G0[a + W]);
+  }
+  const float* gn = G0 + (q - 1) + ((q - 1) >> 3);  // padded address of position q - 1 (= 6 mod 8)
+  for (int gi = 0; gi < ngroups; gi++, gn -= 9, P4 += 4) {
+    const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};  // 8 taps of the pair, (2i, 2i + 1) per float4
+#pragma unroll
+    for (int u = 0; u < 8; u++) {  // tap u: output r uses slot (r - u) & 7, then slot (7 - u) & 7 refills
+      const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
+#pragma unroll
+      for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 7], acc[r]);
+      const int o = u < 7 ? -u : -8;  // the last group's refills read padding: never used
+      w[(7 - u) & 7] = make_float2(gn[o], gn[o + W]);
+    }
+  }
+}
+__device__ __forceinline__ void poly_fir_item(const float* Gf, int W, const float* Pt, int ntaps, int nmi0, int nn,
+                                              int pi, int t8, float (&res)[8]) {
+  const int s = pi >> 1, h = pi & 1;
+  float2 acc[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) acc[r] = make_float2(0.f, 0.f);
+  {  // far pair s: tap groups [g0, g1) of ntaps / 8
+    const int ng = ntaps >> 3, gh = (ng + 1) >> 1, g0 = h ? gh : 0, g1 = h ? ng : gh;
+    const float4* P4 = reinterpret_cast<const float4*>(Pt) + s * (ntaps >> 1) + g0 * 4;
+    poly_fir_range(Gf + (2 * s) * W, W, P4, t8 + ntaps - 1 - 8 * g0, g1 - g0, acc);
+  }
+  {  // near pair s: its window's tap groups [g0, g1) of nn / 8 (tap mi = nmi0 + 8 g0 first)
+    const int ng = nn >> 3, gh = (ng + 1) >> 1, g0 = h ? gh : 0, g1 = h ? ng : gh;
+    const float4* P4 = reinterpret_cast<const float4*>(Pt + 4 * ntaps) + s * (nn >> 1) + g0 * 4;
+    poly_fir_range(Gf + (4 + 2 * s) * W, W, P4, t8 + ntaps - 1 - nmi0 - 8 * g0, g1 - g0, acc);
+  }
+#pragma unroll
+  for (int r = 0; r < 8; r++) res[r] = acc[r].x + acc[r].y;
+}
 
 // CL = false: persistent CTAs taking (RIR, tile) items from a queue (large calls).  CL = true (small calls): a
 // thread-block cluster of S CTAs per item — rank r aggregates the tile's columns r, r + S, ... into its own G,
@@ -328,7 +383,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
 #endif
   PT_MARK(0);
   PS_MARK(0);
-  for (int i = tid; i < ntaps * kPolyD; i += kPolyThreads) Pt[i] = A.poly_P[i];
+  for (int i = tid; i < poly_tab_floats(ntaps, A.poly_nn); i += kPolyThreads) Pt[i] = A.poly_P[i];
+  // (the FIR window nmi0 / nn and the rotation Q = Pt + 4 ntaps + 4 nn are re-read from the parameter bank where
+  // used: no registers held across the image loop)
   PS_MARK(1);
   if (tid == 0) sm.pf_valid = 0;  // read by thread 0 only, after the loop top's barrier
   bool bz_ready = false;          // sm.bz holds this call's z factors (single-room calls)
@@ -719,8 +776,12 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
                                 : (float)((double)((long long)ca * 16384 + fb) * T.inv_scale);
             }
           }
+          const float* Qr = Pt + 4 * ntaps + 4 * A.poly_nn;
 #pragma unroll
-          for (int d = 0; d < kPolyD; d++) stf[d * Pq + pi] = v[d];
+          for (int par = 0; par < 2; par++)  // rotated channels (reading R13): stf holds G' = Q G
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+              stf[(2 * k + par) * Pq + pi] = poly_rot1(Qr + (par * 4 + k) * 4, v[par], v[2 + par], v[4 + par], v[6 + par]);
         }
         if (bad) atomicOr(A.status, kStatusCapacity);
       }
@@ -733,36 +794,16 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       }
       cl.sync();  // every rank has gathered: the staging areas are free
       PT_MARK(5);
-      // FIR over this rank's R outputs with the persistent path's arithmetic (so the same bits): item (channel pair
-      // gq, 8 consecutive outputs) — a sliding register window, FFMA2 over the taps in order — then per output the
-      // pairs' partials ((p0 + p1) + (p2 + p3)); all positions are local to the rank (o0 is its first output)
-      float* red = reinterpret_cast<float*>(sm.col);  // [4 pairs][R]
+      // FIR over this rank's R outputs with the persistent path's arithmetic (so the same bits): item (partial pi,
+      // 8 consecutive outputs) of poly_fir_item, then per output the partials ((p0 + p1) + (p2 + p3)); all positions
+      // are local to the rank (o0 is its first output)
+      float* red = reinterpret_cast<float*>(sm.col);  // [4 partials][R]
       for (int it = tid; it < 4 * (R >> 3); it += kPolyThreads) {
-        const int gq = it / (R >> 3), t8 = 8 * (it - gq * (R >> 3));
-        const float* G0 = Gf + (2 * gq) * W;  // channel 2 gq; channel 2 gq + 1 sits W words further
-        const float4* P4 = reinterpret_cast<const float4*>(Pt) + gq * (ntaps >> 1);  // pair gq: taps (2i, 2i+1)
-        float2 acc[8], wv[8];
-        const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (q = 7 mod 8)
+        const int pi = it / (R >> 3), t8 = 8 * (it - pi * (R >> 3));
+        float res[8];
+        poly_fir_item(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, res);
 #pragma unroll
-        for (int r = 0; r < 8; r++) {
-          acc[r] = make_float2(0.f, 0.f);
-          const int a = (q + r) + ((q + r) >> 3);
-          wv[r] = make_float2(G0[a], G0[a + W]);
-        }
-        const float* gn = G0 + (q - 1) + ((q - 1) >> 3);
-        for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P4 += 4) {
-          const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};
-#pragma unroll
-          for (int u = 0; u < 8; u++) {
-            const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
-#pragma unroll
-            for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, wv[(r - u) & 7], acc[r]);
-            const int o = u < 7 ? -u : -8;  // the last group's refills read padding: never used
-            wv[(7 - u) & 7] = make_float2(gn[o], gn[o + W]);
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < 8; r++) red[gq * R + t8 + r] = acc[r].x + acc[r].y;
+        for (int r = 0; r < 8; r++) red[pi * R + t8 + r] = res[r];
       }
       __syncthreads();
       for (int o = tid; o < R; o += kPolyThreads) {
@@ -784,10 +825,23 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       float* Gf = reinterpret_cast<float*>(Ga);
       long long wi_next = 0;
       if (tid == 0) wi_next = atomicAdd(work_counter, 1);  // the next item's index; its latency hides under the work
+      // every thread converts whole positions (all 8 channels) and rotates them in place: G' = Q G (reading R13)
+      const float* Qr = Pt + 4 * ntaps + 4 * A.poly_nn;
       if (T.two_word) {
-        for (int i = tid; i < kPolyD * W; i += kPolyThreads)
-          Gf[i] = (i >= kLast * W && i < (kLast + 1) * W) ? (float)((double)Ga[i] * 16384.0 * T.inv_scale)
-                                                          : (float)((double)((long long)Ga[i] * 16384 + Gb[i]) * T.inv_scale);
+        for (int p = tid; p < W; p += kPolyThreads) {
+          float v[kPolyD];
+#pragma unroll
+          for (int d = 0; d < kPolyD; d++) {
+            const int i = d * W + p;
+            v[d] = d == kLast ? (float)((double)Ga[i] * 16384.0 * T.inv_scale)
+                              : (float)((double)((long long)Ga[i] * 16384 + Gb[i]) * T.inv_scale);
+          }
+#pragma unroll
+          for (int par = 0; par < 2; par++)
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+              Gf[(2 * k + par) * W + p] = poly_rot1(Qr + (par * 4 + k) * 4, v[par], v[2 + par], v[4 + par], v[6 + par]);
+        }
       } else {  // single word, |sum| < 2^31: one rounding to fp32 (I2FP, ALU pipe), then an exact power-of-two scale
         // each thread owns 4 positions of every plane: it reads their counts from the last channel's low bits
         // and removes count x 0x4B400000 (the raw-bit deposits of poly_add) from every channel
@@ -798,12 +852,23 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           const uint4 c = reinterpret_cast<const uint4*>(Ga)[kLast * w4 + q];
           const uint4 n = make_uint4(c.x & mask, c.y & mask, c.z & mask, c.w & mask);
   #pragma unroll
-          for (int d = 0; d < kPolyD; d++) {
-            const unsigned off = d < kLast ? 0x4B400000u : d == kLast ? kLastOff : 0u;  // planes past kLast stay 0
-            const uint4 v = d == kLast ? c : reinterpret_cast<const uint4*>(Ga)[d * w4 + q];
-            reinterpret_cast<float4*>(Gf)[d * w4 + q] =
-                make_float4((float)(int)(v.x - n.x * off) * is, (float)(int)(v.y - n.y * off) * is,
-                            (float)(int)(v.z - n.z * off) * is, (float)(int)(v.w - n.w * off) * is);
+          for (int par = 0; par < 2; par++) {  // one parity at a time: its 4 planes are read before any is written
+            float4 v[4];
+  #pragma unroll
+            for (int i = 0; i < 4; i++) {
+              const int d = 2 * i + par;
+              const unsigned off = d < kLast ? 0x4B400000u : d == kLast ? kLastOff : 0u;  // planes past kLast stay 0
+              const uint4 u = d == kLast ? c : reinterpret_cast<const uint4*>(Ga)[d * w4 + q];
+              v[i] = make_float4((float)(int)(u.x - n.x * off) * is, (float)(int)(u.y - n.y * off) * is,
+                                 (float)(int)(u.z - n.z * off) * is, (float)(int)(u.w - n.w * off) * is);
+            }
+  #pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const float* qk = Qr + (par * 4 + k) * 4;
+              reinterpret_cast<float4*>(Gf)[(2 * k + par) * w4 + q] =
+                  make_float4(poly_rot1(qk, v[0].x, v[1].x, v[2].x, v[3].x), poly_rot1(qk, v[0].y, v[1].y, v[2].y, v[3].y),
+                              poly_rot1(qk, v[0].z, v[1].z, v[2].z, v[3].z), poly_rot1(qk, v[0].w, v[1].w, v[2].w, v[3].w));
+            }
           }
         }
       }
@@ -826,49 +891,38 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         asm volatile("cp.async.commit_group;\n" ::: "memory");
       }
 
-      // ---- 3. 8-channel FIR: h[k] = sum_m sum_d P_d[m] G_d[k - m] --------------------------------
-      // Thread group gq (THREADS/4 threads) applies channel pair gq to 8 consecutive outputs per thread with a
-      // sliding register window (one new position per tap); the 4 groups' partial sums meet in shared memory.
-      // ntaps is padded to a multiple of 8 with zero taps, so in every unrolled group of 8 taps the new
-      // positions q - mi - 1 - u sit at fixed offsets 0 .. -6, -8 of one padded address (q = 7 mod 8).
+      // ---- 3. FIR: h[k] = sum_m sum_d P'_d[m] G'_d[k - m] (reading R13: rotated channels 0..3 over all ntaps
+      // taps, 4..7 over the nn taps of their window) ------------------------------------------------------------
+      // 512 items (partial pi = 2 s + h, 8 consecutive outputs), kPolyPasses per thread (poly_fir_item: a sliding
+      // register window per channel pair); the 4 partial sums meet in shared memory.  ntaps is padded to a multiple of
+      // 8 with zero taps, so in every unrolled group of 8 taps the new positions sit at fixed offsets 0 .. -6, -8 of
+      // one padded address.
       {
-        const int gq = tid / kPolyGroup, lt = tid % kPolyGroup;
-        const float* G0 = Gf + (2 * gq) * W;  // channel 2 gq; channel 2 gq + 1 sits W words further
-        float part[kPolyPasses][8];
+        static_assert(kPolyPasses <= 2, "earlier passes' partials are parked in the column records (THREADS x 8 floats)");
+        float4* park = reinterpret_cast<float4*>(sm.col);  // free during the FIR; keeps registers for the window
+        float part[8];
   #pragma unroll
         for (int pass = 0; pass < kPolyPasses; pass++) {
-          const int t8 = pass * kPolyPass + 8 * lt;
-          const float4* P4 = reinterpret_cast<const float4*>(Pt) + gq * (ntaps >> 1);  // pair gq: taps (2i, 2i+1)
-          float2 acc[8], w[8];
-          const int q = t8 + ntaps - 1;  // position of output t8 at tap mi = 0 (m = m_lo)
-  #pragma unroll
-          for (int r = 0; r < 8; r++) {
-            acc[r] = make_float2(0.f, 0.f);
-            const int a = (q + r) + ((q + r) >> 3);
-            w[r] = make_float2(G0[a], G0[a + W]);
+          const int it = pass * kPolyThreads + tid, pi = it >> 7, t8 = 8 * (it & 127);
+          poly_fir_item(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, part);
+          if (pass < kPolyPasses - 1) {
+            park[2 * tid] = make_float4(part[0], part[1], part[2], part[3]);
+            park[2 * tid + 1] = make_float4(part[4], part[5], part[6], part[7]);
           }
-          const float* gn = G0 + (q - 1) + ((q - 1) >> 3);  // padded address of position q - 1 (= 6 mod 8)
-          for (int mi = 0; mi < ntaps; mi += 8, gn -= 9, P4 += 4) {
-            const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};  // taps mi .. mi + 7 of channel pair gq
-  #pragma unroll
-            for (int u = 0; u < 8; u++) {  // tap mi + u: output r uses slot (r - u) & 7, then slot (7 - u) & 7 refills
-              const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
-  #pragma unroll
-              for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 7], acc[r]);
-              const int o = u < 7 ? -u : -8;  // the last group's refills read padding: never used
-              w[(7 - u) & 7] = make_float2(gn[o], gn[o + W]);
-            }
-          }
-  #pragma unroll
-          for (int r = 0; r < 8; r++) part[pass][r] = acc[r].x + acc[r].y;
         }
-        __syncthreads();  // every group is done reading G: its planes take the 4 x kPolyTC partial sums
+        __syncthreads();  // every item is done reading G: its planes take the 4 x kPolyTC partial sums
         float* red = Gf;
   #pragma unroll
         for (int pass = 0; pass < kPolyPasses; pass++) {
-          float4* r4 = reinterpret_cast<float4*>(red + gq * kPolyTC + pass * kPolyPass + 8 * lt);
-          r4[0] = make_float4(part[pass][0], part[pass][1], part[pass][2], part[pass][3]);
-          r4[1] = make_float4(part[pass][4], part[pass][5], part[pass][6], part[pass][7]);
+          const int it = pass * kPolyThreads + tid, pi = it >> 7, t8 = 8 * (it & 127);
+          float4* r4 = reinterpret_cast<float4*>(red + pi * kPolyTC + t8);
+          if (pass < kPolyPasses - 1) {
+            r4[0] = park[2 * tid];
+            r4[1] = park[2 * tid + 1];
+          } else {
+            r4[0] = make_float4(part[0], part[1], part[2], part[3]);
+            r4[1] = make_float4(part[4], part[5], part[6], part[7]);
+          }
         }
       }
       __syncthreads();
@@ -899,7 +953,7 @@ static size_t poly_smem_bytes(int ntaps, bool two_word, bool cluster = false) {
   (void)cluster;
   const size_t W = (size_t)poly_w(ntaps);
   return sizeof(PolySmem<THREADS>) + (two_word ? 2 : 1) * kPolyD * W * sizeof(int) +
-         (size_t)ntaps * kPolyD * sizeof(float);
+         (size_t)poly_tab_floats(ntaps, kPolyMaxNear) * sizeof(float);
 }
 
 size_t ism_poly_smem_bytes(int ntaps, bool two_word) { return poly_smem_bytes<512>(ntaps, two_word); }

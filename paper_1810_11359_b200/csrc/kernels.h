@@ -78,8 +78,10 @@ struct IsmArgs {
   unsigned long long tex;  // cudaTextureObject_t
   float texQ, tex_off;     // Q and half + 0.5 (texel centres)
   // polyphase mode (reading R11): delta'(m - phi) = sum_d P[m - mlo][d] T_d(2 phi - 1), m = mlo .. mlo + ntaps - 1
-  const float* poly_P;     // device [ntaps][8]
+  // FIR tables (reading R13, abi.cu poly_fir_tables): far [2][ntaps][2], near [2][nn][2] (taps nmi0 ..), Q [8][8]
+  const float* poly_P;
   int poly_ntaps, poly_mlo;
+  int poly_nmi0, poly_nn;
   int poly_gbz;            // some tile of the call starts in the two-word scheme: zero the fine plane Gb per tile
   int poly_gb;             // set by the launcher: the fine plane Gb is allocated (two-word tiles, guard's last rung)
   int poly_force2;         // test hook (opts.split == -2): every tile uses the two-word scheme

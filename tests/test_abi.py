@@ -191,6 +191,39 @@ def test_poly_table_reproduces_eq6(P, oracle, fs):
         P.poly_table(Tw, 300000.0)  # Tw fs > 1022 taps
 
 
+@pytest.mark.parametrize("fs", [8000.0, 16000.0, 22050.0, 44100.0, 48000.0, 96000.0])
+def test_poly_fir_table_reproduces_eq6(P, oracle, fs):
+    """Reading R13: the rotated, low-rank FIR form the kernel runs (channels G' = Q G; rotated channels 4..7 only
+    on their nn-tap window) reproduces the oracle's Eq. 6 windowed sinc at every integer tap and fractional delay
+    to < 1e-6 of its peak, as the unrotated table does; Q is orthogonal and block diagonal over the parities."""
+    Tw = 4e-3
+    F = P.poly_fir_table(Tw, fs)
+    far, near, Qc, mlo, nmi0, nn = F["far"], F["near"], F["Q"], F["mlo"], F["nmi0"], F["nn"]
+    n = far.shape[1]
+    Q = np.zeros((8, 8))
+    for par in range(2):
+        for k in range(4):
+            for i in range(4):
+                Q[2 * k + par, 2 * i + par] = Qc[par, k, i]
+    assert np.abs(Q @ Q.T - np.eye(8)).max() < 1e-6
+    assert nn % 8 == 0 and nmi0 % 8 == 0 and nn in (16, 24) and nmi0 <= -6 - mlo and nmi0 + nn >= 8 - mlo
+    Pr = np.zeros((n, 8))  # rotated coefficients per tap
+    Pr[:, 0:4] = far.transpose(1, 0, 2).reshape(n, 4)
+    Pr[nmi0:nmi0 + nn, 4:8] = near.transpose(1, 0, 2).reshape(nn, 4)
+    rng = np.random.default_rng(int(fs) + 1)
+    phi = np.concatenate([rng.random(200), [0.0, 1e-7, 0.5, 1 - 6e-8]])
+    T = np.cos(np.arange(8)[:, None] * np.arccos(2 * phi - 1)[None, :])  # T_d(2 phi - 1)
+    approx = Pr @ (Q @ T)                                                  # [tap, phi]
+    worst = 0.0
+    for mi in range(n):
+        m = mlo + mi
+        exact = np.array([oracle.windowed_sinc((m - f) / fs, Tw, fs / 2) for f in phi])
+        worst = max(worst, float(np.max(np.abs(approx[mi] - exact))))
+    assert worst < 1e-6, worst
+    tab, mlo0 = P.poly_table(Tw, fs)  # the same expansion: unrotated channels = Q^T rotated
+    assert mlo0 == mlo and tab.shape[0] == n
+
+
 def test_batch_extent_on_host(P):
     """gpurir_batch_extent (the binding's output-size check of a batch call): max(out_offset + ceil(Tmax fs)),
     reading C9 / R1, computed on the host without a device; -1 for invalid arguments."""
