@@ -50,7 +50,6 @@ ISSUE_SLOTS_PER_TAP = 13  # algorithmic FP32-pipe issue slots 
 # Polyphase kernel (mode poly, reading R11 / §5.5): algorithmic lane-ops per in-range image (Eqs. 1-4:
 # 13, the 8 Chebyshev channel values: 14, their 8 deposits) and per output sample (the FIR: 2H taps x 8 MACs)
 POLY_OPS_PER_IMAGE = 35
-POLY_CHANNELS = 8
 
 
 def workload_name(mode="fp32"):
@@ -533,14 +532,16 @@ def main():
     pk, pk_kind = peaks()
     f_clk = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
     issue_peak = 148 * 128 * f_clk  # FP32 lane issue slots / s (B200_PROFILING.md unit counts)
-    ntaps_fir = int(round(2 * H))
-    poly_ops = imgs_launch * POLY_OPS_PER_IMAGE + M_PER_GPU * nISM * ntaps_fir * POLY_CHANNELS
+    fir = P.poly_fir_table(4e-3, sc.fs)  # the FIR the kernel runs (reading R13): 4 ntaps + 4 nn MACs per output
+    fir_macs = 4 * fir["far"].shape[1] + 4 * fir["nn"]
+    poly_ops = imgs_launch * POLY_OPS_PER_IMAGE + M_PER_GPU * nISM * fir_macs
     if args.mode == "poly":
         achieved = poly_ops / ism_avg_s
-        basis = (f"{POLY_OPS_PER_IMAGE} lane-ops per in-range image x {imgs_launch:.4g} images + {ntaps_fir} taps x "
-                 f"{POLY_CHANNELS} channels per output sample x {M_PER_GPU * nISM} samples per launch (exact image "
-                 f"count on 256 sampled receivers); peak = 148 SM x 128 lanes x {f_clk / 1e6:.0f} MHz "
-                 f"({pk_kind} sm_max_mhz); the kernel's time includes the fused diffuse tail, not counted as work")
+        basis = (f"{POLY_OPS_PER_IMAGE} lane-ops per in-range image x {imgs_launch:.4g} images + {fir_macs} MACs per "
+                 f"output sample (rotated low-rank FIR, R13: 4 channels x {fir['far'].shape[1]} taps + 4 x {fir['nn']}) "
+                 f"x {M_PER_GPU * nISM} samples per launch (exact image count on 256 sampled receivers); peak = 148 SM x "
+                 f"128 lanes x {f_clk / 1e6:.0f} MHz ({pk_kind} sm_max_mhz); the kernel's time includes the fused "
+                 f"diffuse tail, not counted as work")
         kname = "ism_poly_kernel"
     else:
         achieved = taps_launch * ISSUE_SLOTS_PER_TAP / ism_avg_s
@@ -612,12 +613,13 @@ def main():
         "paper_context": "gpuRIR V100 fp32, 1024 RIRs, T60 0.7 s diffuse: 195.69 ms = 5,233 RIRs/s (P:362); "
                          "different fs/positions/pattern, context only",
     }
+    # the timed step's RIRs for the parity leg, read before the direct-kernel A/B below reuses `out`
+    rows = out[0, :8192].cpu().numpy() if not args.no_cpu_baseline and world == 1 else None
     if args.mode == "poly":  # the direct-tap fp32 kernel on the same step, for the A/B (not part of `value`)
         line["direct_fp32"] = direct_ab(P, torch, sc, beta, nb, src, rcv, orv, base, out, flush, stream,
                                         taps_launch, issue_peak)
     line["lib"] = lib
-    if not args.no_cpu_baseline and world == 1:
-        rows = out[0, :8192].cpu().numpy()
+    if rows is not None:
         line["cpu_baseline"], line["parity"] = cpu_baseline(W.cfg3(M_PER_GPU, "diffuse"), gpu_rows=rows)
     if not args.no_sweep and world == 1:
         line["sweep"] = sweep(P, torch, dev, flush)
@@ -963,8 +965,9 @@ def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev, lib):
     taps = float(np.mean([t for t, _ in ti]))
     taps_launch = taps * n_pts * n_mic
     if args.mode == "poly":
-        ism_work = (float(np.mean([i for _, i in ti])) * POLY_OPS_PER_IMAGE + nISM * round(2 * H) * POLY_CHANNELS) \
-            * n_pts * n_mic
+        fir = P.poly_fir_table(4e-3, sc.fs)  # the FIR the kernel runs (reading R13)
+        fir_macs = 4 * fir["far"].shape[1] + 4 * fir["nn"]
+        ism_work = (float(np.mean([i for _, i in ti])) * POLY_OPS_PER_IMAGE + nISM * fir_macs) * n_pts * n_mic
     else:
         ism_work = taps_launch * ISSUE_SLOTS_PER_TAP
     ism_ach = ism_work / (ism_ms / 1000.0)
@@ -975,8 +978,8 @@ def run_trajectory(args, P, torch, dev, rank, world, dist, local_dev, lib):
     roof_ism = {"bound": "alu", "achieved": ism_ach / 1e12, "peak": issue_peak / 1e12,
                 "unit": "T FP32-lane-issue-slots/s", "frac": ism_ach / issue_peak, "traffic": None,
                 "kernel": "ism_poly_kernel" if args.mode == "poly" else "ism_ws_kernel<0>",
-                "basis": (f"{POLY_OPS_PER_IMAGE} lane-ops per in-range image + {round(2 * H)} taps x {POLY_CHANNELS} "
-                          f"channels per output sample" if args.mode == "poly" else
+                "basis": (f"{POLY_OPS_PER_IMAGE} lane-ops per in-range image + {fir_macs} MACs per output sample "
+                          f"(rotated low-rank FIR, R13)" if args.mode == "poly" else
                           f"{ISSUE_SLOTS_PER_TAP} issue slots per in-window tap x {taps_launch:.4g} taps per launch")
                 + f" (exact counts on {len(pairs)} sampled pairs)"}
     roof_tr = traj_roofline(n_sig, n_pts, n_mic, nS, tr_ms, pk, pk_kind)

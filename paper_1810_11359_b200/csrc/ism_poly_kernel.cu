@@ -299,6 +299,12 @@ __host__ __device__ constexpr int poly_tab_floats(int ntaps, int nn) { return 4 
 __device__ __forceinline__ float poly_rot1(const float* q, float a, float b, float c, float d) {
   return fmaf(q[3], d, fmaf(q[2], c, fmaf(q[1], b, q[0] * a)));
 }
+// the same for two positions at once (FMUL2 / FFMA2: each lane rounds exactly as poly_rot1)
+__device__ __forceinline__ float2 poly_rot2(const float* q, float2 a, float2 b, float2 c, float2 d) {
+  const float2 q0 = make_float2(q[0], q[0]), q1 = make_float2(q[1], q[1]), q2 = make_float2(q[2], q[2]),
+               q3 = make_float2(q[3], q[3]);
+  return __ffma2_rn(q3, d, __ffma2_rn(q2, c, __ffma2_rn(q1, b, __fmul2_rn(q0, a))));
+}
 
 // One FIR item (reading R13): outputs t8 .. t8 + 7 of partial pi = 2 s + h — the far channel pair s (rotated
 // channels 2 s, 2 s + 1) over tap half h of its ntaps taps, then the near pair s (channels 4 + 2 s, 5 + 2 s) over
@@ -865,9 +871,11 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
   #pragma unroll
             for (int k = 0; k < 4; k++) {
               const float* qk = Qr + (par * 4 + k) * 4;
-              reinterpret_cast<float4*>(Gf)[(2 * k + par) * w4 + q] =
-                  make_float4(poly_rot1(qk, v[0].x, v[1].x, v[2].x, v[3].x), poly_rot1(qk, v[0].y, v[1].y, v[2].y, v[3].y),
-                              poly_rot1(qk, v[0].z, v[1].z, v[2].z, v[3].z), poly_rot1(qk, v[0].w, v[1].w, v[2].w, v[3].w));
+              const float2 lo = poly_rot2(qk, make_float2(v[0].x, v[0].y), make_float2(v[1].x, v[1].y),
+                                          make_float2(v[2].x, v[2].y), make_float2(v[3].x, v[3].y));
+              const float2 hi = poly_rot2(qk, make_float2(v[0].z, v[0].w), make_float2(v[1].z, v[1].w),
+                                          make_float2(v[2].z, v[2].w), make_float2(v[3].z, v[3].w));
+              reinterpret_cast<float4*>(Gf)[(2 * k + par) * w4 + q] = make_float4(lo.x, lo.y, hi.x, hi.y);
             }
           }
         }
