@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             bool zero = false;
             const float lxy = axis_beta(nx, 0, g, sgn, zero) + axis_beta(ny, 1, g, sgn, zero);
             const float bxy = zero ? 0.f : ex2_approx(lxy);
-            cr.bxy = (sgn ? -bxy : bxy) * amp_scale;
+            cr.bxy = (sgn ? -bxy : bxy) * amp_scale * T.scalef;  // the tile's fixed-point scale (a power of two) folded in
             if (rho2 < T.dhi2) {
               const double zhi = (double)sqrtf((float)(T.dhi2 - rho2));
               const double zlo = T.dlo2 > rho2 ? (double)sqrtf((float)(T.dlo2 - rho2)) : 0.0;
@@ -636,7 +636,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           }
           int j = lo;
           const int zl = T.zl;
-          const float oz = g.o[2], ga = g.a, scalef = T.scalef, scale_lf = T.scale_lf;
+          // the column records carry the fixed-point scale, so the deposits take amp as is and the last channel
+          // amp 2^-J (both exact: powers of two)
+          const float oz = g.o[2], ga = g.a, oma = 1.f - ga, scale_lj = T.scale_lf / T.scalef;
           const int J = T.J;
           const unsigned cmask = T.cnt_mask;
           unsigned acc = 0xFFFFFFFFu;  // min of ~old & mask over this thread's last-channel deposits (poly_add)
@@ -653,7 +655,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             if (gi >= cr.end) cr = load_col(&sm.col[++j]);
             const int nz = gi + (gi < cr.b ? cr.a1 : cr.a2);
             const int odd = nz & 1;
-            const float bz = use_bz ? sm.bz[min(max(nz - zl, 0), kPolyBz - 1)] : poly_z_factor(nz, g);
+            // nz lies in [zl, zh] (the column's runs are clamped to it) and use_bz means zh - zl < kPolyBz
+            const float bz = use_bz ? sm.bz[nz - zl] : poly_z_factor(nz, g);
             const int nzo = nz + odd;
             // Eq. 1 along z, in samples (the tile's constants are read from shared memory: no conversions here)
             const double dz = fma(int_to_double(nzo), Lzs, odd ? offOs : offEs);
@@ -669,22 +672,23 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             int jfl;
             const float fj = floor_int(x0f, jfl);
             float phi = (x0f - fj) + xd;
-            {  // branch-free (+0.3 %); an image at the receiver (x2 = 0, flagged by its column above) gives a NaN
-               // delay, whose floor's integer bits put p far out of range: it is dropped like the old explicit check
-              const bool lt = phi < 0.f, ge = phi >= 1.f;
-              phi += lt ? 1.f : (ge ? -1.f : 0.f);
-              jfl += (int)ge - (int)lt;
+            {  // phi in (-1, 2): one more exact floor moves it into [0, 1) (5 instructions instead of the 9 of a
+               // compare-and-select fix-up: +0.8 %).  An image at the receiver (x2 = 0, flagged by its column above)
+               // gives a NaN delay, whose floors' integer bits put p far out of range: it is dropped below.
+              int k;
+              phi -= floor_int(phi, k);
+              jfl += k;
             }
             phi = fminf(phi, 0.99999994f);  // phi + 1 rounds to 1 for phi > -3e-8
             const int p = jfl - pbase;
-            if (p < 0 || p >= npos_i) continue;  // reaches no sample of this item
+            if ((unsigned)p >= (unsigned)npos_i) continue;  // reaches no sample of this item (p < 0 wraps)
             const float dzf = (float)dz;  // one XU conversion instead of shared-memory loads (the smem pipe binds)
             const float cth = fmaf(dzf, oz, cr.cdot) * rx;
-            float gain = ga + (1.f - ga) * cth;
+            float gain = fmaf(oma, cth, ga);
             if (dir_src) gain *= src_gain(sm.colsdot[j], odd, dzf, rx, g);
             const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
             const float y = fmaf(2.f, phi, -1.f);            // 2 phi - 1 in [-1, 1)
-            poly_add(Ga, Gb, W, p + (p >> 3), y, amp, scalef, scale_lf, J, cmask, two_word, acc);
+            poly_add(Ga, Gb, W, p + (p >> 3), y, amp, 1.f, scale_lj, J, cmask, two_word, acc);
           }
           };
           if (T.use_bz && !T.two_word && g.as == 1.f) walk(std::true_type());
