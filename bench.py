@@ -196,7 +196,7 @@ def oracle_rate(sc, beta, nb, n_rir, base_index=0, nthreads=0):
     return n_rir / dt, dt, h
 
 
-def cpu_baseline(sc, gpu_rows=None, budget_s=15.0):
+def cpu_baseline(sc, gpu_rows=None, budget_s=15.0, kernel=None):
     """The oracle (oracle/, -O3 -march=native built on this host) on the host cores, on a bounded sample of the
     workload: all cores, then one thread.  With gpu_rows (the timed step's output rows [M, nS] as a host array)
     it also returns the step's parity against the oracle RIRs it just computed (reading C20)."""
@@ -227,7 +227,8 @@ def cpu_baseline(sc, gpu_rows=None, budget_s=15.0):
         err = np.abs(g - r_).max(axis=1) / np.where(peak > 0, peak, 1.0)
         parity = {"max_err_over_peak": float(err.max()), "median_err_over_peak": float(np.median(err)), "n": n,
                   "tol": 1e-4, "ok": bool(err.max() <= 1e-4),
-                  "what": f"the timed step's RIRs 0..{n - 1} (all samples, tail included) vs the oracle's (C20)"}
+                  "what": f"the timed step's RIRs 0..{n - 1} (all samples, tail included) vs the oracle's (C20)",
+                  "kernel": kernel}
     return out, parity
 
 
@@ -620,7 +621,7 @@ def main():
                                         taps_launch, issue_peak)
     line["lib"] = lib
     if rows is not None:
-        line["cpu_baseline"], line["parity"] = cpu_baseline(W.cfg3(M_PER_GPU, "diffuse"), gpu_rows=rows)
+        line["cpu_baseline"], line["parity"] = cpu_baseline(W.cfg3(M_PER_GPU, "diffuse"), gpu_rows=rows, kernel=kname)
     if not args.no_sweep and world == 1:
         line["sweep"] = sweep(P, torch, dev, flush)
     print(json.dumps(line), flush=True)
