@@ -208,6 +208,17 @@ __device__ __forceinline__ float poly_z_factor(int nz, const RirGeom& g) {
   return sgn ? -v : v;
 }
 
+// The same for a single-room call straight from the call's arguments (no RirGeom needed: the z factor reads
+// only the z walls' log2 |beta|, signs and zero flags)
+__device__ __forceinline__ float poly_z_factor_args(int nz, const IsmArgs& A) {
+  RirGeom g;
+  g.lb[4] = A.lb[4];
+  g.lb[5] = A.lb[5];
+  g.neg = A.neg;
+  g.zero = A.zero;
+  return poly_z_factor(nz, g);
+}
+
 // One image's 8 channel values A T_d(y), d = 0..7, added to G[.][p] as integers v = round(A T_d 2^s).  The
 // tile's scale bounds |A| by its closest possible image, so |v| <= 2^bits; sums of integers commute, so G does
 // not depend on the order in which images arrive (deterministic, shard-invariant).
@@ -405,6 +416,10 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       for (int i = tid - 32; i < n4; i += kPolyThreads - 32) reinterpret_cast<int4*>(Ga)[i] = make_int4(0, 0, 0, 0);
       if (both)
         for (int i = tid - 32; i < n4; i += kPolyThreads - 32) reinterpret_cast<int4*>(Gb)[i] = make_int4(0, 0, 0, 0);
+      // a single-room call's z-factor table depends only on the call's arguments: built here, beside thread 0's
+      // setup, instead of after it (the cluster items of small calls build it for their one item: -0.5 us)
+      if (!A.jobs && !bz_ready && A.nb[2] <= kPolyBz)
+        for (int i = tid - 32; i < A.nb[2]; i += kPolyThreads - 32) sm.bz[i] = poly_z_factor_args(i - A.nb[2] / 2, A);
     } else if (tid == 0) {
       long long wi;
       int sub = 0, nsub = 1;  // this cluster's output sub-range of the item, of nsub
@@ -546,7 +561,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     const PolyTile& T = sm.ti;
     const RirGeom& g = T.g;
     // the z factors depend only on the room: once per CTA for a single-room call, per item for a batch of rooms
-    if (T.use_bz && (A.jobs || !bz_ready))
+    // (single-room calls with nb_z <= kPolyBz: built before the barrier above, T.zl = -(nb_z / 2))
+    if (T.use_bz && (A.jobs || !(bz_ready || A.nb[2] <= kPolyBz)))
       for (int i = tid; i <= T.zh - T.zl; i += kPolyThreads) sm.bz[i] = poly_z_factor(T.zl + i, g);
     bz_ready = true;
 
