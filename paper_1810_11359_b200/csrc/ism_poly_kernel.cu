@@ -73,8 +73,10 @@ template <int THREADS> struct PolyCfg {
   static constexpr int kCols = THREADS;         // lattice columns per enumeration batch
   static constexpr int kGroup = THREADS / 4;    // FIR threads per channel pair
   static constexpr int kPass = 8 * kGroup;      // outputs per FIR pass (8 per thread)
-  static constexpr int kPasses = kPolyTC / kPass;
-  static_assert(THREADS >= 1024 || kPolyTC % kPass == 0, "FIR passes of 4 channel-pair groups x 8 outputs per thread");  // 1024: cluster items only
+  // FIR items (4 partials x kPolyTC / 8 blocks of 8 outputs) per thread: 2 (256 threads), 1 (512), 1 with half the
+  // threads idle (1024: persistent CTAs of calls with at most one item per SM, and cluster items)
+  static constexpr int kPasses = THREADS >= 1024 ? 1 : kPolyTC / kPass;
+  static_assert(THREADS >= 1024 || kPolyTC % kPass == 0, "FIR passes of 4 channel-pair groups x 8 outputs per thread");
 };
 
 // One nonempty lattice column of a batch (32 B, two 16-B loads; lengths in samples, x fs / c).  Its
@@ -930,9 +932,10 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         float4* park = reinterpret_cast<float4*>(sm.col);  // free during the FIR; keeps registers for the window
         float part[8];
   #pragma unroll
+        constexpr int kItems = 4 * (kPolyTC / 8);  // (1024-thread CTAs: threads >= kItems idle here)
         for (int pass = 0; pass < kPolyPasses; pass++) {
           const int it = pass * kPolyThreads + tid, pi = it >> 7, t8 = 8 * (it & 127);
-          poly_fir_item(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, part);
+          if (it < kItems) poly_fir_item(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, part);
           if (pass < kPolyPasses - 1) {
             park[2 * tid] = make_float4(part[0], part[1], part[2], part[3]);
             park[2 * tid + 1] = make_float4(part[4], part[5], part[6], part[7]);
@@ -943,6 +946,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
   #pragma unroll
         for (int pass = 0; pass < kPolyPasses; pass++) {
           const int it = pass * kPolyThreads + tid, pi = it >> 7, t8 = 8 * (it & 127);
+          if (it >= kItems) break;
           float4* r4 = reinterpret_cast<float4*>(red + pi * kPolyTC + t8);
           if (pass < kPolyPasses - 1) {
             r4[0] = park[2 * tid];
@@ -1099,7 +1103,10 @@ int ism_poly_cluster_size(long long n_work, int num_sms, int split, int ntaps, b
   }();
   if (threads) *threads = 512;
   if (split > 0) return split;
-  if (split < 0 || n_work >= 2LL * num_sms) return 0;
+  // cluster items only for the smallest calls: from ~48 items (16 receivers of config 3 (i)) one persistent CTA per
+  // item is faster — one heavy tile per CTA costs ~37 us, while clusters of 4-8 CTAs per tile pay their exchange and
+  // run in several waves (graph-timed, tools/mid_calls.py: 24 receivers 50.5 -> 37.1 us, 96: 104 -> 54 us)
+  if (split < 0 || n_work >= 2LL * num_sms || n_work > kPolyClusterMaxItems) return 0;
   int S = 4;
   while (S < 16 && n_work * S < 2LL * num_sms) S *= 2;
   // items whose output ranges the planner may split (poly_plan_subs) get clusters of 8: sub-ranges add the
@@ -1198,6 +1205,13 @@ cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, in
   if (!two_word && 4 * s256 <= 224 * 1024 && n_work >= 16LL * num_sms) {
     B.poly_gb = 0;
     return launch_poly<256>(B, n_work, counter, s256, num_sms, stream);
+  }
+  // at most one item per SM: one 1024-thread CTA per item (twice the warps of a 512-thread CTA on each tile; the fine
+  // plane always fits), the same bits as every other shape
+  static const bool no1024 = getenv("GPURIR_POLY_NO1024") != nullptr;  // A/B switch
+  if (n_work <= num_sms && !no1024) {
+    B.poly_gb = 1;
+    return launch_poly<1024>(B, n_work, counter, poly_smem_bytes<1024>(A.poly_ntaps, true), num_sms, stream);
   }
   // 512-thread CTAs carry the fine plane whenever two of them still fit an SM with it (the guard's redo)
   const size_t s1 = poly_smem_bytes<512>(A.poly_ntaps, false), s2 = poly_smem_bytes<512>(A.poly_ntaps, true);

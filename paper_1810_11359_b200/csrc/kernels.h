@@ -8,6 +8,7 @@
 namespace gpurir {
 
 constexpr int kPolyMaxItems = 64;  // polyphase small calls: work items whose output range may be split
+constexpr int kPolyClusterMaxItems = 40;  // polyphase calls of at most this many (tile, RIR) items run cluster items
 
 // One RIR of a multi-room batch (device copy built by the host planner).
 struct alignas(16) BatchJob {
