@@ -931,11 +931,12 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         static_assert(kPolyPasses <= 2, "earlier passes' partials are parked in the column records (THREADS x 8 floats)");
         float4* park = reinterpret_cast<float4*>(sm.col);  // free during the FIR; keeps registers for the window
         float part[8];
-  #pragma unroll
         constexpr int kItems = 4 * (kPolyTC / 8);  // (1024-thread CTAs: threads >= kItems idle here)
+        constexpr bool kIdle = kPolyThreads * kPolyPasses > kItems;
+  #pragma unroll
         for (int pass = 0; pass < kPolyPasses; pass++) {
           const int it = pass * kPolyThreads + tid, pi = it >> 7, t8 = 8 * (it & 127);
-          if (it < kItems) poly_fir_item(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, part);
+          if (!kIdle || it < kItems) poly_fir_item(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, part);
           if (pass < kPolyPasses - 1) {
             park[2 * tid] = make_float4(part[0], part[1], part[2], part[3]);
             park[2 * tid + 1] = make_float4(part[4], part[5], part[6], part[7]);
@@ -946,7 +947,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
   #pragma unroll
         for (int pass = 0; pass < kPolyPasses; pass++) {
           const int it = pass * kPolyThreads + tid, pi = it >> 7, t8 = 8 * (it & 127);
-          if (it >= kItems) break;
+          if (kIdle && it >= kItems) break;
           float4* r4 = reinterpret_cast<float4*>(red + pi * kPolyTC + t8);
           if (pass < kPolyPasses - 1) {
             r4[0] = park[2 * tid];
@@ -1202,7 +1203,13 @@ cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, in
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   const size_t s256 = poly_smem_bytes<256>(A.poly_ntaps, false);
-  if (!two_word && 4 * s256 <= 224 * 1024 && n_work >= 16LL * num_sms) {
+  // 256-thread CTAs (4 per SM) from 7 items per SM: graph-timed on config 3 (i) (tools/mid_calls.py --large), 7.8 items
+  // per SM 105 vs 109 us, 15.6: 193 vs 208 us, but 5.2: 86 vs 79 us (fewer, wider CTAs keep the heavy tiles moving)
+  static const long long min256 = [] {  // GPURIR_POLY_MIN256: A/B of the threshold (items per SM)
+    const char* e = getenv("GPURIR_POLY_MIN256");
+    return e ? atoll(e) : 7LL;
+  }();
+  if (!two_word && 4 * s256 <= 224 * 1024 && n_work >= min256 * num_sms) {
     B.poly_gb = 0;
     return launch_poly<256>(B, n_work, counter, s256, num_sms, stream);
   }

@@ -54,6 +54,8 @@ def timed(sc, split, reps=20):
 
 GRAPH = "--graph" in sys.argv
 Ms = (1, 2, 4, 8, 12, 16, 24, 32, 48, 64, 96, 128, 192, 256) if GRAPH else (4, 8, 16, 32, 48, 64, 96, 128, 192, 256)
+if "--large" in sys.argv:
+    Ms = (64, 96, 128, 192, 256, 384, 512, 768, 1024, 2048)
 for M in Ms:
     sc = W.cfg3(M, "diffuse")
     ta, oa = timed(sc, 0)
