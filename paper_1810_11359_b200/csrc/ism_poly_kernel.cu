@@ -137,7 +137,7 @@ __device__ __noinline__ void poly_fused_tail(PolyTile& T, const float* red, cons
   const int nISM = T.te, nS = T.tail_nS;
   if (tid < 32) {
     float env0, alpha, rho;
-    const int t0 = T.t0;
+    const int t0 = T.ot0;  // red holds the item's outputs (the last sub-range of a split tile holds the window)
     if (hg)
       tail_envelope([&](int k) { return hg[k]; }, nISM, win, T.x_dp, T.tail_kappa, tid, env0, alpha, rho);
     else
@@ -173,6 +173,19 @@ struct alignas(16) PolySmem {
   int pf_valid;
   float pf_in[12];
 };
+
+// Work entry w of a call with a split plan (IsmArgs::poly_cmap, poly_plan_subs): its item and output sub-range
+__device__ __forceinline__ long long poly_decode(const IsmArgs& A, long long w, int& sub, int& nsub) {
+  if (A.poly_nitems <= 0) {
+    sub = 0;
+    nsub = 1;
+    return w;
+  }
+  const int cm = A.poly_cmap[w];
+  sub = (cm >> 8) & 0xF;
+  nsub = 1 << (cm >> 12);
+  return cm & 0xFF;
+}
 
 // exact q = n / d, r = n % d (0 <= n < 2^53, d >= 1) from a host reciprocal: the fp64 estimate is off by at most one
 __device__ __forceinline__ long long poly_divmod(long long n, long long d, double inv_d, long long& r) {
@@ -425,28 +438,26 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
     } else if (tid == 0) {
       long long wi;
       int sub = 0, nsub = 1;  // this cluster's output sub-range of the item, of nsub
+      long long w;  // the call's work entry: a cluster, or the queue's next entry
       if (CL) {
-        const int ci = (int)(blockIdx.x / S);
-        if (A.poly_nitems > 0) {  // the last item i with poly_first[i] <= ci
-          int lo = 0, hi = A.poly_nitems - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if ((int)A.poly_first[mid] <= ci) lo = mid; else hi = mid - 1;
-          }
-          wi = lo;
-          sub = ci - (int)A.poly_first[lo];
-          nsub = (int)A.poly_first[lo + 1] - (int)A.poly_first[lo];
-        } else {
-          wi = ci;
-        }
+        w = (long long)(blockIdx.x / S);
       } else if (sm.pf_valid) {  // prefetched during the previous item's filter
         asm volatile("cp.async.wait_all;\n" ::: "memory");
-        wi = sm.pf_wi;
+        w = sm.pf_wi;
       } else {
-        wi = atomicAdd(work_counter, 1);
+        w = atomicAdd(work_counter, 1);
       }
       PolyTile& T = sm.ti;
-      T.next = wi < n_work;
+      if (CL) {  // every cluster has an entry; n_work counts items
+        wi = poly_decode(A, w, sub, nsub);
+        T.next = wi < n_work;
+      } else if constexpr (THREADS >= 1024) {  // n_work counts queue entries (split plans: calls of <= 1 item per SM)
+        T.next = w < n_work;
+        wi = T.next ? poly_decode(A, w, sub, nsub) : w;  // the item and this entry's output sub-range
+      } else {   // 256- and 512-thread CTAs: one entry per item
+        T.next = w < n_work;
+        wi = w;
+      }
       PS_MARK(2);
       if (wi < n_work) {
         int m, tile, nISM;
@@ -909,7 +920,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         sm.pf_valid = 1;
         if (!A.jobs && wi_next < n_work) {
           long long rm, mr;
-          (void)poly_divmod(wi_next, A.M, A.invM, rm);
+          int s_, n_;
+          (void)poly_divmod(THREADS >= 1024 ? poly_decode(A, wi_next, s_, n_) : wi_next, A.M, A.invM, rm);
           const int ms = (int)poly_divmod(rm, A.M_rcv, A.invMrcv, mr);
           for (int k = 0; k < 3; k++) {
             poly_cp4(&sm.pf_in[k], A.pos_src + 3 * ms + k);
@@ -963,8 +975,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         const float* red = Gf;
   #pragma unroll
         for (int h = 0; h < kPolyTC / kPolyThreads; h++) {
-          const int t = tid + h * kPolyThreads, k = T.t0 + t;
-          if (k < T.te)
+          // the item's outputs: a sub-range of the tile under a split plan (1024-thread CTAs), else the whole tile
+          const int t = tid + h * kPolyThreads, k = (THREADS >= 1024 ? T.ot0 : T.t0) + t;
+          if (k < (THREADS >= 1024 ? T.ote : T.te))
             A.out[T.row + k] = (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
         }
         if (T.tail)
@@ -1164,10 +1177,13 @@ static long long poly_plan_subs(IsmArgs& B, long long n_work, long long cmax) {
     total += ns[(size_t)best];
     ns[(size_t)best] *= 2;
   }
+  if (total > kPolyMaxSubItems) return n_work;  // (cannot happen: cmax is at most one wave) no plan
   int first = 0;
   for (long long wi = 0; wi < n_work; wi++) {
     B.poly_first[wi] = (unsigned short)first;
-    first += ns[(size_t)wi];
+    const int k = ns[(size_t)wi], lg = k == 4 ? 2 : k == 2 ? 1 : 0;
+    for (int sub = 0; sub < k; sub++) B.poly_cmap[first + sub] = (unsigned short)(wi | sub << 8 | lg << 12);
+    first += k;
   }
   B.poly_first[n_work] = (unsigned short)first;
   B.poly_nitems = (int)n_work;
@@ -1218,7 +1234,13 @@ cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, in
   static const bool no1024 = getenv("GPURIR_POLY_NO1024") != nullptr;  // A/B switch
   if (n_work <= num_sms && !no1024) {
     B.poly_gb = 1;
-    return launch_poly<1024>(B, n_work, counter, poly_smem_bytes<1024>(A.poly_ntaps, true), num_sms, stream);
+    // heavy tiles' output ranges split over the idle SMs (as for cluster items; each part its own CTA and queue
+    // entry, enumerating only its thin shell of images, with the whole tile's fixed-point format: the same bits)
+    static const bool nosub = getenv("GPURIR_POLY_NOSUB") != nullptr;  // A/B switch
+    long long n_entries = n_work;
+    B.poly_nitems = 0;
+    if (split == 0 && !A.jobs && n_work <= kPolyMaxItems && !nosub) n_entries = poly_plan_subs(B, n_work, num_sms);
+    return launch_poly<1024>(B, n_entries, counter, poly_smem_bytes<1024>(A.poly_ntaps, true), num_sms, stream);
   }
   // 512-thread CTAs carry the fine plane whenever two of them still fit an SM with it (the guard's redo)
   const size_t s1 = poly_smem_bytes<512>(A.poly_ntaps, false), s2 = poly_smem_bytes<512>(A.poly_ntaps, true);

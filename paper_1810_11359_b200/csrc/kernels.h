@@ -7,7 +7,8 @@
 
 namespace gpurir {
 
-constexpr int kPolyMaxItems = 64;  // polyphase small calls: work items whose output range may be split
+constexpr int kPolyMaxItems = 160;  // polyphase calls whose work items' output ranges may be split (<= 1 item per SM)
+constexpr int kPolyMaxSubItems = 160;  // the split plan's (item, sub-range) entries: at most one wave
 constexpr int kPolyClusterMaxItems = 40;  // polyphase calls of at most this many (tile, RIR) items run cluster items
 
 // One RIR of a multi-room batch (device copy built by the host planner).
@@ -105,6 +106,8 @@ struct IsmArgs {
   // (= tile x RIR work item) owns clusters [poly_first[i], poly_first[i + 1]); poly_nitems = 0: one cluster each
   int poly_nitems;
   unsigned short poly_first[kPolyMaxItems + 1];
+  // the same plan per cluster (cluster items) or per queue entry (persistent CTAs): item | sub << 8 | log2(nsub) << 12
+  unsigned short poly_cmap[kPolyMaxSubItems];
 };
 
 struct TailArgs {
