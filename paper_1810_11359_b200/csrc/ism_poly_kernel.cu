@@ -1117,10 +1117,14 @@ int ism_poly_cluster_size(long long n_work, int num_sms, int split, int ntaps, b
   }();
   if (threads) *threads = 512;
   if (split > 0) return split;
-  // cluster items only for the smallest calls: from ~48 items (16 receivers of config 3 (i)) one persistent CTA per
-  // item is faster — one heavy tile per CTA costs ~37 us, while clusters of 4-8 CTAs per tile pay their exchange and
-  // run in several waves (graph-timed, tools/mid_calls.py: 24 receivers 50.5 -> 37.1 us, 96: 104 -> 54 us)
-  if (split < 0 || n_work >= 2LL * num_sms || n_work > kPolyClusterMaxItems) return 0;
+  // cluster items only for the smallest calls: from ~32 items persistent CTAs (one per item, heavy tiles' output ranges
+  // split over the idle SMs) are faster, while clusters of 4-8 CTAs per tile pay their exchange and run in several
+  // waves (graph-timed, tools/mid_calls.py: 8 receivers of config 3 (i) 19.9 vs 26.3 us, 12: 30.0 vs 25.8 us)
+  static const long long cl_max = [] {  // GPURIR_POLY_CL_MAX: A/B of the threshold
+    const char* e = getenv("GPURIR_POLY_CL_MAX");
+    return e ? atoll(e) : (long long)kPolyClusterMaxItems;
+  }();
+  if (split < 0 || n_work >= 2LL * num_sms || n_work > cl_max) return 0;
   int S = 4;
   while (S < 16 && n_work * S < 2LL * num_sms) S *= 2;
   // items whose output ranges the planner may split (poly_plan_subs) get clusters of 8: sub-ranges add the

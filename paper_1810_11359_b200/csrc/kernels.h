@@ -9,7 +9,7 @@ namespace gpurir {
 
 constexpr int kPolyMaxItems = 160;  // polyphase calls whose work items' output ranges may be split (<= 1 item per SM)
 constexpr int kPolyMaxSubItems = 160;  // the split plan's (item, sub-range) entries: at most one wave
-constexpr int kPolyClusterMaxItems = 40;  // polyphase calls of at most this many (tile, RIR) items run cluster items
+constexpr int kPolyClusterMaxItems = 32;  // polyphase calls of at most this many (tile, RIR) items run cluster items
 
 // One RIR of a multi-room batch (device copy built by the host planner).
 struct alignas(16) BatchJob {
