@@ -182,9 +182,9 @@ __device__ __forceinline__ long long poly_decode(const IsmArgs& A, long long w, 
     return w;
   }
   const int cm = A.poly_cmap[w];
-  sub = (cm >> 8) & 0xF;
+  sub = (cm >> 10) & 3;
   nsub = 1 << (cm >> 12);
-  return cm & 0xFF;
+  return cm & 0x3FF;
 }
 
 // exact q = n / d, r = n % d (0 <= n < 2^53, d >= 1) from a host reciprocal: the fp64 estimate is off by at most one
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       if (CL) {  // every cluster has an entry; n_work counts items
         wi = poly_decode(A, w, sub, nsub);
         T.next = wi < n_work;
-      } else if constexpr (THREADS >= 1024) {  // n_work counts queue entries (split plans: calls of <= 1 item per SM)
+      } else if constexpr (THREADS >= 512) {  // n_work counts queue entries (split plans: calls of <= 2 items per SM)
         T.next = w < n_work;
         wi = T.next ? poly_decode(A, w, sub, nsub) : w;  // the item and this entry's output sub-range
       } else {   // 256- and 512-thread CTAs: one entry per item
@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         if (!A.jobs && wi_next < n_work) {
           long long rm, mr;
           int s_, n_;
-          (void)poly_divmod(THREADS >= 1024 ? poly_decode(A, wi_next, s_, n_) : wi_next, A.M, A.invM, rm);
+          (void)poly_divmod(THREADS >= 512 ? poly_decode(A, wi_next, s_, n_) : wi_next, A.M, A.invM, rm);
           const int ms = (int)poly_divmod(rm, A.M_rcv, A.invMrcv, mr);
           for (int k = 0; k < 3; k++) {
             poly_cp4(&sm.pf_in[k], A.pos_src + 3 * ms + k);
@@ -975,9 +975,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         const float* red = Gf;
   #pragma unroll
         for (int h = 0; h < kPolyTC / kPolyThreads; h++) {
-          // the item's outputs: a sub-range of the tile under a split plan (1024-thread CTAs), else the whole tile
-          const int t = tid + h * kPolyThreads, k = (THREADS >= 1024 ? T.ot0 : T.t0) + t;
-          if (k < (THREADS >= 1024 ? T.ote : T.te))
+          // the item's outputs: a sub-range of the tile under a split plan (512- and 1024-thread CTAs), else the tile
+          const int t = tid + h * kPolyThreads, k = (THREADS >= 512 ? T.ot0 : T.t0) + t;
+          if (k < (THREADS >= 512 ? T.ote : T.te))
             A.out[T.row + k] = (red[t] + red[kPolyTC + t]) + (red[2 * kPolyTC + t] + red[3 * kPolyTC + t]);
         }
         if (T.tail)
@@ -1186,7 +1186,7 @@ static long long poly_plan_subs(IsmArgs& B, long long n_work, long long cmax) {
   for (long long wi = 0; wi < n_work; wi++) {
     B.poly_first[wi] = (unsigned short)first;
     const int k = ns[(size_t)wi], lg = k == 4 ? 2 : k == 2 ? 1 : 0;
-    for (int sub = 0; sub < k; sub++) B.poly_cmap[first + sub] = (unsigned short)(wi | sub << 8 | lg << 12);
+    for (int sub = 0; sub < k; sub++) B.poly_cmap[first + sub] = (unsigned short)(wi | sub << 10 | lg << 12);
     first += k;
   }
   B.poly_first[n_work] = (unsigned short)first;
@@ -1236,11 +1236,11 @@ cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, in
   // at most one item per SM: one 1024-thread CTA per item (twice the warps of a 512-thread CTA on each tile; the fine
   // plane always fits), the same bits as every other shape
   static const bool no1024 = getenv("GPURIR_POLY_NO1024") != nullptr;  // A/B switch
+  static const bool nosub = getenv("GPURIR_POLY_NOSUB") != nullptr;     // A/B switch: no output-range splits
   if (n_work <= num_sms && !no1024) {
     B.poly_gb = 1;
     // heavy tiles' output ranges split over the idle SMs (as for cluster items; each part its own CTA and queue
     // entry, enumerating only its thin shell of images, with the whole tile's fixed-point format: the same bits)
-    static const bool nosub = getenv("GPURIR_POLY_NOSUB") != nullptr;  // A/B switch
     long long n_entries = n_work;
     B.poly_nitems = 0;
     if (split == 0 && !A.jobs && n_work <= kPolyMaxItems && !nosub) n_entries = poly_plan_subs(B, n_work, num_sms);
@@ -1249,7 +1249,12 @@ cudaError_t launch_ism_poly(const IsmArgs& A, long long n_work, int* counter, in
   // 512-thread CTAs carry the fine plane whenever two of them still fit an SM with it (the guard's redo)
   const size_t s1 = poly_smem_bytes<512>(A.poly_ntaps, false), s2 = poly_smem_bytes<512>(A.poly_ntaps, true);
   B.poly_gb = two_word || 2 * (s2 + 1024) <= 228 * 1024;
-  return launch_poly<512>(B, n_work, counter, B.poly_gb ? s2 : s1, num_sms, stream);
+  // up to two items per SM: the heavy tiles' output ranges split over the free CTA slots, as above
+  long long n_entries = n_work;
+  B.poly_nitems = 0;
+  if (split == 0 && !A.jobs && n_work <= 2LL * num_sms && n_work <= kPolyMaxItems && !nosub)
+    n_entries = poly_plan_subs(B, n_work, 2LL * num_sms);
+  return launch_poly<512>(B, n_entries, counter, B.poly_gb ? s2 : s1, num_sms, stream);
 }
 
 }  // namespace gpurir

@@ -7,8 +7,8 @@
 
 namespace gpurir {
 
-constexpr int kPolyMaxItems = 160;  // polyphase calls whose work items' output ranges may be split (<= 1 item per SM)
-constexpr int kPolyMaxSubItems = 160;  // the split plan's (item, sub-range) entries: at most one wave
+constexpr int kPolyMaxItems = 320;  // polyphase calls whose work items' output ranges may be split (<= 2 items per SM)
+constexpr int kPolyMaxSubItems = 320;  // the split plan's (item, sub-range) entries: at most one wave
 constexpr int kPolyClusterMaxItems = 32;  // polyphase calls of at most this many (tile, RIR) items run cluster items
 
 // One RIR of a multi-room batch (device copy built by the host planner).
@@ -106,7 +106,7 @@ struct IsmArgs {
   // (= tile x RIR work item) owns clusters [poly_first[i], poly_first[i + 1]); poly_nitems = 0: one cluster each
   int poly_nitems;
   unsigned short poly_first[kPolyMaxItems + 1];
-  // the same plan per cluster (cluster items) or per queue entry (persistent CTAs): item | sub << 8 | log2(nsub) << 12
+  // the same plan per cluster (cluster items) or per queue entry (persistent CTAs): item | sub << 10 | log2(nsub) << 12
   unsigned short poly_cmap[kPolyMaxSubItems];
 };
 

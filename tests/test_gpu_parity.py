@@ -848,6 +848,22 @@ def test_poly_cluster_matches_persistent(P, oracle, case):
         assert np.array_equal(run_gpu(P, sc, beta, nb, mode="poly", split=split), ref), split
 
 
+@pytest.mark.parametrize("M", [16, 90])
+def test_poly_split_plan_persistent_bit_identical(P, oracle, M):
+    """Calls of at most two work items per SM split their heavy tiles' output ranges over the free CTA slots (one
+    queue entry per part, 1024- or 512-thread persistent CTAs): 16 receivers (48 items) and 90 receivers (270
+    items, item indices past 8 bits in the plan map) give the bits of the unsplit persistent call (split = -1),
+    and the oracle at the fp32 tolerance."""
+    sc = W.cfg3(M, "diffuse")
+    beta, nb = derive(oracle, sc)
+    ref = run_gpu(P, sc, beta, nb, mode="poly", split=-1)
+    assert np.array_equal(run_gpu(P, sc, beta, nb, mode="poly"), ref)
+    for m in (0, M - 1):
+        r = oracle.simulate_rir(sc.room, beta, sc.pos_src, sc.pos_rcv[m:m + 1], nb, sc.Tdiff, sc.Tmax, fs=sc.fs,
+                                pattern=sc.pattern, orV_rcv=sc.orV_rcv[m:m + 1], seed=sc.seed, rir_index_base=m)
+        assert rel_err(ref[:, m], r[:, 0]).max() <= TOL["poly"], m
+
+
 def test_poly_parts_scratch_self_cleaning(P, oracle):
     """Small calls split their heavy tiles into parts whose integer planes meet in a global scratch slot that
     the last part zeroes again: back-to-back calls of different sizes and sampling rates on one stream (which
