@@ -225,6 +225,31 @@ def test_poly_fir_table_reproduces_eq6(P, oracle, fs):
     assert mlo0 == mlo and tab.shape[0] == n
 
 
+@pytest.mark.parametrize("Tw,fs", [(2e-3, 16000.0), (2e-3, 48000.0), (8e-3, 16000.0), (8e-3, 48000.0), (16e-3, 16000.0)])
+def test_poly_fir_table_other_windows(P, oracle, Tw, fs):
+    """Reading R13 at other window lengths T_w (2-16 ms: 32-384 taps): the rotated low-rank FIR equals the
+    unrotated expansion to < 1e-7 and the oracle's Eq. 6 to < 1e-6 of its peak at every tap."""
+    F = P.poly_fir_table(Tw, fs)
+    far, near, Qc, mlo, nmi0, nn = F["far"], F["near"], F["Q"], F["mlo"], F["nmi0"], F["nn"]
+    n = far.shape[1]
+    Q = np.zeros((8, 8))
+    for par in range(2):
+        for k in range(4):
+            for i in range(4):
+                Q[2 * k + par, 2 * i + par] = Qc[par, k, i]
+    Pr = np.zeros((n, 8))
+    Pr[:, 0:4] = far.transpose(1, 0, 2).reshape(n, 4)
+    Pr[nmi0:nmi0 + nn, 4:8] = near.transpose(1, 0, 2).reshape(nn, 4)
+    phi = np.linspace(0.0, 1.0, 61)[:-1]
+    T = np.cos(np.arange(8)[:, None] * np.arccos(2 * phi - 1)[None, :])
+    approx = Pr @ (Q @ T)
+    tab, _ = P.poly_table(Tw, fs)
+    assert np.abs(approx - tab.astype(np.float64) @ T).max() < 1e-7
+    worst = max(float(np.max(np.abs(approx[mi] - [oracle.windowed_sinc((mlo + mi - f) / fs, Tw, fs / 2) for f in phi])))
+                for mi in range(n))
+    assert worst < 1e-6, worst
+
+
 def test_batch_extent_on_host(P):
     """gpurir_batch_extent (the binding's output-size check of a batch call): max(out_offset + ceil(Tmax fs)),
     reading C9 / R1, computed on the host without a device; -1 for invalid arguments."""
