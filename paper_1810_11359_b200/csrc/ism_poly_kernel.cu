@@ -415,7 +415,12 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
 #endif
   PT_MARK(0);
   PS_MARK(0);
-  for (int i = tid; i < poly_tab_floats(ntaps, A.poly_nn); i += kPolyThreads) Pt[i] = A.poly_P[i];
+  if constexpr (CL) {  // small calls: threads >= 32 copy the table, thread 0 goes straight to its item's setup
+    if (tid >= 32)
+      for (int i = tid - 32; i < poly_tab_floats(ntaps, A.poly_nn); i += kPolyThreads - 32) Pt[i] = A.poly_P[i];
+  } else {
+    for (int i = tid; i < poly_tab_floats(ntaps, A.poly_nn); i += kPolyThreads) Pt[i] = A.poly_P[i];
+  }
   // (the FIR window nmi0 / nn and the rotation Q = Pt + 4 ntaps + 4 nn are re-read from the parameter bank where
   // used: no registers held across the image loop)
   PS_MARK(1);
@@ -480,7 +485,19 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           if (!CL && sm.pf_valid)  // the inputs were fetched with the index
             geom_from(A.L, sm.pf_in, sm.pf_in + 3, A.orv ? sm.pf_in + 6 : zero3, A.nb, A.pattern,
                       A.ors ? sm.pf_in + 9 : zero3, A.spkr_pattern, A.lb, A.neg, A.zero, T.g, A.status);
-          else
+          else if constexpr (CL) {  // small calls: all 12 inputs in flight at once (geom_from stores into shared
+                                    // memory, which the compiler must assume the input pointers alias)
+            float in[12];
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+              in[k] = A.pos_src[3 * ms + k];
+              in[3 + k] = A.pos_rcv[3 * mr + k];
+              in[6 + k] = A.orv ? A.orv[3 * mr + k] : 0.f;
+              in[9 + k] = A.ors ? A.ors[3 * ms + k] : 0.f;
+            }
+            geom_from(A.L, in, in + 3, in + 6, A.nb, A.pattern, in + 9, A.spkr_pattern, A.lb, A.neg, A.zero, T.g,
+                      A.status);
+          } else
             geom_from(A.L, A.pos_src + 3 * ms, A.pos_rcv + 3 * mr, A.orv ? A.orv + 3 * mr : zero3, A.nb, A.pattern,
                       A.ors ? A.ors + 3 * ms : zero3, A.spkr_pattern, A.lb, A.neg, A.zero, T.g, A.status);
         }
@@ -496,10 +513,11 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         T.t0 = max(0, T.te - kPolyTC);
         // the item's outputs: sub-range `sub` of nsub equal end-aligned parts (nsub > 1 only for full tiles; the
         // fixed-point format below stays the whole tile's); positions cover the nominal part + the halo
-        {
-          const int Ls = kPolyTC / nsub;
+        {  // parts of Ls outputs, a multiple of 128 (so a cluster rank's share stays a multiple of 8 for S <= 16):
+           // 1024 / nsub for a full tile; a partial (first) tile's first part takes what is left
+          const int Ls = nsub > 1 ? (((T.te - T.t0 + nsub - 1) / nsub + 127) & ~127) : kPolyTC;
           T.ote = T.te - (nsub - 1 - sub) * Ls;
-          T.ot0 = nsub > 1 ? T.ote - Ls : T.t0;
+          T.ot0 = nsub > 1 ? max(T.t0, T.ote - Ls) : T.t0;
           T.npos_i = Ls + ntaps - 1;
         }
         if (A.jobs) {
@@ -1180,6 +1198,16 @@ static long long poly_plan_subs(IsmArgs& B, long long n_work, long long cmax) {
     if (best < 0 || total + ns[(size_t)best] > cmax) break;
     total += ns[(size_t)best];
     ns[(size_t)best] *= 2;
+  }
+  // a partial (first) tile holds few images but still all its outputs on one cluster, whose exchange and filter then
+  // finish last (config 1: 704 outputs): split it in two when there is room
+  for (long long wi = 0; wi < n_work; wi++) {
+    const int tile = B.nTiles - 1 - (int)(wi / B.M);
+    const long long te = B.nISM - (long long)(B.nTiles - 1 - tile) * kPolyTC, t0 = std::max(0LL, te - kPolyTC);
+    if (full[(size_t)wi] || ns[(size_t)wi] != 1 || te - t0 <= kPolyTC / 2 || total + 1 > cmax) continue;
+    if (last[(size_t)wi] && B.poly_tail && (((te - t0 + 1) / 2 + 127) & ~127) < B.tail_win) continue;
+    ns[(size_t)wi] = 2;
+    total += 1;
   }
   if (total > kPolyMaxSubItems) return n_work;  // (cannot happen: cmax is at most one wave) no plan
   int first = 0;
