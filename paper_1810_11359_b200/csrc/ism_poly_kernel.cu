@@ -159,6 +159,63 @@ __device__ __noinline__ void poly_fused_tail(PolyTile& T, const float* red, cons
   (void)nthreads;
 }
 
+// The fused tail of a cluster item (every rank of the tail tile's cluster calls it): the same samples as
+// poly_fused_tail, but each thread first computes its first Philox block's noise (Philox words, the logistic
+// transform and the envelope's decay factor; none of it depends on the envelope's level env0) while the cluster
+// waits for every rank's outputs; after the envelope only the level multiplies in, in tail_quad's order (same bits).
+__device__ __noinline__ void poly_fused_tail_cl(PolyTile& T, const float* hg, int tid, float* out, int win,
+                                                unsigned long long seed, int q_first, int q_stride) {
+  const int nISM = T.te, nS = T.tail_nS;
+  const float alpha = -T.tail_kappa * 0.72134752044448170368f, rho = tail_ex2(alpha);  // as tail_envelope
+  const PhiloxKey key = philox_key(make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  const long long qend = (long long)((nS + 3) >> 2), q = (long long)(nISM >> 2) + q_first + tid;
+  float L[4] = {0.f, 0.f, 0.f, 0.f}, x = 0.f;
+  if (q < qend) {
+    const uint4 w = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)((unsigned long long)q >> 32),
+                                             (uint32_t)T.tail_rglob, (uint32_t)(T.tail_rglob >> 32)), key);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const float f = __uint_as_float(0x3F800000u | (ws[j] >> 9));
+      const float u = f - 0.99999994039535522461f;
+      L[j] = tail_lg2(u) - tail_lg2(1.f - u);
+    }
+    x = tail_ex2(alpha * (float)(q * 4 - nISM));
+  }
+  __threadfence();
+  cg::this_cluster().sync();  // the tile's samples are in global memory once every rank is here
+  if (tid < 32) {
+    float env0, a_, r_;
+    tail_envelope([&](int k) { return hg[k]; }, nISM, win, T.x_dp, T.tail_kappa, tid, env0, a_, r_);
+    if (tid == 0) T.tenv[0] = env0;
+  }
+  __syncthreads();
+  const float env0 = T.tenv[0];
+  float* row = out + T.row;
+  const bool aligned = (reinterpret_cast<uintptr_t>(row) & 15) == 0;
+  if (q < qend) {  // tail_quad's last steps for the precomputed block
+    float e = env0 * x, vals[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      vals[j] = e * L[j];
+      e *= rho;
+    }
+    const long long k0 = q * 4;
+    float* o = row + k0;
+    if (aligned && k0 >= nISM && k0 + 3 < nS) {
+      *reinterpret_cast<float4*>(o) = make_float4(vals[0], vals[1], vals[2], vals[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const long long k = k0 + j;
+        if (k >= nISM && k < nS) o[j] = vals[j];
+      }
+    }
+  }
+  for (long long qq = q + q_stride; qq < qend; qq += q_stride)
+    tail_quad(qq, nISM, nS, env0, alpha, rho, key, T.tail_rglob, row, aligned);
+}
+
 template <int THREADS>
 struct alignas(16) PolySmem {
   PolyTile ti;
@@ -868,12 +925,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         if (k < T.ote) A.out[T.row + k] = (red[o] + red[R + o]) + (red[2 * R + o] + red[3 * R + o]);
       }
       PT_MARK(6);
-      if (T.tail) {  // uniform over the cluster: the tile's samples are in global memory once every rank is here
-        __threadfence();
-        cl.sync();
-        poly_fused_tail(sm.ti, nullptr, A.out + T.row, tid, kPolyThreads, A.out, A.tail_win, A.tail_seed,
-                        rank * kPolyThreads, S * kPolyThreads);
-      }
+      if (T.tail)  // uniform over the cluster
+        poly_fused_tail_cl(sm.ti, A.out + T.row, tid, A.out, A.tail_win, A.tail_seed, rank * kPolyThreads,
+                           S * kPolyThreads);
       PT_MARK(7);
       PT_DUMP();
       break;  // one item per cluster (no rank reads another's shared memory)
