@@ -270,8 +270,8 @@ static void jacobi4(double a[4][4], double w[4], double v[4][4]) {
 // slowly with m), so after an orthogonal change of channel basis G' = Q G — per parity (P_d[1 - m] =
 // (-1)^d P_d[m], Eq. 6 is even, so Q is block diagonal over even / odd d), rows the eigenvectors of the far taps'
 // Gram matrix sum_m P[m] P[m]^T by decreasing eigenvalue — only the rotated channels 0..3 need the whole support;
-// channels 4..7 keep an aligned window of nn = 16 (or 24) taps around m = 0, 1 (the far-tap coefficients dropped
-// there are < 1e-8: their eigenvalues).  The kernel converts G, rotates it by Q and runs the FIR on
+// channels 4..7 keep a window of nn = 8 taps, m = -3 .. 4, around m = 0, 1 (the coefficients dropped outside it
+// are < 5e-8 of the peak at 8-96 kHz and T_w = 2-8 ms, against the expansion's 4.3e-7).  The kernel converts G, rotates it by Q and runs the FIR on
 // 4 ntaps + 4 nn taps per output instead of 8 ntaps.  Device table: far [2 pairs][ntaps][2] (rotated channels
 // (0, 1), (2, 3)), near [2 pairs][nn][2] (channels (4, 5), (6, 7)) for taps mi = nmi0 .. nmi0 + nn - 1, then
 // Q [parity][k][i] (32 floats): rotated channel 2 k + par = sum_i Q[par][k][i] G_{2 i + par}, the k-th
@@ -280,8 +280,8 @@ void poly_fir_tables(const std::vector<float>& tab, int npad, int mlo, std::vect
                      int* nn_out) {
   auto Pd = [&](int mi, int d) { return (double)tab[((size_t)(d >> 1) * npad + mi) * 2 + (d & 1)]; };
   const int mc = -mlo;                         // tap index of m = 0
-  const int nmi0 = std::max(0, ((mc - 6) / 8) * 8);  // the window covers m = -6 .. 7 (mi = mc - 6 .. mc + 7)
-  const int nn = std::min(npad - nmi0, ((mc + 8 - nmi0 + 7) / 8) * 8);
+  const int nn = std::min(8, npad);            // the window: m = -3 .. 4 (dropped coefficients < 5e-8 at 8-96 kHz)
+  const int nmi0 = std::max(0, std::min(mc - 3, npad - nn));
   double Q[8][8] = {};
   for (int par = 0; par < 2; par++) {
     double a[4][4] = {}, w[4], v[4][4];

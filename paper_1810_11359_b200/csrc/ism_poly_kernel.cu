@@ -372,7 +372,7 @@ __host__ __device__ constexpr int poly_plane_words(int ntaps) {
 }
 constexpr int kPolyWFixTaps = 64;
 constexpr int kPolyWFix = poly_plane_words(kPolyWFixTaps);
-constexpr int kPolyMaxNear = 24;  // rotated near channels' tap window (abi.cu poly_fir_tables: 16 or 24)
+constexpr int kPolyMaxNear = 8;   // rotated near channels' tap window (abi.cu poly_fir_tables: 8 taps)
 // floats of the FIR tables in shared memory (reading R13): far [2][ntaps][2], near [2][nn][2], Q [2][4][4]
 __host__ __device__ constexpr int poly_tab_floats(int ntaps, int nn) { return 4 * ntaps + 4 * nn + 32; }
 
@@ -425,10 +425,27 @@ __device__ __forceinline__ void poly_fir_item(const float* Gf, int W, const floa
     const float4* P4 = reinterpret_cast<const float4*>(Pt) + s * (ntaps >> 1) + g0 * 4;
     poly_fir_range(Gf + (2 * s) * W, W, P4, t8 + ntaps - 1 - 8 * g0, g1 - g0, acc);
   }
-  {  // near pair s: its window's tap groups [g0, g1) of nn / 8 (tap mi = nmi0 + 8 g0 first)
-    const int ng = nn >> 3, gh = (ng + 1) >> 1, g0 = h ? gh : 0, g1 = h ? ng : gh;
-    const float4* P4 = reinterpret_cast<const float4*>(Pt + 4 * ntaps) + s * (nn >> 1) + g0 * 4;
-    poly_fir_range(Gf + (4 + 2 * s) * W, W, P4, t8 + ntaps - 1 - nmi0 - 8 * g0, g1 - g0, acc);
+  if (h == 0) {  // near pair s: its window's 8 taps mi = nmi0 .. nmi0 + 7 (any alignment: runtime refill addresses)
+    const float* G0 = Gf + (4 + 2 * s) * W;
+    const float4* P4 = reinterpret_cast<const float4*>(Pt + 4 * ntaps) + s * (nn >> 1);
+    const int q = t8 + ntaps - 1 - nmi0;  // position of output t8 at the window's first tap
+    float2 w[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const int a = (q + r) + ((q + r) >> 3);
+      w[r] = make_float2(G0[a], G0[a + W]);
+    }
+    const float4 pq[4] = {P4[0], P4[1], P4[2], P4[3]};
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const float2 pc = (u & 1) ? make_float2(pq[u >> 1].z, pq[u >> 1].w) : make_float2(pq[u >> 1].x, pq[u >> 1].y);
+#pragma unroll
+      for (int r = 0; r < 8; r++) acc[r] = __ffma2_rn(pc, w[(r - u) & 7], acc[r]);
+      if (u < 7) {
+        const int pn = q - 1 - u, a = pn + (pn >> 3);
+        w[(7 - u) & 7] = make_float2(G0[a], G0[a + W]);
+      }
+    }
   }
 #pragma unroll
   for (int r = 0; r < 8; r++) res[r] = acc[r].x + acc[r].y;
@@ -1019,7 +1036,9 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         constexpr bool kIdle = kPolyThreads * kPolyPasses > kItems;
   #pragma unroll
         for (int pass = 0; pass < kPolyPasses; pass++) {
-          const int it = pass * kPolyThreads + tid, pi = it >> 7, t8 = 8 * (it & 127);
+          // two passes: a thread takes partials (0, 3) or (1, 2), one with and one without the near taps
+          const int it = pass * kPolyThreads + tid, pi0 = it >> 7, pi = (kPolyPasses == 2 && pass == 1) ? 5 - pi0 : pi0,
+                    t8 = 8 * (it & 127);
           if (!kIdle || it < kItems) poly_fir_item(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, part);
           if (pass < kPolyPasses - 1) {
             park[2 * tid] = make_float4(part[0], part[1], part[2], part[3]);
@@ -1030,7 +1049,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
         float* red = Gf;
   #pragma unroll
         for (int pass = 0; pass < kPolyPasses; pass++) {
-          const int it = pass * kPolyThreads + tid, pi = it >> 7, t8 = 8 * (it & 127);
+          const int it = pass * kPolyThreads + tid, pi0 = it >> 7, pi = (kPolyPasses == 2 && pass == 1) ? 5 - pi0 : pi0,
+                    t8 = 8 * (it & 127);
           if (kIdle && it >= kItems) break;
           float4* r4 = reinterpret_cast<float4*>(red + pi * kPolyTC + t8);
           if (pass < kPolyPasses - 1) {
