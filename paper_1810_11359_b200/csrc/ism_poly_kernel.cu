@@ -372,7 +372,7 @@ __host__ __device__ constexpr int poly_plane_words(int ntaps) {
 }
 constexpr int kPolyWFixTaps = 64;
 constexpr int kPolyWFix = poly_plane_words(kPolyWFixTaps);
-constexpr int kPolyMaxNear = 8;   // rotated near channels' tap window (abi.cu poly_fir_tables: 8 taps)
+constexpr int kPolyMaxNear = 24;  // rotated near channels' tap window (abi.cu poly_fir_tables: 8, or 16-24 for > 64 taps)
 // floats of the FIR tables in shared memory (reading R13): far [2][ntaps][2], near [2][nn][2], Q [2][4][4]
 __host__ __device__ constexpr int poly_tab_floats(int ntaps, int nn) { return 4 * ntaps + 4 * nn + 32; }
 
@@ -414,6 +414,7 @@ __device__ __forceinline__ void poly_fir_range(const float* G0, int W, const flo
     }
   }
 }
+template <bool kNear8>
 __device__ __forceinline__ void poly_fir_item(const float* Gf, int W, const float* Pt, int ntaps, int nmi0, int nn,
                                               int pi, int t8, float (&res)[8]) {
   const int s = pi >> 1, h = pi & 1;
@@ -425,7 +426,11 @@ __device__ __forceinline__ void poly_fir_item(const float* Gf, int W, const floa
     const float4* P4 = reinterpret_cast<const float4*>(Pt) + s * (ntaps >> 1) + g0 * 4;
     poly_fir_range(Gf + (2 * s) * W, W, P4, t8 + ntaps - 1 - 8 * g0, g1 - g0, acc);
   }
-  if (h == 0) {  // near pair s: its window's 8 taps mi = nmi0 .. nmi0 + 7 (any alignment: runtime refill addresses)
+  if constexpr (!kNear8) {  // tables of > 64 taps: the near pair's aligned window, tap groups [g0, g1) of nn / 8
+    const int ng = nn >> 3, gh = (ng + 1) >> 1, g0 = h ? gh : 0, g1 = h ? ng : gh;
+    const float4* P4 = reinterpret_cast<const float4*>(Pt + 4 * ntaps) + s * (nn >> 1) + g0 * 4;
+    poly_fir_range(Gf + (4 + 2 * s) * W, W, P4, t8 + ntaps - 1 - nmi0 - 8 * g0, g1 - g0, acc);
+  } else if (h == 0) {  // near pair s: its window's 8 taps mi = nmi0 .. nmi0 + 7 (any alignment: runtime refills)
     const float* G0 = Gf + (4 + 2 * s) * W;
     const float4* P4 = reinterpret_cast<const float4*>(Pt + 4 * ntaps) + s * (nn >> 1);
     const int q = t8 + ntaps - 1 - nmi0;  // position of output t8 at the window's first tap
@@ -932,7 +937,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
       for (int it = tid; it < 4 * (R >> 3); it += kPolyThreads) {
         const int pi = it / (R >> 3), t8 = 8 * (it - pi * (R >> 3));
         float res[8];
-        poly_fir_item(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, res);
+        poly_fir_item<(WFIX > 0)>(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, res);
 #pragma unroll
         for (int r = 0; r < 8; r++) red[pi * R + t8 + r] = res[r];
       }
@@ -1039,7 +1044,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           // two passes: a thread takes partials (0, 3) or (1, 2), one with and one without the near taps
           const int it = pass * kPolyThreads + tid, pi0 = it >> 7, pi = (kPolyPasses == 2 && pass == 1) ? 5 - pi0 : pi0,
                     t8 = 8 * (it & 127);
-          if (!kIdle || it < kItems) poly_fir_item(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, part);
+          if (!kIdle || it < kItems) poly_fir_item<(WFIX > 0)>(Gf, W, Pt, ntaps, A.poly_nmi0, A.poly_nn, pi, t8, part);
           if (pass < kPolyPasses - 1) {
             park[2 * tid] = make_float4(part[0], part[1], part[2], part[3]);
             park[2 * tid + 1] = make_float4(part[4], part[5], part[6], part[7]);

@@ -194,7 +194,7 @@ def test_poly_table_reproduces_eq6(P, oracle, fs):
 @pytest.mark.parametrize("fs", [3000.0, 8000.0, 16000.0, 22050.0, 44100.0, 48000.0, 96000.0])
 def test_poly_fir_table_reproduces_eq6(P, oracle, fs):
     """Reading R13: the rotated, low-rank FIR form the kernel runs (channels G' = Q G; rotated channels 4..7 only
-    on their 8-tap window m = -3 .. 4) reproduces the oracle's Eq. 6 windowed sinc at every integer tap and fractional delay
+    on their window: 8 taps m = -3 .. 4 for tables of <= 64 taps, else 16-24 aligned taps) reproduces the oracle's Eq. 6 windowed sinc at every integer tap and fractional delay
     to < 1e-6 of its peak, as the unrotated table does; Q is orthogonal and block diagonal over the parities."""
     Tw = 4e-3
     F = P.poly_fir_table(Tw, fs)
@@ -206,8 +206,11 @@ def test_poly_fir_table_reproduces_eq6(P, oracle, fs):
             for i in range(4):
                 Q[2 * k + par, 2 * i + par] = Qc[par, k, i]
     assert np.abs(Q @ Q.T - np.eye(8)).max() < 1e-6
-    assert nn == 8 and 0 <= nmi0 and nmi0 + nn <= n
-    assert nmi0 == min(-3 - mlo, n - 8) or nmi0 == 0  # the window m = -3 .. 4 (clamped to the table)
+    assert 0 <= nmi0 and nmi0 + nn <= n
+    if n <= 64:  # the window m = -3 .. 4 (clamped to the table)
+        assert nn == 8 and (nmi0 == min(-3 - mlo, n - 8) or nmi0 == 0)
+    else:        # longer tables: an aligned 16- or 24-tap window covering m = -6 .. 7
+        assert nn in (16, 24) and nmi0 % 8 == 0 and nmi0 <= -6 - mlo and nmi0 + nn >= 8 - mlo
     Pr = np.zeros((n, 8))  # rotated coefficients per tap
     Pr[:, 0:4] = far.transpose(1, 0, 2).reshape(n, 4)
     Pr[nmi0:nmi0 + nn, 4:8] = near.transpose(1, 0, 2).reshape(nn, 4)
