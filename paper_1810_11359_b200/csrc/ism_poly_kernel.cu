@@ -755,8 +755,10 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             const int end = incl & 0xFFFFF, start = end - cnt, k = (incl >> 20) - 1;
             cr.end = end;
             cr.b = start + r1n;          // first candidate of the second n_z run
-            cr.a1 = r1lo - start;        // n_z = gi + a1 on the first run
-            cr.a2 = r2lo - r1n - start;  // n_z = gi + a2 on the second
+            // n_z + 2^31 = gi + a1 on the first run, gi + a2 on the second (mod 2^32): the walk forms the
+            // exponent-bias bits of its int -> double conversion directly
+            cr.a1 = (int)((unsigned)(r1lo - start) + 0x80000000u);
+            cr.a2 = (int)((unsigned)(r2lo - r1n - start) + 0x80000000u);
             sm.col[k] = cr;
             sm.colpre[k] = end;
             sm.colsdot[k] = sdot;
@@ -775,6 +777,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           }
           int j = lo;
           const int zl = T.zl;
+          const unsigned zlb = (unsigned)zl + 0x80000000u;
           // the column records carry the fixed-point scale, so the deposits take amp as is and the last channel
           // amp 2^-J (both exact: powers of two)
           const float oz = g.o[2], ga = g.a, oma = 1.f - ga, scale_lj = T.scale_lf / T.scalef;
@@ -792,13 +795,13 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           for (int gi = g0; gi < g1; gi++) {  // every lane runs R candidates: the walk keeps the warp converged
             // compacted columns are nonempty and gi advances by one: a change moves exactly one column on
             if (gi >= cr.end) cr = load_col(&sm.col[++j]);
-            const int nz = gi + (gi < cr.b ? cr.a1 : cr.a2);
-            const int odd = nz & 1;
+            const unsigned nzb = (unsigned)gi + (unsigned)(gi < cr.b ? cr.a1 : cr.a2);  // n_z + 2^31
+            const int odd = (int)(nzb & 1u);
             // nz lies in [zl, zh] (the column's runs are clamped to it) and use_bz means zh - zl < kPolyBz
-            const float bz = use_bz ? sm.bz[nz - zl] : poly_z_factor(nz, g);
-            const int nzo = nz + odd;
-            // Eq. 1 along z, in samples (the tile's constants are read from shared memory: no conversions here)
-            const double dz = fma(int_to_double(nzo), Lzs, odd ? offOs : offEs);
+            const float bz = use_bz ? sm.bz[nzb - zlb] : poly_z_factor((int)(nzb - 0x80000000u), g);
+            const unsigned nzob = nzb + (unsigned)odd;
+            // Eq. 1 along z, in samples: (2^52 + 2^31 + n_zo) as raw bits minus 2^52 + 2^31 (int_to_double)
+            const double dz = fma(__hiloint2double(0x43300000, (int)nzob) - 4503601774854144.0, Lzs, odd ? offOs : offEs);
             const double x2 = fma(dz, dz, cr.rho2);                             // (d fs / c)^2
 
             float x0f, xd, rx;  // x = x0f + xd (xd the fp64 Newton correction); rx = 1/x
