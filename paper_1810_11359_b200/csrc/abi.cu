@@ -387,6 +387,8 @@ int setup_mode(DeviceState* d, const gpurir_opts& o, double fs, double H, cudaSt
     const PolyEntry* P = ensure_poly(d, o.Tw, fs, stream, &st);
     if (!P) return st;
     A.poly_P = P->dev; A.poly_ntaps = P->ntaps; A.poly_mlo = P->mlo; A.poly_nmi0 = P->nmi0; A.poly_nn = P->nn;
+    A.poly_i2d_bias = 4503601774854144.0;
+    A.poly_m1 = -1.f;
   }
   return GPURIR_OK;
 }

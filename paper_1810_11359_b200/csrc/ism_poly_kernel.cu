@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             const float bz = use_bz ? sm.bz[nzb - zlb] : poly_z_factor((int)(nzb - 0x80000000u), g);
             const unsigned nzob = nzb + (unsigned)odd;
             // Eq. 1 along z, in samples: (2^52 + 2^31 + n_zo) as raw bits minus 2^52 + 2^31 (int_to_double)
-            const double dz = fma(__hiloint2double(0x43300000, (int)nzob) - 4503601774854144.0, Lzs, odd ? offOs : offEs);
+            const double dz = fma(__hiloint2double(0x43300000, (int)nzob) - A.poly_i2d_bias, Lzs, odd ? offOs : offEs);
             const double x2 = fma(dz, dz, cr.rho2);                             // (d fs / c)^2
 
             float x0f, xd, rx;  // x = x0f + xd (xd the fp64 Newton correction); rx = 1/x
@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             float gain = fmaf(oma, cth, ga);
             if (dir_src) gain *= src_gain(sm.colsdot[j], odd, dzf, rx, g);
             const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
-            const float y = fmaf(2.f, phi, -1.f);            // 2 phi - 1 in [-1, 1)
+            const float y = fmaf(2.f, phi, A.poly_m1);        // 2 phi - 1 in [-1, 1)
             poly_add(Ga, Gb, W, p + (p >> 3), y, amp, 1.f, scale_lj, J, cmask, two_word, acc);
           }
           };

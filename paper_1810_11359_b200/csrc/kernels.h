@@ -84,6 +84,10 @@ struct IsmArgs {
   const float* poly_P;
   int poly_ntaps, poly_mlo;
   int poly_nmi0, poly_nn;
+  // constants of the image walk read as parameter-bank operands (literals would be re-materialised every image at
+  // the 64-register cap): 2^52 + 2^31 (the int -> double trick's bias) and -1
+  double poly_i2d_bias;
+  float poly_m1;
   int poly_gbz;            // some tile of the call starts in the two-word scheme: zero the fine plane Gb per tile
   int poly_gb;             // set by the launcher: the fine plane Gb is allocated (two-word tiles, guard's last rung)
   int poly_force2;         // test hook (opts.split == -2): every tile uses the two-word scheme
