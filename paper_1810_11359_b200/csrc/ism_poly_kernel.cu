@@ -305,6 +305,7 @@ __device__ __forceinline__ float poly_z_factor_args(int nz, const IsmArgs& A) {
 //     d), round(A T_d 2^s) from the low mantissa bits of A 2^s T_d + 1.5 2^23 (exact for |v| < 2^22);
 //   two words (bits = 28): v = a 2^14 + b, b in [0, 2^14), into two int32 planes (2^17 terms of headroom); the
 //     last channel puts round(v 2^-14) in its coarse plane and counts in its fine plane (J = 17).
+template <bool kCountFirst>
 __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int W, int p, float y, float amp, float scale,
                                          float scale_l, int J, unsigned mask, bool two_word, unsigned& acc) {
   constexpr int kLast = kPolyChannels - 1;
@@ -312,7 +313,8 @@ __device__ __forceinline__ void poly_add(int* Ga, int* Gb, int W, int p, float y
     // the deposits are the raw bit patterns 0x4B400000 + v of A 2^s T_d + 1.5 2^23: the sums carry count x
     // 0x4B400000 (mod 2^32), removed at the conversion with the exact count of the last channel's low bits
     const float as = amp * scale, y2 = 2.f * y, magic = 12582912.f;  // power-of-two scales: exact
-    if constexpr (kPolyChannels == 8) {  // the counting deposit first: its returned word's latency hides under the
+    if constexpr (kCountFirst && kPolyChannels == 8) {  // the counting deposit first: its returned word's latency
+                                                          // hides under the other seven (persistent CTAs; see below)
                                          // other seven (+0.2 %, A/B 3 rounds; the same integer sums)
       float Tc[8];
       Tc[0] = 1.f; Tc[1] = y;
@@ -830,7 +832,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             if (dir_src) gain *= src_gain(sm.colsdot[j], odd, dzf, rx, g);
             const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
             const float y = fmaf(2.f, phi, A.poly_m1);        // 2 phi - 1 in [-1, 1)
-            poly_add(Ga, Gb, W, p + (p >> 3), y, amp, 1.f, scale_lj, J, cmask, two_word, acc);
+            // (cluster items keep the original deposit order: their code is tuned for latency, measured separately)
+            poly_add<!CL>(Ga, Gb, W, p + (p >> 3), y, amp, 1.f, scale_lj, J, cmask, two_word, acc);
           }
           };
           if (T.use_bz && !T.two_word && g.as == 1.f) walk(std::true_type());
