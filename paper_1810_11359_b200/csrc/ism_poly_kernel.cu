@@ -7,22 +7,26 @@
 //     delta'(m - phi) = sum_d P_d[m] T_d(2 phi - 1),   d = 0..7   (max error 4.3e-7, host fit),
 // the RIR becomes a fixed 8-channel FIR filter applied to per-sample image aggregates:
 //     h[k] = sum_m sum_d P_d[m] G_d[k - m],   G_d[j] = sum_{n: j_n = j} A_n T_d(2 phi_n - 1).
-// Persistent CTAs (THREADS = 256 x 4 per SM for large single-word calls, else 512 x 2) take (RIR,
-// 1024-sample tile) work items from a global counter; per item the CTA
+// Persistent CTAs (THREADS = 256 x 4 per SM from 7 items per SM, 512 x 2 below, 1024 x 1 for calls of at most
+// one item per SM; calls of <= 2 items per SM split their heavy tiles' output ranges over the free CTA slots)
+// take (RIR, 1024-sample tile) work items from a global counter; per item the CTA
 //   1. enumerates the tile's shell of images column by column (as ism_ws_kernel; nonempty columns
 //      compacted by the candidate scan) and adds each image's 8 channel values into G in shared memory —
 //      as fixed point with integer reductions (one int32 word per channel, or two for tiles dense enough to
 //      need them; the scale is per tile), so the sums are exact and independent of the order the images
 //      arrive in (deterministic, shard-invariant); the fraction of the delay comes from the exact floor of
 //      the fp32 estimate plus its fp64 correction;
-//   2. converts G to fp32 in place and runs the 8-channel FIR (2H taps): 4 channel-pair groups x THREADS/4
-//      threads x 8 consecutive outputs with a sliding register window, partial sums meeting in shared
-//      memory; the tile is written once, coalesced.
+//   2. converts G to fp32 in place, rotates each position's 8 values by Q (reading R13: G' = Q G, per parity)
+//      and runs the FIR: rotated channels 0..3 over all 2H taps, 4..7 over an 8-tap window around the image
+//      (288 instead of 512 MACs per output at 16 kHz), 4 partials x 8 consecutive outputs per thread item with a
+//      sliding register window, partial sums meeting in shared memory; the tile is written once, coalesced.
+// Small calls (<= 32 items) run cluster items instead: a tile's columns split over a thread-block cluster whose
+// ranks' integer planes meet through L2 (same bits as the persistent CTAs).
 // The kernel is bound by shared-memory wavefronts (80 % of peak: the random-position reductions and the
 // FIR's loads), so the loops keep their constants in registers rather than re-reading them from shared
 // memory.
 // Work per output sample no longer grows with the image density (690 in-window taps per sample at config
-// 3 (i)): the filter costs 2H x 8 MACs, the aggregation 8 channel updates per image.
+// 3 (i)): the filter costs 4 x 2H + 4 x 8 MACs, the aggregation 8 channel updates per image.
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <mutex>
