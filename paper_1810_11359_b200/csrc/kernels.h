@@ -9,6 +9,7 @@ namespace gpurir {
 
 constexpr int kPolyMaxItems = 320;  // polyphase calls whose work items' output ranges may be split (<= 2 items per SM)
 constexpr int kPolyMaxSubItems = 320;  // the split plan's (item, sub-range) entries: at most one wave
+static_assert(kPolyMaxItems < 1024 && kPolyMaxSubItems <= 65535, "plan map: item | sub << 10 | log2(nsub) << 12");
 constexpr int kPolyClusterMaxItems = 32;  // polyphase calls of at most this many (tile, RIR) items run cluster items
 
 // One RIR of a multi-room batch (device copy built by the host planner).
