@@ -791,11 +791,15 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           const unsigned cmask = T.cnt_mask;
           unsigned acc = 0xFFFFFFFFu;  // min of ~old & mask over this thread's last-channel deposits (poly_add)
           PolyColRec cr = load_col(&sm.col[j]);  // the current column's record, in registers
-          // the walk, compiled twice: the common case (single word, omni source, z factors from the table) with
-          // its flags as constants — fewer live registers, so fewer loop constants re-read from shared memory —
-          // and the general case with runtime flags
-          auto walk = [&](auto fast) {
-          constexpr bool kFast = decltype(fast)::value;
+          // the walk, compiled three times: the common case (single word, omni source, z factors from the table)
+          // with its flags as constants — fewer live registers, so fewer loop constants re-read from shared memory —
+          // once more for single-room persistent calls (pattern constants from the parameter bank: +0.2 %), and the
+          // general case with runtime flags
+          auto walk = [&](auto fast, auto single) {
+          constexpr bool kFast = decltype(fast)::value, kSingle = decltype(single)::value;
+          // single-room calls: the receiver pattern's constants straight from the parameter bank (uniform registers,
+          // off the 64-register budget of the loop)
+          const float gaw = kSingle ? pattern_const(A.pattern) : ga, omaw = kSingle ? 1.f - pattern_const(A.pattern) : oma;
           const bool use_bz = kFast || T.use_bz, dir_src = !kFast && g.as != 1.f, two_word = !kFast && T.two_word;
           const double Lzs = T.Lzs, offEs = T.offEs, offOs = T.offOs;
           for (int gi = g0; gi < g1; gi++) {  // every lane runs R candidates: the walk keeps the warp converged
@@ -832,7 +836,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             if ((unsigned)p >= (unsigned)npos_i) continue;  // reaches no sample of this item (p < 0 wraps)
             const float dzf = (float)dz;  // one XU conversion instead of shared-memory loads (the smem pipe binds)
             const float cth = fmaf(dzf, oz, cr.cdot) * rx;
-            float gain = fmaf(oma, cth, ga);
+            float gain = fmaf(omaw, cth, gaw);
             if (dir_src) gain *= src_gain(sm.colsdot[j], odd, dzf, rx, g);
             const float amp = cr.bxy * bz * gain * rx;       // Eq. 4
             const float y = fmaf(2.f, phi, A.poly_m1);        // 2 phi - 1 in [-1, 1)
@@ -840,8 +844,12 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
             poly_add<!CL>(Ga, Gb, W, p + (p >> 3), y, amp, 1.f, scale_lj, J, cmask, two_word, acc);
           }
           };
-          if (T.use_bz && !T.two_word && g.as == 1.f) walk(std::true_type());
-          else walk(std::false_type());
+          if (T.use_bz && !T.two_word && g.as == 1.f) {
+            if (!CL && !A.jobs) walk(std::true_type(), std::true_type());
+            else walk(std::true_type(), std::false_type());
+          } else {
+            walk(std::false_type(), std::false_type());
+          }
           if (acc == 0u) sm.ti.ovf = 1;  // a position of this tile reached its count capacity
         }
         __syncthreads();  // column records are replaced by the next batch
