@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           PolyColRec cr = load_col(&sm.col[j]);  // the current column's record, in registers
           // the walk, compiled three times: the common case (single word, omni source, z factors from the table)
           // with its flags as constants — fewer live registers, so fewer loop constants re-read from shared memory —
-          // once more for single-room persistent calls (pattern constants from the parameter bank: +0.2 %), and the
+          // once more for single-room calls on 256-thread CTAs (pattern constants from the parameter bank: +0.2 %), and the
           // general case with runtime flags
           auto walk = [&](auto fast, auto single) {
           constexpr bool kFast = decltype(fast)::value, kSingle = decltype(single)::value;
@@ -845,7 +845,8 @@ __global__ void __launch_bounds__(THREADS, PolyCfg<THREADS>::kCtasPerSm)
           }
           };
           if (T.use_bz && !T.two_word && g.as == 1.f) {
-            if (!CL && !A.jobs) walk(std::true_type(), std::true_type());
+            // (256-thread CTAs only: in the 512-thread variant the extra instantiation cost config 4 8 %)
+            if (!CL && THREADS == 256 && !A.jobs) walk(std::true_type(), std::true_type());
             else walk(std::true_type(), std::false_type());
           } else {
             walk(std::false_type(), std::false_type());
